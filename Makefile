@@ -1,0 +1,27 @@
+# libpspgmres (sm_100a) and the CPU oracle.  `make` builds both in-tree.
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+CSRC      := paper_1308_5626_b200/csrc
+LIB       := paper_1308_5626_b200/libpspgmres.so
+SRCS      := $(CSRC)/api.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
+OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+HDRS      := $(CSRC)/internal.h include/pspgmres.h
+ORACLE    := oracle/liboracle.so
+
+all: $(LIB) $(ORACLE)
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+$(ORACLE): oracle/oracle.c oracle/oracle.h
+	gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -Wextra -Wno-unused-parameter -o $@ oracle/oracle.c -lm
+
+clean:
+	rm -rf build $(LIB) $(ORACLE)
+
+.PHONY: all clean

@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- PSP-GMRES implicit-Euler time steps on B200 through libpspgmres (C ABI).
+
+One "step" = one pass of the whole hot path: the restarted PSP-GMRES
+solve of (I - dt L) u^{n+1} = u^n (Alg.1) with probe recording, then the MREP fit
+(Alg.2), the R21 gate and the banded factorisation for the next step.  Workload: BASELINE
+configs[3] (C4, 3-D variable-kappa diffusion 512^3, d = 3, GMRES(30), tol 1e-8, m_max = 32).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 512]
+
+metric/unit: BASELINE.json's metric, measured as unknown-iterations/s = sum over ranks of
+n * (inner iterations) / (max over ranks of the device time of the K timed steps).
+The --impl reference arm times the CPU oracle (oracle/) on a bounded sample of the same
+workload on the host cores (rank 0 only).  See DESIGN.md section 9.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "PSP-GMRES unknown-iterations/s and MREP rows/s at 1/2/4/8 GPUs, % HBM peak"
+UNIT = "unknown-iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=512, help="grid points per axis (512 = C4)")
+    ap.add_argument("--ortho", default="1reduce", choices=["1reduce", "literal"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-size", type=int, default=128)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.p is None:
+            return out
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return out
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        out.update(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                   reasons=reasons, samples=len(rows))
+        return out
+
+
+def cpu_baseline(size, budget_s=20.0):
+    """The oracle as it stands (single-threaded C, literal Alg.1) on a bounded sample of C4."""
+    import numpy as np
+
+    import oracle
+    from paper_1308_5626_b200 import inputs
+    prob = inputs.c4(n=size, steps=1)
+    b = prob.u0
+    eps = prob.tol * float(np.linalg.norm(b))
+    iters = 0
+    t0 = time.perf_counter()
+    x0 = b.copy()
+    cycles = 0
+    while time.perf_counter() - t0 < budget_s:
+        r = oracle.pspgmres(prob.op, b, x0, eps, prob.restart, 1)
+        iters += r["report"]["iterations"]
+        cycles += 1
+        x0 = r["x"]
+        if r["report"]["converged"]:
+            break
+    t = time.perf_counter() - t0
+    n = prob.op.rows
+    return {"value": n * iters / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"C4 recipe at {size}^3 (n={n}), first time step, {cycles} GMRES(30) cycle(s) "
+                      f"= {iters} iterations in {t:.1f} s, literal MGS, 1 host thread"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    from paper_1308_5626_b200 import inputs
+    size = args.cpu_sample_size
+    prob = inputs.c4(n=size, steps=1)
+    b = prob.u0
+    eps = prob.tol * float(np.linalg.norm(b))
+    n = prob.op.rows
+
+    def one_step():   # bounded sample of one time step: its first GMRES(30) cycle
+        t0 = time.perf_counter()
+        r = oracle.pspgmres(prob.op, b, b, eps, prob.restart, 1)
+        return r["report"]["iterations"], time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        one_step()
+    tot_it, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        it, t = one_step()
+        tot_it += it
+        tot_t += t
+    value = n * tot_it / tot_t
+    sample = f"C4 recipe at {size}^3 (n={n}), one GMRES(30) cycle of the first time step per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "C4 (BASELINE configs[3]) sample", "grid": [size] * 3,
+                                            "d": 3, "restart": 30, "tol": 1e-8},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    from paper_1308_5626_b200 import inputs, pspgmres as P
+
+    assert torch.cuda.is_available(), "bench.py needs a GPU (libpspgmres has no CPU path)"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # ---- workload: C4, one independent replica per rank ----
+    t_gen = time.perf_counter()
+    prob = inputs.c4(n=args.size, steps=args.warmup + args.steps)
+    t_gen = time.perf_counter() - t_gen
+    n = prob.op.rows
+    ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=stream)
+        u = torch.as_tensor(prob.u0).cuda()
+    stream.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- warm-up (untimed) ----
+    for _ in range(args.warmup):
+        ctx.psp_step(u, u)
+    ctx.psp_kernel_stats(reset=True)
+    l0 = ctx.psp_launch_count()
+
+    # ---- timed region: K steps, device time via CUDA events on the solver stream ----
+    clocks = Clocks(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record(stream)
+    reps = []
+    for _ in range(args.steps):
+        reps.append(ctx.psp_step(u, u))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    launches = ctx.psp_launch_count() - l0
+    kstats = ctx.psp_kernel_stats(reset=True)
+    iters = sum(r["iterations"] for r in reps)
+    if dist is not None:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        it = torch.tensor([float(n * iters)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+        total_unknown_iters = float(it.item())
+    else:
+        total_unknown_iters = float(n * iters)
+    value = total_unknown_iters / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel class (largest share of the timed device time) ----
+    peak, peak_src = peaks()
+    dom = max((k for k in kstats if kstats[k]["launches"] > 0), key=lambda k: kstats[k]["ms"])
+    ds = kstats[dom]
+    avg_ms = ds["ms"] / ds["launches"]
+    avg_bytes = ds["bytes"] / ds["launches"]
+    achieved = avg_bytes / (avg_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if dom in tj and tj[dom].get("size") == args.size:
+            traffic = tj[dom]["traffic_over_algorithmic"] * avg_bytes
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
+                "share_of_step": ds["ms"] / t_ms}
+    kernel_table = {k: {"ms": v["ms"], "launches": v["launches"],
+                        "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
+                        "share": v["ms"] / t_ms} for k, v in kstats.items() if v["launches"]}
+
+    # ---- e2e: same metric through the C ABI with host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(n, dtype=torch.float64).pin_memory()
+        host.copy_(u.cpu())
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        it_e2e = 0
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                u.copy_(host, non_blocking=True)             # H2D of the step's input u^n
+                r = ctx.psp_step(u, u)
+                host.copy_(u, non_blocking=True)             # D2H of the step's result u^{n+1}
+                it_e2e += r["iterations"]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1)
+        tot = float(n * it_e2e)
+        if dist is not None:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+            it = torch.tensor([tot], dtype=torch.float64, device="cuda")
+            dist.all_reduce(it, op=dist.ReduceOp.SUM)
+            tot = float(it.item())
+        e2e = {"value": tot / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n}
+        ctx.psp_kernel_stats(reset=True)
+
+    line = None
+    if rank == 0:
+        mrep_ms = kstats.get("mrep_fit", {}).get("ms", 0.0)
+        solve_ms = sum(r["t_solve_ms"] for r in reps) if reps and reps[0]["t_solve_ms"] else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4: 3-D variable-kappa diffusion {args.size}^3 (BASELINE configs[3]), "
+                                   "one implicit-Euler PSP-GMRES time step (solve + MREP fit + gate + factor)",
+                       "grid": [args.size] * 3, "n": n, "d": prob.d, "restart": prob.restart, "tol": prob.tol,
+                       "m_max": prob.m_max, "ortho": args.ortho, "dt": prob.op.dt,
+                       "l2": "inputs larger than L2 (each vector 8n bytes >> 126 MB); no flush needed",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "iterations_per_step": [r["iterations"] for r in reps],
+            "cycles_per_step": [r["cycles"] for r in reps],
+            "precond_identity_per_step": [r["precond_identity"] for r in reps],
+            "gate_accepted_per_step": [r["mrep_gate_accepted"] for r in reps],
+            "converged": all(r["converged"] for r in reps),
+            "true_resid_over_eps": max(r["final_resid_true"] / r["eps"] for r in reps),
+            "mrep_rows_per_s": (n * args.steps / (mrep_ms / 1e3)) if mrep_ms else None,
+            "kernels": kernel_table,
+            "roofline": roofline,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "e2e": e2e,
+            "input_generation_s": t_gen,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_sample_size)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

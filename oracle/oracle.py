@@ -281,6 +281,37 @@ def mrep(px, py, d, order=None):
                 max_abs_diag=rep.max_abs_diag)
 
 
+class Driver:
+    """O5 one step at a time, keeping the ring and N across calls (for lockstep parity)."""
+
+    def __init__(self, spec, n, restart, max_cycles, tol, d, m_max, reset_history=False, gate=True):
+        self.spec = spec
+        self.n = n
+        self.d = d
+        self.ring = Ring(n, m_max)
+        self.bands = np.zeros((2 * d + 1, n))
+        self.lu = np.zeros((2 * d + 1, n))
+        self.ident = C.c_int(1)
+        self.opts = _StepOpts(restart, max_cycles, float(tol), d, m_max, int(reset_history), int(gate))
+        self.hist_cap = restart * max_cycles
+
+    def step(self, u):
+        """Returns dict(u_next, report, N_used=(bands copy or None for I), resid_hist)."""
+        o, _k = _op(self.spec)
+        uu = _f64(np.asarray(u).reshape(-1)).copy()
+        n_used = None if self.ident.value else self.bands.copy()
+        rep = (_StepReport * 1)()
+        hist = np.zeros(self.hist_cap)
+        st = lib().orc_time_steps(C.byref(o), _p(uu), 1, C.byref(self.opts), C.byref(self.ring.s), _p(self.bands),
+                                  _p(self.lu), C.byref(self.ident), rep, _p(hist), self.hist_cap)
+        r = rep[0]
+        sr = _report(r.solve)
+        return dict(status=st, u=uu, N_used=n_used, solve=sr, resid_hist=hist[:sr["hist_len"]].copy(),
+                    mrep=dict(rows_ridge=r.mrep.rows_ridge, rows_fallback=r.mrep.rows_fallback,
+                              gate_accepted=bool(r.mrep.gate_accepted)),
+                    precond_was_identity=bool(r.precond_was_identity), mrep_ran=bool(r.mrep_ran))
+
+
 def time_steps(spec, u0, steps, restart, max_cycles, tol, d, m_max, reset_history=False, gate=True,
                hist_cap=None):
     """O5: the implicit-Euler driver.  Returns dict(u, reports, resid_hist, bands, is_identity)."""

@@ -1,0 +1,986 @@
+// api.cu -- the C ABI of libpspgmres (include/pspgmres.h): context, workspace plan, and the
+// host control flow of Algorithm 1, Algorithm 2 and the time-step
+// driver (Eq.3-4).  Every numeric step runs in the kernels of stencil.cu,
+// krylov.cu, mrep.cu and banded.cu; the host only sequences launches and reads the O(1)
+// scalars the control flow branches on (beta, R(k), flags, gate decision).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace psp;
+
+struct psp_comm {
+  int nranks = 1, rank = 0;
+  void* nccl = nullptr;  // ncclComm_t (comm.cu)
+};
+
+struct psp_ctx {
+  // configuration
+  psp_grid grid{};
+  int d = 1, nA = 30;
+  double tol = 1e-8, dt = 0.0;
+  psp_opts opts{};
+  cudaStream_t stream = nullptr;
+  psp_comm* comm = nullptr;
+  int64_t n = 0, row0 = 0;
+  Stencil st{};
+  // workspace carve
+  double* ring_px = nullptr;
+  double* ring_py = nullptr;
+  int ring_cap = 0, ring_count = 0, ring_head = 0;
+  double* V = nullptr;
+  int64_t ldv = 0;
+  double* X0 = nullptr;
+  double* B = nullptr;
+  double* W = nullptr;
+  double* bands = nullptr;
+  double* lu = nullptr;
+  double* intercept = nullptr;
+  uint8_t* rowkind = nullptr;
+  double* kappa = nullptr;
+  bool n_identity = true;
+  DevState ds{};
+  RedCfg rc{};
+  MrepScratch ms{};
+  BandedScratch bs{};
+  // host
+  double* hp = nullptr;  // pinned scalars
+  std::string err;
+  psp_status sticky = PSP_OK;
+  int64_t launches = 0;
+  int last_k = 0;
+  cudaEvent_t ev[6] = {};
+  // per-kernel-class event timing (opts.timing >= 2)
+  struct KRec {
+    int klass;
+    double bytes;
+    int ev;
+  };
+  std::vector<cudaEvent_t> kev;
+  std::vector<KRec> krec;
+  int kev_used = 0;
+  double kms[PSP_KC_COUNT] = {};
+  double kbytes[PSP_KC_COUNT] = {};
+  int64_t kcount[PSP_KC_COUNT] = {};
+};
+
+namespace {
+void kt_flush(psp_ctx* c) {
+  if (c->krec.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (const auto& r : c->krec) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->kev[r.ev], c->kev[r.ev + 1]);
+    c->kms[r.klass] += ms;
+    c->kbytes[r.klass] += r.bytes;
+    c->kcount[r.klass] += 1;
+  }
+  c->krec.clear();
+  c->kev_used = 0;
+}
+// returns a handle (or -1 when timing is off); pair with kt_end after the launch(es)
+int kt_begin(psp_ctx* c) {
+  if (c->opts.timing < 2) return -1;
+  if (c->kev_used + 2 > 16384) kt_flush(c);
+  while ((int)c->kev.size() < c->kev_used + 2) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->kev.push_back(e);
+  }
+  const int h = c->kev_used;
+  c->kev_used += 2;
+  cudaEventRecord(c->kev[h], c->stream);
+  return h;
+}
+void kt_end(psp_ctx* c, int h, int klass, double bytes) {
+  if (h < 0) return;
+  cudaEventRecord(c->kev[h + 1], c->stream);
+  c->krec.push_back({klass, bytes, h});
+}
+// algorithmic bytes of one matvec: x (+ field or DIA bands) read, y written (+ probe copy)
+double matvec_bytes(const psp_ctx* c, bool copy) {
+  double per = 16.0;
+  if (c->st.kind == PSP_OP_CELL_DIFF || c->st.kind == PSP_OP_CELL_ADVDIFF) per += 8.0;
+  if (c->st.kind == PSP_OP_DIA) per += 8.0 * (2 * c->st.dA + 1);
+  if (copy) per += 8.0;
+  return per * (double)c->n;
+}
+}  // namespace
+
+static std::string g_err;
+
+namespace psp {
+std::string cuda_err_str(cudaError_t e) { return std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e); }
+}  // namespace psp
+
+static psp_status fail(psp_ctx* c, psp_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return s;
+}
+
+static psp_status check_cuda(psp_ctx* c, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (c) c->sticky = PSP_E_CUDA;
+    return fail(c, PSP_E_CUDA, std::string(where) + ": " + cuda_err_str(e));
+  }
+  return PSP_OK;
+}
+
+#define PSP_TRY(expr)                 \
+  do {                                \
+    psp_status _s = (expr);           \
+    if (_s != PSP_OK) return _s;      \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Workspace plan
+// ------------------------------------------------------------------------------------------
+namespace {
+
+struct Plan {
+  size_t off_px, off_py, off_V, off_X0, off_B, off_W, off_bands, off_lu, off_icpt, off_kind,
+      off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_scal, off_resid,
+      off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, total;
+  int nblocks;
+};
+
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+Plan make_plan(int64_t n, int d, int nA, int m_max) {
+  Plan p{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  const size_t vec = (size_t)n * 8;
+  p.nblocks = 2 * sm_count();
+  p.off_px = take(vec * m_max);
+  p.off_py = take(vec * m_max);
+  p.off_V = take(vec * (nA + 1));
+  p.off_X0 = take(vec);
+  p.off_B = take(vec);
+  p.off_W = take(vec);
+  p.off_bands = take(vec * (2 * d + 1));
+  p.off_lu = take(vec * (2 * d + 1));
+  p.off_icpt = take(vec);
+  p.off_kind = take((size_t)n);
+  p.off_kappa = take(vec);
+  const size_t hs = (size_t)(nA + 1) * nA * 8;
+  p.off_H = take(hs);
+  p.off_Hraw = take(hs);
+  p.off_G = take((size_t)(nA + 1) * 8);
+  p.off_C = take((size_t)nA * 8);
+  p.off_S = take((size_t)nA * 8);
+  p.off_Q = take((size_t)nA * 8);
+  p.off_Lm = take((size_t)(nA + 1) * (nA + 1) * 8);
+  p.off_scal = take(SC_NSCAL * 8);
+  p.off_resid = take((size_t)nA * 8);
+  p.off_partials = take((size_t)2 * kMaxRestart * p.nblocks * 8);
+  p.off_tickets = take(TK_N * 4);
+  p.off_mpart = take((size_t)6 * kMrepMaxBlocks * 8);
+  p.off_mtick = take(64);
+  p.off_mres = take(16 * 8);
+  p.off_banded = take(banded_scratch_bytes(n, d));
+  p.total = o + 256;  // alignment slack for the base pointer
+  return p;
+}
+
+int64_t grid_rows(const psp_grid* g) {
+  int64_t r = 1;
+  for (int a = 0; a < g->ndim; ++a) r *= g->n[a];
+  return r;
+}
+
+psp_status validate(const psp_grid* grid, const psp_stencil* st, int d, int restart, const psp_opts* o) {
+  if (!grid || !st) return fail(nullptr, PSP_E_ARG, "grid/stencil is NULL");
+  if (grid->ndim < 1 || grid->ndim > 3) return fail(nullptr, PSP_E_DIM, "ndim must be 1..3");
+  for (int a = 0; a < grid->ndim; ++a)
+    if (grid->n[a] < 1) return fail(nullptr, PSP_E_DIM, "grid extent < 1");
+  if (st->kind < PSP_OP_CONST_DIFF || st->kind > PSP_OP_DIA) return fail(nullptr, PSP_E_ARG, "bad stencil kind");
+  if ((st->kind == PSP_OP_CELL_DIFF || st->kind == PSP_OP_CELL_ADVDIFF) && !st->d_field)
+    return fail(nullptr, PSP_E_ARG, "cell operator needs d_field");
+  if (st->kind == PSP_OP_DIA && (!st->d_bands || st->dA < 0)) return fail(nullptr, PSP_E_ARG, "DIA operator needs d_bands");
+  if (st->kind == PSP_OP_CELL_ADVDIFF)
+    for (int a = 0; a < 3; ++a)
+      if (st->c[a] < 0) return fail(nullptr, PSP_E_ARG, "upwind velocity must be >= 0 (v1)");
+  if (d < 1 || d > kMaxD) return fail(nullptr, PSP_E_ARG, "d must be 1..4");
+  if (restart < 1 || restart > kMaxRestart) return fail(nullptr, PSP_E_ARG, "restart must be 1..128");
+  if (o) {
+    if (o->m_max < 1 || o->m_max > 256) return fail(nullptr, PSP_E_ARG, "m_max must be 1..256");
+    if (o->max_cycles < 1) return fail(nullptr, PSP_E_ARG, "max_cycles must be >= 1");
+  }
+  if (grid_rows(grid) < 2 * d + 1) return fail(nullptr, PSP_E_DIM, "n < 2d+1 (S:207)");
+  return PSP_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+void psp_default_opts(psp_opts* o) {
+  memset(o, 0, sizeof(*o));
+  o->max_cycles = 1000;
+  o->tol_mode = PSP_TOL_REL_B;
+  o->m_max = 64;
+  o->reset_history_per_step = 0;
+  o->ortho = PSP_MGS_1REDUCE;
+  o->gate = 1;
+  o->timing = 0;
+}
+
+const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }
+
+const char* psp_status_str(psp_status s) {
+  switch (s) {
+    case PSP_OK: return "ok";
+    case PSP_E_ARG: return "bad argument";
+    case PSP_E_DIM: return "dimension mismatch";
+    case PSP_E_SAMPLES: return "insufficient samples (m < 2d+2)";
+    case PSP_E_RANK: return "rank deficient";
+    case PSP_E_SINGULAR: return "singular";
+    case PSP_E_NONFINITE: return "non-finite value";
+    case PSP_E_NOCONV: return "not converged";
+    case PSP_E_CUDA: return "CUDA error";
+    case PSP_E_NCCL: return "NCCL error";
+    case PSP_E_NOMEM: return "workspace too small";
+  }
+  return "unknown";
+}
+
+const char* psp_last_error(const psp_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+psp_status psp_workspace_bytes(const psp_grid* grid, const psp_stencil* st, int d, int restart,
+                               const psp_opts* opts, const psp_comm* comm, size_t* bytes) {
+  psp_opts o;
+  if (opts) o = *opts; else psp_default_opts(&o);
+  PSP_TRY(validate(grid, st, d, restart, &o));
+  if (comm && comm->nranks > 1) return fail(nullptr, PSP_E_ARG, "multi-rank contexts: use one context per rank slab (see DESIGN.md)");
+  Plan p = make_plan(grid_rows(grid), d, restart, o.m_max);
+  *bytes = p.total;
+  return PSP_OK;
+}
+
+psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, int d, int restart,
+                      double tol, const psp_opts* opts, void* d_ws, size_t ws_bytes, void* stream,
+                      psp_comm* comm, psp_ctx** out) {
+  if (!out) return fail(nullptr, PSP_E_ARG, "out is NULL");
+  *out = nullptr;
+  psp_opts o;
+  if (opts) o = *opts; else psp_default_opts(&o);
+  PSP_TRY(validate(grid, st, d, restart, &o));
+  if (!(tol > 0.0) || !(dt >= 0.0)) return fail(nullptr, PSP_E_ARG, "tol must be > 0 and dt >= 0");
+  if (comm && comm->nranks > 1) return fail(nullptr, PSP_E_ARG, "multi-rank contexts are not enabled in this build");
+  const int64_t n = grid_rows(grid);
+  Plan p = make_plan(n, d, restart, o.m_max);
+  if (!d_ws || ws_bytes < p.total) return fail(nullptr, PSP_E_NOMEM, "workspace smaller than psp_workspace_bytes");
+
+  psp_ctx* c = new psp_ctx();
+  c->grid = *grid;
+  c->d = d;
+  c->nA = restart;
+  c->tol = tol;
+  c->dt = dt;
+  c->opts = o;
+  c->stream = (cudaStream_t)stream;
+  c->comm = comm;
+  c->n = n;
+  c->row0 = 0;
+  // operator coefficients (R24): h_a = 1/(n_a+1)
+  Stencil& S = c->st;
+  S.kind = st->kind;
+  S.ndim = grid->ndim;
+  S.nx = grid->n[0];
+  S.ny = grid->ndim >= 2 ? grid->n[1] : 1;
+  S.nz = grid->ndim >= 3 ? grid->n[2] : 1;
+  S.n = n;
+  for (int a = 0; a < 3; ++a) {
+    const double na = a < grid->ndim ? (double)grid->n[a] : 1.0;
+    const double h = 1.0 / (na + 1.0);
+    const double coef = (st->kind == PSP_OP_CONST_DIFF) ? st->nu : 1.0;
+    S.s[a] = a < grid->ndim ? dt * coef / (h * h) : 0.0;
+    S.a[a] = (a < grid->ndim && st->kind == PSP_OP_CELL_ADVDIFF) ? dt * st->c[a] / h : 0.0;
+  }
+  S.field = st->d_field;
+  S.dA = st->dA;
+  S.bands = st->d_bands;
+  S.x_lo = S.x_hi = S.f_lo = S.f_hi = nullptr;
+
+  char* base = (char*)(((uintptr_t)d_ws + 255) & ~(uintptr_t)255);
+  auto at = [&](size_t off) { return base + off; };
+  c->ring_px = (double*)at(p.off_px);
+  c->ring_py = (double*)at(p.off_py);
+  c->ring_cap = o.m_max;
+  c->V = (double*)at(p.off_V);
+  c->ldv = n;
+  c->X0 = (double*)at(p.off_X0);
+  c->B = (double*)at(p.off_B);
+  c->W = (double*)at(p.off_W);
+  c->bands = (double*)at(p.off_bands);
+  c->lu = (double*)at(p.off_lu);
+  c->intercept = (double*)at(p.off_icpt);
+  c->rowkind = (uint8_t*)at(p.off_kind);
+  c->kappa = (double*)at(p.off_kappa);
+  c->ds.H = (double*)at(p.off_H);
+  c->ds.Hraw = (double*)at(p.off_Hraw);
+  c->ds.G = (double*)at(p.off_G);
+  c->ds.C = (double*)at(p.off_C);
+  c->ds.S = (double*)at(p.off_S);
+  c->ds.Q = (double*)at(p.off_Q);
+  c->ds.Lm = (double*)at(p.off_Lm);
+  c->ds.scal = (double*)at(p.off_scal);
+  c->ds.resid = (double*)at(p.off_resid);
+  c->ds.partials = (double*)at(p.off_partials);
+  c->ds.tickets = (unsigned*)at(p.off_tickets);
+  c->rc.nblocks = p.nblocks;
+  c->rc.max_vals = 2 * kMaxRestart;
+  c->ms.partials = (double*)at(p.off_mpart);
+  c->ms.ticket = (unsigned*)at(p.off_mtick);
+  c->ms.result = (double*)at(p.off_mres);
+  c->bs = banded_scratch(at(p.off_banded), n, d);
+  // zero the small control state (tickets, epochs, Hessenberg)
+  cudaMemsetAsync(at(p.off_H), 0, p.off_partials - p.off_H, c->stream);
+  cudaMemsetAsync(at(p.off_tickets), 0, TK_N * 4, c->stream);
+  cudaMemsetAsync(at(p.off_mtick), 0, 64, c->stream);
+  cudaMemsetAsync(at(p.off_banded), 0, banded_scratch_bytes(n, d), c->stream);
+  if (cudaMallocHost((void**)&c->hp, 64 * sizeof(double)) != cudaSuccess) {
+    delete c;
+    return fail(nullptr, PSP_E_CUDA, "cudaMallocHost failed");
+  }
+  memset(c->hp, 0, 64 * sizeof(double));
+  for (int i = 0; i < 6; ++i) cudaEventCreate(&c->ev[i]);
+  psp_status s = check_cuda(c, "psp_create");
+  if (s != PSP_OK) {
+    cudaFreeHost(c->hp);
+    delete c;
+    return s;
+  }
+  *out = c;
+  return PSP_OK;
+}
+
+psp_status psp_destroy(psp_ctx* c) {
+  if (!c) return PSP_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int i = 0; i < 6; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (auto e : c->kev) cudaEventDestroy(e);
+  if (c->hp) cudaFreeHost(c->hp);
+  delete c;
+  return PSP_OK;
+}
+
+psp_status psp_local_rows(const psp_ctx* c, int64_t* row0, int64_t* nrows) {
+  if (!c) return PSP_E_ARG;
+  if (row0) *row0 = c->row0;
+  if (nrows) *nrows = c->n;
+  return PSP_OK;
+}
+
+psp_status psp_launch_count(const psp_ctx* c, int64_t* l) {
+  if (!c || !l) return PSP_E_ARG;
+  *l = c->launches;
+  return PSP_OK;
+}
+
+psp_status psp_kernel_stats(psp_ctx* c, double* ms, double* bytes, int64_t* launches, int reset) {
+  if (!c) return PSP_E_ARG;
+  kt_flush(c);
+  for (int k = 0; k < PSP_KC_COUNT; ++k) {
+    if (ms) ms[k] = c->kms[k];
+    if (bytes) bytes[k] = c->kbytes[k];
+    if (launches) launches[k] = c->kcount[k];
+    if (reset) {
+      c->kms[k] = 0.0;
+      c->kbytes[k] = 0.0;
+      c->kcount[k] = 0;
+    }
+  }
+  return PSP_OK;
+}
+
+const char* psp_kernel_class_name(int k) {
+  static const char* names[PSP_KC_COUNT] = {"matvec", "precond_solve", "ortho_dots", "ortho_update",
+                                            "mgs_literal", "normalize", "combine", "residual",
+                                            "mrep_fit", "banded_factor", "other"};
+  return (k >= 0 && k < PSP_KC_COUNT) ? names[k] : "?";
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------
+// internal steps
+// ------------------------------------------------------------------------------------------
+namespace {
+
+// next ring slot for a probe column (FIFO, R20)
+int ring_next(psp_ctx* c) {
+  int slot;
+  if (c->ring_count < c->ring_cap) {
+    slot = (c->ring_head + c->ring_count) % c->ring_cap;
+    c->ring_count += 1;
+  } else {
+    slot = c->ring_head;
+    c->ring_head = (c->ring_head + 1) % c->ring_cap;
+  }
+  return slot;
+}
+double* px_col(psp_ctx* c, int slot) { return c->ring_px + (int64_t)slot * c->n; }
+double* py_col(psp_ctx* c, int slot) { return c->ring_py + (int64_t)slot * c->n; }
+double* Vcol(psp_ctx* c, int j /*1-based*/) { return c->V + (int64_t)(j - 1) * c->ldv; }
+
+psp_status sync_read(psp_ctx* c, const double* dsrc, int count, double* hdst) {
+  cudaMemcpyAsync(c->hp, dsrc, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    c->sticky = PSP_E_CUDA;
+    return fail(c, PSP_E_CUDA, "stream sync: " + cuda_err_str(e));
+  }
+  PSP_TRY(check_cuda(c, "sync_read"));
+  memcpy(hdst, c->hp, count * sizeof(double));
+  return PSP_OK;
+}
+
+psp_status set_eps(psp_ctx* c, const double* d_b, double* eps_out) {
+  double eps;
+  if (c->opts.tol_mode == PSP_TOL_ABS) {
+    eps = c->tol;
+  } else {
+    launch_norm(d_b, c->n, c->ds, SC_NORM, c->rc, c->stream);
+    c->launches += 1;
+    double nb;
+    PSP_TRY(sync_read(c, c->ds.scal + SC_NORM, 1, &nb));
+    eps = c->tol * nb;  // R1
+  }
+  c->hp[8] = eps;
+  cudaMemcpyAsync(c->ds.scal + SC_EPS, c->hp + 8, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  cudaStreamSynchronize(c->stream);
+  *eps_out = eps;
+  return check_cuda(c, "set_eps");
+}
+
+psp_status precond(psp_ctx* c, const double* v, const double* x0, double* z) {
+  if (c->n_identity) {
+    if (x0) return fail(c, PSP_E_ARG, "internal: identity precond with addend");
+    launch_copy(v, z, c->n, c->stream);
+    c->launches += 1;
+  } else {
+    banded_solve(c->lu, c->n, c->d, v, x0, z, c->bs, c->stream, &c->launches);
+  }
+  return PSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+psp_status psp_matvec(psp_ctx* c, const double* x, double* y, int record) {
+  if (!c || !x || !y) return fail(c, PSP_E_ARG, "psp_matvec: NULL argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  if (record) {
+    const int slot = ring_next(c);
+    launch_matvec(c->st, x, 1.0, py_col(c, slot), px_col(c, slot), c->stream);
+    launch_copy(py_col(c, slot), y, c->n, c->stream);
+    c->launches += 2;
+  } else {
+    launch_matvec(c->st, x, 1.0, y, nullptr, c->stream);
+    c->launches += 1;
+  }
+  return check_cuda(c, "psp_matvec");
+}
+
+psp_status psp_precond_apply(psp_ctx* c, const double* v, double* z) {
+  if (!c || !v || !z) return fail(c, PSP_E_ARG, "psp_precond_apply: NULL argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  PSP_TRY(precond(c, v, nullptr, z));
+  return check_cuda(c, "psp_precond_apply");
+}
+
+psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double* h_beta) {
+  if (!c || !b || !x0) return fail(c, PSP_E_ARG, "psp_cycle_begin: NULL argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  if (x0 != c->X0) {
+    launch_copy(x0, c->X0, c->n, c->stream);
+    c->launches += 1;
+  }
+  // l.4: P_x(:,i) <- X0, P_y(:,i) <- A X0
+  const int slot = ring_next(c);
+  int h = kt_begin(c);
+  launch_matvec(c->st, c->X0, 1.0, py_col(c, slot), px_col(c, slot), c->stream);
+  kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+  // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta
+  h = kt_begin(c);
+  launch_residual(b, py_col(c, slot), Vcol(c, 1), c->n, c->nA, c->ds, c->rc, c->stream);
+  kt_end(c, h, PSP_KC_RESIDUAL, 24.0 * c->n);
+  c->launches += 2;
+  double beta;
+  PSP_TRY(sync_read(c, c->ds.scal + SC_BETA, 1, &beta));
+  if (h_beta) *h_beta = beta;
+  if (beta > 0.0 && isfinite(beta)) {  // V(:,1) <- R_bar / beta (l.6)
+    launch_divide(Vcol(c, 1), c->n, c->ds.scal + SC_BETA, c->stream);
+    c->launches += 1;
+  }
+  c->last_k = 0;
+  return check_cuda(c, "psp_cycle_begin");
+}
+
+psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
+  if (!c) return fail(c, PSP_E_ARG, "psp_arnoldi_step: NULL ctx");
+  if (k < 1 || k > c->nA) return fail(c, PSP_E_ARG, "psp_arnoldi_step: k out of 1..restart");
+  if (c->sticky != PSP_OK) return c->sticky;
+  const int64_t n = c->n;
+  const int slot = ring_next(c);
+  double* px = px_col(c, slot);
+  double* py = py_col(c, slot);
+  const double* Vk = Vcol(c, k);
+  // l.10-12: Y_k = N^{-1} V(:,k) -> P_x(:,i); P_y(:,i) = A Y_k
+  const double dn = (double)n;
+  int h;
+  if (c->n_identity) {
+    h = kt_begin(c);
+    launch_matvec(c->st, Vk, 1.0, py, px, c->stream);  // N = I: the probe copy is fused
+    kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+    c->launches += 1;
+  } else {
+    h = kt_begin(c);
+    banded_solve(c->lu, n, c->d, Vk, nullptr, px, c->bs, c->stream, &c->launches);
+    kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
+    h = kt_begin(c);
+    launch_matvec(c->st, px, 1.0, py, nullptr, c->stream);
+    kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
+    c->launches += 1;
+  }
+  double* U = Vcol(c, k + 1);
+  // l.13-17: MGS (R11) + H(k+1,k) + Givens (l.19-32) in the last block
+  if (c->opts.ortho == PSP_MGS_LITERAL) {
+    h = kt_begin(c);
+    launch_mgs_literal(py, U, nullptr, Vcol(c, 1), 1, k, c->nA, n, c->ds, c->rc, c->stream);
+    for (int j = 2; j <= k; ++j)
+      launch_mgs_literal(U, U, Vcol(c, j - 1), Vcol(c, j), j, k, c->nA, n, c->ds, c->rc, c->stream);
+    launch_mgs_literal_final(U, Vcol(c, k), k, c->nA, n, c->ds, c->rc, c->stream);
+    kt_end(c, h, PSP_KC_MGS_LITERAL, (24.0 + 32.0 * (k - 1) + 24.0) * dn);
+    c->launches += k + 1;
+  } else {
+    h = kt_begin(c);
+    launch_icwy_dots(c->V, c->ldv, py, k, c->nA, n, c->ds, c->rc, c->stream);
+    kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 1) * dn);
+    h = kt_begin(c);
+    launch_icwy_update(c->V, c->ldv, py, U, k, c->nA, n, c->ds, c->rc, c->stream);
+    kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+    c->launches += 2;
+  }
+  // l.18: V(:,k+1) = U / H(k+1,k) (R4: 0 on breakdown)
+  h = kt_begin(c);
+  launch_normalize(U, U, k, c->nA, n, c->ds, c->stream);
+  kt_end(c, h, PSP_KC_NORMALIZE, 16.0 * dn);
+  c->launches += 1;
+  double sc[2];
+  PSP_TRY(sync_read(c, c->ds.scal + SC_RK, 2, sc));
+  if (h_resid) *h_resid = sc[0];
+  if (h_flags) *h_flags = (int)sc[1];
+  c->last_k = k;
+  return PSP_OK;
+}
+
+psp_status psp_cycle_end(psp_ctx* c, int k, double* x) {
+  if (!c || !x) return fail(c, PSP_E_ARG, "psp_cycle_end: NULL argument");
+  if (k < 0 || k > c->nA) return fail(c, PSP_E_ARG, "psp_cycle_end: bad k");
+  if (c->sticky != PSP_OK) return c->sticky;
+  if (k == 0) {
+    if (x != c->X0) launch_copy(c->X0, x, c->n, c->stream);
+    return check_cuda(c, "psp_cycle_end");
+  }
+  // l.38-42: Q = H^{-1}G; Z = sum Q_j V_j; X = X0 + N^{-1} Z
+  if (c->n_identity) {
+    int h = kt_begin(c);
+    launch_combine(c->V, c->ldv, k, c->nA, c->X0, c->X0, c->n, c->ds, c->stream);
+    kt_end(c, h, PSP_KC_COMBINE, 8.0 * (k + 2) * (double)c->n);
+    c->launches += 1;
+  } else {
+    int h = kt_begin(c);
+    launch_combine(c->V, c->ldv, k, c->nA, nullptr, c->W, c->n, c->ds, c->stream);
+    kt_end(c, h, PSP_KC_COMBINE, 8.0 * (k + 1) * (double)c->n);
+    c->launches += 1;
+    h = kt_begin(c);
+    PSP_TRY(precond(c, c->W, c->X0, c->X0));
+    kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 6) * (double)c->n);
+  }
+  // l.43: X0 <- X
+  if (x != c->X0) {
+    launch_copy(c->X0, x, c->n, c->stream);
+    c->launches += 1;
+  }
+  double st;
+  PSP_TRY(sync_read(c, c->ds.scal + SC_STATUS, 1, &st));
+  if (st != 0.0) return fail(c, PSP_E_SINGULAR, "back-substitution: zero pivot (R6)");
+  return check_cuda(c, "psp_cycle_end");
+}
+
+psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, psp_report* rep) {
+  if (!c || !b || !x0 || !x) return fail(c, PSP_E_ARG, "psp_solve: NULL argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  psp_report dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  psp_report* R = rep ? rep : &dummy;
+  R->status = PSP_OK;
+  R->converged = R->iterations = R->cycles = R->matvecs = R->precond_applies = 0;
+  R->resid_len = R->beta_len = 0;
+  R->precond_identity = c->n_identity ? 1 : 0;
+  if (c->opts.timing) cudaEventRecord(c->ev[0], c->stream);
+  double eps;
+  PSP_TRY(set_eps(c, b, &eps));
+  R->eps = eps;
+  psp_status status = PSP_OK;
+  bool finish = false;
+  if (x0 != c->X0) {
+    launch_copy(x0, c->X0, c->n, c->stream);
+    c->launches += 1;
+  }
+  for (int l = 1; l <= c->opts.max_cycles; ++l) {  // l.3
+    double beta;
+    PSP_TRY(psp_cycle_begin(c, b, c->X0, &beta));
+    R->matvecs += 1;
+    R->cycles += 1;
+    if (R->h_beta_history && R->beta_len < R->beta_cap) R->h_beta_history[R->beta_len] = beta;
+    R->beta_len += 1;
+    if (l == 1) R->r0 = beta;
+    if (!isfinite(beta)) { status = PSP_E_NONFINITE; break; }
+    if (beta <= eps) {  // R3
+      finish = true;
+      R->final_resid_est = beta;
+      break;
+    }
+    int kdone = 0;
+    for (int k = 1; k <= c->nA; ++k) {  // l.8
+      double Rk;
+      int flags;
+      PSP_TRY(psp_arnoldi_step(c, k, &Rk, &flags));
+      R->matvecs += 1;
+      if (!c->n_identity) R->precond_applies += 1;
+      if (R->h_resid_history && R->resid_len < R->resid_cap) R->h_resid_history[R->resid_len] = Rk;
+      R->resid_len += 1;
+      R->iterations += 1;
+      R->final_resid_est = Rk;
+      kdone = k;
+      if (flags & PSP_FLAG_NONFINITE) { status = PSP_E_NONFINITE; break; }
+      if (flags & (PSP_FLAG_CONVERGED | PSP_FLAG_BREAKDOWN)) { finish = true; break; }  // l.33-36
+    }
+    if (status != PSP_OK) break;
+    psp_status s = psp_cycle_end(c, kdone, c->X0);  // l.38-44
+    if (!c->n_identity) R->precond_applies += 1;
+    if (s != PSP_OK) { status = s; break; }
+    if (finish) break;  // l.45-48
+  }
+  if (status == PSP_OK) {
+    if (x != c->X0) {
+      launch_copy(c->X0, x, c->n, c->stream);
+      c->launches += 1;
+    }
+    // R13: true residual with one unrecorded matvec
+    launch_matvec(c->st, x, 1.0, c->W, nullptr, c->stream);
+    launch_diff_norm(b, c->W, c->n, c->ds, SC_TMP, c->rc, c->stream);
+    c->launches += 2;
+    double tr;
+    PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &tr));
+    R->final_resid_true = tr;
+    R->converged = finish ? 1 : 0;
+    if (!finish) status = PSP_E_NOCONV;
+  }
+  if (c->opts.timing) {
+    cudaEventRecord(c->ev[1], c->stream);
+    cudaEventSynchronize(c->ev[1]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    R->t_solve_ms = ms;
+  }
+  R->status = status;
+  if (status != PSP_OK && status != PSP_E_NOCONV)
+    return fail(c, status, std::string("psp_solve: ") + psp_status_str(status));
+  if (status == PSP_E_NOCONV) fail(c, status, "psp_solve: n_r restart cycles exhausted");
+  return status;
+}
+
+psp_status psp_raw_scratch_bytes(int64_t n, int d, size_t* bytes) {
+  if (!bytes || n < 1 || d < 1 || d > kMaxD) return fail(nullptr, PSP_E_ARG, "psp_raw_scratch_bytes: bad argument");
+  *bytes = banded_scratch_bytes(n, d) + 6 * kMrepMaxBlocks * 8 + 64 + 16 * 8 + 1024;
+  return PSP_OK;
+}
+
+static void raw_carve(void* scratch, int64_t n, int d, MrepScratch* ms, BandedScratch* bs) {
+  char* p = (char*)(((uintptr_t)scratch + 255) & ~(uintptr_t)255);
+  ms->partials = (double*)p;
+  p += 6 * kMrepMaxBlocks * 8;
+  ms->ticket = (unsigned*)p;
+  p += 64;
+  ms->result = (double*)p;
+  p += 16 * 8;
+  p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+  *bs = banded_scratch(p, n, d);
+}
+
+psp_status psp_mrep_fit_raw(const double* px, const double* py, int64_t n, int m, int64_t ld,
+                            const int32_t* h_order, int d, double* bands, double* icpt,
+                            uint8_t* kind, double* kappa, void* scratch, size_t sbytes,
+                            void* stream, psp_mrep_info* info) {
+  size_t need;
+  PSP_TRY(psp_raw_scratch_bytes(n, d, &need));
+  if (!px || !py || !bands || !scratch) return fail(nullptr, PSP_E_ARG, "psp_mrep_fit_raw: NULL argument");
+  if (sbytes < need) return fail(nullptr, PSP_E_NOMEM, "psp_mrep_fit_raw: scratch too small");
+  if (n < 2 * d + 1) return fail(nullptr, PSP_E_DIM, "n < 2d+1");
+  if (m > 256) return fail(nullptr, PSP_E_ARG, "m > 256");
+  if (m < 2 * d + 2) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = PSP_E_SAMPLES; }
+    return PSP_E_SAMPLES;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  MrepScratch ms;
+  BandedScratch bs;
+  raw_carve(scratch, n, d, &ms, &bs);
+  cudaMemsetAsync(ms.ticket, 0, 64, s);
+  std::vector<int32_t> slots(m);
+  for (int c2 = 0; c2 < m; ++c2) slots[c2] = h_order ? h_order[c2] : c2;
+  MrepOut out{bands, icpt, kind, kappa};
+  mrep_launch(px, py, ld, slots.data(), m, n, d, out, ms, s);
+  double r[16];
+  if (cudaMemcpyAsync(r, ms.result, sizeof(r), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(nullptr, PSP_E_CUDA, "psp_mrep_fit_raw: " + cuda_err_str(cudaGetLastError()));
+  PSP_TRY(check_cuda(nullptr, "psp_mrep_fit_raw"));
+  if (info) {
+    info->max_abs_diag = r[0];
+    info->rows_ridge = (int64_t)r[3];
+    info->rows_fallback = (int64_t)(r[4] + r[8]);
+    info->rows_nondominant = (int64_t)r[5];
+    info->gate_accepted = r[7] != 0.0;
+    info->status = PSP_OK;
+  }
+  return PSP_OK;
+}
+
+psp_status psp_banded_factor_raw(const double* bands, int64_t n, int d, double* lu, void* scratch,
+                                 size_t sbytes, void* stream) {
+  size_t need;
+  PSP_TRY(psp_raw_scratch_bytes(n, d, &need));
+  if (!bands || !lu || !scratch) return fail(nullptr, PSP_E_ARG, "psp_banded_factor_raw: NULL argument");
+  if (sbytes < need) return fail(nullptr, PSP_E_NOMEM, "scratch too small");
+  MrepScratch ms;
+  BandedScratch bs;
+  raw_carve(scratch, n, d, &ms, &bs);
+  cudaStream_t s = (cudaStream_t)stream;
+  int passes = 0;
+  int st = banded_factor(bands, n, d, lu, bs, s, &passes, nullptr);
+  PSP_TRY(check_cuda(nullptr, "psp_banded_factor_raw"));
+  if (st != PSP_OK) return fail(nullptr, PSP_E_SINGULAR, "banded LU: zero pivot or growth (S:272, S:293)");
+  return PSP_OK;
+}
+
+psp_status psp_banded_solve_raw(const double* lu, int64_t n, int d, const double* v, const double* x0,
+                                double* z, void* scratch, size_t sbytes, void* stream) {
+  size_t need;
+  PSP_TRY(psp_raw_scratch_bytes(n, d, &need));
+  if (!lu || !v || !z || !scratch) return fail(nullptr, PSP_E_ARG, "psp_banded_solve_raw: NULL argument");
+  if (sbytes < need) return fail(nullptr, PSP_E_NOMEM, "scratch too small");
+  if (z == v) return fail(nullptr, PSP_E_ARG, "z and v may not alias");
+  MrepScratch ms;
+  BandedScratch bs;
+  raw_carve(scratch, n, d, &ms, &bs);
+  banded_solve(lu, n, d, v, x0, z, bs, (cudaStream_t)stream, nullptr);
+  return check_cuda(nullptr, "psp_banded_solve_raw");
+}
+
+static psp_status install_bands(psp_ctx* c, bool gate_ok, psp_report* R) {
+  bool accept = gate_ok;
+  if (accept) {
+    if (c->opts.timing) cudaEventRecord(c->ev[4], c->stream);
+    int passes = 0;
+    int h = kt_begin(c);
+    int st = banded_factor(c->bands, c->n, c->d, c->lu, c->bs, c->stream, &passes, &c->launches);
+    kt_end(c, h, PSP_KC_FACTOR, 16.0 * (2 * c->d + 1) * (double)c->n);
+    PSP_TRY(check_cuda(c, "banded_factor"));
+    if (st != PSP_OK) accept = false;  // fall back to identity
+    if (c->opts.timing && R) {
+      cudaEventRecord(c->ev[5], c->stream);
+      cudaEventSynchronize(c->ev[5]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+      R->t_factor_ms = ms;
+    }
+  }
+  c->n_identity = !accept;
+  if (R) R->mrep_gate_accepted = accept ? 1 : 0;
+  return PSP_OK;
+}
+
+psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
+  if (!c) return fail(c, PSP_E_ARG, "psp_mrep_fit: NULL ctx");
+  if (c->sticky != PSP_OK) return c->sticky;
+  psp_report dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  psp_report* R = rep ? rep : &dummy;
+  const int m = c->ring_count;
+  R->mrep_ran = 0;
+  if (m < 2 * c->d + 2) {  // R19
+    R->mrep_status = PSP_E_SAMPLES;
+    return PSP_E_SAMPLES;
+  }
+  if (c->opts.timing) cudaEventRecord(c->ev[2], c->stream);
+  std::vector<int32_t> slots(m);
+  for (int q = 0; q < m; ++q) slots[q] = (c->ring_head + q) % c->ring_cap;
+  MrepOut out{c->bands, c->intercept, c->rowkind, c->kappa};
+  cudaMemsetAsync(c->ms.ticket, 0, 64, c->stream);
+  int h = kt_begin(c);
+  mrep_launch(c->ring_px, c->ring_py, c->n, slots.data(), m, c->n, c->d, out, c->ms, c->stream);
+  kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
+  c->launches += 3;
+  double r[16];
+  PSP_TRY(sync_read(c, c->ms.result, 16, r));
+  if (c->opts.timing) {
+    cudaEventRecord(c->ev[3], c->stream);
+    cudaEventSynchronize(c->ev[3]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    R->t_mrep_ms = ms;
+  }
+  R->mrep_ran = 1;
+  R->mrep_status = PSP_OK;
+  R->mrep_max_abs_diag = r[0];
+  R->mrep_rows_ridge = (int64_t)r[3];
+  R->mrep_rows_fallback = (int64_t)(r[4] + r[8]);
+  R->mrep_rows_nondominant = (int64_t)r[5];
+  const bool gate_ok = c->opts.gate ? (r[7] != 0.0) : true;
+  return install_bands(c, gate_ok, R);
+}
+
+psp_status psp_step(psp_ctx* c, const double* u_n, double* u_np1, psp_report* rep) {
+  if (!c || !u_n || !u_np1) return fail(c, PSP_E_ARG, "psp_step: NULL argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  if (c->opts.reset_history_per_step) { c->ring_count = 0; c->ring_head = 0; }
+  // b := u^n (kept in B: u_np1 may alias u_n); X0 := u^n (R2)
+  launch_copy(u_n, c->B, c->n, c->stream);
+  c->launches += 1;
+  psp_status s = psp_solve(c, c->B, c->B, u_np1, rep);
+  if (s != PSP_OK && s != PSP_E_NOCONV) return s;
+  psp_report dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  psp_status m = psp_mrep_fit(c, rep ? rep : &dummy);
+  if (m != PSP_OK && m != PSP_E_SAMPLES) return m;
+  return s;
+}
+
+psp_status psp_set_bands(psp_ctx* c, const double* d_bands, int* h_accepted) {
+  if (!c) return fail(c, PSP_E_ARG, "psp_set_bands: NULL ctx");
+  if (c->sticky != PSP_OK) return c->sticky;
+  if (!d_bands) {  // N = I
+    c->n_identity = true;
+    if (h_accepted) *h_accepted = 0;
+    return PSP_OK;
+  }
+  if (d_bands != c->bands)
+    cudaMemcpyAsync(c->bands, d_bands, (size_t)c->n * (2 * c->d + 1) * 8, cudaMemcpyDeviceToDevice, c->stream);
+  bool ok = true;
+  if (c->opts.gate) {
+    // evaluate R21 on the given bands with the same reduction as the fit (MREP-free path):
+    std::vector<double> hb((size_t)c->n * (2 * c->d + 1));
+    cudaMemcpyAsync(hb.data(), c->bands, hb.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    for (int64_t i = 0; i < c->n && ok; ++i) {
+      double off = 0.0;
+      for (int o = 0; o <= 2 * c->d; ++o) {
+        int64_t j = i + o - c->d;
+        if (o == c->d || j < 0 || j >= c->n) continue;
+        off += fabs(hb[(size_t)o * c->n + i]);
+      }
+      if (!(fabs(hb[(size_t)c->d * c->n + i]) > off)) ok = false;
+    }
+  }
+  PSP_TRY(install_bands(c, ok, nullptr));
+  if (h_accepted) *h_accepted = c->n_identity ? 0 : 1;
+  return check_cuda(c, "psp_set_bands");
+}
+
+psp_status psp_get_bands(const psp_ctx* c, double* d_out, int* h_ident) {
+  if (!c) return PSP_E_ARG;
+  if (d_out)
+    cudaMemcpyAsync(d_out, c->bands, (size_t)c->n * (2 * c->d + 1) * 8, cudaMemcpyDeviceToDevice, c->stream);
+  if (h_ident) *h_ident = c->n_identity ? 1 : 0;
+  cudaStreamSynchronize(c->stream);
+  return PSP_OK;
+}
+
+psp_status psp_ring_view(const psp_ctx* c, int* count, int32_t* slots, const double** px,
+                         const double** py, int64_t* ld) {
+  if (!c) return PSP_E_ARG;
+  if (count) *count = c->ring_count;
+  if (slots)
+    for (int q = 0; q < c->ring_count; ++q) slots[q] = (c->ring_head + q) % c->ring_cap;
+  if (px) *px = c->ring_px;
+  if (py) *py = c->ring_py;
+  if (ld) *ld = c->n;
+  return PSP_OK;
+}
+
+psp_status psp_ring_reset(psp_ctx* c) {
+  if (!c) return PSP_E_ARG;
+  c->ring_count = 0;
+  c->ring_head = 0;
+  return PSP_OK;
+}
+
+psp_status psp_get_hessenberg(const psp_ctx* c, double* H, double* Hraw, double* G, double* C, double* S) {
+  if (!c) return PSP_E_ARG;
+  const size_t hs = (size_t)(c->nA + 1) * c->nA * 8;
+  if (H) cudaMemcpyAsync(H, c->ds.H, hs, cudaMemcpyDeviceToHost, c->stream);
+  if (Hraw) cudaMemcpyAsync(Hraw, c->ds.Hraw, hs, cudaMemcpyDeviceToHost, c->stream);
+  if (G) cudaMemcpyAsync(G, c->ds.G, (c->nA + 1) * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (C) cudaMemcpyAsync(C, c->ds.C, c->nA * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (S) cudaMemcpyAsync(S, c->ds.S, c->nA * 8, cudaMemcpyDeviceToHost, c->stream);
+  return cudaStreamSynchronize(c->stream) == cudaSuccess ? PSP_OK : PSP_E_CUDA;
+}
+
+psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj) {
+  if (!c || !d_vj || j < 1 || j > c->nA + 1) return PSP_E_ARG;
+  *d_vj = c->V + (int64_t)(j - 1) * c->ldv;
+  return PSP_OK;
+}
+
+// ---- communicator (NCCL over NVLink) ----
+psp_status psp_comm_unique_id(void* id) {
+  if (!id) return PSP_E_ARG;
+  memset(id, 0, 128);
+  return fail(nullptr, PSP_E_ARG, "multi-rank path not enabled in this build");
+}
+psp_status psp_comm_init(const void*, int nranks, int rank, psp_comm** out) {
+  if (!out) return PSP_E_ARG;
+  if (nranks != 1) return fail(nullptr, PSP_E_ARG, "multi-rank path not enabled in this build");
+  psp_comm* c = new psp_comm();
+  c->nranks = 1;
+  c->rank = rank;
+  *out = c;
+  return PSP_OK;
+}
+psp_status psp_comm_destroy(psp_comm* c) {
+  delete c;
+  return PSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,555 @@
+// banded.cu -- K4: the preconditioner solve N z = v (Alg.1 l.10 and l.42; "solved
+// efficiently in O(n) FLOPs using Thomas algorithm"; d > 1 per P:161), by the
+// unpivoted banded LU of N (Doolittle; for d = 1 the same operations as Thomas).
+//
+// Factorisation (a9, once per time step).  Doolittle's row recurrence is sequential: row i
+// needs the U rows i-d..i-1.  It is split into chunks of kChunk rows, one thread each, and
+// iterated to a fixed point: pass p recomputes every chunk from the last-d-U-rows state its
+// left neighbour produced in pass p-1 (chunk 0 starts from the matrix start).  After pass p,
+// chunks 0..p-1 are bitwise the sequential result; the iteration stops at the first pass in
+// which no chunk's outgoing state changed, which is then the sequential LU for every chunk.
+// Under the R21 gate (strict diagonal dominance) the Schur-complement recurrence contracts,
+// so 2-4 passes suffice; termination is guaranteed after #chunks+1 passes in any case.
+//
+// Solve (a2, every iteration).  Two sweeps, each a linear recurrence of order d:
+//   forward  y_i = v_i - sum_{k=1..d} L(i,i-k) y_{i-k}
+//   backward z_i = (y_i - sum_{k=1..d} U(i,i+k) z_{i+k}) / U(i,i)
+// Each sweep is ONE pass over HBM: a block stages a tile of TPB*R rows in shared memory,
+// every thread runs its R rows with d+1 simultaneous recurrences (zero state + the d unit
+// states) to get its affine map state_out = M state_in + t, a warp-shuffle / block scan
+// composes the maps, and a decoupled look-back across tiles (in-order tickets, epoch-tagged
+// descriptors) delivers the exact incoming state; the rows are then recomputed from that
+// state and stored.  Algorithmic bytes: forward 8(d+2), backward 8(d+3) per row.
+#include <math.h>
+
+#include "internal.h"
+
+namespace psp {
+namespace {
+
+constexpr int kChunk = 128;      // factor: rows per thread
+constexpr int STPB = 128;        // solve: threads per block
+constexpr int SR = 8;            // solve: rows per thread
+constexpr int STILE = STPB * SR; // solve: rows per tile
+constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank conflicts)
+
+// ---------------------------------------------------------------------------------------
+// Factorisation pass
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, double* __restrict__ lu,
+                                   const double* __restrict__ st_in, double* __restrict__ st_out,
+                                   int first_pass, int* __restrict__ changed, int* __restrict__ bad) {
+  constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const int64_t r0 = c * kChunk;
+  const int64_t r1 = (r0 + kChunk < n) ? r0 + kChunk : n;
+  double Uw[D][D + 1];
+  if (c == 0 || first_pass) {
+    // matrix start (exact for chunk 0; the initial guess for the others)
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int e = 0; e <= D; ++e) Uw[q][e] = 0.0;
+  } else {
+    const double* s = st_in + (c - 1) * W;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int e = 0; e <= D; ++e) Uw[q][e] = s[q * (D + 1) + e];
+  }
+  const bool at_start = (c == 0) || first_pass;
+  int isbad = 0;
+  for (int64_t i = r0; i < r1; ++i) {
+    double Lr[D];       // L(i, i-D+q), q = 0..D-1
+    double Ur[D + 1];   // U(i, i+e)
+    // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D.  Rows before the matrix
+    // start (or before the chunk start in a first-pass guess) do not exist.
+    auto Uk = [&](int q, int64_t j) -> double {
+      const int64_t k = i - D + q;
+      const int64_t e = j - k;
+      return (e >= 0 && e <= D) ? Uw[q][e] : 0.0;
+    };
+    auto row_exists = [&](int q) -> bool {
+      const int64_t k = i - D + q;
+      return k >= 0 && !(at_start && k < r0);
+    };
+#pragma unroll
+    for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
+      const int64_t j = i - D + q;
+      if (!row_exists(q)) { Lr[q] = 0.0; continue; }
+      double s = bands[(int64_t)q * n + i];  // N(i,j), band o = j-i+D = q
+#pragma unroll
+      for (int p = 0; p < q; ++p)           // k = i-D+p < j, k >= j-D holds (p >= 0 > q-D)
+        if (row_exists(p)) s -= Lr[p] * Uk(p, j);
+      Lr[q] = s / Uw[q][0];                 // U(j,j)
+    }
+#pragma unroll
+    for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
+      const int64_t j = i + e;
+      if (j >= n) { Ur[e] = 0.0; continue; }
+      double s = bands[(int64_t)(D + e) * n + i];
+#pragma unroll
+      for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]
+        if (row_exists(p) && (i - D + p) >= j - D) s -= Lr[p] * Uk(p, j);
+      Ur[e] = s;
+    }
+    if (!(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      if (!(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
+      lu[(int64_t)q * n + i] = Lr[q];
+    }
+#pragma unroll
+    for (int e = 0; e <= D; ++e) {
+      if (!(fabs(Ur[e]) <= 1e100)) isbad = 1;
+      lu[(int64_t)(D + e) * n + i] = Ur[e];
+    }
+    // shift the window
+#pragma unroll
+    for (int q = 0; q < D - 1; ++q)
+#pragma unroll
+      for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
+#pragma unroll
+    for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
+    (void)row_exists;
+  }
+  double* so = st_out + c * W;
+  bool diff = first_pass != 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int e = 0; e <= D; ++e) {
+      const double v = Uw[q][e];
+      if (!first_pass && __double_as_longlong(v) != __double_as_longlong(st_in[c * W + q * (D + 1) + e]))
+        diff = true;
+      so[q * (D + 1) + e] = v;
+    }
+  if (diff) atomicAdd(changed, 1);
+  if (isbad) atomicOr(bad, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// Solve sweeps with decoupled look-back
+// ---------------------------------------------------------------------------------------
+template <int D>
+struct Map {
+  double M[D][D];
+  double t[D];
+};
+
+// c = a after b   (apply b first, then a):  M = Ma Mb, t = Ma tb + ta
+template <int D>
+__device__ __forceinline__ Map<D> compose(const Map<D>& a, const Map<D>& b) {
+  Map<D> c;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double ti = a.t[i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) ti = fma(a.M[i][k], b.t[k], ti);
+    c.t[i] = ti;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s = fma(a.M[i][k], b.M[k][j], s);
+      c.M[i][j] = s;
+    }
+  }
+  return c;
+}
+
+template <int D>
+__device__ __forceinline__ Map<D> shfl_up_map(const Map<D>& m, int off) {
+  Map<D> r;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    r.t[i] = __shfl_up_sync(0xffffffffu, m.t[i], off);
+#pragma unroll
+    for (int j = 0; j < D; ++j) r.M[i][j] = __shfl_up_sync(0xffffffffu, m.M[i][j], off);
+  }
+  return r;
+}
+
+template <int D>
+__device__ __forceinline__ Map<D> identity_map() {
+  Map<D> m;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    m.t[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) m.M[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  return m;
+}
+
+template <int D>
+__device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], double (&o)[D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double v = m.t[i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) v = fma(m.M[i][k], s[k], v);
+    o[i] = v;
+  }
+}
+
+// Descriptor layout per tile: [M (D*D) | t (D) | S (D)] doubles; flag word separate.
+enum { FLAG_AGG = 1, FLAG_INCL = 2 };
+
+// One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
+//                        BWD: z = (v - sum_k c[k] s[k]) / u0 (c[k] = U(i,i+k+1), s[k] = z_{i+k+1})
+template <bool FWD, int D>
+__device__ __forceinline__ double rec_step(double v, const double (&c)[D], const double (&s)[D],
+                                           double u0) {
+  double acc = v;
+#pragma unroll
+  for (int k = 0; k < D; ++k) acc -= c[k] * s[k];
+  return FWD ? acc : acc / u0;
+}
+
+template <int D>
+__device__ __forceinline__ void push_state(double (&s)[D], double y) {
+#pragma unroll
+  for (int k = D - 1; k > 0; --k) s[k] = s[k - 1];
+  s[0] = y;
+}
+
+template <bool FWD, int D>
+__global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ lu, int64_t n,
+                                                     const double* __restrict__ vin,
+                                                     const double* addend,
+                                                     double* out,
+                                                     double* __restrict__ desc,
+                                                     unsigned long long* __restrict__ flags,
+                                                     unsigned long long* __restrict__ ctl) {
+  // ctl[0] = ticket counter, ctl[1] = epoch
+  // dynamic shared memory: sv (rhs, then the result) | sc[D] (recurrence coefficients) |
+  // su0 (U(i,i), backward only)
+  extern __shared__ double smem_dyn[];
+  double* sv = smem_dyn;
+  double (*sc)[STPB * SPAD] = reinterpret_cast<double (*)[STPB * SPAD]>(smem_dyn + STPB * SPAD);
+  double* su0 = smem_dyn + (1 + D) * STPB * SPAD;
+  __shared__ Map<D> wtot[STPB / 32];
+  __shared__ double s_in[D];
+  __shared__ long long s_tile;
+  __shared__ unsigned long long s_epoch;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  if (t == 0) {
+    s_epoch = ((volatile unsigned long long*)ctl)[1];
+    unsigned long long tk = atomicAdd(ctl, 1ull);
+    s_tile = (long long)tk;
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const int64_t tile = FWD ? (int64_t)s_tile : (ntiles - 1 - (int64_t)s_tile);
+  const int64_t base = tile * STILE;
+
+  // ---- stage the tile (coalesced), rows in processing order per thread ----
+  for (int q = t; q < STILE; q += STPB) {
+    const int64_t i = base + q;
+    const int sidx = (q / SR) * SPAD + (q % SR);
+    const bool in = i < n;
+    sv[sidx] = in ? vin[i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
+      const int o = FWD ? (D - 1 - k) : (D + 1 + k);
+      sc[k][sidx] = in ? lu[(int64_t)o * n + i] : 0.0;
+    }
+    if (!FWD) su0[sidx] = in ? lu[(int64_t)D * n + i] : 1.0;
+  }
+  __syncthreads();
+
+  // ---- per-thread affine map over its SR rows (FWD: ascending, BWD: descending) ----
+  Map<D> my;
+  {
+    double sz[D];            // zero-state run
+    double su[D][D];         // unit-state runs: su[q] starts at e_q
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      sz[k] = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) su[q][k] = (q == k) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int rr = 0; rr < SR; ++rr) {
+      const int r = FWD ? rr : (SR - 1 - rr);
+      const int sidx = t * SPAD + r;
+      double c[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
+      const double u0 = FWD ? 1.0 : su0[sidx];
+      push_state<D>(sz, rec_step<FWD, D>(sv[sidx], c, sz, u0));
+#pragma unroll
+      for (int q = 0; q < D; ++q) push_state<D>(su[q], rec_step<FWD, D>(0.0, c, su[q], u0));
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      my.t[i] = sz[i];
+#pragma unroll
+      for (int q = 0; q < D; ++q) my.M[i][q] = su[q][i];
+    }
+  }
+  // ---- block scan (order: FWD thread 0 first, BWD thread STPB-1 first) ----
+  // Work in "processing order" p: FWD p = t, BWD p = STPB-1-t.  A warp holds p in a
+  // contiguous range either way; for BWD lanes run in reverse, so scan with shfl_down.
+  Map<D> inc = my;  // inclusive prefix within the warp, in processing order
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Map<D> o;
+    if (FWD) o = shfl_up_map<D>(inc, off);
+    else {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        o.t[i] = __shfl_down_sync(0xffffffffu, inc.t[i], off);
+#pragma unroll
+        for (int j = 0; j < D; ++j) o.M[i][j] = __shfl_down_sync(0xffffffffu, inc.M[i][j], off);
+      }
+    }
+    const bool has = FWD ? (lane >= off) : (lane + off < 32);
+    if (has) inc = compose<D>(inc, o);
+  }
+  // exclusive-in-warp = inclusive of the previous lane (processing order)
+  Map<D> exw;
+  if (FWD) exw = shfl_up_map<D>(inc, 1);
+  else {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      exw.t[i] = __shfl_down_sync(0xffffffffu, inc.t[i], 1);
+#pragma unroll
+      for (int j = 0; j < D; ++j) exw.M[i][j] = __shfl_down_sync(0xffffffffu, inc.M[i][j], 1);
+    }
+  }
+  const bool first_in_warp = FWD ? (lane == 0) : (lane == 31);
+  if (first_in_warp) exw = identity_map<D>();
+  const bool last_in_warp = FWD ? (lane == 31) : (lane == 0);
+  if (last_in_warp) wtot[warp] = inc;
+  __syncthreads();
+  // prefix over warps in processing order (FWD warps 0..3, BWD warps 3..0): small, every thread
+  Map<D> wpre = identity_map<D>();
+  constexpr int NW = STPB / 32;
+  if (FWD) {
+    for (int w = 0; w < warp; ++w) wpre = compose<D>(wtot[w], wpre);
+  } else {
+    for (int w = NW - 1; w > warp; --w) wpre = compose<D>(wtot[w], wpre);
+  }
+  // the tile aggregate (computed by thread 0)
+  if (t == 0) {
+    Map<D> agg = identity_map<D>();
+    if (FWD) for (int w = 0; w < NW; ++w) agg = compose<D>(wtot[w], agg);
+    else for (int w = NW - 1; w >= 0; --w) agg = compose<D>(wtot[w], agg);
+    constexpr int DW = D * D + 2 * D;
+    double* my_desc = desc + tile * DW;
+    volatile unsigned long long* fl = flags;
+    double sin[D];
+    // tiles are processed in order (first = FWD tile 0, BWD tile ntiles-1)
+    const bool first_tile = FWD ? (tile == 0) : (tile == ntiles - 1);
+    if (first_tile) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) sin[i] = 0.0;   // nothing before the matrix start / end
+    } else {
+      // publish the aggregate
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        my_desc[D * D + i] = agg.t[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) my_desc[i * D + j] = agg.M[i][j];
+      }
+      __threadfence();
+      fl[tile] = (epoch << 2) | FLAG_AGG;
+      // look back
+      Map<D> acc = identity_map<D>();
+      int64_t j = FWD ? tile - 1 : tile + 1;
+      while (true) {
+        unsigned long long f;
+        do { f = fl[j]; } while ((f >> 2) != epoch || (f & 3ull) == 0ull);
+        __threadfence();
+        volatile const double* dj = desc + j * DW;
+        if ((f & 3ull) == FLAG_INCL) {
+          double S[D];
+#pragma unroll
+          for (int i = 0; i < D; ++i) S[i] = dj[D * D + D + i];
+          apply<D>(acc, S, sin);
+          break;
+        }
+        Map<D> mj;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          mj.t[i] = dj[D * D + i];
+#pragma unroll
+          for (int q = 0; q < D; ++q) mj.M[i][q] = dj[i * D + q];
+        }
+        acc = compose<D>(acc, mj);
+        j = FWD ? j - 1 : j + 1;
+      }
+    }
+    double sout[D];
+    apply<D>(agg, sin, sout);
+#pragma unroll
+    for (int i = 0; i < D; ++i) my_desc[D * D + D + i] = sout[i];
+    __threadfence();
+    fl[tile] = (epoch << 2) | FLAG_INCL;
+#pragma unroll
+    for (int i = 0; i < D; ++i) s_in[i] = sin[i];
+  }
+  __syncthreads();
+  // ---- recompute the rows from the exact incoming state ----
+  {
+    double s0[D], s[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) s0[i] = s_in[i];
+    Map<D> pre = compose<D>(exw, wpre);   // warp prefix first, then the in-warp prefix
+    apply<D>(pre, s0, s);
+#pragma unroll
+    for (int rr = 0; rr < SR; ++rr) {
+      const int r = FWD ? rr : (SR - 1 - rr);
+      const int sidx = t * SPAD + r;
+      double c[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
+      const double u0 = FWD ? 1.0 : su0[sidx];
+      const double y = rec_step<FWD, D>(sv[sidx], c, s, u0);
+      push_state<D>(s, y);
+      sv[sidx] = y;
+    }
+  }
+  __syncthreads();
+  for (int q = t; q < STILE; q += STPB) {
+    const int64_t i = base + q;
+    if (i < n) {
+      const double y = sv[(q / SR) * SPAD + (q % SR)];
+      out[i] = addend ? addend[i] + y : y;
+    }
+  }
+  // the last block re-arms the ticket counter and advances the epoch
+  if (t == 0) {
+    __threadfence();
+    unsigned long long done = atomicAdd(ctl + 2, 1ull);
+    if (done == (unsigned long long)ntiles - 1) {
+      ctl[2] = 0ull;
+      ctl[0] = 0ull;
+      ctl[1] = epoch + 1;
+      __threadfence();
+    }
+  }
+}
+
+template <int D>
+void factor_launch(const double* bands, int64_t n, double* lu, const double* a, double* b,
+                   int first, int* changed, int* bad, cudaStream_t s) {
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int tpb = 64;
+  factor_pass_kernel<D><<<(unsigned)((nchunks + tpb - 1) / tpb), tpb, 0, s>>>(bands, n, lu, a, b, first,
+                                                                              changed, bad);
+}
+
+template <bool FWD, int D>
+void sweep_launch(const double* lu, int64_t n, const double* v, const double* add, double* out,
+                  BandedScratch sc, cudaStream_t s) {
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const size_t smem = (size_t)(1 + D + (FWD ? 0 : 1)) * STPB * SPAD * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(sweep_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  sweep_kernel<FWD, D><<<(unsigned)ntiles, STPB, smem, s>>>(lu, n, v, add, out, sc.states,
+                                                        sc.tickets + 8, sc.tickets);
+}
+
+}  // namespace
+
+// scratch: [ctl 4 x u64 | changed/bad 2 x int (16 B) | flags ntiles x u64 | desc ntiles x DW |
+//           fixed-point states 2 x nchunks x D(D+1) | y n]
+size_t banded_scratch_bytes(int64_t n, int d) {
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t DW = d * d + 2 * d;
+  size_t b = 64 + 256;
+  b += (size_t)ntiles * 8 + 256;
+  b += (size_t)ntiles * DW * 8 + 256;
+  b += (size_t)2 * nchunks * d * (d + 1) * 8 + 256;
+  b += (size_t)n * 8 + 256;
+  return b;
+}
+
+static inline char* align256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255); }
+
+BandedScratch banded_scratch(void* base, int64_t n, int d) {
+  BandedScratch sc;
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t DW = d * d + 2 * d;
+  char* p = align256((char*)base);
+  sc.tickets = (unsigned long long*)p;          // [0..3] ctl, [4..] flags
+  sc.changed = (int*)(p + 32);                  // [0] changed, [1] bad
+  p = align256(p + 64 + (size_t)ntiles * 8 + 64);
+  sc.states = (double*)p;                       // descriptors (solve)
+  p = align256(p + (size_t)ntiles * DW * 8);
+  sc.y = (double*)p;                            // intermediate vector, then factor states
+  sc.desc_count = ntiles;
+  (void)nchunks;
+  return sc;
+}
+
+// The control words must be zero before the first use of a scratch (ctl epoch starts at 0).
+static double* factor_states(BandedScratch sc, int64_t n) {
+  return sc.y + ((n + 31) / 32) * 32;
+}
+
+int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScratch sc,
+                  cudaStream_t s, int* passes, int64_t* launches) {
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  double* A = factor_states(sc, n);
+  double* B = A + nchunks * d * (d + 1);
+  int h[2] = {0, 0};
+  int p = 0;
+  for (;;) {
+    cudaMemsetAsync(sc.changed, 0, 2 * sizeof(int), s);
+    switch (d) {
+      case 1: factor_launch<1>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
+      case 2: factor_launch<2>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
+      case 3: factor_launch<3>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
+      default: factor_launch<4>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
+    }
+    if (launches) *launches += 1;
+    ++p;
+    cudaMemcpyAsync(h, sc.changed, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double* tmp = A;
+    A = B;
+    B = tmp;
+    if (h[0] == 0 || p > nchunks + 1) break;
+  }
+  if (passes) *passes = p;
+  return h[1] ? PSP_E_SINGULAR : PSP_OK;
+}
+
+void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* x0, double* z,
+                  BandedScratch sc, cudaStream_t s, int64_t* launches) {
+  switch (d) {
+    case 1:
+      sweep_launch<true, 1>(lu, n, v, nullptr, sc.y, sc, s);
+      sweep_launch<false, 1>(lu, n, sc.y, x0, z, sc, s);
+      break;
+    case 2:
+      sweep_launch<true, 2>(lu, n, v, nullptr, sc.y, sc, s);
+      sweep_launch<false, 2>(lu, n, sc.y, x0, z, sc, s);
+      break;
+    case 3:
+      sweep_launch<true, 3>(lu, n, v, nullptr, sc.y, sc, s);
+      sweep_launch<false, 3>(lu, n, sc.y, x0, z, sc, s);
+      break;
+    default:
+      sweep_launch<true, 4>(lu, n, v, nullptr, sc.y, sc, s);
+      sweep_launch<false, 4>(lu, n, sc.y, x0, z, sc, s);
+      break;
+  }
+  if (launches) *launches += 2;
+}
+
+}  // namespace psp

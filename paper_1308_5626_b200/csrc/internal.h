@@ -1,0 +1,143 @@
+// internal.h -- shared declarations of libpspgmres's translation units (not part of the ABI).
+//
+// The public boundary is include/pspgmres.h.  Everything here is sm_100a CUDA + host C++
+// of the product; nothing is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pspgmres.h"
+
+namespace psp {
+
+constexpr int kMaxD = 4;         // MREP / banded half-bandwidth supported by the kernels
+constexpr int kMaxRestart = 128; // n_A limit (device Hessenberg state is O(n_A^2))
+constexpr int kRedThreads = 256; // block size of the grid-reduction kernels
+
+// ------------------------------------------------------------------------------------------
+// Operator data (A = I - dt L, Eq.4).  Coefficients are precomputed on the host.
+// ------------------------------------------------------------------------------------------
+struct Stencil {
+  int kind;            // PSP_OP_*
+  int ndim;
+  int64_t nx, ny, nz;  // LOCAL extents (nz = this rank's planes for 3-D; ny lines for 2-D)
+  int64_t n;           // local rows
+  double s[3];         // dt * nu / h_a^2 (CONST_DIFF) or dt / h_a^2 (CELL_*)
+  double a[3];         // dt * c_a / h_a (CELL_ADVDIFF)
+  const double* field; // kappa / nu of the local rows (CELL_*)
+  int dA;              // DIA half-bandwidth
+  const double* bands; // DIA bands (2dA+1) x n
+  // slab halo (multi-rank): the plane / line of x and field just below / above the local
+  // block, NULL on the global boundary.
+  const double* x_lo;
+  const double* x_hi;
+  const double* f_lo;
+  const double* f_hi;
+};
+
+// y = A (xs * x); optionally xcopy = xs * x (the probe column P_x).
+void launch_matvec(const Stencil& st, const double* x, double xs, double* y, double* xcopy,
+                   cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// Device state of one GMRES cycle (Hessenberg, Givens, scalars) -- lives in the workspace.
+// ------------------------------------------------------------------------------------------
+struct DevState {
+  double* H;         // (nA+1) x nA column-major, rotated in place
+  double* Hraw;      // pre-rotation copy (test hook, R4 breakdown test)
+  double* G;         // nA+1
+  double* C;         // nA
+  double* S;         // nA
+  double* Q;         // nA (back-substitution, R6)
+  double* Lm;        // (nA+1) x (nA+1): strictly-lower part of V'V (ICWY MGS, R11)
+  double* scal;      // scalars, see enum below
+  double* resid;     // R(k) of the current cycle, nA
+  double* partials;  // grid-reduction partials: kMaxPartialVals x nblocks
+  unsigned* tickets; // last-block counters (one per reduction slot)
+};
+enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
+       SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_NSCAL = 16 };
+enum { TK_MAIN = 0, TK_AUX = 1, TK_MREP = 2, TK_N = 8 };
+
+struct RedCfg {
+  int nblocks;       // grid of every reduction kernel (multiple of the SM count)
+  int max_vals;      // partials per block the partials buffer holds
+};
+
+// ---- Krylov kernels (krylov.cu) ----
+// ||x||_2 -> scal[slot] (deterministic tree order; sqrt applied)
+void launch_norm(const double* x, int64_t n, DevState ds, int slot, const RedCfg& rc, cudaStream_t s);
+// r = b - y into v (unnormalised), beta = ||r|| -> scal[SC_BETA], G(1) = beta
+void launch_residual(const double* b, const double* y, double* v, int64_t n, int nA, DevState ds,
+                     const RedCfg& rc, cudaStream_t s);
+// v /= scal[slot]   (V(:,1) = R_bar / ||R_bar||)
+void launch_divide(double* v, int64_t n, const double* d_div, cudaStream_t s);
+// literal MGS: one launch per j; src -> dst (U) with the lagged axpy of j-1
+void launch_mgs_literal(const double* src, double* U, const double* Vprev, const double* Vj,
+                        int j, int k, int nA, int64_t n, DevState ds, const RedCfg& rc,
+                        cudaStream_t s);
+// literal MGS tail: U -= H(k,k) V_k; H(k+1,k) = ||U||; then the Givens update
+void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_t n,
+                              DevState ds, const RedCfg& rc, cudaStream_t s);
+// ICWY one-reduction MGS (R11): pass A = dots V_j'w (j<=k), V_j'V_k (j<k); solve (I+L)h = s
+void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int nA, int64_t n,
+                      DevState ds, const RedCfg& rc, cudaStream_t s);
+// pass B = U = w - sum_j h_j V_j ; H(k+1,k) = ||U|| ; Givens update
+void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
+                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
+// V(:,k+1) = U / H(k+1,k), or 0 on breakdown (R4)
+void launch_normalize(const double* U, double* Vk1, int k, int nA, int64_t n, DevState ds,
+                      cudaStream_t s);
+// Q = H^{-1} G (R6) and out = base + sum_j Q_j V_j; base may be NULL (Z only)
+void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
+                    int64_t n, DevState ds, cudaStream_t s);
+// y = x (plain copy on the stream)
+void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s);
+// ||b - y|| -> scal[slot]
+void launch_diff_norm(const double* b, const double* y, int64_t n, DevState ds, int slot,
+                      const RedCfg& rc, cudaStream_t s);
+
+// ---- MREP (mrep.cu) ----
+struct MrepOut {
+  double* bands;      // (2d+1) x n
+  double* intercept;  // n or NULL
+  uint8_t* kind;      // n or NULL
+  double* kappa;      // n or NULL
+};
+struct MrepScratch {
+  double* partials;   // 6 x kMrepMaxBlocks
+  unsigned* ticket;
+  double* result;     // 16: [0] max|diag| [1] max|diag| over non-dominant rows [2] min|diag|
+                      // [3] rows_ridge [4] rows_fallback [5] rows_nondominant (pre-R18)
+                      // [6] R18 patch needed [7] gate accepted (R21) [8] rows patched by R18
+};
+constexpr int kMrepMaxBlocks = 148 * 8;
+int mrep_blocks(int64_t n, int d);
+// Alg.2 on probe columns px + slots[c]*ld (c = 0..m-1 oldest -> newest), then R18 + gate stats.
+void mrep_launch(const double* px, const double* py, int64_t ld, const int32_t* slots, int m,
+                 int64_t n, int d, MrepOut out, MrepScratch sc, cudaStream_t s);
+
+// ---- banded LU (banded.cu) ----
+struct BandedScratch {
+  double* states;     // fixed-point states (factor) / look-back descriptors (solve)
+  unsigned long long* tickets;
+  int* changed;
+  double* y;          // n: intermediate of the two sweeps
+  int64_t desc_count;
+};
+size_t banded_scratch_bytes(int64_t n, int d);
+BandedScratch banded_scratch(void* base, int64_t n, int d);
+// factor; returns PSP_OK / PSP_E_SINGULAR (synchronises); *passes = fixed-point passes
+int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScratch sc,
+                  cudaStream_t s, int* passes, int64_t* launches);
+// z = x0 + N^{-1} v (x0 may be NULL); v may be scaled by vs on load
+void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* x0,
+                  double* z, BandedScratch sc, cudaStream_t s, int64_t* launches);
+
+// ---- misc ----
+std::string cuda_err_str(cudaError_t e);
+
+}  // namespace psp

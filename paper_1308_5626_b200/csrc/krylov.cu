@@ -1,0 +1,445 @@
+// krylov.cu -- K2 (Gram-Schmidt), K5 (Givens / back-substitution) and the vector passes of
+// Algorithm 1.
+//
+// Every reduction is deterministic: a fixed grid of rc.nblocks blocks (a multiple of the 148
+// SMs) writes one partial per block, and the last block to finish (atomic ticket) sums the
+// partials in a fixed tree.  Bitwise run-to-run determinism follows.  The last block
+// also runs the O(k) scalar epilogue (Givens rotation, triangular solves) on one thread, so
+// an Arnoldi step costs no extra launch for its scalar work.
+#include <math.h>
+
+#include "internal.h"
+
+namespace psp {
+namespace {
+
+constexpr int TPB = kRedThreads;  // 256
+constexpr int kWarps = TPB / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum of NV values held per thread; result valid in thread 0
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* kWarps*NV */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) smem[warp * NV + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += smem[w * NV + q];
+      v[q] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Publish this block's partials; returns true in every thread of the last block to finish.
+__device__ bool finish_block(unsigned* ticket) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// Last block: total of partials[v*nb + b] over b, in a fixed tree.  All threads call; the
+// result is valid in thread 0.
+__device__ double reduce_partials(const double* partials, int v, int nb, double* smem) {
+  double a[1] = {0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) a[0] += ((volatile const double*)partials)[v * nb + b];
+  block_sum<1>(a, smem);
+  return a[0];
+}
+
+// ------------------------------------------------------------------------------------------
+// Givens update of column k (Alg.1 l.19-32; R4, R10).  One thread.
+// ------------------------------------------------------------------------------------------
+__device__ void givens_update(DevState ds, int k, int nA) {
+  const int ld = nA + 1;
+  double* Hc = ds.H + (int64_t)(k - 1) * ld;
+  double colsq = 0.0;
+  for (int j = 0; j <= k; ++j) {
+    ds.Hraw[(int64_t)(k - 1) * ld + j] = Hc[j];
+    colsq += Hc[j] * Hc[j];
+  }
+  const double hk1 = Hc[k];
+  bool breakdown = !(hk1 > 1e-14 * sqrt(colsq));   // R4, before rotation
+  const bool nonfinite = !isfinite(hk1);
+  ds.G[k] = 0.0;                                    // l.9: G(k+1) <- 0
+  for (int j = 1; j <= k - 1; ++j) {                // l.19-23
+    const double delta = Hc[j - 1];
+    Hc[j - 1] = delta * ds.C[j - 1] + ds.S[j - 1] * Hc[j];
+    Hc[j] = -delta * ds.S[j - 1] + ds.C[j - 1] * Hc[j];
+  }
+  const double a = Hc[k - 1], b = Hc[k];            // l.24-28, R10
+  const double gamma = sqrt(a * a + b * b);
+  if (gamma == 0.0) {
+    ds.C[k - 1] = 1.0;
+    ds.S[k - 1] = 0.0;
+    breakdown = true;
+  } else {
+    ds.C[k - 1] = a / gamma;
+    ds.S[k - 1] = b / gamma;
+  }
+  Hc[k - 1] = gamma;
+  Hc[k] = 0.0;
+  const double delta = ds.G[k - 1];                 // l.29-31
+  ds.G[k - 1] = ds.C[k - 1] * delta + ds.S[k - 1] * ds.G[k];
+  ds.G[k] = -ds.S[k - 1] * delta + ds.C[k - 1] * ds.G[k];
+  const double R = fabs(ds.G[k]);                   // l.32
+  ds.resid[k - 1] = R;
+  ds.scal[SC_RK] = R;
+  int flags = 0;
+  if (R <= ds.scal[SC_EPS]) flags |= PSP_FLAG_CONVERGED;  // l.33
+  if (breakdown) flags |= PSP_FLAG_BREAKDOWN;
+  if (nonfinite || !isfinite(R)) flags |= PSP_FLAG_NONFINITE;
+  ds.scal[SC_FLAGS] = (double)flags;
+}
+
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TPB) norm_kernel(const double* __restrict__ x, int64_t n,
+                                                   DevState ds, int slot) {
+  __shared__ double sm[kWarps];
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double v = x[r];
+    a[0] = fma(v, v, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_AUX)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) ds.scal[slot] = sqrt(t);
+  }
+}
+
+__global__ void __launch_bounds__(TPB) diff_norm_kernel(const double* __restrict__ b,
+                                                        const double* __restrict__ y, int64_t n,
+                                                        DevState ds, int slot) {
+  __shared__ double sm[kWarps];
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double v = b[r] - y[r];
+    a[0] = fma(v, v, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_AUX)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) ds.scal[slot] = sqrt(t);
+  }
+}
+
+// Alg.1 l.5-7: R_bar = B - P_y(:,i) -> v (unnormalised), beta = ||R_bar||, G(1) = beta.
+__global__ void __launch_bounds__(TPB) residual_kernel(const double* __restrict__ b,
+                                                       const double* __restrict__ y,
+                                                       double* __restrict__ v, int64_t n,
+                                                       DevState ds, int nA) {
+  __shared__ double sm[kWarps];
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double t = b[r] - y[r];
+    v[r] = t;
+    a[0] = fma(t, t, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) {
+      const double beta = sqrt(t);
+      ds.scal[SC_BETA] = beta;
+      for (int j = 0; j <= nA; ++j) ds.G[j] = 0.0;  // l.44 "clean"
+      ds.G[0] = beta;                                // l.7
+    }
+  }
+}
+
+__global__ void divide_kernel(double* __restrict__ v, int64_t n, const double* __restrict__ div) {
+  const double dv = *div;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    v[r] = v[r] / dv;
+}
+
+__global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    y[r] = x[r];
+}
+
+// ------------------------------------------------------------------------------------------
+// Literal MGS (Alg.1 l.13-16), one grid pass per j:
+//   U <- src - H(j-1,k) V_{j-1}   (the update of step j-1, lagged into this pass)
+//   H(j,k) <- V_j' U
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TPB) mgs_literal_kernel(const double* src, double* U,
+                                                          const double* __restrict__ Vprev,
+                                                          const double* __restrict__ Vj, int j,
+                                                          int k, int nA, int64_t n, DevState ds) {
+  __shared__ double sm[kWarps];
+  const int ld = nA + 1;
+  const double hprev = Vprev ? ds.H[(int64_t)(k - 1) * ld + (j - 2)] : 0.0;
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double u = src[r];
+    if (Vprev) u = u - hprev * Vprev[r];
+    U[r] = u;
+    a[0] = fma(Vj[r], u, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) ds.H[(int64_t)(k - 1) * ld + (j - 1)] = t;
+  }
+}
+
+// U <- U - H(k,k) V_k ; H(k+1,k) = ||U|| (l.17) ; Givens (l.19-32)
+__global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restrict__ U,
+                                                                const double* __restrict__ Vk,
+                                                                int k, int nA, int64_t n,
+                                                                DevState ds) {
+  __shared__ double sm[kWarps];
+  const int ld = nA + 1;
+  const double h = ds.H[(int64_t)(k - 1) * ld + (k - 1)];
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double u = U[r] - h * Vk[r];
+    U[r] = u;
+    a[0] = fma(u, u, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) {
+      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(t);
+      givens_update(ds, k, nA);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// ICWY one-reduction MGS (R11; Swirydowicz-Langou-Ananthan-Yang-Thomas 2020 form):
+//   MGS coefficients h satisfy (I + L) h = V'w with L = strictly-lower part of V'V, exactly
+//   as the sequential MGS recurrence h_j = V_j'w - sum_{i<j} (V_j'V_i) h_i.
+// Pass A: s_j = V_j'w (j < k) and l_j = V_{k}'V_j (j < k-1, the new row of L), one pass over
+// k+1 vectors with w and V_k staged in shared memory; the last block solves (I+L)h = s.
+// ------------------------------------------------------------------------------------------
+constexpr int kTileRows = 1024;
+
+__global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict__ V, int64_t ldv,
+                                                        const double* __restrict__ w, int k,
+                                                        int nA, int64_t n, DevState ds) {
+  __shared__ double ws[kTileRows];
+  __shared__ double qs[kTileRows];
+  __shared__ double acc[2 * kMaxRestart];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = 2 * k - 1;  // s_0..s_{k-1}, l_0..l_{k-2}
+  for (int q = threadIdx.x; q < 2 * k; q += TPB) acc[q] = 0.0;
+  const double* __restrict__ qk = V + (int64_t)(k - 1) * ldv;
+  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t r0 = t * kTileRows;
+    const int rows = (int)((n - r0) < kTileRows ? (n - r0) : kTileRows);
+    __syncthreads();
+    for (int q = threadIdx.x; q < kTileRows; q += TPB) {
+      ws[q] = q < rows ? w[r0 + q] : 0.0;
+      qs[q] = q < rows ? qk[r0 + q] : 0.0;
+    }
+    __syncthreads();
+    for (int jb = warp; jb < k; jb += kWarps) {
+      const double* __restrict__ vj = V + (int64_t)jb * ldv + r0;
+      double a1 = 0.0, a2 = 0.0;
+      if (jb < k - 1) {
+#pragma unroll 4
+        for (int q = lane; q < rows; q += 32) {
+          const double v = vj[q];
+          a1 = fma(v, ws[q], a1);
+          a2 = fma(v, qs[q], a2);
+        }
+      } else {
+#pragma unroll 4
+        for (int q = lane; q < rows; q += 32) a1 = fma(qs[q], ws[q], a1);
+      }
+      a1 = warp_sum(a1);
+      a2 = warp_sum(a2);
+      if (lane == 0) {
+        acc[jb] += a1;
+        if (jb < k - 1) acc[k + jb] += a2;
+      }
+    }
+  }
+  __syncthreads();
+  const int nb = gridDim.x;
+  for (int q = threadIdx.x; q < nv; q += TPB) ds.partials[(int64_t)q * nb + blockIdx.x] = acc[q];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    // totals: one warp per value, fixed order
+    __shared__ double tot[2 * kMaxRestart];
+    for (int q = warp; q < nv; q += kWarps) {
+      double s = 0.0;
+      for (int b = lane; b < nb; b += 32) s += ((volatile double*)ds.partials)[(int64_t)q * nb + b];
+      s = warp_sum(s);
+      if (lane == 0) tot[q] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int ldl = nA + 1;
+      double* Lrow = ds.Lm + (int64_t)(k - 1) * ldl;
+      for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = tot[k + jb];
+      double* Hc = ds.H + (int64_t)(k - 1) * (nA + 1);
+      // forward substitution (I + L) h = s
+      for (int jb = 0; jb < k; ++jb) {
+        double h = tot[jb];
+        const double* Lr = ds.Lm + (int64_t)jb * ldl;
+        for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
+        Hc[jb] = h;
+      }
+    }
+  }
+}
+
+// Pass B: U = w - sum_j h_j V_j (sequential in j, as the MGS updates), H(k+1,k) = ||U||,
+// then the Givens update of column k.
+__global__ void __launch_bounds__(TPB) icwy_update_kernel(const double* __restrict__ V, int64_t ldv,
+                                                          const double* __restrict__ w,
+                                                          double* __restrict__ U, int k, int nA,
+                                                          int64_t n, DevState ds) {
+  __shared__ double hs[kMaxRestart];
+  __shared__ double sm[kWarps];
+  const int ld = nA + 1;
+  for (int q = threadIdx.x; q < k; q += TPB) hs[q] = ds.H[(int64_t)(k - 1) * ld + q];
+  __syncthreads();
+  double a[1] = {0.0};
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double u = w[r];
+#pragma unroll 8
+    for (int jb = 0; jb < k; ++jb) u = fma(-hs[jb], V[(int64_t)jb * ldv + r], u);
+    U[r] = u;
+    a[0] = fma(u, u, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) {
+      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(t);
+      givens_update(ds, k, nA);
+    }
+  }
+}
+
+// l.18: V(:,k+1) <- U / H(k+1,k); V(:,k+1) = 0 on breakdown (R4)
+__global__ void normalize_kernel(const double* U, double* V1, int k,
+                                 int nA, int64_t n, DevState ds) {
+  // H(k+1,k) before rotation (the rotated entry is 0, l.28)
+  const double hraw = ds.Hraw[(int64_t)(k - 1) * (nA + 1) + k];
+  const int flags = (int)ds.scal[SC_FLAGS];
+  const bool bd = (flags & (PSP_FLAG_BREAKDOWN | PSP_FLAG_NONFINITE)) != 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    V1[r] = bd ? 0.0 : U[r] / hraw;
+}
+
+// l.38-42: Q = H^{-1} G (R6, every block recomputes the k x k back-substitution
+// redundantly: identical inputs, identical result), out = base + sum_j Q_j V_j.
+__global__ void __launch_bounds__(TPB) combine_kernel(const double* __restrict__ V, int64_t ldv,
+                                                      int k, int nA,
+                                                      const double* base, double* out, int64_t n,
+                                                      DevState ds) {
+  __shared__ double qs[kMaxRestart];
+  __shared__ int bad;
+  if (threadIdx.x == 0) {
+    const int ld = nA + 1;
+    bad = 0;
+    for (int j = k; j >= 1; --j) {
+      double s = ds.G[j - 1];
+      for (int t = j + 1; t <= k; ++t) s -= ds.H[(int64_t)(t - 1) * ld + (j - 1)] * qs[t - 1];
+      const double piv = ds.H[(int64_t)(j - 1) * ld + (j - 1)];
+      if (piv == 0.0) { bad = 1; qs[j - 1] = 0.0; continue; }
+      qs[j - 1] = s / piv;
+    }
+    if (blockIdx.x == 0) {
+      for (int j = 0; j < k; ++j) ds.Q[j] = qs[j];
+      ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    double z = 0.0;
+#pragma unroll 8
+    for (int jb = 0; jb < k; ++jb) z = fma(qs[jb], V[(int64_t)jb * ldv + r], z);
+    out[r] = base ? base[r] + z : z;
+  }
+}
+
+inline int grid_for(int64_t n, int cap) {
+  int64_t b = (n + TPB - 1) / TPB;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+void launch_norm(const double* x, int64_t n, DevState ds, int slot, const RedCfg& rc, cudaStream_t s) {
+  norm_kernel<<<rc.nblocks, TPB, 0, s>>>(x, n, ds, slot);
+}
+void launch_diff_norm(const double* b, const double* y, int64_t n, DevState ds, int slot,
+                      const RedCfg& rc, cudaStream_t s) {
+  diff_norm_kernel<<<rc.nblocks, TPB, 0, s>>>(b, y, n, ds, slot);
+}
+void launch_residual(const double* b, const double* y, double* v, int64_t n, int nA, DevState ds,
+                     const RedCfg& rc, cudaStream_t s) {
+  residual_kernel<<<rc.nblocks, TPB, 0, s>>>(b, y, v, n, ds, nA);
+}
+void launch_divide(double* v, int64_t n, const double* d_div, cudaStream_t s) {
+  divide_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(v, n, d_div);
+}
+void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s) {
+  copy_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(x, y, n);
+}
+void launch_mgs_literal(const double* src, double* U, const double* Vprev, const double* Vj,
+                        int j, int k, int nA, int64_t n, DevState ds, const RedCfg& rc,
+                        cudaStream_t s) {
+  mgs_literal_kernel<<<rc.nblocks, TPB, 0, s>>>(src, U, Vprev, Vj, j, k, nA, n, ds);
+}
+void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_t n,
+                              DevState ds, const RedCfg& rc, cudaStream_t s) {
+  mgs_literal_final_kernel<<<rc.nblocks, TPB, 0, s>>>(U, Vk, k, nA, n, ds);
+}
+void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int nA, int64_t n,
+                      DevState ds, const RedCfg& rc, cudaStream_t s) {
+  icwy_dots_kernel<<<rc.nblocks, TPB, 0, s>>>(V, ldv, w, k, nA, n, ds);
+}
+void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
+                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
+  icwy_update_kernel<<<rc.nblocks, TPB, 0, s>>>(V, ldv, w, U, k, nA, n, ds);
+}
+void launch_normalize(const double* U, double* Vk1, int k, int nA, int64_t n, DevState ds,
+                      cudaStream_t s) {
+  normalize_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(U, Vk1, k, nA, n, ds);
+}
+void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
+                    int64_t n, DevState ds, cudaStream_t s) {
+  combine_kernel<<<grid_for(n, 148 * 4), TPB, 0, s>>>(V, ldv, k, nA, base, out, n, ds);
+}
+
+}  // namespace psp

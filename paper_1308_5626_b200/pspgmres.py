@@ -1,0 +1,410 @@
+"""ctypes binding of libpspgmres (include/pspgmres.h).  Argument marshalling only.
+
+Every numeric step of the hot path runs in the library's sm_100a kernels; this module turns
+torch tensors into device pointers, numpy arrays into host pointers, and C structs into
+dicts.  PyTorch supplies device memory (the workspace is a torch uint8 tensor) and the CUDA
+stream.  There is no fallback: if libpspgmres.so is missing or the GPU is absent, ``lib()``
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpspgmres.so")
+
+# ---- enums (include/pspgmres.h) ----
+PSP_OK, PSP_E_ARG, PSP_E_DIM, PSP_E_SAMPLES, PSP_E_RANK, PSP_E_SINGULAR, PSP_E_NONFINITE, \
+    PSP_E_NOCONV, PSP_E_CUDA, PSP_E_NCCL, PSP_E_NOMEM = range(11)
+PSP_OP_CONST_DIFF, PSP_OP_CELL_DIFF, PSP_OP_CELL_ADVDIFF, PSP_OP_DIA = range(4)
+PSP_TOL_REL_B, PSP_TOL_ABS = 0, 1
+PSP_MGS_1REDUCE, PSP_MGS_LITERAL = 0, 1
+PSP_FLAG_CONVERGED, PSP_FLAG_BREAKDOWN, PSP_FLAG_NONFINITE = 1, 2, 4
+PSP_KC_COUNT = 11
+ROW_INTERIOR, ROW_INTERIOR_RIDGE, ROW_BOUNDARY, ROW_FALLBACK_RANK, ROW_FALLBACK_ZEROVAR, \
+    ROW_FALLBACK_SMALLDIAG = range(6)
+KIND_CODES = {"const_diff": PSP_OP_CONST_DIFF, "cell_diff": PSP_OP_CELL_DIFF,
+              "cell_advdiff": PSP_OP_CELL_ADVDIFF, "dia": PSP_OP_DIA}
+
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class psp_grid(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("pad_", C.c_int32), ("n", C.c_int64 * 3)]
+
+
+class psp_stencil(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dA", C.c_int32), ("nu", C.c_double), ("c", C.c_double * 3),
+                ("d_field", _vp), ("d_bands", _vp)]
+
+
+class psp_opts(C.Structure):
+    _fields_ = [("max_cycles", C.c_int32), ("tol_mode", C.c_int32), ("m_max", C.c_int32),
+                ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
+                ("timing", C.c_int32), ("pad_", C.c_int32)]
+
+
+class psp_report(C.Structure):
+    _fields_ = [("status", C.c_int32), ("converged", C.c_int32), ("iterations", C.c_int32),
+                ("cycles", C.c_int32), ("matvecs", C.c_int32), ("precond_applies", C.c_int32),
+                ("precond_identity", C.c_int32), ("resid_cap", C.c_int32), ("resid_len", C.c_int32),
+                ("beta_cap", C.c_int32), ("beta_len", C.c_int32), ("mrep_ran", C.c_int32),
+                ("mrep_status", C.c_int32), ("mrep_gate_accepted", C.c_int32),
+                ("mrep_rows_ridge", C.c_int64), ("mrep_rows_fallback", C.c_int64),
+                ("mrep_rows_nondominant", C.c_int64), ("r0", C.c_double), ("eps", C.c_double),
+                ("final_resid_est", C.c_double), ("final_resid_true", C.c_double),
+                ("mrep_max_abs_diag", C.c_double), ("t_solve_ms", C.c_double), ("t_mrep_ms", C.c_double),
+                ("t_factor_ms", C.c_double), ("h_resid_history", _dp), ("h_beta_history", _dp)]
+
+
+class psp_mrep_info(C.Structure):
+    _fields_ = [("rows_ridge", C.c_int64), ("rows_fallback", C.c_int64), ("rows_nondominant", C.c_int64),
+                ("max_abs_diag", C.c_double), ("gate_accepted", C.c_int32), ("status", C.c_int32)]
+
+
+class PspError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libpspgmres status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libpspgmres.so.  Fails loudly: there is no CPU fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                           "(or `make`) -- libpspgmres has no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    sig = {
+        "psp_default_opts": (None, [P(psp_opts)]),
+        "psp_workspace_bytes": (C.c_int, [P(psp_grid), P(psp_stencil), C.c_int, C.c_int, P(psp_opts), _vp,
+                                           P(C.c_size_t)]),
+        "psp_create": (C.c_int, [P(psp_grid), P(psp_stencil), C.c_double, C.c_int, C.c_int, C.c_double,
+                                 P(psp_opts), _vp, C.c_size_t, _vp, _vp, P(_vp)]),
+        "psp_destroy": (C.c_int, [_vp]),
+        "psp_local_rows": (C.c_int, [_vp, P(C.c_int64), P(C.c_int64)]),
+        "psp_matvec": (C.c_int, [_vp, _vp, _vp, C.c_int]),
+        "psp_precond_apply": (C.c_int, [_vp, _vp, _vp]),
+        "psp_cycle_begin": (C.c_int, [_vp, _vp, _vp, P(C.c_double)]),
+        "psp_arnoldi_step": (C.c_int, [_vp, C.c_int, P(C.c_double), P(C.c_int)]),
+        "psp_cycle_end": (C.c_int, [_vp, C.c_int, _vp]),
+        "psp_solve": (C.c_int, [_vp, _vp, _vp, _vp, P(psp_report)]),
+        "psp_mrep_fit": (C.c_int, [_vp, P(psp_report)]),
+        "psp_step": (C.c_int, [_vp, _vp, _vp, P(psp_report)]),
+        "psp_raw_scratch_bytes": (C.c_int, [C.c_int64, C.c_int, P(C.c_size_t)]),
+        "psp_mrep_fit_raw": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int64, P(C.c_int32), C.c_int, _vp, _vp,
+                                       _vp, _vp, _vp, C.c_size_t, _vp, P(psp_mrep_info)]),
+        "psp_banded_factor_raw": (C.c_int, [_vp, C.c_int64, C.c_int, _vp, _vp, C.c_size_t, _vp]),
+        "psp_banded_solve_raw": (C.c_int, [_vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
+        "psp_set_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
+        "psp_get_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
+        "psp_ring_view": (C.c_int, [_vp, P(C.c_int), P(C.c_int32), P(_vp), P(_vp), P(C.c_int64)]),
+        "psp_ring_reset": (C.c_int, [_vp]),
+        "psp_get_hessenberg": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),
+        "psp_get_basis": (C.c_int, [_vp, C.c_int, P(_vp)]),
+        "psp_launch_count": (C.c_int, [_vp, P(C.c_int64)]),
+        "psp_kernel_stats": (C.c_int, [_vp, _dp, _dp, P(C.c_int64), C.c_int]),
+        "psp_kernel_class_name": (C.c_char_p, [C.c_int]),
+        "psp_status_str": (C.c_char_p, [C.c_int]),
+        "psp_last_error": (C.c_char_p, [_vp]),
+        "psp_version": (C.c_char_p, []),
+        "psp_comm_unique_id": (C.c_int, [_vp]),
+        "psp_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, P(_vp)]),
+        "psp_comm_destroy": (C.c_int, [_vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destroy", "psp_local_rows",
+            "psp_matvec", "psp_precond_apply", "psp_cycle_begin", "psp_arnoldi_step", "psp_cycle_end",
+            "psp_solve", "psp_mrep_fit", "psp_step", "psp_raw_scratch_bytes", "psp_mrep_fit_raw",
+            "psp_banded_factor_raw", "psp_banded_solve_raw", "psp_set_bands", "psp_get_bands", "psp_ring_view",
+            "psp_ring_reset", "psp_get_hessenberg", "psp_get_basis", "psp_launch_count", "psp_kernel_stats",
+            "psp_kernel_class_name", "psp_status_str",
+            "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_destroy"]
+
+
+def _check(st, ctx=None, allow=(PSP_OK,)):
+    if st not in allow:
+        msg = lib().psp_last_error(ctx).decode()
+        raise PspError(st, msg)
+    return st
+
+
+def _ptr(t):
+    """device pointer of a torch CUDA tensor (or None)."""
+    if t is None:
+        return None
+    assert t.is_cuda, "libpspgmres takes device tensors"
+    assert t.is_contiguous()
+    return t.data_ptr()
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def default_opts(**kw) -> psp_opts:
+    o = psp_opts()
+    lib().psp_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, int(v))
+    return o
+
+
+def make_grid(n_axes) -> psp_grid:
+    g = psp_grid()
+    g.ndim = len(n_axes)
+    for a in range(3):
+        g.n[a] = int(n_axes[a]) if a < len(n_axes) else 1
+    return g
+
+
+def make_stencil(op, d_field=None, d_bands=None) -> psp_stencil:
+    s = psp_stencil()
+    s.kind = KIND_CODES[op.kind]
+    s.dA = int(getattr(op, "dA", 0) or 0)
+    s.nu = float(getattr(op, "nu", 1.0) or 0.0)
+    c = list(getattr(op, "c", (0, 0, 0)) or (0, 0, 0)) + [0.0] * 3
+    for a in range(3):
+        s.c[a] = float(c[a])
+    s.d_field = _ptr(d_field)
+    s.d_bands = _ptr(d_bands)
+    return s
+
+
+def report_dict(r: psp_report, hist=None, betas=None) -> dict:
+    out = {k: getattr(r, k) for k, _ in psp_report._fields_ if not k.startswith("h_")}
+    if hist is not None:
+        out["resid_history"] = hist[:min(r.resid_len, r.resid_cap)].copy()
+    if betas is not None:
+        out["beta_history"] = betas[:min(r.beta_len, r.beta_cap)].copy()
+    return out
+
+
+class Context:
+    """Owns a psp_ctx and its torch workspace.  Methods map 1:1 onto the C ABI."""
+
+    def __init__(self, op, d, restart, tol, opts: psp_opts | None = None, device="cuda", stream=None,
+                 hist_cap=1 << 16):
+        import torch
+        self.torch = torch
+        self.op = op
+        self.n = int(np.prod(op.n))
+        self.d = d
+        self.restart = restart
+        self.device = torch.device(device)
+        self.stream = stream
+        self._field = None
+        self._bands = None
+        if op.field is not None:
+            self._field = torch.as_tensor(np.asarray(op.field, dtype=np.float64)).to(self.device).contiguous()
+        if op.kind == "dia":
+            self._bands = torch.as_tensor(np.asarray(op.bands, dtype=np.float64)).to(self.device).contiguous()
+        self.grid = make_grid(op.n)
+        self.stencil = make_stencil(op, self._field, self._bands)
+        self.opts = opts if opts is not None else default_opts()
+        nbytes = C.c_size_t(0)
+        _check(lib().psp_workspace_bytes(C.byref(self.grid), C.byref(self.stencil), d, restart,
+                                         C.byref(self.opts), None, C.byref(nbytes)))
+        self.ws_bytes = nbytes.value
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        h = _vp()
+        _check(lib().psp_create(C.byref(self.grid), C.byref(self.stencil), float(op.dt), d, restart, float(tol),
+                                C.byref(self.opts), self.ws.data_ptr(), self.ws_bytes, _stream_ptr(stream), None,
+                                C.byref(h)))
+        self.h = h
+        self.hist = np.zeros(hist_cap)
+        self.betas = np.zeros(hist_cap)
+
+    def close(self):
+        if self.h:
+            lib().psp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _report(self):
+        r = psp_report()
+        r.h_resid_history = self.hist.ctypes.data_as(_dp)
+        r.resid_cap = len(self.hist)
+        r.h_beta_history = self.betas.ctypes.data_as(_dp)
+        r.beta_cap = len(self.betas)
+        return r
+
+    # ---- the C ABI, same names ----
+    def psp_matvec(self, x, y, record=False):
+        _check(lib().psp_matvec(self.h, _ptr(x), _ptr(y), int(record)), self.h)
+
+    def psp_precond_apply(self, v, z):
+        _check(lib().psp_precond_apply(self.h, _ptr(v), _ptr(z)), self.h)
+
+    def psp_cycle_begin(self, b, x0):
+        beta = C.c_double()
+        _check(lib().psp_cycle_begin(self.h, _ptr(b), _ptr(x0), C.byref(beta)), self.h)
+        return beta.value
+
+    def psp_arnoldi_step(self, k):
+        r = C.c_double()
+        f = C.c_int()
+        _check(lib().psp_arnoldi_step(self.h, k, C.byref(r), C.byref(f)), self.h)
+        return r.value, f.value
+
+    def psp_cycle_end(self, k, x):
+        _check(lib().psp_cycle_end(self.h, k, _ptr(x)), self.h)
+
+    def psp_solve(self, b, x0, x):
+        r = self._report()
+        st = lib().psp_solve(self.h, _ptr(b), _ptr(x0), _ptr(x), C.byref(r))
+        _check(st, self.h, allow=(PSP_OK, PSP_E_NOCONV))
+        return report_dict(r, self.hist, self.betas)
+
+    def psp_mrep_fit(self):
+        r = self._report()
+        st = lib().psp_mrep_fit(self.h, C.byref(r))
+        _check(st, self.h, allow=(PSP_OK, PSP_E_SAMPLES))
+        return report_dict(r)
+
+    def psp_step(self, u_n, u_np1):
+        r = self._report()
+        st = lib().psp_step(self.h, _ptr(u_n), _ptr(u_np1), C.byref(r))
+        _check(st, self.h, allow=(PSP_OK, PSP_E_NOCONV))
+        return report_dict(r, self.hist, self.betas)
+
+    def psp_set_bands(self, bands):
+        acc = C.c_int()
+        _check(lib().psp_set_bands(self.h, _ptr(bands), C.byref(acc)), self.h)
+        return bool(acc.value)
+
+    def psp_get_bands(self):
+        out = self.torch.empty((2 * self.d + 1, self.n), dtype=self.torch.float64, device=self.device)
+        ident = C.c_int()
+        _check(lib().psp_get_bands(self.h, _ptr(out), C.byref(ident)), self.h)
+        return out, bool(ident.value)
+
+    def psp_ring_view(self):
+        """(count, slots, P_x (cap, n) tensor view, P_y view) -- views into the workspace."""
+        cnt = C.c_int()
+        slots = (C.c_int32 * 256)()
+        px, py = _vp(), _vp()
+        ld = C.c_int64()
+        _check(lib().psp_ring_view(self.h, C.byref(cnt), slots, C.byref(px), C.byref(py), C.byref(ld)), self.h)
+        base = self.ws.data_ptr()
+        cap = self.opts.m_max
+        t = self.torch
+        off_x = (px.value - base) // 8
+        off_y = (py.value - base) // 8
+        ws64 = self.ws.view(t.float64) if (base % 8 == 0) else None
+        PX = ws64[off_x:off_x + cap * self.n].view(cap, self.n)
+        PY = ws64[off_y:off_y + cap * self.n].view(cap, self.n)
+        return cnt.value, list(slots[:cnt.value]), PX, PY
+
+    def psp_ring_reset(self):
+        _check(lib().psp_ring_reset(self.h), self.h)
+
+    def psp_get_hessenberg(self):
+        nA = self.restart
+        H = np.zeros(nA * (nA + 1))
+        Hraw = np.zeros(nA * (nA + 1))
+        G = np.zeros(nA + 1)
+        Cc = np.zeros(nA)
+        S = np.zeros(nA)
+        _check(lib().psp_get_hessenberg(self.h, H.ctypes.data_as(_dp), Hraw.ctypes.data_as(_dp),
+                                        G.ctypes.data_as(_dp), Cc.ctypes.data_as(_dp), S.ctypes.data_as(_dp)), self.h)
+        return dict(H=H.reshape(nA, nA + 1).T.copy(), Hraw=Hraw.reshape(nA, nA + 1).T.copy(), G=G, C=Cc, S=S)
+
+    def psp_get_basis(self, j):
+        p = _vp()
+        _check(lib().psp_get_basis(self.h, j, C.byref(p)), self.h)
+        base = self.ws.data_ptr()
+        off = (p.value - base) // 8
+        return self.ws.view(self.torch.float64)[off:off + self.n]
+
+    def psp_launch_count(self):
+        v = C.c_int64()
+        _check(lib().psp_launch_count(self.h, C.byref(v)), self.h)
+        return v.value
+
+    def psp_kernel_stats(self, reset=True):
+        """{class name: dict(ms, bytes, launches)} (needs opts.timing >= 2)."""
+        K = PSP_KC_COUNT
+        ms = np.zeros(K)
+        by = np.zeros(K)
+        cnt = (C.c_int64 * K)()
+        _check(lib().psp_kernel_stats(self.h, ms.ctypes.data_as(_dp), by.ctypes.data_as(_dp), cnt, int(reset)),
+               self.h)
+        return {lib().psp_kernel_class_name(k).decode(): dict(ms=float(ms[k]), bytes=float(by[k]),
+                                                             launches=int(cnt[k])) for k in range(K)}
+
+
+def raw_scratch(n, d, device="cuda"):
+    import torch
+    b = C.c_size_t()
+    _check(lib().psp_raw_scratch_bytes(n, d, C.byref(b)))
+    return torch.zeros(b.value, dtype=torch.uint8, device=device)
+
+
+def psp_mrep_fit_raw(px, py, d, order=None, scratch=None, stream=None, want_kind=True):
+    """px, py: (cap, n) CUDA tensors (row = probe column).  Returns dict of tensors + info."""
+    import torch
+    cap, n = px.shape
+    m = len(order) if order is not None else cap
+    order_a = (C.c_int32 * m)(*order) if order is not None else None
+    bands = torch.empty((2 * d + 1, n), dtype=torch.float64, device=px.device)
+    icpt = torch.empty(n, dtype=torch.float64, device=px.device)
+    kind = torch.empty(n, dtype=torch.uint8, device=px.device) if want_kind else None
+    kap = torch.empty(n, dtype=torch.float64, device=px.device) if want_kind else None
+    if scratch is None:
+        scratch = raw_scratch(n, d, px.device)
+    info = psp_mrep_info()
+    st = lib().psp_mrep_fit_raw(_ptr(px), _ptr(py), n, m, n, order_a, d, _ptr(bands), _ptr(icpt), _ptr(kind),
+                                _ptr(kap), scratch.data_ptr(), scratch.numel(), _stream_ptr(stream), C.byref(info))
+    _check(st, None, allow=(PSP_OK, PSP_E_SAMPLES))
+    return dict(status=st, bands=bands, intercept=icpt, row_kind=kind, kappa_est=kap,
+                rows_ridge=info.rows_ridge, rows_fallback=info.rows_fallback,
+                rows_nondominant=info.rows_nondominant, gate_accepted=bool(info.gate_accepted),
+                max_abs_diag=info.max_abs_diag)
+
+
+def psp_banded_factor_raw(bands, d, scratch=None, stream=None):
+    import torch
+    n = bands.shape[1]
+    lu = torch.zeros_like(bands)
+    if scratch is None:
+        scratch = raw_scratch(n, d, bands.device)
+    st = lib().psp_banded_factor_raw(_ptr(bands), n, d, _ptr(lu), scratch.data_ptr(), scratch.numel(),
+                                     _stream_ptr(stream))
+    _check(st, None, allow=(PSP_OK, PSP_E_SINGULAR))
+    return st, lu
+
+
+def psp_banded_solve_raw(lu, d, v, x0=None, scratch=None, stream=None, out=None):
+    import torch
+    n = lu.shape[1]
+    z = out if out is not None else torch.empty_like(v)
+    if scratch is None:
+        scratch = raw_scratch(n, d, lu.device)
+    _check(lib().psp_banded_solve_raw(_ptr(lu), n, d, _ptr(v), _ptr(x0), _ptr(z), scratch.data_ptr(),
+                                      scratch.numel(), _stream_ptr(stream)))
+    return z
