@@ -246,8 +246,10 @@ psp_status psp_ring_reset(psp_ctx* ctx);
  * Hraw (same, before rotation), G (restart+1), C, S (restart).  Any pointer may be NULL. */
 psp_status psp_get_hessenberg(const psp_ctx* ctx, double* h_H, double* h_Hraw, double* h_G,
                               double* h_C, double* h_S);
-/* Device pointer to Krylov column V(:,j), 1 <= j <= restart+1. */
-psp_status psp_get_basis(const psp_ctx* ctx, int j, const double** d_vj);
+/* Krylov column V(:,j), 1 <= j <= restart+1, of the current cycle: the columns are stored
+ * unnormalised (lagged normalisation), V(:,j) = *h_scale * (*d_vj)[0..n_loc).  h_scale may be
+ * NULL.  Synchronises when h_scale is requested. */
+psp_status psp_get_basis(const psp_ctx* ctx, int j, const double** d_vj, double* h_scale);
 /* Kernel launches issued by this context so far (the bench's gpu_launches). */
 psp_status psp_launch_count(const psp_ctx* ctx, int64_t* h_launches);
 

@@ -148,7 +148,7 @@ namespace {
 
 struct Plan {
   size_t off_px, off_py, off_V, off_X0, off_B, off_W, off_bands, off_lu, off_icpt, off_kind,
-      off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_scal, off_resid,
+      off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
       off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, total;
   int nblocks;
 };
@@ -173,7 +173,7 @@ Plan make_plan(int64_t n, int d, int nA, int m_max) {
     return at;
   };
   const size_t vec = (size_t)n * 8;
-  p.nblocks = 2 * sm_count();
+  p.nblocks = 8 * sm_count();
   p.off_px = take(vec * m_max);
   p.off_py = take(vec * m_max);
   p.off_V = take(vec * (nA + 1));
@@ -193,6 +193,7 @@ Plan make_plan(int64_t n, int d, int nA, int m_max) {
   p.off_S = take((size_t)nA * 8);
   p.off_Q = take((size_t)nA * 8);
   p.off_Lm = take((size_t)(nA + 1) * (nA + 1) * 8);
+  p.off_alpha = take((size_t)(nA + 1) * 8);
   p.off_scal = take(SC_NSCAL * 8);
   p.off_resid = take((size_t)nA * 8);
   p.off_partials = take((size_t)2 * kMaxRestart * p.nblocks * 8);
@@ -348,6 +349,7 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ds.S = (double*)at(p.off_S);
   c->ds.Q = (double*)at(p.off_Q);
   c->ds.Lm = (double*)at(p.off_Lm);
+  c->ds.alpha = (double*)at(p.off_alpha);
   c->ds.scal = (double*)at(p.off_scal);
   c->ds.resid = (double*)at(p.off_resid);
   c->ds.partials = (double*)at(p.off_partials);
@@ -485,7 +487,7 @@ psp_status precond(psp_ctx* c, const double* v, const double* x0, double* z) {
     launch_copy(v, z, c->n, c->stream);
     c->launches += 1;
   } else {
-    banded_solve(c->lu, c->n, c->d, v, x0, z, c->bs, c->stream, &c->launches);
+    banded_solve(c->lu, c->n, c->d, v, nullptr, x0, z, c->bs, c->stream, &c->launches);
   }
   return PSP_OK;
 }
@@ -499,11 +501,11 @@ psp_status psp_matvec(psp_ctx* c, const double* x, double* y, int record) {
   if (c->sticky != PSP_OK) return c->sticky;
   if (record) {
     const int slot = ring_next(c);
-    launch_matvec(c->st, x, 1.0, py_col(c, slot), px_col(c, slot), c->stream);
+    launch_matvec(c->st, x, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
     launch_copy(py_col(c, slot), y, c->n, c->stream);
     c->launches += 2;
   } else {
-    launch_matvec(c->st, x, 1.0, y, nullptr, c->stream);
+    launch_matvec(c->st, x, nullptr, y, nullptr, c->stream);
     c->launches += 1;
   }
   return check_cuda(c, "psp_matvec");
@@ -526,7 +528,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   // l.4: P_x(:,i) <- X0, P_y(:,i) <- A X0
   const int slot = ring_next(c);
   int h = kt_begin(c);
-  launch_matvec(c->st, c->X0, 1.0, py_col(c, slot), px_col(c, slot), c->stream);
+  launch_matvec(c->st, c->X0, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
   // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta
   h = kt_begin(c);
@@ -536,10 +538,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   double beta;
   PSP_TRY(sync_read(c, c->ds.scal + SC_BETA, 1, &beta));
   if (h_beta) *h_beta = beta;
-  if (beta > 0.0 && isfinite(beta)) {  // V(:,1) <- R_bar / beta (l.6)
-    launch_divide(Vcol(c, 1), c->n, c->ds.scal + SC_BETA, c->stream);
-    c->launches += 1;
-  }
+  // V(:,1) <- R_bar / beta (l.6): stored unnormalised with alpha_1 = 1/beta (krylov.cu)
   c->last_k = 0;
   return check_cuda(c, "psp_cycle_begin");
 }
@@ -558,15 +557,15 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
   int h;
   if (c->n_identity) {
     h = kt_begin(c);
-    launch_matvec(c->st, Vk, 1.0, py, px, c->stream);  // N = I: the probe copy is fused
+    launch_matvec(c->st, Vk, c->ds.alpha + (k - 1), py, px, c->stream);  // N = I: probe copy fused
     kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
     c->launches += 1;
   } else {
     h = kt_begin(c);
-    banded_solve(c->lu, n, c->d, Vk, nullptr, px, c->bs, c->stream, &c->launches);
+    banded_solve(c->lu, n, c->d, Vk, c->ds.alpha + (k - 1), nullptr, px, c->bs, c->stream, &c->launches);
     kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
     h = kt_begin(c);
-    launch_matvec(c->st, px, 1.0, py, nullptr, c->stream);
+    launch_matvec(c->st, px, nullptr, py, nullptr, c->stream);
     kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
     c->launches += 1;
   }
@@ -589,11 +588,8 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
     kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
     c->launches += 2;
   }
-  // l.18: V(:,k+1) = U / H(k+1,k) (R4: 0 on breakdown)
-  h = kt_begin(c);
-  launch_normalize(U, U, k, c->nA, n, c->ds, c->stream);
-  kt_end(c, h, PSP_KC_NORMALIZE, 16.0 * dn);
-  c->launches += 1;
+  // l.18: V(:,k+1) = U / H(k+1,k) (R4: 0 on breakdown) -- lagged: alpha_{k+1} is set
+  // by the Givens epilogue and folded into every reader of V(:,k+1)
   double sc[2];
   PSP_TRY(sync_read(c, c->ds.scal + SC_RK, 2, sc));
   if (h_resid) *h_resid = sc[0];
@@ -697,7 +693,7 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
       c->launches += 1;
     }
     // R13: true residual with one unrecorded matvec
-    launch_matvec(c->st, x, 1.0, c->W, nullptr, c->stream);
+    launch_matvec(c->st, x, nullptr, c->W, nullptr, c->stream);
     launch_diff_norm(b, c->W, c->n, c->ds, SC_TMP, c->rc, c->stream);
     c->launches += 2;
     double tr;
@@ -804,7 +800,7 @@ psp_status psp_banded_solve_raw(const double* lu, int64_t n, int d, const double
   MrepScratch ms;
   BandedScratch bs;
   raw_carve(scratch, n, d, &ms, &bs);
-  banded_solve(lu, n, d, v, x0, z, bs, (cudaStream_t)stream, nullptr);
+  banded_solve(lu, n, d, v, nullptr, x0, z, bs, (cudaStream_t)stream, nullptr);
   return check_cuda(nullptr, "psp_banded_solve_raw");
 }
 
@@ -957,9 +953,14 @@ psp_status psp_get_hessenberg(const psp_ctx* c, double* H, double* Hraw, double*
   return cudaStreamSynchronize(c->stream) == cudaSuccess ? PSP_OK : PSP_E_CUDA;
 }
 
-psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj) {
+psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj, double* h_scale) {
   if (!c || !d_vj || j < 1 || j > c->nA + 1) return PSP_E_ARG;
   *d_vj = c->V + (int64_t)(j - 1) * c->ldv;
+  if (h_scale) {
+    cudaMemcpyAsync(c->hp + 16, c->ds.alpha + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;
+    *h_scale = c->hp[16];
+  }
   return PSP_OK;
 }
 

@@ -220,6 +220,7 @@ __device__ __forceinline__ void push_state(double (&s)[D], double y) {
 template <bool FWD, int D>
 __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ lu, int64_t n,
                                                      const double* __restrict__ vin,
+                                                     const double* vscale,
                                                      const double* addend,
                                                      double* out,
                                                      double* __restrict__ desc,
@@ -249,11 +250,12 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
   const int64_t base = tile * STILE;
 
   // ---- stage the tile (coalesced), rows in processing order per thread ----
+  const double vsc = vscale ? *vscale : 1.0;
   for (int q = t; q < STILE; q += STPB) {
     const int64_t i = base + q;
     const int sidx = (q / SR) * SPAD + (q % SR);
     const bool in = i < n;
-    sv[sidx] = in ? vin[i] : 0.0;
+    sv[sidx] = in ? vsc * vin[i] : 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
@@ -448,8 +450,8 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
 }
 
 template <bool FWD, int D>
-void sweep_launch(const double* lu, int64_t n, const double* v, const double* add, double* out,
-                  BandedScratch sc, cudaStream_t s) {
+void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
+                  double* out, BandedScratch sc, cudaStream_t s) {
   const int64_t ntiles = (n + STILE - 1) / STILE;
   const size_t smem = (size_t)(1 + D + (FWD ? 0 : 1)) * STPB * SPAD * sizeof(double);
   static bool attr_set = false;
@@ -457,7 +459,7 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* ad
     cudaFuncSetAttribute(sweep_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  sweep_kernel<FWD, D><<<(unsigned)ntiles, STPB, smem, s>>>(lu, n, v, add, out, sc.states,
+  sweep_kernel<FWD, D><<<(unsigned)ntiles, STPB, smem, s>>>(lu, n, v, vs, add, out, sc.states,
                                                         sc.tickets + 8, sc.tickets);
 }
 
@@ -529,24 +531,25 @@ int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScrat
   return h[1] ? PSP_E_SINGULAR : PSP_OK;
 }
 
-void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* x0, double* z,
+void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
+                  const double* x0, double* z,
                   BandedScratch sc, cudaStream_t s, int64_t* launches) {
   switch (d) {
     case 1:
-      sweep_launch<true, 1>(lu, n, v, nullptr, sc.y, sc, s);
-      sweep_launch<false, 1>(lu, n, sc.y, x0, z, sc, s);
+      sweep_launch<true, 1>(lu, n, v, vs, nullptr, sc.y, sc, s);
+      sweep_launch<false, 1>(lu, n, sc.y, nullptr, x0, z, sc, s);
       break;
     case 2:
-      sweep_launch<true, 2>(lu, n, v, nullptr, sc.y, sc, s);
-      sweep_launch<false, 2>(lu, n, sc.y, x0, z, sc, s);
+      sweep_launch<true, 2>(lu, n, v, vs, nullptr, sc.y, sc, s);
+      sweep_launch<false, 2>(lu, n, sc.y, nullptr, x0, z, sc, s);
       break;
     case 3:
-      sweep_launch<true, 3>(lu, n, v, nullptr, sc.y, sc, s);
-      sweep_launch<false, 3>(lu, n, sc.y, x0, z, sc, s);
+      sweep_launch<true, 3>(lu, n, v, vs, nullptr, sc.y, sc, s);
+      sweep_launch<false, 3>(lu, n, sc.y, nullptr, x0, z, sc, s);
       break;
     default:
-      sweep_launch<true, 4>(lu, n, v, nullptr, sc.y, sc, s);
-      sweep_launch<false, 4>(lu, n, sc.y, x0, z, sc, s);
+      sweep_launch<true, 4>(lu, n, v, vs, nullptr, sc.y, sc, s);
+      sweep_launch<false, 4>(lu, n, sc.y, nullptr, x0, z, sc, s);
       break;
   }
   if (launches) *launches += 2;

@@ -39,7 +39,8 @@ struct Stencil {
 };
 
 // y = A (xs * x); optionally xcopy = xs * x (the probe column P_x).
-void launch_matvec(const Stencil& st, const double* x, double xs, double* y, double* xcopy,
+// xs: device scalar (the lagged normalisation of a Krylov column) or NULL for 1.
+void launch_matvec(const Stencil& st, const double* x, const double* xs, double* y, double* xcopy,
                    cudaStream_t s);
 
 // ------------------------------------------------------------------------------------------
@@ -53,6 +54,7 @@ struct DevState {
   double* S;         // nA
   double* Q;         // nA (back-substitution, R6)
   double* Lm;        // (nA+1) x (nA+1): strictly-lower part of V'V (ICWY MGS, R11)
+  double* alpha;     // nA+1: V(:,j) = alpha[j-1] * stored column (lagged normalisation)
   double* scal;      // scalars, see enum below
   double* resid;     // R(k) of the current cycle, nA
   double* partials;  // grid-reduction partials: kMaxPartialVals x nblocks
@@ -73,8 +75,6 @@ void launch_norm(const double* x, int64_t n, DevState ds, int slot, const RedCfg
 // r = b - y into v (unnormalised), beta = ||r|| -> scal[SC_BETA], G(1) = beta
 void launch_residual(const double* b, const double* y, double* v, int64_t n, int nA, DevState ds,
                      const RedCfg& rc, cudaStream_t s);
-// v /= scal[slot]   (V(:,1) = R_bar / ||R_bar||)
-void launch_divide(double* v, int64_t n, const double* d_div, cudaStream_t s);
 // literal MGS: one launch per j; src -> dst (U) with the lagged axpy of j-1
 void launch_mgs_literal(const double* src, double* U, const double* Vprev, const double* Vj,
                         int j, int k, int nA, int64_t n, DevState ds, const RedCfg& rc,
@@ -88,9 +88,6 @@ void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int 
 // pass B = U = w - sum_j h_j V_j ; H(k+1,k) = ||U|| ; Givens update
 void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
-// V(:,k+1) = U / H(k+1,k), or 0 on breakdown (R4)
-void launch_normalize(const double* U, double* Vk1, int k, int nA, int64_t n, DevState ds,
-                      cudaStream_t s);
 // Q = H^{-1} G (R6) and out = base + sum_j Q_j V_j; base may be NULL (Z only)
 void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s);
@@ -133,9 +130,9 @@ BandedScratch banded_scratch(void* base, int64_t n, int d);
 // factor; returns PSP_OK / PSP_E_SINGULAR (synchronises); *passes = fixed-point passes
 int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScratch sc,
                   cudaStream_t s, int* passes, int64_t* launches);
-// z = x0 + N^{-1} v (x0 may be NULL); v may be scaled by vs on load
-void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* x0,
-                  double* z, BandedScratch sc, cudaStream_t s, int64_t* launches);
+// z = x0 + N^{-1} (vs * v) (x0 may be NULL; vs: device scalar or NULL for 1)
+void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
+                  const double* x0, double* z, BandedScratch sc, cudaStream_t s, int64_t* launches);
 
 // ---- misc ----
 std::string cuda_err_str(cudaError_t e);

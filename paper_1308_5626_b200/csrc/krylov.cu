@@ -1,11 +1,19 @@
 // krylov.cu -- K2 (Gram-Schmidt), K5 (Givens / back-substitution) and the vector passes of
 // Algorithm 1.
 //
-// Every reduction is deterministic: a fixed grid of rc.nblocks blocks (a multiple of the 148
-// SMs) writes one partial per block, and the last block to finish (atomic ticket) sums the
-// partials in a fixed tree.  Bitwise run-to-run determinism follows.  The last block
-// also runs the O(k) scalar epilogue (Givens rotation, triangular solves) on one thread, so
-// an Arnoldi step costs no extra launch for its scalar work.
+// Lagged normalisation: the Krylov columns are stored unnormalised, V(:,j) = alpha_j * Vs(:,j)
+// with alpha_j = 1/||R_bar|| (j = 1) or 1/H(j,j-1) kept on the device; every
+// reader folds alpha_j into its coefficient, so line 18's division costs no pass over memory.
+//
+// Every reduction is deterministic: a fixed grid of blocks writes one partial per block, and
+// the last block to finish (atomic ticket) sums the partials in a fixed order.  Bitwise
+// run-to-run determinism follows.  The last block also runs the O(k) scalar epilogue
+// (Givens rotation, triangular solves) on one thread, so an Arnoldi step costs no extra
+// launch for its scalar work.
+//
+// Streaming kernels keep RPT rows per thread in registers (rows t + TPB*i of a TPB*RPT tile)
+// and walk the k basis vectors in chunks of JC, so each thread has JC*RPT independent 8-byte
+// loads in flight: enough bytes in flight per SM to cover the HBM latency.
 #include <math.h>
 
 #include "internal.h"
@@ -15,6 +23,9 @@ namespace {
 
 constexpr int TPB = kRedThreads;  // 256
 constexpr int kWarps = TPB / 32;
+constexpr int RPT = 8;            // rows per thread in the register-tiled passes
+constexpr int TILE = TPB * RPT;   // 2048 rows
+constexpr int JC = 4;             // basis vectors per chunk
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -58,8 +69,7 @@ __device__ bool finish_block(unsigned* ticket) {
   return s_last;
 }
 
-// Last block: total of partials[v*nb + b] over b, in a fixed tree.  All threads call; the
-// result is valid in thread 0.
+// Last block: total of partials[v*nb + b] over b, fixed order.  Result valid in thread 0.
 __device__ double reduce_partials(const double* partials, int v, int nb, double* smem) {
   double a[1] = {0.0};
   for (int b = threadIdx.x; b < nb; b += blockDim.x) a[0] += ((volatile const double*)partials)[v * nb + b];
@@ -68,7 +78,8 @@ __device__ double reduce_partials(const double* partials, int v, int nb, double*
 }
 
 // ------------------------------------------------------------------------------------------
-// Givens update of column k (Alg.1 l.19-32; R4, R10).  One thread.
+// Givens update of column k (Alg.1 l.19-32; R4, R10).  One thread.  Also sets the
+// lagged normalisation alpha_{k+1} = 1/H(k+1,k) of V(:,k+1) (l.18; 0 on breakdown).
 // ------------------------------------------------------------------------------------------
 __device__ void givens_update(DevState ds, int k, int nA) {
   const int ld = nA + 1;
@@ -81,6 +92,7 @@ __device__ void givens_update(DevState ds, int k, int nA) {
   const double hk1 = Hc[k];
   bool breakdown = !(hk1 > 1e-14 * sqrt(colsq));   // R4, before rotation
   const bool nonfinite = !isfinite(hk1);
+  ds.alpha[k] = (breakdown || nonfinite) ? 0.0 : 1.0 / hk1;
   ds.G[k] = 0.0;                                    // l.9: G(k+1) <- 0
   for (int j = 1; j <= k - 1; ++j) {                // l.19-23
     const double delta = Hc[j - 1];
@@ -146,7 +158,8 @@ __global__ void __launch_bounds__(TPB) diff_norm_kernel(const double* __restrict
   }
 }
 
-// Alg.1 l.5-7: R_bar = B - P_y(:,i) -> v (unnormalised), beta = ||R_bar||, G(1) = beta.
+// Alg.1 l.5-7: R_bar = B - P_y(:,i) -> V(:,1) (unnormalised), beta = ||R_bar||,
+// G(1) = beta, alpha_1 = 1/beta (l.6).
 __global__ void __launch_bounds__(TPB) residual_kernel(const double* __restrict__ b,
                                                        const double* __restrict__ y,
                                                        double* __restrict__ v, int64_t n,
@@ -167,15 +180,9 @@ __global__ void __launch_bounds__(TPB) residual_kernel(const double* __restrict_
       ds.scal[SC_BETA] = beta;
       for (int j = 0; j <= nA; ++j) ds.G[j] = 0.0;  // l.44 "clean"
       ds.G[0] = beta;                                // l.7
+      ds.alpha[0] = (beta > 0.0 && isfinite(beta)) ? 1.0 / beta : 0.0;
     }
   }
-}
-
-__global__ void divide_kernel(double* __restrict__ v, int64_t n, const double* __restrict__ div) {
-  const double dv = *div;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x)
-    v[r] = v[r] / dv;
 }
 
 __global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
@@ -186,8 +193,8 @@ __global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y
 
 // ------------------------------------------------------------------------------------------
 // Literal MGS (Alg.1 l.13-16), one grid pass per j:
-//   U <- src - H(j-1,k) V_{j-1}   (the update of step j-1, lagged into this pass)
-//   H(j,k) <- V_j' U
+//   U <- src - H(j-1,k) V(:,j-1)   (the update of step j-1, lagged into this pass)
+//   H(j,k) <- V(:,j)' U
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TPB) mgs_literal_kernel(const double* src, double* U,
                                                           const double* __restrict__ Vprev,
@@ -195,11 +202,11 @@ __global__ void __launch_bounds__(TPB) mgs_literal_kernel(const double* src, dou
                                                           int k, int nA, int64_t n, DevState ds) {
   __shared__ double sm[kWarps];
   const int ld = nA + 1;
-  const double hprev = Vprev ? ds.H[(int64_t)(k - 1) * ld + (j - 2)] : 0.0;
+  const double hprev = Vprev ? ds.H[(int64_t)(k - 1) * ld + (j - 2)] * ds.alpha[j - 2] : 0.0;
   double a[1] = {0.0};
   for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
     double u = src[r];
-    if (Vprev) u = u - hprev * Vprev[r];
+    if (Vprev) u = fma(-hprev, Vprev[r], u);
     U[r] = u;
     a[0] = fma(Vj[r], u, a[0]);
   }
@@ -207,21 +214,21 @@ __global__ void __launch_bounds__(TPB) mgs_literal_kernel(const double* src, dou
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) ds.H[(int64_t)(k - 1) * ld + (j - 1)] = t;
+    if (threadIdx.x == 0) ds.H[(int64_t)(k - 1) * ld + (j - 1)] = ds.alpha[j - 1] * t;
   }
 }
 
-// U <- U - H(k,k) V_k ; H(k+1,k) = ||U|| (l.17) ; Givens (l.19-32)
+// U <- U - H(k,k) V(:,k) ; H(k+1,k) = ||U|| (l.17) ; Givens (l.19-32)
 __global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restrict__ U,
                                                                 const double* __restrict__ Vk,
                                                                 int k, int nA, int64_t n,
                                                                 DevState ds) {
   __shared__ double sm[kWarps];
   const int ld = nA + 1;
-  const double h = ds.H[(int64_t)(k - 1) * ld + (k - 1)];
+  const double h = ds.H[(int64_t)(k - 1) * ld + (k - 1)] * ds.alpha[k - 1];
   double a[1] = {0.0};
   for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
-    double u = U[r] - h * Vk[r];
+    double u = fma(-h, Vk[r], U[r]);
     U[r] = u;
     a[0] = fma(u, u, a[0]);
   }
@@ -237,61 +244,87 @@ __global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restri
 }
 
 // ------------------------------------------------------------------------------------------
-// ICWY one-reduction MGS (R11; Swirydowicz-Langou-Ananthan-Yang-Thomas 2020 form):
-//   MGS coefficients h satisfy (I + L) h = V'w with L = strictly-lower part of V'V, exactly
-//   as the sequential MGS recurrence h_j = V_j'w - sum_{i<j} (V_j'V_i) h_i.
-// Pass A: s_j = V_j'w (j < k) and l_j = V_{k}'V_j (j < k-1, the new row of L), one pass over
-// k+1 vectors with w and V_k staged in shared memory; the last block solves (I+L)h = s.
+// ICWY one-reduction MGS (R11; the Swirydowicz-Langou-Ananthan-Yang-Thomas 2020 form):
+// the MGS coefficients satisfy (I + L) h = V'w with L = strictly-lower part of V'V, exactly
+// the sequential MGS recurrence h_j = V_j'w - sum_{i<j} (V_j'V_i) h_i.
+// Pass A: s_j = V_j'w (j <= k) and l_j = V_k'V_j (j < k, the new row of L) in one pass over
+// the k+1 vectors; the last block solves (I + L) h = s into H(1..k, k).
 // ------------------------------------------------------------------------------------------
-constexpr int kTileRows = 1024;
+template <int C, bool FULL>
+__device__ __forceinline__ void dots_chunk(const double* __restrict__ V, int64_t ldv, int j0,
+                                           const double (&wr)[RPT], const double (&qr)[RPT],
+                                           int64_t n, int64_t r0, int lane, int k, double* acc) {
+  double as[C], al[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    as[c] = 0.0;
+    al[c] = 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const double* __restrict__ vj = V + (int64_t)(j0 + c) * ldv;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = r0 + (int64_t)TPB * i;
+      const double v = (FULL || r < n) ? vj[r] : 0.0;
+      as[c] = fma(v, wr[i], as[c]);
+      al[c] = fma(v, qr[i], al[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const double s1 = warp_sum(as[c]);
+    const double s2 = warp_sum(al[c]);
+    if (lane == 0) {
+      acc[j0 + c] += s1;
+      acc[k + j0 + c] += s2;
+    }
+  }
+}
 
+template <bool FULL>
+__device__ __forceinline__ void dots_tile(const double* __restrict__ V, int64_t ldv,
+                                          const double* __restrict__ w, int k, int64_t n,
+                                          int64_t r0, int lane, double* acc) {
+  const double* __restrict__ qk = V + (int64_t)(k - 1) * ldv;
+  double wr[RPT], qr[RPT];
+  double sk = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int64_t r = r0 + (int64_t)TPB * i;
+    wr[i] = (FULL || r < n) ? w[r] : 0.0;
+    qr[i] = (FULL || r < n) ? qk[r] : 0.0;
+    sk = fma(qr[i], wr[i], sk);
+  }
+  int j0 = 0;
+  for (; j0 + JC <= k - 1; j0 += JC) dots_chunk<JC, FULL>(V, ldv, j0, wr, qr, n, r0, lane, k, acc);
+  for (; j0 < k - 1; ++j0) dots_chunk<1, FULL>(V, ldv, j0, wr, qr, n, r0, lane, k, acc);
+  sk = warp_sum(sk);
+  if (lane == 0) acc[k - 1] += sk;
+}
 __global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict__ V, int64_t ldv,
                                                         const double* __restrict__ w, int k,
                                                         int nA, int64_t n, DevState ds) {
-  __shared__ double ws[kTileRows];
-  __shared__ double qs[kTileRows];
-  __shared__ double acc[2 * kMaxRestart];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = 2 * k - 1;  // s_0..s_{k-1}, l_0..l_{k-2}
-  for (int q = threadIdx.x; q < 2 * k; q += TPB) acc[q] = 0.0;
-  const double* __restrict__ qk = V + (int64_t)(k - 1) * ldv;
-  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t r0 = t * kTileRows;
-    const int rows = (int)((n - r0) < kTileRows ? (n - r0) : kTileRows);
-    __syncthreads();
-    for (int q = threadIdx.x; q < kTileRows; q += TPB) {
-      ws[q] = q < rows ? w[r0 + q] : 0.0;
-      qs[q] = q < rows ? qk[r0 + q] : 0.0;
-    }
-    __syncthreads();
-    for (int jb = warp; jb < k; jb += kWarps) {
-      const double* __restrict__ vj = V + (int64_t)jb * ldv + r0;
-      double a1 = 0.0, a2 = 0.0;
-      if (jb < k - 1) {
-#pragma unroll 4
-        for (int q = lane; q < rows; q += 32) {
-          const double v = vj[q];
-          a1 = fma(v, ws[q], a1);
-          a2 = fma(v, qs[q], a2);
-        }
-      } else {
-#pragma unroll 4
-        for (int q = lane; q < rows; q += 32) a1 = fma(qs[q], ws[q], a1);
-      }
-      a1 = warp_sum(a1);
-      a2 = warp_sum(a2);
-      if (lane == 0) {
-        acc[jb] += a1;
-        if (jb < k - 1) acc[k + jb] += a2;
-      }
-    }
+  __shared__ double accw[kWarps][2 * kMaxRestart];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
+  const int nv = 2 * k - 1;  // s_0..s_{k-1} at [0,k), l_0..l_{k-2} at [k, 2k-1)
+  for (int q = lane; q < 2 * k; q += 32) accw[warp][q] = 0.0;
+  __syncwarp();
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t nfull = n / TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TILE + t;
+    if (tile < nfull) dots_tile<true>(V, ldv, w, k, n, r0, lane, accw[warp]);
+    else dots_tile<false>(V, ldv, w, k, n, r0, lane, accw[warp]);
   }
   __syncthreads();
   const int nb = gridDim.x;
-  for (int q = threadIdx.x; q < nv; q += TPB) ds.partials[(int64_t)q * nb + blockIdx.x] = acc[q];
+  for (int q = t; q < nv; q += TPB) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) s += accw[w2][q];
+    ds.partials[(int64_t)q * nb + blockIdx.x] = s;
+  }
   if (finish_block(ds.tickets + TK_MAIN)) {
-    // totals: one warp per value, fixed order
     __shared__ double tot[2 * kMaxRestart];
     for (int q = warp; q < nv; q += kWarps) {
       double s = 0.0;
@@ -300,14 +333,15 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict
       if (lane == 0) tot[q] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t == 0) {
       const int ldl = nA + 1;
+      const double ak = ds.alpha[k - 1];
       double* Lrow = ds.Lm + (int64_t)(k - 1) * ldl;
-      for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = tot[k + jb];
+      for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = ds.alpha[jb] * ak * tot[k + jb];
       double* Hc = ds.H + (int64_t)(k - 1) * (nA + 1);
-      // forward substitution (I + L) h = s
+      // forward substitution (I + L) h = s,  s_j = alpha_j V_j'w
       for (int jb = 0; jb < k; ++jb) {
-        double h = tot[jb];
+        double h = ds.alpha[jb] * tot[jb];
         const double* Lr = ds.Lm + (int64_t)jb * ldl;
         for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
         Hc[jb] = h;
@@ -316,55 +350,95 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict
   }
 }
 
-// Pass B: U = w - sum_j h_j V_j (sequential in j, as the MGS updates), H(k+1,k) = ||U||,
-// then the Givens update of column k.
+// Pass B tile: URPT rows per thread, UJC basis vectors per chunk (URPT*UJC = 32 loads in
+// flight per thread); bounds checks only in the last, partial tile.
+constexpr int URPT = 4;
+constexpr int UJC = 8;
+constexpr int UTILE = TPB * URPT;
+
+template <bool FULL>
+__device__ __forceinline__ void update_tile(const double* __restrict__ V, int64_t ldv,
+                                            const double* __restrict__ w, double* __restrict__ U,
+                                            const double* hs, int k, int64_t n, int64_t r0,
+                                            double& acc) {
+  double u[URPT];
+#pragma unroll
+  for (int i = 0; i < URPT; ++i) {
+    const int64_t r = r0 + (int64_t)TPB * i;
+    u[i] = (FULL || r < n) ? w[r] : 0.0;
+  }
+  int jb = 0;
+  for (; jb + UJC <= k; jb += UJC) {
+    double v[UJC][URPT];
+#pragma unroll
+    for (int c = 0; c < UJC; ++c)
+#pragma unroll
+      for (int i = 0; i < URPT; ++i) {
+        const int64_t r = r0 + (int64_t)TPB * i;
+        v[c][i] = (FULL || r < n) ? V[(int64_t)(jb + c) * ldv + r] : 0.0;
+      }
+#pragma unroll
+    for (int c = 0; c < UJC; ++c)
+#pragma unroll
+      for (int i = 0; i < URPT; ++i) u[i] = fma(-hs[jb + c], v[c][i], u[i]);
+  }
+  for (; jb < k; ++jb) {
+    double v[URPT];
+#pragma unroll
+    for (int i = 0; i < URPT; ++i) {
+      const int64_t r = r0 + (int64_t)TPB * i;
+      v[i] = (FULL || r < n) ? V[(int64_t)jb * ldv + r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < URPT; ++i) u[i] = fma(-hs[jb], v[i], u[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < URPT; ++i) {
+    const int64_t r = r0 + (int64_t)TPB * i;
+    if (FULL || r < n) {
+      U[r] = u[i];
+      acc = fma(u[i], u[i], acc);
+    }
+  }
+}
+
+// Pass B: U = w - sum_j h_j alpha_j V_j (sequential in j, as the MGS updates), H(k+1,k) =
+// ||U||, then the Givens update of column k.
 __global__ void __launch_bounds__(TPB) icwy_update_kernel(const double* __restrict__ V, int64_t ldv,
                                                           const double* __restrict__ w,
                                                           double* __restrict__ U, int k, int nA,
                                                           int64_t n, DevState ds) {
   __shared__ double hs[kMaxRestart];
   __shared__ double sm[kWarps];
-  const int ld = nA + 1;
-  for (int q = threadIdx.x; q < k; q += TPB) hs[q] = ds.H[(int64_t)(k - 1) * ld + q];
+  const int ld = nA + 1, t = threadIdx.x;
+  for (int q = t; q < k; q += TPB) hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
   __syncthreads();
   double a[1] = {0.0};
-  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
-    double u = w[r];
-#pragma unroll 8
-    for (int jb = 0; jb < k; ++jb) u = fma(-hs[jb], V[(int64_t)jb * ldv + r], u);
-    U[r] = u;
-    a[0] = fma(u, u, a[0]);
+  const int64_t ntiles = (n + UTILE - 1) / UTILE;
+  const int64_t nfull = n / UTILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * UTILE + t;
+    if (tile < nfull) update_tile<true>(V, ldv, w, U, hs, k, n, r0, a[0]);
+    else update_tile<false>(V, ldv, w, U, hs, k, n, r0, a[0]);
   }
   block_sum<1>(a, sm);
-  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (t == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
-    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) {
-      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(t);
+    double tt = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (t == 0) {
+      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(tt);
       givens_update(ds, k, nA);
     }
   }
 }
 
-// l.18: V(:,k+1) <- U / H(k+1,k); V(:,k+1) = 0 on breakdown (R4)
-__global__ void normalize_kernel(const double* U, double* V1, int k,
-                                 int nA, int64_t n, DevState ds) {
-  // H(k+1,k) before rotation (the rotated entry is 0, l.28)
-  const double hraw = ds.Hraw[(int64_t)(k - 1) * (nA + 1) + k];
-  const int flags = (int)ds.scal[SC_FLAGS];
-  const bool bd = (flags & (PSP_FLAG_BREAKDOWN | PSP_FLAG_NONFINITE)) != 0;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x)
-    V1[r] = bd ? 0.0 : U[r] / hraw;
-}
-
 // l.38-42: Q = H^{-1} G (R6, every block recomputes the k x k back-substitution
-// redundantly: identical inputs, identical result), out = base + sum_j Q_j V_j.
+// redundantly: identical inputs, identical result), out = base + sum_j Q_j alpha_j V_j.
 __global__ void __launch_bounds__(TPB) combine_kernel(const double* __restrict__ V, int64_t ldv,
-                                                      int k, int nA,
-                                                      const double* base, double* out, int64_t n,
-                                                      DevState ds) {
+                                                      int k, int nA, const double* base,
+                                                      double* out, int64_t n, DevState ds) {
   __shared__ double qs[kMaxRestart];
+  __shared__ double qa[kMaxRestart];
   __shared__ int bad;
   if (threadIdx.x == 0) {
     const int ld = nA + 1;
@@ -376,22 +450,44 @@ __global__ void __launch_bounds__(TPB) combine_kernel(const double* __restrict__
       if (piv == 0.0) { bad = 1; qs[j - 1] = 0.0; continue; }
       qs[j - 1] = s / piv;
     }
+    for (int j = 0; j < k; ++j) qa[j] = qs[j] * ds.alpha[j];
     if (blockIdx.x == 0) {
       for (int j = 0; j < k; ++j) ds.Q[j] = qs[j];
       ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
     }
   }
   __syncthreads();
-  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
-    double z = 0.0;
-#pragma unroll 8
-    for (int jb = 0; jb < k; ++jb) z = fma(qs[jb], V[(int64_t)jb * ldv + r], z);
-    out[r] = base ? base[r] + z : z;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int t = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TILE + t;
+    double z[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) z[i] = 0.0;
+    for (int jb = 0; jb < k; ++jb) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t r = r0 + (int64_t)TPB * i;
+        const double v = r < n ? V[(int64_t)jb * ldv + r] : 0.0;
+        z[i] = fma(qa[jb], v, z[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = r0 + (int64_t)TPB * i;
+      if (r < n) out[r] = base ? base[r] + z[i] : z[i];
+    }
   }
 }
 
 inline int grid_for(int64_t n, int cap) {
   int64_t b = (n + TPB - 1) / TPB;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+inline int tiles_grid(int64_t n, int cap) {
+  int64_t b = (n + TILE - 1) / TILE;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;
@@ -410,9 +506,6 @@ void launch_residual(const double* b, const double* y, double* v, int64_t n, int
                      const RedCfg& rc, cudaStream_t s) {
   residual_kernel<<<rc.nblocks, TPB, 0, s>>>(b, y, v, n, ds, nA);
 }
-void launch_divide(double* v, int64_t n, const double* d_div, cudaStream_t s) {
-  divide_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(v, n, d_div);
-}
 void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s) {
   copy_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(x, y, n);
 }
@@ -427,19 +520,18 @@ void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_
 }
 void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int nA, int64_t n,
                       DevState ds, const RedCfg& rc, cudaStream_t s) {
-  icwy_dots_kernel<<<rc.nblocks, TPB, 0, s>>>(V, ldv, w, k, nA, n, ds);
+  // grid: 4 blocks per SM for the dots, 8 for the update (measured best, tools/ortho_micro.cu)
+  icwy_dots_kernel<<<tiles_grid(n, rc.nblocks / 2), TPB, 0, s>>>(V, ldv, w, k, nA, n, ds);
 }
 void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
-  icwy_update_kernel<<<rc.nblocks, TPB, 0, s>>>(V, ldv, w, U, k, nA, n, ds);
-}
-void launch_normalize(const double* U, double* Vk1, int k, int nA, int64_t n, DevState ds,
-                      cudaStream_t s) {
-  normalize_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(U, Vk1, k, nA, n, ds);
+  int64_t ub = (n + UTILE - 1) / UTILE;
+  if (ub > rc.nblocks) ub = rc.nblocks;
+  icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, ldv, w, U, k, nA, n, ds);
 }
 void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {
-  combine_kernel<<<grid_for(n, 148 * 4), TPB, 0, s>>>(V, ldv, k, nA, base, out, n, ds);
+  combine_kernel<<<tiles_grid(n, 148 * 4), TPB, 0, s>>>(V, ldv, k, nA, base, out, n, ds);
 }
 
 }  // namespace psp

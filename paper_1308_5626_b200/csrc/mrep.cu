@@ -23,7 +23,7 @@ namespace psp {
 namespace {
 
 constexpr int TPB = 256;
-constexpr int CB = 8;          // probe columns staged per shared-memory round
+constexpr int CB = 12;         // probe columns staged per shared-memory round
 constexpr int kMaxM = 256;     // probe columns supported
 
 struct Cols {
@@ -44,34 +44,53 @@ __device__ __forceinline__ double band_abs_off_sum(const double* row /*2d+1 coef
   return off;
 }
 
-// Cholesky of the packed-by-row P x P SPD matrix in place (R17).  Returns false on failure.
+// Interior-row fit.  Writes bands / intercept / kind / kappa for rows d <= r < n-d and the
+// per-block gate statistics.
+// packed lower-triangular index (row a >= col b)
+__host__ __device__ constexpr int pk(int a, int b) { return a * (a + 1) / 2 + b; }
+
+// Gram of row r (thread t) from the lagged sums in shared memory:
+// G[0][0] = m, G[1+a][0] = S(r-d+a), G[1+b][1+a] = C_{b-a}(r-d+a) (b >= a); + lambda on the diagonal
+template <int D>
+__device__ __forceinline__ void assemble(double (&A)[(2 * D + 2) * (2 * D + 3) / 2], const double* ex,
+                                         int t, int m, double lambda) {
+  A[pk(0, 0)] = (double)m + lambda;
+#pragma unroll
+  for (int a = 0; a <= 2 * D; ++a) {
+    A[pk(1 + a, 0)] = ex[(2 * D + 1) * TPB + (t - D + a)];
+#pragma unroll
+    for (int b = a; b <= 2 * D; ++b) A[pk(1 + b, 1 + a)] = ex[(b - a) * TPB + (t - D + a)];
+    A[pk(1 + a, 1 + a)] += lambda;
+  }
+}
+
+// in-place Cholesky of the packed P x P matrix (R17); false on a pivot^2 <= 0 or non-finite
 template <int P>
-__device__ __forceinline__ bool chol(double (&A)[P][P]) {
+__device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2]) {
 #pragma unroll
   for (int j = 0; j < P; ++j) {
-    double s = A[j][j];
+    double s = A[pk(j, j)];
 #pragma unroll
-    for (int k = 0; k < j; ++k) s -= A[j][k] * A[j][k];
+    for (int k = 0; k < j; ++k) s -= A[pk(j, k)] * A[pk(j, k)];
     if (!(s > 0.0) || !isfinite(s)) return false;
     const double ljj = sqrt(s);
-    A[j][j] = ljj;
+    A[pk(j, j)] = ljj;
 #pragma unroll
     for (int i = j + 1; i < P; ++i) {
-      double t = A[i][j];
+      double u = A[pk(i, j)];
 #pragma unroll
-      for (int k = 0; k < j; ++k) t -= A[i][k] * A[j][k];
-      A[i][j] = t / ljj;
+      for (int k = 0; k < j; ++k) u -= A[pk(i, k)] * A[pk(j, k)];
+      A[pk(i, j)] = u / ljj;
     }
   }
   return true;
 }
 
-// Interior-row fit.  Writes bands / intercept / kind / kappa for rows d <= r < n-d and the
-// per-block gate statistics.
 template <int D>
-__global__ void __launch_bounds__(TPB) mrep_interior_kernel(Cols cols, int m, int64_t n,
-                                                            MrepOut out, MrepScratch sc) {
+__global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m, int64_t n,
+                                                               MrepOut out, MrepScratch sc) {
   constexpr int P = 2 * D + 2;
+  constexpr int NP = P * (P + 1) / 2;
   constexpr int TILE = TPB + 3 * D;                 // rows [i0-2D, i0-D+TPB+2D)
   __shared__ double xs[CB][TILE];
   __shared__ double ex[(2 * D + 2) * TPB];
@@ -91,6 +110,10 @@ __global__ void __launch_bounds__(TPB) mrep_interior_kernel(Cols cols, int m, in
   const bool rvalid = (r >= 0 && r < n);
   for (int c0 = 0; c0 < m; c0 += CB) {
     const int cn = (m - c0) < CB ? (m - c0) : CB;
+    double yv[CB];
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc)                 // this row's P_y samples of the chunk
+      yv[cc] = (cc < cn && rvalid) ? __ldg(cols.py + (int64_t)cols.slot[c0 + cc] * cols.ld + r) : 0.0;
     __syncthreads();
     for (int cc = 0; cc < cn; ++cc) {
       const double* __restrict__ colx = cols.px + (int64_t)cols.slot[c0 + cc] * cols.ld;
@@ -100,16 +123,17 @@ __global__ void __launch_bounds__(TPB) mrep_interior_kernel(Cols cols, int m, in
       }
     }
     __syncthreads();
-    for (int cc = 0; cc < cn; ++cc) {
-      const double yv = rvalid ? __ldg(cols.py + (int64_t)cols.slot[c0 + cc] * cols.ld + r) : 0.0;
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+      if (cc >= cn) break;
       const double* xr = &xs[cc][t + D];            // xr[l] = P_x(r + l), l in [-D, 2D]
       const double x0 = xr[0];
       Ssum += x0;
-      Tsum += yv;
+      Tsum += yv[cc];
 #pragma unroll
       for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xr[l], Cl[l]);
 #pragma unroll
-      for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xr[l - D], yv, Dl[l]);
+      for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xr[l - D], yv[cc], Dl[l]);
     }
   }
   // exchange C_l(r), S(r) with the neighbours ((2D+2) x TPB doubles)
@@ -121,52 +145,30 @@ __global__ void __launch_bounds__(TPB) mrep_interior_kernel(Cols cols, int m, in
 
   const bool emit = (t >= D && t < TPB - D) && r >= D && r < n - D;
   if (emit) {
-    double G[P][P], rhs[P];
-    // P:111-122 via the lagged sums
-    G[0][0] = (double)m;
-    rhs[0] = Tsum;
-#pragma unroll
-    for (int a = 0; a <= 2 * D; ++a) {
-      G[0][1 + a] = G[1 + a][0] = ex[(2 * D + 1) * TPB + (t - D + a)];
-      rhs[1 + a] = Dl[a];
-#pragma unroll
-      for (int b = a; b <= 2 * D; ++b) {
-        const double v = ex[(b - a) * TPB + (t - D + a)];
-        G[1 + a][1 + b] = v;
-        G[1 + b][1 + a] = v;
-      }
-    }
-    double L[P][P];
-#pragma unroll
-    for (int a = 0; a < P; ++a)
-#pragma unroll
-      for (int b = 0; b < P; ++b) L[a][b] = G[a][b];
-    bool ok = chol<P>(L);
+    double A[NP];
+    assemble<D>(A, ex, t, m, 0.0);
+    bool ok = chol_packed<P>(A);
     double kap = INFINITY;
     if (ok) {
-      double lmax = L[0][0], lmin = L[0][0];
+      double lmax = A[pk(0, 0)], lmin = A[pk(0, 0)];
 #pragma unroll
       for (int j = 1; j < P; ++j) {
-        lmax = fmax(lmax, L[j][j]);
-        lmin = fmin(lmin, L[j][j]);
+        lmax = fmax(lmax, A[pk(j, j)]);
+        lmin = fmin(lmin, A[pk(j, j)]);
       }
       kap = (lmax / lmin) * (lmax / lmin);
     }
     int kind = PSP_ROW_INTERIOR;
-    if (!ok || kap > 1e12) {                        // S:226 ridge retry
-      double tr = 0.0;
+    if (!ok || kap > 1e12) {                        // S:226 ridge retry on G + lambda I
+      double tr = (double)m;
 #pragma unroll
-      for (int j = 0; j < P; ++j) tr += G[j][j];
+      for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TPB + (t - D + a)];   // diag = C_0(r-d+a)
       const double lambda = 1e-10 * tr / (double)P;
-#pragma unroll
-      for (int a = 0; a < P; ++a)
-#pragma unroll
-        for (int b = 0; b < P; ++b) L[a][b] = G[a][b] + (a == b ? lambda : 0.0);
-      ok = chol<P>(L);
+      assemble<D>(A, ex, t, m, lambda);
+      ok = chol_packed<P>(A);
       kind = PSP_ROW_INTERIOR_RIDGE;
       nridge += 1.0;
     }
-    double beta[P];
     double row[2 * D + 1];
     double icpt = 0.0;
     if (!ok) {                                      // identity row
@@ -178,21 +180,21 @@ __global__ void __launch_bounds__(TPB) mrep_interior_kernel(Cols cols, int m, in
       double z[P];
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        double s = rhs[i];
+        double s = (i == 0) ? Tsum : Dl[i - 1];
 #pragma unroll
-        for (int k = 0; k < i; ++k) s -= L[i][k] * z[k];
-        z[i] = s / L[i][i];
+        for (int k = 0; k < i; ++k) s -= A[pk(i, k)] * z[k];
+        z[i] = s / A[pk(i, i)];
       }
 #pragma unroll
       for (int i = P - 1; i >= 0; --i) {
         double s = z[i];
 #pragma unroll
-        for (int k = i + 1; k < P; ++k) s -= L[k][i] * beta[k];
-        beta[i] = s / L[i][i];
+        for (int k = i + 1; k < P; ++k) s -= A[pk(k, i)] * z[k];
+        z[i] = s / A[pk(i, i)];
       }
-      icpt = beta[0];                               // R15: reported, never installed
+      icpt = z[0];                                  // R15: reported, never installed
 #pragma unroll
-      for (int o = 0; o <= 2 * D; ++o) row[o] = beta[1 + o];  // R14: N(i, i+o-d) = N*(o+2)
+      for (int o = 0; o <= 2 * D; ++o) row[o] = z[1 + o];  // R14: N(i, i+o-d) = N*(o+2)
     }
 #pragma unroll
     for (int o = 0; o <= 2 * D; ++o) out.bands[(int64_t)o * n + r] = row[o];

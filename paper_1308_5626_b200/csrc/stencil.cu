@@ -50,7 +50,7 @@ __device__ __forceinline__ Nb neighbour(const Stencil& st, const double* __restr
 
 template <int KIND, int NDIM>
 __global__ void __launch_bounds__(128) matvec_kernel(Stencil st, const double* __restrict__ x,
-                                                     double xs, double* __restrict__ y,
+                                                     const double* xsp, double* __restrict__ y,
                                                      double* __restrict__ xcopy) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = blockIdx.y;
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(128) matvec_kernel(Stencil st, const double* _
   const int64_t g = i + st.nx * (j + st.ny * k);
   const double* __restrict__ f = st.field;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  const double xs = xsp ? *xsp : 1.0;
   const double xc = __ldg(x + g);
   const double fc = cell ? __ldg(f + g) : 0.0;
   double acc = 0.0;  // sum over faces of s_a * k_f * (x_c - x_nb) + upwind terms
@@ -94,8 +95,9 @@ __global__ void __launch_bounds__(128) matvec_kernel(Stencil st, const double* _
 }
 
 __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ bands,
-                                  const double* __restrict__ x, double xs, double* __restrict__ y,
+                                  const double* __restrict__ x, const double* xsp, double* __restrict__ y,
                                   double* __restrict__ xcopy) {
+  const double xs = xsp ? *xsp : 1.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -110,7 +112,7 @@ __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ 
 }
 
 template <int KIND>
-void launch_kind(const Stencil& st, const double* x, double xs, double* y, double* xcopy,
+void launch_kind(const Stencil& st, const double* x, const double* xs, double* y, double* xcopy,
                  cudaStream_t s) {
   dim3 block(128);
   dim3 grid((unsigned)((st.nx + 127) / 128), (unsigned)st.ny, (unsigned)st.nz);
@@ -123,7 +125,7 @@ void launch_kind(const Stencil& st, const double* x, double xs, double* y, doubl
 
 }  // namespace
 
-void launch_matvec(const Stencil& st, const double* x, double xs, double* y, double* xcopy,
+void launch_matvec(const Stencil& st, const double* x, const double* xs, double* y, double* xcopy,
                    cudaStream_t s) {
   switch (st.kind) {
     case PSP_OP_CONST_DIFF: launch_kind<PSP_OP_CONST_DIFF>(st, x, xs, y, xcopy, s); break;

@@ -111,7 +111,7 @@ def lib():
         "psp_ring_view": (C.c_int, [_vp, P(C.c_int), P(C.c_int32), P(_vp), P(_vp), P(C.c_int64)]),
         "psp_ring_reset": (C.c_int, [_vp]),
         "psp_get_hessenberg": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),
-        "psp_get_basis": (C.c_int, [_vp, C.c_int, P(_vp)]),
+        "psp_get_basis": (C.c_int, [_vp, C.c_int, P(_vp), P(C.c_double)]),
         "psp_launch_count": (C.c_int, [_vp, P(C.c_int64)]),
         "psp_kernel_stats": (C.c_int, [_vp, _dp, _dp, P(C.c_int64), C.c_int]),
         "psp_kernel_class_name": (C.c_char_p, [C.c_int]),
@@ -335,11 +335,13 @@ class Context:
         return dict(H=H.reshape(nA, nA + 1).T.copy(), Hraw=Hraw.reshape(nA, nA + 1).T.copy(), G=G, C=Cc, S=S)
 
     def psp_get_basis(self, j):
+        """V(:,j) as a new tensor (stored column times its lagged normalisation)."""
         p = _vp()
-        _check(lib().psp_get_basis(self.h, j, C.byref(p)), self.h)
+        sc = C.c_double()
+        _check(lib().psp_get_basis(self.h, j, C.byref(p), C.byref(sc)), self.h)
         base = self.ws.data_ptr()
         off = (p.value - base) // 8
-        return self.ws.view(self.torch.float64)[off:off + self.n]
+        return self.ws.view(self.torch.float64)[off:off + self.n] * sc.value
 
     def psp_launch_count(self):
         v = C.c_int64()
