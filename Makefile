@@ -4,9 +4,9 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 CSRC      := paper_1308_5626_b200/csrc
 LIB       := paper_1308_5626_b200/libpspgmres.so
-SRCS      := $(CSRC)/api.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
+SRCS      := $(CSRC)/api.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/fused.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
-HDRS      := $(CSRC)/internal.h include/pspgmres.h
+HDRS      := $(CSRC)/internal.h $(CSRC)/givens.cuh include/pspgmres.h
 ORACLE    := oracle/liboracle.so
 
 all: $(LIB) $(ORACLE)

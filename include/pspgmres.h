@@ -85,7 +85,9 @@ typedef struct {
   int32_t ortho;                   /* PSP_MGS_*; default PSP_MGS_1REDUCE                    */
   int32_t gate;                    /* apply the R21 dominance gate; default 1               */
   int32_t timing;                  /* record per-phase CUDA-event times in the report       */
-  int32_t pad_;
+  int32_t fused;                   /* with N = I and ICWY MGS, run each Arnoldi step as one  */
+                                   /* fused pass (update + matvec + dots, DESIGN.md s.6);    */
+                                   /* default 0 (opt-in: latency-bound in this version)      */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */
@@ -237,9 +239,11 @@ psp_status psp_banded_solve_raw(const double* d_lu, int64_t n, int d, const doub
 psp_status psp_set_bands(psp_ctx* ctx, const double* d_bands, int* h_accepted);
 /* Copy the current N into d_bands_out ((2d+1) x n_loc); *h_is_identity = 1 when N = I. */
 psp_status psp_get_bands(const psp_ctx* ctx, double* d_bands_out, int* h_is_identity);
-/* Probe ring view: column c (oldest -> newest) is at *d_px + slots[c]*ld (slots: host array
- * of at least m_max entries, may be NULL). */
-psp_status psp_ring_view(const psp_ctx* ctx, int* h_count, int32_t* h_slots,
+/* Probe ring view: the c-th oldest recorded probe (c < *h_count) is
+ *   P_x(:,c) = h_scale[c] * (*d_px + h_slots[c]*ld)[0..n_loc),  P_y(:,c) likewise with *d_py
+ * (the fused path stores probes unnormalised with their Krylov scale).  Host arrays h_slots /
+ * h_scale of at least m_max entries; any output may be NULL.  Synchronises for h_scale. */
+psp_status psp_ring_view(const psp_ctx* ctx, int* h_count, int32_t* h_slots, double* h_scale,
                          const double** d_px, const double** d_py, int64_t* ld);
 psp_status psp_ring_reset(psp_ctx* ctx);
 /* Hessenberg state of the current cycle: H ((restart+1) x restart col-major, rotated),
@@ -260,7 +264,7 @@ psp_status psp_launch_count(const psp_ctx* ctx, int64_t* h_launches);
 enum {
   PSP_KC_MATVEC = 0, PSP_KC_PRECOND = 1, PSP_KC_ORTHO_DOTS = 2, PSP_KC_ORTHO_UPDATE = 3,
   PSP_KC_MGS_LITERAL = 4, PSP_KC_NORMALIZE = 5, PSP_KC_COMBINE = 6, PSP_KC_RESIDUAL = 7,
-  PSP_KC_MREP = 8, PSP_KC_FACTOR = 9, PSP_KC_OTHER = 10, PSP_KC_COUNT = 11
+  PSP_KC_MREP = 8, PSP_KC_FACTOR = 9, PSP_KC_OTHER = 10, PSP_KC_FUSED = 11, PSP_KC_COUNT = 12
 };
 psp_status psp_kernel_stats(psp_ctx* ctx, double* h_ms, double* h_bytes, int64_t* h_launches,
                             int reset);

@@ -34,7 +34,12 @@ struct psp_ctx {
   // workspace carve
   double* ring_px = nullptr;
   double* ring_py = nullptr;
+  double* slot_scale = nullptr;  // per physical slot: the recorded probe is scale * column
   int ring_cap = 0, ring_count = 0, ring_head = 0;
+  int ring_phys = 0;             // ring_cap + 1: the slot after the newest is always free
+  // fused Arnoldi cycle (N = I): V(:,j) lives in ring slot vslot[j] (unnormalised)
+  bool cycle_fused = false;
+  int vslot[kMaxRestart + 2] = {};
   double* V = nullptr;
   int64_t ldv = 0;
   double* X0 = nullptr;
@@ -149,6 +154,7 @@ namespace {
 struct Plan {
   size_t off_px, off_py, off_V, off_X0, off_B, off_W, off_bands, off_lu, off_icpt, off_kind,
       off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
+      off_sscale,
       off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, total;
   int nblocks;
 };
@@ -174,8 +180,9 @@ Plan make_plan(int64_t n, int d, int nA, int m_max) {
   };
   const size_t vec = (size_t)n * 8;
   p.nblocks = 8 * sm_count();
-  p.off_px = take(vec * m_max);
-  p.off_py = take(vec * m_max);
+  p.off_px = take(vec * (m_max + 1));  // m_max probes + the free slot (fused path)
+  p.off_py = take(vec * (m_max + 1));
+  p.off_sscale = take((size_t)(m_max + 1) * 8);
   p.off_V = take(vec * (nA + 1));
   p.off_X0 = take(vec);
   p.off_B = take(vec);
@@ -248,6 +255,7 @@ void psp_default_opts(psp_opts* o) {
   o->ortho = PSP_MGS_1REDUCE;
   o->gate = 1;
   o->timing = 0;
+  o->fused = 0;  // the fused pass is correct but latency-bound: opt-in
 }
 
 const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }
@@ -332,6 +340,8 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ring_px = (double*)at(p.off_px);
   c->ring_py = (double*)at(p.off_py);
   c->ring_cap = o.m_max;
+  c->ring_phys = o.m_max + 1;
+  c->slot_scale = (double*)at(p.off_sscale);
   c->V = (double*)at(p.off_V);
   c->ldv = n;
   c->X0 = (double*)at(p.off_X0);
@@ -370,6 +380,7 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
     return fail(nullptr, PSP_E_CUDA, "cudaMallocHost failed");
   }
   memset(c->hp, 0, 64 * sizeof(double));
+  c->hp[32] = 1.0;  // the pinned constant 1.0 (scale of probes recorded normalised)
   for (int i = 0; i < 6; ++i) cudaEventCreate(&c->ev[i]);
   psp_status s = check_cuda(c, "psp_create");
   if (s != PSP_OK) {
@@ -424,7 +435,7 @@ psp_status psp_kernel_stats(psp_ctx* c, double* ms, double* bytes, int64_t* laun
 const char* psp_kernel_class_name(int k) {
   static const char* names[PSP_KC_COUNT] = {"matvec", "precond_solve", "ortho_dots", "ortho_update",
                                             "mgs_literal", "normalize", "combine", "residual",
-                                            "mrep_fit", "banded_factor", "other"};
+                                            "mrep_fit", "banded_factor", "other", "arnoldi_fused"};
   return (k >= 0 && k < PSP_KC_COUNT) ? names[k] : "?";
 }
 
@@ -435,21 +446,34 @@ const char* psp_kernel_class_name(int k) {
 // ------------------------------------------------------------------------------------------
 namespace {
 
-// next ring slot for a probe column (FIFO, R20)
+// The probe ring (FIFO of capacity m_max, R20) over m_max+1 physical slots: the slot after the
+// newest probe is always free, so a fused pass can write the next probe before it is known
+// whether it will be recorded (a cycle may converge first).
+int ring_peek(const psp_ctx* c) { return (c->ring_head + c->ring_count) % c->ring_phys; }
+// record a probe column: returns its slot (the free slot), evicting the oldest when full
 int ring_next(psp_ctx* c) {
-  int slot;
-  if (c->ring_count < c->ring_cap) {
-    slot = (c->ring_head + c->ring_count) % c->ring_cap;
-    c->ring_count += 1;
-  } else {
-    slot = c->ring_head;
-    c->ring_head = (c->ring_head + 1) % c->ring_cap;
-  }
+  const int slot = ring_peek(c);
+  if (c->ring_count < c->ring_cap) c->ring_count += 1;
+  else c->ring_head = (c->ring_head + 1) % c->ring_phys;
   return slot;
 }
+int ring_slot(const psp_ctx* c, int q) { return (c->ring_head + q) % c->ring_phys; }  // q-th oldest
 double* px_col(psp_ctx* c, int slot) { return c->ring_px + (int64_t)slot * c->n; }
 double* py_col(psp_ctx* c, int slot) { return c->ring_py + (int64_t)slot * c->n; }
 double* Vcol(psp_ctx* c, int j /*1-based*/) { return c->V + (int64_t)(j - 1) * c->ldv; }
+// a probe recorded normalised (scale 1)
+void set_unit_scale(psp_ctx* c, int slot) {
+  cudaMemcpyAsync(c->slot_scale + slot, c->hp + 32, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+}
+// the Krylov basis of the current cycle
+Basis basis(const psp_ctx* c) {
+  if (c->cycle_fused) return Basis{c->ring_px, c->n, c->vslot[1], c->ring_phys};
+  return Basis{c->V, c->ldv, 0, c->nA + 1};
+}
+bool fused_eligible(const psp_ctx* c) {
+  return c->opts.fused && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE &&
+         c->ring_cap >= c->nA + 1 && fused_supported(c->st, c->nA);
+}
 
 psp_status sync_read(psp_ctx* c, const double* dsrc, int count, double* hdst) {
   cudaMemcpyAsync(c->hp, dsrc, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
@@ -501,6 +525,7 @@ psp_status psp_matvec(psp_ctx* c, const double* x, double* y, int record) {
   if (c->sticky != PSP_OK) return c->sticky;
   if (record) {
     const int slot = ring_next(c);
+    set_unit_scale(c, slot);
     launch_matvec(c->st, x, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
     launch_copy(py_col(c, slot), y, c->n, c->stream);
     c->launches += 2;
@@ -518,6 +543,13 @@ psp_status psp_precond_apply(psp_ctx* c, const double* v, double* z) {
   return check_cuda(c, "psp_precond_apply");
 }
 
+// algorithmic bytes of the fused pass of step k (k = 0: the cycle-start pass)
+static double fused_bytes(const psp_ctx* c, int k) {
+  const bool cell = c->st.kind == PSP_OP_CELL_DIFF || c->st.kind == PSP_OP_CELL_ADVDIFF;
+  const double per = 8.0 * (k + 1 + (cell ? 1 : 0) + (k > 0 ? 1 : 0) + 1);
+  return per * (double)c->n;
+}
+
 psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double* h_beta) {
   if (!c || !b || !x0) return fail(c, PSP_E_ARG, "psp_cycle_begin: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
@@ -525,20 +557,36 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
     launch_copy(x0, c->X0, c->n, c->stream);
     c->launches += 1;
   }
+  c->cycle_fused = fused_eligible(c);
   // l.4: P_x(:,i) <- X0, P_y(:,i) <- A X0
   const int slot = ring_next(c);
+  set_unit_scale(c, slot);
   int h = kt_begin(c);
   launch_matvec(c->st, c->X0, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
-  // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta
+  // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta.  V(:,1) <- R_bar/beta
+  // (l.6) is stored unnormalised with alpha_1 = 1/beta.  On the fused path V(:,1) goes straight
+  // into the ring slot where it will be recorded as the probe Y_1 (N = I, l.11).
+  double* v1 = Vcol(c, 1);
+  if (c->cycle_fused) {
+    c->vslot[1] = ring_peek(c);
+    v1 = px_col(c, c->vslot[1]);
+  }
   h = kt_begin(c);
-  launch_residual(b, py_col(c, slot), Vcol(c, 1), c->n, c->nA, c->ds, c->rc, c->stream);
+  launch_residual(b, py_col(c, slot), v1, c->n, c->nA, c->ds, c->rc, c->stream);
   kt_end(c, h, PSP_KC_RESIDUAL, 24.0 * c->n);
   c->launches += 2;
   double beta;
   PSP_TRY(sync_read(c, c->ds.scal + SC_BETA, 1, &beta));
   if (h_beta) *h_beta = beta;
-  // V(:,1) <- R_bar / beta (l.6): stored unnormalised with alpha_1 = 1/beta (krylov.cu)
+  if (c->cycle_fused && beta > 0.0 && isfinite(beta)) {
+    // cycle-start pass: A V(:,1) -> P_y of the next slot and step 1's MGS coefficient
+    h = kt_begin(c);
+    launch_fused(c->st, basis(c), 0, c->nA, v1, nullptr, py_col(c, c->vslot[1]), c->slot_scale,
+                 c->vslot[1], c->ds, c->stream);
+    kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
+    c->launches += 1;
+  }
   c->last_k = 0;
   return check_cuda(c, "psp_cycle_begin");
 }
@@ -548,45 +596,69 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
   if (k < 1 || k > c->nA) return fail(c, PSP_E_ARG, "psp_arnoldi_step: k out of 1..restart");
   if (c->sticky != PSP_OK) return c->sticky;
   const int64_t n = c->n;
-  const int slot = ring_next(c);
-  double* px = px_col(c, slot);
-  double* py = py_col(c, slot);
-  const double* Vk = Vcol(c, k);
-  // l.10-12: Y_k = N^{-1} V(:,k) -> P_x(:,i); P_y(:,i) = A Y_k
   const double dn = (double)n;
   int h;
-  if (c->n_identity) {
-    h = kt_begin(c);
-    launch_matvec(c->st, Vk, c->ds.alpha + (k - 1), py, px, c->stream);  // N = I: probe copy fused
-    kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+  if (c->cycle_fused) {
+    // l.10-12: the probe (Y_k, A Y_k) = (V_k, A V_k) was written by the previous pass into the
+    // free slot; recording it makes it the newest probe.
+    const int slot = ring_next(c);
+    if (slot != c->vslot[k]) return fail(c, PSP_E_ARG, "psp_arnoldi_step: steps out of order (fused cycle)");
+    if (k < c->nA) {
+      // l.13-18 of step k, then l.10-16 of step k+1, in one pass
+      const int dst = ring_peek(c);
+      c->vslot[k + 1] = dst;
+      h = kt_begin(c);
+      launch_fused(c->st, basis(c), k, c->nA, py_col(c, slot), px_col(c, dst), py_col(c, dst),
+                   c->slot_scale, dst, c->ds, c->stream);
+      kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
+    } else {
+      // the last step of the cycle: only H(k+1,k) = ||U|| is needed (V(:,k+1) is never used)
+      h = kt_begin(c);
+      launch_icwy_update(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds,
+                         c->rc, c->stream);
+      kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+    }
     c->launches += 1;
   } else {
-    h = kt_begin(c);
-    banded_solve(c->lu, n, c->d, Vk, c->ds.alpha + (k - 1), nullptr, px, c->bs, c->stream, &c->launches);
-    kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
-    h = kt_begin(c);
-    launch_matvec(c->st, px, nullptr, py, nullptr, c->stream);
-    kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
-    c->launches += 1;
-  }
-  double* U = Vcol(c, k + 1);
-  // l.13-17: MGS (R11) + H(k+1,k) + Givens (l.19-32) in the last block
-  if (c->opts.ortho == PSP_MGS_LITERAL) {
-    h = kt_begin(c);
-    launch_mgs_literal(py, U, nullptr, Vcol(c, 1), 1, k, c->nA, n, c->ds, c->rc, c->stream);
-    for (int j = 2; j <= k; ++j)
-      launch_mgs_literal(U, U, Vcol(c, j - 1), Vcol(c, j), j, k, c->nA, n, c->ds, c->rc, c->stream);
-    launch_mgs_literal_final(U, Vcol(c, k), k, c->nA, n, c->ds, c->rc, c->stream);
-    kt_end(c, h, PSP_KC_MGS_LITERAL, (24.0 + 32.0 * (k - 1) + 24.0) * dn);
-    c->launches += k + 1;
-  } else {
-    h = kt_begin(c);
-    launch_icwy_dots(c->V, c->ldv, py, k, c->nA, n, c->ds, c->rc, c->stream);
-    kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 1) * dn);
-    h = kt_begin(c);
-    launch_icwy_update(c->V, c->ldv, py, U, k, c->nA, n, c->ds, c->rc, c->stream);
-    kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
-    c->launches += 2;
+    const int slot = ring_next(c);
+    set_unit_scale(c, slot);
+    double* px = px_col(c, slot);
+    double* py = py_col(c, slot);
+    const double* Vk = Vcol(c, k);
+    // l.10-12: Y_k = N^{-1} V(:,k) -> P_x(:,i); P_y(:,i) = A Y_k
+    if (c->n_identity) {
+      h = kt_begin(c);
+      launch_matvec(c->st, Vk, c->ds.alpha + (k - 1), py, px, c->stream);  // N = I: probe copy fused
+      kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+      c->launches += 1;
+    } else {
+      h = kt_begin(c);
+      banded_solve(c->lu, n, c->d, Vk, c->ds.alpha + (k - 1), nullptr, px, c->bs, c->stream, &c->launches);
+      kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
+      h = kt_begin(c);
+      launch_matvec(c->st, px, nullptr, py, nullptr, c->stream);
+      kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
+      c->launches += 1;
+    }
+    double* U = Vcol(c, k + 1);
+    // l.13-17: MGS (R11) + H(k+1,k) + Givens (l.19-32) in the last block
+    if (c->opts.ortho == PSP_MGS_LITERAL) {
+      h = kt_begin(c);
+      launch_mgs_literal(py, U, nullptr, Vcol(c, 1), 1, k, c->nA, n, c->ds, c->rc, c->stream);
+      for (int j = 2; j <= k; ++j)
+        launch_mgs_literal(U, U, Vcol(c, j - 1), Vcol(c, j), j, k, c->nA, n, c->ds, c->rc, c->stream);
+      launch_mgs_literal_final(U, Vcol(c, k), k, c->nA, n, c->ds, c->rc, c->stream);
+      kt_end(c, h, PSP_KC_MGS_LITERAL, (24.0 + 32.0 * (k - 1) + 24.0) * dn);
+      c->launches += k + 1;
+    } else {
+      h = kt_begin(c);
+      launch_icwy_dots(basis(c), py, k, c->nA, n, c->ds, c->rc, c->stream);
+      kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 1) * dn);
+      h = kt_begin(c);
+      launch_icwy_update(basis(c), py, nullptr, U, k, c->nA, n, c->ds, c->rc, c->stream);
+      kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+      c->launches += 2;
+    }
   }
   // l.18: V(:,k+1) = U / H(k+1,k) (R4: 0 on breakdown) -- lagged: alpha_{k+1} is set
   // by the Givens epilogue and folded into every reader of V(:,k+1)
@@ -609,12 +681,12 @@ psp_status psp_cycle_end(psp_ctx* c, int k, double* x) {
   // l.38-42: Q = H^{-1}G; Z = sum Q_j V_j; X = X0 + N^{-1} Z
   if (c->n_identity) {
     int h = kt_begin(c);
-    launch_combine(c->V, c->ldv, k, c->nA, c->X0, c->X0, c->n, c->ds, c->stream);
+    launch_combine(basis(c), k, c->nA, c->X0, c->X0, c->n, c->ds, c->stream);
     kt_end(c, h, PSP_KC_COMBINE, 8.0 * (k + 2) * (double)c->n);
     c->launches += 1;
   } else {
     int h = kt_begin(c);
-    launch_combine(c->V, c->ldv, k, c->nA, nullptr, c->W, c->n, c->ds, c->stream);
+    launch_combine(basis(c), k, c->nA, nullptr, c->W, c->n, c->ds, c->stream);
     kt_end(c, h, PSP_KC_COMBINE, 8.0 * (k + 1) * (double)c->n);
     c->launches += 1;
     h = kt_begin(c);
@@ -756,7 +828,7 @@ psp_status psp_mrep_fit_raw(const double* px, const double* py, int64_t n, int m
   std::vector<int32_t> slots(m);
   for (int c2 = 0; c2 < m; ++c2) slots[c2] = h_order ? h_order[c2] : c2;
   MrepOut out{bands, icpt, kind, kappa};
-  mrep_launch(px, py, ld, slots.data(), m, n, d, out, ms, s);
+  mrep_launch(px, py, nullptr, ld, slots.data(), m, n, d, out, ms, s);
   double r[16];
   if (cudaMemcpyAsync(r, ms.result, sizeof(r), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
@@ -841,11 +913,11 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
   }
   if (c->opts.timing) cudaEventRecord(c->ev[2], c->stream);
   std::vector<int32_t> slots(m);
-  for (int q = 0; q < m; ++q) slots[q] = (c->ring_head + q) % c->ring_cap;
+  for (int q = 0; q < m; ++q) slots[q] = ring_slot(c, q);
   MrepOut out{c->bands, c->intercept, c->rowkind, c->kappa};
   cudaMemsetAsync(c->ms.ticket, 0, 64, c->stream);
   int h = kt_begin(c);
-  mrep_launch(c->ring_px, c->ring_py, c->n, slots.data(), m, c->n, c->d, out, c->ms, c->stream);
+  mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms, c->stream);
   kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
   c->launches += 3;
   double r[16];
@@ -923,12 +995,18 @@ psp_status psp_get_bands(const psp_ctx* c, double* d_out, int* h_ident) {
   return PSP_OK;
 }
 
-psp_status psp_ring_view(const psp_ctx* c, int* count, int32_t* slots, const double** px,
-                         const double** py, int64_t* ld) {
+psp_status psp_ring_view(const psp_ctx* c, int* count, int32_t* slots, double* scale,
+                         const double** px, const double** py, int64_t* ld) {
   if (!c) return PSP_E_ARG;
   if (count) *count = c->ring_count;
   if (slots)
-    for (int q = 0; q < c->ring_count; ++q) slots[q] = (c->ring_head + q) % c->ring_cap;
+    for (int q = 0; q < c->ring_count; ++q) slots[q] = ring_slot(c, q);
+  if (scale && c->ring_count > 0) {
+    std::vector<double> all(c->ring_phys);
+    cudaMemcpyAsync(all.data(), c->slot_scale, all.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;
+    for (int q = 0; q < c->ring_count; ++q) scale[q] = all[ring_slot(c, q)];
+  }
   if (px) *px = c->ring_px;
   if (py) *py = c->ring_py;
   if (ld) *ld = c->n;
@@ -955,7 +1033,7 @@ psp_status psp_get_hessenberg(const psp_ctx* c, double* H, double* Hraw, double*
 
 psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj, double* h_scale) {
   if (!c || !d_vj || j < 1 || j > c->nA + 1) return PSP_E_ARG;
-  *d_vj = c->V + (int64_t)(j - 1) * c->ldv;
+  *d_vj = c->cycle_fused ? c->ring_px + (int64_t)c->vslot[j] * c->n : c->V + (int64_t)(j - 1) * c->ldv;
   if (h_scale) {
     cudaMemcpyAsync(c->hp + 16, c->ds.alpha + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;

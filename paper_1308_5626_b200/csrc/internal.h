@@ -69,6 +69,16 @@ struct RedCfg {
   int max_vals;      // partials per block the partials buffer holds
 };
 
+// Krylov basis columns V(:,j), j = 0..: either a plain column-major array (s1 = 0, cap large)
+// or consecutive slots of the probe ring (the fused path stores V(:,j) in P_x slots).
+struct Basis {
+  const double* base;
+  int64_t ld;
+  int s1;
+  int cap;
+  __host__ __device__ const double* col(int j) const { return base + (int64_t)((s1 + j) % cap) * ld; }
+};
+
 // ---- Krylov kernels (krylov.cu) ----
 // ||x||_2 -> scal[slot] (deterministic tree order; sqrt applied)
 void launch_norm(const double* x, int64_t n, DevState ds, int slot, const RedCfg& rc, cudaStream_t s);
@@ -83,19 +93,26 @@ void launch_mgs_literal(const double* src, double* U, const double* Vprev, const
 void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_t n,
                               DevState ds, const RedCfg& rc, cudaStream_t s);
 // ICWY one-reduction MGS (R11): pass A = dots V_j'w (j<=k), V_j'V_k (j<k); solve (I+L)h = s
-void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int nA, int64_t n,
+void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n,
                       DevState ds, const RedCfg& rc, cudaStream_t s);
 // pass B = U = w - sum_j h_j V_j ; H(k+1,k) = ||U|| ; Givens update
-void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
+void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
 // Q = H^{-1} G (R6) and out = base + sum_j Q_j V_j; base may be NULL (Z only)
-void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
+void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s);
 // y = x (plain copy on the stream)
 void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s);
 // ||b - y|| -> scal[slot]
 void launch_diff_norm(const double* b, const double* y, int64_t n, DevState ds, int slot,
                       const RedCfg& rc, cudaStream_t s);
+
+// ---- fused single-pass Arnoldi step for N = I (fused.cu) ----
+bool fused_supported(const Stencil& st, int k);
+// finish step k (u = V_{k+1} -> dstx, A u -> dsty, H(k+1,k), Givens, alpha_{k+1} ->
+// slot_scale[dst_slot]) and compute step k+1's MGS coefficients; k = 0 is the cycle-start pass
+void launch_fused(const Stencil& st, Basis V, int k, int nA, const double* src, double* dstx,
+                  double* dsty, double* slot_scale, int dst_slot, DevState ds, cudaStream_t s);
 
 // ---- MREP (mrep.cu) ----
 struct MrepOut {
@@ -114,8 +131,10 @@ struct MrepScratch {
 constexpr int kMrepMaxBlocks = 148 * 8;
 int mrep_blocks(int64_t n, int d);
 // Alg.2 on probe columns px + slots[c]*ld (c = 0..m-1 oldest -> newest), then R18 + gate stats.
-void mrep_launch(const double* px, const double* py, int64_t ld, const int32_t* slots, int m,
-                 int64_t n, int d, MrepOut out, MrepScratch sc, cudaStream_t s);
+// slot_scale (device, per slot, may be NULL): the recorded probe is slot_scale[slot] * column.
+void mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
+                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
+                 cudaStream_t s);
 
 // ---- banded LU (banded.cu) ----
 struct BandedScratch {

@@ -16,6 +16,7 @@
 // loads in flight: enough bytes in flight per SM to cover the HBM latency.
 #include <math.h>
 
+#include "givens.cuh"
 #include "internal.h"
 
 namespace psp {
@@ -77,52 +78,6 @@ __device__ double reduce_partials(const double* partials, int v, int nb, double*
   return a[0];
 }
 
-// ------------------------------------------------------------------------------------------
-// Givens update of column k (Alg.1 l.19-32; R4, R10).  One thread.  Also sets the
-// lagged normalisation alpha_{k+1} = 1/H(k+1,k) of V(:,k+1) (l.18; 0 on breakdown).
-// ------------------------------------------------------------------------------------------
-__device__ void givens_update(DevState ds, int k, int nA) {
-  const int ld = nA + 1;
-  double* Hc = ds.H + (int64_t)(k - 1) * ld;
-  double colsq = 0.0;
-  for (int j = 0; j <= k; ++j) {
-    ds.Hraw[(int64_t)(k - 1) * ld + j] = Hc[j];
-    colsq += Hc[j] * Hc[j];
-  }
-  const double hk1 = Hc[k];
-  bool breakdown = !(hk1 > 1e-14 * sqrt(colsq));   // R4, before rotation
-  const bool nonfinite = !isfinite(hk1);
-  ds.alpha[k] = (breakdown || nonfinite) ? 0.0 : 1.0 / hk1;
-  ds.G[k] = 0.0;                                    // l.9: G(k+1) <- 0
-  for (int j = 1; j <= k - 1; ++j) {                // l.19-23
-    const double delta = Hc[j - 1];
-    Hc[j - 1] = delta * ds.C[j - 1] + ds.S[j - 1] * Hc[j];
-    Hc[j] = -delta * ds.S[j - 1] + ds.C[j - 1] * Hc[j];
-  }
-  const double a = Hc[k - 1], b = Hc[k];            // l.24-28, R10
-  const double gamma = sqrt(a * a + b * b);
-  if (gamma == 0.0) {
-    ds.C[k - 1] = 1.0;
-    ds.S[k - 1] = 0.0;
-    breakdown = true;
-  } else {
-    ds.C[k - 1] = a / gamma;
-    ds.S[k - 1] = b / gamma;
-  }
-  Hc[k - 1] = gamma;
-  Hc[k] = 0.0;
-  const double delta = ds.G[k - 1];                 // l.29-31
-  ds.G[k - 1] = ds.C[k - 1] * delta + ds.S[k - 1] * ds.G[k];
-  ds.G[k] = -ds.S[k - 1] * delta + ds.C[k - 1] * ds.G[k];
-  const double R = fabs(ds.G[k]);                   // l.32
-  ds.resid[k - 1] = R;
-  ds.scal[SC_RK] = R;
-  int flags = 0;
-  if (R <= ds.scal[SC_EPS]) flags |= PSP_FLAG_CONVERGED;  // l.33
-  if (breakdown) flags |= PSP_FLAG_BREAKDOWN;
-  if (nonfinite || !isfinite(R)) flags |= PSP_FLAG_NONFINITE;
-  ds.scal[SC_FLAGS] = (double)flags;
-}
 
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TPB) norm_kernel(const double* __restrict__ x, int64_t n,
@@ -251,7 +206,7 @@ __global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restri
 // the k+1 vectors; the last block solves (I + L) h = s into H(1..k, k).
 // ------------------------------------------------------------------------------------------
 template <int C, bool FULL>
-__device__ __forceinline__ void dots_chunk(const double* __restrict__ V, int64_t ldv, int j0,
+__device__ __forceinline__ void dots_chunk(Basis V, int j0,
                                            const double (&wr)[RPT], const double (&qr)[RPT],
                                            int64_t n, int64_t r0, int lane, int k, double* acc) {
   double as[C], al[C];
@@ -262,7 +217,7 @@ __device__ __forceinline__ void dots_chunk(const double* __restrict__ V, int64_t
   }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const double* __restrict__ vj = V + (int64_t)(j0 + c) * ldv;
+    const double* __restrict__ vj = V.col(j0 + c);
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int64_t r = r0 + (int64_t)TPB * i;
@@ -283,10 +238,10 @@ __device__ __forceinline__ void dots_chunk(const double* __restrict__ V, int64_t
 }
 
 template <bool FULL>
-__device__ __forceinline__ void dots_tile(const double* __restrict__ V, int64_t ldv,
+__device__ __forceinline__ void dots_tile(Basis V,
                                           const double* __restrict__ w, int k, int64_t n,
                                           int64_t r0, int lane, double* acc) {
-  const double* __restrict__ qk = V + (int64_t)(k - 1) * ldv;
+  const double* __restrict__ qk = V.col(k - 1);
   double wr[RPT], qr[RPT];
   double sk = 0.0;
 #pragma unroll
@@ -297,12 +252,12 @@ __device__ __forceinline__ void dots_tile(const double* __restrict__ V, int64_t 
     sk = fma(qr[i], wr[i], sk);
   }
   int j0 = 0;
-  for (; j0 + JC <= k - 1; j0 += JC) dots_chunk<JC, FULL>(V, ldv, j0, wr, qr, n, r0, lane, k, acc);
-  for (; j0 < k - 1; ++j0) dots_chunk<1, FULL>(V, ldv, j0, wr, qr, n, r0, lane, k, acc);
+  for (; j0 + JC <= k - 1; j0 += JC) dots_chunk<JC, FULL>(V, j0, wr, qr, n, r0, lane, k, acc);
+  for (; j0 < k - 1; ++j0) dots_chunk<1, FULL>(V, j0, wr, qr, n, r0, lane, k, acc);
   sk = warp_sum(sk);
   if (lane == 0) acc[k - 1] += sk;
 }
-__global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict__ V, int64_t ldv,
+__global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
                                                         const double* __restrict__ w, int k,
                                                         int nA, int64_t n, DevState ds) {
   __shared__ double accw[kWarps][2 * kMaxRestart];
@@ -314,8 +269,8 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(const double* __restrict
   const int64_t nfull = n / TILE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * TILE + t;
-    if (tile < nfull) dots_tile<true>(V, ldv, w, k, n, r0, lane, accw[warp]);
-    else dots_tile<false>(V, ldv, w, k, n, r0, lane, accw[warp]);
+    if (tile < nfull) dots_tile<true>(V, w, k, n, r0, lane, accw[warp]);
+    else dots_tile<false>(V, w, k, n, r0, lane, accw[warp]);
   }
   __syncthreads();
   const int nb = gridDim.x;
@@ -357,15 +312,14 @@ constexpr int UJC = 8;
 constexpr int UTILE = TPB * URPT;
 
 template <bool FULL>
-__device__ __forceinline__ void update_tile(const double* __restrict__ V, int64_t ldv,
-                                            const double* __restrict__ w, double* __restrict__ U,
+__device__ __forceinline__ void update_tile(Basis V, const double* w, double wsc, double* U,
                                             const double* hs, int k, int64_t n, int64_t r0,
                                             double& acc) {
   double u[URPT];
 #pragma unroll
   for (int i = 0; i < URPT; ++i) {
     const int64_t r = r0 + (int64_t)TPB * i;
-    u[i] = (FULL || r < n) ? w[r] : 0.0;
+    u[i] = (w != nullptr && (FULL || r < n)) ? wsc * w[r] : 0.0;
   }
   int jb = 0;
   for (; jb + UJC <= k; jb += UJC) {
@@ -375,7 +329,7 @@ __device__ __forceinline__ void update_tile(const double* __restrict__ V, int64_
 #pragma unroll
       for (int i = 0; i < URPT; ++i) {
         const int64_t r = r0 + (int64_t)TPB * i;
-        v[c][i] = (FULL || r < n) ? V[(int64_t)(jb + c) * ldv + r] : 0.0;
+        v[c][i] = (FULL || r < n) ? V.col(jb + c)[r] : 0.0;
       }
 #pragma unroll
     for (int c = 0; c < UJC; ++c)
@@ -387,7 +341,7 @@ __device__ __forceinline__ void update_tile(const double* __restrict__ V, int64_
 #pragma unroll
     for (int i = 0; i < URPT; ++i) {
       const int64_t r = r0 + (int64_t)TPB * i;
-      v[i] = (FULL || r < n) ? V[(int64_t)jb * ldv + r] : 0.0;
+      v[i] = (FULL || r < n) ? V.col(jb)[r] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < URPT; ++i) u[i] = fma(-hs[jb], v[i], u[i]);
@@ -404,8 +358,8 @@ __device__ __forceinline__ void update_tile(const double* __restrict__ V, int64_
 
 // Pass B: U = w - sum_j h_j alpha_j V_j (sequential in j, as the MGS updates), H(k+1,k) =
 // ||U||, then the Givens update of column k.
-__global__ void __launch_bounds__(TPB) icwy_update_kernel(const double* __restrict__ V, int64_t ldv,
-                                                          const double* __restrict__ w,
+__global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double* __restrict__ w,
+                                                          const double* ws,
                                                           double* __restrict__ U, int k, int nA,
                                                           int64_t n, DevState ds) {
   __shared__ double hs[kMaxRestart];
@@ -413,13 +367,14 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(const double* __restri
   const int ld = nA + 1, t = threadIdx.x;
   for (int q = t; q < k; q += TPB) hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
   __syncthreads();
+  const double wsc = ws ? *ws : 1.0;  // scale of w (the fused path stores A u unnormalised)
   double a[1] = {0.0};
   const int64_t ntiles = (n + UTILE - 1) / UTILE;
   const int64_t nfull = n / UTILE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * UTILE + t;
-    if (tile < nfull) update_tile<true>(V, ldv, w, U, hs, k, n, r0, a[0]);
-    else update_tile<false>(V, ldv, w, U, hs, k, n, r0, a[0]);
+    if (tile < nfull) update_tile<true>(V, w, wsc, U, hs, k, n, r0, a[0]);
+    else update_tile<false>(V, w, wsc, U, hs, k, n, r0, a[0]);
   }
   block_sum<1>(a, sm);
   if (t == 0) ds.partials[blockIdx.x] = a[0];
@@ -434,8 +389,7 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(const double* __restri
 
 // l.38-42: Q = H^{-1} G (R6, every block recomputes the k x k back-substitution
 // redundantly: identical inputs, identical result), out = base + sum_j Q_j alpha_j V_j.
-__global__ void __launch_bounds__(TPB) combine_kernel(const double* __restrict__ V, int64_t ldv,
-                                                      int k, int nA, const double* base,
+__global__ void __launch_bounds__(TPB) combine_kernel(Basis V, int k, int nA, const double* base,
                                                       double* out, int64_t n, DevState ds) {
   __shared__ double qs[kMaxRestart];
   __shared__ double qa[kMaxRestart];
@@ -450,33 +404,21 @@ __global__ void __launch_bounds__(TPB) combine_kernel(const double* __restrict__
       if (piv == 0.0) { bad = 1; qs[j - 1] = 0.0; continue; }
       qs[j - 1] = s / piv;
     }
-    for (int j = 0; j < k; ++j) qa[j] = qs[j] * ds.alpha[j];
+    for (int j = 0; j < k; ++j) qa[j] = -qs[j] * ds.alpha[j];  // update_tile subtracts
     if (blockIdx.x == 0) {
       for (int j = 0; j < k; ++j) ds.Q[j] = qs[j];
       ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
     }
   }
   __syncthreads();
-  const int64_t ntiles = (n + TILE - 1) / TILE;
-  const int t = threadIdx.x;
+  // out = base - sum_j qa_j V_j with qa = -Q alpha (the register-tiled update pass)
+  const int64_t ntiles = (n + UTILE - 1) / UTILE;
+  const int64_t nfull = n / UTILE;
+  double unused = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * TILE + t;
-    double z[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) z[i] = 0.0;
-    for (int jb = 0; jb < k; ++jb) {
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int64_t r = r0 + (int64_t)TPB * i;
-        const double v = r < n ? V[(int64_t)jb * ldv + r] : 0.0;
-        z[i] = fma(qa[jb], v, z[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int64_t r = r0 + (int64_t)TPB * i;
-      if (r < n) out[r] = base ? base[r] + z[i] : z[i];
-    }
+    const int64_t r0 = tile * UTILE + threadIdx.x;
+    if (tile < nfull) update_tile<true>(V, base, 1.0, out, qa, k, n, r0, unused);
+    else update_tile<false>(V, base, 1.0, out, qa, k, n, r0, unused);
   }
 }
 
@@ -518,20 +460,22 @@ void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_
                               DevState ds, const RedCfg& rc, cudaStream_t s) {
   mgs_literal_final_kernel<<<rc.nblocks, TPB, 0, s>>>(U, Vk, k, nA, n, ds);
 }
-void launch_icwy_dots(const double* V, int64_t ldv, const double* w, int k, int nA, int64_t n,
+void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n,
                       DevState ds, const RedCfg& rc, cudaStream_t s) {
   // grid: 4 blocks per SM for the dots, 8 for the update (measured best, tools/ortho_micro.cu)
-  icwy_dots_kernel<<<tiles_grid(n, rc.nblocks / 2), TPB, 0, s>>>(V, ldv, w, k, nA, n, ds);
+  icwy_dots_kernel<<<tiles_grid(n, rc.nblocks / 2), TPB, 0, s>>>(V, w, k, nA, n, ds);
 }
-void launch_icwy_update(const double* V, int64_t ldv, const double* w, double* U, int k,
+void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
   int64_t ub = (n + UTILE - 1) / UTILE;
   if (ub > rc.nblocks) ub = rc.nblocks;
-  icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, ldv, w, U, k, nA, n, ds);
+  icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds);
 }
-void launch_combine(const double* V, int64_t ldv, int k, int nA, const double* base, double* out,
+void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {
-  combine_kernel<<<tiles_grid(n, 148 * 4), TPB, 0, s>>>(V, ldv, k, nA, base, out, n, ds);
+  int64_t cb = (n + UTILE - 1) / UTILE;
+  if (cb > 148 * 8) cb = 148 * 8;
+  combine_kernel<<<(int)(cb < 1 ? 1 : cb), TPB, 0, s>>>(V, k, nA, base, out, n, ds);
 }
 
 }  // namespace psp

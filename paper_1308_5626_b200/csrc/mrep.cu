@@ -29,8 +29,10 @@ constexpr int kMaxM = 256;     // probe columns supported
 struct Cols {
   const double* px;            // column c of P_x at px + slot[c]*ld
   const double* py;
+  const double* scale;         // per slot: the probe is scale[slot] * column (NULL: 1)
   int64_t ld;
   int32_t slot[kMaxM];
+  __device__ double sc(int c) const { return scale ? __ldg(scale + slot[c]) : 1.0; }
 };
 
 __device__ __forceinline__ double band_abs_off_sum(const double* row /*2d+1 coeffs*/, int d,
@@ -113,13 +115,14 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
     double yv[CB];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc)                 // this row's P_y samples of the chunk
-      yv[cc] = (cc < cn && rvalid) ? __ldg(cols.py + (int64_t)cols.slot[c0 + cc] * cols.ld + r) : 0.0;
+      yv[cc] = (cc < cn && rvalid) ? cols.sc(c0 + cc) * __ldg(cols.py + (int64_t)cols.slot[c0 + cc] * cols.ld + r) : 0.0;
     __syncthreads();
     for (int cc = 0; cc < cn; ++cc) {
       const double* __restrict__ colx = cols.px + (int64_t)cols.slot[c0 + cc] * cols.ld;
+      const double scx = cols.sc(c0 + cc);
       for (int q = t; q < TILE; q += TPB) {
         const int64_t rr = tile0 + q;
-        xs[cc][q] = (rr >= 0 && rr < n) ? __ldg(colx + rr) : 0.0;
+        xs[cc][q] = (rr >= 0 && rr < n) ? scx * __ldg(colx + rr) : 0.0;
       }
     }
     __syncthreads();
@@ -274,15 +277,15 @@ __global__ void mrep_boundary_kernel(Cols cols, int m, int64_t n, int d, MrepOut
     const int64_t i = (t < d) ? t : (n - 2 * d + t);
     double mx = 0.0, my = 0.0;
     for (int c = 0; c < m; ++c) {
-      mx += cols.px[(int64_t)cols.slot[c] * cols.ld + i];
-      my += cols.py[(int64_t)cols.slot[c] * cols.ld + i];
+      mx += cols.sc(c) * cols.px[(int64_t)cols.slot[c] * cols.ld + i];
+      my += cols.sc(c) * cols.py[(int64_t)cols.slot[c] * cols.ld + i];
     }
     mx /= (double)m;
     my /= (double)m;
     double sxx = 0.0, sxy = 0.0;
     for (int c = 0; c < m; ++c) {
-      const double dx = cols.px[(int64_t)cols.slot[c] * cols.ld + i] - mx;
-      const double dy = cols.py[(int64_t)cols.slot[c] * cols.ld + i] - my;
+      const double dx = cols.sc(c) * cols.px[(int64_t)cols.slot[c] * cols.ld + i] - mx;
+      const double dy = cols.sc(c) * cols.py[(int64_t)cols.slot[c] * cols.ld + i] - my;
       sxx += dx * dx;
       sxy += dx * dy;
     }
@@ -340,11 +343,13 @@ int mrep_blocks(int64_t n, int d) {
   return (int)(t < kMrepMaxBlocks ? t : kMrepMaxBlocks);
 }
 
-void mrep_launch(const double* px, const double* py, int64_t ld, const int32_t* slots, int m,
-                 int64_t n, int d, MrepOut out, MrepScratch sc, cudaStream_t s) {
+void mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
+                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
+                 cudaStream_t s) {
   Cols cols;
   cols.px = px;
   cols.py = py;
+  cols.scale = slot_scale;
   cols.ld = ld;
   for (int c = 0; c < m && c < kMaxM; ++c) cols.slot[c] = slots ? slots[c] : c;
   cudaMemsetAsync(sc.result, 0, 16 * sizeof(double), s);

@@ -23,7 +23,7 @@ PSP_OP_CONST_DIFF, PSP_OP_CELL_DIFF, PSP_OP_CELL_ADVDIFF, PSP_OP_DIA = range(4)
 PSP_TOL_REL_B, PSP_TOL_ABS = 0, 1
 PSP_MGS_1REDUCE, PSP_MGS_LITERAL = 0, 1
 PSP_FLAG_CONVERGED, PSP_FLAG_BREAKDOWN, PSP_FLAG_NONFINITE = 1, 2, 4
-PSP_KC_COUNT = 11
+PSP_KC_COUNT = 12
 ROW_INTERIOR, ROW_INTERIOR_RIDGE, ROW_BOUNDARY, ROW_FALLBACK_RANK, ROW_FALLBACK_ZEROVAR, \
     ROW_FALLBACK_SMALLDIAG = range(6)
 KIND_CODES = {"const_diff": PSP_OP_CONST_DIFF, "cell_diff": PSP_OP_CELL_DIFF,
@@ -45,7 +45,7 @@ class psp_stencil(C.Structure):
 class psp_opts(C.Structure):
     _fields_ = [("max_cycles", C.c_int32), ("tol_mode", C.c_int32), ("m_max", C.c_int32),
                 ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
-                ("timing", C.c_int32), ("pad_", C.c_int32)]
+                ("timing", C.c_int32), ("fused", C.c_int32)]
 
 
 class psp_report(C.Structure):
@@ -108,7 +108,7 @@ def lib():
         "psp_banded_solve_raw": (C.c_int, [_vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
         "psp_set_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
         "psp_get_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
-        "psp_ring_view": (C.c_int, [_vp, P(C.c_int), P(C.c_int32), P(_vp), P(_vp), P(C.c_int64)]),
+        "psp_ring_view": (C.c_int, [_vp, P(C.c_int), P(C.c_int32), _dp, P(_vp), P(_vp), P(C.c_int64)]),
         "psp_ring_reset": (C.c_int, [_vp]),
         "psp_get_hessenberg": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),
         "psp_get_basis": (C.c_int, [_vp, C.c_int, P(_vp), P(C.c_double)]),
@@ -304,21 +304,25 @@ class Context:
         return out, bool(ident.value)
 
     def psp_ring_view(self):
-        """(count, slots, P_x (cap, n) tensor view, P_y view) -- views into the workspace."""
+        """(count, slots, P_x, P_y): the recorded probes oldest -> newest as new (count, n) tensors
+        (each column times its recorded scale)."""
         cnt = C.c_int()
-        slots = (C.c_int32 * 256)()
+        slots = (C.c_int32 * 257)()
+        scale = np.zeros(257)
         px, py = _vp(), _vp()
         ld = C.c_int64()
-        _check(lib().psp_ring_view(self.h, C.byref(cnt), slots, C.byref(px), C.byref(py), C.byref(ld)), self.h)
+        _check(lib().psp_ring_view(self.h, C.byref(cnt), slots, scale.ctypes.data_as(_dp), C.byref(px),
+                                   C.byref(py), C.byref(ld)), self.h)
         base = self.ws.data_ptr()
-        cap = self.opts.m_max
+        phys = self.opts.m_max + 1
         t = self.torch
-        off_x = (px.value - base) // 8
-        off_y = (py.value - base) // 8
-        ws64 = self.ws.view(t.float64) if (base % 8 == 0) else None
-        PX = ws64[off_x:off_x + cap * self.n].view(cap, self.n)
-        PY = ws64[off_y:off_y + cap * self.n].view(cap, self.n)
-        return cnt.value, list(slots[:cnt.value]), PX, PY
+        ws64 = self.ws.view(t.float64)
+        PXr = ws64[(px.value - base) // 8:(px.value - base) // 8 + phys * self.n].view(phys, self.n)
+        PYr = ws64[(py.value - base) // 8:(py.value - base) // 8 + phys * self.n].view(phys, self.n)
+        m = cnt.value
+        sl = list(slots[:m])
+        sc = t.tensor(scale[:m], dtype=t.float64, device=self.device)[:, None]
+        return m, sl, PXr[sl] * sc, PYr[sl] * sc
 
     def psp_ring_reset(self):
         _check(lib().psp_ring_reset(self.h), self.h)

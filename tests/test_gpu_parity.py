@@ -74,7 +74,7 @@ def test_matvec_parity(torch, P, orc, name, mk):
     # recording: the ring holds (x, A x)
     ctx.psp_matvec(xt, yt, record=True)
     cnt, slots, PX, PY = ctx.psp_ring_view()
-    assert cnt == 1 and torch.equal(PX[slots[0]], xt) and torch.equal(PY[slots[0]], yt)
+    assert cnt == 1 and torch.equal(PX[0], xt) and torch.equal(PY[0], yt)
     ctx.close()
 
 
@@ -212,8 +212,11 @@ def test_mrep_insufficient_samples(torch, P):
 # ------------------------------------------------------------------------------------------
 # T4-T6: Algorithm 1 and the time-step driver
 # ------------------------------------------------------------------------------------------
-def run_gpu_steps(torch, P, prob, steps, ortho):
-    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho)
+MODES = {"fused": dict(ortho=0, fused=1), "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
+
+
+def run_gpu_steps(torch, P, prob, steps, mode):
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, **MODES[mode])
     ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts)
     u = dev(torch, prob.u0)
     reps = []
@@ -276,8 +279,8 @@ LOCKSTEP_CASES = [
 
 
 @pytest.mark.parametrize("name,mk,steps", LOCKSTEP_CASES, ids=[c[0] for c in LOCKSTEP_CASES])
-@pytest.mark.parametrize("ortho", [0, 1], ids=["1reduce", "literal"])
-def test_lockstep_parity(torch, P, orc, name, mk, steps, ortho):
+@pytest.mark.parametrize("mode", list(MODES))
+def test_lockstep_parity(torch, P, orc, name, mk, steps, mode):
     """Each time step on identical inputs: the GPU solves from the oracle's u^s with the oracle's
     N_s (an oracle output, installed through psp_set_bands), and the GPU MREP fits the oracle's
     probe ring.  (Free-running, the probes of later cycles sit at the FP64 floor of
@@ -286,7 +289,7 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, ortho):
     prob = mk()
     n = prob.op.rows
     drv = orc.Driver(prob.op, n, prob.restart, prob.max_cycles, prob.tol, prob.d, prob.m_max)
-    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho)
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, **MODES[mode])
     ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts)
     u = prob.u0.copy()
     for s in range(steps):
@@ -318,14 +321,14 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, ortho):
     ctx.close()
 
 
-@pytest.mark.parametrize("ortho", [0, 1], ids=["1reduce", "literal"])
-def test_free_running_c1(torch, P, orc, ortho):
+@pytest.mark.parametrize("mode", list(MODES))
+def test_free_running_c1(torch, P, orc, mode):
     """The whole driver on the GPU (its own probes, fits, gates) vs the oracle's: the first step
     (N = I on both sides) to T4/T6; later steps to T5 (+-1 iteration, same cycles), the same
     gate decisions, both converged, the interior rows of both N equal to A's (PN4 closed form)."""
     prob = inputs.c1()
     r = orc.time_steps(prob.op, prob.u0, prob.steps, prob.restart, prob.max_cycles, prob.tol, prob.d, prob.m_max)
-    g = run_gpu_steps(torch, P, prob, prob.steps, ortho)
+    g = run_gpu_steps(torch, P, prob, prob.steps, mode)
     for s, (gr, orr) in enumerate(zip(g["reports"], r["reports"])):
         o = orr["solve"]
         assert gr["cycles"] == o["cycles"] and abs(gr["iterations"] - o["iterations"]) <= 1, s
@@ -342,12 +345,13 @@ def test_free_running_c1(torch, P, orc, ortho):
     g["ctx"].close()
 
 
-def test_arnoldi_cycle_invariants(torch, P, orc):
+@pytest.mark.parametrize("fused", [1, 0], ids=["fused", "split"])
+def test_arnoldi_cycle_invariants(torch, P, orc, fused):
     # one cycle through the step-level ABI: Hessenberg vs oracle trace; V orthonormal;
     # Arnoldi relation on the recorded probes (P_y(:,i_k) = V_{k+1} Hbar(:,k))
     prob = inputs.c4(n=12, steps=1)
     n_A = 10
-    opts = P.default_opts(m_max=32)
+    opts = P.default_opts(m_max=32, fused=fused)
     ctx = P.Context(prob.op, d=3, restart=n_A, tol=1e-30, opts=opts)
     b = dev(torch, prob.u0)
     x0 = torch.zeros_like(b)
@@ -359,13 +363,16 @@ def test_arnoldi_cycle_invariants(torch, P, orc):
     assert beta == pytest.approx(r["beta_hist"][0], rel=1e-14)
     assert np.all(np.abs(np.array(res) - r["resid_hist"]) <= 1e-8 * r["resid_hist"] + 1e-12 * beta)  # T4
     assert np.max(np.abs(hs["Hraw"] - t["Hraw"])) <= 1e-11 * np.abs(t["Hraw"]).max()
-    V = torch.stack([ctx.psp_get_basis(j) for j in range(1, n_A + 2)], dim=1).cpu().numpy()
-    assert np.max(np.abs(V.T @ V - np.eye(n_A + 1))) <= 1e-12
+    # (the fused path never stores V(:,n_A+1): only its norm H(n_A+1,n_A) is used)
+    nv = n_A if fused else n_A + 1
+    V = torch.stack([ctx.psp_get_basis(j) for j in range(1, nv + 1)], dim=1).cpu().numpy()
+    assert np.max(np.abs(V.T @ V - np.eye(nv))) <= 1e-12
     cnt, slots, PX, PY = ctx.psp_ring_view()
     assert cnt == n_A + 1
-    PYh = PY.cpu().numpy()
-    for k in range(1, n_A + 1):
-        lhs = PYh[slots[k]]
+    PXh, PYh = PX.cpu().numpy(), PY.cpu().numpy()
+    for k in range(1, nv):
+        assert np.max(np.abs(PXh[k] - V[:, k - 1])) <= 1e-15 * np.abs(V[:, k - 1]).max()   # Y_k = V_k (N = I)
+        lhs = PYh[k]
         rhs = V[:, :k + 1] @ hs["Hraw"][:k + 1, k - 1]
         assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.abs(lhs).max()
     x = torch.empty_like(b)
@@ -394,7 +401,7 @@ def test_edge_cases(torch, P, orc):
 
 def test_determinism(torch, P):
     prob = inputs.c1(n=512, steps=2)
-    a = run_gpu_steps(torch, P, prob, 2, 0)
-    b = run_gpu_steps(torch, P, prob, 2, 0)
+    a = run_gpu_steps(torch, P, prob, 2, "fused")
+    b = run_gpu_steps(torch, P, prob, 2, "fused")
     assert np.array_equal(a["u"], b["u"])
     assert np.array_equal(a["reports"][0]["resid_history"], b["reports"][0]["resid_history"])
