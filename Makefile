@@ -4,7 +4,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 CSRC      := paper_1308_5626_b200/csrc
 LIB       := paper_1308_5626_b200/libpspgmres.so
-SRCS      := $(CSRC)/api.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/fused.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
+SRCS      := $(CSRC)/api.cu $(CSRC)/comm.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/fused.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS      := $(CSRC)/internal.h $(CSRC)/givens.cuh include/pspgmres.h
 ORACLE    := oracle/liboracle.so
@@ -16,7 +16,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnccl
 
 $(ORACLE): oracle/oracle.c oracle/oracle.h
 	gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -Wextra -Wno-unused-parameter -o $@ oracle/oracle.c -lm

@@ -131,7 +131,20 @@ enum { PSP_FLAG_CONVERGED = 1, PSP_FLAG_BREAKDOWN = 2, PSP_FLAG_NONFINITE = 4 };
  * psp_comm_unique_id).  Collective over nranks processes.  *out is owned by the library. */
 psp_status psp_comm_unique_id(void* h_id_128);
 psp_status psp_comm_init(const void* h_nccl_unique_id, int nranks, int rank, psp_comm** out);
+/* Test backend: nranks communicators of an in-process group (out: nranks handles) whose ranks
+ * live on ONE device, each driven by its own host thread; every collective synchronises the
+ * caller's stream, meets the other ranks at a host barrier and moves data with cudaMemcpy, so
+ * no kernel ever waits on another rank.  Same call sequence and results as NCCL ranks. */
+psp_status psp_comm_loopback_create(int nranks, psp_comm** out);
 psp_status psp_comm_destroy(psp_comm* comm);
+
+/* The slab decomposition of a multi-rank context: contiguous blocks of the slowest
+ * grid axis (z for 3-D, y for 2-D, the index for 1-D), balanced to within one plane, in global
+ * lexicographic order.  Rank `rank` of `nranks` owns rows [row0, row0 + nrows), i.e. planes
+ * [slab0, slab0 + slab_len) of that axis.  Pure host function.  PSP_E_DIM if a rank would get
+ * no plane. */
+psp_status psp_partition(const psp_grid* grid, int nranks, int rank, int64_t* row0, int64_t* nrows,
+                         int64_t* slab0, int64_t* slab_len);
 
 /* ---------------------------------------------------------------------------------------- */
 /* Context lifecycle.                                                                        */
@@ -149,6 +162,11 @@ psp_status psp_workspace_bytes(const psp_grid* grid, const psp_stencil* stencil,
  *   tol: see opts->tol_mode; opts: NULL = defaults; d_workspace/ws_bytes: caller-owned device
  *   memory of at least psp_workspace_bytes (256-byte aligned); stream: cudaStream_t;
  *   comm: NULL for one GPU.  N starts as I.
+ * Multi-rank (comm with nranks > 1): every rank calls psp_create with the same GLOBAL grid; the
+ * context owns the psp_partition slab of its rank, and d_field, every vector argument of the
+ * calls below and the workspace are this rank's LOCAL rows.  All calls are then collective
+ * (same calls, same order on every rank) and the reports are identical on every rank.  DIA
+ * operators and the fused pass are single-rank only.
  * Errors: PSP_E_ARG (bad d, restart, tol, kind), PSP_E_DIM (grid), PSP_E_NOMEM. */
 psp_status psp_create(const psp_grid* grid, const psp_stencil* stencil, double dt, int d,
                       int restart, double tol, const psp_opts* opts, void* d_workspace,

@@ -16,11 +16,6 @@
 
 using namespace psp;
 
-struct psp_comm {
-  int nranks = 1, rank = 0;
-  void* nccl = nullptr;  // ncclComm_t (comm.cu)
-};
-
 struct psp_ctx {
   // configuration
   psp_grid grid{};
@@ -30,7 +25,19 @@ struct psp_ctx {
   cudaStream_t stream = nullptr;
   psp_comm* comm = nullptr;
   int64_t n = 0, row0 = 0;
+  int64_t n_global = 0;
   Stencil st{};
+  // multi-rank (slab decomposition along the slowest axis)
+  bool multi = false;
+  int nranks = 1, rank = 0;
+  int64_t plane = 1;             // rows per slab unit (halo size of the stencil)
+  double* hx_lo = nullptr;       // halo planes of the matvec input (received per matvec)
+  double* hx_hi = nullptr;
+  double* hf_lo = nullptr;       // halo planes of the coefficient field (received at create)
+  double* hf_hi = nullptr;
+  double* mh_send = nullptr;     // MREP halo rows: [lo|hi] x m_max x d, packed for the send
+  double* mh_recv = nullptr;     //   and received ([lo|hi] x m_max x d)
+  double* bmisc = nullptr;       // banded multi-rank scratch (maps, states)
   // workspace carve
   double* ring_px = nullptr;
   double* ring_py = nullptr;
@@ -154,7 +161,7 @@ namespace {
 struct Plan {
   size_t off_px, off_py, off_V, off_X0, off_B, off_W, off_bands, off_lu, off_icpt, off_kind,
       off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
-      off_sscale,
+      off_sscale, off_halo, off_rpart, off_mhalo, off_bmisc,
       off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, total;
   int nblocks;
 };
@@ -170,7 +177,7 @@ int sm_count() {
   return sms;
 }
 
-Plan make_plan(int64_t n, int d, int nA, int m_max) {
+Plan make_plan(int64_t n, int d, int nA, int m_max, int64_t plane = 1, int nranks = 1) {
   Plan p{};
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -209,6 +216,10 @@ Plan make_plan(int64_t n, int d, int nA, int m_max) {
   p.off_mtick = take(64);
   p.off_mres = take(16 * 8);
   p.off_banded = take(banded_scratch_bytes(n, d));
+  p.off_halo = take((size_t)4 * plane * 8);
+  p.off_rpart = take((size_t)(2 * kMaxRestart + 16) * 8);
+  p.off_mhalo = take((size_t)4 * (m_max + 1) * d * 8);
+  p.off_bmisc = take(banded_misc_doubles(d, nranks) * 8);
   p.total = o + 256;  // alignment slack for the base pointer
   return p;
 }
@@ -279,13 +290,49 @@ const char* psp_status_str(psp_status s) {
 
 const char* psp_last_error(const psp_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
 
+// Slab decomposition: contiguous blocks of the slowest axis (z for 3-D, y for
+// 2-D, the index for 1-D), balanced to within one plane; the global lexicographic row order is
+// kept, so rank r owns rows [row0, row0 + nrows).
+psp_status psp_partition(const psp_grid* grid, int nranks, int rank, int64_t* row0, int64_t* nrows,
+                         int64_t* slab0, int64_t* slab_len) {
+  if (!grid || grid->ndim < 1 || grid->ndim > 3 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(nullptr, PSP_E_ARG, "psp_partition: bad argument");
+  const int ax = grid->ndim - 1;
+  const int64_t N = grid->n[ax];
+  if (N < nranks) return fail(nullptr, PSP_E_DIM, "psp_partition: fewer planes than ranks");
+  int64_t plane = 1;
+  for (int a = 0; a < ax; ++a) plane *= grid->n[a];
+  const int64_t base = N / nranks, rem = N % nranks;
+  const int64_t s0 = rank * base + (rank < rem ? rank : rem);
+  const int64_t len = base + (rank < rem ? 1 : 0);
+  if (row0) *row0 = s0 * plane;
+  if (nrows) *nrows = len * plane;
+  if (slab0) *slab0 = s0;
+  if (slab_len) *slab_len = len;
+  return PSP_OK;
+}
+
+static psp_status local_layout(const psp_grid* grid, const psp_stencil* st, int d, const psp_comm* comm,
+                               int64_t* n_loc, int64_t* row0, int64_t* slab0, int64_t* slab_len,
+                               int64_t* plane) {
+  const int nr = comm ? comm->nranks : 1, rk = comm ? comm->rank : 0;
+  PSP_TRY(psp_partition(grid, nr, rk, row0, n_loc, slab0, slab_len));
+  *plane = *n_loc / *slab_len;
+  if (nr > 1) {
+    if (st->kind == PSP_OP_DIA) return fail(nullptr, PSP_E_ARG, "multi-rank: DIA operators are single-rank only");
+    if (*n_loc < 2 * d + 1) return fail(nullptr, PSP_E_DIM, "multi-rank: each rank needs >= 2d+1 rows");
+  }
+  return PSP_OK;
+}
+
 psp_status psp_workspace_bytes(const psp_grid* grid, const psp_stencil* st, int d, int restart,
                                const psp_opts* opts, const psp_comm* comm, size_t* bytes) {
   psp_opts o;
   if (opts) o = *opts; else psp_default_opts(&o);
   PSP_TRY(validate(grid, st, d, restart, &o));
-  if (comm && comm->nranks > 1) return fail(nullptr, PSP_E_ARG, "multi-rank contexts: use one context per rank slab (see DESIGN.md)");
-  Plan p = make_plan(grid_rows(grid), d, restart, o.m_max);
+  int64_t n_loc, row0, s0, sl, plane;
+  PSP_TRY(local_layout(grid, st, d, comm, &n_loc, &row0, &s0, &sl, &plane));
+  Plan p = make_plan(n_loc, d, restart, o.m_max, plane, comm ? comm->nranks : 1);
   *bytes = p.total;
   return PSP_OK;
 }
@@ -299,9 +346,10 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   if (opts) o = *opts; else psp_default_opts(&o);
   PSP_TRY(validate(grid, st, d, restart, &o));
   if (!(tol > 0.0) || !(dt >= 0.0)) return fail(nullptr, PSP_E_ARG, "tol must be > 0 and dt >= 0");
-  if (comm && comm->nranks > 1) return fail(nullptr, PSP_E_ARG, "multi-rank contexts are not enabled in this build");
-  const int64_t n = grid_rows(grid);
-  Plan p = make_plan(n, d, restart, o.m_max);
+  int64_t n, row0, slab0, slab_len, plane;
+  PSP_TRY(local_layout(grid, st, d, comm, &n, &row0, &slab0, &slab_len, &plane));
+  const int nranks = comm ? comm->nranks : 1;
+  Plan p = make_plan(n, d, restart, o.m_max, plane, nranks);
   if (!d_ws || ws_bytes < p.total) return fail(nullptr, PSP_E_NOMEM, "workspace smaller than psp_workspace_bytes");
 
   psp_ctx* c = new psp_ctx();
@@ -314,14 +362,22 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->stream = (cudaStream_t)stream;
   c->comm = comm;
   c->n = n;
-  c->row0 = 0;
-  // operator coefficients (R24): h_a = 1/(n_a+1)
+  c->row0 = row0;
+  c->n_global = grid_rows(grid);
+  c->nranks = nranks;
+  c->rank = comm ? comm->rank : 0;
+  c->multi = nranks > 1;
+  c->plane = plane;
+  // operator coefficients (R24): h_a = 1/(n_a+1) of the GLOBAL grid; local extents per slab
   Stencil& S = c->st;
   S.kind = st->kind;
   S.ndim = grid->ndim;
   S.nx = grid->n[0];
   S.ny = grid->ndim >= 2 ? grid->n[1] : 1;
   S.nz = grid->ndim >= 3 ? grid->n[2] : 1;
+  if (grid->ndim == 3) S.nz = slab_len;
+  else if (grid->ndim == 2) S.ny = slab_len;
+  else S.nx = slab_len;
   S.n = n;
   for (int a = 0; a < 3; ++a) {
     const double na = a < grid->ndim ? (double)grid->n[a] : 1.0;
@@ -364,17 +420,27 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ds.resid = (double*)at(p.off_resid);
   c->ds.partials = (double*)at(p.off_partials);
   c->ds.tickets = (unsigned*)at(p.off_tickets);
+  c->ds.rpart = (double*)at(p.off_rpart);
+  c->ds.multi = c->multi ? 1 : 0;
   c->rc.nblocks = p.nblocks;
   c->rc.max_vals = 2 * kMaxRestart;
   c->ms.partials = (double*)at(p.off_mpart);
   c->ms.ticket = (unsigned*)at(p.off_mtick);
   c->ms.result = (double*)at(p.off_mres);
   c->bs = banded_scratch(at(p.off_banded), n, d);
+  c->hx_lo = (double*)at(p.off_halo);
+  c->hx_hi = c->hx_lo + plane;
+  c->hf_lo = c->hx_hi + plane;
+  c->hf_hi = c->hf_lo + plane;
+  c->mh_send = (double*)at(p.off_mhalo);
+  c->mh_recv = c->mh_send + 2 * (size_t)(o.m_max + 1) * d;
+  c->bmisc = (double*)at(p.off_bmisc);
   // zero the small control state (tickets, epochs, Hessenberg)
   cudaMemsetAsync(at(p.off_H), 0, p.off_partials - p.off_H, c->stream);
   cudaMemsetAsync(at(p.off_tickets), 0, TK_N * 4, c->stream);
   cudaMemsetAsync(at(p.off_mtick), 0, 64, c->stream);
   cudaMemsetAsync(at(p.off_banded), 0, banded_scratch_bytes(n, d), c->stream);
+  cudaMemsetAsync(at(p.off_halo), 0, (size_t)4 * plane * 8, c->stream);
   if (cudaMallocHost((void**)&c->hp, 64 * sizeof(double)) != cudaSuccess) {
     delete c;
     return fail(nullptr, PSP_E_CUDA, "cudaMallocHost failed");
@@ -382,6 +448,16 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   memset(c->hp, 0, 64 * sizeof(double));
   c->hp[32] = 1.0;  // the pinned constant 1.0 (scale of probes recorded normalised)
   for (int i = 0; i < 6; ++i) cudaEventCreate(&c->ev[i]);
+  // multi-rank: the coefficient field's halo planes, once (the field is fixed per context)
+  if (c->multi && S.field) {
+    if (comm->sendrecv(S.field, c->hf_lo, plane, S.field + (n - plane), c->hf_hi, plane, c->stream)) {
+      cudaFreeHost(c->hp);
+      delete c;
+      return fail(nullptr, PSP_E_NCCL, "psp_create: field halo exchange failed");
+    }
+    S.f_lo = c->rank > 0 ? c->hf_lo : nullptr;
+    S.f_hi = c->rank < nranks - 1 ? c->hf_hi : nullptr;
+  }
   psp_status s = check_cuda(c, "psp_create");
   if (s != PSP_OK) {
     cudaFreeHost(c->hp);
@@ -471,8 +547,35 @@ Basis basis(const psp_ctx* c) {
   return Basis{c->V, c->ldv, 0, c->nA + 1};
 }
 bool fused_eligible(const psp_ctx* c) {
-  return c->opts.fused && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE &&
+  // (multi-rank: the fused pass would need the halo planes of u in the middle of the pass)
+  return c->opts.fused && !c->multi && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE &&
          c->ring_cap >= c->nA + 1 && fused_supported(c->st, c->nA);
+}
+
+// y = A (xs x) [+ probe copy]; multi-rank: first the slab halo planes of x from rank-1 / rank+1
+psp_status matvec(psp_ctx* c, const double* x, const double* xs, double* y, double* xcopy) {
+  Stencil st = c->st;
+  if (c->multi) {
+    const int64_t pl = c->plane;
+    if (c->comm->sendrecv(x, c->hx_lo, (size_t)pl, x + (c->n - pl), c->hx_hi, (size_t)pl, c->stream))
+      return fail(c, PSP_E_NCCL, "matvec halo exchange failed");
+    st.x_lo = c->rank > 0 ? c->hx_lo : nullptr;
+    st.x_hi = c->rank < c->nranks - 1 ? c->hx_hi : nullptr;
+  }
+  launch_matvec(st, x, xs, y, xcopy, c->stream);
+  c->launches += 1;
+  return PSP_OK;
+}
+
+// multi-rank: all-reduce this rank's reduction totals, then run the scalar epilogue on every
+// rank (identical inputs -> identical decisions on every rank)
+psp_status finish_reduce(psp_ctx* c, int kind, int nv, int k, int j, int slot) {
+  if (!c->multi) return PSP_OK;
+  if (c->comm->allreduce(c->ds.rpart, (size_t)nv, 0, c->stream))
+    return fail(c, PSP_E_NCCL, "all-reduce failed");
+  launch_epilogue(kind, c->ds, k, c->nA, j, slot, c->stream);
+  c->launches += 1;
+  return PSP_OK;
 }
 
 psp_status sync_read(psp_ctx* c, const double* dsrc, int count, double* hdst) {
@@ -494,6 +597,7 @@ psp_status set_eps(psp_ctx* c, const double* d_b, double* eps_out) {
   } else {
     launch_norm(d_b, c->n, c->ds, SC_NORM, c->rc, c->stream);
     c->launches += 1;
+    PSP_TRY(finish_reduce(c, EPI_NORM, 1, 0, 0, SC_NORM));
     double nb;
     PSP_TRY(sync_read(c, c->ds.scal + SC_NORM, 1, &nb));
     eps = c->tol * nb;  // R1
@@ -505,15 +609,22 @@ psp_status set_eps(psp_ctx* c, const double* d_b, double* eps_out) {
   return check_cuda(c, "set_eps");
 }
 
+// z = x0 + N^{-1} (vs v) with the accepted N (banded LU of K4), multi-rank aware
+psp_status precond_scaled(psp_ctx* c, const double* v, const double* vs, double* z, const double* x0 = nullptr) {
+  if (banded_solve(c->lu, c->n, c->d, v, vs, x0, z, c->bs, c->stream, &c->launches, c->multi ? c->comm : nullptr,
+                   c->bmisc))
+    return fail(c, PSP_E_NCCL, "banded solve: collective failed");
+  return PSP_OK;
+}
+
 psp_status precond(psp_ctx* c, const double* v, const double* x0, double* z) {
   if (c->n_identity) {
     if (x0) return fail(c, PSP_E_ARG, "internal: identity precond with addend");
     launch_copy(v, z, c->n, c->stream);
     c->launches += 1;
-  } else {
-    banded_solve(c->lu, c->n, c->d, v, nullptr, x0, z, c->bs, c->stream, &c->launches);
+    return PSP_OK;
   }
-  return PSP_OK;
+  return precond_scaled(c, v, nullptr, z, x0);
 }
 
 }  // namespace
@@ -526,12 +637,11 @@ psp_status psp_matvec(psp_ctx* c, const double* x, double* y, int record) {
   if (record) {
     const int slot = ring_next(c);
     set_unit_scale(c, slot);
-    launch_matvec(c->st, x, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
+    PSP_TRY(matvec(c, x, nullptr, py_col(c, slot), px_col(c, slot)));
     launch_copy(py_col(c, slot), y, c->n, c->stream);
-    c->launches += 2;
-  } else {
-    launch_matvec(c->st, x, nullptr, y, nullptr, c->stream);
     c->launches += 1;
+  } else {
+    PSP_TRY(matvec(c, x, nullptr, y, nullptr));
   }
   return check_cuda(c, "psp_matvec");
 }
@@ -562,7 +672,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   const int slot = ring_next(c);
   set_unit_scale(c, slot);
   int h = kt_begin(c);
-  launch_matvec(c->st, c->X0, nullptr, py_col(c, slot), px_col(c, slot), c->stream);
+  PSP_TRY(matvec(c, c->X0, nullptr, py_col(c, slot), px_col(c, slot)));
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
   // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta.  V(:,1) <- R_bar/beta
   // (l.6) is stored unnormalised with alpha_1 = 1/beta.  On the fused path V(:,1) goes straight
@@ -575,7 +685,8 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   h = kt_begin(c);
   launch_residual(b, py_col(c, slot), v1, c->n, c->nA, c->ds, c->rc, c->stream);
   kt_end(c, h, PSP_KC_RESIDUAL, 24.0 * c->n);
-  c->launches += 2;
+  c->launches += 1;
+  PSP_TRY(finish_reduce(c, EPI_RESIDUAL, 1, 0, 0, 0));
   double beta;
   PSP_TRY(sync_read(c, c->ds.scal + SC_BETA, 1, &beta));
   if (h_beta) *h_beta = beta;
@@ -628,34 +739,38 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
     // l.10-12: Y_k = N^{-1} V(:,k) -> P_x(:,i); P_y(:,i) = A Y_k
     if (c->n_identity) {
       h = kt_begin(c);
-      launch_matvec(c->st, Vk, c->ds.alpha + (k - 1), py, px, c->stream);  // N = I: probe copy fused
+      PSP_TRY(matvec(c, Vk, c->ds.alpha + (k - 1), py, px));  // N = I: probe copy fused
       kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
-      c->launches += 1;
     } else {
       h = kt_begin(c);
-      banded_solve(c->lu, n, c->d, Vk, c->ds.alpha + (k - 1), nullptr, px, c->bs, c->stream, &c->launches);
+      PSP_TRY(precond_scaled(c, Vk, c->ds.alpha + (k - 1), px));
       kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
       h = kt_begin(c);
-      launch_matvec(c->st, px, nullptr, py, nullptr, c->stream);
+      PSP_TRY(matvec(c, px, nullptr, py, nullptr));
       kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
-      c->launches += 1;
     }
     double* U = Vcol(c, k + 1);
     // l.13-17: MGS (R11) + H(k+1,k) + Givens (l.19-32) in the last block
     if (c->opts.ortho == PSP_MGS_LITERAL) {
       h = kt_begin(c);
       launch_mgs_literal(py, U, nullptr, Vcol(c, 1), 1, k, c->nA, n, c->ds, c->rc, c->stream);
-      for (int j = 2; j <= k; ++j)
+      PSP_TRY(finish_reduce(c, EPI_MGS, 1, k, 1, 0));
+      for (int j = 2; j <= k; ++j) {
         launch_mgs_literal(U, U, Vcol(c, j - 1), Vcol(c, j), j, k, c->nA, n, c->ds, c->rc, c->stream);
+        PSP_TRY(finish_reduce(c, EPI_MGS, 1, k, j, 0));
+      }
       launch_mgs_literal_final(U, Vcol(c, k), k, c->nA, n, c->ds, c->rc, c->stream);
+      PSP_TRY(finish_reduce(c, EPI_MGS_FINAL, 1, k, 0, 0));
       kt_end(c, h, PSP_KC_MGS_LITERAL, (24.0 + 32.0 * (k - 1) + 24.0) * dn);
       c->launches += k + 1;
     } else {
       h = kt_begin(c);
       launch_icwy_dots(basis(c), py, k, c->nA, n, c->ds, c->rc, c->stream);
+      PSP_TRY(finish_reduce(c, EPI_DOTS, 2 * k - 1, k, 0, 0));
       kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 1) * dn);
       h = kt_begin(c);
       launch_icwy_update(basis(c), py, nullptr, U, k, c->nA, n, c->ds, c->rc, c->stream);
+      PSP_TRY(finish_reduce(c, EPI_UPDATE, 1, k, 0, 0));
       kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
       c->launches += 2;
     }
@@ -765,9 +880,10 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
       c->launches += 1;
     }
     // R13: true residual with one unrecorded matvec
-    launch_matvec(c->st, x, nullptr, c->W, nullptr, c->stream);
+    PSP_TRY(matvec(c, x, nullptr, c->W, nullptr));
     launch_diff_norm(b, c->W, c->n, c->ds, SC_TMP, c->rc, c->stream);
-    c->launches += 2;
+    c->launches += 1;
+    PSP_TRY(finish_reduce(c, EPI_NORM, 1, 0, 0, SC_TMP));
     double tr;
     PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &tr));
     R->final_resid_true = tr;
@@ -828,7 +944,7 @@ psp_status psp_mrep_fit_raw(const double* px, const double* py, int64_t n, int m
   std::vector<int32_t> slots(m);
   for (int c2 = 0; c2 < m; ++c2) slots[c2] = h_order ? h_order[c2] : c2;
   MrepOut out{bands, icpt, kind, kappa};
-  mrep_launch(px, py, nullptr, ld, slots.data(), m, n, d, out, ms, s);
+  mrep_launch(px, py, nullptr, ld, slots.data(), m, n, d, out, ms, s, MrepMulti{nullptr, nullptr, nullptr, 0, n});
   double r[16];
   if (cudaMemcpyAsync(r, ms.result, sizeof(r), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
@@ -856,7 +972,7 @@ psp_status psp_banded_factor_raw(const double* bands, int64_t n, int d, double* 
   raw_carve(scratch, n, d, &ms, &bs);
   cudaStream_t s = (cudaStream_t)stream;
   int passes = 0;
-  int st = banded_factor(bands, n, d, lu, bs, s, &passes, nullptr);
+  int st = banded_factor(bands, n, d, lu, bs, s, &passes, nullptr, nullptr, nullptr);
   PSP_TRY(check_cuda(nullptr, "psp_banded_factor_raw"));
   if (st != PSP_OK) return fail(nullptr, PSP_E_SINGULAR, "banded LU: zero pivot or growth (S:272, S:293)");
   return PSP_OK;
@@ -872,7 +988,7 @@ psp_status psp_banded_solve_raw(const double* lu, int64_t n, int d, const double
   MrepScratch ms;
   BandedScratch bs;
   raw_carve(scratch, n, d, &ms, &bs);
-  banded_solve(lu, n, d, v, nullptr, x0, z, bs, (cudaStream_t)stream, nullptr);
+  banded_solve(lu, n, d, v, nullptr, x0, z, bs, (cudaStream_t)stream, nullptr, nullptr, nullptr);
   return check_cuda(nullptr, "psp_banded_solve_raw");
 }
 
@@ -882,7 +998,9 @@ static psp_status install_bands(psp_ctx* c, bool gate_ok, psp_report* R) {
     if (c->opts.timing) cudaEventRecord(c->ev[4], c->stream);
     int passes = 0;
     int h = kt_begin(c);
-    int st = banded_factor(c->bands, c->n, c->d, c->lu, c->bs, c->stream, &passes, &c->launches);
+    int st = banded_factor(c->bands, c->n, c->d, c->lu, c->bs, c->stream, &passes, &c->launches,
+                           c->multi ? c->comm : nullptr, c->bmisc);
+    if (st == PSP_E_NCCL) return fail(c, PSP_E_NCCL, "banded factor: collective failed");
     kt_end(c, h, PSP_KC_FACTOR, 16.0 * (2 * c->d + 1) * (double)c->n);
     PSP_TRY(check_cuda(c, "banded_factor"));
     if (st != PSP_OK) accept = false;  // fall back to identity
@@ -917,7 +1035,10 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
   MrepOut out{c->bands, c->intercept, c->rowkind, c->kappa};
   cudaMemsetAsync(c->ms.ticket, 0, 64, c->stream);
   int h = kt_begin(c);
-  mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms, c->stream);
+  MrepMulti mm{c->multi ? c->comm : nullptr, c->mh_send, c->mh_recv, c->row0, c->n_global};
+  if (mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms,
+                  c->stream, mm))
+    return fail(c, PSP_E_NCCL, "MREP: collective failed");
   kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
   c->launches += 3;
   double r[16];
@@ -974,11 +1095,20 @@ psp_status psp_set_bands(psp_ctx* c, const double* d_bands, int* h_accepted) {
     for (int64_t i = 0; i < c->n && ok; ++i) {
       double off = 0.0;
       for (int o = 0; o <= 2 * c->d; ++o) {
-        int64_t j = i + o - c->d;
-        if (o == c->d || j < 0 || j >= c->n) continue;
+        int64_t j = c->row0 + i + o - c->d;  // global column
+        if (o == c->d || j < 0 || j >= c->n_global) continue;
         off += fabs(hb[(size_t)o * c->n + i]);
       }
       if (!(fabs(hb[(size_t)c->d * c->n + i]) > off)) ok = false;
+    }
+    if (c->multi) {  // one decision for the whole matrix
+      c->hp[9] = ok ? 1.0 : 0.0;
+      cudaMemcpyAsync(c->ds.scal + SC_TMP, c->hp + 9, 8, cudaMemcpyHostToDevice, c->stream);
+      if (c->comm->allreduce(c->ds.scal + SC_TMP, 1, 2, c->stream))
+        return fail(c, PSP_E_NCCL, "psp_set_bands: gate all-reduce failed");
+      double g;
+      PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &g));
+      ok = g > 0.5;
     }
   }
   PSP_TRY(install_bands(c, ok, nullptr));
@@ -1039,26 +1169,6 @@ psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj, double* h
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;
     *h_scale = c->hp[16];
   }
-  return PSP_OK;
-}
-
-// ---- communicator (NCCL over NVLink) ----
-psp_status psp_comm_unique_id(void* id) {
-  if (!id) return PSP_E_ARG;
-  memset(id, 0, 128);
-  return fail(nullptr, PSP_E_ARG, "multi-rank path not enabled in this build");
-}
-psp_status psp_comm_init(const void*, int nranks, int rank, psp_comm** out) {
-  if (!out) return PSP_E_ARG;
-  if (nranks != 1) return fail(nullptr, PSP_E_ARG, "multi-rank path not enabled in this build");
-  psp_comm* c = new psp_comm();
-  c->nranks = 1;
-  c->rank = rank;
-  *out = c;
-  return PSP_OK;
-}
-psp_status psp_comm_destroy(psp_comm* c) {
-  delete c;
   return PSP_OK;
 }
 

@@ -39,7 +39,10 @@ constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank con
 template <int D>
 __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, double* __restrict__ lu,
                                    const double* __restrict__ st_in, double* __restrict__ st_out,
-                                   int first_pass, int* __restrict__ changed, int* __restrict__ bad) {
+                                   int first_pass, int* __restrict__ changed, int* __restrict__ bad,
+                                   const double* __restrict__ prev, int has_prev, int has_next) {
+  // has_prev / has_next (multi-rank): the global matrix continues before row 0 / after row n-1
+  // of this block (rows of rank-1 / rank+1), so the band entries reaching there are real
   constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -47,7 +50,14 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   const int64_t r0 = c * kChunk;
   const int64_t r1 = (r0 + kChunk < n) ? r0 + kChunk : n;
   double Uw[D][D + 1];
-  if (c == 0 || first_pass) {
+  // chunk 0 of rank r > 0 (after the first pass): the last-D-U-rows state of rank r-1
+  const bool from_prev = (c == 0) && (prev != nullptr) && !first_pass;
+  if (from_prev) {
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int e = 0; e <= D; ++e) Uw[q][e] = prev[q * (D + 1) + e];
+  } else if (c == 0 || first_pass) {
     // matrix start (exact for chunk 0; the initial guess for the others)
 #pragma unroll
     for (int q = 0; q < D; ++q)
@@ -60,7 +70,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
       for (int e = 0; e <= D; ++e) Uw[q][e] = s[q * (D + 1) + e];
   }
-  const bool at_start = (c == 0) || first_pass;
+  const bool at_start = !from_prev && ((c == 0) || first_pass);
   int isbad = 0;
   for (int64_t i = r0; i < r1; ++i) {
     double Lr[D];       // L(i, i-D+q), q = 0..D-1
@@ -74,7 +84,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
     };
     auto row_exists = [&](int q) -> bool {
       const int64_t k = i - D + q;
-      return k >= 0 && !(at_start && k < r0);
+      return (k >= 0 || has_prev) && !(at_start && k < r0);
     };
 #pragma unroll
     for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
@@ -89,7 +99,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
     for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
       const int64_t j = i + e;
-      if (j >= n) { Ur[e] = 0.0; continue; }
+      if (j >= n && !has_next) { Ur[e] = 0.0; continue; }
       double s = bands[(int64_t)(D + e) * n + i];
 #pragma unroll
       for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]
@@ -225,8 +235,12 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
                                                      double* out,
                                                      double* __restrict__ desc,
                                                      unsigned long long* __restrict__ flags,
-                                                     unsigned long long* __restrict__ ctl) {
-  // ctl[0] = ticket counter, ctl[1] = epoch
+                                                     unsigned long long* __restrict__ ctl,
+                                                     const double* s_in0, double* s_out) {
+  // ctl[0] = ticket counter, ctl[1] = epoch.  vin == NULL: zero right-hand side (homogeneous).
+  // s_in0 (d doubles, may be NULL = 0): the state entering this rank's first row in processing
+  // order (multi-rank); s_out (may be NULL): receives the state after its last row.
+  // out == NULL: nothing is written (the zero-state pass of a multi-rank sweep).
   // dynamic shared memory: sv (rhs, then the result) | sc[D] (recurrence coefficients) |
   // su0 (U(i,i), backward only)
   extern __shared__ double smem_dyn[];
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
     const int64_t i = base + q;
     const int sidx = (q / SR) * SPAD + (q % SR);
     const bool in = i < n;
-    sv[sidx] = in ? vsc * vin[i] : 0.0;
+    sv[sidx] = (in && vin) ? vsc * vin[i] : 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
@@ -280,6 +294,7 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
 #pragma unroll
     for (int rr = 0; rr < SR; ++rr) {
       const int r = FWD ? rr : (SR - 1 - rr);
+      if (base + (int64_t)t * SR + r >= n) continue;   // padding rows are transparent
       const int sidx = t * SPAD + r;
       double c[D];
 #pragma unroll
@@ -351,8 +366,9 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
     // tiles are processed in order (first = FWD tile 0, BWD tile ntiles-1)
     const bool first_tile = FWD ? (tile == 0) : (tile == ntiles - 1);
     if (first_tile) {
+      // nothing before the matrix start / end, or (multi-rank) the state from the neighbour rank
 #pragma unroll
-      for (int i = 0; i < D; ++i) sin[i] = 0.0;   // nothing before the matrix start / end
+      for (int i = 0; i < D; ++i) sin[i] = s_in0 ? s_in0[i] : 0.0;
     } else {
       // publish the aggregate
 #pragma unroll
@@ -395,6 +411,10 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
     for (int i = 0; i < D; ++i) my_desc[D * D + D + i] = sout[i];
     __threadfence();
     fl[tile] = (epoch << 2) | FLAG_INCL;
+    const bool last_tile = FWD ? (tile == ntiles - 1) : (tile == 0);
+    if (last_tile && s_out)
+#pragma unroll
+      for (int i = 0; i < D; ++i) s_out[i] = sout[i];
 #pragma unroll
     for (int i = 0; i < D; ++i) s_in[i] = sin[i];
   }
@@ -409,6 +429,7 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
 #pragma unroll
     for (int rr = 0; rr < SR; ++rr) {
       const int r = FWD ? rr : (SR - 1 - rr);
+      if (base + (int64_t)t * SR + r >= n) continue;   // padding rows are transparent
       const int sidx = t * SPAD + r;
       double c[D];
 #pragma unroll
@@ -420,13 +441,14 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
     }
   }
   __syncthreads();
-  for (int q = t; q < STILE; q += STPB) {
-    const int64_t i = base + q;
-    if (i < n) {
-      const double y = sv[(q / SR) * SPAD + (q % SR)];
-      out[i] = addend ? addend[i] + y : y;
+  if (out != nullptr)
+    for (int q = t; q < STILE; q += STPB) {
+      const int64_t i = base + q;
+      if (i < n) {
+        const double y = sv[(q / SR) * SPAD + (q % SR)];
+        out[i] = addend ? addend[i] + y : y;
+      }
     }
-  }
   // the last block re-arms the ticket counter and advances the epoch
   if (t == 0) {
     __threadfence();
@@ -442,16 +464,18 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
 
 template <int D>
 void factor_launch(const double* bands, int64_t n, double* lu, const double* a, double* b,
-                   int first, int* changed, int* bad, cudaStream_t s) {
+                   int first, int* changed, int* bad, const double* prev, int has_prev, int has_next,
+                   cudaStream_t s) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int tpb = 64;
   factor_pass_kernel<D><<<(unsigned)((nchunks + tpb - 1) / tpb), tpb, 0, s>>>(bands, n, lu, a, b, first,
-                                                                              changed, bad);
+                                                                              changed, bad, prev, has_prev,
+                                                                              has_next);
 }
 
 template <bool FWD, int D>
 void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
-                  double* out, BandedScratch sc, cudaStream_t s) {
+                  double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out) {
   const int64_t ntiles = (n + STILE - 1) / STILE;
   const size_t smem = (size_t)(1 + D + (FWD ? 0 : 1)) * STPB * SPAD * sizeof(double);
   static bool attr_set = false;
@@ -460,7 +484,60 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
     attr_set = true;
   }
   sweep_kernel<FWD, D><<<(unsigned)ntiles, STPB, smem, s>>>(lu, n, v, vs, add, out, sc.states,
-                                                        sc.tickets + 8, sc.tickets);
+                                                        sc.tickets + 8, sc.tickets, s_in0, s_out);
+}
+
+void sweep(bool fwd, int d, const double* lu, int64_t n, const double* v, const double* vs,
+           const double* add, double* out, BandedScratch sc, cudaStream_t s, const double* s_in0,
+           double* s_out) {
+#define PSP_SWEEP(DD)                                                            \
+  if (fwd) sweep_launch<true, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out); \
+  else sweep_launch<false, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out);
+  switch (d) {
+    case 1: PSP_SWEEP(1) break;
+    case 2: PSP_SWEEP(2) break;
+    case 3: PSP_SWEEP(3) break;
+    default: PSP_SWEEP(4) break;
+  }
+#undef PSP_SWEEP
+}
+
+// multi-rank helpers (one thread)
+__global__ void flags_to_double_kernel(const int* f, double* out) {
+  out[0] = (double)f[0];
+  out[1] = (double)f[1];
+}
+__global__ void unit_vector_kernel(double* e, int d, int i) {
+  for (int q = 0; q < d; ++q) e[q] = (q == i) ? 1.0 : 0.0;
+}
+__global__ void copy_col_kernel(const double* src, double* M, int d, int i) {
+  for (int q = 0; q < d; ++q) M[q * d + i] = src[q];   // column i of the row-major d x d map
+}
+// incoming state of this rank: compose the affine maps s <- M_q s + t_q of the ranks before it
+// (forward: q = 0..rank-1; backward: q = nranks-1..rank+1); identical arithmetic on every rank
+__global__ void compose_states_kernel(const double* Mall, const double* tall, int d, int nranks,
+                                      int rank, int fwd, double* sin) {
+  double s[kMaxD] = {0.0, 0.0, 0.0, 0.0}, t2[kMaxD];
+  if (fwd) {
+    for (int q = 0; q < rank; ++q) {
+      for (int i = 0; i < d; ++i) {
+        double v = tall[q * d + i];
+        for (int j = 0; j < d; ++j) v = fma(Mall[(q * d + i) * d + j], s[j], v);
+        t2[i] = v;
+      }
+      for (int i = 0; i < d; ++i) s[i] = t2[i];
+    }
+  } else {
+    for (int q = nranks - 1; q > rank; --q) {
+      for (int i = 0; i < d; ++i) {
+        double v = tall[q * d + i];
+        for (int j = 0; j < d; ++j) v = fma(Mall[(q * d + i) * d + j], s[j], v);
+        t2[i] = v;
+      }
+      for (int i = 0; i < d; ++i) s[i] = t2[i];
+    }
+  }
+  for (int i = 0; i < d; ++i) sin[i] = s[i];
 }
 
 }  // namespace
@@ -484,7 +561,6 @@ static inline char* align256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(
 BandedScratch banded_scratch(void* base, int64_t n, int d) {
   BandedScratch sc;
   const int64_t ntiles = (n + STILE - 1) / STILE;
-  const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t DW = d * d + 2 * d;
   char* p = align256((char*)base);
   sc.tickets = (unsigned long long*)p;          // [0..3] ctl, [4..] flags
@@ -494,7 +570,6 @@ BandedScratch banded_scratch(void* base, int64_t n, int d) {
   p = align256(p + (size_t)ntiles * DW * 8);
   sc.y = (double*)p;                            // intermediate vector, then factor states
   sc.desc_count = ntiles;
-  (void)nchunks;
   return sc;
 }
 
@@ -503,56 +578,117 @@ static double* factor_states(BandedScratch sc, int64_t n) {
   return sc.y + ((n + 31) / 32) * 32;
 }
 
+// misc (multi-rank) layout, doubles: [prev W | dummy W | flags 2 | e d | col d | Mf p*d*d |
+// Mb p*d*d | t d | tall p*d | sin d]
+namespace {
+struct Misc {
+  double *prev, *dummy, *flags, *e, *col, *mine, *Mf, *Mb, *t, *tall, *sin;
+  Misc(double* m, int d, int p) {
+    const int W = d * (d + 1);
+    prev = m;
+    dummy = prev + W;
+    flags = dummy + W;
+    e = flags + 2;
+    col = e + d;
+    mine = col + d;
+    Mf = mine + d * d;
+    Mb = Mf + (size_t)p * d * d;
+    t = Mb + (size_t)p * d * d;
+    tall = t + d;
+    sin = tall + (size_t)p * d;
+  }
+};
+}  // namespace
+
+size_t banded_misc_doubles(int d, int nranks) {
+  return (size_t)2 * d * (d + 1) + 2 + 2 * d + d * d + (size_t)2 * nranks * d * d + d +
+         (size_t)nranks * d + d;
+}
+
 int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScratch sc,
-                  cudaStream_t s, int* passes, int64_t* launches) {
+                  cudaStream_t s, int* passes, int64_t* launches, psp_comm* comm, double* misc) {
+  const bool multi = comm && comm->nranks > 1;
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int W = d * (d + 1);
   double* A = factor_states(sc, n);
-  double* B = A + nchunks * d * (d + 1);
+  double* B = A + nchunks * W;
+  Misc M(misc, d, multi ? comm->nranks : 1);
   int h[2] = {0, 0};
+  double hd[2] = {0.0, 0.0};
   int p = 0;
   for (;;) {
     cudaMemsetAsync(sc.changed, 0, 2 * sizeof(int), s);
+    const double* prev = (multi && comm->rank > 0 && p > 0) ? M.prev : nullptr;
+    const int hp = (multi && comm->rank > 0) ? 1 : 0;
+    const int hn = (multi && comm->rank < comm->nranks - 1) ? 1 : 0;
     switch (d) {
-      case 1: factor_launch<1>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
-      case 2: factor_launch<2>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
-      case 3: factor_launch<3>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
-      default: factor_launch<4>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, s); break;
+      case 1: factor_launch<1>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
+      case 2: factor_launch<2>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
+      case 3: factor_launch<3>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
+      default: factor_launch<4>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
     }
     if (launches) *launches += 1;
     ++p;
-    cudaMemcpyAsync(h, sc.changed, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    if (multi) {
+      // the outgoing state of this rank's last chunk goes to rank+1 (its chunk 0 next pass)
+      if (comm->sendrecv(M.dummy, M.prev, (size_t)W, B + (nchunks - 1) * W, M.dummy, (size_t)W, s)) return PSP_E_NCCL;
+      flags_to_double_kernel<<<1, 1, 0, s>>>(sc.changed, M.flags);
+      if (comm->allreduce(M.flags, 2, 0, s)) return PSP_E_NCCL;
+      cudaMemcpyAsync(hd, M.flags, 2 * sizeof(double), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      h[0] = (int)hd[0];
+      h[1] = (int)hd[1];
+    } else {
+      cudaMemcpyAsync(h, sc.changed, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+    }
     double* tmp = A;
     A = B;
     B = tmp;
-    if (h[0] == 0 || p > nchunks + 1) break;
+    if (h[0] == 0 || p > nchunks * (multi ? comm->nranks : 1) + 1) break;
   }
   if (passes) *passes = p;
-  return h[1] ? PSP_E_SINGULAR : PSP_OK;
+  if (h[1]) return PSP_E_SINGULAR;
+  if (multi) {
+    // this rank's homogeneous transfer maps (forward and backward), d unit-state sweeps each,
+    // all-gathered so that every rank can compose the states entering it (banded_solve)
+    for (int fwd = 1; fwd >= 0; --fwd) {
+      for (int i = 0; i < d; ++i) {
+        unit_vector_kernel<<<1, 1, 0, s>>>(M.e, d, i);
+        sweep(fwd != 0, d, lu, n, nullptr, nullptr, nullptr, nullptr, sc, s, M.e, M.col);
+        copy_col_kernel<<<1, 1, 0, s>>>(M.col, M.mine, d, i);
+      }
+      if (comm->allgather(M.mine, fwd ? M.Mf : M.Mb, (size_t)d * d, s)) return PSP_E_NCCL;
+      if (launches) *launches += 3 * d;
+    }
+  }
+  return PSP_OK;
 }
 
-void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
-                  const double* x0, double* z,
-                  BandedScratch sc, cudaStream_t s, int64_t* launches) {
-  switch (d) {
-    case 1:
-      sweep_launch<true, 1>(lu, n, v, vs, nullptr, sc.y, sc, s);
-      sweep_launch<false, 1>(lu, n, sc.y, nullptr, x0, z, sc, s);
-      break;
-    case 2:
-      sweep_launch<true, 2>(lu, n, v, vs, nullptr, sc.y, sc, s);
-      sweep_launch<false, 2>(lu, n, sc.y, nullptr, x0, z, sc, s);
-      break;
-    case 3:
-      sweep_launch<true, 3>(lu, n, v, vs, nullptr, sc.y, sc, s);
-      sweep_launch<false, 3>(lu, n, sc.y, nullptr, x0, z, sc, s);
-      break;
-    default:
-      sweep_launch<true, 4>(lu, n, v, vs, nullptr, sc.y, sc, s);
-      sweep_launch<false, 4>(lu, n, sc.y, nullptr, x0, z, sc, s);
-      break;
+// z = x0 + N^{-1}(vs v).  Multi-rank: each sweep runs twice -- a zero-state pass that only
+// yields this rank's outgoing state t_r, an all-gather of the t's, the state entering this rank
+// composed from the ranks before it (maps from banded_factor), then the exact pass.
+int banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
+                 const double* x0, double* z, BandedScratch sc, cudaStream_t s, int64_t* launches,
+                 psp_comm* comm, double* misc) {
+  if (!(comm && comm->nranks > 1)) {
+    sweep(true, d, lu, n, v, vs, nullptr, sc.y, sc, s, nullptr, nullptr);
+    sweep(false, d, lu, n, sc.y, nullptr, x0, z, sc, s, nullptr, nullptr);
+    if (launches) *launches += 2;
+    return PSP_OK;
   }
-  if (launches) *launches += 2;
+  Misc M(misc, d, comm->nranks);
+  for (int fwd = 1; fwd >= 0; --fwd) {
+    const double* vin = fwd ? v : sc.y;
+    const double* vsc = fwd ? vs : nullptr;
+    sweep(fwd != 0, d, lu, n, vin, vsc, nullptr, nullptr, sc, s, nullptr, M.t);
+    if (comm->allgather(M.t, M.tall, (size_t)d, s)) return PSP_E_NCCL;
+    compose_states_kernel<<<1, 1, 0, s>>>(fwd ? M.Mf : M.Mb, M.tall, d, comm->nranks, comm->rank, fwd,
+                                          M.sin);
+    sweep(fwd != 0, d, lu, n, vin, vsc, fwd ? nullptr : x0, fwd ? sc.y : z, sc, s, M.sin, nullptr);
+  }
+  if (launches) *launches += 6;
+  return PSP_OK;
 }
 
 }  // namespace psp

@@ -1,0 +1,168 @@
+// comm.cu -- the communicator behind psp_comm: NCCL over NVLink/NVSwitch for real ranks (one
+// process per GPU), and an in-process loopback group for testing the multi-rank code path with
+// several contexts on ONE device (host-mediated: every collective synchronises the caller's
+// stream, meets the other ranks at a host barrier and copies device buffers with cudaMemcpy;
+// no kernel ever waits on another rank's kernel).
+//
+// Collectives used by the hot path:
+//   allreduce      -- Arnoldi dots / norms (sum), MREP gate statistics (max/min/sum)
+//   sendrecv       -- slab halos: one plane for the stencil, d rows x m probes for MREP,
+//                     the fixed-point state of the banded factorisation
+//   allgather      -- per-rank affine maps / states of the partitioned banded sweeps
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+ncclRedOp_t nccl_op(int op) { return op == 1 ? ncclMax : (op == 2 ? ncclMin : ncclSum); }
+
+struct NcclComm : psp_comm {
+  ncclComm_t c = nullptr;
+  ~NcclComm() override {
+    if (c) ncclCommDestroy(c);
+  }
+  int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
+    return ncclAllReduce(d, d, count, ncclDouble, nccl_op(op), c, s) == ncclSuccess ? 0 : 1;
+  }
+  int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
+               double* recv_hi, size_t n_hi, cudaStream_t s) override {
+    if (ncclGroupStart() != ncclSuccess) return 1;
+    if (rank > 0 && n_lo) {
+      ncclSend(send_lo, n_lo, ncclDouble, rank - 1, c, s);
+      ncclRecv(recv_lo, n_lo, ncclDouble, rank - 1, c, s);
+    }
+    if (rank < nranks - 1 && n_hi) {
+      ncclSend(send_hi, n_hi, ncclDouble, rank + 1, c, s);
+      ncclRecv(recv_hi, n_hi, ncclDouble, rank + 1, c, s);
+    }
+    return ncclGroupEnd() == ncclSuccess ? 0 : 1;
+  }
+  int allgather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+    return ncclAllGather(send, recv, count, ncclDouble, c, s) == ncclSuccess ? 0 : 1;
+  }
+};
+
+// ---- loopback group: nranks contexts on one device, one host thread per rank ----
+struct LoopGroup {
+  int n;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<const double*> p_lo, p_hi, p_all;  // published device pointers
+  std::vector<std::vector<double>> host;          // host slots for reductions
+  explicit LoopGroup(int nr) : n(nr), p_lo(nr), p_hi(nr), p_all(nr), host(nr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LoopComm : psp_comm {
+  std::shared_ptr<LoopGroup> g;
+  int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) return 1;
+    g->host[rank].resize(count);
+    if (cudaMemcpy(g->host[rank].data(), d, count * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    g->barrier();
+    std::vector<double> r(g->host[0]);
+    for (int q = 1; q < nranks; ++q)  // rank order: identical on every rank
+      for (size_t i = 0; i < count; ++i) {
+        const double v = g->host[q][i];
+        r[i] = op == 0 ? r[i] + v : (op == 1 ? (v > r[i] ? v : r[i]) : (v < r[i] ? v : r[i]));
+      }
+    g->barrier();
+    return cudaMemcpy(d, r.data(), count * 8, cudaMemcpyHostToDevice) == cudaSuccess ? 0 : 1;
+  }
+  int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
+               double* recv_hi, size_t n_hi, cudaStream_t s) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) return 1;
+    g->p_lo[rank] = send_lo;
+    g->p_hi[rank] = send_hi;
+    g->barrier();
+    int err = 0;
+    if (rank > 0 && n_lo && cudaMemcpy(recv_lo, g->p_hi[rank - 1], n_lo * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
+    if (rank < nranks - 1 && n_hi && cudaMemcpy(recv_hi, g->p_lo[rank + 1], n_hi * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
+    g->barrier();
+    return err;
+  }
+  int allgather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) return 1;
+    g->p_all[rank] = send;
+    g->barrier();
+    int err = 0;
+    for (int q = 0; q < nranks; ++q)
+      if (cudaMemcpy(recv + q * count, g->p_all[q], count * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
+    g->barrier();
+    return err;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+psp_status psp_comm_unique_id(void* id) {
+  if (!id) return PSP_E_ARG;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return PSP_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id, &u, sizeof(u));
+  return PSP_OK;
+}
+
+psp_status psp_comm_init(const void* id, int nranks, int rank, psp_comm** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return PSP_E_ARG;
+  auto* c = new NcclComm();
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks > 1) {
+    if (!id) {
+      delete c;
+      return PSP_E_ARG;
+    }
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof(u));
+    if (ncclCommInitRank(&c->c, nranks, u, rank) != ncclSuccess) {
+      delete c;
+      return PSP_E_NCCL;
+    }
+  }
+  *out = c;
+  return PSP_OK;
+}
+
+psp_status psp_comm_loopback_create(int nranks, psp_comm** out) {
+  if (!out || nranks < 1) return PSP_E_ARG;
+  auto g = std::make_shared<LoopGroup>(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    auto* c = new LoopComm();
+    c->nranks = nranks;
+    c->rank = r;
+    c->g = g;
+    out[r] = c;
+  }
+  return PSP_OK;
+}
+
+psp_status psp_comm_destroy(psp_comm* c) {
+  delete c;
+  return PSP_OK;
+}
+
+}  // extern "C"

@@ -11,6 +11,18 @@
 
 #include "../../include/pspgmres.h"
 
+// The communicator (comm.cu): NCCL for real ranks, a host-mediated loopback group for testing.
+// op: 0 sum, 1 max, 2 min.  sendrecv exchanges with rank-1 (lo) and rank+1 (hi): send_lo goes
+// to rank-1 and recv_lo receives rank-1's send_hi, and symmetrically.  Return 0 on success.
+struct psp_comm {
+  int nranks = 1, rank = 0;
+  virtual ~psp_comm() {}
+  virtual int allreduce(double* d, size_t count, int op, cudaStream_t s) = 0;
+  virtual int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
+                       double* recv_hi, size_t n_hi, cudaStream_t s) = 0;
+  virtual int allgather(const double* send, double* recv, size_t count, cudaStream_t s) = 0;
+};
+
 namespace psp {
 
 constexpr int kMaxD = 4;         // MREP / banded half-bandwidth supported by the kernels
@@ -59,7 +71,13 @@ struct DevState {
   double* resid;     // R(k) of the current cycle, nA
   double* partials;  // grid-reduction partials: kMaxPartialVals x nblocks
   unsigned* tickets; // last-block counters (one per reduction slot)
+  double* rpart;     // multi-rank: this rank's totals, all-reduced before the epilogue
+  int multi;         // 1: reductions stop at rpart (the host all-reduces, then epilogue_kernel)
 };
+// scalar epilogues of the grid reductions (krylov.cu); multi-rank runs them as a 1-thread
+// kernel on the all-reduced ds.rpart
+enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5 };
+void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s);
 enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
        SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_NSCAL = 16 };
 enum { TK_MAIN = 0, TK_AUX = 1, TK_MREP = 2, TK_N = 8 };
@@ -129,12 +147,22 @@ struct MrepScratch {
                       // [6] R18 patch needed [7] gate accepted (R21) [8] rows patched by R18
 };
 constexpr int kMrepMaxBlocks = 148 * 8;
-int mrep_blocks(int64_t n, int d);
 // Alg.2 on probe columns px + slots[c]*ld (c = 0..m-1 oldest -> newest), then R18 + gate stats.
+// Multi-rank MREP: the d P_x rows on each side of this rank's block come from the neighbours
+// (send/recv: [lo|hi] x m x d doubles each), rows are global row0 + local, of gN in total;
+// the gate statistics are all-reduced.  comm NULL: one rank (row0 = 0, gN = n).
+struct MrepMulti {
+  psp_comm* comm;
+  double* send;
+  double* recv;
+  int64_t row0;
+  int64_t gN;
+};
 // slot_scale (device, per slot, may be NULL): the recorded probe is slot_scale[slot] * column.
-void mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
-                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
-                 cudaStream_t s);
+// Returns 0, or 1 when a collective failed.
+int mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
+                const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
+                cudaStream_t s, MrepMulti mm);
 
 // ---- banded LU (banded.cu) ----
 struct BandedScratch {
@@ -146,12 +174,16 @@ struct BandedScratch {
 };
 size_t banded_scratch_bytes(int64_t n, int d);
 BandedScratch banded_scratch(void* base, int64_t n, int d);
-// factor; returns PSP_OK / PSP_E_SINGULAR (synchronises); *passes = fixed-point passes
+// multi-rank scratch of the banded solver (doubles): chunk states, rank maps, gathered states
+size_t banded_misc_doubles(int d, int nranks);
+// factor; returns PSP_OK / PSP_E_SINGULAR / PSP_E_NCCL (synchronises); *passes = fixed-point
+// passes.  comm (may be NULL) + misc: the rows are this rank's block of a global banded matrix.
 int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScratch sc,
-                  cudaStream_t s, int* passes, int64_t* launches);
+                  cudaStream_t s, int* passes, int64_t* launches, psp_comm* comm, double* misc);
 // z = x0 + N^{-1} (vs * v) (x0 may be NULL; vs: device scalar or NULL for 1)
-void banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
-                  const double* x0, double* z, BandedScratch sc, cudaStream_t s, int64_t* launches);
+int banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
+                 const double* x0, double* z, BandedScratch sc, cudaStream_t s, int64_t* launches,
+                 psp_comm* comm, double* misc);
 
 // ---- misc ----
 std::string cuda_err_str(cudaError_t e);

@@ -78,6 +78,61 @@ __device__ double reduce_partials(const double* partials, int v, int nb, double*
   return a[0];
 }
 
+// ------------------------------------------------------------------------------------------
+// Scalar epilogues of the reductions (one thread), from the totals tot[]
+// ------------------------------------------------------------------------------------------
+__device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, const double* tot) {
+  const int ld = nA + 1;
+  switch (kind) {
+    case EPI_NORM:
+      ds.scal[slot] = sqrt(tot[0]);
+      break;
+    case EPI_RESIDUAL: {  // Alg.1 l.5-7
+      const double beta = sqrt(tot[0]);
+      ds.scal[SC_BETA] = beta;
+      for (int q = 0; q <= nA; ++q) ds.G[q] = 0.0;  // l.44 "clean"
+      ds.G[0] = beta;                                // l.7 (P:42)
+      ds.alpha[0] = (beta > 0.0 && isfinite(beta)) ? 1.0 / beta : 0.0;
+      break;
+    }
+    case EPI_MGS:  // l.14: H(j,k) = V(:,j)' U
+      ds.H[(int64_t)(k - 1) * ld + (j - 1)] = ds.alpha[j - 1] * tot[0];
+      break;
+    case EPI_MGS_FINAL:
+    case EPI_UPDATE:  // l.17: H(k+1,k) = ||U||, then Givens (l.19-32)
+      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(tot[0]);
+      givens_update(ds, k, nA);
+      break;
+    case EPI_DOTS: {  // ICWY: the new row of L and (I + L) h = s (R11)
+      const double ak = ds.alpha[k - 1];
+      double* Lrow = ds.Lm + (int64_t)(k - 1) * ld;
+      for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = ds.alpha[jb] * ak * tot[k + jb];
+      double* Hc = ds.H + (int64_t)(k - 1) * ld;
+      for (int jb = 0; jb < k; ++jb) {  // s_j = alpha_j V_j'w
+        double h = ds.alpha[jb] * tot[jb];
+        const double* Lr = ds.Lm + (int64_t)jb * ld;
+        for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
+        Hc[jb] = h;
+      }
+      break;
+    }
+  }
+}
+
+// last block, thread 0: run the epilogue, or (multi-rank) park this rank's totals in rpart for
+// the host's all-reduce, after which launch_epilogue runs the same epilogue on every rank
+__device__ void finish_scalar(const DevState& ds, int kind, int k, int nA, int j, int slot,
+                              const double* tot, int nv) {
+  if (ds.multi) {
+    for (int v = 0; v < nv; ++v) ds.rpart[v] = tot[v];
+  } else {
+    epilogue(kind, ds, k, nA, j, slot, tot);
+  }
+}
+
+__global__ void epilogue_kernel(int kind, DevState ds, int k, int nA, int j, int slot) {
+  epilogue(kind, ds, k, nA, j, slot, ds.rpart);
+}
 
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TPB) norm_kernel(const double* __restrict__ x, int64_t n,
@@ -92,7 +147,7 @@ __global__ void __launch_bounds__(TPB) norm_kernel(const double* __restrict__ x,
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_AUX)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) ds.scal[slot] = sqrt(t);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_NORM, 0, 0, 0, slot, &t, 1);
   }
 }
 
@@ -109,7 +164,7 @@ __global__ void __launch_bounds__(TPB) diff_norm_kernel(const double* __restrict
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_AUX)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) ds.scal[slot] = sqrt(t);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_NORM, 0, 0, 0, slot, &t, 1);
   }
 }
 
@@ -130,13 +185,7 @@ __global__ void __launch_bounds__(TPB) residual_kernel(const double* __restrict_
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) {
-      const double beta = sqrt(t);
-      ds.scal[SC_BETA] = beta;
-      for (int j = 0; j <= nA; ++j) ds.G[j] = 0.0;  // l.44 "clean"
-      ds.G[0] = beta;                                // l.7 (P:42)
-      ds.alpha[0] = (beta > 0.0 && isfinite(beta)) ? 1.0 / beta : 0.0;
-    }
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_RESIDUAL, 0, nA, 0, 0, &t, 1);
   }
 }
 
@@ -169,8 +218,9 @@ __global__ void __launch_bounds__(TPB) mgs_literal_kernel(const double* src, dou
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) ds.H[(int64_t)(k - 1) * ld + (j - 1)] = ds.alpha[j - 1] * t;
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_MGS, k, nA, j, 0, &t, 1);
   }
+  (void)ld;
 }
 
 // U <- U - H(k,k) V(:,k) ; H(k+1,k) = ||U|| (l.17) ; Givens (l.19-32)
@@ -191,10 +241,7 @@ __global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restri
   if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
     double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (threadIdx.x == 0) {
-      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(t);
-      givens_update(ds, k, nA);
-    }
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_MGS_FINAL, k, nA, 0, 0, &t, 1);
   }
 }
 
@@ -288,20 +335,7 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
       if (lane == 0) tot[q] = s;
     }
     __syncthreads();
-    if (t == 0) {
-      const int ldl = nA + 1;
-      const double ak = ds.alpha[k - 1];
-      double* Lrow = ds.Lm + (int64_t)(k - 1) * ldl;
-      for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = ds.alpha[jb] * ak * tot[k + jb];
-      double* Hc = ds.H + (int64_t)(k - 1) * (nA + 1);
-      // forward substitution (I + L) h = s,  s_j = alpha_j V_j'w
-      for (int jb = 0; jb < k; ++jb) {
-        double h = ds.alpha[jb] * tot[jb];
-        const double* Lr = ds.Lm + (int64_t)jb * ldl;
-        for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
-        Hc[jb] = h;
-      }
-    }
+    if (t == 0) finish_scalar(ds, EPI_DOTS, k, nA, 0, 0, tot, nv);
   }
 }
 
@@ -380,10 +414,7 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double*
   if (t == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
     double tt = reduce_partials(ds.partials, 0, gridDim.x, sm);
-    if (t == 0) {
-      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(tt);
-      givens_update(ds, k, nA);
-    }
+    if (t == 0) finish_scalar(ds, EPI_UPDATE, k, nA, 0, 0, &tt, 1);
   }
 }
 
@@ -470,6 +501,9 @@ void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, i
   int64_t ub = (n + UTILE - 1) / UTILE;
   if (ub > rc.nblocks) ub = rc.nblocks;
   icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds);
+}
+void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s) {
+  epilogue_kernel<<<1, 1, 0, s>>>(kind, ds, k, nA, j, slot);
 }
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {

@@ -30,9 +30,20 @@ struct Cols {
   const double* px;            // column c of P_x at px + slot[c]*ld
   const double* py;
   const double* scale;         // per slot: the probe is scale[slot] * column (NULL: 1)
+  const double* hlo;           // multi-rank: P_x rows row0-d..row0-1, [c*d + q] (NULL: none)
+  const double* hhi;           //   and rows row0+n..row0+n+d-1
+  int64_t grow0, gN;           // global index of local row 0; global rows
+  int hd;                      // halo depth (= d)
   int64_t ld;
   int32_t slot[kMaxM];
   __device__ double sc(int c) const { return scale ? __ldg(scale + slot[c]) : 1.0; }
+  // raw P_x(local row rr, column c) for rr in [-hd, n + hd); 0 beyond the global matrix
+  __device__ double xraw(int c, int64_t rr, int64_t n) const {
+    if (rr >= 0 && rr < n) return __ldg(px + (int64_t)slot[c] * ld + rr);
+    if (rr < 0 && rr >= -hd && hlo) return __ldg(hlo + (int64_t)c * hd + (rr + hd));
+    if (rr >= n && rr < n + hd && hhi) return __ldg(hhi + (int64_t)c * hd + (rr - n));
+    return 0.0;
+  }
 };
 
 __device__ __forceinline__ double band_abs_off_sum(const double* row /*2d+1 coeffs*/, int d,
@@ -118,12 +129,8 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
       yv[cc] = (cc < cn && rvalid) ? cols.sc(c0 + cc) * __ldg(cols.py + (int64_t)cols.slot[c0 + cc] * cols.ld + r) : 0.0;
     __syncthreads();
     for (int cc = 0; cc < cn; ++cc) {
-      const double* __restrict__ colx = cols.px + (int64_t)cols.slot[c0 + cc] * cols.ld;
       const double scx = cols.sc(c0 + cc);
-      for (int q = t; q < TILE; q += TPB) {
-        const int64_t rr = tile0 + q;
-        xs[cc][q] = (rr >= 0 && rr < n) ? scx * __ldg(colx + rr) : 0.0;
-      }
+      for (int q = t; q < TILE; q += TPB) xs[cc][q] = scx * cols.xraw(c0 + cc, tile0 + q, n);
     }
     __syncthreads();
 #pragma unroll
@@ -146,7 +153,8 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
   ex[(2 * D + 1) * TPB + t] = Ssum;
   __syncthreads();
 
-  const bool emit = (t >= D && t < TPB - D) && r >= D && r < n - D;
+  const int64_t gr = cols.grow0 + r;                 // global row (multi-rank slabs)
+  const bool emit = (t >= D && t < TPB - D) && r >= 0 && r < n && gr >= D && gr < cols.gN - D;
   if (emit) {
     double A[NP];
     assemble<D>(A, ex, t, m, 0.0);
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
     const double ad = fabs(row[D]);
     maxdiag = fmax(maxdiag, ad);
     mindiag = fmin(mindiag, ad);
-    if (!(ad > band_abs_off_sum(row, D, r, n))) { nnd += 1.0; maxdiag_nd = fmax(maxdiag_nd, ad); }
+    if (!(ad > band_abs_off_sum(row, D, gr, cols.gN))) { nnd += 1.0; maxdiag_nd = fmax(maxdiag_nd, ad); }
   }
   }  // tiles
   // block reduction of the gate statistics (max, max, min, sum, sum, sum)
@@ -273,8 +281,10 @@ __global__ void mrep_boundary_kernel(Cols cols, int m, int64_t n, int d, MrepOut
   __shared__ double st[64][6];
   const int t = threadIdx.x;
   double v[6] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0};
-  if (t < 2 * d) {
-    const int64_t i = (t < d) ? t : (n - 2 * d + t);
+  // global boundary rows g < d and g >= gN - d that this rank owns (local i = g - grow0)
+  const int64_t g = (t < d) ? t : (cols.gN - 2 * d + t);
+  const int64_t i = g - cols.grow0;
+  if (t < 2 * d && i >= 0 && i < n) {
     double mx = 0.0, my = 0.0;
     for (int c = 0; c < m; ++c) {
       mx += cols.sc(c) * cols.px[(int64_t)cols.slot[c] * cols.ld + i];
@@ -335,23 +345,53 @@ __global__ void mrep_patch_kernel(int64_t n, int d, MrepOut out, MrepScratch sc)
   if ((threadIdx.x & 31) == 0 && cnt != 0.0) atomicAdd(sc.result + 8, cnt);  // exact integers
 }
 
-}  // namespace
-
 // The real entry point (api.cpp): column base pointers + slot order.
 int mrep_blocks(int64_t n, int d) {
   int64_t t = (n + (TPB - 2 * d) - 1) / (TPB - 2 * d);
   return (int)(t < kMrepMaxBlocks ? t : kMrepMaxBlocks);
 }
 
-void mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
-                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
-                 cudaStream_t s) {
+__global__ void mrep_pack_kernel(Cols cols, int m, int64_t n, int d, double* send) {
+  // send[0 .. m*d): rows 0..d-1 (for rank-1), send[m*d ..): rows n-d..n-1 (for rank+1), raw
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 2 * m * d; q += gridDim.x * blockDim.x) {
+    const int side = q / (m * d), c = (q / d) % m, k = q % d;
+    const int64_t rr = side == 0 ? k : n - d + k;
+    send[q] = __ldg(cols.px + (int64_t)cols.slot[c] * cols.ld + rr);
+  }
+}
+
+// multi-rank: R18 / R21 decisions from the all-reduced statistics
+__global__ void mrep_decide_kernel(MrepScratch sc) {
+  const double* a = sc.result;
+  const double thr = 1e-12 * a[0];
+  sc.result[6] = (a[2] < thr) ? 1.0 : 0.0;
+  sc.result[7] = (a[5] == 0.0 || a[1] < thr) ? 1.0 : 0.0;
+}
+
+}  // namespace
+
+int mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
+                const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
+                cudaStream_t s, MrepMulti mm) {
+  const bool multi = mm.comm && mm.comm->nranks > 1;
   Cols cols;
   cols.px = px;
   cols.py = py;
   cols.scale = slot_scale;
   cols.ld = ld;
+  cols.hlo = cols.hhi = nullptr;
+  cols.hd = d;
+  cols.grow0 = multi ? mm.row0 : 0;
+  cols.gN = multi ? mm.gN : n;
   for (int c = 0; c < m && c < kMaxM; ++c) cols.slot[c] = slots ? slots[c] : c;
+  if (multi) {
+    // the d P_x rows beyond each end of this rank's block (Alg.2's P_x(i-d..i+d,:))
+    mrep_pack_kernel<<<4, 256, 0, s>>>(cols, m, n, d, mm.send);
+    const size_t cnt = (size_t)m * d;
+    if (mm.comm->sendrecv(mm.send, mm.recv, cnt, mm.send + cnt, mm.recv + cnt, cnt, s)) return 1;
+    cols.hlo = mm.comm->rank > 0 ? mm.recv : nullptr;
+    cols.hhi = mm.comm->rank < mm.comm->nranks - 1 ? mm.recv + cnt : nullptr;
+  }
   cudaMemsetAsync(sc.result, 0, 16 * sizeof(double), s);
   mrep_boundary_kernel<<<1, 64, 0, s>>>(cols, m, n, d, out, sc);
   const int nb = mrep_blocks(n, d);  // grid-stride over row tiles
@@ -361,9 +401,18 @@ void mrep_launch(const double* px, const double* py, const double* slot_scale, i
     case 3: mrep_interior_kernel<3><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
     default: mrep_interior_kernel<4><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
   }
+  if (multi) {
+    // R18 needs the global max |N(i,i)|, R21 the global non-dominant statistics
+    if (mm.comm->allreduce(sc.result + 0, 2, 1, s)) return 1;  // max |diag|, max over non-dominant
+    if (mm.comm->allreduce(sc.result + 2, 1, 2, s)) return 1;  // min |diag|
+    if (mm.comm->allreduce(sc.result + 3, 3, 0, s)) return 1;  // counts
+    mrep_decide_kernel<<<1, 1, 0, s>>>(sc);
+  }
   int pb = (int)((n + 255) / 256);
   if (pb > 148 * 8) pb = 148 * 8;
   mrep_patch_kernel<<<pb, 256, 0, s>>>(n, d, out, sc);
+  if (multi && mm.comm->allreduce(sc.result + 8, 1, 0, s)) return 1;  // rows patched by R18
+  return 0;
 }
 
 }  // namespace psp

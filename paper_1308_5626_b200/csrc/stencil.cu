@@ -34,12 +34,13 @@ __device__ __forceinline__ Nb neighbour(const Stencil& st, const double* __restr
     return r;
   }
   // leaving the local block along the slab axis: halo planes (the slowest axis of ndim)
-  const bool slab_axis = (st.ndim == 3 && AXIS == 2) || (st.ndim == 2 && AXIS == 1);
+  const bool slab_axis = (st.ndim == 3 && AXIS == 2) || (st.ndim == 2 && AXIS == 1) ||
+                         (st.ndim == 1 && AXIS == 0);
   if (slab_axis) {
     const double* hx = (DIR < 0) ? st.x_lo : st.x_hi;
     const double* hf = (DIR < 0) ? st.f_lo : st.f_hi;
     if (hx != nullptr) {
-      int64_t off = (st.ndim == 3) ? (i + st.nx * j) : i;
+      int64_t off = (st.ndim == 3) ? (i + st.nx * j) : (st.ndim == 2 ? i : 0);
       r.x = __ldg(hx + off);
       if (need_f) r.f = __ldg(hf + off);
       r.in = true;

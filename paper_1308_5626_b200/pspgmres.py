@@ -120,7 +120,10 @@ def lib():
         "psp_version": (C.c_char_p, []),
         "psp_comm_unique_id": (C.c_int, [_vp]),
         "psp_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, P(_vp)]),
+        "psp_comm_loopback_create": (C.c_int, [C.c_int, P(_vp)]),
         "psp_comm_destroy": (C.c_int, [_vp]),
+        "psp_partition": (C.c_int, [P(psp_grid), C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                    P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -136,7 +139,39 @@ EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destro
             "psp_banded_factor_raw", "psp_banded_solve_raw", "psp_set_bands", "psp_get_bands", "psp_ring_view",
             "psp_ring_reset", "psp_get_hessenberg", "psp_get_basis", "psp_launch_count", "psp_kernel_stats",
             "psp_kernel_class_name", "psp_status_str",
-            "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_destroy"]
+            "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_loopback_create",
+            "psp_comm_destroy", "psp_partition"]
+
+
+def psp_partition(n_axes, nranks, rank):
+    """(row0, nrows, slab0, slab_len) of rank's slab (pure host function of the library)."""
+    g = make_grid(n_axes)
+    out = [C.c_int64() for _ in range(4)]
+    _check(lib().psp_partition(C.byref(g), nranks, rank, *[C.byref(o) for o in out]))
+    return tuple(o.value for o in out)
+
+
+def psp_comm_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().psp_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def psp_comm_init(uid: bytes, nranks: int, rank: int):
+    h = _vp()
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    _check(lib().psp_comm_init(buf, nranks, rank, C.byref(h)))
+    return h
+
+
+def psp_comm_loopback_create(nranks: int):
+    arr = (_vp * nranks)()
+    _check(lib().psp_comm_loopback_create(nranks, arr))
+    return [_vp(a) for a in arr]
+
+
+def psp_comm_destroy(h):
+    lib().psp_comm_destroy(h)
 
 
 def _check(st, ctx=None, allow=(PSP_OK,)):
@@ -203,32 +238,40 @@ class Context:
     """Owns a psp_ctx and its torch workspace.  Methods map 1:1 onto the C ABI."""
 
     def __init__(self, op, d, restart, tol, opts: psp_opts | None = None, device="cuda", stream=None,
-                 hist_cap=1 << 16):
+                 hist_cap=1 << 16, comm=None, nranks=1, rank=0, field_local=None):
+        """comm: a psp_comm handle (None: one rank).  With nranks > 1 the context owns rank's
+        psp_partition slab: vectors passed to it are local rows [row0, row0 + n); the coefficient
+        field is sliced from op.field unless field_local (a local CUDA tensor) is given."""
         import torch
         self.torch = torch
         self.op = op
-        self.n = int(np.prod(op.n))
+        self.nranks, self.rank = nranks, rank
+        self.row0, self.n, _, _ = psp_partition(op.n, nranks, rank)
         self.d = d
         self.restart = restart
         self.device = torch.device(device)
         self.stream = stream
         self._field = None
         self._bands = None
-        if op.field is not None:
-            self._field = torch.as_tensor(np.asarray(op.field, dtype=np.float64)).to(self.device).contiguous()
+        if field_local is not None:
+            self._field = field_local
+        elif op.field is not None:
+            f = np.asarray(op.field, dtype=np.float64).reshape(-1)[self.row0:self.row0 + self.n]
+            self._field = torch.as_tensor(np.ascontiguousarray(f)).to(self.device)
         if op.kind == "dia":
             self._bands = torch.as_tensor(np.asarray(op.bands, dtype=np.float64)).to(self.device).contiguous()
         self.grid = make_grid(op.n)
         self.stencil = make_stencil(op, self._field, self._bands)
         self.opts = opts if opts is not None else default_opts()
+        self.comm = comm
         nbytes = C.c_size_t(0)
         _check(lib().psp_workspace_bytes(C.byref(self.grid), C.byref(self.stencil), d, restart,
-                                         C.byref(self.opts), None, C.byref(nbytes)))
+                                         C.byref(self.opts), comm, C.byref(nbytes)))
         self.ws_bytes = nbytes.value
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         h = _vp()
         _check(lib().psp_create(C.byref(self.grid), C.byref(self.stencil), float(op.dt), d, restart, float(tol),
-                                C.byref(self.opts), self.ws.data_ptr(), self.ws_bytes, _stream_ptr(stream), None,
+                                C.byref(self.opts), self.ws.data_ptr(), self.ws_bytes, _stream_ptr(stream), comm,
                                 C.byref(h)))
         self.h = h
         self.hist = np.zeros(hist_cap)
