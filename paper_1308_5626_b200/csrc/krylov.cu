@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(TPB) mgs_literal_final_kernel(double* __restri
 // the k+1 vectors; the last block solves (I + L) h = s into H(1..k, k).
 // ------------------------------------------------------------------------------------------
 template <int C, bool FULL>
-__device__ __forceinline__ void dots_chunk(Basis V, int j0,
+__device__ __forceinline__ void dots_chunk(const double* const* cp, int j0,
                                            const double (&wr)[RPT], const double (&qr)[RPT],
                                            int64_t n, int64_t r0, int lane, int k, double* acc) {
   double as[C], al[C];
@@ -264,7 +264,7 @@ __device__ __forceinline__ void dots_chunk(Basis V, int j0,
   }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const double* __restrict__ vj = V.col(j0 + c);
+    const double* __restrict__ vj = cp[j0 + c];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int64_t r = r0 + (int64_t)TPB * i;
@@ -285,10 +285,10 @@ __device__ __forceinline__ void dots_chunk(Basis V, int j0,
 }
 
 template <bool FULL>
-__device__ __forceinline__ void dots_tile(Basis V,
+__device__ __forceinline__ void dots_tile(const double* const* cp,
                                           const double* __restrict__ w, int k, int64_t n,
                                           int64_t r0, int lane, double* acc) {
-  const double* __restrict__ qk = V.col(k - 1);
+  const double* __restrict__ qk = cp[k - 1];
   double wr[RPT], qr[RPT];
   double sk = 0.0;
 #pragma unroll
@@ -299,8 +299,8 @@ __device__ __forceinline__ void dots_tile(Basis V,
     sk = fma(qr[i], wr[i], sk);
   }
   int j0 = 0;
-  for (; j0 + JC <= k - 1; j0 += JC) dots_chunk<JC, FULL>(V, j0, wr, qr, n, r0, lane, k, acc);
-  for (; j0 < k - 1; ++j0) dots_chunk<1, FULL>(V, j0, wr, qr, n, r0, lane, k, acc);
+  for (; j0 + JC <= k - 1; j0 += JC) dots_chunk<JC, FULL>(cp, j0, wr, qr, n, r0, lane, k, acc);
+  for (; j0 < k - 1; ++j0) dots_chunk<1, FULL>(cp, j0, wr, qr, n, r0, lane, k, acc);
   sk = warp_sum(sk);
   if (lane == 0) acc[k - 1] += sk;
 }
@@ -308,7 +308,10 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
                                                         const double* __restrict__ w, int k,
                                                         int nA, int64_t n, DevState ds) {
   __shared__ double accw[kWarps][2 * kMaxRestart];
+  __shared__ const double* cp[kMaxRestart + 1];   // V(:,j) resolved once (ring slots)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
+  for (int q = t; q < k; q += TPB) cp[q] = V.col(q);
+  __syncthreads();
   const int nv = 2 * k - 1;  // s_0..s_{k-1} at [0,k), l_0..l_{k-2} at [k, 2k-1)
   for (int q = lane; q < 2 * k; q += 32) accw[warp][q] = 0.0;
   __syncwarp();
@@ -316,8 +319,8 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
   const int64_t nfull = n / TILE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * TILE + t;
-    if (tile < nfull) dots_tile<true>(V, w, k, n, r0, lane, accw[warp]);
-    else dots_tile<false>(V, w, k, n, r0, lane, accw[warp]);
+    if (tile < nfull) dots_tile<true>(cp, w, k, n, r0, lane, accw[warp]);
+    else dots_tile<false>(cp, w, k, n, r0, lane, accw[warp]);
   }
   __syncthreads();
   const int nb = gridDim.x;
@@ -346,7 +349,7 @@ constexpr int UJC = 8;
 constexpr int UTILE = TPB * URPT;
 
 template <bool FULL>
-__device__ __forceinline__ void update_tile(Basis V, const double* w, double wsc, double* U,
+__device__ __forceinline__ void update_tile(const double* const* cp, const double* w, double wsc, double* U,
                                             const double* hs, int k, int64_t n, int64_t r0,
                                             double& acc) {
   double u[URPT];
@@ -363,7 +366,7 @@ __device__ __forceinline__ void update_tile(Basis V, const double* w, double wsc
 #pragma unroll
       for (int i = 0; i < URPT; ++i) {
         const int64_t r = r0 + (int64_t)TPB * i;
-        v[c][i] = (FULL || r < n) ? V.col(jb + c)[r] : 0.0;
+        v[c][i] = (FULL || r < n) ? cp[jb + c][r] : 0.0;
       }
 #pragma unroll
     for (int c = 0; c < UJC; ++c)
@@ -375,7 +378,7 @@ __device__ __forceinline__ void update_tile(Basis V, const double* w, double wsc
 #pragma unroll
     for (int i = 0; i < URPT; ++i) {
       const int64_t r = r0 + (int64_t)TPB * i;
-      v[i] = (FULL || r < n) ? V.col(jb)[r] : 0.0;
+      v[i] = (FULL || r < n) ? cp[jb][r] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < URPT; ++i) u[i] = fma(-hs[jb], v[i], u[i]);
@@ -398,8 +401,12 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double*
                                                           int64_t n, DevState ds) {
   __shared__ double hs[kMaxRestart];
   __shared__ double sm[kWarps];
+  __shared__ const double* cp[kMaxRestart + 1];
   const int ld = nA + 1, t = threadIdx.x;
-  for (int q = t; q < k; q += TPB) hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
+  for (int q = t; q < k; q += TPB) {
+    hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
+    cp[q] = V.col(q);
+  }
   __syncthreads();
   const double wsc = ws ? *ws : 1.0;  // scale of w (the fused path stores A u unnormalised)
   double a[1] = {0.0};
@@ -407,8 +414,8 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double*
   const int64_t nfull = n / UTILE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * UTILE + t;
-    if (tile < nfull) update_tile<true>(V, w, wsc, U, hs, k, n, r0, a[0]);
-    else update_tile<false>(V, w, wsc, U, hs, k, n, r0, a[0]);
+    if (tile < nfull) update_tile<true>(cp, w, wsc, U, hs, k, n, r0, a[0]);
+    else update_tile<false>(cp, w, wsc, U, hs, k, n, r0, a[0]);
   }
   block_sum<1>(a, sm);
   if (t == 0) ds.partials[blockIdx.x] = a[0];
@@ -424,7 +431,9 @@ __global__ void __launch_bounds__(TPB) combine_kernel(Basis V, int k, int nA, co
                                                       double* out, int64_t n, DevState ds) {
   __shared__ double qs[kMaxRestart];
   __shared__ double qa[kMaxRestart];
+  __shared__ const double* cp[kMaxRestart + 1];
   __shared__ int bad;
+  for (int q = threadIdx.x; q < k; q += TPB) cp[q] = V.col(q);
   if (threadIdx.x == 0) {
     const int ld = nA + 1;
     bad = 0;
@@ -448,8 +457,8 @@ __global__ void __launch_bounds__(TPB) combine_kernel(Basis V, int k, int nA, co
   double unused = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * UTILE + threadIdx.x;
-    if (tile < nfull) update_tile<true>(V, base, 1.0, out, qa, k, n, r0, unused);
-    else update_tile<false>(V, base, 1.0, out, qa, k, n, r0, unused);
+    if (tile < nfull) update_tile<true>(cp, base, 1.0, out, qa, k, n, r0, unused);
+    else update_tile<false>(cp, base, 1.0, out, qa, k, n, r0, unused);
   }
 }
 

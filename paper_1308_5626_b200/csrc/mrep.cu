@@ -19,6 +19,10 @@
 
 #include "internal.h"
 
+#ifndef PSP_MREP_MINB
+#define PSP_MREP_MINB 2   // resident blocks per SM of the TMA MREP kernel
+#endif
+
 namespace psp {
 namespace {
 
@@ -46,12 +50,13 @@ struct Cols {
   }
 };
 
-__device__ __forceinline__ double band_abs_off_sum(const double* row /*2d+1 coeffs*/, int d,
-                                                   int64_t i, int64_t n) {
+template <int D>
+__device__ __forceinline__ double band_abs_off_sum(const double (&row)[2 * D + 1], int64_t i, int64_t n) {
   double off = 0.0;
-  for (int o = 0; o <= 2 * d; ++o) {
-    int64_t j = i + o - d;
-    if (o == d || j < 0 || j >= n) continue;
+#pragma unroll
+  for (int o = 0; o <= 2 * D; ++o) {
+    const int64_t j = i + o - D;
+    if (o == D || j < 0 || j >= n) continue;
     off += fabs(row[o]);
   }
   return off;
@@ -77,41 +82,161 @@ __device__ __forceinline__ void assemble(double (&A)[(2 * D + 2) * (2 * D + 3) /
   }
 }
 
-// in-place Cholesky of the packed P x P matrix (R17); false on a pivot^2 <= 0 or non-finite
+// in-place Cholesky of the packed P x P matrix (R17); false on a pivot^2 <= 0 or non-finite.
+// Stores 1 / L_jj on the diagonal (one division per column; the solves multiply by it: each
+// multiply-by-reciprocal adds at most one rounding, inside T3's 8 P u kappa_2(G) bound) and
+// returns max_j L_jj, min_j L_jj for the condition estimate.  Straight-line (no early exit), so
+// the packed matrix stays in registers.
 template <int P>
-__device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2]) {
+__device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2], double& lmax, double& lmin) {
+  bool ok = true;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     double s = A[pk(j, j)];
 #pragma unroll
     for (int k = 0; k < j; ++k) s -= A[pk(j, k)] * A[pk(j, k)];
-    if (!(s > 0.0) || !isfinite(s)) return false;
-    const double ljj = sqrt(s);
-    A[pk(j, j)] = ljj;
+    ok = ok && (s > 0.0) && isfinite(s);
+    const double ljj = sqrt(ok ? s : 1.0);
+    lmax = (j == 0) ? ljj : fmax(lmax, ljj);
+    lmin = (j == 0) ? ljj : fmin(lmin, ljj);
+    const double inv = 1.0 / ljj;
+    A[pk(j, j)] = inv;
 #pragma unroll
     for (int i = j + 1; i < P; ++i) {
       double u = A[pk(i, j)];
 #pragma unroll
       for (int k = 0; k < j; ++k) u -= A[pk(i, k)] * A[pk(j, k)];
-      A[pk(i, j)] = u / ljj;
+      A[pk(i, j)] = u * inv;
     }
   }
-  return true;
+  return ok;
 }
 
+// Gate statistics of one block: max|diag|, max|diag| over non-dominant rows, min|diag|,
+// rows ridged, rows fallen back, rows non-dominant (R18 / R21)
+struct GateStats {
+  double v[6] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0};
+};
+
+// The fit of one interior row from the exchanged lagged sums: Gram assembly,
+// Cholesky + condition estimate + one ridge retry (R17), solve, band install (R14, R15),
+// diagnostics and gate statistics.  ex: (2D+2) x TPB sums of the tile's rows; t: this row's
+// index in the tile; r: local row; gr: global row.
 template <int D>
-__global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m, int64_t n,
-                                                               MrepOut out, MrepScratch sc) {
+__device__ __forceinline__ void fit_row(const double* ex, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
+                                        int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
   constexpr int P = 2 * D + 2;
   constexpr int NP = P * (P + 1) / 2;
+  double A[NP];
+  double lmax = 0.0, lmin = 0.0, kap = INFINITY, lambda = 0.0;
+  bool ok = false;
+  int kind = PSP_ROW_INTERIOR;
+#pragma unroll 1
+  for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
+    assemble<D>(A, ex, t, m, lambda);
+    ok = chol_packed<P>(A, lmax, lmin);
+    if (attempt == 0) {
+      kap = ok ? (lmax / lmin) * (lmax / lmin) : INFINITY;
+      if (ok && kap <= 1e12) break;
+      // S:226 ridge retry on G + lambda I
+      double tr = (double)m;
+#pragma unroll
+      for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TPB + (t - D + a)];   // diag = C_0(r-d+a)
+      lambda = 1e-10 * tr / (double)P;
+      kind = PSP_ROW_INTERIOR_RIDGE;
+      g.v[3] += 1.0;
+    }
+  }
+  double row[2 * D + 1];
+  double icpt = 0.0;
+  if (!ok) {                                      // identity row
+    kind = PSP_ROW_FALLBACK_RANK;
+    g.v[4] += 1.0;
+#pragma unroll
+    for (int o = 0; o <= 2 * D; ++o) row[o] = (o == D) ? 1.0 : 0.0;
+  } else {
+    double z[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double s = (i == 0) ? Tsum : Dl[i - 1];
+#pragma unroll
+      for (int k = 0; k < i; ++k) s -= A[pk(i, k)] * z[k];
+      z[i] = s * A[pk(i, i)];
+    }
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+      double s = z[i];
+#pragma unroll
+      for (int k = i + 1; k < P; ++k) s -= A[pk(k, i)] * z[k];
+      z[i] = s * A[pk(i, i)];
+    }
+    icpt = z[0];                                  // R15: reported, never installed
+#pragma unroll
+    for (int o = 0; o <= 2 * D; ++o) row[o] = z[1 + o];  // R14: N(i, i+o-d) = N*(o+2)
+  }
+#pragma unroll
+  for (int o = 0; o <= 2 * D; ++o) out.bands[(int64_t)o * n + r] = row[o];
+  if (out.intercept) out.intercept[r] = icpt;
+  if (out.kind) out.kind[r] = (uint8_t)kind;
+  if (out.kappa) out.kappa[r] = kap;
+  const double ad = fabs(row[D]);
+  g.v[0] = fmax(g.v[0], ad);
+  g.v[2] = fmin(g.v[2], ad);
+  if (!(ad > band_abs_off_sum<D>(row, gr, gN))) { g.v[5] += 1.0; g.v[1] = fmax(g.v[1], ad); }
+}
+
+// Merge a block's gate statistics into result[0..5]: max / min of non-negative doubles through
+// their bit patterns (order-preserving), counts as exact integer adds -> order-independent.
+__device__ void merge_stats(GateStats& g, double* red /* 8 warps x 6 */, double* result) {
+  const int t = threadIdx.x, nw = blockDim.x / 32;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    g.v[0] = fmax(g.v[0], __shfl_xor_sync(0xffffffffu, g.v[0], o));
+    g.v[1] = fmax(g.v[1], __shfl_xor_sync(0xffffffffu, g.v[1], o));
+    g.v[2] = fmin(g.v[2], __shfl_xor_sync(0xffffffffu, g.v[2], o));
+    g.v[3] += __shfl_xor_sync(0xffffffffu, g.v[3], o);
+    g.v[4] += __shfl_xor_sync(0xffffffffu, g.v[4], o);
+    g.v[5] += __shfl_xor_sync(0xffffffffu, g.v[5], o);
+  }
+  if ((t & 31) == 0)
+    for (int q = 0; q < 6; ++q) red[(t >> 5) * 6 + q] = g.v[q];
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < nw; ++w) {
+      g.v[0] = fmax(g.v[0], red[w * 6 + 0]);
+      g.v[1] = fmax(g.v[1], red[w * 6 + 1]);
+      g.v[2] = fmin(g.v[2], red[w * 6 + 2]);
+      g.v[3] += red[w * 6 + 3];
+      g.v[4] += red[w * 6 + 4];
+      g.v[5] += red[w * 6 + 5];
+    }
+    unsigned long long* ru = reinterpret_cast<unsigned long long*>(result);
+    if (g.v[0] > 0.0) atomicMax(ru + 0, (unsigned long long)__double_as_longlong(g.v[0]));
+    if (g.v[1] > 0.0) atomicMax(ru + 1, (unsigned long long)__double_as_longlong(g.v[1]));
+    if (g.v[2] < INFINITY) atomicMin(ru + 2, (unsigned long long)__double_as_longlong(g.v[2]));
+    if (g.v[3] != 0.0) atomicAdd(result + 3, g.v[3]);
+    if (g.v[4] != 0.0) atomicAdd(result + 4, g.v[4]);
+    if (g.v[5] != 0.0) atomicAdd(result + 5, g.v[5]);
+  }
+}
+
+// Generic interior-row kernel (any row range, multi-rank halos): thread t accumulates the sums
+// of row r = i0 - D + t of a 256-row tile that emits rows [i0, i0 + 256 - 2D).  It runs the
+// tiles the TMA kernel below cannot (the first and last tiles of the local block) -- tiles
+// [0, t_lo) and [t_hi, ntiles) -- or all tiles when t_lo == t_hi.
+template <int D>
+__global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m, int64_t n, int64_t t_lo,
+                                                               int64_t t_hi, MrepOut out, MrepScratch sc) {
   constexpr int TILE = TPB + 3 * D;                 // rows [i0-2D, i0-D+TPB+2D)
   __shared__ double xs[CB][TILE];
   __shared__ double ex[(2 * D + 2) * TPB];
-  __shared__ double red[TPB / 32][6];
+  __shared__ double red[TPB / 32 * 6];
   const int t = threadIdx.x;
-  double maxdiag = 0.0, maxdiag_nd = 0.0, mindiag = INFINITY, nridge = 0.0, nfb = 0.0, nnd = 0.0;
+  GateStats gs;
   const int64_t ntiles = (n + (TPB - 2 * D) - 1) / (TPB - 2 * D);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t nedge = t_lo + (ntiles - t_hi);
+  for (int64_t q = blockIdx.x; q < nedge; q += gridDim.x) {
+  const int64_t tile = q < t_lo ? q : t_hi + (q - t_lo);
   const int64_t i0 = tile * (TPB - 2 * D);
   const int64_t r = i0 - D + t;                     // the row this thread accumulates for
   const int64_t tile0 = i0 - 2 * D;
@@ -130,7 +255,7 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
     __syncthreads();
     for (int cc = 0; cc < cn; ++cc) {
       const double scx = cols.sc(c0 + cc);
-      for (int q = t; q < TILE; q += TPB) xs[cc][q] = scx * cols.xraw(c0 + cc, tile0 + q, n);
+      for (int qq = t; qq < TILE; qq += TPB) xs[cc][qq] = scx * cols.xraw(c0 + cc, tile0 + qq, n);
     }
     __syncthreads();
 #pragma unroll
@@ -155,124 +280,184 @@ __global__ void __launch_bounds__(TPB, 2) mrep_interior_kernel(Cols cols, int m,
 
   const int64_t gr = cols.grow0 + r;                 // global row (multi-rank slabs)
   const bool emit = (t >= D && t < TPB - D) && r >= 0 && r < n && gr >= D && gr < cols.gN - D;
-  if (emit) {
-    double A[NP];
-    assemble<D>(A, ex, t, m, 0.0);
-    bool ok = chol_packed<P>(A);
-    double kap = INFINITY;
-    if (ok) {
-      double lmax = A[pk(0, 0)], lmin = A[pk(0, 0)];
-#pragma unroll
-      for (int j = 1; j < P; ++j) {
-        lmax = fmax(lmax, A[pk(j, j)]);
-        lmin = fmin(lmin, A[pk(j, j)]);
-      }
-      kap = (lmax / lmin) * (lmax / lmin);
-    }
-    int kind = PSP_ROW_INTERIOR;
-    if (!ok || kap > 1e12) {                        // S:226 ridge retry on G + lambda I
-      double tr = (double)m;
-#pragma unroll
-      for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TPB + (t - D + a)];   // diag = C_0(r-d+a)
-      const double lambda = 1e-10 * tr / (double)P;
-      assemble<D>(A, ex, t, m, lambda);
-      ok = chol_packed<P>(A);
-      kind = PSP_ROW_INTERIOR_RIDGE;
-      nridge += 1.0;
-    }
-    double row[2 * D + 1];
-    double icpt = 0.0;
-    if (!ok) {                                      // identity row
-      kind = PSP_ROW_FALLBACK_RANK;
-      nfb += 1.0;
-#pragma unroll
-      for (int o = 0; o <= 2 * D; ++o) row[o] = (o == D) ? 1.0 : 0.0;
-    } else {
-      double z[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        double s = (i == 0) ? Tsum : Dl[i - 1];
-#pragma unroll
-        for (int k = 0; k < i; ++k) s -= A[pk(i, k)] * z[k];
-        z[i] = s / A[pk(i, i)];
-      }
-#pragma unroll
-      for (int i = P - 1; i >= 0; --i) {
-        double s = z[i];
-#pragma unroll
-        for (int k = i + 1; k < P; ++k) s -= A[pk(k, i)] * z[k];
-        z[i] = s / A[pk(i, i)];
-      }
-      icpt = z[0];                                  // R15: reported, never installed
-#pragma unroll
-      for (int o = 0; o <= 2 * D; ++o) row[o] = z[1 + o];  // R14: N(i, i+o-d) = N*(o+2)
-    }
-#pragma unroll
-    for (int o = 0; o <= 2 * D; ++o) out.bands[(int64_t)o * n + r] = row[o];
-    if (out.intercept) out.intercept[r] = icpt;
-    if (out.kind) out.kind[r] = (uint8_t)kind;
-    if (out.kappa) out.kappa[r] = kap;
-    const double ad = fabs(row[D]);
-    maxdiag = fmax(maxdiag, ad);
-    mindiag = fmin(mindiag, ad);
-    if (!(ad > band_abs_off_sum(row, D, gr, cols.gN))) { nnd += 1.0; maxdiag_nd = fmax(maxdiag_nd, ad); }
-  }
+  if (emit) fit_row<D>(ex, t, m, Tsum, Dl, r, n, gr, cols.gN, out, gs);
   }  // tiles
-  // block reduction of the gate statistics (max, max, min, sum, sum, sum)
-  double v[6] = {maxdiag, maxdiag_nd, mindiag, nridge, nfb, nnd};
+  merge_stats(gs, red, sc.result);
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA-pipelined interior kernel (the bulk of the rows).  Same tiles and per-row arithmetic as
+// the generic kernel (thread t accumulates sum row s0 + t, s0 = i0 - D, of the 256-row tile that
+// emits [i0, i0 + 256 - 2D)), but the probe columns are staged by one thread with
+// cp.async.bulk (1-D TMA bulk copies) into an NST-deep ring of shared-memory stages of CB
+// columns each -- P_x rows [s0 - D, s0 + 256 + 2D) and P_y rows [s0, s0 + 256), widened to
+// 16-byte boundaries -- with completion on one mbarrier per stage.  HBM reads run ahead of the
+// FMAs and of the per-row Cholesky phase without holding registers, and a warp's shared-memory
+// reads are 32 consecutive doubles (conflict-free).  All columns must share the 16-byte
+// alignment parity (sx, sy; checked on the host, else the generic kernel runs everything).
+// ------------------------------------------------------------------------------------------
+constexpr int TCB = 4;         // probe columns per stage
+constexpr int TNST = 4;        // stages
+
+template <int D>
+struct TmaCfg {
+  static constexpr int PXW = ((TPB + 3 * D + 2) + 1) / 2 * 2;   // P_x stage row (doubles)
+  static constexpr int PYW = TPB + 2;                            // P_y stage row
+  static constexpr int STAGE = TCB * (PXW + PYW);                // doubles per stage
+  static constexpr size_t SMEM = (size_t)TNST * STAGE * 8 + (size_t)(2 * D + 2) * TPB * 8 + 16 * TNST;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct TmaCols {
+  const double* px;
+  const double* py;
+  int64_t ld;
+  int sx, sy;                  // row shift of the P_x / P_y segments in a stage (0 / 1)
+  int32_t slot[kMaxM];
+};
+
+template <int D>
+__global__ void __launch_bounds__(TPB, PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
+                                                          int m, int64_t n, int64_t gN, int64_t grow0,
+                                                          int64_t t_lo, int64_t t_hi, MrepOut out,
+                                                          MrepScratch sc) {
+  using Cfg = TmaCfg<D>;
+  constexpr int E = TPB - 2 * D;                   // rows emitted per tile
+  constexpr int LX = ((TPB + 3 * D) + 1) & ~1;     // P_x segment length (shift 0) ...
+  constexpr int LX1 = ((TPB + 3 * D + 1) + 1) & ~1;//   ... and with shift 1
+  constexpr int LY = TPB, LY1 = TPB + 2;
+  extern __shared__ __align__(16) double sm[];
+  double* stages = sm;                             // [TNST][TCB x PXW | TCB x PYW]
+  double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TPB]: C_l, S of the tile's rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (2 * D + 2) * TPB);
+  __shared__ double scs[kMaxM];                    // per-column probe scale
+  __shared__ double red[TPB / 32 * 6];
+  const int t = threadIdx.x;
+  for (int c = t; c < m; c += TPB) scs[c] = scale ? scale[cols.slot[c]] : 1.0;
+  if (t == 0) {
+    for (int q = 0; q < TNST; ++q) mbar_init(bars + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int lx = cols.sx ? LX1 : LX, ly = cols.sy ? LY1 : LY;
+  const int nch = (m + TCB - 1) / TCB;
+  const int64_t my_tiles = (t_hi - t_lo - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t total = my_tiles * nch;
+  auto issue = [&](int64_t q) {                   // thread 0: stage the columns of load q
+    const int64_t tile = t_lo + blockIdx.x + (q / nch) * gridDim.x;
+    const int ch = (int)(q % nch);
+    const int stg = (int)(q % TNST);
+    double* st = stages + (size_t)stg * Cfg::STAGE;
+    const int64_t s0 = tile * E - D;
+    const int c0 = ch * TCB;
+    const int cn = (m - c0) < TCB ? (m - c0) : TCB;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bars + stg, 8u * (unsigned)(cn * (lx + ly)));
+    for (int cc = 0; cc < cn; ++cc) {
+      const int c = c0 + cc;
+      const double* bxp = cols.px + (int64_t)cols.slot[c] * cols.ld;
+      const double* byp = cols.py + (int64_t)cols.slot[c] * cols.ld;
+      bulk_g2s(st + cc * Cfg::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + stg);
+      bulk_g2s(st + TCB * Cfg::PXW + cc * Cfg::PYW, byp + (s0 - cols.sy), 8u * ly, bars + stg);
+    }
+  };
+  if (t == 0)
+    for (int64_t q = 0; q < total && q < TNST; ++q) issue(q);
+
+  GateStats gs;
+  double Cl[2 * D + 1], Dl[2 * D + 1], Ssum = 0.0, Tsum = 0.0;
+  const int xo = cols.sx + t, yo = cols.sy + t;    // this row's offsets in a stage row
+  for (int64_t q = 0; q < total; ++q) {
+    const int stg = (int)(q % TNST);
+    const int ch = (int)(q % nch);
+    if (ch == 0) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v[0] = fmax(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
-    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
-    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], o));
-    v[3] += __shfl_xor_sync(0xffffffffu, v[3], o);
-    v[4] += __shfl_xor_sync(0xffffffffu, v[4], o);
-    v[5] += __shfl_xor_sync(0xffffffffu, v[5], o);
-  }
-  if ((t & 31) == 0)
-    for (int q = 0; q < 6; ++q) red[t >> 5][q] = v[q];
-  __syncthreads();
-  if (t == 0) {
-    for (int w = 1; w < TPB / 32; ++w) {
-      v[0] = fmax(v[0], red[w][0]);
-      v[1] = fmax(v[1], red[w][1]);
-      v[2] = fmin(v[2], red[w][2]);
-      v[3] += red[w][3];
-      v[4] += red[w][4];
-      v[5] += red[w][5];
+      for (int l = 0; l <= 2 * D; ++l) { Cl[l] = 0.0; Dl[l] = 0.0; }
+      Ssum = Tsum = 0.0;
     }
-    for (int q = 0; q < 6; ++q) sc.partials[(int64_t)q * gridDim.x + blockIdx.x] = v[q];
-  }
-  // last block: fold in the boundary rows (result[0..5] written by the boundary kernel) and
-  // evaluate R18 / R21
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (t == 0) {
-    unsigned tk = atomicAdd(sc.ticket, 1u);
-    s_last = (tk == gridDim.x - 1);
-    if (s_last) *sc.ticket = 0u;
-  }
-  __syncthreads();
-  if (s_last && t == 0) {
-    __threadfence();
-    volatile double* pp = sc.partials;
-    volatile double* res = sc.result;
-    double a[6] = {res[0], res[1], res[2], res[3], res[4], res[5]};
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      a[0] = fmax(a[0], pp[0 * gridDim.x + b]);
-      a[1] = fmax(a[1], pp[1 * gridDim.x + b]);
-      a[2] = fmin(a[2], pp[2 * gridDim.x + b]);
-      a[3] += pp[3 * gridDim.x + b];
-      a[4] += pp[4 * gridDim.x + b];
-      a[5] += pp[5 * gridDim.x + b];
+    mbar_wait(bars + stg, (unsigned)((q / TNST) & 1));
+    const double* st = stages + (size_t)stg * Cfg::STAGE;
+    const int c0 = ch * TCB;                       // m % TCB == 0 (host check)
+#pragma unroll
+    for (int cc = 0; cc < TCB; ++cc) {
+      const double sc = scs[c0 + cc];
+      const double* xr = st + cc * Cfg::PXW + xo;  // xr[k] = P_x(r - D + k), r = s0 + t
+      double xw[3 * D + 1];
+#pragma unroll
+      for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
+      double yv = st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
+      if (sc != 1.0) {                             // uniform: the probe's recorded scale
+#pragma unroll
+        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = sc * xw[k];
+        yv = sc * yv;
+      }
+      const double x0 = xw[D];
+      Ssum += x0;
+      Tsum += yv;
+#pragma unroll
+      for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+#pragma unroll
+      for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
     }
-    for (int q = 0; q < 6; ++q) res[q] = a[q];
-    // R18 threshold and the R21 decision: every non-dominant row must be patched to identity
-    const double thr = 1e-12 * a[0];
-    res[6] = (a[2] < thr) ? 1.0 : 0.0;                       // some row needs the R18 patch
-    res[7] = (a[5] == 0.0 || a[1] < thr) ? 1.0 : 0.0;        // gate accepted (R21)
+    __syncthreads();                               // every thread is done with stage stg
+    if (t == 0 && q + TNST < total) issue(q + TNST);
+    if (ch == nch - 1) {
+      // exchange C_l, S of the tile's 256 sum rows, then fit the emitted rows
+#pragma unroll
+      for (int l = 0; l <= 2 * D; ++l) ex[l * TPB + t] = Cl[l];
+      ex[(2 * D + 1) * TPB + t] = Ssum;
+      __syncthreads();
+      const int64_t tile = t_lo + blockIdx.x + (q / nch) * gridDim.x;
+      const int64_t r = tile * E - D + t;
+      if (t >= D && t < TPB - D) fit_row<D>(ex, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+      __syncthreads();                             // ex is rewritten by the next tile
+    }
   }
+  merge_stats(gs, red, sc.result);
+}
+
+template <int D>
+void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_t gN, int64_t grow0, int64_t t_lo,
+                int64_t t_hi, MrepOut out, MrepScratch sc, int nb, cudaStream_t s) {
+  const size_t smem = TmaCfg<D>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mrep_tma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  mrep_tma_kernel<D><<<nb, TPB, smem, s>>>(tc, scale, m, n, gN, grow0, t_lo, t_hi, out, sc);
 }
 
 // Boundary rows, R16 two-pass centred OLS, one thread per row.
@@ -345,12 +530,6 @@ __global__ void mrep_patch_kernel(int64_t n, int d, MrepOut out, MrepScratch sc)
   if ((threadIdx.x & 31) == 0 && cnt != 0.0) atomicAdd(sc.result + 8, cnt);  // exact integers
 }
 
-// The real entry point (api.cpp): column base pointers + slot order.
-int mrep_blocks(int64_t n, int d) {
-  int64_t t = (n + (TPB - 2 * d) - 1) / (TPB - 2 * d);
-  return (int)(t < kMrepMaxBlocks ? t : kMrepMaxBlocks);
-}
-
 __global__ void mrep_pack_kernel(Cols cols, int m, int64_t n, int d, double* send) {
   // send[0 .. m*d): rows 0..d-1 (for rank-1), send[m*d ..): rows n-d..n-1 (for rank+1), raw
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 2 * m * d; q += gridDim.x * blockDim.x) {
@@ -393,21 +572,60 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
     cols.hhi = mm.comm->rank < mm.comm->nranks - 1 ? mm.recv + cnt : nullptr;
   }
   cudaMemsetAsync(sc.result, 0, 16 * sizeof(double), s);
-  mrep_boundary_kernel<<<1, 64, 0, s>>>(cols, m, n, d, out, sc);
-  const int nb = mrep_blocks(n, d);  // grid-stride over row tiles
-  switch (d) {
-    case 1: mrep_interior_kernel<1><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
-    case 2: mrep_interior_kernel<2><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
-    case 3: mrep_interior_kernel<3><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
-    default: mrep_interior_kernel<4><<<nb, TPB, 0, s>>>(cols, m, n, out, sc); break;
+  mrep_boundary_kernel<<<1, 64, 0, s>>>(cols, m, n, d, out, sc);   // writes result[0..5]
+  // tiles of 256 - 2d emitted rows; [t_lo, t_hi) go to the TMA kernel (their P_x / P_y rows,
+  // widened by one row for 16-byte alignment, lie inside this rank's block)
+  const int64_t E = TPB - 2 * d;
+  const int64_t ntiles = (n + E - 1) / E;
+  int64_t t_lo = 1, t_hi = (n - (TPB + d + 1)) >= 0 ? (n - (TPB + d + 1)) / E + 1 : 0;
+  if (t_hi > ntiles) t_hi = ntiles;
+  // the TMA kernel needs every column's P_x (and P_y) segments to share a 16-byte parity
+  int sxp = -1, syp = -1;
+  bool uniform = true;
+  for (int c = 0; c < m && c < kMaxM; ++c) {
+    const int64_t bx = (int64_t)(((uintptr_t)(px + (int64_t)cols.slot[c] * ld)) >> 3);
+    const int64_t by = (int64_t)(((uintptr_t)(py + (int64_t)cols.slot[c] * ld)) >> 3);
+    const int px_par = (int)(bx & 1), py_par = (int)((by + (E - d)) & 1);   // rows s0-d (even), s0
+    if (sxp < 0) { sxp = px_par; syp = py_par; }
+    uniform = uniform && px_par == sxp && py_par == syp;
+    uniform = uniform && ((((uintptr_t)(px + (int64_t)cols.slot[c] * ld)) & 7) == 0) &&
+              ((((uintptr_t)(py + (int64_t)cols.slot[c] * ld)) & 7) == 0);
+  }
+  if (t_hi < t_lo || m > kMaxM || m % TCB != 0 || !uniform) t_lo = t_hi = ntiles;
+  const int64_t nedge = t_lo + (ntiles - t_hi);
+  if (nedge > 0) {
+    const int nb = (int)(nedge < kMrepMaxBlocks ? nedge : kMrepMaxBlocks);
+    switch (d) {
+      case 1: mrep_interior_kernel<1><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
+      case 2: mrep_interior_kernel<2><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
+      case 3: mrep_interior_kernel<3><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
+      default: mrep_interior_kernel<4><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
+    }
+  }
+  if (t_hi > t_lo) {
+    TmaCols tc;
+    tc.px = px;
+    tc.py = py;
+    tc.ld = ld;
+    tc.sx = sxp;
+    tc.sy = syp;
+    for (int c = 0; c < m; ++c) tc.slot[c] = cols.slot[c];
+    const int64_t nt = t_hi - t_lo;
+    const int nb = (int)(nt < 148 * 2 ? nt : 148 * 2);
+    switch (d) {
+      case 1: launch_tma<1>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
+      case 2: launch_tma<2>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
+      case 3: launch_tma<3>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
+      default: launch_tma<4>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
+    }
   }
   if (multi) {
     // R18 needs the global max |N(i,i)|, R21 the global non-dominant statistics
     if (mm.comm->allreduce(sc.result + 0, 2, 1, s)) return 1;  // max |diag|, max over non-dominant
     if (mm.comm->allreduce(sc.result + 2, 1, 2, s)) return 1;  // min |diag|
     if (mm.comm->allreduce(sc.result + 3, 3, 0, s)) return 1;  // counts
-    mrep_decide_kernel<<<1, 1, 0, s>>>(sc);
   }
+  mrep_decide_kernel<<<1, 1, 0, s>>>(sc);
   int pb = (int)((n + 255) / 256);
   if (pb > 148 * 8) pb = 148 * 8;
   mrep_patch_kernel<<<pb, 256, 0, s>>>(n, d, out, sc);

@@ -8,6 +8,10 @@
 // 126 MB L2), so DRAM sees each array once.
 #include "internal.h"
 
+#ifndef PSP_MARCH_MINB
+#define PSP_MARCH_MINB 3   // resident blocks per SM of the vectorised march kernel
+#endif
+
 namespace psp {
 namespace {
 
@@ -95,6 +99,269 @@ __global__ void __launch_bounds__(128) matvec_kernel(Stencil st, const double* _
   if (xcopy != nullptr) xcopy[g] = xs * xc;
 }
 
+// ------------------------------------------------------------------------------------------
+// 2.5-D marching kernel for 2-D / 3-D grids (the C2-C4 operators).  A block owns a BX x BY
+// tile of the (x, y) plane and marches a chunk of planes along the slab axis (z in 3-D, y in
+// 2-D, where the tile is BX x 1).  The slab-axis neighbours stay in registers (a queue of the
+// planes below / at / above, prefetched two planes ahead), the in-plane neighbours come from a
+// double-buffered shared-memory copy of the plane with its one-point halo ring, so DRAM sees
+// x and the coefficient field once per chunk (+2 halo planes per chunk) and the kernel keeps
+// 2 x 8 B loads per thread in flight for the next two planes.  Arithmetic per point is the
+// same sequence of operations as matvec_kernel (bitwise-identical results).
+// ------------------------------------------------------------------------------------------
+struct MarchView {
+  int64_t nx, ny, nz;        // tile plane nx x ny, march axis nz
+  double s[3], a[3];         // axis 0 = x, 1 = in-plane y (3-D only), 2 = march axis
+  const double* field;
+  const double* x_lo;        // multi-rank halo planes along the march axis (NULL: Dirichlet)
+  const double* x_hi;
+  const double* f_lo;
+  const double* f_hi;
+  int zc;                    // planes per block
+};
+
+template <int KIND, int BX, int BY>
+__global__ void __launch_bounds__(BX * BY, 4) march_matvec_kernel(MarchView v, const double* __restrict__ x,
+                                                              const double* xsp, double* __restrict__ y,
+                                                              double* __restrict__ xcopy) {
+  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  constexpr bool HASY = BY > 1;
+  constexpr int SX = BX + 2, SY = HASY ? BY + 2 : 1;
+  __shared__ double sx[2][SY][SX];
+  __shared__ double sf[2][cell ? SY : 1][cell ? SX : 1];
+  const double* __restrict__ f = v.field;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * BX + tx;
+  const int64_t j = HASY ? (int64_t)blockIdx.y * BY + ty : 0;
+  const int64_t z0 = (int64_t)blockIdx.z * v.zc;
+  const int64_t z1 = (z0 + v.zc < v.nz) ? z0 + v.zc : v.nz;
+  const bool in = i < v.nx && j < v.ny;
+  const int64_t plane = v.nx * v.ny;
+  const int64_t col = i + v.nx * j;          // in-plane index
+  const int sy = HASY ? ty + 1 : 0;
+  // halo duty: x halo for tx == 0 / BX-1, y halo for ty == 0 / BY-1
+  const int hxdir = (tx == 0) ? -1 : (tx == BX - 1 ? 1 : 0);
+  const int hydir = HASY ? ((ty == 0) ? -1 : (ty == BY - 1 ? 1 : 0)) : 0;
+  const bool hx_in = hxdir != 0 && (i + hxdir) >= 0 && (i + hxdir) < v.nx && j < v.ny;
+  const bool hy_in = hydir != 0 && (j + hydir) >= 0 && (j + hydir) < v.ny && i < v.nx;
+  const int64_t hx_col = col + hxdir;
+  const int64_t hy_col = col + hydir * v.nx;
+
+  // march-axis value of x / field at plane p (halo planes beyond the local slab)
+  auto ldx = [&](int64_t p) -> double {
+    if (!in) return 0.0;
+    if (p >= 0 && p < v.nz) return __ldg(x + col + plane * p);
+    if (p < 0 && v.x_lo) return __ldg(v.x_lo + col);
+    if (p >= v.nz && v.x_hi) return __ldg(v.x_hi + col);
+    return 0.0;
+  };
+  auto ldf = [&](int64_t p) -> double {
+    if (!cell || !in) return 0.0;
+    if (p >= 0 && p < v.nz) return __ldg(f + col + plane * p);
+    if (p < 0 && v.f_lo) return __ldg(v.f_lo + col);
+    if (p >= v.nz && v.f_hi) return __ldg(v.f_hi + col);
+    return 0.0;
+  };
+  const bool lo_in = v.x_lo != nullptr;      // a neighbour plane exists below local plane 0
+  const bool hi_in = v.x_hi != nullptr;
+  const double xs = xsp ? *xsp : 1.0;
+
+  double xb = ldx(z0 - 1), xc = ldx(z0), xt = ldx(z0 + 1), xt2 = ldx(z0 + 2);
+  double fb = ldf(z0 - 1), fc = ldf(z0), ft = ldf(z0 + 1), ft2 = ldf(z0 + 2);
+  double hxv = 0.0, hxf = 0.0, hyv = 0.0, hyf = 0.0;   // halo of the current plane
+  if (hx_in && z0 < v.nz) { hxv = __ldg(x + hx_col + plane * z0); if (cell) hxf = __ldg(f + hx_col + plane * z0); }
+  if (hy_in && z0 < v.nz) { hyv = __ldg(x + hy_col + plane * z0); if (cell) hyf = __ldg(f + hy_col + plane * z0); }
+
+  for (int64_t z = z0; z < z1; ++z) {
+    const int b = (int)(z & 1);
+    // prefetch: plane z+3 of the centre column, the halo of plane z+1
+    const double xt3 = ldx(z + 3), ft3 = ldf(z + 3);
+    double nhxv = 0.0, nhxf = 0.0, nhyv = 0.0, nhyf = 0.0;
+    if (z + 1 < z1) {
+      if (hx_in) { nhxv = __ldg(x + hx_col + plane * (z + 1)); if (cell) nhxf = __ldg(f + hx_col + plane * (z + 1)); }
+      if (hy_in) { nhyv = __ldg(x + hy_col + plane * (z + 1)); if (cell) nhyf = __ldg(f + hy_col + plane * (z + 1)); }
+    }
+    // stage plane z
+    sx[b][sy][tx + 1] = xc;
+    if (cell) sf[b][sy][tx + 1] = fc;
+    if (hxdir) {
+      sx[b][sy][tx + 1 + hxdir] = hxv;
+      if (cell) sf[b][sy][tx + 1 + hxdir] = hxf;
+    }
+    if (HASY && hydir) {
+      sx[b][sy + hydir][tx + 1] = hyv;
+      if (cell) sf[b][sy + hydir][tx + 1] = hyf;
+    }
+    __syncthreads();
+    if (in) {
+      double acc = 0.0;  // sum over faces of s_a * k_f * (x_c - x_nb) + upwind terms
+      auto face = [&](double xn, double fn, bool nin, double s) {
+        const double kf = cell ? (nin ? 0.5 * (fc + fn) : fc) : 1.0;
+        acc = fma(s * kf, xc - xn, acc);
+      };
+      {
+        const bool inw = i > 0, ine = i + 1 < v.nx;
+        const double xw = inw ? sx[b][sy][tx] : 0.0, xe = ine ? sx[b][sy][tx + 2] : 0.0;
+        face(xw, cell && inw ? sf[b][sy][tx] : 0.0, inw, v.s[0]);
+        face(xe, cell && ine ? sf[b][sy][tx + 2] : 0.0, ine, v.s[0]);
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], xc - xw, acc);
+      }
+      if (HASY) {
+        const bool ins = j > 0, inn = j + 1 < v.ny;
+        const double xsn = ins ? sx[b][sy - 1][tx + 1] : 0.0, xnn = inn ? sx[b][sy + 1][tx + 1] : 0.0;
+        face(xsn, cell && ins ? sf[b][sy - 1][tx + 1] : 0.0, ins, v.s[1]);
+        face(xnn, cell && inn ? sf[b][sy + 1][tx + 1] : 0.0, inn, v.s[1]);
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], xc - xsn, acc);
+      }
+      {
+        const bool inb = z > 0 || lo_in, int_ = z + 1 < v.nz || hi_in;
+        face(xb, fb, inb, v.s[2]);
+        face(xt, ft, int_, v.s[2]);
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], xc - xb, acc);
+      }
+      const int64_t g = col + plane * z;
+      y[g] = xs * (xc + acc);
+      if (xcopy != nullptr) xcopy[g] = xs * xc;
+    }
+    xb = xc; xc = xt; xt = xt2; xt2 = xt3;
+    fb = fc; fc = ft; ft = ft2; ft2 = ft3;
+    hxv = nhxv; hxf = nhxf; hyv = nhyv; hyf = nhyf;
+  }
+}
+
+// Vectorised, barrier-free variant (the C2-C4 hot path).  Every thread owns two x-adjacent
+// points of one (x, y) line and marches the slab axis: the slab-axis neighbours are a register
+// queue prefetched three planes ahead (16-byte loads), the x neighbours come from the adjacent
+// lanes by warp shuffles (one 8-byte load per tile row for lanes 0 / 31), the in-plane y
+// neighbours are 16-byte loads of the lines j-1 / j+1, which the neighbouring warps of the block
+// load as their own centre lines (L1 / L2 hits), so DRAM sees x and the coefficient field
+// about once.  No shared memory and no barriers: warps run independently.  The domain
+// boundary is folded into the data: a missing neighbour is x = 0 with the centre's
+// coefficient, so every face is w = (s/2)(k_c + k_nb), acc += w (x_c - x_nb) -- for a boundary
+// face (s/2)(2 k_c) = s k_c exactly, the value the scalar kernels use.  Needs nx even and
+// 16-byte aligned vectors (checked at launch; otherwise march_matvec_kernel runs).
+template <int KIND, int BY>
+__global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march3_kernel(MarchView v, const double* __restrict__ x,
+                                                                    const double* xsp, double* __restrict__ y,
+                                                                    double* __restrict__ xcopy) {
+  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  constexpr bool HASY = BY > 1;
+  constexpr int TW = 64;
+  const double* __restrict__ f = v.field;
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * TW + 2 * lane;    // first of this thread's two points
+  const int64_t j = HASY ? (int64_t)blockIdx.y * BY + ty : 0;
+  const int64_t z0 = (int64_t)blockIdx.z * v.zc;
+  const int64_t z1 = (z0 + v.zc < v.nz) ? z0 + v.zc : v.nz;
+  const bool in = i < v.nx && j < v.ny;                     // nx even: both points or none
+  const int64_t plane = v.nx * v.ny;
+  const int64_t col = in ? i + v.nx * j : 0;                 // outside: loads of point 0, no stores
+  const bool has_w = i > 0, has_e = i + 2 < v.nx;
+  const bool has_s = HASY && in && j > 0, has_n = HASY && in && j + 1 < v.ny;
+  const bool lo_in = v.x_lo != nullptr, hi_in = v.x_hi != nullptr;
+  const double xs = xsp ? *xsp : 1.0;
+  const double hs0 = 0.5 * v.s[0], hs1 = 0.5 * v.s[1], hs2 = 0.5 * v.s[2];
+  const double s0c = v.s[0], s1c = v.s[1], s2c = v.s[2];
+
+  auto ld2 = [&](const double* a, const double* lo, const double* hi, int64_t p) -> double2 {
+    if (p >= 0 && p < v.nz) return __ldg(reinterpret_cast<const double2*>(a + col + plane * p));
+    if (p < 0 && lo) return __ldg(reinterpret_cast<const double2*>(lo + col));
+    if (p >= v.nz && hi) return __ldg(reinterpret_cast<const double2*>(hi + col));
+    return make_double2(0.0, 0.0);
+  };
+  const double2 zero2 = make_double2(0.0, 0.0);
+  double2 xb = ld2(x, v.x_lo, v.x_hi, z0 - 1), xc = ld2(x, v.x_lo, v.x_hi, z0);
+  double2 xt = ld2(x, v.x_lo, v.x_hi, z0 + 1), xt2 = ld2(x, v.x_lo, v.x_hi, z0 + 2);
+  double2 fb = zero2, fc = zero2, ft = zero2, ft2 = zero2;
+  if (cell) {
+    fb = ld2(f, v.f_lo, v.f_hi, z0 - 1); fc = ld2(f, v.f_lo, v.f_hi, z0);
+    ft = ld2(f, v.f_lo, v.f_hi, z0 + 1); ft2 = ld2(f, v.f_lo, v.f_hi, z0 + 2);
+  }
+  const double* px3 = x + col + plane * (z0 + 3);
+  const double* pf3 = f + col + plane * (z0 + 3);
+  const double* pxz = x + col + plane * z0;                  // plane z (in-plane neighbour loads)
+  const double* pfz = f + col + plane * z0;
+  double* py = y + col + plane * z0;
+  double* pc = xcopy ? xcopy + col + plane * z0 : nullptr;
+
+  for (int64_t z = z0; z < z1; ++z) {
+    double2 xt3 = zero2, ft3 = zero2;
+    if (z + 3 < v.nz) {
+      xt3 = __ldg(reinterpret_cast<const double2*>(px3));
+      if (cell) ft3 = __ldg(reinterpret_cast<const double2*>(pf3));
+    } else if (z + 3 == v.nz) {
+      xt3 = ld2(x, v.x_lo, v.x_hi, z + 3);
+      if (cell) ft3 = ld2(f, v.f_lo, v.f_hi, z + 3);
+    }
+    // in-plane y neighbours (L1 / L2): missing -> x = 0, k = k_c
+    double2 xsn = zero2, xnn = zero2, fsn = fc, fnn = fc;
+    if (has_s) {
+      xsn = __ldg(reinterpret_cast<const double2*>(pxz - v.nx));
+      if (cell) fsn = __ldg(reinterpret_cast<const double2*>(pfz - v.nx));
+    }
+    if (has_n) {
+      xnn = __ldg(reinterpret_cast<const double2*>(pxz + v.nx));
+      if (cell) fnn = __ldg(reinterpret_cast<const double2*>(pfz + v.nx));
+    }
+    // x neighbours: the adjacent lanes' points; lanes 0 / 31 load across the tile edge
+    double xw = __shfl_up_sync(0xffffffffu, xc.y, 1), xe = __shfl_down_sync(0xffffffffu, xc.x, 1);
+    double fw = 0.0, fe = 0.0;
+    if (cell) {
+      fw = __shfl_up_sync(0xffffffffu, fc.y, 1);
+      fe = __shfl_down_sync(0xffffffffu, fc.x, 1);
+    }
+    if (lane == 0 && in && has_w) { xw = __ldg(pxz - 1); if (cell) fw = __ldg(pfz - 1); }
+    if (lane == 31 && in && has_e) { xe = __ldg(pxz + 2); if (cell) fe = __ldg(pfz + 2); }
+    if (!has_w) { xw = 0.0; fw = fc.x; }
+    if (!has_e) { xe = 0.0; fe = fc.y; }
+    // slab-axis boundary (uniform per block)
+    if (z == 0 && !lo_in) fb = fc;
+    if (z + 1 == v.nz && !hi_in) ft = fc;
+    auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
+                     double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
+      double acc = 0.0;
+      if (cell) {
+        acc = fma(hs0 * (k + fwv), c - xwv, acc);
+        acc = fma(hs0 * (k + fev), c - xev, acc);
+      } else {
+        acc = fma(s0c, c - xwv, acc);
+        acc = fma(s0c, c - xev, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
+      if (HASY) {
+        if (cell) {
+          acc = fma(hs1 * (k + fsv), c - xsv, acc);
+          acc = fma(hs1 * (k + fnv), c - xnv, acc);
+        } else {
+          acc = fma(s1c, c - xsv, acc);
+          acc = fma(s1c, c - xnv, acc);
+        }
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
+      }
+      if (cell) {
+        acc = fma(hs2 * (k + fbv), c - xbv, acc);
+        acc = fma(hs2 * (k + ftv), c - xtv, acc);
+      } else {
+        acc = fma(s2c, c - xbv, acc);
+        acc = fma(s2c, c - xtv, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
+      return xs * (c + acc);
+    };
+    if (in) {
+      double2 out;
+      out.x = point(xc.x, fc.x, xw, fw, xc.y, fc.y, xsn.x, fsn.x, xnn.x, fnn.x, xb.x, fb.x, xt.x, ft.x);
+      out.y = point(xc.y, fc.y, xc.x, fc.x, xe, fe, xsn.y, fsn.y, xnn.y, fnn.y, xb.y, fb.y, xt.y, ft.y);
+      *reinterpret_cast<double2*>(py) = out;
+      if (pc) *reinterpret_cast<double2*>(pc) = make_double2(xs * xc.x, xs * xc.y);
+    }
+    px3 += plane; pf3 += plane; pxz += plane; pfz += plane; py += plane;
+    if (pc) pc += plane;
+    xb = xc; xc = xt; xt = xt2; xt2 = xt3;
+    fb = fc; fc = ft; ft = ft2; ft2 = ft3;
+  }
+}
+
 __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ bands,
                                   const double* __restrict__ x, const double* xsp, double* __restrict__ y,
                                   double* __restrict__ xcopy) {
@@ -112,15 +379,71 @@ __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ 
   }
 }
 
+inline int64_t planes_per_block(int64_t tiles, int64_t nz) {
+  // about 8 resident waves of blocks, at least 16 planes per block (halo re-reads of 2 planes
+  // per chunk <= 12.5%)
+  int64_t zc = (tiles * nz) / (148 * 8 * 8);
+  if (zc < 16) zc = 16;
+  if (zc > nz) zc = nz;
+  if (zc < 1) zc = 1;
+  return zc;
+}
+
+template <int KIND, int BX, int BY>
+void launch_march(const MarchView& v0, const double* x, const double* xs, double* y, double* xcopy,
+                  cudaStream_t s) {
+  MarchView v = v0;
+  const int64_t zc = planes_per_block(((v.nx + BX - 1) / BX) * ((v.ny + BY - 1) / BY), v.nz);
+  v.zc = (int)zc;
+  dim3 grid((unsigned)((v.nx + BX - 1) / BX), (unsigned)((v.ny + BY - 1) / BY),
+            (unsigned)((v.nz + zc - 1) / zc));
+  march_matvec_kernel<KIND, BX, BY><<<grid, dim3(BX, BY), 0, s>>>(v, x, xs, y, xcopy);
+}
+
+template <int KIND, int BY>
+void launch_march2(const MarchView& v0, const double* x, const double* xs, double* y, double* xcopy,
+                   cudaStream_t s) {
+  MarchView v = v0;
+  const int64_t zc = planes_per_block(((v.nx + 63) / 64) * ((v.ny + BY - 1) / BY), v.nz);
+  v.zc = (int)zc;
+  dim3 grid((unsigned)((v.nx + 63) / 64), (unsigned)((v.ny + BY - 1) / BY), (unsigned)((v.nz + zc - 1) / zc));
+  march3_kernel<KIND, BY><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 template <int KIND>
 void launch_kind(const Stencil& st, const double* x, const double* xs, double* y, double* xcopy,
                  cudaStream_t s) {
-  dim3 block(128);
-  dim3 grid((unsigned)((st.nx + 127) / 128), (unsigned)st.ny, (unsigned)st.nz);
-  switch (st.ndim) {
-    case 1: matvec_kernel<KIND, 1><<<grid, block, 0, s>>>(st, x, xs, y, xcopy); break;
-    case 2: matvec_kernel<KIND, 2><<<grid, block, 0, s>>>(st, x, xs, y, xcopy); break;
-    default: matvec_kernel<KIND, 3><<<grid, block, 0, s>>>(st, x, xs, y, xcopy); break;
+  if (st.ndim == 1) {
+    dim3 grid((unsigned)((st.nx + 127) / 128), 1, 1);
+    matvec_kernel<KIND, 1><<<grid, 128, 0, s>>>(st, x, xs, y, xcopy);
+    return;
+  }
+  const bool vec_ok = (st.nx % 2 == 0) && aligned16(x) && aligned16(y) && aligned16(xcopy) &&
+                      aligned16(st.field) && aligned16(st.x_lo) && aligned16(st.x_hi) &&
+                      aligned16(st.f_lo) && aligned16(st.f_hi);
+  MarchView v;
+  v.field = st.field;
+  v.x_lo = st.x_lo;
+  v.x_hi = st.x_hi;
+  v.f_lo = st.f_lo;
+  v.f_hi = st.f_hi;
+  v.zc = 1;
+  v.s[0] = st.s[0];
+  v.a[0] = st.a[0];
+  if (st.ndim == 3) {
+    v.nx = st.nx; v.ny = st.ny; v.nz = st.nz;
+    v.s[1] = st.s[1]; v.a[1] = st.a[1];
+    v.s[2] = st.s[2]; v.a[2] = st.a[2];
+    if (vec_ok) launch_march2<KIND, 8>(v, x, xs, y, xcopy, s);
+    else launch_march<KIND, 32, 8>(v, x, xs, y, xcopy, s);
+  } else {
+    v.nx = st.nx; v.ny = 1; v.nz = st.ny;
+    v.s[1] = 0.0; v.a[1] = 0.0;
+    v.s[2] = st.s[1]; v.a[2] = st.a[1];
+    if (vec_ok) launch_march2<KIND, 1>(v, x, xs, y, xcopy, s);
+    else launch_march<KIND, 256, 1>(v, x, xs, y, xcopy, s);
   }
 }
 

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpspgmres.so")
+# PSP_LIB: tuning experiments only (an alternative build of the same sources)
+LIB_PATH = os.environ.get("PSP_LIB") or os.path.join(_HERE, "libpspgmres.so")
 
 # ---- enums (include/pspgmres.h) ----
 PSP_OK, PSP_E_ARG, PSP_E_DIM, PSP_E_SAMPLES, PSP_E_RANK, PSP_E_SINGULAR, PSP_E_NONFINITE, \

@@ -119,10 +119,28 @@ def test_banded_singular_detected(torch, P):
 # ------------------------------------------------------------------------------------------
 # T3: MREP fit
 # ------------------------------------------------------------------------------------------
-def compare_mrep(g, r, d, n, max_excluded_frac=1e-4):
-    """T3: per row, inf-norm error <= 1e-10 (kappa <= 1e5) else 1e-15 kappa, relative to the
-    row; row kinds and the gate equal.  Rows whose ridge decision (kappa_est vs 1e12, R17) is
-    within x2 of the threshold on either side are excluded and counted."""
+def gram_cond2(px, d):
+    """kappa_2 of every interior row's Gram G_i = X* X*^T, X* = [1; P_x(i-d..i+d, :)],
+    formed in numpy from the probes (0 for boundary rows)."""
+    px = np.asarray(px)
+    m, n = px.shape
+    out = np.zeros(n)
+    if n <= 2 * d:
+        return out
+    rows = np.arange(d, n - d)[:, None] + np.arange(-d, d + 1)[None, :]          # (ni, 2d+1)
+    X = np.concatenate([np.ones((len(rows), 1, m)), px[:, rows].transpose(1, 2, 0)], axis=1)
+    sv = np.linalg.svd(X @ X.transpose(0, 2, 1), compute_uv=False)
+    with np.errstate(divide="ignore"):
+        out[d:n - d] = np.where(sv[:, -1] > 0, sv[:, 0] / sv[:, -1], np.inf)
+    return out
+
+
+def compare_mrep(g, r, d, n, px, max_excluded_frac=1e-4):
+    """T3: per row, inf-norm error relative to the row <= 1e-10 when kappa_2(G_i) <= 1e5, else
+    <= 8 P u kappa_2(G_i) (each side within the Cholesky forward-error bound 4 P u kappa_2 of
+    the normal equations, T3); row kinds and the gate equal.  Rows whose ridge decision
+    (kappa_est vs 1e12, R17) is within x2 of the threshold on either side are excluded and
+    counted."""
     bands = g["bands"].cpu().numpy()
     kind = g["row_kind"].cpu().numpy()
     kg = g["kappa_est"].cpu().numpy()
@@ -137,8 +155,10 @@ def compare_mrep(g, r, d, n, max_excluded_frac=1e-4):
     ok = ~near & (kind != 1)          # ridged rows: the ridge solution itself is compared below
     scale = np.maximum(np.abs(r["bands"]).max(axis=0), 1e-300)
     err = np.abs(bands - r["bands"]).max(axis=0) / scale
-    kfin = np.where(np.isfinite(kap), kap, 1e300)
-    tol = np.maximum(np.where(kap <= 1e5, 1e-10, 1e-15 * kfin), 1e-10)
+    k2 = gram_cond2(px, d)
+    P_ = 2 * d + 2
+    tol = np.where(k2 <= 1e5, 1e-10, 8 * P_ * 2.0 ** -53 * np.where(np.isfinite(k2), k2, 1e300))
+    tol = np.maximum(tol, 1e-10)
     assert np.all(err[ok] <= tol[ok]), (np.max(err[ok] / tol[ok]), np.nonzero(ok)[0][np.argmax(err[ok] / tol[ok])])
     ridged = ~near & (kind == 1)
     if ridged.any():   # ridge-regularised system: kappa <= ~1e12 -> attainable 1e-15 * 1e12
@@ -154,7 +174,7 @@ def test_mrep_parity_c5(torch, P, orc, d, n, m):
     g5 = inputs.c5_numpy(n, m, d, seed=7)
     r = orc.mrep(g5["px"], g5["py"], d)
     g = P.psp_mrep_fit_raw(dev(torch, g5["px"]), dev(torch, g5["py"]), d)
-    compare_mrep(g, r, d, n)
+    compare_mrep(g, r, d, n, g5["px"])
     assert g["gate_accepted"]
     icpt = g["intercept"].cpu().numpy()
     assert np.max(np.abs(icpt - r["intercept"])) <= 1e-9
@@ -172,7 +192,7 @@ def test_mrep_ring_order_and_noiseless_recovery(torch, P, orc):
     order = list(np.random.default_rng(0).permutation(m))
     r = orc.mrep(px, py, d, order=order)
     g = P.psp_mrep_fit_raw(dev(torch, px), dev(torch, py), d, order=order)
-    compare_mrep(g, r, d, n)
+    compare_mrep(g, r, d, n, px)
     b = g["bands"].cpu().numpy()
     assert np.max(np.abs(b[:, d:n - d] - g5["bands"][:, d:n - d])) <= 1e-10 * np.abs(g5["bands"]).max()
 
@@ -315,7 +335,7 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, mode):
             # dependent (kappa(Gram) up to 1e16), so the unridged/ridged decision of those rows
             # is decided by rounding; they are excluded from the kind/coefficient comparison
             # (every excluded row has kappa_est > 1e9 on one side, by construction)
-            compare_mrep(g, o, prob.d, n, max_excluded_frac=1.0)
+            compare_mrep(g, o, prob.d, n, px, max_excluded_frac=1.0)
             assert o["gate_accepted"] == r["mrep"]["gate_accepted"]
         u = r["u"]
     ctx.close()
