@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=512, help="grid points per axis (512 = C4)")
     ap.add_argument("--ortho", default="1reduce", choices=["1reduce", "literal"])
+    ap.add_argument("--fused", type=int, default=0, help="1: single-pass fused Arnoldi step (N = I)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-size", type=int, default=128)
@@ -194,7 +195,7 @@ def main():
     t_gen = time.perf_counter() - t_gen
     n = prob.op.rows
     ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
-    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2)
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2, fused=args.fused)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=stream)
@@ -306,7 +307,7 @@ def main():
             "config": {"workload": f"C4: 3-D variable-kappa diffusion {args.size}^3 (BASELINE configs[3]), "
                                    "one implicit-Euler PSP-GMRES time step (solve + MREP fit + gate + factor)",
                        "grid": [args.size] * 3, "n": n, "d": prob.d, "restart": prob.restart, "tol": prob.tol,
-                       "m_max": prob.m_max, "ortho": args.ortho, "dt": prob.op.dt,
+                       "m_max": prob.m_max, "ortho": args.ortho + ("-fused" if args.fused else ""), "dt": prob.op.dt,
                        "l2": "inputs larger than L2 (each vector 8n bytes >> 126 MB); no flush needed",
                        "parallelism": "replicas" if world > 1 else "single"},
             "iterations_per_step": [r["iterations"] for r in reps],

@@ -693,8 +693,9 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   if (c->cycle_fused && beta > 0.0 && isfinite(beta)) {
     // cycle-start pass: A V(:,1) -> P_y of the next slot and step 1's MGS coefficient
     h = kt_begin(c);
-    launch_fused(c->st, basis(c), 0, c->nA, v1, nullptr, py_col(c, c->vslot[1]), c->slot_scale,
-                 c->vslot[1], c->ds, c->stream);
+    const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, 0, c->nA, c->vslot[1], 1,
+                                nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream);
+    if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
     kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
     c->launches += 1;
   }
@@ -719,8 +720,9 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
       const int dst = ring_peek(c);
       c->vslot[k + 1] = dst;
       h = kt_begin(c);
-      launch_fused(c->st, basis(c), k, c->nA, py_col(c, slot), px_col(c, dst), py_col(c, dst),
-                   c->slot_scale, dst, c->ds, c->stream);
+      const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, slot, 0,
+                                  px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream);
+      if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
       kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
     } else {
       // the last step of the cycle: only H(k+1,k) = ||U|| is needed (V(:,k+1) is never used)

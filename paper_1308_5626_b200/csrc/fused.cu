@@ -13,13 +13,20 @@
 // Bytes per row and step: k basis columns + w~_k + kappa read, u + w~ written = 8(k+4), against
 // 8(2k+7) for separate matvec / dots / update passes.
 //
-// Work layout: a block owns a TX x TY column of the grid and marches a chunk of planes along the
-// slowest axis (2-D grids march y, 1-D grids are a single line).  Every thread owns one point of
-// the tile plus its one-point halo ring (TX*TY interior threads + NH halo threads): per plane it
-// issues all its loads at once (the k basis values, w~_k and kappa) and computes U at its point;
-// the halo is recomputed from the L2-resident basis instead of exchanged.  Then w~ = A u on the
-// previous plane from three U planes in shared memory, and that plane's dot products against
-// V_j(p-1), which the interior threads parked in shared memory (Vsave) one plane earlier.
+// Work layout: a block of TX x TY threads owns a TX x TY tile of the (x, y) plane (3-D: 32 x 16
+// or 32 x 8; 2-D / 1-D: 256 x 1) and marches a chunk of planes along the slowest axis.  One
+// thread = one point.  Tiles overlap: threads on the tile edge compute u at their point (the
+// stencil halo) but emit nothing, so no block ever waits for another (in x the tile starts two
+// points before its interior: a TMA box's inner start must be 16-byte aligned).  Operands arrive by TMA: one elected thread issues, per plane, a tensor-tile load
+// (cp.async.bulk.tensor, 4-D map over the probe ring: x, y, plane, slot) for each of the k basis
+// columns, for w~_k and for kappa into a 3-deep ring of shared-memory stages (planes p, p+1,
+// p+2 resident), completion on one mbarrier per stage; out-of-grid boxes are zero-filled by the
+// TMA unit, which is exactly the Dirichlet extension u = 0.  Per plane p: u(p+1) from stage p+1
+// (and the l_j = V_j'u products), w~(p) = A u(p) from u(p-1), u(p+1) in registers and the
+// in-plane neighbours of plane p in shared memory (one barrier per plane), t_j = V_j(p)'w~(p)
+// from stage p; then stage p is refilled with plane p+3.  Registers hold only the
+// accumulators, so HBM streams while the block computes.
+#include <cuda.h>
 #include <math.h>
 
 #include "givens.cuh"
@@ -28,40 +35,19 @@
 namespace psp {
 namespace {
 
-template <int TX, int TY>
-struct Tile {
-  static constexpr bool HASY = TY > 1;               // y halo rows (3-D tiles)
-  static constexpr int HX = TX + 2, HY = HASY ? TY + 2 : TY, HP = HX * HY;
-  static constexpr int NI = TX * TY;                 // interior points
-  static constexpr int NH = HP - NI;                 // halo points
-  static constexpr int THREADS = ((NI + NH + 31) / 32) * 32;
-  // interior point i -> halo-tile index
-  __device__ static int interior_h(int i) { return (i / TX + (HASY ? 1 : 0)) * HX + (i % TX + 1); }
-  // halo point h -> halo-tile coordinates
-  __device__ static void halo_xy(int h, int& hx, int& hy) {
-    if (!HASY) { hx = (h == 0) ? 0 : HX - 1; hy = 0; return; }
-    if (h < HX) { hx = h; hy = 0; return; }
-    h -= HX;
-    if (h < HX) { hx = h; hy = HY - 1; return; }
-    h -= HX;
-    if (h < TY) { hx = 0; hy = 1 + h; return; }
-    h -= TY;
-    hx = HX - 1;
-    hy = 1 + h;
-  }
-};
-
 struct FusedArgs {
   Stencil st;          // 3-D view (1-D / 2-D mapped to nx x 1 x nz)
-  Basis V;             // V(:,1..k) (raw, scales ds.alpha)
   int k;               // step being finished; 0 = cycle-start pass (u = src, no update)
   int nA;
-  const double* src;   // w~_k (raw, scale ds.alpha[k-1]); k = 0: V_1 raw (R_bar)
+  int vs1, cap;        // V(:,j+1) = ring P_x slot (vs1 + j) % cap
+  int src_slot;        // w~_k: ring P_y slot (k = 0: V_1 = ring P_x slot)
+  int src_px;          // 1: src lives in the P_x ring
   double* dstx;        // u -> ring P_x slot of step k+1 (unused when k = 0)
   double* dsty;        // w~ -> ring P_y slot of step k+1
   double* slot_scale;  // per-slot probe scale
   int dst_slot;
-  int zchunk;          // planes per block along the march axis
+  int zchunk;          // planes per tile along the march axis
+  int64_t tiles_x, tiles_y, ntiles;
   DevState ds;
 };
 
@@ -71,206 +57,308 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Transposing butterfly: v[0..7] per lane -> returns, in every lane l, the sum over the warp of
+// v[l & 7] (9 double shuffles for 8 values).
+__device__ __forceinline__ double butterfly8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int m = 4, h = 4; m >= 1; m >>= 1, h >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? v[j] : v[j + h];
+      const double keep = up ? v[j + h] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  double r = v[0];
+  r += __shfl_xor_sync(0xffffffffu, r, 8);
+  r += __shfl_xor_sync(0xffffffffu, r, 16);
+  return r;
+}
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// 4-D tensor tile (x, y, plane, slot) -> shared memory, completion on bar
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int x, int y, int z, int sl, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(sl), "r"(su32(bar))
+      : "memory");
+}
+
+template <int TX, int TY, int KMAX>
+struct FCfg {
+  static constexpr int NT = TX * TY;
+  static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
+  static constexpr int STAGE = NB * NT;                      // doubles
+  // as many stages as fit in 225 KB (planes p and p+1 are resident, the rest are in flight)
+  static constexpr int NSTF = (int)((225 * 1024 - 2 * NT * 8 - 256) / (STAGE * 8));
+  static constexpr int NST = NSTF > 6 ? 6 : NSTF;
+  static_assert(NST >= 3, "a stage ring needs planes p, p+1 and one in flight");
+  static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)2 * NT * 8 + 64 + 128;
+};
+
 template <int KIND, int TX, int TY, int KMAX>
-__global__ void __launch_bounds__(Tile<TX, TY>::THREADS, (KMAX <= 16 ? 2 : 1)) fused_arnoldi_kernel(FusedArgs a) {
-  using T = Tile<TX, TY>;
-  constexpr int HX = T::HX, HP = T::HP, NI = T::NI, NH = T::NH, NT = T::THREADS;
-  constexpr int YOFF = T::HASY ? HX : 0;             // halo-tile stride of a y step
+__global__ void __launch_bounds__(TX * TY, 1)
+    fused_tma_kernel(const __grid_constant__ CUtensorMap mpx, const __grid_constant__ CUtensorMap mpy,
+                     const __grid_constant__ CUtensorMap mkap, FusedArgs a) {
+  using Cfg = FCfg<TX, TY, KMAX>;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
-  constexpr int NW = NT / 32;
-  constexpr int JPW = (KMAX + NW - 1) / NW;  // basis vectors per warp in the dot phase
-  extern __shared__ double smem[];
-  double* Up = smem;                 // [3][HP]  u planes (ring)
-  double* Kp = Up + 3 * HP;          // [3][HP]  kappa planes (cell kinds)
-  double* Wt = Kp + 3 * HP;          // [NI]     w~ of the previous plane (interior)
-  double* Vsave = Wt + NI;           // [KMAX][NI] V_j of the previous plane (interior)
+  constexpr bool HASY = TY > 1;
+  constexpr int NT = Cfg::NT, NW = NT / 32, NST = Cfg::NST;
+  constexpr bool REG = KMAX <= 16;           // per-thread accumulators (else per-plane butterflies)
+  constexpr int NCH = (KMAX + 7) / 8;
+  constexpr int NACC = REG ? KMAX : NCH;
+  extern __shared__ __align__(128) double fsm[];
+  // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
+  double* stages = fsm + (((128u - (su32(fsm) & 127u)) & 127u) >> 3);
+  double* Us = stages + NST * Cfg::STAGE;    // [2][NT] u of planes p, p+1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Us + 2 * NT);
   __shared__ double hs[KMAX];
-  __shared__ const double* colp[KMAX];   // V(:,j) base pointers (ring slots resolved once)
-  __shared__ double accs[2 * KMAX + 2];
-  __shared__ double red[NW][2];
+  __shared__ int vslot[KMAX];
   __shared__ double tot[2 * KMAX + 2];
   __shared__ bool s_last;
 
   const Stencil& st = a.st;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int lx = threadIdx.x, ly = threadIdx.y, t = ly * TX + lx, lane = t & 31, warp = t >> 5;
   const int k = a.k;
   const int ld = a.nA + 1;
-  if (t < k) hs[t] = a.ds.H[(int64_t)(k - 1) * ld + t] * a.ds.alpha[t];
-  if (t < KMAX) colp[t] = (t < k) ? a.V.col(t) : a.src;
+  if (t < KMAX) {
+    hs[t] = (t < k) ? a.ds.H[(int64_t)(k - 1) * ld + t] * a.ds.alpha[t] : 0.0;
+    vslot[t] = (a.vs1 + t) % a.cap;
+  }
+  // columns j >= k are never loaded: zero them once in every stage (coefficient 0, product 0)
+  for (int s = 0; s < NST; ++s)
+    for (int j = k; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + t] = 0.0;
+  if (t == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(bars + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mpx)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mpy)) : "memory");
+    if (cell) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mkap)) : "memory");
+  }
   const double wsc = (k >= 1) ? a.ds.alpha[k - 1] : 1.0;
   __syncthreads();
 
-  // tile position
-  const int64_t tiles_x = (st.nx + TX - 1) / TX;
-  const int64_t tiles_y = (st.ny + TY - 1) / TY;
-  int64_t b = blockIdx.x;
-  const int64_t tx_i = b % tiles_x;
-  b /= tiles_x;
-  const int64_t ty_i = b % tiles_y;
-  const int64_t zc_i = b / tiles_y;
-  const int64_t x0 = tx_i * TX, y0 = ty_i * TY;
-  const int64_t z0 = zc_i * a.zchunk;
-  const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
+  const int nload = (k == 0 ? 0 : k) + 1 + (cell ? 1 : 0);
+  const unsigned stage_bytes = (unsigned)(nload * NT * 8);
+  unsigned phase_bits = 0;                   // parity of each stage's next completion
 
-  // this thread's point: interior (t < NI) or halo (NI <= t < NI + NH)
-  const bool interior = t < NI;
-  const bool active = t < NI + NH;
-  int hx = 0, hy = 0, hidx = 0;
-  if (interior) {
-    hidx = T::interior_h(t);
-    hx = t % TX + 1;
-    hy = t / TX + (T::HASY ? 1 : 0);
-  } else if (active) {
-    T::halo_xy(t - NI, hx, hy);
-    hidx = hy * HX + hx;
-  }
-  const int64_t gx = x0 - 1 + hx, gy = y0 + hy - (T::HASY ? 1 : 0);
-  const bool in_grid = active && gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
-  const int64_t gcol = gx + st.nx * gy;   // index within a plane
-
-  double nu = 0.0, tu = 0.0;          // u'u and u'w~ over this thread's interior points
-  double at[JPW], al[JPW];            // t_j and l_j partials for the warp's basis vectors
+  double accl[NACC], acct[NACC];
 #pragma unroll
-  for (int q = 0; q < JPW; ++q) { at[q] = 0.0; al[q] = 0.0; }
+  for (int c = 0; c < NACC; ++c) { accl[c] = 0.0; acct[c] = 0.0; }
+  double nu = 0.0, tu = 0.0;
+  const double hsx = 0.5 * st.s[0], hsy = 0.5 * st.s[1], hsz = 0.5 * st.s[2];
   const int64_t plane = st.nx * st.ny;
 
-  const int64_t p_begin = (z0 > 0) ? z0 - 1 : 0;
-  for (int64_t p = p_begin; p <= z1; ++p) {
-    const bool have_p = p < st.nz;               // U(p) exists (else Dirichlet 0 beyond the grid)
-    const int slot = (int)(p % 3);
-    double vr[KMAX];
-    // ---- U(p) at this thread's point: every load of the plane issued together ----
-    if (have_p && active) {
-      double u = 0.0;
-      if (in_grid) {
-        const int64_t g = gcol + plane * p;
-        const double s0 = __ldg(a.src + g);
-        if (cell) Kp[slot * HP + hidx] = __ldg(st.field + g);
-        if (k == 0) {
-          u = s0;
-        } else {
+  auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, double f, double (&acc)[NACC]) {
+    if (REG) {
 #pragma unroll
-          for (int j = 0; j < KMAX; ++j) vr[j] = (j < k) ? __ldg(colp[j] + g) : 0.0;
-          u = wsc * s0;
+      for (int j = 0; j < KMAX; ++j) acc[j] = fma(vcol[j * NT + t], f, acc[j]);
+    } else {
 #pragma unroll
-          for (int j = 0; j < KMAX; ++j)
-            if (j < k) u = fma(-hs[j], vr[j], u);
-        }
-        if (interior && p >= z0 && p < z1) {
-          if (k > 0) a.dstx[g] = u;
-          nu = fma(u, u, nu);
+      for (int c = 0; c < NCH; ++c) {
+        if (c * 8 >= k) break;                   // uniform
+        double v8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v8[q] = vcol[(c * 8 + q) * NT + t] * f;
+        acc[c] += butterfly8(v8, lane);
+      }
+    }
+  };
+
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    int64_t b = tile;
+    const int64_t txi = b % a.tiles_x;
+    b /= a.tiles_x;
+    const int64_t tyi = b % a.tiles_y;
+    const int64_t zci = b / a.tiles_y;
+    // the box's inner start must be 16-byte aligned: x0 even, halo lanes 1 and TX-2
+    const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
+    const int64_t z0 = zci * a.zchunk;
+    const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
+    const int64_t gx = x0 + lx, gy = y0 + ly;
+    const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
+    const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
+    const bool own = interior && in_grid;
+    const int64_t col = in_grid ? gx + st.nx * gy : 0;
+    const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
+
+    // stage of plane q (q from z0-1): (q - z0 + 1) % NST
+    // warp 0: the boxes of plane q, one box per lane (lane 0 arms the barrier with the byte count)
+    auto issue = [&](int64_t q) {
+      const int si = (int)((q - z0 + 1) % NST);
+      double* sb = stages + (size_t)si * Cfg::STAGE;
+      const int zq = (int)q;                     // may be -1 or nz: zero-filled by the TMA unit
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0) mbar_expect_tx(bars + si, stage_bytes);
+      for (int j = lane; j < nload; j += 32) {
+        if (j < (k > 0 ? k : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], bars + si);
+        else if (j == (k > 0 ? k : 0)) tma4(sb + KMAX * NT, a.src_px ? &mpx : &mpy, x0, y0, zq, a.src_slot, bars + si);
+        else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, bars + si);
+      }
+    };
+    auto wait_stage = [&](int64_t q) -> const double* {
+      const int si = (int)((q - z0 + 1) % NST);
+      mbar_wait(bars + si, (phase_bits >> si) & 1u);
+      phase_bits ^= (1u << si);
+      return stages + (size_t)si * Cfg::STAGE;
+    };
+    auto form_u = [&](const double* sb) -> double {   // u at this thread's point of the staged plane
+      const double s0 = sb[KMAX * NT + t];
+      if (k == 0) return s0;
+      double u = wsc * s0;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) u = fma(-hs[j], sb[j * NT + t], u);
+      return u;
+    };
+
+    if (warp == 0)
+      for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
+    // prologue: u(z0-1), u(z0) (+ l-products of plane z0)
+    const double* sbm = wait_stage(z0 - 1);
+    double ub = (z0 >= 1 && in_grid) ? form_u(sbm) : 0.0;
+    double kb = cell ? sbm[(KMAX + 1) * NT + t] : 0.0;
+    const double* sbc = wait_stage(z0);
+    double uc = in_grid ? form_u(sbc) : 0.0;
+    double kc = cell ? sbc[(KMAX + 1) * NT + t] : 0.0;
+    if (own && k > 0) a.dstx[col + plane * z0] = uc;
+    {
+      const double f = own ? uc : 0.0;
+      nu = fma(f, f, nu);
+      if (k > 0) add_products(sbc, f, accl);
+    }
+    Us[(z0 & 1) * NT + t] = uc;
+    __syncthreads();                              // stage z0-1 consumed; Us(z0) visible
+    if (warp == 0 && z0 - 1 + NST <= z1) issue(z0 - 1 + NST);
+
+    for (int64_t p = z0; p < z1; ++p) {
+      const int bp = (int)(p & 1), bn = bp ^ 1;
+      const int64_t pn = p + 1;
+      // stage p (resident: t-dots, in-plane kappa), stage p+1 (u(p+1))
+      const double* sp = stages + (size_t)((p - z0 + 1) % NST) * Cfg::STAGE;
+      double un = 0.0, kt = 0.0;
+      if (pn <= z1) {                             // plane z1 (halo above the chunk) was loaded too
+        const double* sn = wait_stage(pn);
+        un = (pn < st.nz && in_grid) ? form_u(sn) : 0.0;
+        kt = cell ? sn[(KMAX + 1) * NT + t] : 0.0;
+        if (pn < z1) {
+          if (own && k > 0) a.dstx[col + plane * pn] = un;
+          const double f = own ? un : 0.0;
+          nu = fma(f, f, nu);
+          if (k > 0) add_products(sn, f, accl);
         }
       }
-      Up[slot * HP + hidx] = u;
-    }
-    __syncthreads();
-    // ---- w~ = A u on plane q = p-1 ----
-    const int64_t q = p - 1;
-    const bool do_q = (q >= z0) && (q < z1);
-    if (do_q && interior) {
-      const int qs = (int)(q % 3);
+      // w~ = A u at plane p
       double w = 0.0;
-      if (in_grid) {
-        const double* Uq = Up + qs * HP;
-        const double* Kq = Kp + qs * HP;
-        const double xc = Uq[hidx];
-        const double fc = cell ? Kq[hidx] : 0.0;
+      if (own) {
+        const double c0 = uc;
         double acc = 0.0;
-        auto face = [&](double xn, double fn, bool inside, double s) {
-          const double kf = cell ? (inside ? 0.5 * (fc + fn) : fc) : 1.0;
-          acc = fma(s * kf, xc - xn, acc);
+        const double* Up = Us + bp * NT;
+        const double* Kp = sp + (KMAX + 1) * NT;
+        auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
+          const double kf = cell ? (nin ? hsv * (kc + fn) : s * kc) : s;
+          acc = fma(kf, c0 - (nin ? xn : 0.0), acc);
         };
-        {  // x neighbours
-          const bool inw = gx > 0, ine = gx + 1 < st.nx;
-          const double xw = Uq[hidx - 1], xe = Uq[hidx + 1];
-          face(xw, cell ? Kq[hidx - 1] : 0.0, inw, st.s[0]);
-          face(xe, cell ? Kq[hidx + 1] : 0.0, ine, st.s[0]);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], xc - xw, acc);
+        const double xw = Up[t - 1], xe = Up[t + 1];
+        face(xw, cell ? Kp[t - 1] : 0.0, nb_w, st.s[0], hsx);
+        face(xe, cell ? Kp[t + 1] : 0.0, nb_e, st.s[0], hsx);
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - (nb_w ? xw : 0.0), acc);
+        if (HASY) {
+          const double xs_ = Up[t - TX], xn_ = Up[t + TX];
+          face(xs_, cell ? Kp[t - TX] : 0.0, nb_s, st.s[1], hsy);
+          face(xn_, cell ? Kp[t + TX] : 0.0, nb_n, st.s[1], hsy);
+          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - (nb_s ? xs_ : 0.0), acc);
         }
-        if (T::HASY) {  // y neighbours
-          const bool ins = gy > 0, inn = gy + 1 < st.ny;
-          const double xs = Uq[hidx - YOFF], xn = Uq[hidx + YOFF];
-          face(xs, cell ? Kq[hidx - YOFF] : 0.0, ins, st.s[1]);
-          face(xn, cell ? Kq[hidx + YOFF] : 0.0, inn, st.s[1]);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], xc - xs, acc);
+        if (st.nz > 1) {
+          const bool inb = p > 0, int_ = p + 1 < st.nz;
+          face(ub, kb, inb, st.s[2], hsz);
+          face(un, kt, int_, st.s[2], hsz);
+          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - (inb ? ub : 0.0), acc);
         }
-        if (st.nz > 1) {  // z neighbours (the march axis)
-          const bool inb = q > 0, int_ = q + 1 < st.nz;
-          const int sb = (int)((q + 2) % 3), stp = (int)((q + 1) % 3);
-          const double xb = inb ? Up[sb * HP + hidx] : 0.0;
-          const double xt = int_ ? Up[stp * HP + hidx] : 0.0;
-          face(xb, cell && inb ? Kp[sb * HP + hidx] : 0.0, inb, st.s[2]);
-          face(xt, cell && int_ ? Kp[stp * HP + hidx] : 0.0, int_, st.s[2]);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], xc - xb, acc);
-        }
-        w = xc + acc;
-        a.dsty[gcol + plane * q] = w;
-        tu = fma(xc, w, tu);
+        w = c0 + acc;
+        a.dsty[col + plane * p] = w;
+        tu = fma(c0, w, tu);
       }
-      Wt[t] = w;
+      if (k > 0) add_products(sp, w, acct);       // t_j = V_j(p)' w~(p); w = 0 off emitted points
+      Us[bn * NT + t] = un;
+      __syncthreads();                            // stage p consumed; Us(p+1) visible
+      if (warp == 0 && p + NST <= z1) issue(p + NST);
+      ub = uc; uc = un;
+      kb = kc; kc = kt;
     }
-    __syncthreads();
-    // ---- dots of plane q against V_j(q) (parked in Vsave one plane ago) ----
-    if (do_q && k > 0) {
-      const double* Uq = Up + (int)(q % 3) * HP;
-#pragma unroll
-      for (int jj = 0; jj < JPW; ++jj) {
-        const int j = warp + NW * jj;
-        if (j < k) {
-          const double* vs = Vsave + (int64_t)j * NI;
-          double s1 = 0.0, s2 = 0.0;
-          for (int pt = lane; pt < NI; pt += 32) {
-            const double v = vs[pt];
-            s1 = fma(v, Wt[pt], s1);
-            s2 = fma(v, Uq[T::interior_h(pt)], s2);
-          }
-          at[jj] += s1;
-          al[jj] += s2;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- park V_j(p) for the next plane's dots ----
-    if (have_p && k > 0 && interior && p >= z0 && p < z1) {
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j)
-        if (j < k) Vsave[(int64_t)j * NI + t] = in_grid ? vr[j] : 0.0;
-    }
+    // drain: every issued stage has been waited on (planes z0-1 .. z1), so the barriers'
+    // parities stay in step for the next tile
   }
 
-  // ---- block reduction: [t_0..t_{k-1}, l_0..l_{k-1}, t_u, nu] ----
+  // REG: reduce every accumulator across the warp once
+  double outl[NCH], outt[NCH];
+  if (REG) {
 #pragma unroll
-  for (int jj = 0; jj < JPW; ++jj) {
-    const int j = warp + NW * jj;
-    const double s1 = warp_sum(at[jj]);
-    const double s2 = warp_sum(al[jj]);
-    if (lane == 0 && j < k) {
-      accs[j] = s1;
-      accs[KMAX + j] = s2;
+    for (int c = 0; c < NCH; ++c) {
+      double v8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = (c * 8 + q < NACC) ? accl[c * 8 + q] : 0.0;
+      outl[c] = butterfly8(v8, lane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = (c * 8 + q < NACC) ? acct[c * 8 + q] : 0.0;
+      outt[c] = butterfly8(v8, lane);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      outl[c] = accl[c];
+      outt[c] = acct[c];
+    }
+  }
+  // ---- block reduction: [t_0..t_{k-1}, l_0..l_{k-1}, t_u, nu]; the stages are free now ----
+  __syncthreads();
+  double* accs = stages;                          // [NW][2 KMAX + 2]
+  constexpr int AW = 2 * KMAX + 2;
+  if (lane < 8) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int j = c * 8 + lane;
+      if (j < KMAX) {
+        accs[warp * AW + j] = outt[c];
+        accs[warp * AW + KMAX + j] = outl[c];
+      }
     }
   }
   nu = warp_sum(nu);
   tu = warp_sum(tu);
   if (lane == 0) {
-    red[warp][0] = tu;
-    red[warp][1] = nu;
+    accs[warp * AW + 2 * KMAX] = tu;
+    accs[warp * AW + 2 * KMAX + 1] = nu;
   }
   __syncthreads();
   const int nv = 2 * k + 2;
   const int nb = gridDim.x;
-  if (t == 0) {
-    double s_tu = 0.0, s_nu = 0.0;
-    for (int w = 0; w < NW; ++w) {
-      s_tu += red[w][0];
-      s_nu += red[w][1];
-    }
-    accs[2 * KMAX] = s_tu;
-    accs[2 * KMAX + 1] = s_nu;
-  }
-  __syncthreads();
   for (int v = t; v < nv; v += NT) {
-    const double val = (v < k) ? accs[v] : (v < 2 * k ? accs[KMAX + v - k] : accs[2 * KMAX + (v - 2 * k)]);
-    a.ds.partials[(int64_t)v * nb + blockIdx.x] = val;
+    const int src = (v < k) ? v : (v < 2 * k ? KMAX + v - k : 2 * KMAX + (v - 2 * k));
+    double sum = 0.0;
+    for (int w2 = 0; w2 < NW; ++w2) sum += accs[w2 * AW + src];
+    a.ds.partials[(int64_t)v * nb + blockIdx.x] = sum;
   }
   __threadfence();
   __syncthreads();
@@ -282,12 +370,11 @@ __global__ void __launch_bounds__(Tile<TX, TY>::THREADS, (KMAX <= 16 ? 2 : 1)) f
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // totals in a fixed order (one warp per value)
-  for (int v = warp; v < nv; v += NW) {
-    double s = 0.0;
-    for (int bb = lane; bb < nb; bb += 32) s += ((volatile double*)a.ds.partials)[(int64_t)v * nb + bb];
-    s = warp_sum(s);
-    if (lane == 0) tot[v] = s;
+  for (int v = warp; v < nv; v += NW) {          // totals in a fixed order (one warp per value)
+    double sum = 0.0;
+    for (int bb = lane; bb < nb; bb += 32) sum += ((volatile double*)a.ds.partials)[(int64_t)v * nb + bb];
+    sum = warp_sum(sum);
+    if (lane == 0) tot[v] = sum;
   }
   __syncthreads();
   if (t != 0) return;
@@ -316,43 +403,95 @@ __global__ void __launch_bounds__(Tile<TX, TY>::THREADS, (KMAX <= 16 ? 2 : 1)) f
   }
 }
 
-template <int TX, int TY>
-int zchunk_for(const Stencil& st) {
-  const int64_t tiles = ((st.nx + TX - 1) / TX) * ((st.ny + TY - 1) / TY);
-  int64_t zc = tiles * st.nz / (148 * 8);   // ~8 waves of one block per SM
-  if (zc > 128) zc = 128;
-  if (zc < 8) zc = 8;
-  if (zc > st.nz) zc = st.nz;
-  return (int)zc;
+// ---- tensor maps (driver entry point fetched through the runtime: no -lcuda) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
 }
+
+// 4-D map (x, y, plane, slot) over nslots columns of n doubles at base; box TX x TY x 1 x 1
+int g_map_err = 0;   // last cuTensorMapEncodeTiled result (diagnostics)
+bool make_map(CUtensorMap* m, const double* base, const Stencil& st, int nslots, int TX, int TY) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) { g_map_err = -1; return false; }
+  cuuint64_t dims[4] = {(cuuint64_t)st.nx, (cuuint64_t)st.ny, (cuuint64_t)st.nz, (cuuint64_t)nslots};
+  cuuint64_t strides[3] = {(cuuint64_t)st.nx * 8, (cuuint64_t)(st.nx * st.ny) * 8,
+                           (cuuint64_t)(st.nx * st.ny * st.nz) * 8};
+  cuuint32_t box[4] = {(cuuint32_t)TX, (cuuint32_t)TY, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  g_map_err = (int)r;
+  return r == CUDA_SUCCESS;
+}
+
+struct MapCache {
+  const double* px = nullptr;
+  const double* py = nullptr;
+  const double* field = nullptr;
+  int64_t nx = 0, ny = 0, nz = 0;
+  int cap = 0, tx = 0, ty = 0;
+  CUtensorMap mpx, mpy, mk;
+  bool ok = false;
+};
 
 template <int KIND, int TX, int TY, int KMAX>
-void launch_t(FusedArgs a, cudaStream_t s) {
-  using T = Tile<TX, TY>;
-  const size_t smem = (size_t)(6 * T::HP + T::NI + (size_t)KMAX * T::NI) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fused_arnoldi_kernel<KIND, TX, TY, KMAX>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
+  using Cfg = FCfg<TX, TY, KMAX>;
+  static MapCache mc;
+  const Stencil& st = a.st;
+  if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != st.field || mc.nx != st.nx ||
+      mc.ny != st.ny || mc.nz != st.nz || mc.cap != a.cap) {
+    mc.ok = make_map(&mc.mpx, ring_px, st, a.cap, TX, TY) && make_map(&mc.mpy, ring_py, st, a.cap, TX, TY) &&
+            (st.field == nullptr || make_map(&mc.mk, st.field, st, 1, TX, TY));
+    if (st.field == nullptr) mc.mk = mc.mpx;
+    mc.px = ring_px; mc.py = ring_py; mc.field = st.field;
+    mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)Cfg::SMEM);
+      attr = true;
+    }
   }
-  a.zchunk = zchunk_for<TX, TY>(a.st);
-  const int64_t tiles = ((a.st.nx + TX - 1) / TX) * ((a.st.ny + TY - 1) / TY) *
-                        ((a.st.nz + a.zchunk - 1) / a.zchunk);
-  fused_arnoldi_kernel<KIND, TX, TY, KMAX><<<(unsigned)tiles, T::THREADS, smem, s>>>(a);
-}
-
-template <int KIND, int TX, int TY>
-void launch_k(const FusedArgs& a, cudaStream_t s) {
-  if (a.k <= 8) launch_t<KIND, TX, TY, 8>(a, s);
-  else if (a.k <= 16) launch_t<KIND, TX, TY, 16>(a, s);
-  else launch_t<KIND, TX, TY, 32>(a, s);
+  a.tiles_x = (st.nx + (TX - 4) - 1) / (TX - 4);
+  a.tiles_y = TY > 1 ? (st.ny + (TY - 2) - 1) / (TY - 2) : st.ny;
+  const int64_t txy = a.tiles_x * a.tiles_y;
+  int64_t zc = txy * st.nz / (148 * 4);            // about 4 tiles per SM
+  if (zc > 64) zc = 64;
+  if (zc < 8) zc = 8;
+  if (zc > st.nz) zc = st.nz;
+  a.zchunk = (int)zc;
+  a.ntiles = txy * ((st.nz + zc - 1) / zc);
+  if (!mc.ok) return g_map_err ? g_map_err : -1;
+  int64_t grid = 148;                              // one resident block per SM (persistent)
+  if (grid > a.ntiles) grid = a.ntiles;
+  fused_tma_kernel<KIND, TX, TY, KMAX><<<(unsigned)grid, dim3(TX, TY), Cfg::SMEM, s>>>(mc.mpx, mc.mpy, mc.mk, a);
+  return 0;
 }
 
 template <int KIND>
-void launch_kind(const FusedArgs& a, bool three_d, cudaStream_t s) {
-  if (three_d) launch_k<KIND, 32, 8>(a, s);
-  else launch_k<KIND, 256, 1>(a, s);
+int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, cudaStream_t s) {
+  if (three_d) {
+    if (a.k <= 8) return launch_t<KIND, 32, 16, 8>(a, rpx, rpy, s);
+    if (a.k <= 16) return launch_t<KIND, 32, 16, 16>(a, rpx, rpy, s);
+    if (a.k <= 24) return launch_t<KIND, 32, 8, 24>(a, rpx, rpy, s);
+    return launch_t<KIND, 32, 8, 32>(a, rpx, rpy, s);
+  }
+  if (a.k <= 8) return launch_t<KIND, 256, 1, 8>(a, rpx, rpy, s);
+  if (a.k <= 16) return launch_t<KIND, 256, 1, 16>(a, rpx, rpy, s);
+  return launch_t<KIND, 256, 1, 32>(a, rpx, rpy, s);
 }
 
 // 3-D view of the local grid for the fused pass: the march axis is the slowest one
@@ -377,28 +516,34 @@ Stencil march_view(const Stencil& st) {
 }  // namespace
 
 bool fused_supported(const Stencil& st, int k) {
-  return st.kind != PSP_OP_DIA && k <= 32 && st.x_lo == nullptr && st.x_hi == nullptr;
+  // TMA maps need 16-byte row strides (nx even) and coordinates that fit int32
+  return st.kind != PSP_OP_DIA && k <= 32 && st.x_lo == nullptr && st.x_hi == nullptr && st.nx % 2 == 0 &&
+         st.nx * st.ny * st.nz < ((int64_t)1 << 31) && encode_fn() != nullptr;
 }
 
-void launch_fused(const Stencil& st0, Basis V, int k, int nA, const double* src, double* dstx,
-                  double* dsty, double* slot_scale, int dst_slot, DevState ds, cudaStream_t s) {
+int launch_fused(const Stencil& st0, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
+                  int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
+                  DevState ds, cudaStream_t s) {
   FusedArgs a;
   a.st = march_view(st0);
-  a.V = V;
   a.k = k;
   a.nA = nA;
-  a.src = src;
+  a.vs1 = vs1;
+  a.cap = cap;
+  a.src_slot = src_slot;
+  a.src_px = src_px;
   a.dstx = dstx;
   a.dsty = dsty;
   a.slot_scale = slot_scale;
   a.dst_slot = dst_slot;
   a.zchunk = 1;
+  a.tiles_x = a.tiles_y = a.ntiles = 1;
   a.ds = ds;
   const bool three_d = st0.ndim == 3;
   switch (st0.kind) {
-    case PSP_OP_CONST_DIFF: launch_kind<PSP_OP_CONST_DIFF>(a, three_d, s); break;
-    case PSP_OP_CELL_DIFF: launch_kind<PSP_OP_CELL_DIFF>(a, three_d, s); break;
-    default: launch_kind<PSP_OP_CELL_ADVDIFF>(a, three_d, s); break;
+    case PSP_OP_CONST_DIFF: return launch_kind<PSP_OP_CONST_DIFF>(a, three_d, ring_px, ring_py, s);
+    case PSP_OP_CELL_DIFF: return launch_kind<PSP_OP_CELL_DIFF>(a, three_d, ring_px, ring_py, s);
+    default: return launch_kind<PSP_OP_CELL_ADVDIFF>(a, three_d, ring_px, ring_py, s);
   }
 }
 

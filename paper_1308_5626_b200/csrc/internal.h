@@ -129,8 +129,10 @@ void launch_diff_norm(const double* b, const double* y, int64_t n, DevState ds, 
 bool fused_supported(const Stencil& st, int k);
 // finish step k (u = V_{k+1} -> dstx, A u -> dsty, H(k+1,k), Givens, alpha_{k+1} ->
 // slot_scale[dst_slot]) and compute step k+1's MGS coefficients; k = 0 is the cycle-start pass
-void launch_fused(const Stencil& st, Basis V, int k, int nA, const double* src, double* dstx,
-                  double* dsty, double* slot_scale, int dst_slot, DevState ds, cudaStream_t s);
+// returns 0, or the cuTensorMapEncodeTiled error of the operand maps
+int launch_fused(const Stencil& st, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
+                  int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
+                  DevState ds, cudaStream_t s);
 
 // ---- MREP (mrep.cu) ----
 struct MrepOut {

@@ -69,15 +69,15 @@ __host__ __device__ constexpr int pk(int a, int b) { return a * (a + 1) / 2 + b;
 
 // Gram of row r (thread t) from the lagged sums in shared memory:
 // G[0][0] = m, G[1+a][0] = S(r-d+a), G[1+b][1+a] = C_{b-a}(r-d+a) (b >= a); + lambda on the diagonal
-template <int D>
+template <int D, int TS>
 __device__ __forceinline__ void assemble(double (&A)[(2 * D + 2) * (2 * D + 3) / 2], const double* ex,
                                          int t, int m, double lambda) {
   A[pk(0, 0)] = (double)m + lambda;
 #pragma unroll
   for (int a = 0; a <= 2 * D; ++a) {
-    A[pk(1 + a, 0)] = ex[(2 * D + 1) * TPB + (t - D + a)];
+    A[pk(1 + a, 0)] = ex[(2 * D + 1) * TS + (t - D + a)];
 #pragma unroll
-    for (int b = a; b <= 2 * D; ++b) A[pk(1 + b, 1 + a)] = ex[(b - a) * TPB + (t - D + a)];
+    for (int b = a; b <= 2 * D; ++b) A[pk(1 + b, 1 + a)] = ex[(b - a) * TS + (t - D + a)];
     A[pk(1 + a, 1 + a)] += lambda;
   }
 }
@@ -120,9 +120,9 @@ struct GateStats {
 
 // The fit of one interior row from the exchanged lagged sums: Gram assembly,
 // Cholesky + condition estimate + one ridge retry (R17), solve, band install (R14, R15),
-// diagnostics and gate statistics.  ex: (2D+2) x TPB sums of the tile's rows; t: this row's
+// diagnostics and gate statistics.  ex: (2D+2) x TS sums of the tile's rows; t: this row's
 // index in the tile; r: local row; gr: global row.
-template <int D>
+template <int D, int TS>
 __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
                                         int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
   constexpr int P = 2 * D + 2;
@@ -133,7 +133,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double T
   int kind = PSP_ROW_INTERIOR;
 #pragma unroll 1
   for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
-    assemble<D>(A, ex, t, m, lambda);
+    assemble<D, TS>(A, ex, t, m, lambda);
     ok = chol_packed<P>(A, lmax, lmin);
     if (attempt == 0) {
       kap = ok ? (lmax / lmin) * (lmax / lmin) : INFINITY;
@@ -141,7 +141,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double T
       // S:226 ridge retry on G + lambda I
       double tr = (double)m;
 #pragma unroll
-      for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TPB + (t - D + a)];   // diag = C_0(r-d+a)
+      for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TS + (t - D + a)];   // diag = C_0(r-d+a)
       lambda = 1e-10 * tr / (double)P;
       kind = PSP_ROW_INTERIOR_RIDGE;
       g.v[3] += 1.0;
@@ -221,23 +221,24 @@ __device__ void merge_stats(GateStats& g, double* red /* 8 warps x 6 */, double*
 }
 
 // Generic interior-row kernel (any row range, multi-rank halos): thread t accumulates the sums
-// of row r = i0 - D + t of a 256-row tile that emits rows [i0, i0 + 256 - 2D).  It runs the
-// tiles the TMA kernel below cannot (the first and last tiles of the local block) -- tiles
-// [0, t_lo) and [t_hi, ntiles) -- or all tiles when t_lo == t_hi.
+// of row r = i0 - D + t of a 256-row tile that emits rows [i0, i0 + 256 - 2D).  It fits the rows
+// of [a0, a1) and [b0, b1) (tiles start at a0 / b0; emission is clipped to the range) -- the
+// rows the TMA kernel below does not take, or every row.
 template <int D>
-__global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m, int64_t n, int64_t t_lo,
-                                                               int64_t t_hi, MrepOut out, MrepScratch sc) {
+__global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m, int64_t n, int64_t a0, int64_t a1,
+                                                               int64_t b0, int64_t b1, MrepOut out, MrepScratch sc) {
   constexpr int TILE = TPB + 3 * D;                 // rows [i0-2D, i0-D+TPB+2D)
+  constexpr int64_t E = TPB - 2 * D;
   __shared__ double xs[CB][TILE];
   __shared__ double ex[(2 * D + 2) * TPB];
   __shared__ double red[TPB / 32 * 6];
   const int t = threadIdx.x;
   GateStats gs;
-  const int64_t ntiles = (n + (TPB - 2 * D) - 1) / (TPB - 2 * D);
-  const int64_t nedge = t_lo + (ntiles - t_hi);
-  for (int64_t q = blockIdx.x; q < nedge; q += gridDim.x) {
-  const int64_t tile = q < t_lo ? q : t_hi + (q - t_lo);
-  const int64_t i0 = tile * (TPB - 2 * D);
+  const int64_t na = a1 > a0 ? (a1 - a0 + E - 1) / E : 0;
+  const int64_t nbt = b1 > b0 ? (b1 - b0 + E - 1) / E : 0;
+  for (int64_t q = blockIdx.x; q < na + nbt; q += gridDim.x) {
+  const int64_t i0 = q < na ? a0 + q * E : b0 + (q - na) * E;
+  const int64_t rend = q < na ? a1 : b1;            // emission stops at the range end
   const int64_t r = i0 - D + t;                     // the row this thread accumulates for
   const int64_t tile0 = i0 - 2 * D;
 
@@ -279,8 +280,8 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
   __syncthreads();
 
   const int64_t gr = cols.grow0 + r;                 // global row (multi-rank slabs)
-  const bool emit = (t >= D && t < TPB - D) && r >= 0 && r < n && gr >= D && gr < cols.gN - D;
-  if (emit) fit_row<D>(ex, t, m, Tsum, Dl, r, n, gr, cols.gN, out, gs);
+  const bool emit = (t >= D && t < TPB - D) && r >= 0 && r < n && r < rend && gr >= D && gr < cols.gN - D;
+  if (emit) fit_row<D, TPB>(ex, t, m, Tsum, Dl, r, n, gr, cols.gN, out, gs);
   }  // tiles
   merge_stats(gs, red, sc.result);
 }
@@ -296,15 +297,16 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
 // reads are 32 consecutive doubles (conflict-free).  All columns must share the 16-byte
 // alignment parity (sx, sy; checked on the host, else the generic kernel runs everything).
 // ------------------------------------------------------------------------------------------
+constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kernel
 constexpr int TCB = 4;         // probe columns per stage
 constexpr int TNST = 4;        // stages
 
 template <int D>
 struct TmaCfg {
-  static constexpr int PXW = ((TPB + 3 * D + 2) + 1) / 2 * 2;   // P_x stage row (doubles)
-  static constexpr int PYW = TPB + 2;                            // P_y stage row
+  static constexpr int PXW = ((TT + 3 * D + 2) + 1) / 2 * 2;    // P_x stage row (doubles)
+  static constexpr int PYW = TT + 2;                             // P_y stage row
   static constexpr int STAGE = TCB * (PXW + PYW);                // doubles per stage
-  static constexpr size_t SMEM = (size_t)TNST * STAGE * 8 + (size_t)(2 * D + 2) * TPB * 8 + 16 * TNST;
+  static constexpr size_t SMEM = (size_t)TNST * STAGE * 8 + (size_t)(2 * D + 2) * TT * 8 + 16 * TNST;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -348,45 +350,51 @@ struct TmaCols {
 };
 
 template <int D>
-__global__ void __launch_bounds__(TPB, PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
-                                                          int m, int64_t n, int64_t gN, int64_t grow0,
-                                                          int64_t t_lo, int64_t t_hi, MrepOut out,
-                                                          MrepScratch sc) {
+__global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
+                                                                      int m, int64_t n, int64_t gN, int64_t grow0,
+                                                                      int64_t R0, int64_t ntile, MrepOut out,
+                                                                      MrepScratch sc) {
   using Cfg = TmaCfg<D>;
-  constexpr int E = TPB - 2 * D;                   // rows emitted per tile
-  constexpr int LX = ((TPB + 3 * D) + 1) & ~1;     // P_x segment length (shift 0) ...
-  constexpr int LX1 = ((TPB + 3 * D + 1) + 1) & ~1;//   ... and with shift 1
-  constexpr int LY = TPB, LY1 = TPB + 2;
+  constexpr int E = TT - 2 * D;                    // rows emitted per tile
+  constexpr int LX = ((TT + 3 * D) + 1) & ~1;      // P_x segment length (shift 0) ...
+  constexpr int LX1 = ((TT + 3 * D + 1) + 1) & ~1; //   ... and with shift 1
+  constexpr int LY = TT, LY1 = TT + 2;
   extern __shared__ __align__(16) double sm[];
   double* stages = sm;                             // [TNST][TCB x PXW | TCB x PYW]
-  double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TPB]: C_l, S of the tile's rows
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (2 * D + 2) * TPB);
+  double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TT]: C_l, S of the tile's rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (2 * D + 2) * TT);
   __shared__ double scs[kMaxM];                    // per-column probe scale
-  __shared__ double red[TPB / 32 * 6];
+  __shared__ double red[TT / 32 * 6];
+  __shared__ int s_unit;
   const int t = threadIdx.x;
-  for (int c = t; c < m; c += TPB) scs[c] = scale ? scale[cols.slot[c]] : 1.0;
+  if (t == 0) s_unit = 1;
+  __syncthreads();
+  for (int c = t; c < m; c += TT) {
+    scs[c] = scale ? scale[cols.slot[c]] : 1.0;
+    if (scs[c] != 1.0) s_unit = 0;
+  }
   if (t == 0) {
     for (int q = 0; q < TNST; ++q) mbar_init(bars + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const bool unit = s_unit != 0;                   // every recorded probe scale is 1
 
   const int lx = cols.sx ? LX1 : LX, ly = cols.sy ? LY1 : LY;
-  const int nch = (m + TCB - 1) / TCB;
-  const int64_t my_tiles = (t_hi - t_lo - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int nch = m / TCB;                         // m % TCB == 0 (host check)
+  const int64_t my_tiles = (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t total = my_tiles * nch;
   auto issue = [&](int64_t q) {                   // thread 0: stage the columns of load q
-    const int64_t tile = t_lo + blockIdx.x + (q / nch) * gridDim.x;
+    const int64_t tile = blockIdx.x + (q / nch) * gridDim.x;
     const int ch = (int)(q % nch);
     const int stg = (int)(q % TNST);
     double* st = stages + (size_t)stg * Cfg::STAGE;
-    const int64_t s0 = tile * E - D;
-    const int c0 = ch * TCB;
-    const int cn = (m - c0) < TCB ? (m - c0) : TCB;
+    const int64_t s0 = R0 + tile * E - D;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bars + stg, 8u * (unsigned)(cn * (lx + ly)));
-    for (int cc = 0; cc < cn; ++cc) {
-      const int c = c0 + cc;
+    mbar_expect_tx(bars + stg, 8u * (unsigned)(TCB * (lx + ly)));
+#pragma unroll
+    for (int cc = 0; cc < TCB; ++cc) {
+      const int c = ch * TCB + cc;
       const double* bxp = cols.px + (int64_t)cols.slot[c] * cols.ld;
       const double* byp = cols.py + (int64_t)cols.slot[c] * cols.ld;
       bulk_g2s(st + cc * Cfg::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + stg);
@@ -409,39 +417,52 @@ __global__ void __launch_bounds__(TPB, PSP_MREP_MINB) mrep_tma_kernel(TmaCols co
     }
     mbar_wait(bars + stg, (unsigned)((q / TNST) & 1));
     const double* st = stages + (size_t)stg * Cfg::STAGE;
-    const int c0 = ch * TCB;                       // m % TCB == 0 (host check)
+    if (unit) {
 #pragma unroll
-    for (int cc = 0; cc < TCB; ++cc) {
-      const double sc = scs[c0 + cc];
-      const double* xr = st + cc * Cfg::PXW + xo;  // xr[k] = P_x(r - D + k), r = s0 + t
-      double xw[3 * D + 1];
+      for (int cc = 0; cc < TCB; ++cc) {
+        const double* xr = st + cc * Cfg::PXW + xo;  // xr[k] = P_x(r - D + k), r = s0 + t
+        double xw[3 * D + 1];
 #pragma unroll
-      for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
-      double yv = st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
-      if (sc != 1.0) {                             // uniform: the probe's recorded scale
+        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
+        const double yv = st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
+        const double x0 = xw[D];
+        Ssum += x0;
+        Tsum += yv;
 #pragma unroll
-        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = sc * xw[k];
-        yv = sc * yv;
+        for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
       }
-      const double x0 = xw[D];
-      Ssum += x0;
-      Tsum += yv;
+    } else {
+      const int c0 = ch * TCB;
 #pragma unroll
-      for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+      for (int cc = 0; cc < TCB; ++cc) {
+        const double sc = scs[c0 + cc];
+        const double* xr = st + cc * Cfg::PXW + xo;
+        double xw[3 * D + 1];
 #pragma unroll
-      for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
+        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = sc * xr[k];
+        const double yv = sc * st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
+        const double x0 = xw[D];
+        Ssum += x0;
+        Tsum += yv;
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
+      }
     }
     __syncthreads();                               // every thread is done with stage stg
     if (t == 0 && q + TNST < total) issue(q + TNST);
     if (ch == nch - 1) {
-      // exchange C_l, S of the tile's 256 sum rows, then fit the emitted rows
+      // exchange C_l, S of the tile's TT sum rows, then fit the emitted rows
 #pragma unroll
-      for (int l = 0; l <= 2 * D; ++l) ex[l * TPB + t] = Cl[l];
-      ex[(2 * D + 1) * TPB + t] = Ssum;
+      for (int l = 0; l <= 2 * D; ++l) ex[l * TT + t] = Cl[l];
+      ex[(2 * D + 1) * TT + t] = Ssum;
       __syncthreads();
-      const int64_t tile = t_lo + blockIdx.x + (q / nch) * gridDim.x;
-      const int64_t r = tile * E - D + t;
-      if (t >= D && t < TPB - D) fit_row<D>(ex, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+      const int64_t tile = blockIdx.x + (q / nch) * gridDim.x;
+      const int64_t r = R0 + tile * E - D + t;
+      if (t >= D && t < TT - D) fit_row<D, TT>(ex, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
       __syncthreads();                             // ex is rewritten by the next tile
     }
   }
@@ -449,15 +470,15 @@ __global__ void __launch_bounds__(TPB, PSP_MREP_MINB) mrep_tma_kernel(TmaCols co
 }
 
 template <int D>
-void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_t gN, int64_t grow0, int64_t t_lo,
-                int64_t t_hi, MrepOut out, MrepScratch sc, int nb, cudaStream_t s) {
+void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_t gN, int64_t grow0, int64_t R0,
+                int64_t ntile, MrepOut out, MrepScratch sc, int nb, cudaStream_t s) {
   const size_t smem = TmaCfg<D>::SMEM;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(mrep_tma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  mrep_tma_kernel<D><<<nb, TPB, smem, s>>>(tc, scale, m, n, gN, grow0, t_lo, t_hi, out, sc);
+  mrep_tma_kernel<D><<<nb, TT, smem, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
 }
 
 // Boundary rows, R16 two-pass centred OLS, one thread per row.
@@ -573,36 +594,37 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
   }
   cudaMemsetAsync(sc.result, 0, 16 * sizeof(double), s);
   mrep_boundary_kernel<<<1, 64, 0, s>>>(cols, m, n, d, out, sc);   // writes result[0..5]
-  // tiles of 256 - 2d emitted rows; [t_lo, t_hi) go to the TMA kernel (their P_x / P_y rows,
-  // widened by one row for 16-byte alignment, lie inside this rank's block)
-  const int64_t E = TPB - 2 * d;
-  const int64_t ntiles = (n + E - 1) / E;
-  int64_t t_lo = 1, t_hi = (n - (TPB + d + 1)) >= 0 ? (n - (TPB + d + 1)) / E + 1 : 0;
-  if (t_hi > ntiles) t_hi = ntiles;
+  // rows [R0, R1) go to the TMA kernel (tiles of TT - 2d emitted rows whose P_x / P_y rows,
+  // widened by one row for 16-byte alignment, lie inside this rank's block), the rest to the
+  // generic kernel
+  const int64_t Et = TT - 2 * d;
+  const int64_t R0 = 2 * d + 2;
+  int64_t ntile = (n - 1 - 3 * d - R0) >= 0 ? (n - 1 - 3 * d - R0) / Et : 0;
   // the TMA kernel needs every column's P_x (and P_y) segments to share a 16-byte parity
   int sxp = -1, syp = -1;
   bool uniform = true;
   for (int c = 0; c < m && c < kMaxM; ++c) {
-    const int64_t bx = (int64_t)(((uintptr_t)(px + (int64_t)cols.slot[c] * ld)) >> 3);
-    const int64_t by = (int64_t)(((uintptr_t)(py + (int64_t)cols.slot[c] * ld)) >> 3);
-    const int px_par = (int)(bx & 1), py_par = (int)((by + (E - d)) & 1);   // rows s0-d (even), s0
+    const uintptr_t ax = (uintptr_t)(px + (int64_t)cols.slot[c] * ld);
+    const uintptr_t ay = (uintptr_t)(py + (int64_t)cols.slot[c] * ld);
+    const int px_par = (int)((ax >> 3) & 1), py_par = (int)(((ay >> 3) + (uintptr_t)(R0 - d)) & 1);
     if (sxp < 0) { sxp = px_par; syp = py_par; }
-    uniform = uniform && px_par == sxp && py_par == syp;
-    uniform = uniform && ((((uintptr_t)(px + (int64_t)cols.slot[c] * ld)) & 7) == 0) &&
-              ((((uintptr_t)(py + (int64_t)cols.slot[c] * ld)) & 7) == 0);
+    uniform = uniform && px_par == sxp && py_par == syp && (ax & 7) == 0 && (ay & 7) == 0;
   }
-  if (t_hi < t_lo || m > kMaxM || m % TCB != 0 || !uniform) t_lo = t_hi = ntiles;
-  const int64_t nedge = t_lo + (ntiles - t_hi);
-  if (nedge > 0) {
-    const int nb = (int)(nedge < kMrepMaxBlocks ? nedge : kMrepMaxBlocks);
+  if (ntile < 1 || m > kMaxM || m % TCB != 0 || !uniform) ntile = 0;
+  const int64_t R1 = ntile > 0 ? R0 + ntile * Et : n;
+  const int64_t a0 = 0, a1 = ntile > 0 ? R0 : n, b0 = R1, b1 = ntile > 0 ? n : n;
+  {
+    const int64_t E = TPB - 2 * d;
+    const int64_t nt = (a1 - a0 + E - 1) / E + (b1 > b0 ? (b1 - b0 + E - 1) / E : 0);
+    const int nb = (int)(nt < kMrepMaxBlocks ? (nt > 0 ? nt : 1) : kMrepMaxBlocks);
     switch (d) {
-      case 1: mrep_interior_kernel<1><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
-      case 2: mrep_interior_kernel<2><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
-      case 3: mrep_interior_kernel<3><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
-      default: mrep_interior_kernel<4><<<nb, TPB, 0, s>>>(cols, m, n, t_lo, t_hi, out, sc); break;
+      case 1: mrep_interior_kernel<1><<<nb, TPB, 0, s>>>(cols, m, n, a0, a1, b0, b1, out, sc); break;
+      case 2: mrep_interior_kernel<2><<<nb, TPB, 0, s>>>(cols, m, n, a0, a1, b0, b1, out, sc); break;
+      case 3: mrep_interior_kernel<3><<<nb, TPB, 0, s>>>(cols, m, n, a0, a1, b0, b1, out, sc); break;
+      default: mrep_interior_kernel<4><<<nb, TPB, 0, s>>>(cols, m, n, a0, a1, b0, b1, out, sc); break;
     }
   }
-  if (t_hi > t_lo) {
+  if (ntile > 0) {
     TmaCols tc;
     tc.px = px;
     tc.py = py;
@@ -610,13 +632,12 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
     tc.sx = sxp;
     tc.sy = syp;
     for (int c = 0; c < m; ++c) tc.slot[c] = cols.slot[c];
-    const int64_t nt = t_hi - t_lo;
-    const int nb = (int)(nt < 148 * 2 ? nt : 148 * 2);
+    const int nb = (int)(ntile < 148 * 4 ? ntile : 148 * 4);
     switch (d) {
-      case 1: launch_tma<1>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
-      case 2: launch_tma<2>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
-      case 3: launch_tma<3>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
-      default: launch_tma<4>(tc, slot_scale, m, n, cols.gN, cols.grow0, t_lo, t_hi, out, sc, nb, s); break;
+      case 1: launch_tma<1>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
+      case 2: launch_tma<2>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
+      case 3: launch_tma<3>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
+      default: launch_tma<4>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
     }
   }
   if (multi) {

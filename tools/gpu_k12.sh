@@ -1,0 +1,3 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+./tools/tma_probe 10
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 120 --timeout-method=thread -k "fused" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log; grep -E "passed|failed|Error|rc " gpurun_out/pytest_gpu.log | head -12
