@@ -24,11 +24,15 @@
 
 #include "internal.h"
 
+#ifndef PSP_SWEEP_MINB
+#define PSP_SWEEP_MINB 2   // resident 256-thread sweep blocks per SM
+#endif
+
 namespace psp {
 namespace {
 
 constexpr int kChunk = 128;      // factor: rows per thread
-constexpr int STPB = 128;        // solve: threads per block
+constexpr int STPB = 256;        // solve: threads per block
 constexpr int SR = 8;            // solve: rows per thread
 constexpr int STILE = STPB * SR; // solve: rows per tile
 constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank conflicts)
@@ -206,8 +210,18 @@ __device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], dou
   }
 }
 
-// Descriptor layout per tile: [M (D*D) | t (D) | S (D)] doubles; flag word separate.
-enum { FLAG_AGG = 1, FLAG_INCL = 2 };
+// Descriptor layout per tile: [M (D*D) | t (D) | S (D)] doubles: the tile's affine map and
+// the exact state entering it.
+//
+// A sweep is three launches, each free of cross-block waits:
+//   tile_map_kernel    every tile's affine map state_out = M state_in + t (zero-state run plus
+//                      the d unit-state runs of the recurrence over its rows), one tile / block;
+//   tile_scan_kernel   one block composes the maps in processing order: exact incoming state of
+//                      every tile (and the state after the last row, s_out);
+//   tile_apply_kernel  every tile re-runs its rows from its exact incoming state and writes out.
+// The coefficients and the right-hand side are read twice (8(2d+3) B/row forward, 8(2d+5)
+// backward instead of 8(d+2) / 8(d+3)), traded for bandwidth-bound launches with no look-back
+// chain: a single-pass chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
 
 // One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
 //                        BWD: z = (v - sum_k c[k] s[k]) / u0 (c[k] = U(i,i+k+1), s[k] = z_{i+k+1})
@@ -228,204 +242,242 @@ __device__ __forceinline__ void push_state(double (&s)[D], double y) {
 }
 
 template <bool FWD, int D>
-__global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ lu, int64_t n,
-                                                     const double* __restrict__ vin,
-                                                     const double* vscale,
-                                                     const double* addend,
-                                                     double* out,
-                                                     double* __restrict__ desc,
-                                                     unsigned long long* __restrict__ flags,
-                                                     unsigned long long* __restrict__ ctl,
-                                                     const double* s_in0, double* s_out) {
-  // ctl[0] = ticket counter, ctl[1] = epoch.  vin == NULL: zero right-hand side (homogeneous).
-  // s_in0 (d doubles, may be NULL = 0): the state entering this rank's first row in processing
-  // order (multi-rank); s_out (may be NULL): receives the state after its last row.
-  // out == NULL: nothing is written (the zero-state pass of a multi-rank sweep).
-  // dynamic shared memory: sv (rhs, then the result) | sc[D] (recurrence coefficients) |
-  // su0 (U(i,i), backward only)
-  extern __shared__ double smem_dyn[];
-  double* sv = smem_dyn;
-  double (*sc)[STPB * SPAD] = reinterpret_cast<double (*)[STPB * SPAD]>(smem_dyn + STPB * SPAD);
-  double* su0 = smem_dyn + (1 + D) * STPB * SPAD;
-  __shared__ Map<D> wtot[STPB / 32];
-  __shared__ double s_in[D];
-  __shared__ long long s_tile;
-  __shared__ unsigned long long s_epoch;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t ntiles = (n + STILE - 1) / STILE;
-  if (t == 0) {
-    s_epoch = ((volatile unsigned long long*)ctl)[1];
-    unsigned long long tk = atomicAdd(ctl, 1ull);
-    s_tile = (long long)tk;
-  }
-  __syncthreads();
-  const unsigned long long epoch = s_epoch;
-  const int64_t tile = FWD ? (int64_t)s_tile : (ntiles - 1 - (int64_t)s_tile);
-  const int64_t base = tile * STILE;
+struct TileSmem {
+  static constexpr int NA = 1 + D + (FWD ? 0 : 1);
+  static constexpr size_t BYTES = (size_t)NA * STPB * SPAD * sizeof(double);
+};
 
-  // ---- stage the tile (coalesced), rows in processing order per thread ----
-  const double vsc = vscale ? *vscale : 1.0;
-  for (int q = t; q < STILE; q += STPB) {
-    const int64_t i = base + q;
-    const int sidx = (q / SR) * SPAD + (q % SR);
-    const bool in = i < n;
-    sv[sidx] = (in && vin) ? vsc * vin[i] : 0.0;
+// stage the tile's rows (coalesced) into the per-thread padded layout: sv (rhs), sc[k]
+// (recurrence coefficients), su0 (U(i,i), backward); padding rows are transparent
+template <bool FWD, int D>
+__device__ __forceinline__ void stage_tile(double* sv, const double* __restrict__ lu, int64_t n,
+                                           const double* __restrict__ vin, double vsc, int64_t base) {
+  double* sc0 = sv + STPB * SPAD;
+  double* su0 = sv + (1 + D) * STPB * SPAD;
+  constexpr int IT = STILE / STPB;              // rows per thread of the coalesced copy
+  constexpr int NA = 1 + D + (FWD ? 0 : 1);
+  // every load of the tile is issued before the first shared-memory store (one latency per tile)
+  double r[IT][NA];
+  const bool full = base + STILE <= n;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int64_t i = base + threadIdx.x + it * STPB;
+    const bool in = full || i < n;
+    r[it][0] = (in && vin) ? __ldg(vin + i) : 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
       const int o = FWD ? (D - 1 - k) : (D + 1 + k);
-      sc[k][sidx] = in ? lu[(int64_t)o * n + i] : 0.0;
+      r[it][1 + k] = in ? __ldg(lu + (int64_t)o * n + i) : 0.0;
     }
-    if (!FWD) su0[sidx] = in ? lu[(int64_t)D * n + i] : 1.0;
+    if (!FWD) r[it][1 + D] = in ? __ldg(lu + (int64_t)D * n + i) : 1.0;
   }
-  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int q = threadIdx.x + it * STPB;
+    const int sidx = (q / SR) * SPAD + (q % SR);
+    sv[sidx] = vsc * r[it][0];
+#pragma unroll
+    for (int k = 0; k < D; ++k) sc0[k * STPB * SPAD + sidx] = r[it][1 + k];
+    if (!FWD) su0[sidx] = r[it][1 + D];
+  }
+}
 
-  // ---- per-thread affine map over its SR rows (FWD: ascending, BWD: descending) ----
-  Map<D> my;
-  {
-    double sz[D];            // zero-state run
-    double su[D][D];         // unit-state runs: su[q] starts at e_q
+// this thread's SR rows as an affine map (FWD ascending, BWD descending)
+template <bool FWD, int D>
+__device__ __forceinline__ Map<D> thread_map(const double* sv, int64_t base, int64_t n) {
+  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
+  const double* su0 = sv + (1 + D) * STPB * SPAD;
+  const int t = threadIdx.x;
+  double sz[D];            // zero-state run
+  double su[D][D];         // unit-state runs: su[q] starts at e_q
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      sz[k] = 0.0;
+  for (int k = 0; k < D; ++k) {
+    sz[k] = 0.0;
 #pragma unroll
-      for (int q = 0; q < D; ++q) su[q][k] = (q == k) ? 1.0 : 0.0;
-    }
-#pragma unroll
-    for (int rr = 0; rr < SR; ++rr) {
-      const int r = FWD ? rr : (SR - 1 - rr);
-      if (base + (int64_t)t * SR + r >= n) continue;   // padding rows are transparent
-      const int sidx = t * SPAD + r;
-      double c[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
-      const double u0 = FWD ? 1.0 : su0[sidx];
-      push_state<D>(sz, rec_step<FWD, D>(sv[sidx], c, sz, u0));
-#pragma unroll
-      for (int q = 0; q < D; ++q) push_state<D>(su[q], rec_step<FWD, D>(0.0, c, su[q], u0));
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      my.t[i] = sz[i];
-#pragma unroll
-      for (int q = 0; q < D; ++q) my.M[i][q] = su[q][i];
-    }
+    for (int q = 0; q < D; ++q) su[q][k] = (q == k) ? 1.0 : 0.0;
   }
-  // ---- block scan (order: FWD thread 0 first, BWD thread STPB-1 first) ----
-  // Work in "processing order" p: FWD p = t, BWD p = STPB-1-t.  A warp holds p in a
-  // contiguous range either way; for BWD lanes run in reverse, so scan with shfl_down.
+#pragma unroll
+  for (int rr = 0; rr < SR; ++rr) {
+    const int r = FWD ? rr : (SR - 1 - rr);
+    if (base + (int64_t)t * SR + r >= n) continue;   // padding rows are transparent
+    const int sidx = t * SPAD + r;
+    double c[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
+    const double u0 = FWD ? 1.0 : su0[sidx];
+    push_state<D>(sz, rec_step<FWD, D>(sv[sidx], c, sz, u0));
+#pragma unroll
+    for (int q = 0; q < D; ++q) push_state<D>(su[q], rec_step<FWD, D>(0.0, c, su[q], u0));
+  }
+  Map<D> my;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    my.t[i] = sz[i];
+#pragma unroll
+    for (int q = 0; q < D; ++q) my.M[i][q] = su[q][i];
+  }
+  return my;
+}
+
+// block scan of the thread maps in processing order (FWD thread 0 first, BWD thread STPB-1
+// first): returns this thread's exclusive prefix; agg (valid in every thread) = the whole tile
+template <bool FWD, int D>
+__device__ __forceinline__ Map<D> block_prefix(const Map<D>& my, Map<D>* wtot, Map<D>& agg) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  constexpr int NW = STPB / 32;
   Map<D> inc = my;  // inclusive prefix within the warp, in processing order
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     Map<D> o;
-    if (FWD) o = shfl_up_map<D>(inc, off);
-    else {
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        o.t[i] = __shfl_down_sync(0xffffffffu, inc.t[i], off);
+    for (int i = 0; i < D; ++i) {
+      o.t[i] = FWD ? __shfl_up_sync(0xffffffffu, inc.t[i], off) : __shfl_down_sync(0xffffffffu, inc.t[i], off);
 #pragma unroll
-        for (int j = 0; j < D; ++j) o.M[i][j] = __shfl_down_sync(0xffffffffu, inc.M[i][j], off);
-      }
+      for (int j = 0; j < D; ++j)
+        o.M[i][j] = FWD ? __shfl_up_sync(0xffffffffu, inc.M[i][j], off) : __shfl_down_sync(0xffffffffu, inc.M[i][j], off);
     }
     const bool has = FWD ? (lane >= off) : (lane + off < 32);
     if (has) inc = compose<D>(inc, o);
   }
-  // exclusive-in-warp = inclusive of the previous lane (processing order)
-  Map<D> exw;
-  if (FWD) exw = shfl_up_map<D>(inc, 1);
-  else {
+  Map<D> exw;  // exclusive-in-warp = inclusive of the previous lane (processing order)
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    exw.t[i] = FWD ? __shfl_up_sync(0xffffffffu, inc.t[i], 1) : __shfl_down_sync(0xffffffffu, inc.t[i], 1);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      exw.M[i][j] = FWD ? __shfl_up_sync(0xffffffffu, inc.M[i][j], 1) : __shfl_down_sync(0xffffffffu, inc.M[i][j], 1);
+  }
+  if (FWD ? (lane == 0) : (lane == 31)) exw = identity_map<D>();
+  if (FWD ? (lane == 31) : (lane == 0)) wtot[warp] = inc;
+  __syncthreads();
+  Map<D> wpre = identity_map<D>();
+  agg = identity_map<D>();
+  if (FWD) {
+    for (int w = 0; w < NW; ++w) {
+      if (w == warp) wpre = agg;
+      agg = compose<D>(wtot[w], agg);
+    }
+  } else {
+    for (int w = NW - 1; w >= 0; --w) {
+      if (w == warp) wpre = agg;
+      agg = compose<D>(wtot[w], agg);
+    }
+  }
+  __syncthreads();   // wtot may be reused
+  return compose<D>(exw, wpre);   // warp prefix first, then the in-warp prefix
+}
+
+// Block b owns the contiguous range of tiles [b L, (b+1) L) in processing order (FWD:
+// ascending tiles, BWD: descending).  tile_map_kernel composes its tiles' maps into the range
+// map; tile_scan_kernel turns the range maps into exact incoming range states; tile_apply_kernel
+// walks the range again from that state (each tile's map, recomputed, carries the state on).
+template <bool FWD, int D>
+__global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restrict__ lu, int64_t n,
+                                                            const double* __restrict__ vin, const double* vscale,
+                                                            int64_t L, double* __restrict__ rmap) {
+  extern __shared__ double smem_dyn[];
+  __shared__ Map<D> wtot[STPB / 32];
+  constexpr int DW = D * D + 2 * D;
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const double vsc = vscale ? *vscale : 1.0;
+  Map<D> range = identity_map<D>();
+  const int64_t p0 = (int64_t)blockIdx.x * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int64_t tile = FWD ? p : ntiles - 1 - p;
+    const int64_t base = tile * STILE;
+    stage_tile<FWD, D>(smem_dyn, lu, n, vin, vsc, base);
+    __syncthreads();
+    const Map<D> my = thread_map<FWD, D>(smem_dyn, base, n);
+    Map<D> agg;
+    block_prefix<FWD, D>(my, wtot, agg);
+    range = compose<D>(agg, range);
+  }
+  if (threadIdx.x == 0) {
+    double* dd = rmap + blockIdx.x * DW;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      exw.t[i] = __shfl_down_sync(0xffffffffu, inc.t[i], 1);
+      dd[D * D + i] = range.t[i];
 #pragma unroll
-      for (int j = 0; j < D; ++j) exw.M[i][j] = __shfl_down_sync(0xffffffffu, inc.M[i][j], 1);
+      for (int j = 0; j < D; ++j) dd[i * D + j] = range.M[i][j];
     }
   }
-  const bool first_in_warp = FWD ? (lane == 0) : (lane == 31);
-  if (first_in_warp) exw = identity_map<D>();
-  const bool last_in_warp = FWD ? (lane == 31) : (lane == 0);
-  if (last_in_warp) wtot[warp] = inc;
-  __syncthreads();
-  // prefix over warps in processing order (FWD warps 0..3, BWD warps 3..0): small, every thread
-  Map<D> wpre = identity_map<D>();
-  constexpr int NW = STPB / 32;
-  if (FWD) {
-    for (int w = 0; w < warp; ++w) wpre = compose<D>(wtot[w], wpre);
-  } else {
-    for (int w = NW - 1; w > warp; --w) wpre = compose<D>(wtot[w], wpre);
-  }
-  // the tile aggregate (computed by thread 0)
-  if (t == 0) {
-    Map<D> agg = identity_map<D>();
-    if (FWD) for (int w = 0; w < NW; ++w) agg = compose<D>(wtot[w], agg);
-    else for (int w = NW - 1; w >= 0; --w) agg = compose<D>(wtot[w], agg);
-    constexpr int DW = D * D + 2 * D;
-    double* my_desc = desc + tile * DW;
-    volatile unsigned long long* fl = flags;
-    double sin[D];
-    // tiles are processed in order (first = FWD tile 0, BWD tile ntiles-1)
-    const bool first_tile = FWD ? (tile == 0) : (tile == ntiles - 1);
-    if (first_tile) {
-      // nothing before the matrix start / end, or (multi-rank) the state from the neighbour rank
+}
+
+// one block: exact incoming state of every range (processing order), s_out after the last
+constexpr int SCAN_T = 1024;
+template <bool FWD, int D>
+__global__ void __launch_bounds__(SCAN_T, 1) tile_scan_kernel(int nr, double* __restrict__ rmap,
+                                                               const double* s_in0, double* s_out) {
+  extern __shared__ double smem_dyn[];
+  Map<D>* sm = reinterpret_cast<Map<D>*>(smem_dyn);   // [SCAN_T]
+  constexpr int DW = D * D + 2 * D;
+  const int t = threadIdx.x;
+  Map<D> m = identity_map<D>();
+  if (t < nr) {
+    const double* dd = rmap + t * DW;
 #pragma unroll
-      for (int i = 0; i < D; ++i) sin[i] = s_in0 ? s_in0[i] : 0.0;
-    } else {
-      // publish the aggregate
+    for (int i = 0; i < D; ++i) {
+      m.t[i] = dd[D * D + i];
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        my_desc[D * D + i] = agg.t[i];
-#pragma unroll
-        for (int j = 0; j < D; ++j) my_desc[i * D + j] = agg.M[i][j];
-      }
-      __threadfence();
-      fl[tile] = (epoch << 2) | FLAG_AGG;
-      // look back
-      Map<D> acc = identity_map<D>();
-      int64_t j = FWD ? tile - 1 : tile + 1;
-      while (true) {
-        unsigned long long f;
-        do { f = fl[j]; } while ((f >> 2) != epoch || (f & 3ull) == 0ull);
-        __threadfence();
-        volatile const double* dj = desc + j * DW;
-        if ((f & 3ull) == FLAG_INCL) {
-          double S[D];
-#pragma unroll
-          for (int i = 0; i < D; ++i) S[i] = dj[D * D + D + i];
-          apply<D>(acc, S, sin);
-          break;
-        }
-        Map<D> mj;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          mj.t[i] = dj[D * D + i];
-#pragma unroll
-          for (int q = 0; q < D; ++q) mj.M[i][q] = dj[i * D + q];
-        }
-        acc = compose<D>(acc, mj);
-        j = FWD ? j - 1 : j + 1;
-      }
+      for (int j = 0; j < D; ++j) m.M[i][j] = dd[i * D + j];
     }
-    double sout[D];
-    apply<D>(agg, sin, sout);
-#pragma unroll
-    for (int i = 0; i < D; ++i) my_desc[D * D + D + i] = sout[i];
-    __threadfence();
-    fl[tile] = (epoch << 2) | FLAG_INCL;
-    const bool last_tile = FWD ? (tile == ntiles - 1) : (tile == 0);
-    if (last_tile && s_out)
-#pragma unroll
-      for (int i = 0; i < D; ++i) s_out[i] = sout[i];
-#pragma unroll
-    for (int i = 0; i < D; ++i) s_in[i] = sin[i];
   }
+  sm[t] = m;
   __syncthreads();
-  // ---- recompute the rows from the exact incoming state ----
-  {
-    double s0[D], s[D];
+  for (int off = 1; off < SCAN_T; off <<= 1) {      // inclusive (later ranges applied last)
+    Map<D> o = identity_map<D>();
+    if (t >= off) o = sm[t - off];
+    __syncthreads();
+    if (t >= off) sm[t] = compose<D>(sm[t], o);
+    __syncthreads();
+  }
+  double s0[D], s[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) s0[i] = s_in[i];
-    Map<D> pre = compose<D>(exw, wpre);   // warp prefix first, then the in-warp prefix
-    apply<D>(pre, s0, s);
+  for (int i = 0; i < D; ++i) s0[i] = s_in0 ? s_in0[i] : 0.0;
+  if (t > 0) apply<D>(sm[t - 1], s0, s);
+  else
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = s0[i];
+  if (t < nr)
+#pragma unroll
+    for (int i = 0; i < D; ++i) rmap[t * DW + D * D + D + i] = s[i];
+  if (s_out && t == SCAN_T - 1) {
+    double so[D];
+    apply<D>(sm[SCAN_T - 1], s0, so);
+#pragma unroll
+    for (int i = 0; i < D; ++i) s_out[i] = so[i];
+  }
+}
+
+template <bool FWD, int D>
+__global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __restrict__ lu, int64_t n,
+                                                              const double* __restrict__ vin, const double* vscale,
+                                                              const double* addend, double* out, int64_t L,
+                                                              const double* __restrict__ rmap) {
+  extern __shared__ double smem_dyn[];
+  __shared__ Map<D> wtot[STPB / 32];
+  constexpr int DW = D * D + 2 * D;
+  const int t = threadIdx.x;
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const double vsc = vscale ? *vscale : 1.0;
+  double* sv = smem_dyn;
+  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
+  const double* su0 = sv + (1 + D) * STPB * SPAD;
+  double s0[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) s0[i] = rmap[blockIdx.x * DW + D * D + D + i];
+  const int64_t p0 = (int64_t)blockIdx.x * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int64_t tile = FWD ? p : ntiles - 1 - p;
+    const int64_t base = tile * STILE;
+    stage_tile<FWD, D>(sv, lu, n, vin, vsc, base);
+    __syncthreads();
+    const Map<D> my = thread_map<FWD, D>(sv, base, n);
+    Map<D> agg;
+    const Map<D> pre = block_prefix<FWD, D>(my, wtot, agg);
+    double st[D];
+    apply<D>(pre, s0, st);
 #pragma unroll
     for (int rr = 0; rr < SR; ++rr) {
       const int r = FWD ? rr : (SR - 1 - rr);
@@ -435,13 +487,15 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
 #pragma unroll
       for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
       const double u0 = FWD ? 1.0 : su0[sidx];
-      const double y = rec_step<FWD, D>(sv[sidx], c, s, u0);
-      push_state<D>(s, y);
+      const double y = rec_step<FWD, D>(sv[sidx], c, st, u0);
+      push_state<D>(st, y);
       sv[sidx] = y;
     }
-  }
-  __syncthreads();
-  if (out != nullptr)
+    double s1[D];                                   // the state after this tile
+    apply<D>(agg, s0, s1);
+#pragma unroll
+    for (int i = 0; i < D; ++i) s0[i] = s1[i];
+    __syncthreads();
     for (int q = t; q < STILE; q += STPB) {
       const int64_t i = base + q;
       if (i < n) {
@@ -449,16 +503,7 @@ __global__ void __launch_bounds__(STPB) sweep_kernel(const double* __restrict__ 
         out[i] = addend ? addend[i] + y : y;
       }
     }
-  // the last block re-arms the ticket counter and advances the epoch
-  if (t == 0) {
-    __threadfence();
-    unsigned long long done = atomicAdd(ctl + 2, 1ull);
-    if (done == (unsigned long long)ntiles - 1) {
-      ctl[2] = 0ull;
-      ctl[0] = 0ull;
-      ctl[1] = epoch + 1;
-      __threadfence();
-    }
+    __syncthreads();
   }
 }
 
@@ -477,14 +522,25 @@ template <bool FWD, int D>
 void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
                   double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out) {
   const int64_t ntiles = (n + STILE - 1) / STILE;
-  const size_t smem = (size_t)(1 + D + (FWD ? 0 : 1)) * STPB * SPAD * sizeof(double);
+  const size_t smem = TileSmem<FWD, D>::BYTES;
+  const size_t ssmem = (size_t)SCAN_T * sizeof(Map<D>);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(sweep_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tile_map_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tile_apply_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tile_scan_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
     attr_set = true;
   }
-  sweep_kernel<FWD, D><<<(unsigned)ntiles, STPB, smem, s>>>(lu, n, v, vs, add, out, sc.states,
-                                                        sc.tickets + 8, sc.tickets, s_in0, s_out);
+  // ranges: at most SCAN_T blocks (2 resident per SM), each a contiguous run of L tiles
+  int64_t nb = ntiles < 148 * 2 * 3 ? ntiles : 148 * 2 * 3;
+  if (nb > SCAN_T) nb = SCAN_T;
+  if (nb < 1) nb = 1;
+  const int64_t L = (ntiles + nb - 1) / nb;
+  nb = (ntiles + L - 1) / L;
+  if (ntiles > 0) tile_map_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, L, sc.states);
+  tile_scan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>(ntiles > 0 ? (int)nb : 0, sc.states, s_in0, s_out);
+  if (out != nullptr && ntiles > 0)
+    tile_apply_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
 }
 
 void sweep(bool fwd, int d, const double* lu, int64_t n, const double* v, const double* vs,
