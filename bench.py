@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-size", type=int, default=128)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas instead of one z-slab-sharded problem")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 MREP / banded-solve kernel sweep point")
+    ap.add_argument("--c5-log2n", type=int, default=26)
     return ap.parse_args()
 
 
@@ -131,6 +135,54 @@ def cpu_baseline(size, budget_s=20.0):
                       f"= {iters} iterations in {t:.1f} s, literal MGS, 1 host thread"}
 
 
+def c5_point(log2n, m, d, peak):
+    """One C5 sweep point (BASELINE configs[4]): MREP fit, banded factor and two-sweep solve on
+    device-generated probes (inputs.c5_torch recipe), each timed with CUDA events."""
+    import torch
+
+    from paper_1308_5626_b200 import inputs, pspgmres as P
+    n = 1 << log2n
+    g = inputs.c5_torch(n, m, d, seed=0)
+    scratch = P.raw_scratch(n, d)
+    s = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    fit = {}
+
+    def do_fit():
+        fit.update(P.psp_mrep_fit_raw(g["px"], g["py"], d, scratch=scratch, want_kind=False))
+    t_fit = timed(do_fit, 3)
+    bands = fit["bands"]
+    lu_box = {}
+
+    def do_factor():
+        lu_box["st"], lu_box["lu"] = P.psp_banded_factor_raw(bands, d, scratch=scratch)
+    t_fac = timed(do_factor, 1)
+    z = torch.empty_like(g["v"])
+    t_sol = timed(lambda: P.psp_banded_solve_raw(lu_box["lu"], d, g["v"], scratch=scratch, out=z), 10)
+    b_fit, b_sol, b_fac = 16 * m + 8 * (2 * d + 1), 8 * (2 * d + 5), 16 * (2 * d + 1)
+
+    def rl(b, t):
+        ach = b * n / (t / 1e3) / 1e9
+        return {"ms": t, "rows_per_s": n / (t / 1e3), "bytes_per_row": b, "achieved_GBps": ach,
+                "frac": ach / peak}
+    out = {"workload": f"C5 (BASELINE configs[4]) n=2^{log2n}, m={m}, d={d}", "gate_accepted": fit["gate_accepted"],
+           "mrep_fit": rl(b_fit, t_fit), "banded_factor": rl(b_fac, t_fac), "banded_solve": rl(b_sol, t_sol)}
+    del g, scratch, bands, lu_box, z
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -189,17 +241,35 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    # ---- workload: C4, one independent replica per rank ----
+    # ---- workload: C4 512^3.  N > 1: one problem, z-slab sharded over the ranks (SURVEY 8(e):
+    #      halo planes by NCCL send/recv, all-reduced Arnoldi scalars); --replicas: one
+    #      independent replica per rank ----
     t_gen = time.perf_counter()
     prob = inputs.c4(n=args.size, steps=args.warmup + args.steps)
     t_gen = time.perf_counter() - t_gen
     n = prob.op.rows
+    sharded = world > 1 and not args.replicas
+    comm = None
+    if sharded:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(P.psp_comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = P.psp_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
     ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
     opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2, fused=args.fused)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=stream)
-        u = torch.as_tensor(prob.u0).cuda()
+        if sharded:
+            ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=stream,
+                            comm=comm, nranks=world, rank=rank)
+            u = torch.as_tensor(prob.u0[ctx.row0:ctx.row0 + ctx.n]).cuda()
+        else:
+            ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=stream)
+            u = torch.as_tensor(prob.u0).cuda()
+    n_local = ctx.n
+    prob.u0 = None
+    prob.op.field = None
     stream.synchronize()
 
     def barrier():
@@ -235,8 +305,9 @@ def main():
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
+        # sharded: every rank iterates the same global problem (n unknowns); replicas: sum
         it = torch.tensor([float(n * iters)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+        dist.all_reduce(it, op=dist.ReduceOp.MAX if sharded else dist.ReduceOp.SUM)
         total_unknown_iters = float(it.item())
     else:
         total_unknown_iters = float(n * iters)
@@ -268,7 +339,7 @@ def main():
     # ---- e2e: same metric through the C ABI with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        host = torch.empty(n, dtype=torch.float64).pin_memory()
+        host = torch.empty(n_local, dtype=torch.float64).pin_memory()
         host.copy_(u.cpu())
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -291,9 +362,10 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
             it = torch.tensor([tot], dtype=torch.float64, device="cuda")
-            dist.all_reduce(it, op=dist.ReduceOp.SUM)
+            dist.all_reduce(it, op=dist.ReduceOp.MAX if sharded else dist.ReduceOp.SUM)
             tot = float(it.item())
-        e2e = {"value": tot / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n}
+        e2e = {"value": tot / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,
+               "d2h_bytes_per_step": 8 * n_local}
         ctx.psp_kernel_stats(reset=True)
 
     line = None
@@ -303,13 +375,14 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C4: 3-D variable-kappa diffusion {args.size}^3 (BASELINE configs[3]), "
                                    "one implicit-Euler PSP-GMRES time step (solve + MREP fit + gate + factor)",
                        "grid": [args.size] * 3, "n": n, "d": prob.d, "restart": prob.restart, "tol": prob.tol,
                        "m_max": prob.m_max, "ortho": args.ortho + ("-fused" if args.fused else ""), "dt": prob.op.dt,
                        "l2": "inputs larger than L2 (each vector 8n bytes >> 126 MB); no flush needed",
-                       "parallelism": "replicas" if world > 1 else "single"},
+                       "parallelism": (f"z-slab x{world} (NCCL halo + all-reduce)" if sharded else
+                                       ("replicas" if world > 1 else "single"))},
             "iterations_per_step": [r["iterations"] for r in reps],
             "cycles_per_step": [r["cycles"] for r in reps],
             "precond_identity_per_step": [r["precond_identity"] for r in reps],
@@ -326,8 +399,37 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample_size)
-        print(json.dumps(line), flush=True)
     ctx.close()
+    if comm is not None:
+        P.psp_comm_destroy(comm)
+    del ctx, u
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    if line is not None and world == 1 and not args.no_c5:
+        # the north star's per-kernel targets (matvec from the C4 step above; MREP fit and the
+        # banded solve on a C5 point, where the gate accepts N)
+        try:
+            c5 = c5_point(args.c5_log2n, 32, 3, peak)
+        except Exception as e:  # noqa: BLE001 -- the C4 line stands; say what failed
+            c5 = {"error": f"{type(e).__name__}: {e}"[:300]}
+            line["c5"] = c5
+            print(json.dumps(line), flush=True)
+            if dist is not None:
+                dist.destroy_process_group()
+            return 0
+        line["c5"] = c5
+        mv = kstats.get("matvec", {})
+        line["kernel_rooflines"] = {
+            "matvec": {"achieved_GBps": kernel_table.get("matvec", {}).get("GBps"), "peak": peak,
+                       "frac": (kernel_table.get("matvec", {}).get("GBps") or 0.0) / peak,
+                       "bytes_per_row": 32, "workload": "C4 step (probe copy fused)"} if mv else None,
+            "mrep_fit": {"achieved_GBps": c5["mrep_fit"]["achieved_GBps"], "peak": peak,
+                         "frac": c5["mrep_fit"]["frac"], "workload": c5["workload"]},
+            "banded_solve": {"achieved_GBps": c5["banded_solve"]["achieved_GBps"], "peak": peak,
+                             "frac": c5["banded_solve"]["frac"], "workload": c5["workload"]}}
+    if line is not None:
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
