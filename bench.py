@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=512, help="grid points per axis (512 = C4)")
     ap.add_argument("--ortho", default="1reduce", choices=["1reduce", "literal"])
-    ap.add_argument("--fused", type=int, default=0, help="1: single-pass fused Arnoldi step (N = I)")
+    ap.add_argument("--fused", type=int, default=1,
+                    help="1: ring-resident Krylov basis, steps fused_kmin..fused_kmax as one fused pass; 0: split passes")
+    ap.add_argument("--fused-kmin", type=int, default=None)
+    ap.add_argument("--fused-kmax", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-size", type=int, default=128)
@@ -257,7 +260,12 @@ def main():
         dist.broadcast(uid, 0)
         comm = P.psp_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
     ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
-    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2, fused=args.fused)
+    fk = {}
+    if args.fused_kmin is not None:
+        fk["fused_kmin"] = args.fused_kmin
+    if args.fused_kmax is not None:
+        fk["fused_kmax"] = args.fused_kmax
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, ortho=ortho, timing=2, fused=args.fused, **fk)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         if sharded:
@@ -379,7 +387,9 @@ def main():
             "config": {"workload": f"C4: 3-D variable-kappa diffusion {args.size}^3 (BASELINE configs[3]), "
                                    "one implicit-Euler PSP-GMRES time step (solve + MREP fit + gate + factor)",
                        "grid": [args.size] * 3, "n": n, "d": prob.d, "restart": prob.restart, "tol": prob.tol,
-                       "m_max": prob.m_max, "ortho": args.ortho + ("-fused" if args.fused else ""), "dt": prob.op.dt,
+                       "m_max": prob.m_max,
+                       "ortho": args.ortho + (f"-ring(fused k={opts.fused_kmin}..{opts.fused_kmax})" if args.fused else "-split"),
+                       "dt": prob.op.dt,
                        "l2": "inputs larger than L2 (each vector 8n bytes >> 126 MB); no flush needed",
                        "parallelism": (f"z-slab x{world} (NCCL halo + all-reduce)" if sharded else
                                        ("replicas" if world > 1 else "single"))},

@@ -85,9 +85,15 @@ typedef struct {
   int32_t ortho;                   /* PSP_MGS_*; default PSP_MGS_1REDUCE                    */
   int32_t gate;                    /* apply the R21 dominance gate; default 1               */
   int32_t timing;                  /* record per-phase CUDA-event times in the report       */
-  int32_t fused;                   /* with N = I and ICWY MGS, run each Arnoldi step as one  */
-                                   /* fused pass (update + matvec + dots, DESIGN.md s.6);    */
-                                   /* default 0 (opt-in: latency-bound in this version)      */
+  int32_t fused;                   /* with N = I and ICWY MGS, keep the Krylov basis in the  */
+                                   /* probe ring (no probe copies) and run steps              */
+                                   /* fused_kmin <= k <= fused_kmax as one fused pass         */
+                                   /* (update + matvec + dots, DESIGN.md s.6), the other      */
+                                   /* steps as update / matvec / dots passes on the ring;     */
+                                   /* default 1                                               */
+  int32_t fused_kmin;              /* first step run as a fused pass; default 2               */
+  int32_t fused_kmax;              /* last step run as a fused pass; default 16 (wider steps  */
+                                   /* hold more basis tiles than shared memory stages well)   */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */

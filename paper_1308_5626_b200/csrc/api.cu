@@ -266,7 +266,9 @@ void psp_default_opts(psp_opts* o) {
   o->ortho = PSP_MGS_1REDUCE;
   o->gate = 1;
   o->timing = 0;
-  o->fused = 0;  // the fused pass is correct but latency-bound: opt-in
+  o->fused = 1;
+  o->fused_kmin = 2;
+  o->fused_kmax = 16;
 }
 
 const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }
@@ -546,10 +548,11 @@ Basis basis(const psp_ctx* c) {
   if (c->cycle_fused) return Basis{c->ring_px, c->n, c->vslot[1], c->ring_phys};
   return Basis{c->V, c->ldv, 0, c->nA + 1};
 }
+// a ring-resident cycle: the Krylov basis lives in the probe ring (single rank: the fused pass
+// would need the halo planes of u in the middle of the pass)
 bool fused_eligible(const psp_ctx* c) {
-  // (multi-rank: the fused pass would need the halo planes of u in the middle of the pass)
   return c->opts.fused && !c->multi && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE &&
-         c->ring_cap >= c->nA + 1 && fused_supported(c->st, c->nA);
+         c->ring_cap >= c->nA + 1;
 }
 
 // y = A (xs x) [+ probe copy]; multi-rank: first the slab halo planes of x from rank-1 / rank+1
@@ -653,6 +656,38 @@ psp_status psp_precond_apply(psp_ctx* c, const double* v, double* z) {
   return check_cuda(c, "psp_precond_apply");
 }
 
+// step k of a ring-resident cycle as one fused pass (update + matvec + dots) or as separate
+// passes: the policy of opts.fused_kmin / fused_kmax
+static bool fused_pass(const psp_ctx* c, int k) {
+  return k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, c->nA);
+}
+
+// The ring-resident step without the fused pass (k = 0: the cycle start, V(:,1) already in its
+// slot): [k >= 1: V(:,k+1) = alpha_k w~_k - sum_j h_j alpha_j V(:,j) into the next slot, H(k+1,k),
+// Givens, alpha_{k+1} (l.13-32)]; w~_{k+1} = A V(:,k+1) unnormalised into the slot's P_y
+// (l.11-12, no probe copy); the MGS coefficients of step k+1 (l.13-16 / R11).
+static psp_status ring_split_step(psp_ctx* c, int k, int src_slot, int dst) {
+  const int64_t n = c->n;
+  const double dn = (double)n;
+  int h;
+  if (k >= 1) {
+    h = kt_begin(c);
+    launch_icwy_update(basis(c), py_col(c, src_slot), c->ds.alpha + (k - 1), px_col(c, dst), k, c->nA, n, c->ds,
+                       c->rc, c->stream);
+    kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+    c->launches += 1;
+  }
+  cudaMemcpyAsync(c->slot_scale + dst, c->ds.alpha + k, sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  h = kt_begin(c);
+  PSP_TRY(matvec(c, px_col(c, dst), nullptr, py_col(c, dst), nullptr));
+  kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
+  h = kt_begin(c);
+  launch_icwy_dots(basis(c), py_col(c, dst), k + 1, c->nA, n, 1, c->ds, c->rc, c->stream);
+  kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 2) * dn);
+  c->launches += 1;
+  return PSP_OK;
+}
+
 // algorithmic bytes of the fused pass of step k (k = 0: the cycle-start pass)
 static double fused_bytes(const psp_ctx* c, int k) {
   const bool cell = c->st.kind == PSP_OP_CELL_DIFF || c->st.kind == PSP_OP_CELL_ADVDIFF;
@@ -692,12 +727,16 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   if (h_beta) *h_beta = beta;
   if (c->cycle_fused && beta > 0.0 && isfinite(beta)) {
     // cycle-start pass: A V(:,1) -> P_y of the next slot and step 1's MGS coefficient
-    h = kt_begin(c);
-    const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, 0, c->nA, c->vslot[1], 1,
-                                nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream);
-    if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
-    kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
-    c->launches += 1;
+    if (fused_pass(c, 0)) {
+      h = kt_begin(c);
+      const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, 0, c->nA, c->vslot[1],
+                                  1, nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream);
+      if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+      kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
+      c->launches += 1;
+    } else {
+      PSP_TRY(ring_split_step(c, 0, c->vslot[1], c->vslot[1]));
+    }
   }
   c->last_k = 0;
   return check_cuda(c, "psp_cycle_begin");
@@ -716,20 +755,26 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
     const int slot = ring_next(c);
     if (slot != c->vslot[k]) return fail(c, PSP_E_ARG, "psp_arnoldi_step: steps out of order (fused cycle)");
     if (k < c->nA) {
-      // l.13-18 of step k, then l.10-16 of step k+1, in one pass
+      // l.13-18 of step k, then l.10-16 of step k+1: one fused pass or three ring passes
       const int dst = ring_peek(c);
       c->vslot[k + 1] = dst;
-      h = kt_begin(c);
-      const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, slot, 0,
-                                  px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream);
-      if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
-      kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
+      if (fused_pass(c, k)) {
+        h = kt_begin(c);
+        const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, slot, 0,
+                                    px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream);
+        if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+        kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
+        c->launches += 1;
+      } else {
+        PSP_TRY(ring_split_step(c, k, slot, dst));
+      }
     } else {
       // the last step of the cycle: only H(k+1,k) = ||U|| is needed (V(:,k+1) is never used)
       h = kt_begin(c);
       launch_icwy_update(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds,
                          c->rc, c->stream);
       kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+      c->launches += 1;
     }
     c->launches += 1;
   } else {
@@ -767,7 +812,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
       c->launches += k + 1;
     } else {
       h = kt_begin(c);
-      launch_icwy_dots(basis(c), py, k, c->nA, n, c->ds, c->rc, c->stream);
+      launch_icwy_dots(basis(c), py, k, c->nA, n, 0, c->ds, c->rc, c->stream);
       PSP_TRY(finish_reduce(c, EPI_DOTS, 2 * k - 1, k, 0, 0));
       kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 1) * dn);
       h = kt_begin(c);

@@ -76,7 +76,8 @@ struct DevState {
 };
 // scalar epilogues of the grid reductions (krylov.cu); multi-rank runs them as a 1-thread
 // kernel on the all-reduced ds.rpart
-enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5 };
+// EPI_DOTS_RAW: the ring-resident step, w = A V_k unnormalised (scale alpha_k), so h_j carries alpha_k too
+enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5, EPI_DOTS_RAW = 6 };
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s);
 enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
        SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_NSCAL = 16 };
@@ -111,7 +112,8 @@ void launch_mgs_literal(const double* src, double* U, const double* Vprev, const
 void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_t n,
                               DevState ds, const RedCfg& rc, cudaStream_t s);
 // ICWY one-reduction MGS (R11): pass A = dots V_j'w (j<=k), V_j'V_k (j<k); solve (I+L)h = s
-void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n,
+// w_raw: w = A V(:,k) unnormalised (ring-resident basis), h_j = alpha_j alpha_k V_j'w
+void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n, int w_raw,
                       DevState ds, const RedCfg& rc, cudaStream_t s);
 // pass B = U = w - sum_j h_j V_j ; H(k+1,k) = ||U|| ; Givens update
 void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,

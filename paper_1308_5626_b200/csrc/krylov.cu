@@ -103,13 +103,14 @@ __device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, 
       ds.H[(int64_t)(k - 1) * ld + k] = sqrt(tot[0]);
       givens_update(ds, k, nA);
       break;
-    case EPI_DOTS: {  // ICWY: the new row of L and (I + L) h = s (R11)
+    case EPI_DOTS:
+    case EPI_DOTS_RAW: {  // ICWY: the new row of L and (I + L) h = s (R11)
       const double ak = ds.alpha[k - 1];
       double* Lrow = ds.Lm + (int64_t)(k - 1) * ld;
       for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = ds.alpha[jb] * ak * tot[k + jb];
       double* Hc = ds.H + (int64_t)(k - 1) * ld;
-      for (int jb = 0; jb < k; ++jb) {  // s_j = alpha_j V_j'w
-        double h = ds.alpha[jb] * tot[jb];
+      for (int jb = 0; jb < k; ++jb) {  // s_j = alpha_j V_j'w (raw w: alpha_j alpha_k V_j'w~)
+        double h = (kind == EPI_DOTS_RAW) ? ds.alpha[jb] * ak * tot[jb] : ds.alpha[jb] * tot[jb];
         const double* Lr = ds.Lm + (int64_t)jb * ld;
         for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
         Hc[jb] = h;
@@ -306,7 +307,7 @@ __device__ __forceinline__ void dots_tile(const double* const* cp,
 }
 __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
                                                         const double* __restrict__ w, int k,
-                                                        int nA, int64_t n, DevState ds) {
+                                                        int nA, int64_t n, int w_raw, DevState ds) {
   __shared__ double accw[kWarps][2 * kMaxRestart];
   __shared__ const double* cp[kMaxRestart + 1];   // V(:,j) resolved once (ring slots)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
       if (lane == 0) tot[q] = s;
     }
     __syncthreads();
-    if (t == 0) finish_scalar(ds, EPI_DOTS, k, nA, 0, 0, tot, nv);
+    if (t == 0) finish_scalar(ds, w_raw ? EPI_DOTS_RAW : EPI_DOTS, k, nA, 0, 0, tot, nv);
   }
 }
 
@@ -500,15 +501,31 @@ void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_
                               DevState ds, const RedCfg& rc, cudaStream_t s) {
   mgs_literal_final_kernel<<<rc.nblocks, TPB, 0, s>>>(U, Vk, k, nA, n, ds);
 }
-void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n,
+// one full wave: the resident blocks per SM of a kernel (a partial second wave of a
+// grid-stride kernel leaves SMs idle for up to a third of the launch)
+template <typename K>
+int wave_blocks(K kernel, int cap) {
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, TPB, 0) != cudaSuccess || per < 1) per = 1;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int b = per * sms;
+  return b < cap ? b : cap;
+}
+
+void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n, int w_raw,
                       DevState ds, const RedCfg& rc, cudaStream_t s) {
-  // grid: 4 blocks per SM for the dots, 8 for the update (measured best, tools/ortho_micro.cu)
-  icwy_dots_kernel<<<tiles_grid(n, rc.nblocks / 2), TPB, 0, s>>>(V, w, k, nA, n, ds);
+  static int wave = 0;
+  if (!wave) wave = wave_blocks(icwy_dots_kernel, rc.nblocks);
+  icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, k, nA, n, w_raw, ds);
 }
 void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
+  static int wave = 0;
+  if (!wave) wave = wave_blocks(icwy_update_kernel, rc.nblocks);
   int64_t ub = (n + UTILE - 1) / UTILE;
-  if (ub > rc.nblocks) ub = rc.nblocks;
+  if (ub > wave) ub = wave;
   icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds);
 }
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s) {
@@ -516,8 +533,10 @@ void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cuda
 }
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {
+  static int wave = 0;
+  if (!wave) wave = wave_blocks(combine_kernel, 148 * 8);
   int64_t cb = (n + UTILE - 1) / UTILE;
-  if (cb > 148 * 8) cb = 148 * 8;
+  if (cb > wave) cb = wave;
   combine_kernel<<<(int)(cb < 1 ? 1 : cb), TPB, 0, s>>>(V, k, nA, base, out, n, ds);
 }
 

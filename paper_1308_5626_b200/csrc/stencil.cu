@@ -9,7 +9,7 @@
 #include "internal.h"
 
 #ifndef PSP_MARCH_MINB
-#define PSP_MARCH_MINB 2   // resident blocks per SM of the vectorised march kernel
+#define PSP_MARCH_MINB 3   // resident blocks per SM of the vectorised march kernel
 #endif
 
 namespace psp {
@@ -247,7 +247,6 @@ __global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
   constexpr bool HASY = BY > 1;
   constexpr int TW = 64;
-  constexpr int Q = 5;                                       // register ring: planes z-1 .. z+3
   const double* __restrict__ f = v.field;
   const int lane = threadIdx.x, ty = threadIdx.y;
   const int64_t i = (int64_t)blockIdx.x * TW + 2 * lane;    // first of this thread's two points
@@ -259,14 +258,11 @@ __global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march
   const int64_t col = in ? i + v.nx * j : 0;                 // outside: loads of point 0, no stores
   const bool has_w = i > 0, has_e = i + 2 < v.nx;
   const bool has_s = HASY && in && j > 0, has_n = HASY && in && j + 1 < v.ny;
-  const bool ldw = lane == 0 && in && has_w, lde = lane == 31 && in && has_e;
   const bool lo_in = v.x_lo != nullptr, hi_in = v.x_hi != nullptr;
   const double xs = xsp ? *xsp : 1.0;
   const double hs0 = 0.5 * v.s[0], hs1 = 0.5 * v.s[1], hs2 = 0.5 * v.s[2];
   const double s0c = v.s[0], s1c = v.s[1], s2c = v.s[2];
-  const int64_t nx = v.nx;
 
-  // plane p of this thread's column (halo planes beyond the slab; zero beyond the domain)
   auto ld2 = [&](const double* a, const double* lo, const double* hi, int64_t p) -> double2 {
     if (p >= 0 && p < v.nz) return __ldg(reinterpret_cast<const double2*>(a + col + plane * p));
     if (p < 0 && lo) return __ldg(reinterpret_cast<const double2*>(lo + col));
@@ -274,99 +270,95 @@ __global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march
     return make_double2(0.0, 0.0);
   };
   const double2 zero2 = make_double2(0.0, 0.0);
-  double2 qx[Q], qf[Q];   // slot (p - z0 + 1) mod Q holds plane p
-#pragma unroll
-  for (int k = 0; k < Q - 1; ++k) {
-    qx[k] = ld2(x, v.x_lo, v.x_hi, z0 - 1 + k);
-    qf[k] = cell ? ld2(f, v.f_lo, v.f_hi, z0 - 1 + k) : zero2;
+  double2 xb = ld2(x, v.x_lo, v.x_hi, z0 - 1), xc = ld2(x, v.x_lo, v.x_hi, z0);
+  double2 xt = ld2(x, v.x_lo, v.x_hi, z0 + 1), xt2 = ld2(x, v.x_lo, v.x_hi, z0 + 2);
+  double2 fb = zero2, fc = zero2, ft = zero2, ft2 = zero2;
+  if (cell) {
+    fb = ld2(f, v.f_lo, v.f_hi, z0 - 1); fc = ld2(f, v.f_lo, v.f_hi, z0);
+    ft = ld2(f, v.f_lo, v.f_hi, z0 + 1); ft2 = ld2(f, v.f_lo, v.f_hi, z0 + 2);
   }
-  qx[Q - 1] = zero2;
-  qf[Q - 1] = zero2;
-  const double* px = x + col;
-  const double* pf = f + col;
-  double* py = y + col;
-  double* pc = xcopy ? xcopy + col : nullptr;
+  const double* px3 = x + col + plane * (z0 + 3);
+  const double* pf3 = f + col + plane * (z0 + 3);
+  const double* pxz = x + col + plane * z0;                  // plane z (in-plane neighbour loads)
+  const double* pfz = f + col + plane * z0;
+  double* py = y + col + plane * z0;
+  double* pc = xcopy ? xcopy + col + plane * z0 : nullptr;
 
-  for (int64_t zz = z0; zz < z1; zz += Q) {
-#pragma unroll
-    for (int u = 0; u < Q; ++u) {
-      const int64_t z = zz + u;
-      if (z >= z1) break;                                    // uniform
-      const int sb = u % Q, sc = (u + 1) % Q, st = (u + 2) % Q, s3 = (u + 4) % Q;
-      const int64_t g = plane * z;
-      // prefetch plane z+3
-      if (z + 3 < v.nz) {
-        qx[s3] = __ldg(reinterpret_cast<const double2*>(px + g + 3 * plane));
-        if (cell) qf[s3] = __ldg(reinterpret_cast<const double2*>(pf + g + 3 * plane));
-      } else {
-        qx[s3] = ld2(x, v.x_lo, v.x_hi, z + 3);
-        if (cell) qf[s3] = ld2(f, v.f_lo, v.f_hi, z + 3);
-      }
-      const double2 xc = qx[sc], fc = qf[sc];
-      double2 xb = qx[sb], fb = qf[sb], xt = qx[st], ft = qf[st];
-      // in-plane y neighbours (L1 / L2): missing -> x = 0, k = k_c
-      double2 xsn = zero2, xnn = zero2, fsn = fc, fnn = fc;
-      if (has_s) {
-        xsn = __ldg(reinterpret_cast<const double2*>(px + g - nx));
-        if (cell) fsn = __ldg(reinterpret_cast<const double2*>(pf + g - nx));
-      }
-      if (has_n) {
-        xnn = __ldg(reinterpret_cast<const double2*>(px + g + nx));
-        if (cell) fnn = __ldg(reinterpret_cast<const double2*>(pf + g + nx));
-      }
-      // x neighbours: the adjacent lanes' points; lanes 0 / 31 load across the tile edge
-      double xw = __shfl_up_sync(0xffffffffu, xc.y, 1), xe = __shfl_down_sync(0xffffffffu, xc.x, 1);
-      double fw = 0.0, fe = 0.0;
-      if (cell) {
-        fw = __shfl_up_sync(0xffffffffu, fc.y, 1);
-        fe = __shfl_down_sync(0xffffffffu, fc.x, 1);
-      }
-      if (ldw) { xw = __ldg(px + g - 1); if (cell) fw = __ldg(pf + g - 1); }
-      if (lde) { xe = __ldg(px + g + 2); if (cell) fe = __ldg(pf + g + 2); }
-      if (!has_w) { xw = 0.0; fw = fc.x; }
-      if (!has_e) { xe = 0.0; fe = fc.y; }
-      // slab-axis boundary (uniform per block)
-      if (z == 0 && !lo_in) fb = fc;
-      if (z + 1 == v.nz && !hi_in) ft = fc;
-      auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
-                       double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
-        double acc = 0.0;
-        if (cell) {
-          acc = fma(hs0 * (k + fwv), c - xwv, acc);
-          acc = fma(hs0 * (k + fev), c - xev, acc);
-        } else {
-          acc = fma(s0c, c - xwv, acc);
-          acc = fma(s0c, c - xev, acc);
-        }
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
-        if (HASY) {
-          if (cell) {
-            acc = fma(hs1 * (k + fsv), c - xsv, acc);
-            acc = fma(hs1 * (k + fnv), c - xnv, acc);
-          } else {
-            acc = fma(s1c, c - xsv, acc);
-            acc = fma(s1c, c - xnv, acc);
-          }
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
-        }
-        if (cell) {
-          acc = fma(hs2 * (k + fbv), c - xbv, acc);
-          acc = fma(hs2 * (k + ftv), c - xtv, acc);
-        } else {
-          acc = fma(s2c, c - xbv, acc);
-          acc = fma(s2c, c - xtv, acc);
-        }
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
-        return xs * (c + acc);
-      };
-      if (in) {
-        double2 out;
-        out.x = point(xc.x, fc.x, xw, fw, xc.y, fc.y, xsn.x, fsn.x, xnn.x, fnn.x, xb.x, fb.x, xt.x, ft.x);
-        out.y = point(xc.y, fc.y, xc.x, fc.x, xe, fe, xsn.y, fsn.y, xnn.y, fnn.y, xb.y, fb.y, xt.y, ft.y);
-        *reinterpret_cast<double2*>(py + g) = out;
-        if (pc) *reinterpret_cast<double2*>(pc + g) = make_double2(xs * xc.x, xs * xc.y);
-      }
+  for (int64_t z = z0; z < z1; ++z) {
+    double2 xt3 = zero2, ft3 = zero2;
+    if (z + 3 < v.nz) {
+      xt3 = __ldg(reinterpret_cast<const double2*>(px3));
+      if (cell) ft3 = __ldg(reinterpret_cast<const double2*>(pf3));
+    } else if (z + 3 == v.nz) {
+      xt3 = ld2(x, v.x_lo, v.x_hi, z + 3);
+      if (cell) ft3 = ld2(f, v.f_lo, v.f_hi, z + 3);
     }
+    // in-plane y neighbours (L1 / L2): missing -> x = 0, k = k_c
+    double2 xsn = zero2, xnn = zero2, fsn = fc, fnn = fc;
+    if (has_s) {
+      xsn = __ldg(reinterpret_cast<const double2*>(pxz - v.nx));
+      if (cell) fsn = __ldg(reinterpret_cast<const double2*>(pfz - v.nx));
+    }
+    if (has_n) {
+      xnn = __ldg(reinterpret_cast<const double2*>(pxz + v.nx));
+      if (cell) fnn = __ldg(reinterpret_cast<const double2*>(pfz + v.nx));
+    }
+    // x neighbours: the adjacent lanes' points; lanes 0 / 31 load across the tile edge
+    double xw = __shfl_up_sync(0xffffffffu, xc.y, 1), xe = __shfl_down_sync(0xffffffffu, xc.x, 1);
+    double fw = 0.0, fe = 0.0;
+    if (cell) {
+      fw = __shfl_up_sync(0xffffffffu, fc.y, 1);
+      fe = __shfl_down_sync(0xffffffffu, fc.x, 1);
+    }
+    if (lane == 0 && in && has_w) { xw = __ldg(pxz - 1); if (cell) fw = __ldg(pfz - 1); }
+    if (lane == 31 && in && has_e) { xe = __ldg(pxz + 2); if (cell) fe = __ldg(pfz + 2); }
+    if (!has_w) { xw = 0.0; fw = fc.x; }
+    if (!has_e) { xe = 0.0; fe = fc.y; }
+    // slab-axis boundary (uniform per block)
+    if (z == 0 && !lo_in) fb = fc;
+    if (z + 1 == v.nz && !hi_in) ft = fc;
+    auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
+                     double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
+      double acc = 0.0;
+      if (cell) {
+        acc = fma(hs0 * (k + fwv), c - xwv, acc);
+        acc = fma(hs0 * (k + fev), c - xev, acc);
+      } else {
+        acc = fma(s0c, c - xwv, acc);
+        acc = fma(s0c, c - xev, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
+      if (HASY) {
+        if (cell) {
+          acc = fma(hs1 * (k + fsv), c - xsv, acc);
+          acc = fma(hs1 * (k + fnv), c - xnv, acc);
+        } else {
+          acc = fma(s1c, c - xsv, acc);
+          acc = fma(s1c, c - xnv, acc);
+        }
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
+      }
+      if (cell) {
+        acc = fma(hs2 * (k + fbv), c - xbv, acc);
+        acc = fma(hs2 * (k + ftv), c - xtv, acc);
+      } else {
+        acc = fma(s2c, c - xbv, acc);
+        acc = fma(s2c, c - xtv, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
+      return xs * (c + acc);
+    };
+    if (in) {
+      double2 out;
+      out.x = point(xc.x, fc.x, xw, fw, xc.y, fc.y, xsn.x, fsn.x, xnn.x, fnn.x, xb.x, fb.x, xt.x, ft.x);
+      out.y = point(xc.y, fc.y, xc.x, fc.x, xe, fe, xsn.y, fsn.y, xnn.y, fnn.y, xb.y, fb.y, xt.y, ft.y);
+      *reinterpret_cast<double2*>(py) = out;
+      if (pc) *reinterpret_cast<double2*>(pc) = make_double2(xs * xc.x, xs * xc.y);
+    }
+    px3 += plane; pf3 += plane; pxz += plane; pfz += plane; py += plane;
+    if (pc) pc += plane;
+    xb = xc; xc = xt; xt = xt2; xt2 = xt3;
+    fb = fc; fc = ft; ft = ft2; ft2 = ft3;
   }
 }
 

@@ -232,7 +232,10 @@ def test_mrep_insufficient_samples(torch, P):
 # ------------------------------------------------------------------------------------------
 # T4-T6: Algorithm 1 and the time-step driver
 # ------------------------------------------------------------------------------------------
-MODES = {"fused": dict(ortho=0, fused=1), "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
+MODES = {"fused": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=32),      # every step one fused pass
+         "ring": dict(ortho=0, fused=1),                                      # default mix on the ring
+         "ringsplit": dict(ortho=0, fused=1, fused_kmin=99, fused_kmax=0),   # ring, no fused pass
+         "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
 
 
 def run_gpu_steps(torch, P, prob, steps, mode):
