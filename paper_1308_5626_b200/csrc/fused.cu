@@ -118,17 +118,42 @@ struct FCfg {
   static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)2 * NT * 8 + 64 + 128;
 };
 
-template <int KIND, int TX, int TY, int KMAX>
-__global__ void __launch_bounds__(TX * TY, 1)
+// Half-warp transposing butterfly (CS = 2): v[0..7] per lane -> lane l holds the sum over the
+// 16 lanes of its half-warp of v[l & 7] (the halves own different basis columns).
+__device__ __forceinline__ double butterfly8_half(double (&v)[8], int lane) {
+#pragma unroll
+  for (int m = 4, h = 4; m >= 1; m >>= 1, h >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? v[j] : v[j + h];
+      const double keep = up ? v[j + h] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  double r = v[0];
+  r += __shfl_xor_sync(0xffffffffu, r, 8);
+  return r;
+}
+
+// CS = 2 (the widest steps): two threads per point, each owning half of the basis columns (the
+// two halves of a warp hold the same 16 points), so a 32 x 8 tile -- the largest whose stage
+// ring fits shared memory at k = 32 -- still runs 16 warps per SM.  The halves' partial MGS
+// updates meet by one shuffle; each half keeps the dot products of its own columns.
+template <int KIND, int TX, int TY, int KMAX, int CS>
+__global__ void __launch_bounds__(TX * TY * CS, 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap mpx, const __grid_constant__ CUtensorMap mpy,
                      const __grid_constant__ CUtensorMap mkap, FusedArgs a) {
   using Cfg = FCfg<TX, TY, KMAX>;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
   constexpr bool HASY = TY > 1;
-  constexpr int NT = Cfg::NT, NW = NT / 32, NST = Cfg::NST;
-  constexpr bool REG = KMAX <= 16;           // per-thread accumulators (else per-plane butterflies)
-  constexpr int NCH = (KMAX + 7) / 8;
-  constexpr int NACC = REG ? KMAX : NCH;
+  constexpr int NT = Cfg::NT, NST = Cfg::NST;      // NT points per tile
+  constexpr int NTH = NT * CS, NW = NTH / 32;       // threads
+  constexpr int KJ = KMAX / CS;                     // basis columns per thread
+  constexpr bool REG = KJ <= 16;           // per-thread accumulators (else per-plane butterflies)
+  constexpr int NCH = (KJ + 7) / 8;
+  constexpr int NACC = REG ? KJ : NCH;
+  static_assert(CS == 1 || CS == 2, "column split 1 or 2");
   extern __shared__ __align__(128) double fsm[];
   // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
   double* stages = fsm + (((128u - (su32(fsm) & 127u)) & 127u) >> 3);
@@ -140,7 +165,12 @@ __global__ void __launch_bounds__(TX * TY, 1)
   __shared__ bool s_last;
 
   const Stencil& st = a.st;
-  const int lx = threadIdx.x, ly = threadIdx.y, t = ly * TX + lx, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.y * TX + threadIdx.x, lane = t & 31, warp = t >> 5;
+  // this thread's point and column half
+  const int half = (CS == 2) ? (lane >> 4) : 0;
+  const int pt = (CS == 2) ? warp * 16 + (lane & 15) : t;
+  const int lx = pt % TX, ly = pt / TX;
+  const int j0 = half * KJ;
   const int k = a.k;
   const int ld = a.nA + 1;
   if (t < KMAX) {
@@ -148,8 +178,9 @@ __global__ void __launch_bounds__(TX * TY, 1)
     vslot[t] = (a.vs1 + t) % a.cap;
   }
   // columns j >= k are never loaded: zero them once in every stage (coefficient 0, product 0)
-  for (int s = 0; s < NST; ++s)
-    for (int j = k; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + t] = 0.0;
+  if (half == 0)
+    for (int s = 0; s < NST; ++s)
+      for (int j = k; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + pt] = 0.0;
   if (t == 0) {
     for (int q = 0; q < NST; ++q) mbar_init(bars + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -171,18 +202,19 @@ __global__ void __launch_bounds__(TX * TY, 1)
   const double hsx = 0.5 * st.s[0], hsy = 0.5 * st.s[1], hsz = 0.5 * st.s[2];
   const int64_t plane = st.nx * st.ny;
 
+  // products of this thread's columns with f (f = 0 for points that are not counted)
   auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, double f, double (&acc)[NACC]) {
     if (REG) {
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) acc[j] = fma(vcol[j * NT + t], f, acc[j]);
+      for (int j = 0; j < KJ; ++j) acc[j] = fma(vcol[(j0 + j) * NT + pt], f, acc[j]);
     } else {
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         if (c * 8 >= k) break;                   // uniform
         double v8[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v8[q] = vcol[(c * 8 + q) * NT + t] * f;
-        acc[c] += butterfly8(v8, lane);
+        for (int q = 0; q < 8; ++q) v8[q] = vcol[(j0 + c * 8 + q) * NT + pt] * f;
+        acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
       }
     }
   };
@@ -201,10 +233,10 @@ __global__ void __launch_bounds__(TX * TY, 1)
     const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
     const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
     const bool own = interior && in_grid;
+    const bool emit = own && half == 0;          // stores and the u / w~ scalars: one thread per point
     const int64_t col = in_grid ? gx + st.nx * gy : 0;
     const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
 
-    // stage of plane q (q from z0-1): (q - z0 + 1) % NST
     // warp 0: the boxes of plane q, one box per lane (lane 0 arms the barrier with the byte count)
     auto issue = [&](int64_t q) {
       const int si = (int)((q - z0 + 1) % NST);
@@ -224,12 +256,16 @@ __global__ void __launch_bounds__(TX * TY, 1)
       phase_bits ^= (1u << si);
       return stages + (size_t)si * Cfg::STAGE;
     };
-    auto form_u = [&](const double* sb) -> double {   // u at this thread's point of the staged plane
-      const double s0 = sb[KMAX * NT + t];
+    auto form_u = [&](const double* sb) -> double {   // u at this point of the staged plane
+      const double s0 = sb[KMAX * NT + pt];
       if (k == 0) return s0;
-      double u = wsc * s0;
+      double u = (half == 0) ? wsc * s0 : 0.0;
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) u = fma(-hs[j], sb[j * NT + t], u);
+      for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], sb[(j0 + j) * NT + pt], u);
+      if (CS == 2) {                             // the halves' partial updates, same sum on both
+        const double o = __shfl_xor_sync(0xffffffffu, u, 16);
+        u = (half == 0) ? u + o : o + u;
+      }
       return u;
     };
 
@@ -237,39 +273,44 @@ __global__ void __launch_bounds__(TX * TY, 1)
       for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
     // prologue: u(z0-1), u(z0) (+ l-products of plane z0)
     const double* sbm = wait_stage(z0 - 1);
-    double ub = (z0 >= 1 && in_grid) ? form_u(sbm) : 0.0;
-    double kb = cell ? sbm[(KMAX + 1) * NT + t] : 0.0;
+    double ub = form_u(sbm);
+    if (!(z0 >= 1 && in_grid)) ub = 0.0;
+    double kb = cell ? sbm[(KMAX + 1) * NT + pt] : 0.0;
     const double* sbc = wait_stage(z0);
-    double uc = in_grid ? form_u(sbc) : 0.0;
-    double kc = cell ? sbc[(KMAX + 1) * NT + t] : 0.0;
-    if (own && k > 0) a.dstx[col + plane * z0] = uc;
+    double uc = form_u(sbc);
+    if (!in_grid) uc = 0.0;
+    double kc = cell ? sbc[(KMAX + 1) * NT + pt] : 0.0;
+    int64_t g = col + plane * z0;                // this point's index at plane p
+    if (emit && k > 0) a.dstx[g] = uc;
     {
       const double f = own ? uc : 0.0;
-      nu = fma(f, f, nu);
+      if (half == 0) nu = fma(f, f, nu);
       if (k > 0) add_products(sbc, f, accl);
     }
-    Us[(z0 & 1) * NT + t] = uc;
+    if (half == 0) Us[(z0 & 1) * NT + pt] = uc;
     __syncthreads();                              // stage z0-1 consumed; Us(z0) visible
     if (warp == 0 && z0 - 1 + NST <= z1) issue(z0 - 1 + NST);
 
+    int sp_i = 1 % NST;                           // stage of plane p
     for (int64_t p = z0; p < z1; ++p) {
       const int bp = (int)(p & 1), bn = bp ^ 1;
       const int64_t pn = p + 1;
       // stage p (resident: t-dots, in-plane kappa), stage p+1 (u(p+1))
-      const double* sp = stages + (size_t)((p - z0 + 1) % NST) * Cfg::STAGE;
+      const double* sp = stages + (size_t)sp_i * Cfg::STAGE;
       double un = 0.0, kt = 0.0;
       if (pn <= z1) {                             // plane z1 (halo above the chunk) was loaded too
         const double* sn = wait_stage(pn);
-        un = (pn < st.nz && in_grid) ? form_u(sn) : 0.0;
-        kt = cell ? sn[(KMAX + 1) * NT + t] : 0.0;
+        un = form_u(sn);
+        if (!(pn < st.nz && in_grid)) un = 0.0;
+        kt = cell ? sn[(KMAX + 1) * NT + pt] : 0.0;
         if (pn < z1) {
-          if (own && k > 0) a.dstx[col + plane * pn] = un;
+          if (emit && k > 0) a.dstx[g + plane] = un;
           const double f = own ? un : 0.0;
-          nu = fma(f, f, nu);
+          if (half == 0) nu = fma(f, f, nu);
           if (k > 0) add_products(sn, f, accl);
         }
       }
-      // w~ = A u at plane p
+      // w~ = A u at plane p (both halves compute it; the first one stores it)
       double w = 0.0;
       if (own) {
         const double c0 = uc;
@@ -280,14 +321,14 @@ __global__ void __launch_bounds__(TX * TY, 1)
           const double kf = cell ? (nin ? hsv * (kc + fn) : s * kc) : s;
           acc = fma(kf, c0 - (nin ? xn : 0.0), acc);
         };
-        const double xw = Up[t - 1], xe = Up[t + 1];
-        face(xw, cell ? Kp[t - 1] : 0.0, nb_w, st.s[0], hsx);
-        face(xe, cell ? Kp[t + 1] : 0.0, nb_e, st.s[0], hsx);
+        const double xw = Up[pt - 1], xe = Up[pt + 1];
+        face(xw, cell ? Kp[pt - 1] : 0.0, nb_w, st.s[0], hsx);
+        face(xe, cell ? Kp[pt + 1] : 0.0, nb_e, st.s[0], hsx);
         if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - (nb_w ? xw : 0.0), acc);
         if (HASY) {
-          const double xs_ = Up[t - TX], xn_ = Up[t + TX];
-          face(xs_, cell ? Kp[t - TX] : 0.0, nb_s, st.s[1], hsy);
-          face(xn_, cell ? Kp[t + TX] : 0.0, nb_n, st.s[1], hsy);
+          const double xs_ = Up[pt - TX], xn_ = Up[pt + TX];
+          face(xs_, cell ? Kp[pt - TX] : 0.0, nb_s, st.s[1], hsy);
+          face(xn_, cell ? Kp[pt + TX] : 0.0, nb_n, st.s[1], hsy);
           if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - (nb_s ? xs_ : 0.0), acc);
         }
         if (st.nz > 1) {
@@ -297,21 +338,25 @@ __global__ void __launch_bounds__(TX * TY, 1)
           if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - (inb ? ub : 0.0), acc);
         }
         w = c0 + acc;
-        a.dsty[col + plane * p] = w;
-        tu = fma(c0, w, tu);
+        if (half == 0) {
+          a.dsty[g] = w;
+          tu = fma(c0, w, tu);
+        }
       }
       if (k > 0) add_products(sp, w, acct);       // t_j = V_j(p)' w~(p); w = 0 off emitted points
-      Us[bn * NT + t] = un;
+      if (half == 0) Us[bn * NT + pt] = un;
       __syncthreads();                            // stage p consumed; Us(p+1) visible
       if (warp == 0 && p + NST <= z1) issue(p + NST);
       ub = uc; uc = un;
       kb = kc; kc = kt;
+      g += plane;
+      if (++sp_i == NST) sp_i = 0;
     }
     // drain: every issued stage has been waited on (planes z0-1 .. z1), so the barriers'
     // parities stay in step for the next tile
   }
 
-  // REG: reduce every accumulator across the warp once
+  // reduce the accumulators across the points of the warp (value -> slot j0 + j)
   double outl[NCH], outt[NCH];
   if (REG) {
 #pragma unroll
@@ -319,10 +364,10 @@ __global__ void __launch_bounds__(TX * TY, 1)
       double v8[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) v8[q] = (c * 8 + q < NACC) ? accl[c * 8 + q] : 0.0;
-      outl[c] = butterfly8(v8, lane);
+      outl[c] = (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
 #pragma unroll
       for (int q = 0; q < 8; ++q) v8[q] = (c * 8 + q < NACC) ? acct[c * 8 + q] : 0.0;
-      outt[c] = butterfly8(v8, lane);
+      outt[c] = (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
     }
   } else {
 #pragma unroll
@@ -335,11 +380,11 @@ __global__ void __launch_bounds__(TX * TY, 1)
   __syncthreads();
   double* accs = stages;                          // [NW][2 KMAX + 2]
   constexpr int AW = 2 * KMAX + 2;
-  if (lane < 8) {
+  if ((lane & 15) < 8 && (CS == 2 || lane < 8)) {
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-      const int j = c * 8 + lane;
-      if (j < KMAX) {
+      const int j = j0 + c * 8 + (lane & 7);
+      if (c * 8 + (lane & 7) < KJ) {
         accs[warp * AW + j] = outt[c];
         accs[warp * AW + KMAX + j] = outl[c];
       }
@@ -354,7 +399,7 @@ __global__ void __launch_bounds__(TX * TY, 1)
   __syncthreads();
   const int nv = 2 * k + 2;
   const int nb = gridDim.x;
-  for (int v = t; v < nv; v += NT) {
+  for (int v = t; v < nv; v += NTH) {
     const int src = (v < k) ? v : (v < 2 * k ? KMAX + v - k : 2 * KMAX + (v - 2 * k));
     double sum = 0.0;
     for (int w2 = 0; w2 < NW; ++w2) sum += accs[w2 * AW + src];
@@ -446,7 +491,7 @@ struct MapCache {
   bool ok = false;
 };
 
-template <int KIND, int TX, int TY, int KMAX>
+template <int KIND, int TX, int TY, int KMAX, int CS>
 int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
   using Cfg = FCfg<TX, TY, KMAX>;
   static MapCache mc;
@@ -460,7 +505,7 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
     mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)Cfg::SMEM);
       attr = true;
     }
@@ -477,21 +522,21 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   if (!mc.ok) return g_map_err ? g_map_err : -1;
   int64_t grid = 148;                              // one resident block per SM (persistent)
   if (grid > a.ntiles) grid = a.ntiles;
-  fused_tma_kernel<KIND, TX, TY, KMAX><<<(unsigned)grid, dim3(TX, TY), Cfg::SMEM, s>>>(mc.mpx, mc.mpy, mc.mk, a);
+  fused_tma_kernel<KIND, TX, TY, KMAX, CS><<<(unsigned)grid, dim3(TX, TY * CS), Cfg::SMEM, s>>>(mc.mpx, mc.mpy, mc.mk, a);
   return 0;
 }
 
 template <int KIND>
 int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, cudaStream_t s) {
   if (three_d) {
-    if (a.k <= 8) return launch_t<KIND, 32, 16, 8>(a, rpx, rpy, s);
-    if (a.k <= 16) return launch_t<KIND, 32, 16, 16>(a, rpx, rpy, s);
-    if (a.k <= 24) return launch_t<KIND, 32, 8, 24>(a, rpx, rpy, s);
-    return launch_t<KIND, 32, 8, 32>(a, rpx, rpy, s);
+    if (a.k <= 8) return launch_t<KIND, 32, 16, 8, 1>(a, rpx, rpy, s);
+    if (a.k <= 16) return launch_t<KIND, 32, 16, 16, 1>(a, rpx, rpy, s);
+    if (a.k <= 24) return launch_t<KIND, 32, 8, 24, 2>(a, rpx, rpy, s);
+    return launch_t<KIND, 32, 8, 32, 2>(a, rpx, rpy, s);
   }
-  if (a.k <= 8) return launch_t<KIND, 256, 1, 8>(a, rpx, rpy, s);
-  if (a.k <= 16) return launch_t<KIND, 256, 1, 16>(a, rpx, rpy, s);
-  return launch_t<KIND, 256, 1, 32>(a, rpx, rpy, s);
+  if (a.k <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, s);
+  if (a.k <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, s);
+  return launch_t<KIND, 256, 1, 32, 2>(a, rpx, rpy, s);
 }
 
 // 3-D view of the local grid for the fused pass: the march axis is the slowest one
