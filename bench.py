@@ -11,7 +11,7 @@ configs[3] (C4, 3-D variable-kappa diffusion 512^3, d = 3, GMRES(30), tol 1e-8, 
 metric/unit: BASELINE.json's metric, measured as unknown-iterations/s = sum over ranks of
 n * (inner iterations) / (max over ranks of the device time of the K timed steps).
 The --impl reference arm times the CPU oracle (oracle/) on a bounded sample of the same
-workload on the host cores (rank 0 only).  See DESIGN.md section 9.
+workload on the host cores (rank 0 only).  See DESIGN.md section 8.
 """
 from __future__ import annotations
 
