@@ -40,14 +40,19 @@ constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank con
 // ---------------------------------------------------------------------------------------
 // Factorisation pass
 // ---------------------------------------------------------------------------------------
-template <int D>
+// One pass over every chunk.  Rows are read (and LU written) four at a time with 16-byte
+// accesses: a thread walks its own chunk, so a warp touches 32 chunks at once and only
+// whole-sector accesses keep DRAM traffic at the algorithmic bytes.  WRITE = 0: a state-only
+// pass (the fixed point is iterated without storing LU; one WRITE pass follows convergence).
+template <int D, bool WRITE>
 __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, double* __restrict__ lu,
                                    const double* __restrict__ st_in, double* __restrict__ st_out,
                                    int first_pass, int* __restrict__ changed, int* __restrict__ bad,
-                                   const double* __restrict__ prev, int has_prev, int has_next) {
+                                   const double* __restrict__ prev, int has_prev, int has_next, int vec) {
   // has_prev / has_next (multi-rank): the global matrix continues before row 0 / after row n-1
   // of this block (rows of rank-1 / rank+1), so the band entries reaching there are real
   constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
+  constexpr int NB = 2 * D + 1;
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
@@ -76,59 +81,94 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   }
   const bool at_start = !from_prev && ((c == 0) || first_pass);
   int isbad = 0;
-  for (int64_t i = r0; i < r1; ++i) {
-    double Lr[D];       // L(i, i-D+q), q = 0..D-1
-    double Ur[D + 1];   // U(i, i+e)
-    // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D.  Rows before the matrix
-    // start (or before the chunk start in a first-pass guess) do not exist.
-    auto Uk = [&](int q, int64_t j) -> double {
-      const int64_t k = i - D + q;
-      const int64_t e = j - k;
-      return (e >= 0 && e <= D) ? Uw[q][e] : 0.0;
-    };
-    auto row_exists = [&](int q) -> bool {
-      const int64_t k = i - D + q;
-      return (k >= 0 || has_prev) && !(at_start && k < r0);
-    };
+  for (int64_t i0 = r0; i0 < r1; i0 += 4) {
+    const int nr = (r1 - i0) < 4 ? (int)(r1 - i0) : 4;
+    double bb[NB][4];
+    if (vec && nr == 4) {
 #pragma unroll
-    for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
-      const int64_t j = i - D + q;
-      if (!row_exists(q)) { Lr[q] = 0.0; continue; }
-      double s = bands[(int64_t)q * n + i];  // N(i,j), band o = j-i+D = q
+      for (int o = 0; o < NB; ++o) {
+        const double2 lo = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0));
+        const double2 hi = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0 + 2));
+        bb[o][0] = lo.x; bb[o][1] = lo.y; bb[o][2] = hi.x; bb[o][3] = hi.y;
+      }
+    } else {
 #pragma unroll
-      for (int p = 0; p < q; ++p)           // k = i-D+p < j, k >= j-D holds (p >= 0 > q-D)
-        if (row_exists(p)) s -= Lr[p] * Uk(p, j);
-      Lr[q] = s / Uw[q][0];                 // U(j,j)
+      for (int o = 0; o < NB; ++o)
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
     }
+    double out[NB][4];
 #pragma unroll
-    for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
-      const int64_t j = i + e;
-      if (j >= n && !has_next) { Ur[e] = 0.0; continue; }
-      double s = bands[(int64_t)(D + e) * n + i];
+    for (int rr = 0; rr < 4; ++rr) {
+      if (rr >= nr) break;
+      const int64_t i = i0 + rr;
+      double Lr[D];       // L(i, i-D+q), q = 0..D-1
+      double Ur[D + 1];   // U(i, i+e)
+      // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D.  Rows before the matrix
+      // start (or before the chunk start in a first-pass guess) do not exist.
+      auto Uk = [&](int q, int64_t j) -> double {
+        const int64_t k = i - D + q;
+        const int64_t e = j - k;
+        return (e >= 0 && e <= D) ? Uw[q][e] : 0.0;
+      };
+      auto row_exists = [&](int q) -> bool {
+        const int64_t k = i - D + q;
+        return (k >= 0 || has_prev) && !(at_start && k < r0);
+      };
 #pragma unroll
-      for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]
-        if (row_exists(p) && (i - D + p) >= j - D) s -= Lr[p] * Uk(p, j);
-      Ur[e] = s;
+      for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
+        const int64_t j = i - D + q;
+        if (!row_exists(q)) { Lr[q] = 0.0; continue; }
+        double sum = bb[q][rr];                 // N(i,j), band o = j-i+D = q
+#pragma unroll
+        for (int p = 0; p < q; ++p)           // k = i-D+p < j, k >= j-D holds (p >= 0 > q-D)
+          if (row_exists(p)) sum -= Lr[p] * Uk(p, j);
+        Lr[q] = sum / Uw[q][0];               // U(j,j)
+      }
+#pragma unroll
+      for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
+        const int64_t j = i + e;
+        if (j >= n && !has_next) { Ur[e] = 0.0; continue; }
+        double sum = bb[D + e][rr];
+#pragma unroll
+        for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]
+          if (row_exists(p) && (i - D + p) >= j - D) sum -= Lr[p] * Uk(p, j);
+        Ur[e] = sum;
+      }
+      if (!(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        if (!(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
+        out[q][rr] = Lr[q];
+      }
+#pragma unroll
+      for (int e = 0; e <= D; ++e) {
+        if (!(fabs(Ur[e]) <= 1e100)) isbad = 1;
+        out[D + e][rr] = Ur[e];
+      }
+      // shift the window
+#pragma unroll
+      for (int q = 0; q < D - 1; ++q)
+#pragma unroll
+        for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
+#pragma unroll
+      for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
     }
-    if (!(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+    if (WRITE) {
+      if (vec && nr == 4) {
 #pragma unroll
-    for (int q = 0; q < D; ++q) {
-      if (!(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
-      lu[(int64_t)q * n + i] = Lr[q];
+        for (int o = 0; o < NB; ++o) {
+          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0) = make_double2(out[o][0], out[o][1]);
+          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0 + 2) = make_double2(out[o][2], out[o][3]);
+        }
+      } else {
+#pragma unroll
+        for (int o = 0; o < NB; ++o)
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (rr < nr) lu[(int64_t)o * n + i0 + rr] = out[o][rr];
+      }
     }
-#pragma unroll
-    for (int e = 0; e <= D; ++e) {
-      if (!(fabs(Ur[e]) <= 1e100)) isbad = 1;
-      lu[(int64_t)(D + e) * n + i] = Ur[e];
-    }
-    // shift the window
-#pragma unroll
-    for (int q = 0; q < D - 1; ++q)
-#pragma unroll
-      for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
-#pragma unroll
-    for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
-    (void)row_exists;
   }
   double* so = st_out + c * W;
   bool diff = first_pass != 0;
@@ -510,12 +550,17 @@ __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __res
 template <int D>
 void factor_launch(const double* bands, int64_t n, double* lu, const double* a, double* b,
                    int first, int* changed, int* bad, const double* prev, int has_prev, int has_next,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool write) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int tpb = 64;
-  factor_pass_kernel<D><<<(unsigned)((nchunks + tpb - 1) / tpb), tpb, 0, s>>>(bands, n, lu, a, b, first,
-                                                                              changed, bad, prev, has_prev,
-                                                                              has_next);
+  const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
+  const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
+  if (write)
+    factor_pass_kernel<D, true><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
+                                                     has_next, vec);
+  else
+    factor_pass_kernel<D, false><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
+                                                      has_next, vec);
 }
 
 template <bool FWD, int D>
@@ -672,16 +717,17 @@ int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScrat
   int h[2] = {0, 0};
   double hd[2] = {0.0, 0.0};
   int p = 0;
+  bool write = false;   // state-only passes until no chunk state changes, then one LU pass
   for (;;) {
     cudaMemsetAsync(sc.changed, 0, 2 * sizeof(int), s);
     const double* prev = (multi && comm->rank > 0 && p > 0) ? M.prev : nullptr;
     const int hp = (multi && comm->rank > 0) ? 1 : 0;
     const int hn = (multi && comm->rank < comm->nranks - 1) ? 1 : 0;
     switch (d) {
-      case 1: factor_launch<1>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
-      case 2: factor_launch<2>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
-      case 3: factor_launch<3>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
-      default: factor_launch<4>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s); break;
+      case 1: factor_launch<1>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s, write); break;
+      case 2: factor_launch<2>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s, write); break;
+      case 3: factor_launch<3>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s, write); break;
+      default: factor_launch<4>(bands, n, lu, A, B, p == 0, sc.changed, sc.changed + 1, prev, hp, hn, s, write); break;
     }
     if (launches) *launches += 1;
     ++p;
@@ -701,7 +747,8 @@ int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScrat
     double* tmp = A;
     A = B;
     B = tmp;
-    if (h[0] == 0 || p > nchunks * (multi ? comm->nranks : 1) + 1) break;
+    if (write) break;                 // the LU pass from the converged states
+    if (h[0] == 0 || p > nchunks * (multi ? comm->nranks : 1) + 1) write = true;
   }
   if (passes) *passes = p;
   if (h[1]) return PSP_E_SINGULAR;
