@@ -428,3 +428,26 @@ def test_determinism(torch, P):
     b = run_gpu_steps(torch, P, prob, 2, "fused")
     assert np.array_equal(a["u"], b["u"])
     assert np.array_equal(a["reports"][0]["resid_history"], b["reports"][0]["resid_history"])
+
+
+@pytest.mark.parametrize("n", [20, 80])
+def test_paper_experiment_f1(torch, P, orc, n):
+    """seven-diagonal A, rhs [1..n], X0 = 0, absolute eps, d = 1.
+    Solve, MREP fit (+ gate), solve again: GPU iteration counts equal the oracle's (T5), for the
+    gated method and for the paper's literal (ungated) one."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "paper_f1", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "paper_f1.py"))
+    f1 = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(f1)
+    op, b = inputs.seven_diagonal(n, seed=0)
+    for gate in (True, False):
+        o1, o2, og = f1.oracle_pair(op, b, gate=gate)
+        g1, g2, gg = f1.gpu_pair(op, b, gate=gate)
+        assert abs(g1 - o1) <= 1
+        if gate:                     # the R21 decision (ungated: the GPU reports N installed)
+            assert og == gg
+        assert (o2 is None) == (g2 is None)
+        if isinstance(o2, int) and isinstance(g2, int):
+            assert abs(g2 - o2) <= 1, (gate, g2, o2)
