@@ -19,6 +19,9 @@
 
 #include "internal.h"
 
+#ifndef PSP_MREP_NST
+#define PSP_MREP_NST 4    // TMA stages of 4 probe columns each (8 or 12 measured slower: fewer CTAs per SM)
+#endif
 #ifndef PSP_MREP_MINB
 #define PSP_MREP_MINB 2   // resident blocks per SM of the TMA MREP kernel
 #endif
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
 // ------------------------------------------------------------------------------------------
 constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kernel
 constexpr int TCB = 4;         // probe columns per stage
-constexpr int TNST = 4;        // stages
+constexpr int TNST = PSP_MREP_NST;   // stages
 
 template <int D>
 struct TmaCfg {
