@@ -6,6 +6,8 @@
 // threads along x; the +-x neighbours come from the same warp's lines, the +-y / +-z
 // neighbours from L1/L2 (three planes of x and kappa are ~12 MB at 512^2, well inside the
 // 126 MB L2), so DRAM sees each array once.
+#include <stdlib.h>
+
 #include "internal.h"
 
 #ifndef PSP_MARCH_MINB
@@ -362,6 +364,127 @@ __global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march
   }
 }
 
+// Four x-adjacent points per thread (two 16-byte accesses per row and array): the per-point
+// cost of loop control, address arithmetic and the y-neighbour loads halves against
+// march3_kernel; z neighbours in a register queue prefetched two planes ahead.  Needs nx % 4 == 0
+// and 16-byte aligned vectors.
+template <int KIND, int BY>
+__global__ void __launch_bounds__(32 * BY, 2) march4_kernel(MarchView v, const double* __restrict__ x,
+                                                           const double* xsp, double* __restrict__ y,
+                                                           double* __restrict__ xcopy) {
+  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  constexpr bool HASY = BY > 1;
+  constexpr int TW = 128;
+  const double* __restrict__ f = v.field;
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * TW + 4 * lane;    // first of this thread's four points
+  const int64_t j = HASY ? (int64_t)blockIdx.y * BY + ty : 0;
+  const int64_t z0 = (int64_t)blockIdx.z * v.zc;
+  const int64_t z1 = (z0 + v.zc < v.nz) ? z0 + v.zc : v.nz;
+  const bool in = i < v.nx && j < v.ny;                     // nx % 4 == 0: all four or none
+  const int64_t plane = v.nx * v.ny;
+  const int64_t col = in ? i + v.nx * j : 0;
+  const bool has_w = i > 0, has_e = i + 4 < v.nx;
+  const bool has_s = HASY && in && j > 0, has_n = HASY && in && j + 1 < v.ny;
+  const bool lo_in = v.x_lo != nullptr, hi_in = v.x_hi != nullptr;
+  const double xs = xsp ? *xsp : 1.0;
+  const double hs0 = 0.5 * v.s[0], hs1 = 0.5 * v.s[1], hs2 = 0.5 * v.s[2];
+  const double s0c = v.s[0], s1c = v.s[1], s2c = v.s[2];
+  struct Q4 { double a, b, c, d; };
+  auto ld4 = [&](const double* base, int64_t off) -> Q4 {
+    const double2 p = __ldg(reinterpret_cast<const double2*>(base + off));
+    const double2 q = __ldg(reinterpret_cast<const double2*>(base + off + 2));
+    return Q4{p.x, p.y, q.x, q.y};
+  };
+  auto plane4 = [&](const double* a, const double* lo, const double* hi, int64_t p) -> Q4 {
+    if (p >= 0 && p < v.nz) return ld4(a, col + plane * p);
+    if (p < 0 && lo) return ld4(lo, col);
+    if (p >= v.nz && hi) return ld4(hi, col);
+    return Q4{0.0, 0.0, 0.0, 0.0};
+  };
+  const Q4 zero4{0.0, 0.0, 0.0, 0.0};
+  Q4 xb = plane4(x, v.x_lo, v.x_hi, z0 - 1), xc = plane4(x, v.x_lo, v.x_hi, z0), xt = plane4(x, v.x_lo, v.x_hi, z0 + 1);
+  Q4 fb = zero4, fc = zero4, ft = zero4;
+  if (cell) {
+    fb = plane4(f, v.f_lo, v.f_hi, z0 - 1); fc = plane4(f, v.f_lo, v.f_hi, z0); ft = plane4(f, v.f_lo, v.f_hi, z0 + 1);
+  }
+  int64_t g = col + plane * z0;
+  for (int64_t z = z0; z < z1; ++z) {
+    // prefetch plane z+2
+    Q4 xt2 = zero4, ft2 = zero4;
+    if (z + 2 < v.nz) {
+      xt2 = ld4(x, g + 2 * plane);
+      if (cell) ft2 = ld4(f, g + 2 * plane);
+    } else if (z + 2 == v.nz) {
+      xt2 = plane4(x, v.x_lo, v.x_hi, z + 2);
+      if (cell) ft2 = plane4(f, v.f_lo, v.f_hi, z + 2);
+    }
+    // in-plane y neighbours (L1 / L2): missing -> x = 0, k = k_c
+    Q4 xsn = zero4, xnn = zero4, fsn = fc, fnn = fc;
+    if (has_s) { xsn = ld4(x, g - v.nx); if (cell) fsn = ld4(f, g - v.nx); }
+    if (has_n) { xnn = ld4(x, g + v.nx); if (cell) fnn = ld4(f, g + v.nx); }
+    // x neighbours across threads: the adjacent lanes; lanes 0 / 31 load across the tile edge
+    double xw = __shfl_up_sync(0xffffffffu, xc.d, 1), xe = __shfl_down_sync(0xffffffffu, xc.a, 1);
+    double fw = 0.0, fe = 0.0;
+    if (cell) {
+      fw = __shfl_up_sync(0xffffffffu, fc.d, 1);
+      fe = __shfl_down_sync(0xffffffffu, fc.a, 1);
+    }
+    if (lane == 0 && in && has_w) { xw = __ldg(x + g - 1); if (cell) fw = __ldg(f + g - 1); }
+    if (lane == 31 && in && has_e) { xe = __ldg(x + g + 4); if (cell) fe = __ldg(f + g + 4); }
+    if (!has_w) { xw = 0.0; fw = fc.a; }
+    if (!has_e) { xe = 0.0; fe = fc.d; }
+    if (z == 0 && !lo_in) fb = fc;
+    if (z + 1 == v.nz && !hi_in) ft = fc;
+    auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
+                     double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
+      double acc = 0.0;
+      if (cell) {
+        acc = fma(hs0 * (k + fwv), c - xwv, acc);
+        acc = fma(hs0 * (k + fev), c - xev, acc);
+      } else {
+        acc = fma(s0c, c - xwv, acc);
+        acc = fma(s0c, c - xev, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
+      if (HASY) {
+        if (cell) {
+          acc = fma(hs1 * (k + fsv), c - xsv, acc);
+          acc = fma(hs1 * (k + fnv), c - xnv, acc);
+        } else {
+          acc = fma(s1c, c - xsv, acc);
+          acc = fma(s1c, c - xnv, acc);
+        }
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
+      }
+      if (cell) {
+        acc = fma(hs2 * (k + fbv), c - xbv, acc);
+        acc = fma(hs2 * (k + ftv), c - xtv, acc);
+      } else {
+        acc = fma(s2c, c - xbv, acc);
+        acc = fma(s2c, c - xtv, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
+      return xs * (c + acc);
+    };
+    if (in) {
+      const double o0 = point(xc.a, fc.a, xw, fw, xc.b, fc.b, xsn.a, fsn.a, xnn.a, fnn.a, xb.a, fb.a, xt.a, ft.a);
+      const double o1 = point(xc.b, fc.b, xc.a, fc.a, xc.c, fc.c, xsn.b, fsn.b, xnn.b, fnn.b, xb.b, fb.b, xt.b, ft.b);
+      const double o2 = point(xc.c, fc.c, xc.b, fc.b, xc.d, fc.d, xsn.c, fsn.c, xnn.c, fnn.c, xb.c, fb.c, xt.c, ft.c);
+      const double o3 = point(xc.d, fc.d, xc.c, fc.c, xe, fe, xsn.d, fsn.d, xnn.d, fnn.d, xb.d, fb.d, xt.d, ft.d);
+      *reinterpret_cast<double2*>(y + g) = make_double2(o0, o1);
+      *reinterpret_cast<double2*>(y + g + 2) = make_double2(o2, o3);
+      if (xcopy) {
+        *reinterpret_cast<double2*>(xcopy + g) = make_double2(xs * xc.a, xs * xc.b);
+        *reinterpret_cast<double2*>(xcopy + g + 2) = make_double2(xs * xc.c, xs * xc.d);
+      }
+    }
+    g += plane;
+    xb = xc; xc = xt; xt = xt2;
+    fb = fc; fc = ft; ft = ft2;
+  }
+}
+
 __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ bands,
                                   const double* __restrict__ x, const double* xsp, double* __restrict__ y,
                                   double* __restrict__ xcopy) {
@@ -401,6 +524,16 @@ void launch_march(const MarchView& v0, const double* x, const double* xs, double
 }
 
 template <int KIND, int BY>
+void launch_march4(const MarchView& v0, const double* x, const double* xs, double* y, double* xcopy,
+                   cudaStream_t s) {
+  MarchView v = v0;
+  const int64_t zc = planes_per_block(((v.nx + 127) / 128) * ((v.ny + BY - 1) / BY), v.nz);
+  v.zc = (int)zc;
+  dim3 grid((unsigned)((v.nx + 127) / 128), (unsigned)((v.ny + BY - 1) / BY), (unsigned)((v.nz + zc - 1) / zc));
+  march4_kernel<KIND, BY><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
+}
+
+template <int KIND, int BY>
 void launch_march2(const MarchView& v0, const double* x, const double* xs, double* y, double* xcopy,
                    cudaStream_t s) {
   MarchView v = v0;
@@ -436,7 +569,8 @@ void launch_kind(const Stencil& st, const double* x, const double* xs, double* y
     v.nx = st.nx; v.ny = st.ny; v.nz = st.nz;
     v.s[1] = st.s[1]; v.a[1] = st.a[1];
     v.s[2] = st.s[2]; v.a[2] = st.a[2];
-    if (vec_ok) launch_march2<KIND, 8>(v, x, xs, y, xcopy, s);
+    if (vec_ok && v.nx % 4 == 0 && !getenv("PSP_MARCH3")) launch_march4<KIND, 8>(v, x, xs, y, xcopy, s);
+    else if (vec_ok) launch_march2<KIND, 8>(v, x, xs, y, xcopy, s);
     else launch_march<KIND, 32, 8>(v, x, xs, y, xcopy, s);
   } else {
     v.nx = st.nx; v.ny = 1; v.nz = st.ny;
