@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
   constexpr bool REG = KJ <= 16;           // per-thread accumulators (else per-plane butterflies)
   constexpr int NCH = (KJ + 7) / 8;
   constexpr int NACC = REG ? KJ : NCH;
+  constexpr bool VREG = KJ <= 8;           // keep a plane's basis values in registers for the l_j
   static_assert(CS == 1 || CS == 2, "column split 1 or 2");
   extern __shared__ __align__(128) double fsm[];
   // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
@@ -250,34 +251,63 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
         else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, bars + si);
       }
     };
+    auto wait_stage_i = [&](int si) -> const double* {
+      mbar_wait(bars + si, (phase_bits >> si) & 1u);
+      phase_bits ^= (1u << si);
+      return stages + (size_t)si * Cfg::STAGE;
+    };
     auto wait_stage = [&](int64_t q) -> const double* {
       const int si = (int)((q - z0 + 1) % NST);
       mbar_wait(bars + si, (phase_bits >> si) & 1u);
       phase_bits ^= (1u << si);
       return stages + (size_t)si * Cfg::STAGE;
     };
-    auto form_u = [&](const double* sb) -> double {   // u at this point of the staged plane
+    // u at this point of the staged plane; vr receives this thread's basis values (the l_j
+    // products reuse them)
+    auto form_u = [&](const double* sb, double (&vr)[KJ]) -> double {
       const double s0 = sb[KMAX * NT + pt];
+      if (VREG) {
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) vr[j] = sb[(j0 + j) * NT + pt];
+      }
       if (k == 0) return s0;
       double u = (half == 0) ? wsc * s0 : 0.0;
 #pragma unroll
-      for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], sb[(j0 + j) * NT + pt], u);
+      for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], VREG ? vr[j] : sb[(j0 + j) * NT + pt], u);
       if (CS == 2) {                             // the halves' partial updates, same sum on both
         const double o = __shfl_xor_sync(0xffffffffu, u, 16);
         u = (half == 0) ? u + o : o + u;
       }
       return u;
     };
+    auto add_products_r = [&](const double (&vr)[KJ], const double* sb, double f, double (&acc)[NACC]) {
+      if (!VREG) {
+        add_products(sb, f, acc);
+      } else if (REG) {
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) acc[j] = fma(vr[j], f, acc[j]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          if (c * 8 >= k) break;                 // uniform
+          double v8[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v8[q] = vr[c * 8 + q] * f;
+          acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
+        }
+      }
+    };
 
     if (warp == 0)
       for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
     // prologue: u(z0-1), u(z0) (+ l-products of plane z0)
+    double vr[KJ];
     const double* sbm = wait_stage(z0 - 1);
-    double ub = form_u(sbm);
+    double ub = form_u(sbm, vr);
     if (!(z0 >= 1 && in_grid)) ub = 0.0;
     double kb = cell ? sbm[(KMAX + 1) * NT + pt] : 0.0;
     const double* sbc = wait_stage(z0);
-    double uc = form_u(sbc);
+    double uc = form_u(sbc, vr);
     if (!in_grid) uc = 0.0;
     double kc = cell ? sbc[(KMAX + 1) * NT + pt] : 0.0;
     int64_t g = col + plane * z0;                // this point's index at plane p
@@ -285,7 +315,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     {
       const double f = own ? uc : 0.0;
       if (half == 0) nu = fma(f, f, nu);
-      if (k > 0) add_products(sbc, f, accl);
+      if (k > 0) add_products_r(vr, sbc, f, accl);
     }
     if (half == 0) Us[(z0 & 1) * NT + pt] = uc;
     __syncthreads();                              // stage z0-1 consumed; Us(z0) visible
@@ -298,16 +328,17 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
       // stage p (resident: t-dots, in-plane kappa), stage p+1 (u(p+1))
       const double* sp = stages + (size_t)sp_i * Cfg::STAGE;
       double un = 0.0, kt = 0.0;
+      const int sn_i = (sp_i + 1 == NST) ? 0 : sp_i + 1;
       if (pn <= z1) {                             // plane z1 (halo above the chunk) was loaded too
-        const double* sn = wait_stage(pn);
-        un = form_u(sn);
+        const double* sn = wait_stage_i(sn_i);
+        un = form_u(sn, vr);
         if (!(pn < st.nz && in_grid)) un = 0.0;
         kt = cell ? sn[(KMAX + 1) * NT + pt] : 0.0;
         if (pn < z1) {
           if (emit && k > 0) a.dstx[g + plane] = un;
           const double f = own ? un : 0.0;
           if (half == 0) nu = fma(f, f, nu);
-          if (k > 0) add_products(sn, f, accl);
+          if (k > 0) add_products_r(vr, sn, f, accl);
         }
       }
       // w~ = A u at plane p (both halves compute it; the first one stores it)
@@ -317,25 +348,27 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
         double acc = 0.0;
         const double* Up = Us + bp * NT;
         const double* Kp = sp + (KMAX + 1) * NT;
+        // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
+        // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
         auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
-          const double kf = cell ? (nin ? hsv * (kc + fn) : s * kc) : s;
-          acc = fma(kf, c0 - (nin ? xn : 0.0), acc);
+          const double kf = cell ? hsv * (kc + (nin ? fn : kc)) : s;
+          acc = fma(kf, c0 - xn, acc);
         };
         const double xw = Up[pt - 1], xe = Up[pt + 1];
         face(xw, cell ? Kp[pt - 1] : 0.0, nb_w, st.s[0], hsx);
         face(xe, cell ? Kp[pt + 1] : 0.0, nb_e, st.s[0], hsx);
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - (nb_w ? xw : 0.0), acc);
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
         if (HASY) {
           const double xs_ = Up[pt - TX], xn_ = Up[pt + TX];
           face(xs_, cell ? Kp[pt - TX] : 0.0, nb_s, st.s[1], hsy);
           face(xn_, cell ? Kp[pt + TX] : 0.0, nb_n, st.s[1], hsy);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - (nb_s ? xs_ : 0.0), acc);
+          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
         }
         if (st.nz > 1) {
           const bool inb = p > 0, int_ = p + 1 < st.nz;
           face(ub, kb, inb, st.s[2], hsz);
           face(un, kt, int_, st.s[2], hsz);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - (inb ? ub : 0.0), acc);
+          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub, acc);
         }
         w = c0 + acc;
         if (half == 0) {

@@ -10,7 +10,7 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 fused = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 kmax = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 prob = inputs.c4(n=size, steps=steps)
-opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, fused=fused, fused_kmax=kmax)
+opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, fused=fused, fused_kmin=0, fused_kmax=kmax)
 ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts)
 u = torch.as_tensor(prob.u0).cuda()
 for s in range(steps):
