@@ -17,6 +17,8 @@
 // sums and emit 256-2d rows (the 2d halo rows are recomputed by the neighbour block).
 #include <math.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 #ifndef PSP_MREP_NST
@@ -90,28 +92,60 @@ __device__ __forceinline__ void assemble(double (&A)[(2 * D + 2) * (2 * D + 3) /
 // multiply-by-reciprocal adds at most one rounding, inside T3's 8 P u kappa_2(G) bound) and
 // returns max_j L_jj, min_j L_jj for the condition estimate.  Straight-line (no early exit), so
 // the packed matrix stays in registers.
-template <int P>
-__device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2], double& lmax, double& lmin) {
-  bool ok = true;
-#pragma unroll
-  for (int j = 0; j < P; ++j) {
-    double s = A[pk(j, j)];
-#pragma unroll
-    for (int k = 0; k < j; ++k) s -= A[pk(j, k)] * A[pk(j, k)];
-    ok = ok && (s > 0.0) && isfinite(s);
-    const double ljj = sqrt(ok ? s : 1.0);
-    lmax = (j == 0) ? ljj : fmax(lmax, ljj);
-    lmin = (j == 0) ? ljj : fmin(lmin, ljj);
-    const double inv = 1.0 / ljj;
-    A[pk(j, j)] = inv;
-#pragma unroll
-    for (int i = j + 1; i < P; ++i) {
-      double u = A[pk(i, j)];
-#pragma unroll
-      for (int k = 0; k < j; ++k) u -= A[pk(i, k)] * A[pk(j, k)];
-      A[pk(i, j)] = u * inv;
-    }
+// compile-time loop: f(std::integral_constant<int, i>) for i in [B, E) (forces full unrolling
+// of the small dense kernels below; a rolled loop would index the packed Gram at run time and
+// send it to local memory)
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
   }
+}
+
+// 1/sqrt(s) for s > 0: the hardware approximation refined by three Newton steps (each doubles
+// the correct bits; within ~1 ulp).  Unlike sqrt() and '/', it has no out-of-line special-case
+// path, whose call would force the packed Gram out of registers around every pivot.
+__device__ __forceinline__ double rsqrt_nr(double s) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double h = 0.5 * s;
+#pragma unroll
+  for (int it = 0; it < 3; ++it) y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// in-place Cholesky of the packed P x P matrix (R17); false on a pivot^2 <= 0 or non-finite.
+// Stores 1/L_jj on the diagonal (the solves multiply by it: each product adds at most one
+// rounding, inside T3's 8 P u kappa_2(G) bound) and returns max_j L_jj and max_j 1/L_jj for
+// the condition estimate (max L_jj / min L_jj)^2 = (max L_jj * max 1/L_jj)^2.
+template <int P>
+__device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2], double& lmax, double& imax) {
+  bool ok = true;
+  static_for<0, P>([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    double s = A[pk(j, j)];
+    static_for<0, j>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      s -= A[pk(j, k)] * A[pk(j, k)];
+    });
+    ok = ok && (s > 0.0) && isfinite(s);
+    const double sv = ok ? s : 1.0;
+    const double inv = rsqrt_nr(sv);               // 1 / L_jj
+    const double ljj = sv * inv;                   // L_jj
+    lmax = (j == 0) ? ljj : fmax(lmax, ljj);
+    imax = (j == 0) ? inv : fmax(imax, inv);
+    A[pk(j, j)] = inv;
+    static_for<j + 1, P>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      double u = A[pk(i, j)];
+      static_for<0, j>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        u -= A[pk(i, k)] * A[pk(j, k)];
+      });
+      A[pk(i, j)] = u * inv;
+    });
+  });
   return ok;
 }
 
@@ -131,21 +165,21 @@ __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double T
   constexpr int P = 2 * D + 2;
   constexpr int NP = P * (P + 1) / 2;
   double A[NP];
-  double lmax = 0.0, lmin = 0.0, kap = INFINITY, lambda = 0.0;
+  double lmax = 0.0, imax = 0.0, kap = INFINITY, lambda = 0.0;
   bool ok = false;
   int kind = PSP_ROW_INTERIOR;
 #pragma unroll 1
   for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
     assemble<D, TS>(A, ex, t, m, lambda);
-    ok = chol_packed<P>(A, lmax, lmin);
+    ok = chol_packed<P>(A, lmax, imax);
     if (attempt == 0) {
-      kap = ok ? (lmax / lmin) * (lmax / lmin) : INFINITY;
+      kap = ok ? (lmax * imax) * (lmax * imax) : INFINITY;
       if (ok && kap <= 1e12) break;
       // S:226 ridge retry on G + lambda I
       double tr = (double)m;
 #pragma unroll
       for (int a = 0; a <= 2 * D; ++a) tr += ex[0 * TS + (t - D + a)];   // diag = C_0(r-d+a)
-      lambda = 1e-10 * tr / (double)P;
+      lambda = (1e-10 / (double)P) * tr;
       kind = PSP_ROW_INTERIOR_RIDGE;
       g.v[3] += 1.0;
     }
@@ -159,20 +193,24 @@ __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double T
     for (int o = 0; o <= 2 * D; ++o) row[o] = (o == D) ? 1.0 : 0.0;
   } else {
     double z[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      double s = (i == 0) ? Tsum : Dl[i - 1];
-#pragma unroll
-      for (int k = 0; k < i; ++k) s -= A[pk(i, k)] * z[k];
-      z[i] = s * A[pk(i, i)];
-    }
-#pragma unroll
-    for (int i = P - 1; i >= 0; --i) {
-      double s = z[i];
-#pragma unroll
-      for (int k = i + 1; k < P; ++k) s -= A[pk(k, i)] * z[k];
-      z[i] = s * A[pk(i, i)];
-    }
+    static_for<0, P>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      double sum = (i == 0) ? Tsum : Dl[i > 0 ? i - 1 : 0];
+      static_for<0, i>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        sum -= A[pk(i, k)] * z[k];
+      });
+      z[i] = sum * A[pk(i, i)];
+    });
+    static_for<0, P>([&](auto ic) {
+      constexpr int i = P - 1 - decltype(ic)::value;
+      double sum = z[i];
+      static_for<i + 1, P>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        sum -= A[pk(k, i)] * z[k];
+      });
+      z[i] = sum * A[pk(i, i)];
+    });
     icpt = z[0];                                  // R15: reported, never installed
 #pragma unroll
     for (int o = 0; o <= 2 * D; ++o) row[o] = z[1 + o];  // R14: N(i, i+o-d) = N*(o+2)
@@ -385,40 +423,44 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
 
   const int lx = cols.sx ? LX1 : LX, ly = cols.sy ? LY1 : LY;
   const int nch = m / TCB;                         // m % TCB == 0 (host check)
-  const int64_t my_tiles = (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t total = my_tiles * nch;
-  auto issue = [&](int64_t q) {                   // thread 0: stage the columns of load q
-    const int64_t tile = blockIdx.x + (q / nch) * gridDim.x;
-    const int ch = (int)(q % nch);
-    const int stg = (int)(q % TNST);
-    double* st = stages + (size_t)stg * Cfg::STAGE;
+  // 32-bit load counters with incremental (tile, chunk, stage) indices: a 64-bit division in
+  // the loop is an out-of-line call whose ABI would push the packed Gram to local memory
+  const int my_tiles = (int)((ntile - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int total = my_tiles * nch;
+  int is_tq = 0, is_ch = 0, is_stg = 0;            // the next load to issue (thread 0)
+  auto issue_next = [&]() {                        // thread 0: stage the columns of the next load
+    const int64_t tile = blockIdx.x + (int64_t)is_tq * gridDim.x;
+    double* st = stages + (size_t)is_stg * Cfg::STAGE;
     const int64_t s0 = R0 + tile * E - D;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bars + stg, 8u * (unsigned)(TCB * (lx + ly)));
+    mbar_expect_tx(bars + is_stg, 8u * (unsigned)(TCB * (lx + ly)));
 #pragma unroll
     for (int cc = 0; cc < TCB; ++cc) {
-      const int c = ch * TCB + cc;
+      const int c = is_ch * TCB + cc;
       const double* bxp = cols.px + (int64_t)cols.slot[c] * cols.ld;
       const double* byp = cols.py + (int64_t)cols.slot[c] * cols.ld;
-      bulk_g2s(st + cc * Cfg::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + stg);
-      bulk_g2s(st + TCB * Cfg::PXW + cc * Cfg::PYW, byp + (s0 - cols.sy), 8u * ly, bars + stg);
+      bulk_g2s(st + cc * Cfg::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + is_stg);
+      bulk_g2s(st + TCB * Cfg::PXW + cc * Cfg::PYW, byp + (s0 - cols.sy), 8u * ly, bars + is_stg);
     }
+    if (++is_ch == nch) { is_ch = 0; ++is_tq; }
+    if (++is_stg == TNST) is_stg = 0;
   };
   if (t == 0)
-    for (int64_t q = 0; q < total && q < TNST; ++q) issue(q);
+    for (int q = 0; q < total && q < TNST; ++q) issue_next();
 
   GateStats gs;
   double Cl[2 * D + 1], Dl[2 * D + 1], Ssum = 0.0, Tsum = 0.0;
   const int xo = cols.sx + t, yo = cols.sy + t;    // this row's offsets in a stage row
-  for (int64_t q = 0; q < total; ++q) {
-    const int stg = (int)(q % TNST);
-    const int ch = (int)(q % nch);
+  int stg = 0, ch = 0, tq = 0;
+  unsigned phase = 0;                              // parity bit per stage
+  for (int q = 0; q < total; ++q) {
     if (ch == 0) {
 #pragma unroll
       for (int l = 0; l <= 2 * D; ++l) { Cl[l] = 0.0; Dl[l] = 0.0; }
       Ssum = Tsum = 0.0;
     }
-    mbar_wait(bars + stg, (unsigned)((q / TNST) & 1));
+    mbar_wait(bars + stg, (phase >> stg) & 1u);
+    phase ^= 1u << stg;
     const double* st = stages + (size_t)stg * Cfg::STAGE;
     if (unit) {
 #pragma unroll
@@ -456,17 +498,22 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
       }
     }
     __syncthreads();                               // every thread is done with stage stg
-    if (t == 0 && q + TNST < total) issue(q + TNST);
+    if (t == 0 && q + TNST < total) issue_next();
+    if (++stg == TNST) stg = 0;
     if (ch == nch - 1) {
       // exchange C_l, S of the tile's TT sum rows, then fit the emitted rows
 #pragma unroll
       for (int l = 0; l <= 2 * D; ++l) ex[l * TT + t] = Cl[l];
       ex[(2 * D + 1) * TT + t] = Ssum;
       __syncthreads();
-      const int64_t tile = blockIdx.x + (q / nch) * gridDim.x;
+      const int64_t tile = blockIdx.x + (int64_t)tq * gridDim.x;
       const int64_t r = R0 + tile * E - D + t;
       if (t >= D && t < TT - D) fit_row<D, TT>(ex, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
       __syncthreads();                             // ex is rewritten by the next tile
+      ch = 0;
+      ++tq;
+    } else {
+      ++ch;
     }
   }
   merge_stats(gs, red, sc.result);
