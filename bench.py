@@ -433,7 +433,7 @@ def main():
         line["kernel_rooflines"] = {
             "matvec": {"achieved_GBps": kernel_table.get("matvec", {}).get("GBps"), "peak": peak,
                        "frac": (kernel_table.get("matvec", {}).get("GBps") or 0.0) / peak,
-                       "bytes_per_row": 32, "workload": "C4 step (probe copy fused)"} if mv else None,
+                       "bytes_per_row": 24, "workload": "C4 step (ring mode: x and kappa read, A x written)"} if mv else None,
             "mrep_fit": {"achieved_GBps": c5["mrep_fit"]["achieved_GBps"], "peak": peak,
                          "frac": c5["mrep_fit"]["frac"], "workload": c5["workload"]},
             "banded_solve": {"achieved_GBps": c5["banded_solve"]["achieved_GBps"], "peak": peak,
