@@ -17,7 +17,7 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 $(ORACLE): oracle/oracle.c oracle/oracle.h
 	gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -Wextra -Wno-unused-parameter -o $@ oracle/oracle.c -lm

@@ -10,6 +10,7 @@
 //                     the fixed-point state of the banded factorisation
 //   allgather      -- per-rank affine maps / states of the partitioned banded sweeps
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 #include <string.h>
 
@@ -22,31 +23,71 @@
 
 namespace {
 
+// NCCL is bound at first use (dlopen of libnccl.so.2), not at load time: a process that uses
+// the library on one GPU never loads NCCL, and in a torch.distributed job the already-loaded
+// libnccl.so.2 of torch is the one bound (loading the system copy first would shadow torch's).
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // torch's copy, if loaded
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+  if (!h) return a;
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+  a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+  a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+  a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+  a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+  a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+  a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+  a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+  a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.AllGather && a.Send && a.Recv &&
+         a.GroupStart && a.GroupEnd;
+  return a;
+}
+
 ncclRedOp_t nccl_op(int op) { return op == 1 ? ncclMax : (op == 2 ? ncclMin : ncclSum); }
 
 struct NcclComm : psp_comm {
   ncclComm_t c = nullptr;
   ~NcclComm() override {
-    if (c) ncclCommDestroy(c);
+    if (c && nccl().ok) nccl().CommDestroy(c);
   }
   int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
-    return ncclAllReduce(d, d, count, ncclDouble, nccl_op(op), c, s) == ncclSuccess ? 0 : 1;
+    return nccl().AllReduce(d, d, count, ncclDouble, nccl_op(op), c, s) == ncclSuccess ? 0 : 1;
   }
   int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
                double* recv_hi, size_t n_hi, cudaStream_t s) override {
-    if (ncclGroupStart() != ncclSuccess) return 1;
+    const NcclApi& A = nccl();
+    if (A.GroupStart() != ncclSuccess) return 1;
     if (rank > 0 && n_lo) {
-      ncclSend(send_lo, n_lo, ncclDouble, rank - 1, c, s);
-      ncclRecv(recv_lo, n_lo, ncclDouble, rank - 1, c, s);
+      A.Send(send_lo, n_lo, ncclDouble, rank - 1, c, s);
+      A.Recv(recv_lo, n_lo, ncclDouble, rank - 1, c, s);
     }
     if (rank < nranks - 1 && n_hi) {
-      ncclSend(send_hi, n_hi, ncclDouble, rank + 1, c, s);
-      ncclRecv(recv_hi, n_hi, ncclDouble, rank + 1, c, s);
+      A.Send(send_hi, n_hi, ncclDouble, rank + 1, c, s);
+      A.Recv(recv_hi, n_hi, ncclDouble, rank + 1, c, s);
     }
-    return ncclGroupEnd() == ncclSuccess ? 0 : 1;
+    return A.GroupEnd() == ncclSuccess ? 0 : 1;
   }
   int allgather(const double* send, double* recv, size_t count, cudaStream_t s) override {
-    return ncclAllGather(send, recv, count, ncclDouble, c, s) == ncclSuccess ? 0 : 1;
+    return nccl().AllGather(send, recv, count, ncclDouble, c, s) == ncclSuccess ? 0 : 1;
   }
 };
 
@@ -120,7 +161,7 @@ extern "C" {
 psp_status psp_comm_unique_id(void* id) {
   if (!id) return PSP_E_ARG;
   ncclUniqueId u;
-  if (ncclGetUniqueId(&u) != ncclSuccess) return PSP_E_NCCL;
+  if (!nccl().ok || nccl().GetUniqueId(&u) != ncclSuccess) return PSP_E_NCCL;
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
   memcpy(id, &u, sizeof(u));
   return PSP_OK;
@@ -138,7 +179,7 @@ psp_status psp_comm_init(const void* id, int nranks, int rank, psp_comm** out) {
     }
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
-    if (ncclCommInitRank(&c->c, nranks, u, rank) != ncclSuccess) {
+    if (!nccl().ok || nccl().CommInitRank(&c->c, nranks, u, rank) != ncclSuccess) {
       delete c;
       return PSP_E_NCCL;
     }
