@@ -253,15 +253,21 @@ __device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], dou
 // Descriptor layout per tile: [M (D*D) | t (D) | S (D)] doubles: the tile's affine map and
 // the exact state entering it.
 //
-// A sweep is three launches, each free of cross-block waits:
-//   tile_map_kernel    every tile's affine map state_out = M state_in + t (zero-state run plus
-//                      the d unit-state runs of the recurrence over its rows), one tile / block;
-//   tile_scan_kernel   one block composes the maps in processing order: exact incoming state of
-//                      every tile (and the state after the last row, s_out);
-//   tile_apply_kernel  every tile re-runs its rows from its exact incoming state and writes out.
-// The coefficients and the right-hand side are read twice (8(2d+3) B/row forward, 8(2d+5)
-// backward instead of 8(d+2) / 8(d+3)), traded for bandwidth-bound launches with no look-back
-// chain: a single-pass chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
+// A sweep is four launches, none with cross-block waits; block b owns a contiguous range of
+// 2048-row tiles in processing order:
+//   tile_map_kernel    walks its range from a zero incoming state: writes y0 (+ addend) and
+//                      composes the range's affine map state_out = M state_in + t (per tile:
+//                      zero-state run plus the d unit-state runs, block scan of thread maps);
+//   tile_scan_kernel   one block composes the <= 1024 range maps: exact incoming state of every
+//                      range (and the state after the last row, s_out);
+//   tile_fix_kernel    one thread per range adds the homogeneous response to its exact incoming
+//                      state, row by row, until it has decayed below 2^-60 of its start (under
+//                      the dominance gate, tens to hundreds of rows);
+//   tile_apply_kernel  re-walks, from the exact state, only the ranges whose response did not
+//                      decay within kFixCap rows.
+// So the coefficients and the right-hand side are read about once (8(d+2) forward, 8(d+3)
+// backward per row, plus the short corrections), with no look-back chain: a single-pass
+// chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
 
 // One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
 //                        BWD: z = (v - sum_k c[k] s[k]) / u0 (c[k] = U(i,i+k+1), s[k] = z_{i+k+1})
@@ -415,25 +421,67 @@ __device__ __forceinline__ Map<D> block_prefix(const Map<D>& my, Map<D>* wtot, M
 template <bool FWD, int D>
 __global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restrict__ lu, int64_t n,
                                                             const double* __restrict__ vin, const double* vscale,
-                                                            int64_t L, double* __restrict__ rmap) {
+                                                            const double* addend, double* out, int64_t L,
+                                                            double* __restrict__ rmap) {
+  // Walks its range from a ZERO incoming state: writes out = addend + y0 (the range's rows solved
+  // as if the state entering the range were 0) and composes the range map (M, t).  The exact
+  // solution differs from y0 only by the homogeneous response to the true incoming state,
+  // which tile_fix_kernel adds (it decays geometrically under the dominance gate).
   extern __shared__ double smem_dyn[];
   __shared__ Map<D> wtot[STPB / 32];
   constexpr int DW = D * D + 2 * D;
+  const int t = threadIdx.x;
   const int64_t ntiles = (n + STILE - 1) / STILE;
   const double vsc = vscale ? *vscale : 1.0;
+  double* sv = smem_dyn;
+  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
+  const double* su0 = sv + (1 + D) * STPB * SPAD;
   Map<D> range = identity_map<D>();
+  double s0[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) s0[i] = 0.0;
   const int64_t p0 = (int64_t)blockIdx.x * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
   for (int64_t p = p0; p < p1; ++p) {
     const int64_t tile = FWD ? p : ntiles - 1 - p;
     const int64_t base = tile * STILE;
-    stage_tile<FWD, D>(smem_dyn, lu, n, vin, vsc, base);
+    stage_tile<FWD, D>(sv, lu, n, vin, vsc, base);
     __syncthreads();
-    const Map<D> my = thread_map<FWD, D>(smem_dyn, base, n);
+    const Map<D> my = thread_map<FWD, D>(sv, base, n);
     Map<D> agg;
-    block_prefix<FWD, D>(my, wtot, agg);
+    const Map<D> pre = block_prefix<FWD, D>(my, wtot, agg);
     range = compose<D>(agg, range);
+    if (out != nullptr) {
+      double st[D];
+      apply<D>(pre, s0, st);
+#pragma unroll
+      for (int rr = 0; rr < SR; ++rr) {
+        const int r = FWD ? rr : (SR - 1 - rr);
+        if (base + (int64_t)t * SR + r >= n) continue;   // padding rows are transparent
+        const int sidx = t * SPAD + r;
+        double c[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) c[k] = sc[k][sidx];
+        const double u0 = FWD ? 1.0 : su0[sidx];
+        const double y = rec_step<FWD, D>(sv[sidx], c, st, u0);
+        push_state<D>(st, y);
+        sv[sidx] = y;
+      }
+      double s1[D];
+      apply<D>(agg, s0, s1);
+#pragma unroll
+      for (int i = 0; i < D; ++i) s0[i] = s1[i];
+      __syncthreads();
+      for (int q = t; q < STILE; q += STPB) {
+        const int64_t i = base + q;
+        if (i < n) {
+          const double y = sv[(q / SR) * SPAD + (q % SR)];
+          out[i] = addend ? addend[i] + y : y;
+        }
+      }
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     double* dd = rmap + blockIdx.x * DW;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -442,6 +490,66 @@ __global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restr
       for (int j = 0; j < D; ++j) dd[i * D + j] = range.M[i][j];
     }
   }
+}
+
+// One thread per range: out += the homogeneous response to the range's exact incoming state,
+// row by row from the range start, until it has decayed below 2^-60 of its initial size (the
+// rows beyond are unchanged to working precision); a range whose response has not decayed
+// within kFixCap rows is flagged for a full re-walk by tile_apply_kernel.
+constexpr int64_t kFixCap = 16384;
+template <bool FWD, int D>
+__global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_t L, int nr, double* out,
+                                const double* __restrict__ rmap, double* __restrict__ full) {
+  constexpr int DW = D * D + 2 * D;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  full[r] = 0.0;
+  double st[D], amax = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    st[i] = rmap[(int64_t)r * DW + D * D + D + i];
+    amax = fmax(amax, fabs(st[i]));
+  }
+  if (!(amax > 0.0)) return;                       // zero incoming state: y0 is exact
+  const double stop = amax * 0x1p-60;
+  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t t0 = (int64_t)r * L, t1 = (t0 + L < ntiles) ? t0 + L : ntiles;
+  // rows of the range in processing order
+  const int64_t lo = (FWD ? t0 : ntiles - t1) * STILE;
+  const int64_t hi = ((FWD ? t1 : ntiles - t0) * STILE < n) ? (FWD ? t1 : ntiles - t0) * STILE : n;
+  const int64_t len = hi - lo;
+  const int64_t cap = len < kFixCap ? len : kFixCap;
+  int64_t q = 0;
+  for (; q < cap; q += 8) {
+    // the coefficients of the next 8 rows first (independent of the recurrence)
+    double c8[8][D], u8[8], o8[8];
+    int64_t idx[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t qq = q + e;
+      idx[e] = FWD ? lo + qq : hi - 1 - qq;
+      const bool ok = qq < cap;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int o = FWD ? (D - 1 - k) : (D + 1 + k);
+        c8[e][k] = ok ? __ldg(lu + (int64_t)o * n + idx[e]) : 0.0;
+      }
+      u8[e] = (!FWD && ok) ? __ldg(lu + (int64_t)D * n + idx[e]) : 1.0;
+      o8[e] = ok ? out[idx[e]] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (q + e >= cap) break;
+      const double y = rec_step<FWD, D>(0.0, c8[e], st, u8[e]);
+      push_state<D>(st, y);
+      out[idx[e]] = o8[e] + y;
+    }
+    double m = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) m = fmax(m, fabs(st[i]));
+    if (m <= stop) return;                         // decayed: the rest of the range is exact
+  }
+  if (q < len) full[r] = 1.0;                      // not decayed within the cap: full re-walk
 }
 
 // one block: exact incoming state of every range (processing order), s_out after the last
@@ -494,7 +602,8 @@ template <bool FWD, int D>
 __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __restrict__ lu, int64_t n,
                                                               const double* __restrict__ vin, const double* vscale,
                                                               const double* addend, double* out, int64_t L,
-                                                              const double* __restrict__ rmap) {
+                                                              const double* __restrict__ rmap,
+                                                              const double* __restrict__ full) {
   extern __shared__ double smem_dyn[];
   __shared__ Map<D> wtot[STPB / 32];
   constexpr int DW = D * D + 2 * D;
@@ -504,6 +613,7 @@ __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __res
   double* sv = smem_dyn;
   const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
   const double* su0 = sv + (1 + D) * STPB * SPAD;
+  if (full != nullptr && full[blockIdx.x] == 0.0) return;   // tile_fix_kernel completed this range
   double s0[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) s0[i] = rmap[blockIdx.x * DW + D * D + D + i];
@@ -582,10 +692,14 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
   if (nb < 1) nb = 1;
   const int64_t L = (ntiles + nb - 1) / nb;
   nb = (ntiles + L - 1) / L;
-  if (ntiles > 0) tile_map_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, L, sc.states);
+  double* full = sc.states + (size_t)SCAN_T * (D * D + 2 * D);   // per-range flag
+  if (ntiles > 0)
+    tile_map_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
   tile_scan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>(ntiles > 0 ? (int)nb : 0, sc.states, s_in0, s_out);
-  if (out != nullptr && ntiles > 0)
-    tile_apply_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
+  if (out != nullptr && ntiles > 0) {
+    tile_fix_kernel<FWD, D><<<(unsigned)((nb + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nb, out, sc.states, full);
+    tile_apply_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states, full);
+  }
 }
 
 void sweep(bool fwd, int d, const double* lu, int64_t n, const double* v, const double* vs,
@@ -651,7 +765,7 @@ size_t banded_scratch_bytes(int64_t n, int d) {
   const int64_t DW = d * d + 2 * d;
   size_t b = 64 + 256;
   b += (size_t)ntiles * 8 + 256;
-  b += (size_t)ntiles * DW * 8 + 256;
+  b += (size_t)((ntiles > SCAN_T ? ntiles : SCAN_T) * DW + SCAN_T) * 8 + 256;   // range maps + flags
   b += (size_t)2 * nchunks * d * (d + 1) * 8 + 256;
   b += (size_t)n * 8 + 256;
   return b;
@@ -667,8 +781,8 @@ BandedScratch banded_scratch(void* base, int64_t n, int d) {
   sc.tickets = (unsigned long long*)p;          // [0..3] ctl, [4..] flags
   sc.changed = (int*)(p + 32);                  // [0] changed, [1] bad
   p = align256(p + 64 + (size_t)ntiles * 8 + 64);
-  sc.states = (double*)p;                       // descriptors (solve)
-  p = align256(p + (size_t)ntiles * DW * 8);
+  sc.states = (double*)p;                       // range maps / states + flags (solve)
+  p = align256(p + (size_t)((ntiles > SCAN_T ? ntiles : SCAN_T) * DW + SCAN_T) * 8);
   sc.y = (double*)p;                            // intermediate vector, then factor states
   sc.desc_count = ntiles;
   return sc;
