@@ -28,6 +28,8 @@
 // accumulators, so HBM streams while the block computes.
 #include <cuda.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "givens.cuh"
 #include "internal.h"
@@ -48,6 +50,10 @@ struct FusedArgs {
   int dst_slot;
   int zchunk;          // planes per tile along the march axis
   int64_t tiles_x, tiles_y, ntiles;
+  // thread-block clusters (clx x cly tiles per cluster, 1 x 1 = none): the CTAs of a cluster
+  // march adjacent tiles in step, so the halo boxes they share are L2 hits, not HBM re-reads
+  int clx, cly, psync;
+  int64_t ctiles_x, ctiles_y, nits;
   DevState ds;
 };
 
@@ -75,6 +81,11 @@ __device__ __forceinline__ double butterfly8(double (&v)[8], int lane) {
   r += __shfl_xor_sync(0xffffffffu, r, 16);
   return r;
 }
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -220,16 +231,35 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     }
   };
 
-  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    int64_t b = tile;
-    const int64_t txi = b % a.tiles_x;
-    b /= a.tiles_x;
-    const int64_t tyi = b % a.tiles_y;
-    const int64_t zci = b / a.tiles_y;
+  const int ncl = a.clx * a.cly;
+  const int64_t it0 = blockIdx.x / ncl, its = gridDim.x / ncl;
+  const int rk = blockIdx.x % ncl;               // rank in the cluster (cluster dims along x)
+  const bool psync = ncl > 1 && a.psync;
+  for (int64_t it = it0; it < a.nits; it += its) {
+    int64_t b = it;
+    const int64_t cxi = b % a.ctiles_x;
+    b /= a.ctiles_x;
+    const int64_t cyi = b % a.ctiles_y;
+    const int64_t zci = b / a.ctiles_y;
+    const int64_t txi = cxi * a.clx + rk % a.clx, tyi = cyi * a.cly + rk / a.clx;
+    if (ncl > 1) {                               // the cluster starts its tiles together
+      cluster_arrive();
+      cluster_wait();
+    }
     // the box's inner start must be 16-byte aligned: x0 even, halo lanes 1 and TX-2
     const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
     const int64_t z0 = zci * a.zchunk;
     const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
+    if (txi >= a.tiles_x || tyi >= a.tiles_y) {  // cluster slot past the grid edge: keep the beat
+      if (psync) {
+        for (int64_t p = z0; p < z1; ++p) {
+          if (p > z0) cluster_wait();
+          cluster_arrive();
+        }
+        cluster_wait();
+      }
+      continue;
+    }
     const int64_t gx = x0 + lx, gy = y0 + ly;
     const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
     const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
@@ -380,6 +410,10 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
       if (half == 0) Us[bn * NT + pt] = un;
       __syncthreads();                            // stage p consumed; Us(p+1) visible
       if (warp == 0 && p + NST <= z1) issue(p + NST);
+      if (psync) {                                // at most one plane apart within the cluster
+        if (p > z0) cluster_wait();
+        cluster_arrive();
+      }
       ub = uc; uc = un;
       kb = kc; kc = kt;
       g += plane;
@@ -387,6 +421,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     }
     // drain: every issued stage has been waited on (planes z0-1 .. z1), so the barriers'
     // parities stay in step for the next tile
+    if (psync) cluster_wait();
   }
 
   // reduce the accumulators across the points of the warp (value -> slot j0 + j)
@@ -549,13 +584,55 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   int64_t zc = txy * st.nz / (148 * 4);            // about 4 tiles per SM
   if (zc > 64) zc = 64;
   if (zc < 8) zc = 8;
+  static const int zc_env = getenv("PSP_FUSED_ZC") ? atoi(getenv("PSP_FUSED_ZC")) : 0;  // tuning knob
+  if (zc_env > 0) zc = zc_env;
   if (zc > st.nz) zc = st.nz;
   a.zchunk = (int)zc;
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
   if (!mc.ok) return g_map_err ? g_map_err : -1;
+  // cluster shape "CXxCY" (tuning knob; default none)
+  static int clx = 1, cly = 1, psync = 0, cl_read = 0;
+  if (!cl_read) {
+    const char* e = getenv("PSP_FUSED_CL");
+    if (e && sscanf(e, "%dx%d", &clx, &cly) != 2) clx = cly = 1;
+    if (clx < 1 || cly < 1 || clx * cly > 8) clx = cly = 1;
+    psync = getenv("PSP_FUSED_PSYNC") ? atoi(getenv("PSP_FUSED_PSYNC")) : 1;
+    cl_read = 1;
+  }
+  a.clx = clx;
+  a.cly = TY > 1 ? cly : 1;
+  a.psync = psync;
+  const int ncl = a.clx * a.cly;
+  a.ctiles_x = (a.tiles_x + a.clx - 1) / a.clx;
+  a.ctiles_y = (a.tiles_y + a.cly - 1) / a.cly;
+  a.nits = a.ctiles_x * a.ctiles_y * ((st.nz + zc - 1) / zc);
+  auto kern = fused_tma_kernel<KIND, TX, TY, KMAX, CS>;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(TX, TY * CS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
   int64_t grid = 148;                              // one resident block per SM (persistent)
-  if (grid > a.ntiles) grid = a.ntiles;
-  fused_tma_kernel<KIND, TX, TY, KMAX, CS><<<(unsigned)grid, dim3(TX, TY * CS), Cfg::SMEM, s>>>(mc.mpx, mc.mpy, mc.mk, a);
+  if (ncl > 1) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)ncl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int maxcl[9] = {0};
+    if (maxcl[ncl] == 0) {
+      cfg.gridDim = dim3((unsigned)(ncl * 148));
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) nc = 148 / ncl;
+      maxcl[ncl] = nc;
+      if (getenv("PSP_FUSED_VERBOSE")) fprintf(stderr, "fused: %d active clusters of %d\n", nc, ncl);
+    }
+    grid = (int64_t)maxcl[ncl] * ncl;
+  }
+  if (grid / ncl > a.nits) grid = a.nits * ncl;
+  cfg.gridDim = dim3((unsigned)grid);
+  if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, a) != cudaSuccess) return -2;
   return 0;
 }
 
