@@ -267,7 +267,7 @@ void psp_default_opts(psp_opts* o) {
   o->gate = 1;
   o->timing = 0;
   o->fused = 1;
-  o->fused_kmin = 4;
+  o->fused_kmin = 2;
   o->fused_kmax = 16;
 }
 

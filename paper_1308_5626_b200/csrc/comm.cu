@@ -114,12 +114,19 @@ struct LoopGroup {
   }
 };
 
+// Every copy runs on the rank's own stream and is waited for before the next barrier: a plain
+// cudaMemcpy runs on the legacy stream, which does not order against the non-blocking streams the
+// contexts run on, and a device-to-device (or pageable host-to-device) cudaMemcpy may return
+// before the copy lands -- the peer could then overwrite its send buffer, or this rank's next
+// kernel read the receive buffer, while the copy is still in flight.
 struct LoopComm : psp_comm {
   std::shared_ptr<LoopGroup> g;
   int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
     if (cudaStreamSynchronize(s) != cudaSuccess) return 1;
     g->host[rank].resize(count);
-    if (cudaMemcpy(g->host[rank].data(), d, count * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    if (cudaMemcpyAsync(g->host[rank].data(), d, count * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return 1;
     g->barrier();
     std::vector<double> r(g->host[0]);
     for (int q = 1; q < nranks; ++q)  // rank order: identical on every rank
@@ -128,7 +135,8 @@ struct LoopComm : psp_comm {
         r[i] = op == 0 ? r[i] + v : (op == 1 ? (v > r[i] ? v : r[i]) : (v < r[i] ? v : r[i]));
       }
     g->barrier();
-    return cudaMemcpy(d, r.data(), count * 8, cudaMemcpyHostToDevice) == cudaSuccess ? 0 : 1;
+    return (cudaMemcpyAsync(d, r.data(), count * 8, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaStreamSynchronize(s) == cudaSuccess) ? 0 : 1;
   }
   int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
                double* recv_hi, size_t n_hi, cudaStream_t s) override {
@@ -137,8 +145,11 @@ struct LoopComm : psp_comm {
     g->p_hi[rank] = send_hi;
     g->barrier();
     int err = 0;
-    if (rank > 0 && n_lo && cudaMemcpy(recv_lo, g->p_hi[rank - 1], n_lo * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
-    if (rank < nranks - 1 && n_hi && cudaMemcpy(recv_hi, g->p_lo[rank + 1], n_hi * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
+    if (rank > 0 && n_lo &&
+        cudaMemcpyAsync(recv_lo, g->p_hi[rank - 1], n_lo * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) err = 1;
+    if (rank < nranks - 1 && n_hi &&
+        cudaMemcpyAsync(recv_hi, g->p_lo[rank + 1], n_hi * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) err = 1;
+    if (cudaStreamSynchronize(s) != cudaSuccess) err = 1;
     g->barrier();
     return err;
   }
@@ -148,7 +159,8 @@ struct LoopComm : psp_comm {
     g->barrier();
     int err = 0;
     for (int q = 0; q < nranks; ++q)
-      if (cudaMemcpy(recv + q * count, g->p_all[q], count * 8, cudaMemcpyDeviceToDevice) != cudaSuccess) err = 1;
+      if (cudaMemcpyAsync(recv + q * count, g->p_all[q], count * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) err = 1;
+    if (cudaStreamSynchronize(s) != cudaSuccess) err = 1;
     g->barrier();
     return err;
   }

@@ -34,6 +34,13 @@
 #include "givens.cuh"
 #include "internal.h"
 
+#ifndef PSP_FUSED_NSTMAX
+#define PSP_FUSED_NSTMAX 12   // stage ring depth cap (narrow steps: many planes in flight)
+#endif
+#ifndef PSP_VREG_MAX
+#define PSP_VREG_MAX 12
+#endif
+
 namespace psp {
 namespace {
 
@@ -123,10 +130,10 @@ struct FCfg {
   static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
   static constexpr int STAGE = NB * NT;                      // doubles
   // as many stages as fit in 225 KB (planes p and p+1 are resident, the rest are in flight)
-  static constexpr int NSTF = (int)((225 * 1024 - 2 * NT * 8 - 256) / (STAGE * 8));
-  static constexpr int NST = NSTF > 6 ? 6 : NSTF;
+  static constexpr int NSTF = (int)((225 * 1024 - 2 * NT * 8 - 256) / (STAGE * 8 + 8));
+  static constexpr int NST = NSTF > PSP_FUSED_NSTMAX ? PSP_FUSED_NSTMAX : NSTF;
   static_assert(NST >= 3, "a stage ring needs planes p, p+1 and one in flight");
-  static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)2 * NT * 8 + 64 + 128;
+  static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)2 * NT * 8 + 8 * NST + 128;
 };
 
 // Half-warp transposing butterfly (CS = 2): v[0..7] per lane -> lane l holds the sum over the
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
   constexpr bool REG = KJ <= 16;           // per-thread accumulators (else per-plane butterflies)
   constexpr int NCH = (KJ + 7) / 8;
   constexpr int NACC = REG ? KJ : NCH;
-  constexpr bool VREG = KJ <= 8;           // keep a plane's basis values in registers for the l_j
+  constexpr bool VREG = KJ <= PSP_VREG_MAX; // keep a plane's basis values in registers for the l_j
   static_assert(CS == 1 || CS == 2, "column split 1 or 2");
   extern __shared__ __align__(128) double fsm[];
   // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
@@ -268,14 +275,21 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     const int64_t col = in_grid ? gx + st.nx * gy : 0;
     const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
 
-    // warp 0: the boxes of plane q, one box per lane (lane 0 arms the barrier with the byte count)
+    // the boxes of plane q (warp 0 arms the barrier with the byte count)
     auto issue = [&](int64_t q) {
       const int si = (int)((q - z0 + 1) % NST);
       double* sb = stages + (size_t)si * Cfg::STAGE;
       const int zq = (int)q;                     // may be -1 or nz: zero-filled by the TMA unit
+      // CS = 2 (k > 16, up to 34 boxes a plane): the boxes are spread over the warps, one lane
+      // each -- a TMA issue is a uniform-datapath instruction, so one warp's boxes serialise and
+      // would carry the plane's issue latency into the next block barrier (a complete_tx that
+      // lands before the expect_tx leaves the tx-count transiently negative, which the mbarrier
+      // allows).  Narrower steps: warp 0's lanes (measured faster there).
+      constexpr int IW = (CS == 2) ? NW : 1;     // issuing warps
+      if (warp >= IW || (IW > 1 && (lane != 0 || warp >= nload))) return;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (lane == 0) mbar_expect_tx(bars + si, stage_bytes);
-      for (int j = lane; j < nload; j += 32) {
+      if (warp == 0 && lane == 0) mbar_expect_tx(bars + si, stage_bytes);
+      for (int j = (IW > 1 ? warp : lane); j < nload; j += (IW > 1 ? NW : 32)) {
         if (j < (k > 0 ? k : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], bars + si);
         else if (j == (k > 0 ? k : 0)) tma4(sb + KMAX * NT, a.src_px ? &mpx : &mpy, x0, y0, zq, a.src_slot, bars + si);
         else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, bars + si);
@@ -328,8 +342,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
       }
     };
 
-    if (warp == 0)
-      for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
+    for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
     // prologue: u(z0-1), u(z0) (+ l-products of plane z0)
     double vr[KJ];
     const double* sbm = wait_stage(z0 - 1);
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     }
     if (half == 0) Us[(z0 & 1) * NT + pt] = uc;
     __syncthreads();                              // stage z0-1 consumed; Us(z0) visible
-    if (warp == 0 && z0 - 1 + NST <= z1) issue(z0 - 1 + NST);
+    if (z0 - 1 + NST <= z1) issue(z0 - 1 + NST);
 
     int sp_i = 1 % NST;                           // stage of plane p
     for (int64_t p = z0; p < z1; ++p) {
@@ -409,7 +422,7 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
       if (k > 0) add_products(sp, w, acct);       // t_j = V_j(p)' w~(p); w = 0 off emitted points
       if (half == 0) Us[bn * NT + pt] = un;
       __syncthreads();                            // stage p consumed; Us(p+1) visible
-      if (warp == 0 && p + NST <= z1) issue(p + NST);
+      if (p + NST <= z1) issue(p + NST);
       if (psync) {                                // at most one plane apart within the cluster
         if (p > z0) cluster_wait();
         cluster_arrive();
@@ -584,21 +597,19 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   int64_t zc = txy * st.nz / (148 * 4);            // about 4 tiles per SM
   if (zc > 64) zc = 64;
   if (zc < 8) zc = 8;
-  static const int zc_env = getenv("PSP_FUSED_ZC") ? atoi(getenv("PSP_FUSED_ZC")) : 0;  // tuning knob
+  const char* zce = getenv("PSP_FUSED_ZC");      // tuning knobs (read per launch: cheap next to a pass)
+  const int zc_env = zce ? atoi(zce) : 0;
   if (zc_env > 0) zc = zc_env;
   if (zc > st.nz) zc = st.nz;
   a.zchunk = (int)zc;
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
   if (!mc.ok) return g_map_err ? g_map_err : -1;
   // cluster shape "CXxCY" (tuning knob; default none)
-  static int clx = 1, cly = 1, psync = 0, cl_read = 0;
-  if (!cl_read) {
-    const char* e = getenv("PSP_FUSED_CL");
-    if (e && sscanf(e, "%dx%d", &clx, &cly) != 2) clx = cly = 1;
-    if (clx < 1 || cly < 1 || clx * cly > 8) clx = cly = 1;
-    psync = getenv("PSP_FUSED_PSYNC") ? atoi(getenv("PSP_FUSED_PSYNC")) : 1;
-    cl_read = 1;
-  }
+  int clx = 1, cly = 1;
+  const char* e = getenv("PSP_FUSED_CL");
+  if (e && sscanf(e, "%dx%d", &clx, &cly) != 2) clx = cly = 1;
+  if (clx < 1 || cly < 1 || clx * cly > 8) clx = cly = 1;
+  const int psync = getenv("PSP_FUSED_PSYNC") ? atoi(getenv("PSP_FUSED_PSYNC")) : 1;
   a.clx = clx;
   a.cly = TY > 1 ? cly : 1;
   a.psync = psync;
@@ -639,7 +650,12 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
 template <int KIND>
 int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, cudaStream_t s) {
   if (three_d) {
+    // stage = (KMAX + 2) boxes: the narrowest instantiation that holds k columns keeps the most
+    // planes in flight (measured at 512^3: k <= 4 1.9 vs 2.3 ms, k = 9..12 3.5-3.8 vs 3.8-4.1 ms).
+    // 32 x 8 tiles for k <= 16 or 16 x 8 tiles for k > 16 were slower (more halo points per tile).
+    if (a.k <= 4) return launch_t<KIND, 32, 16, 4, 1>(a, rpx, rpy, s);
     if (a.k <= 8) return launch_t<KIND, 32, 16, 8, 1>(a, rpx, rpy, s);
+    if (a.k <= 12) return launch_t<KIND, 32, 16, 12, 1>(a, rpx, rpy, s);
     if (a.k <= 16) return launch_t<KIND, 32, 16, 16, 1>(a, rpx, rpy, s);
     if (a.k <= 24) return launch_t<KIND, 32, 8, 24, 2>(a, rpx, rpy, s);
     return launch_t<KIND, 32, 8, 32, 2>(a, rpx, rpy, s);
