@@ -11,21 +11,26 @@
 // column k (l.19-32) and solves (I + L) h = s for step k+1's MGS coefficients.
 //
 // Bytes per row and step: k basis columns + w~_k + kappa read, u + w~ written = 8(k+4), against
-// 8(2k+7) for separate matvec / dots / update passes.
+// 8(2k+7) for separate matvec / dots / update passes.  Measured at 512^3 (tools/kstep.py):
+// k <= 4 1.8 ms, k = 5..8 2.3-2.5, k = 9..12 2.9-3.2, k = 13..16 4.3-5.0 ms a pass; the split
+// passes win from k = 17 (the two-threads-per-point tiles carry 1.6x halo work).
 //
-// Work layout: a block of TX x TY threads owns a TX x TY tile of the (x, y) plane (3-D: 32 x 16
-// or 32 x 8; 2-D / 1-D: 256 x 1) and marches a chunk of planes along the slowest axis.  One
-// thread = one point.  Tiles overlap: threads on the tile edge compute u at their point (the
-// stencil halo) but emit nothing, so no block ever waits for another (in x the tile starts two
-// points before its interior: a TMA box's inner start must be 16-byte aligned).  Operands arrive by TMA: one elected thread issues, per plane, a tensor-tile load
+// Work layout: the compute threads of a block own a TX x TY tile of the (x, y) plane (3-D:
+// 32 x 15, or 32 x 7 with two threads per point for k > 16; 2-D / 1-D: 256 x 1 or 224 x 1) and
+// march a chunk of planes along the slowest axis.  Tiles overlap: threads on the tile edge
+// compute u at their point (the stencil halo) but emit nothing, so no block ever waits for
+// another (in x the tile starts two points before its interior: a TMA box's inner start must be
+// 16-byte aligned).  One extra producer warp issues, per plane, a tensor-tile load
 // (cp.async.bulk.tensor, 4-D map over the probe ring: x, y, plane, slot) for each of the k basis
-// columns, for w~_k and for kappa into a 3-deep ring of shared-memory stages (planes p, p+1,
-// p+2 resident), completion on one mbarrier per stage; out-of-grid boxes are zero-filled by the
-// TMA unit, which is exactly the Dirichlet extension u = 0.  Per plane p: u(p+1) from stage p+1
-// (and the l_j = V_j'u products), w~(p) = A u(p) from u(p-1), u(p+1) in registers and the
-// in-plane neighbours of plane p in shared memory (one barrier per plane), t_j = V_j(p)'w~(p)
-// from stage p; then stage p is refilled with plane p+3.  Registers hold only the
-// accumulators, so HBM streams while the block computes.
+// columns, for w~_k and for kappa into a ring of shared-memory stages (as many as fit: up to 12
+// for narrow steps), completion on one `full` mbarrier per stage; out-of-grid boxes are
+// zero-filled by the TMA unit, which is exactly the Dirichlet extension u = 0.  Per plane p the
+// compute warps form u(p+1) from stage p+1 and publish it (with kappa) to a 4-plane ring, then
+// w~(p) = A u(p) from u(p-1), u(p+1) in registers and the in-plane neighbours of plane p from
+// the ring, and t_j = V_j(p)'w~(p).  For k <= 12 a thread's basis values of plane p+1 are kept
+// in registers for those t_j, so stage p+1 goes back to the producer (an `empty` mbarrier
+// arrival per warp) as soon as u(p+1) is formed: all stages but one are in flight.  There is no
+// block-wide barrier in the plane loop: warps meet only on the u-ring mbarriers.
 #include <cuda.h>
 #include <math.h>
 #include <stdio.h>
@@ -36,9 +41,6 @@
 
 #ifndef PSP_FUSED_NSTMAX
 #define PSP_FUSED_NSTMAX 12   // stage ring depth cap (narrow steps: many planes in flight)
-#endif
-#ifndef PSP_VREG_MAX
-#define PSP_VREG_MAX 12
 #endif
 
 namespace psp {
@@ -57,10 +59,6 @@ struct FusedArgs {
   int dst_slot;
   int zchunk;          // planes per tile along the march axis
   int64_t tiles_x, tiles_y, ntiles;
-  // thread-block clusters (clx x cly tiles per cluster, 1 x 1 = none): the CTAs of a cluster
-  // march adjacent tiles in step, so the halo boxes they share are L2 hits, not HBM re-reads
-  int clx, cly, psync;
-  int64_t ctiles_x, ctiles_y, nits;
   DevState ds;
 };
 
@@ -88,11 +86,6 @@ __device__ __forceinline__ double butterfly8(double (&v)[8], int lane) {
   r += __shfl_xor_sync(0xffffffffu, r, 16);
   return r;
 }
-
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -124,16 +117,22 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int x, i
       : "memory");
 }
 
-template <int TX, int TY, int KMAX>
+template <int TX, int TY, int KMAX, int CS>
 struct FCfg {
   static constexpr int NT = TX * TY;
+  static constexpr int NUB = 4;                              // u (and kappa) plane ring depth
+  // RV: a plane's basis values are held in registers from its u to its t_j products, so its stage
+  // is released as soon as u is formed (all but one stage in flight; the plane's kappa moves to
+  // a kappa plane ring beside the u ring); wider thread column sets (KJ = 16) do not fit the
+  // 128-register budget and keep the stage for the t_j and the stencil's kappa instead
+  static constexpr bool RV = KMAX / CS <= 12;
   static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
   static constexpr int STAGE = NB * NT;                      // doubles
-  // as many stages as fit in 225 KB (planes p and p+1 are resident, the rest are in flight)
-  static constexpr int NSTF = (int)((225 * 1024 - 2 * NT * 8 - 256) / (STAGE * 8 + 8));
+  static constexpr int RING = (RV ? 2 : 1) * NUB * NT;       // u (+ kappa) plane rings, doubles
+  static constexpr int NSTF = (int)((225 * 1024 - RING * 8 - 256) / (STAGE * 8 + 16));
   static constexpr int NST = NSTF > PSP_FUSED_NSTMAX ? PSP_FUSED_NSTMAX : NSTF;
-  static_assert(NST >= 3, "a stage ring needs planes p, p+1 and one in flight");
-  static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)2 * NT * 8 + 8 * NST + 128;
+  static_assert(NST >= 3, "a stage ring needs two resident planes and one in flight");
+  static constexpr size_t SMEM = (size_t)NST * STAGE * 8 + (size_t)RING * 8 + 16 * NST + 8 * NUB + 128;
 };
 
 // Half-warp transposing butterfly (CS = 2): v[0..7] per lane -> lane l holds the sum over the
@@ -156,38 +155,53 @@ __device__ __forceinline__ double butterfly8_half(double (&v)[8], int lane) {
 
 // CS = 2 (the widest steps): two threads per point, each owning half of the basis columns (the
 // two halves of a warp hold the same 16 points), so a 32 x 8 tile -- the largest whose stage
-// ring fits shared memory at k = 32 -- still runs 16 warps per SM.  The halves' partial MGS
-// updates meet by one shuffle; each half keeps the dot products of its own columns.
+// ring fits shared memory at k = 32 -- still runs 16 compute warps per SM.  The halves' partial
+// MGS updates meet by one shuffle; each half keeps the dot products of its own columns.
+//
+// Warp roles: NT*CS compute threads plus one producer warp.  The producer issues the TMA boxes
+// of plane after plane into the stage ring as soon as the compute warps release a stage (one
+// `empty` mbarrier arrival per compute warp), so no compute warp carries the issue and there is
+// no block-wide barrier in the plane loop: the in-plane u values the stencil needs are published
+// through a 4-deep ring of shared-memory planes, each with an mbarrier the compute warps arrive
+// on when they have written it (4 deep: a warp overwriting a plane buffer has already seen
+// every warp's write of the plane two after the one last read from it).
 template <int KIND, int TX, int TY, int KMAX, int CS>
-__global__ void __launch_bounds__(TX * TY * CS, 1)
+__global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap mpx, const __grid_constant__ CUtensorMap mpy,
                      const __grid_constant__ CUtensorMap mkap, FusedArgs a) {
-  using Cfg = FCfg<TX, TY, KMAX>;
+  using Cfg = FCfg<TX, TY, KMAX, CS>;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
   constexpr bool HASY = TY > 1;
   constexpr int NT = Cfg::NT, NST = Cfg::NST;      // NT points per tile
-  constexpr int NTH = NT * CS, NW = NTH / 32;       // threads
+  constexpr int NC = NT * CS, NWC = NC / 32;        // compute threads / warps
+  constexpr int NTH = NC + 32, NW = NWC + 1;        // + the producer warp
+  constexpr int NUB = Cfg::NUB;
   constexpr int KJ = KMAX / CS;                     // basis columns per thread
   constexpr bool REG = KJ <= 16;           // per-thread accumulators (else per-plane butterflies)
   constexpr int NCH = (KJ + 7) / 8;
   constexpr int NACC = REG ? KJ : NCH;
-  constexpr bool VREG = KJ <= PSP_VREG_MAX; // keep a plane's basis values in registers for the l_j
+  constexpr bool RV = Cfg::RV;
   static_assert(CS == 1 || CS == 2, "column split 1 or 2");
+  static_assert(NC % 32 == 0, "whole compute warps");
   extern __shared__ __align__(128) double fsm[];
   // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
   double* stages = fsm + (((128u - (su32(fsm) & 127u)) & 127u) >> 3);
-  double* Us = stages + NST * Cfg::STAGE;    // [2][NT] u of planes p, p+1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Us + 2 * NT);
+  double* Us = stages + NST * Cfg::STAGE;    // [NUB][NT] u planes
+  double* Ks = Us + NUB * NT;                // [NUB][NT] kappa planes (RV)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + NST * Cfg::STAGE + Cfg::RING);
+  uint64_t* empty = full + NST;
+  uint64_t* ubar = empty + NST;
   __shared__ double hs[KMAX];
   __shared__ int vslot[KMAX];
   __shared__ double tot[2 * KMAX + 2];
   __shared__ bool s_last;
 
   const Stencil& st = a.st;
-  const int t = threadIdx.y * TX + threadIdx.x, lane = t & 31, warp = t >> 5;
-  // this thread's point and column half
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool producer = warp == NWC;
+  // this thread's point and column half (the producer warp aliases points 0..31: unused)
   const int half = (CS == 2) ? (lane >> 4) : 0;
-  const int pt = (CS == 2) ? warp * 16 + (lane & 15) : t;
+  const int pt = producer ? lane : ((CS == 2) ? warp * 16 + (lane & 15) : t);
   const int lx = pt % TX, ly = pt / TX;
   const int j0 = half * KJ;
   const int k = a.k;
@@ -197,11 +211,15 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
     vslot[t] = (a.vs1 + t) % a.cap;
   }
   // columns j >= k are never loaded: zero them once in every stage (coefficient 0, product 0)
-  if (half == 0)
+  if (!producer && half == 0)
     for (int s = 0; s < NST; ++s)
       for (int j = k; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + pt] = 0.0;
   if (t == 0) {
-    for (int q = 0; q < NST; ++q) mbar_init(bars + q, 1);
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, NWC);
+    }
+    for (int q = 0; q < NUB; ++q) mbar_init(ubar + q, NWC);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mpx)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mpy)) : "memory");
@@ -212,229 +230,233 @@ __global__ void __launch_bounds__(TX * TY * CS, 1)
 
   const int nload = (k == 0 ? 0 : k) + 1 + (cell ? 1 : 0);
   const unsigned stage_bytes = (unsigned)(nload * NT * 8);
-  unsigned phase_bits = 0;                   // parity of each stage's next completion
 
   double accl[NACC], acct[NACC];
 #pragma unroll
   for (int c = 0; c < NACC; ++c) { accl[c] = 0.0; acct[c] = 0.0; }
   double nu = 0.0, tu = 0.0;
-  const double hsx = 0.5 * st.s[0], hsy = 0.5 * st.s[1], hsz = 0.5 * st.s[2];
-  const int64_t plane = st.nx * st.ny;
 
-  // products of this thread's columns with f (f = 0 for points that are not counted)
-  auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, double f, double (&acc)[NACC]) {
-    if (REG) {
-#pragma unroll
-      for (int j = 0; j < KJ; ++j) acc[j] = fma(vcol[(j0 + j) * NT + pt], f, acc[j]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (c * 8 >= k) break;                   // uniform
-        double v8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v8[q] = vcol[(j0 + c * 8 + q) * NT + pt] * f;
-        acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
-      }
-    }
-  };
-
-  const int ncl = a.clx * a.cly;
-  const int64_t it0 = blockIdx.x / ncl, its = gridDim.x / ncl;
-  const int rk = blockIdx.x % ncl;               // rank in the cluster (cluster dims along x)
-  const bool psync = ncl > 1 && a.psync;
-  for (int64_t it = it0; it < a.nits; it += its) {
-    int64_t b = it;
-    const int64_t cxi = b % a.ctiles_x;
-    b /= a.ctiles_x;
-    const int64_t cyi = b % a.ctiles_y;
-    const int64_t zci = b / a.ctiles_y;
-    const int64_t txi = cxi * a.clx + rk % a.clx, tyi = cyi * a.cly + rk / a.clx;
-    if (ncl > 1) {                               // the cluster starts its tiles together
-      cluster_arrive();
-      cluster_wait();
-    }
-    // the box's inner start must be 16-byte aligned: x0 even, halo lanes 1 and TX-2
-    const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
-    const int64_t z0 = zci * a.zchunk;
-    const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
-    if (txi >= a.tiles_x || tyi >= a.tiles_y) {  // cluster slot past the grid edge: keep the beat
-      if (psync) {
-        for (int64_t p = z0; p < z1; ++p) {
-          if (p > z0) cluster_wait();
-          cluster_arrive();
+  if (producer) {
+    // ---- producer: planes z0-1 .. z1 of every tile, in the order the compute warps take them ----
+    uint32_t gs = 0;                             // running stage count (slot gs % NST)
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      int64_t b = tile;
+      const int64_t txi = b % a.tiles_x;
+      b /= a.tiles_x;
+      const int64_t tyi = b % a.tiles_y;
+      const int64_t zci = b / a.tiles_y;
+      const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
+      const int64_t z0 = zci * a.zchunk;
+      const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
+      for (int64_t q = z0 - 1; q <= z1; ++q, ++gs) {
+        const int si = (int)(gs % NST);
+        // the slot's previous plane released by every compute warp (fresh barrier: passes)
+        mbar_wait(empty + si, ((gs / NST) & 1u) ^ 1u);
+        double* sb = stages + (size_t)si * Cfg::STAGE;
+        const int zq = (int)q;                   // may be -1 or nz: zero-filled by the TMA unit
+        if (lane == 0) mbar_expect_tx(full + si, stage_bytes);
+        __syncwarp();
+        for (int j = lane; j < nload; j += 32) {
+          if (j < (k > 0 ? k : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], full + si);
+          else if (j == (k > 0 ? k : 0)) tma4(sb + KMAX * NT, a.src_px ? &mpx : &mpy, x0, y0, zq, a.src_slot, full + si);
+          else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, full + si);
         }
-        cluster_wait();
       }
-      continue;
     }
-    const int64_t gx = x0 + lx, gy = y0 + ly;
-    const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
-    const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
-    const bool own = interior && in_grid;
-    const bool emit = own && half == 0;          // stores and the u / w~ scalars: one thread per point
-    const int64_t col = in_grid ? gx + st.nx * gy : 0;
-    const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
+  } else {
+    // ---- compute warps ----
+    const double hsx = 0.5 * st.s[0], hsy = 0.5 * st.s[1], hsz = 0.5 * st.s[2];
+    const int64_t plane = st.nx * st.ny;
+    uint32_t gs = 0;                             // running stage count, as the producer's
+    uint32_t us = 0;                             // running u-plane count (ring slot us % NUB)
 
-    // the boxes of plane q (warp 0 arms the barrier with the byte count)
-    auto issue = [&](int64_t q) {
-      const int si = (int)((q - z0 + 1) % NST);
-      double* sb = stages + (size_t)si * Cfg::STAGE;
-      const int zq = (int)q;                     // may be -1 or nz: zero-filled by the TMA unit
-      // CS = 2 (k > 16, up to 34 boxes a plane): the boxes are spread over the warps, one lane
-      // each -- a TMA issue is a uniform-datapath instruction, so one warp's boxes serialise and
-      // would carry the plane's issue latency into the next block barrier (a complete_tx that
-      // lands before the expect_tx leaves the tx-count transiently negative, which the mbarrier
-      // allows).  Narrower steps: warp 0's lanes (measured faster there).
-      constexpr int IW = (CS == 2) ? NW : 1;     // issuing warps
-      if (warp >= IW || (IW > 1 && (lane != 0 || warp >= nload))) return;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (warp == 0 && lane == 0) mbar_expect_tx(bars + si, stage_bytes);
-      for (int j = (IW > 1 ? warp : lane); j < nload; j += (IW > 1 ? NW : 32)) {
-        if (j < (k > 0 ? k : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], bars + si);
-        else if (j == (k > 0 ? k : 0)) tma4(sb + KMAX * NT, a.src_px ? &mpx : &mpy, x0, y0, zq, a.src_slot, bars + si);
-        else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, bars + si);
-      }
-    };
-    auto wait_stage_i = [&](int si) -> const double* {
-      mbar_wait(bars + si, (phase_bits >> si) & 1u);
-      phase_bits ^= (1u << si);
-      return stages + (size_t)si * Cfg::STAGE;
-    };
-    auto wait_stage = [&](int64_t q) -> const double* {
-      const int si = (int)((q - z0 + 1) % NST);
-      mbar_wait(bars + si, (phase_bits >> si) & 1u);
-      phase_bits ^= (1u << si);
-      return stages + (size_t)si * Cfg::STAGE;
-    };
-    // u at this point of the staged plane; vr receives this thread's basis values (the l_j
-    // products reuse them)
-    auto form_u = [&](const double* sb, double (&vr)[KJ]) -> double {
-      const double s0 = sb[KMAX * NT + pt];
-      if (VREG) {
+    // products of this thread's columns with f (f = 0 for points that are not counted)
+    auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, double f, double (&acc)[NACC]) {
+      if (REG) {
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) vr[j] = sb[(j0 + j) * NT + pt];
-      }
-      if (k == 0) return s0;
-      double u = (half == 0) ? wsc * s0 : 0.0;
-#pragma unroll
-      for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], VREG ? vr[j] : sb[(j0 + j) * NT + pt], u);
-      if (CS == 2) {                             // the halves' partial updates, same sum on both
-        const double o = __shfl_xor_sync(0xffffffffu, u, 16);
-        u = (half == 0) ? u + o : o + u;
-      }
-      return u;
-    };
-    auto add_products_r = [&](const double (&vr)[KJ], const double* sb, double f, double (&acc)[NACC]) {
-      if (!VREG) {
-        add_products(sb, f, acc);
-      } else if (REG) {
-#pragma unroll
-        for (int j = 0; j < KJ; ++j) acc[j] = fma(vr[j], f, acc[j]);
+        for (int j = 0; j < KJ; ++j) acc[j] = fma(vcol[(j0 + j) * NT + pt], f, acc[j]);
       } else {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          if (c * 8 >= k) break;                 // uniform
+          if (c * 8 >= k) break;                   // uniform
           double v8[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v8[q] = vr[c * 8 + q] * f;
+          for (int q = 0; q < 8; ++q) v8[q] = vcol[(j0 + c * 8 + q) * NT + pt] * f;
           acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
         }
       }
     };
+    auto acquire = [&](uint32_t g) -> const double* {     // stage g's plane has landed
+      const int si = (int)(g % NST);
+      mbar_wait(full + si, (g / NST) & 1u);
+      return stages + (size_t)si * Cfg::STAGE;
+    };
+    auto release = [&](uint32_t g) {                      // this warp is done with stage g
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + (g % NST))) : "memory");
+    };
+    auto publish_u = [&](uint32_t g, double v, double kv) {  // u (+ kappa) of plane g -> ring slot, signal
+      if (half == 0) {
+        Us[(g % NUB) * NT + pt] = v;
+        if (RV && cell) Ks[(g % NUB) * NT + pt] = kv;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(ubar + (g % NUB))) : "memory");
+    };
+    auto await_u = [&](uint32_t g) -> const double* {    // every warp has published plane g
+      mbar_wait(ubar + (g % NUB), (g / NUB) & 1u);
+      return Us + (g % NUB) * NT;
+    };
 
-    for (int q = 0; q < NST && z0 - 1 + q <= z1; ++q) issue(z0 - 1 + q);
-    // prologue: u(z0-1), u(z0) (+ l-products of plane z0)
-    double vr[KJ];
-    const double* sbm = wait_stage(z0 - 1);
-    double ub = form_u(sbm, vr);
-    if (!(z0 >= 1 && in_grid)) ub = 0.0;
-    double kb = cell ? sbm[(KMAX + 1) * NT + pt] : 0.0;
-    const double* sbc = wait_stage(z0);
-    double uc = form_u(sbc, vr);
-    if (!in_grid) uc = 0.0;
-    double kc = cell ? sbc[(KMAX + 1) * NT + pt] : 0.0;
-    int64_t g = col + plane * z0;                // this point's index at plane p
-    if (emit && k > 0) a.dstx[g] = uc;
-    {
-      const double f = own ? uc : 0.0;
-      if (half == 0) nu = fma(f, f, nu);
-      if (k > 0) add_products_r(vr, sbc, f, accl);
-    }
-    if (half == 0) Us[(z0 & 1) * NT + pt] = uc;
-    __syncthreads();                              // stage z0-1 consumed; Us(z0) visible
-    if (z0 - 1 + NST <= z1) issue(z0 - 1 + NST);
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      int64_t b = tile;
+      const int64_t txi = b % a.tiles_x;
+      b /= a.tiles_x;
+      const int64_t tyi = b % a.tiles_y;
+      const int64_t zci = b / a.tiles_y;
+      // the box's inner start must be 16-byte aligned: x0 even, halo lanes 1 and TX-2
+      const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
+      const int64_t z0 = zci * a.zchunk;
+      const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
+      const int64_t gx = x0 + lx, gy = y0 + ly;
+      const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
+      const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
+      const bool own = interior && in_grid;
+      const bool emit = own && half == 0;        // stores and the u / w~ scalars: one thread per point
+      const int64_t col = in_grid ? gx + st.nx * gy : 0;
+      const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
 
-    int sp_i = 1 % NST;                           // stage of plane p
-    for (int64_t p = z0; p < z1; ++p) {
-      const int bp = (int)(p & 1), bn = bp ^ 1;
-      const int64_t pn = p + 1;
-      // stage p (resident: t-dots, in-plane kappa), stage p+1 (u(p+1))
-      const double* sp = stages + (size_t)sp_i * Cfg::STAGE;
-      double un = 0.0, kt = 0.0;
-      const int sn_i = (sp_i + 1 == NST) ? 0 : sp_i + 1;
-      if (pn <= z1) {                             // plane z1 (halo above the chunk) was loaded too
-        const double* sn = wait_stage_i(sn_i);
-        un = form_u(sn, vr);
+      // u at this point of the staged plane (MGS update of step k, ICWY form)
+      auto form_u = [&](const double* sb) -> double {
+        const double s0 = sb[KMAX * NT + pt];
+        if (k == 0) return s0;
+        double u = (half == 0) ? wsc * s0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], sb[(j0 + j) * NT + pt], u);
+        if (CS == 2) {                           // the halves' partial updates, same sum on both
+          const double o = __shfl_xor_sync(0xffffffffu, u, 16);
+          u = (half == 0) ? u + o : o + u;
+        }
+        return u;
+      };
+      // this thread's basis values of a staged plane -> registers (the plane's l_j products now,
+      // its t_j products one plane later, after which the stage is long released)
+      auto load_vr = [&](const double* sb, double (&vr)[KJ]) {
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) vr[j] = sb[(j0 + j) * NT + pt];
+      };
+      auto add_products_r = [&](const double (&vr)[KJ], double f, double (&acc)[NACC]) {
+        if (REG) {
+#pragma unroll
+          for (int j = 0; j < KJ; ++j) acc[j] = fma(vr[j], f, acc[j]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            if (c * 8 >= k) break;               // uniform
+            double v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v8[q] = vr[c * 8 + q] * f;
+            acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
+          }
+        }
+      };
+      // prologue: u(z0-1) (stage released at once), u(z0) (+ l-products of plane z0)
+      double vr[KJ];
+      const uint32_t gb = gs;                    // stage count of plane z0-1
+      const double* sbm = acquire(gb);
+      double ub = form_u(sbm);
+      double kb = cell ? sbm[(KMAX + 1) * NT + pt] : 0.0;
+      release(gb);
+      if (!(z0 >= 1 && in_grid)) ub = 0.0;
+      int64_t g = col + plane * z0;              // this point's index at plane p
+      const double* sbc = acquire(gb + 1);
+      double uc = form_u(sbc);
+      if (!in_grid) uc = 0.0;
+      double kc = cell ? sbc[(KMAX + 1) * NT + pt] : 0.0;
+      const uint32_t ub0 = us;                   // u-plane count of plane z0
+      publish_u(ub0, uc, kc);
+      if (RV && k > 0) load_vr(sbc, vr);
+      if (RV) release(gb + 1);
+      if (emit && k > 0) a.dstx[g] = uc;
+      {
+        const double f = own ? uc : 0.0;
+        if (half == 0) nu = fma(f, f, nu);
+        if (k > 0) {
+          if (RV) add_products_r(vr, f, accl);
+          else add_products(sbc, f, accl);
+        }
+      }
+
+      for (int64_t p = z0; p < z1; ++p) {
+        const uint32_t gp = gb + 1 + (uint32_t)(p - z0);   // stage of plane p
+        const uint32_t up = ub0 + (uint32_t)(p - z0);      // u plane of p
+        const int64_t pn = p + 1;
+        // u(p+1) from stage p+1 (plane z1, the halo above the chunk, is staged too)
+        const double* sn = acquire(gp + 1);
+        double un = form_u(sn);
         if (!(pn < st.nz && in_grid)) un = 0.0;
-        kt = cell ? sn[(KMAX + 1) * NT + pt] : 0.0;
+        const double kt = cell ? sn[(KMAX + 1) * NT + pt] : 0.0;
+        if (pn < z1) publish_u(up + 1, un, kt);  // the stencil of plane p+1 needs them
+        // w~ = A u at plane p (both halves compute it; the first one stores it)
+        const double* Up = await_u(up);
+        double w = 0.0;
+        if (own) {
+          const double c0 = uc;
+          double acc = 0.0;
+          // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
+          // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
+          const double* Kp = RV ? Ks + (up % NUB) * NT : stages + (size_t)(gp % NST) * Cfg::STAGE + (KMAX + 1) * NT;
+          auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
+            const double kf = cell ? hsv * (kc + (nin ? fn : kc)) : s;
+            acc = fma(kf, c0 - xn, acc);
+          };
+          const double xw = Up[pt - 1], xe = Up[pt + 1];
+          face(xw, cell ? Kp[pt - 1] : 0.0, nb_w, st.s[0], hsx);
+          face(xe, cell ? Kp[pt + 1] : 0.0, nb_e, st.s[0], hsx);
+          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
+          if (HASY) {
+            const double xs_ = Up[pt - TX], xn_ = Up[pt + TX];
+            face(xs_, cell ? Kp[pt - TX] : 0.0, nb_s, st.s[1], hsy);
+            face(xn_, cell ? Kp[pt + TX] : 0.0, nb_n, st.s[1], hsy);
+            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
+          }
+          if (st.nz > 1) {
+            const bool inb = p > 0, int_ = p + 1 < st.nz;
+            face(ub, kb, inb, st.s[2], hsz);
+            face(un, kt, int_, st.s[2], hsz);
+            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub, acc);
+          }
+          w = c0 + acc;
+          if (half == 0) {
+            a.dsty[g] = w;
+            tu = fma(c0, w, tu);
+          }
+        }
+        // t_j = V_j(p)' w~(p); w = 0 off emitted points
+        if (RV) {
+          if (k > 0) add_products_r(vr, w, acct);
+        } else {
+          if (k > 0) add_products(stages + (size_t)(gp % NST) * Cfg::STAGE, w, acct);
+          release(gp);                            // stage p done
+        }
         if (pn < z1) {
+          if (RV && k > 0) load_vr(sn, vr);      // V(p+1): its l_j now, its t_j next plane
           if (emit && k > 0) a.dstx[g + plane] = un;
           const double f = own ? un : 0.0;
           if (half == 0) nu = fma(f, f, nu);
-          if (k > 0) add_products_r(vr, sn, f, accl);
+          if (k > 0) {
+            if (RV) add_products_r(vr, f, accl);
+            else add_products(sn, f, accl);
+          }
         }
+        if (RV || pn == z1) release(gp + 1);      // stage p+1 done (else: after its t_j)
+        ub = uc; uc = un;
+        kb = kc; kc = kt;
+        g += plane;
       }
-      // w~ = A u at plane p (both halves compute it; the first one stores it)
-      double w = 0.0;
-      if (own) {
-        const double c0 = uc;
-        double acc = 0.0;
-        const double* Up = Us + bp * NT;
-        const double* Kp = sp + (KMAX + 1) * NT;
-        // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
-        // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
-        auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
-          const double kf = cell ? hsv * (kc + (nin ? fn : kc)) : s;
-          acc = fma(kf, c0 - xn, acc);
-        };
-        const double xw = Up[pt - 1], xe = Up[pt + 1];
-        face(xw, cell ? Kp[pt - 1] : 0.0, nb_w, st.s[0], hsx);
-        face(xe, cell ? Kp[pt + 1] : 0.0, nb_e, st.s[0], hsx);
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
-        if (HASY) {
-          const double xs_ = Up[pt - TX], xn_ = Up[pt + TX];
-          face(xs_, cell ? Kp[pt - TX] : 0.0, nb_s, st.s[1], hsy);
-          face(xn_, cell ? Kp[pt + TX] : 0.0, nb_n, st.s[1], hsy);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
-        }
-        if (st.nz > 1) {
-          const bool inb = p > 0, int_ = p + 1 < st.nz;
-          face(ub, kb, inb, st.s[2], hsz);
-          face(un, kt, int_, st.s[2], hsz);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub, acc);
-        }
-        w = c0 + acc;
-        if (half == 0) {
-          a.dsty[g] = w;
-          tu = fma(c0, w, tu);
-        }
-      }
-      if (k > 0) add_products(sp, w, acct);       // t_j = V_j(p)' w~(p); w = 0 off emitted points
-      if (half == 0) Us[bn * NT + pt] = un;
-      __syncthreads();                            // stage p consumed; Us(p+1) visible
-      if (p + NST <= z1) issue(p + NST);
-      if (psync) {                                // at most one plane apart within the cluster
-        if (p > z0) cluster_wait();
-        cluster_arrive();
-      }
-      ub = uc; uc = un;
-      kb = kc; kc = kt;
-      g += plane;
-      if (++sp_i == NST) sp_i = 0;
+      gs = gb + (uint32_t)(z1 - z0 + 2);          // planes z0-1 .. z1
+      us = ub0 + (uint32_t)(z1 - z0);             // u planes z0 .. z1-1
     }
-    // drain: every issued stage has been waited on (planes z0-1 .. z1), so the barriers'
-    // parities stay in step for the next tile
-    if (psync) cluster_wait();
   }
 
   // reduce the accumulators across the points of the warp (value -> slot j0 + j)
@@ -574,7 +596,7 @@ struct MapCache {
 
 template <int KIND, int TX, int TY, int KMAX, int CS>
 int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
-  using Cfg = FCfg<TX, TY, KMAX>;
+  using Cfg = FCfg<TX, TY, KMAX, CS>;
   static MapCache mc;
   const Stencil& st = a.st;
   if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != st.field || mc.nx != st.nx ||
@@ -604,44 +626,13 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   a.zchunk = (int)zc;
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
   if (!mc.ok) return g_map_err ? g_map_err : -1;
-  // cluster shape "CXxCY" (tuning knob; default none)
-  int clx = 1, cly = 1;
-  const char* e = getenv("PSP_FUSED_CL");
-  if (e && sscanf(e, "%dx%d", &clx, &cly) != 2) clx = cly = 1;
-  if (clx < 1 || cly < 1 || clx * cly > 8) clx = cly = 1;
-  const int psync = getenv("PSP_FUSED_PSYNC") ? atoi(getenv("PSP_FUSED_PSYNC")) : 1;
-  a.clx = clx;
-  a.cly = TY > 1 ? cly : 1;
-  a.psync = psync;
-  const int ncl = a.clx * a.cly;
-  a.ctiles_x = (a.tiles_x + a.clx - 1) / a.clx;
-  a.ctiles_y = (a.tiles_y + a.cly - 1) / a.cly;
-  a.nits = a.ctiles_x * a.ctiles_y * ((st.nz + zc - 1) / zc);
   auto kern = fused_tma_kernel<KIND, TX, TY, KMAX, CS>;
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(TX, TY * CS);
+  cfg.blockDim = dim3(TX * TY * CS + 32);         // compute warps + the TMA producer warp
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
   int64_t grid = 148;                              // one resident block per SM (persistent)
-  if (ncl > 1) {
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)ncl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    static int maxcl[9] = {0};
-    if (maxcl[ncl] == 0) {
-      cfg.gridDim = dim3((unsigned)(ncl * 148));
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) nc = 148 / ncl;
-      maxcl[ncl] = nc;
-      if (getenv("PSP_FUSED_VERBOSE")) fprintf(stderr, "fused: %d active clusters of %d\n", nc, ncl);
-    }
-    grid = (int64_t)maxcl[ncl] * ncl;
-  }
-  if (grid / ncl > a.nits) grid = a.nits * ncl;
+  if (grid > a.ntiles) grid = a.ntiles;
   cfg.gridDim = dim3((unsigned)grid);
   if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, a) != cudaSuccess) return -2;
   return 0;
@@ -653,16 +644,16 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     // stage = (KMAX + 2) boxes: the narrowest instantiation that holds k columns keeps the most
     // planes in flight (measured at 512^3: k <= 4 1.9 vs 2.3 ms, k = 9..12 3.5-3.8 vs 3.8-4.1 ms).
     // 32 x 8 tiles for k <= 16 or 16 x 8 tiles for k > 16 were slower (more halo points per tile).
-    if (a.k <= 4) return launch_t<KIND, 32, 16, 4, 1>(a, rpx, rpy, s);
-    if (a.k <= 8) return launch_t<KIND, 32, 16, 8, 1>(a, rpx, rpy, s);
-    if (a.k <= 12) return launch_t<KIND, 32, 16, 12, 1>(a, rpx, rpy, s);
-    if (a.k <= 16) return launch_t<KIND, 32, 16, 16, 1>(a, rpx, rpy, s);
-    if (a.k <= 24) return launch_t<KIND, 32, 8, 24, 2>(a, rpx, rpy, s);
-    return launch_t<KIND, 32, 8, 32, 2>(a, rpx, rpy, s);
+    if (a.k <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
+    if (a.k <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
+    if (a.k <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
+    if (a.k <= 16) return launch_t<KIND, 32, 15, 16, 1>(a, rpx, rpy, s);
+    if (a.k <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
+    return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, s);
   }
   if (a.k <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, s);
   if (a.k <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, s);
-  return launch_t<KIND, 256, 1, 32, 2>(a, rpx, rpy, s);
+  return launch_t<KIND, 224, 1, 32, 2>(a, rpx, rpy, s);
 }
 
 // 3-D view of the local grid for the fused pass: the march axis is the slowest one

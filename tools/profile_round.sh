@@ -11,6 +11,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "launches rc $?"
 PCMD="python tools/prof_step.py 512 1 1 16"
 $PCMD > gpurun_out/prof_step.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"fused_tma|icwy_dots|icwy_update|march3|mrep_tma" \
+ncu --set full --clock-control none --import-source on -k regex:"fused_tma|icwy_dots|icwy_update|march4|mrep_tma|tile_map|factor_pass" \
     -s 60 -c 8 -o gpurun_out/prof_full $PCMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc $?"
