@@ -31,7 +31,8 @@
 namespace psp {
 namespace {
 
-constexpr int kChunk = 128;      // factor: rows per thread
+constexpr int kChunk = 512;      // factor: rows per thread
+constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
 constexpr int STPB = 256;        // solve: threads per block
 constexpr int SR = 8;            // solve: rows per thread
 constexpr int STILE = STPB * SR; // solve: rows per tile
@@ -48,7 +49,8 @@ template <int D, bool WRITE>
 __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, double* __restrict__ lu,
                                    const double* __restrict__ st_in, double* __restrict__ st_out,
                                    int first_pass, int* __restrict__ changed, int* __restrict__ bad,
-                                   const double* __restrict__ prev, int has_prev, int has_next, int vec) {
+                                   const double* __restrict__ prev, int has_prev, int has_next, int vec,
+                                   int warm, double* __restrict__ st_start) {
   // has_prev / has_next (multi-rank): the global matrix continues before row 0 / after row n-1
   // of this block (rows of rank-1 / rank+1), so the band entries reaching there are real
   constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
@@ -80,8 +82,19 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
       for (int e = 0; e <= D; ++e) Uw[q][e] = s[q * (D + 1) + e];
   }
   const bool at_start = !from_prev && ((c == 0) || first_pass);
+  // warm start (first pass, warm > 0): the walk begins `warm` rows before the chunk from the
+  // zero state; for a dominant N the state has converged bitwise by the chunk start, which the
+  // caller verifies against the previous chunk's end state (st_start)
+  const int64_t rs = (warm > 0 && first_pass && c > 0) ? (r0 - warm > 0 ? r0 - warm : 0) : r0;
   int isbad = 0;
-  for (int64_t i0 = r0; i0 < r1; i0 += 4) {
+  for (int64_t i0 = rs; i0 < r1; i0 += 4) {
+    const bool live = i0 >= r0;                 // warm-up rows: state only
+    if (warm > 0 && first_pass && c > 0 && i0 == r0) {
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+#pragma unroll
+        for (int e = 0; e <= D; ++e) st_start[c * W + q * (D + 1) + e] = Uw[q][e];
+    }
     const int nr = (r1 - i0) < 4 ? (int)(r1 - i0) : 4;
     double bb[NB][4];
     if (vec && nr == 4) {
@@ -97,7 +110,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
     }
-    double out[NB][4];
+    // results overwrite the consumed band values of their row (bb doubles as the output tile)
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
       if (rr >= nr) break;
@@ -113,7 +126,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
       };
       auto row_exists = [&](int q) -> bool {
         const int64_t k = i - D + q;
-        return (k >= 0 || has_prev) && !(at_start && k < r0);
+        return (k >= 0 || has_prev) && !(at_start && k < rs);
       };
 #pragma unroll
       for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
@@ -135,16 +148,16 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
           if (row_exists(p) && (i - D + p) >= j - D) sum -= Lr[p] * Uk(p, j);
         Ur[e] = sum;
       }
-      if (!(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+      if (live && !(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
 #pragma unroll
       for (int q = 0; q < D; ++q) {
-        if (!(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
-        out[q][rr] = Lr[q];
+        if (live && !(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
+        bb[q][rr] = Lr[q];
       }
 #pragma unroll
       for (int e = 0; e <= D; ++e) {
-        if (!(fabs(Ur[e]) <= 1e100)) isbad = 1;
-        out[D + e][rr] = Ur[e];
+        if (live && !(fabs(Ur[e]) <= 1e100)) isbad = 1;
+        bb[D + e][rr] = Ur[e];
       }
       // shift the window
 #pragma unroll
@@ -154,19 +167,19 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
       for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
     }
-    if (WRITE) {
+    if (WRITE && live) {
       if (vec && nr == 4) {
 #pragma unroll
         for (int o = 0; o < NB; ++o) {
-          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0) = make_double2(out[o][0], out[o][1]);
-          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0 + 2) = make_double2(out[o][2], out[o][3]);
+          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0) = make_double2(bb[o][0], bb[o][1]);
+          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0 + 2) = make_double2(bb[o][2], bb[o][3]);
         }
       } else {
 #pragma unroll
         for (int o = 0; o < NB; ++o)
 #pragma unroll
           for (int rr = 0; rr < 4; ++rr)
-            if (rr < nr) lu[(int64_t)o * n + i0 + rr] = out[o][rr];
+            if (rr < nr) lu[(int64_t)o * n + i0 + rr] = bb[o][rr];
       }
     }
   }
@@ -657,20 +670,31 @@ __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __res
   }
 }
 
+// Warm-start check: chunk c's start state (from its warm-up rows) against chunk c-1's end state,
+// bitwise; any difference sends the factorisation to the exact fixed-point passes.
+__global__ void factor_verify_kernel(const double* __restrict__ st_start, const double* __restrict__ st_end,
+                                     int64_t nchunks, int W, int* __restrict__ changed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (nchunks - 1) * W) return;
+  const int64_t c = i / W + 1, e = i % W;
+  if (__double_as_longlong(st_start[c * W + e]) != __double_as_longlong(st_end[(c - 1) * W + e]))
+    atomicAdd(changed, 1);
+}
+
 template <int D>
 void factor_launch(const double* bands, int64_t n, double* lu, const double* a, double* b,
                    int first, int* changed, int* bad, const double* prev, int has_prev, int has_next,
-                   cudaStream_t s, bool write) {
+                   cudaStream_t s, bool write, int warm = 0, double* st_start = nullptr) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int tpb = 64;
   const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
   if (write)
     factor_pass_kernel<D, true><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
-                                                     has_next, vec);
+                                                     has_next, vec, warm, st_start);
   else
     factor_pass_kernel<D, false><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
-                                                      has_next, vec);
+                                                      has_next, vec, warm, st_start);
 }
 
 template <bool FWD, int D>
@@ -832,6 +856,33 @@ int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScrat
   double hd[2] = {0.0, 0.0};
   int p = 0;
   bool write = false;   // state-only passes until no chunk state changes, then one LU pass
+  if (!multi && nchunks > 1) {
+    // one LU-writing pass from warm-started chunk states (the solve's intermediate vector is
+    // free during the factorisation and holds the start states), then the bitwise check; only
+    // if some chunk's state had not converged do the exact fixed-point passes follow
+    double* S0 = sc.y;
+    cudaMemsetAsync(sc.changed, 0, 2 * sizeof(int), s);
+    switch (d) {
+      case 1: factor_launch<1>(bands, n, lu, A, B, 1, sc.changed, sc.changed + 1, nullptr, 0, 0, s, true, kWarm, S0); break;
+      case 2: factor_launch<2>(bands, n, lu, A, B, 1, sc.changed, sc.changed + 1, nullptr, 0, 0, s, true, kWarm, S0); break;
+      case 3: factor_launch<3>(bands, n, lu, A, B, 1, sc.changed, sc.changed + 1, nullptr, 0, 0, s, true, kWarm, S0); break;
+      default: factor_launch<4>(bands, n, lu, A, B, 1, sc.changed, sc.changed + 1, nullptr, 0, 0, s, true, kWarm, S0); break;
+    }
+    cudaMemsetAsync(sc.changed, 0, sizeof(int), s);   // the pass counted every chunk as changed
+    const int64_t nv = (nchunks - 1) * W;
+    factor_verify_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, s>>>(S0, B, nchunks, W, sc.changed);
+    if (launches) *launches += 2;
+    p = 1;
+    cudaMemcpyAsync(h, sc.changed, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double* tmp = A;
+    A = B;
+    B = tmp;
+    if (h[0] == 0) {
+      if (passes) *passes = p;
+      return h[1] ? PSP_E_SINGULAR : PSP_OK;
+    }
+  }
   for (;;) {
     cudaMemsetAsync(sc.changed, 0, 2 * sizeof(int), s);
     const double* prev = (multi && comm->rank > 0 && p > 0) ? M.prev : nullptr;

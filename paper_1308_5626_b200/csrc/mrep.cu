@@ -22,7 +22,7 @@
 #include "internal.h"
 
 #ifndef PSP_MREP_NST
-#define PSP_MREP_NST 4    // TMA stages of 4 probe columns each (8 or 12 measured slower: fewer CTAs per SM)
+#define PSP_MREP_NST 3    // TMA stages of PSP_MREP_TCB probe columns each
 #endif
 #ifndef PSP_MREP_MINB
 #define PSP_MREP_MINB 2   // resident blocks per SM of the TMA MREP kernel
@@ -339,7 +339,10 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
 // alignment parity (sx, sy; checked on the host, else the generic kernel runs everything).
 // ------------------------------------------------------------------------------------------
 constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kernel
-constexpr int TCB = 4;         // probe columns per stage
+#ifndef PSP_MREP_TCB
+#define PSP_MREP_TCB 8    // probe columns per stage (measured: 8 x 3 stages beats 4 x 4 at d = 3)
+#endif
+constexpr int TCB = PSP_MREP_TCB;   // probe columns per stage
 constexpr int TNST = PSP_MREP_NST;   // stages
 
 template <int D>
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
   const bool unit = s_unit != 0;                   // every recorded probe scale is 1
 
   const int lx = cols.sx ? LX1 : LX, ly = cols.sy ? LY1 : LY;
-  const int nch = m / TCB;                         // m % TCB == 0 (host check)
+  const int nch = (m + TCB - 1) / TCB;             // the last chunk may be partial
   // 32-bit load counters with incremental (tile, chunk, stage) indices: a 64-bit division in
   // the loop is an out-of-line call whose ABI would push the packed Gram to local memory
   const int my_tiles = (int)((ntile - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -433,10 +436,12 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
     double* st = stages + (size_t)is_stg * Cfg::STAGE;
     const int64_t s0 = R0 + tile * E - D;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bars + is_stg, 8u * (unsigned)(TCB * (lx + ly)));
+    const int ncols = (m - is_ch * TCB) < TCB ? (m - is_ch * TCB) : TCB;
+    mbar_expect_tx(bars + is_stg, 8u * (unsigned)(ncols * (lx + ly)));
 #pragma unroll
     for (int cc = 0; cc < TCB; ++cc) {
       const int c = is_ch * TCB + cc;
+      if (c >= m) break;
       const double* bxp = cols.px + (int64_t)cols.slot[c] * cols.ld;
       const double* byp = cols.py + (int64_t)cols.slot[c] * cols.ld;
       bulk_g2s(st + cc * Cfg::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + is_stg);
@@ -462,9 +467,11 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
     mbar_wait(bars + stg, (phase >> stg) & 1u);
     phase ^= 1u << stg;
     const double* st = stages + (size_t)stg * Cfg::STAGE;
+    const int ccn = (m - ch * TCB) < TCB ? (m - ch * TCB) : TCB;   // columns in this chunk
     if (unit) {
 #pragma unroll
       for (int cc = 0; cc < TCB; ++cc) {
+        if (cc >= ccn) break;                      // uniform
         const double* xr = st + cc * Cfg::PXW + xo;  // xr[k] = P_x(r - D + k), r = s0 + t
         double xw[3 * D + 1];
 #pragma unroll
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
       const int c0 = ch * TCB;
 #pragma unroll
       for (int cc = 0; cc < TCB; ++cc) {
+        if (cc >= ccn) break;                      // uniform
         const double sc = scs[c0 + cc];
         const double* xr = st + cc * Cfg::PXW + xo;
         double xw[3 * D + 1];
@@ -660,7 +668,7 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
     if (sxp < 0) { sxp = px_par; syp = py_par; }
     uniform = uniform && px_par == sxp && py_par == syp && (ax & 7) == 0 && (ay & 7) == 0;
   }
-  if (ntile < 1 || m > kMaxM || m % TCB != 0 || !uniform) ntile = 0;
+  if (ntile < 1 || m > kMaxM || !uniform) ntile = 0;
   const int64_t R1 = ntile > 0 ? R0 + ntile * Et : n;
   const int64_t a0 = 0, a1 = ntile > 0 ? R0 : n, b0 = R1, b1 = ntile > 0 ? n : n;
   {

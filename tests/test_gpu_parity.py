@@ -169,7 +169,7 @@ def compare_mrep(g, r, d, n, px, max_excluded_frac=1e-4):
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4])
-@pytest.mark.parametrize("n,m", [(5003, 16), (2000, 32), (700, 64)])
+@pytest.mark.parametrize("n,m", [(5003, 16), (2000, 32), (700, 64), (4001, 13), (3001, 21)])   # m % 8 != 0: partial TMA chunk
 def test_mrep_parity_c5(torch, P, orc, d, n, m):
     g5 = inputs.c5_numpy(n, m, d, seed=7)
     r = orc.mrep(g5["px"], g5["py"], d)
