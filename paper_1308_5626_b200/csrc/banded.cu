@@ -21,6 +21,9 @@
 // descriptors) delivers the exact incoming state; the rows are then recomputed from that
 // state and stored.  Algorithmic bytes: forward 8(d+2), backward 8(d+3) per row.
 #include <math.h>
+#include <stdint.h>
+
+#include <type_traits>
 
 #include "internal.h"
 
@@ -86,6 +89,11 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   // zero state; for a dominant N the state has converged bitwise by the chunk start, which the
   // caller verifies against the previous chunk's end state (st_start)
   const int64_t rs = (warm > 0 && first_pass && c > 0) ? (r0 - warm > 0 ? r0 - warm : 0) : r0;
+  // first row of the walk's existing window rows: rows below lo do not exist
+  const int64_t lo = at_start ? rs : (has_prev ? INT64_MIN / 2 : 0);
+  double Ri[D];       // 1 / U(k,k) of the window rows (unused for rows that do not exist)
+#pragma unroll
+  for (int q = 0; q < D; ++q) Ri[q] = 1.0 / Uw[q][0];
   int isbad = 0;
   for (int64_t i0 = rs; i0 < r1; i0 += 4) {
     const bool live = i0 >= r0;                 // warm-up rows: state only
@@ -110,63 +118,69 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
     }
-    // results overwrite the consumed band values of their row (bb doubles as the output tile)
+    // results overwrite the consumed band values of their row (bb doubles as the output tile).
+    // Groups whose rows all have a full window (no matrix / chunk start within D rows, no matrix
+    // end within D rows) take the check-free copy of the row step.
+    const bool full = (i0 - D >= lo) && (i0 + 3 + D < n || has_next);
+    auto step = [&](auto chk) {
+      constexpr bool C = decltype(chk)::value;
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      if (rr >= nr) break;
-      const int64_t i = i0 + rr;
-      double Lr[D];       // L(i, i-D+q), q = 0..D-1
-      double Ur[D + 1];   // U(i, i+e)
-      // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D.  Rows before the matrix
-      // start (or before the chunk start in a first-pass guess) do not exist.
-      auto Uk = [&](int q, int64_t j) -> double {
-        const int64_t k = i - D + q;
-        const int64_t e = j - k;
-        return (e >= 0 && e <= D) ? Uw[q][e] : 0.0;
-      };
-      auto row_exists = [&](int q) -> bool {
-        const int64_t k = i - D + q;
-        return (k >= 0 || has_prev) && !(at_start && k < rs);
-      };
+      for (int rr = 0; rr < 4; ++rr) {
+        if (rr >= nr) break;
+        const int64_t i = i0 + rr;
+        double Lr[D];       // L(i, i-D+q), q = 0..D-1
+        double Ur[D + 1];   // U(i, i+e)
+        // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D (compile-time after
+        // unrolling).  Rows before the matrix start (or before the walk start of a zero-state
+        // walk) do not exist.
+        auto row_exists = [&](int q) -> bool {
+          if (!C) return true;
+          const int64_t k = i - D + q;
+          return (k >= 0 || has_prev) && !(at_start && k < rs);
+        };
 #pragma unroll
-      for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
-        const int64_t j = i - D + q;
-        if (!row_exists(q)) { Lr[q] = 0.0; continue; }
-        double sum = bb[q][rr];                 // N(i,j), band o = j-i+D = q
+        for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
+          if (!row_exists(q)) { Lr[q] = 0.0; continue; }
+          double sum = bb[q][rr];                 // N(i,j), band o = j-i+D = q
 #pragma unroll
-        for (int p = 0; p < q; ++p)           // k = i-D+p < j, k >= j-D holds (p >= 0 > q-D)
-          if (row_exists(p)) sum -= Lr[p] * Uk(p, j);
-        Lr[q] = sum / Uw[q][0];               // U(j,j)
+          for (int p = 0; p < q; ++p)           // U(k, j), k = i-D+p: window entry e = q - p
+            if (row_exists(p)) sum -= Lr[p] * Uw[p][q - p];
+          Lr[q] = sum * Ri[q];                  // / U(j,j), by its reciprocal
+        }
+#pragma unroll
+        for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
+          if (C && i + e >= n && !has_next) { Ur[e] = 0.0; continue; }
+          double sum = bb[D + e][rr];
+#pragma unroll
+          for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]: window entry D - p + e
+            if (p >= e && row_exists(p)) sum -= Lr[p] * Uw[p][D - p + e];
+          Ur[e] = sum;
+        }
+        if (live && !(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          if (live && !(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
+          bb[q][rr] = Lr[q];
+        }
+#pragma unroll
+        for (int e = 0; e <= D; ++e) {
+          if (live && !(fabs(Ur[e]) <= 1e100)) isbad = 1;
+          bb[D + e][rr] = Ur[e];
+        }
+        // shift the window (and the pivot reciprocals: one division per row)
+#pragma unroll
+        for (int q = 0; q < D - 1; ++q) {
+#pragma unroll
+          for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
+          Ri[q] = Ri[q + 1];
+        }
+#pragma unroll
+        for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
+        Ri[D - 1] = 1.0 / Ur[0];
       }
-#pragma unroll
-      for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
-        const int64_t j = i + e;
-        if (j >= n && !has_next) { Ur[e] = 0.0; continue; }
-        double sum = bb[D + e][rr];
-#pragma unroll
-        for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]
-          if (row_exists(p) && (i - D + p) >= j - D) sum -= Lr[p] * Uk(p, j);
-        Ur[e] = sum;
-      }
-      if (live && !(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
-#pragma unroll
-      for (int q = 0; q < D; ++q) {
-        if (live && !(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
-        bb[q][rr] = Lr[q];
-      }
-#pragma unroll
-      for (int e = 0; e <= D; ++e) {
-        if (live && !(fabs(Ur[e]) <= 1e100)) isbad = 1;
-        bb[D + e][rr] = Ur[e];
-      }
-      // shift the window
-#pragma unroll
-      for (int q = 0; q < D - 1; ++q)
-#pragma unroll
-        for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
-#pragma unroll
-      for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
-    }
+    };
+    if (full) step(std::false_type{});
+    else step(std::true_type{});
     if (WRITE && live) {
       if (vec && nr == 4) {
 #pragma unroll
