@@ -400,6 +400,12 @@ def main():
             "converged": all(r["converged"] for r in reps),
             "true_resid_over_eps": max(r["final_resid_true"] / r["eps"] for r in reps),
             "mrep_rows_per_s": (n * args.steps / (mrep_ms / 1e3)) if mrep_ms else None,
+            # SURVEY 8(d)'s reading: t_solve only (the MREP fit, gate and factor timed apart);
+            # `value` above keeps them inside the step
+            "solve_only": ({"value": n * sum(r["iterations"] for r in reps) / (solve_ms / 1e3),
+                            "unit": UNIT, "ms_per_step": solve_ms / args.steps,
+                            "definition": "n x sum(iterations) / sum(t_solve), CUDA events (opts.timing)"}
+                           if solve_ms else None),
             "kernels": kernel_table,
             "roofline": roofline,
             "gpu_launches": int(launches),
