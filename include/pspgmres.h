@@ -94,6 +94,11 @@ typedef struct {
   int32_t fused_kmin;              /* first step run as a fused pass; default 2               */
   int32_t fused_kmax;              /* last step run as a fused pass; default 16 (wider steps  */
                                    /* hold more basis tiles than shared memory stages well)   */
+  int32_t fused_split_cols;        /* steps k > fused_kmax: the newest fused_split_cols       */
+                                   /* (1..16) basis columns through the fused pass, the older */
+                                   /* k - fused_split_cols through an update pass and a dots  */
+                                   /* pass (DESIGN.md s.6); 0 = three separate passes;        */
+                                   /* default 12                                              */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */

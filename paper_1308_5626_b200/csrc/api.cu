@@ -269,6 +269,7 @@ void psp_default_opts(psp_opts* o) {
   o->fused = 1;
   o->fused_kmin = 2;
   o->fused_kmax = 16;
+  o->fused_split_cols = 12;
 }
 
 const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }
@@ -662,6 +663,43 @@ static bool fused_pass(const psp_ctx* c, int k) {
   return k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, c->nA);
 }
 
+static double fused_bytes(const psp_ctx* c, int k);
+
+// split-column step: a step wider than the fused band whose newest fused_split_cols basis columns
+// go through the fused pass and the older J = k - fused_split_cols through an update and a dots
+// pass (both stream those columns once each, with no stencil halo)
+static bool hyb_pass(const psp_ctx* c, int k) {
+  const int kb = c->opts.fused_split_cols;
+  return kb > 0 && kb <= 16 && k > c->opts.fused_kmax && k - kb >= 1 && fused_supported(c->st, c->nA);
+}
+
+// Step k as three passes over the ring: [A] u' = alpha_k w~_k - sum_{j<J} h_j alpha_j V(:,j) into
+// the scratch vector W (l.13-16, the first J MGS terms); [B] the fused pass over the columns
+// [J, k): u = u' - sum_{J<=j<k} h_j alpha_j V(:,j) -> V(:,k+1) (the next slot), w~_{k+1} = A u
+// (l.11-12) and their inner products with those columns, u and w~; [C] the inner products of
+// V(:,0..J-1) with w~_{k+1} and u, then H(k+1,k), Givens, alpha_{k+1} (l.17-32) and step k+1's
+// MGS coefficients (R11) in its last block.
+static psp_status ring_hyb_step(psp_ctx* c, int k, int src_slot, int dst) {
+  const int64_t n = c->n;
+  const double dn = (double)n;
+  const int kb = c->opts.fused_split_cols, J = k - kb;
+  int h = kt_begin(c);
+  launch_icwy_update(basis(c), py_col(c, src_slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds, c->rc,
+                     c->stream, J);
+  kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (J + 2) * dn);
+  h = kt_begin(c);
+  const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, src_slot, 0,
+                              px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream, J, c->W);
+  if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+  kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, kb));
+  h = kt_begin(c);
+  launch_icwy_dots_hyb(basis(c), py_col(c, dst), px_col(c, dst), J, k, c->nA, n, c->ds, c->rc, c->stream);
+  kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (J + 2) * dn);
+  cudaMemcpyAsync(c->slot_scale + dst, c->ds.alpha + k, sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  c->launches += 3;
+  return PSP_OK;
+}
+
 // The ring-resident step without the fused pass (k = 0: the cycle start, V(:,1) already in its
 // slot): [k >= 1: V(:,k+1) = alpha_k w~_k - sum_j h_j alpha_j V(:,j) into the next slot, H(k+1,k),
 // Givens, alpha_{k+1} (l.13-32)]; w~_{k+1} = A V(:,k+1) unnormalised into the slot's P_y
@@ -765,6 +803,8 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
         if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
         kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
         c->launches += 1;
+      } else if (hyb_pass(c, k)) {
+        PSP_TRY(ring_hyb_step(c, k, slot, dst));
       } else {
         PSP_TRY(ring_split_step(c, k, slot, dst));
       }

@@ -52,7 +52,10 @@ struct FusedArgs {
   int nA;
   int vs1, cap;        // V(:,j+1) = ring P_x slot (vs1 + j) % cap
   int src_slot;        // w~_k: ring P_y slot (k = 0: V_1 = ring P_x slot)
-  int src_px;          // 1: src lives in the P_x ring
+  int src_px;          // 1: src lives in the P_x ring; 2: src is a plain vector (map msrc)
+  int jb;              // first basis column of this pass (split-column step: the columns [jb, k))
+  int hyb;             // 1: split-column step -- src is u' (scale 1), sums go to ds.rpart
+  const double* src_vec;  // src_px = 2
   double* dstx;        // u -> ring P_x slot of step k+1 (unused when k = 0)
   double* dsty;        // w~ -> ring P_y slot of step k+1
   double* slot_scale;  // per-slot probe scale
@@ -168,7 +171,8 @@ __device__ __forceinline__ double butterfly8_half(double (&v)[8], int lane) {
 template <int KIND, int TX, int TY, int KMAX, int CS>
 __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap mpx, const __grid_constant__ CUtensorMap mpy,
-                     const __grid_constant__ CUtensorMap mkap, FusedArgs a) {
+                     const __grid_constant__ CUtensorMap mkap, const __grid_constant__ CUtensorMap msrc,
+                     FusedArgs a) {
   using Cfg = FCfg<TX, TY, KMAX, CS>;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
   constexpr bool HASY = TY > 1;
@@ -205,15 +209,16 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
   const int lx = pt % TX, ly = pt / TX;
   const int j0 = half * KJ;
   const int k = a.k;
+  const int kc = k - a.jb;                       // basis columns of this pass
   const int ld = a.nA + 1;
   if (t < KMAX) {
-    hs[t] = (t < k) ? a.ds.H[(int64_t)(k - 1) * ld + t] * a.ds.alpha[t] : 0.0;
-    vslot[t] = (a.vs1 + t) % a.cap;
+    hs[t] = (t < kc) ? a.ds.H[(int64_t)(k - 1) * ld + a.jb + t] * a.ds.alpha[a.jb + t] : 0.0;
+    vslot[t] = (a.vs1 + a.jb + t) % a.cap;
   }
   // columns j >= k are never loaded: zero them once in every stage (coefficient 0, product 0)
   if (!producer && half == 0)
     for (int s = 0; s < NST; ++s)
-      for (int j = k; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + pt] = 0.0;
+      for (int j = kc; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + pt] = 0.0;
   if (t == 0) {
     for (int q = 0; q < NST; ++q) {
       mbar_init(full + q, 1);
@@ -225,10 +230,10 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mpy)) : "memory");
     if (cell) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mkap)) : "memory");
   }
-  const double wsc = (k >= 1) ? a.ds.alpha[k - 1] : 1.0;
+  const double wsc = (k >= 1 && !a.hyb) ? a.ds.alpha[k - 1] : 1.0;
   __syncthreads();
 
-  const int nload = (k == 0 ? 0 : k) + 1 + (cell ? 1 : 0);
+  const int nload = (k == 0 ? 0 : kc) + 1 + (cell ? 1 : 0);
   const unsigned stage_bytes = (unsigned)(nload * NT * 8);
 
   double accl[NACC], acct[NACC];
@@ -257,8 +262,9 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         if (lane == 0) mbar_expect_tx(full + si, stage_bytes);
         __syncwarp();
         for (int j = lane; j < nload; j += 32) {
-          if (j < (k > 0 ? k : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], full + si);
-          else if (j == (k > 0 ? k : 0)) tma4(sb + KMAX * NT, a.src_px ? &mpx : &mpy, x0, y0, zq, a.src_slot, full + si);
+          if (j < (k > 0 ? kc : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], full + si);
+          else if (j == (k > 0 ? kc : 0))
+            tma4(sb + KMAX * NT, a.src_px == 2 ? &msrc : (a.src_px ? &mpx : &mpy), x0, y0, zq, a.src_slot, full + si);
           else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, full + si);
         }
       }
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       } else {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          if (c * 8 >= k) break;                   // uniform
+          if (c * 8 >= kc) break;                  // uniform
           double v8[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) v8[q] = vcol[(j0 + c * 8 + q) * NT + pt] * f;
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         } else {
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (c * 8 >= k) break;               // uniform
+            if (c * 8 >= kc) break;              // uniform
             double v8[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) v8[q] = vr[c * 8 + q] * f;
@@ -500,10 +506,10 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     accs[warp * AW + 2 * KMAX + 1] = nu;
   }
   __syncthreads();
-  const int nv = 2 * k + 2;
+  const int nv = 2 * kc + 2;
   const int nb = gridDim.x;
   for (int v = t; v < nv; v += NTH) {
-    const int src = (v < k) ? v : (v < 2 * k ? KMAX + v - k : 2 * KMAX + (v - 2 * k));
+    const int src = (v < kc) ? v : (v < 2 * kc ? KMAX + v - kc : 2 * KMAX + (v - 2 * kc));
     double sum = 0.0;
     for (int w2 = 0; w2 < NW; ++w2) sum += accs[w2 * AW + src];
     a.ds.partials[(int64_t)v * nb + blockIdx.x] = sum;
@@ -525,6 +531,10 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     if (lane == 0) tot[v] = sum;
   }
   __syncthreads();
+  if (a.hyb) {                                    // the dots pass that follows finishes the step
+    for (int v = t; v < nv; v += NTH) a.ds.rpart[v] = tot[v];
+    return;
+  }
   if (t != 0) return;
   DevState& ds = a.ds;
   const int ldl = a.nA + 1;
@@ -590,7 +600,8 @@ struct MapCache {
   const double* field = nullptr;
   int64_t nx = 0, ny = 0, nz = 0;
   int cap = 0, tx = 0, ty = 0;
-  CUtensorMap mpx, mpy, mk;
+  const double* src = nullptr;
+  CUtensorMap mpx, mpy, mk, ms;
   bool ok = false;
 };
 
@@ -605,6 +616,7 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
             (st.field == nullptr || make_map(&mc.mk, st.field, st, 1, TX, TY));
     if (st.field == nullptr) mc.mk = mc.mpx;
     mc.px = ring_px; mc.py = ring_py; mc.field = st.field;
+    mc.src = nullptr;
     mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
     static bool attr = false;
     if (!attr) {
@@ -626,6 +638,11 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   a.zchunk = (int)zc;
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
   if (!mc.ok) return g_map_err ? g_map_err : -1;
+  if (a.src_px == 2 && mc.src != a.src_vec) {      // plain-vector source (split-column step)
+    if (!make_map(&mc.ms, a.src_vec, st, 1, TX, TY)) return g_map_err ? g_map_err : -1;
+    mc.src = a.src_vec;
+  }
+  if (a.src_px != 2 && mc.src == nullptr) mc.ms = mc.mpx;
   auto kern = fused_tma_kernel<KIND, TX, TY, KMAX, CS>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(TX * TY * CS + 32);         // compute warps + the TMA producer warp
@@ -634,25 +651,26 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   int64_t grid = 148;                              // one resident block per SM (persistent)
   if (grid > a.ntiles) grid = a.ntiles;
   cfg.gridDim = dim3((unsigned)grid);
-  if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, a) != cudaSuccess) return -2;
+  if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, mc.ms, a) != cudaSuccess) return -2;
   return 0;
 }
 
 template <int KIND>
 int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, cudaStream_t s) {
+  const int kc = a.k - a.jb;                       // basis columns of the pass
   if (three_d) {
     // stage = (KMAX + 2) boxes: the narrowest instantiation that holds k columns keeps the most
     // planes in flight (measured at 512^3: k <= 4 1.9 vs 2.3 ms, k = 9..12 3.5-3.8 vs 3.8-4.1 ms).
     // 32 x 8 tiles for k <= 16 or 16 x 8 tiles for k > 16 were slower (more halo points per tile).
-    if (a.k <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
-    if (a.k <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
-    if (a.k <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
-    if (a.k <= 16) return launch_t<KIND, 32, 15, 16, 1>(a, rpx, rpy, s);
-    if (a.k <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
+    if (kc <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
+    if (kc <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
+    if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
+    if (kc <= 16) return launch_t<KIND, 32, 15, 16, 1>(a, rpx, rpy, s);
+    if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
     return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, s);
   }
-  if (a.k <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, s);
-  if (a.k <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, s);
+  if (kc <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, s);
+  if (kc <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, s);
   return launch_t<KIND, 224, 1, 32, 2>(a, rpx, rpy, s);
 }
 
@@ -685,8 +703,15 @@ bool fused_supported(const Stencil& st, int k) {
 
 int launch_fused(const Stencil& st0, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
                   int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
-                  DevState ds, cudaStream_t s) {
+                  DevState ds, cudaStream_t s, int jb, const double* src_vec) {
   FusedArgs a;
+  a.jb = jb;
+  a.hyb = src_vec != nullptr;
+  a.src_vec = src_vec;
+  if (src_vec != nullptr) {
+    src_px = 2;
+    src_slot = 0;
+  }
   a.st = march_view(st0);
   a.k = k;
   a.nA = nA;

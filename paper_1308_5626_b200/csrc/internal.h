@@ -77,7 +77,9 @@ struct DevState {
 // scalar epilogues of the grid reductions (krylov.cu); multi-rank runs them as a 1-thread
 // kernel on the all-reduced ds.rpart
 // EPI_DOTS_RAW: the ring-resident step, w = A V_k unnormalised (scale alpha_k), so h_j carries alpha_k too
-enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5, EPI_DOTS_RAW = 6 };
+// EPI_HYB: the split-column ring step (fused pass over the last columns + dots over the rest)
+enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5, EPI_DOTS_RAW = 6,
+       EPI_HYB = 7 };
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s);
 enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
        SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_NSCAL = 16 };
@@ -116,8 +118,13 @@ void launch_mgs_literal_final(double* U, const double* Vk, int k, int nA, int64_
 void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n, int w_raw,
                       DevState ds, const RedCfg& rc, cudaStream_t s);
 // pass B = U = w - sum_j h_j V_j ; H(k+1,k) = ||U|| ; Givens update
+// ncols >= 0 and < k: only columns [0, ncols), no norm / epilogue (split-column step, pass A)
 void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
-                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
+                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s, int ncols = -1);
+// split-column step k, pass C: dots of V_0..V_{J-1} and u with w, then the step's epilogue
+// (EPI_HYB, with the fused pass's sums in ds.rpart)
+void launch_icwy_dots_hyb(Basis V, const double* w, const double* u, int J, int k, int nA, int64_t n,
+                          DevState ds, const RedCfg& rc, cudaStream_t s);
 // Q = H^{-1} G (R6) and out = base + sum_j Q_j V_j; base may be NULL (Z only)
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s);
@@ -134,7 +141,7 @@ bool fused_supported(const Stencil& st, int k);
 // returns 0, or the cuTensorMapEncodeTiled error of the operand maps
 int launch_fused(const Stencil& st, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
                   int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
-                  DevState ds, cudaStream_t s);
+                  DevState ds, cudaStream_t s, int jb = 0, const double* src_vec = nullptr);
 
 // ---- MREP (mrep.cu) ----
 struct MrepOut {

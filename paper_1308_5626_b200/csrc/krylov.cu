@@ -117,6 +117,27 @@ __device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, 
       }
       break;
     }
+    case EPI_HYB: {  // split-column ring step k (j = J): as the fused pass's epilogue (fused.cu)
+      // columns [0, J): tot = [s_0..s_J, l_0..l_{J-1}] of the dots pass (s_J = u'w~);
+      // columns [J, k): ds.rpart = [t_J..t_{k-1}, l_J..l_{k-1}, t_u, nu] of the fused pass
+      const int J = j, kk = k - J;
+      const double* hb = ds.rpart;
+      const double t_u = hb[2 * kk], s_nu = hb[2 * kk + 1];
+      ds.H[(int64_t)(k - 1) * ld + k] = sqrt(s_nu);  // l.17: H(k+1,k) = ||U_k||
+      givens_update(ds, k, nA);                       // l.19-32, sets alpha[k] (0 on breakdown)
+      if (k >= nA) break;
+      const double an = ds.alpha[k];
+      double* Lrow = ds.Lm + (int64_t)k * ld;        // the new row of L (R11)
+      for (int jb = 0; jb < k; ++jb) Lrow[jb] = ds.alpha[jb] * an * (jb < J ? tot[J + 1 + jb] : hb[kk + jb - J]);
+      double* Hc = ds.H + (int64_t)k * ld;           // (I + L) h = s for step k+1
+      for (int jb = 0; jb <= k; ++jb) {
+        double h = (jb < k) ? ds.alpha[jb] * an * (jb < J ? tot[jb] : hb[jb - J]) : an * an * t_u;
+        const double* Lr = ds.Lm + (int64_t)jb * ld;
+        for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
+        Hc[jb] = h;
+      }
+      break;
+    }
   }
 }
 
@@ -307,11 +328,14 @@ __device__ __forceinline__ void dots_tile(const double* const* cp,
 }
 __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
                                                         const double* __restrict__ w, int k,
-                                                        int nA, int64_t n, int w_raw, DevState ds) {
+                                                        int nA, int64_t n, int w_raw, DevState ds,
+                                                        const double* last, int kstep) {
+  // last != NULL: column k-1 is `last` (the split-column step's new u), and the epilogue is
+  // EPI_HYB of step kstep with J = k-1 columns from here
   __shared__ double accw[kWarps][2 * kMaxRestart];
   __shared__ const double* cp[kMaxRestart + 1];   // V(:,j) resolved once (ring slots)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
-  for (int q = t; q < k; q += TPB) cp[q] = V.col(q);
+  for (int q = t; q < k; q += TPB) cp[q] = (last != nullptr && q == k - 1) ? last : V.col(q);
   __syncthreads();
   const int nv = 2 * k - 1;  // s_0..s_{k-1} at [0,k), l_0..l_{k-2} at [k, 2k-1)
   for (int q = lane; q < 2 * k; q += 32) accw[warp][q] = 0.0;
@@ -339,7 +363,10 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
       if (lane == 0) tot[q] = s;
     }
     __syncthreads();
-    if (t == 0) finish_scalar(ds, w_raw ? EPI_DOTS_RAW : EPI_DOTS, k, nA, 0, 0, tot, nv);
+    if (t == 0) {
+      if (last != nullptr) epilogue(EPI_HYB, ds, kstep, nA, k - 1, 0, tot);
+      else finish_scalar(ds, w_raw ? EPI_DOTS_RAW : EPI_DOTS, k, nA, 0, 0, tot, nv);
+    }
   }
 }
 
@@ -399,12 +426,13 @@ __device__ __forceinline__ void update_tile(const double* const* cp, const doubl
 __global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double* __restrict__ w,
                                                           const double* ws,
                                                           double* __restrict__ U, int k, int nA,
-                                                          int64_t n, DevState ds) {
+                                                          int64_t n, DevState ds, int ncols) {
+  // ncols < k: the partial update of a split-column step (columns [0, ncols) only, no epilogue)
   __shared__ double hs[kMaxRestart];
   __shared__ double sm[kWarps];
   __shared__ const double* cp[kMaxRestart + 1];
   const int ld = nA + 1, t = threadIdx.x;
-  for (int q = t; q < k; q += TPB) {
+  for (int q = t; q < ncols; q += TPB) {
     hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
     cp[q] = V.col(q);
   }
@@ -415,9 +443,10 @@ __global__ void __launch_bounds__(TPB) icwy_update_kernel(Basis V, const double*
   const int64_t nfull = n / UTILE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * UTILE + t;
-    if (tile < nfull) update_tile<true>(cp, w, wsc, U, hs, k, n, r0, a[0]);
-    else update_tile<false>(cp, w, wsc, U, hs, k, n, r0, a[0]);
+    if (tile < nfull) update_tile<true>(cp, w, wsc, U, hs, ncols, n, r0, a[0]);
+    else update_tile<false>(cp, w, wsc, U, hs, ncols, n, r0, a[0]);
   }
+  if (ncols < k) return;
   block_sum<1>(a, sm);
   if (t == 0) ds.partials[blockIdx.x] = a[0];
   if (finish_block(ds.tickets + TK_MAIN)) {
@@ -518,15 +547,21 @@ void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n, int w_
                       DevState ds, const RedCfg& rc, cudaStream_t s) {
   static int wave = 0;
   if (!wave) wave = wave_blocks(icwy_dots_kernel, rc.nblocks);
-  icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, k, nA, n, w_raw, ds);
+  icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, k, nA, n, w_raw, ds, nullptr, 0);
+}
+void launch_icwy_dots_hyb(Basis V, const double* w, const double* u, int J, int k, int nA, int64_t n,
+                          DevState ds, const RedCfg& rc, cudaStream_t s) {
+  static int wave = 0;
+  if (!wave) wave = wave_blocks(icwy_dots_kernel, rc.nblocks);
+  icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, J + 1, nA, n, 1, ds, u, k);
 }
 void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
-                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
+                        int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s, int ncols) {
   static int wave = 0;
   if (!wave) wave = wave_blocks(icwy_update_kernel, rc.nblocks);
   int64_t ub = (n + UTILE - 1) / UTILE;
   if (ub > wave) ub = wave;
-  icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds);
+  icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds, ncols < 0 ? k : ncols);
 }
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s) {
   epilogue_kernel<<<1, 1, 0, s>>>(kind, ds, k, nA, j, slot);

@@ -47,7 +47,7 @@ class psp_opts(C.Structure):
     _fields_ = [("max_cycles", C.c_int32), ("tol_mode", C.c_int32), ("m_max", C.c_int32),
                 ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
                 ("timing", C.c_int32), ("fused", C.c_int32), ("fused_kmin", C.c_int32),
-                ("fused_kmax", C.c_int32)]
+                ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32)]
 
 
 class psp_report(C.Structure):

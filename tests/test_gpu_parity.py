@@ -234,6 +234,9 @@ def test_mrep_insufficient_samples(torch, P):
 # ------------------------------------------------------------------------------------------
 MODES = {"fused": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=32),      # every step one fused pass
          "ring": dict(ortho=0, fused=1),                                      # default mix on the ring
+         # split-column steps (update + fused over the newest columns + dots) from k = 3 / k = 13
+         "hybrid": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=2, fused_split_cols=2),
+         "hybrid12": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=12, fused_split_cols=12),
          "ringsplit": dict(ortho=0, fused=1, fused_kmin=99, fused_kmax=0),   # ring, no fused pass
          "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
 
