@@ -430,6 +430,12 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ms.partials = (double*)at(p.off_mpart);
   c->ms.ticket = (unsigned*)at(p.off_mtick);
   c->ms.result = (double*)at(p.off_mres);
+  // the split MREP's lagged-sum rows live in the Krylov basis storage (unused in ring mode, and
+  // free between solves in split mode: psp_mrep_fit runs after the solve, Alg.2 / P:30)
+  if (4 * c->d + 4 <= c->nA + 1) {
+    c->ms.sums = c->V;
+    c->ms.sums_n = c->ldv;
+  }
   c->bs = banded_scratch(at(p.off_banded), n, d);
   c->hx_lo = (double*)at(p.off_halo);
   c->hx_hi = c->hx_lo + plane;
@@ -993,7 +999,9 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
 
 psp_status psp_raw_scratch_bytes(int64_t n, int d, size_t* bytes) {
   if (!bytes || n < 1 || d < 1 || d > kMaxD) return fail(nullptr, PSP_E_ARG, "psp_raw_scratch_bytes: bad argument");
-  *bytes = banded_scratch_bytes(n, d) + 6 * kMrepMaxBlocks * 8 + 64 + 16 * 8 + 1024;
+  // + the split MREP's lagged-sum rows ((4d+4) x n doubles)
+  *bytes = banded_scratch_bytes(n, d) + 6 * kMrepMaxBlocks * 8 + 64 + 16 * 8 + 1024 +
+           (size_t)(4 * d + 4) * (size_t)n * 8 + 256;
   return PSP_OK;
 }
 
@@ -1005,6 +1013,10 @@ static void raw_carve(void* scratch, int64_t n, int d, MrepScratch* ms, BandedSc
   p += 64;
   ms->result = (double*)p;
   p += 16 * 8;
+  p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+  ms->sums = (double*)p;
+  ms->sums_n = n;
+  p += (size_t)(4 * d + 4) * (size_t)n * 8;
   p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
   *bs = banded_scratch(p, n, d);
 }

@@ -156,6 +156,8 @@ struct MrepScratch {
   double* result;     // 16: [0] max|diag| [1] max|diag| over non-dominant rows [2] min|diag|
                       // [3] rows_ridge [4] rows_fallback [5] rows_nondominant (pre-R18)
                       // [6] R18 patch needed [7] gate accepted (R21) [8] rows patched by R18
+  double* sums = nullptr;   // optional (4d+4) x sums_n lagged-sum rows: the split MREP (mrep.cu)
+  int64_t sums_n = 0;
 };
 constexpr int kMrepMaxBlocks = 148 * 8;
 // Alg.2 on probe columns px + slots[c]*ld (c = 0..m-1 oldest -> newest), then R18 + gate stats.

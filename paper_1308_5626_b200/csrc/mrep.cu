@@ -74,9 +74,9 @@ __host__ __device__ constexpr int pk(int a, int b) { return a * (a + 1) / 2 + b;
 
 // Gram of row r (thread t) from the lagged sums in shared memory:
 // G[0][0] = m, G[1+a][0] = S(r-d+a), G[1+b][1+a] = C_{b-a}(r-d+a) (b >= a); + lambda on the diagonal
-template <int D, int TS>
+template <int D>
 __device__ __forceinline__ void assemble(double (&A)[(2 * D + 2) * (2 * D + 3) / 2], const double* ex,
-                                         int t, int m, double lambda) {
+                                         int64_t TS, int t, int m, double lambda) {
   A[pk(0, 0)] = (double)m + lambda;
 #pragma unroll
   for (int a = 0; a <= 2 * D; ++a) {
@@ -159,8 +159,8 @@ struct GateStats {
 // Cholesky + condition estimate + one ridge retry (R17), solve, band install (R14, R15),
 // diagnostics and gate statistics.  ex: (2D+2) x TS sums of the tile's rows; t: this row's
 // index in the tile; r: local row; gr: global row.
-template <int D, int TS>
-__device__ __forceinline__ void fit_row(const double* ex, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
+template <int D>
+__device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
                                         int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
   constexpr int P = 2 * D + 2;
   constexpr int NP = P * (P + 1) / 2;
@@ -170,7 +170,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int t, int m, double T
   int kind = PSP_ROW_INTERIOR;
 #pragma unroll 1
   for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
-    assemble<D, TS>(A, ex, t, m, lambda);
+    assemble<D>(A, ex, TS, t, m, lambda);
     ok = chol_packed<P>(A, lmax, imax);
     if (attempt == 0) {
       kap = ok ? (lmax * imax) * (lmax * imax) : INFINITY;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
 
   const int64_t gr = cols.grow0 + r;                 // global row (multi-rank slabs)
   const bool emit = (t >= D && t < TPB - D) && r >= 0 && r < n && r < rend && gr >= D && gr < cols.gN - D;
-  if (emit) fit_row<D, TPB>(ex, t, m, Tsum, Dl, r, n, gr, cols.gN, out, gs);
+  if (emit) fit_row<D>(ex, TPB, t, m, Tsum, Dl, r, n, gr, cols.gN, out, gs);
   }  // tiles
   merge_stats(gs, red, sc.result);
 }
@@ -339,6 +339,12 @@ __global__ void __launch_bounds__(TPB, 1) mrep_interior_kernel(Cols cols, int m,
 // alignment parity (sx, sy; checked on the host, else the generic kernel runs everything).
 // ------------------------------------------------------------------------------------------
 constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kernel
+#ifndef PSP_MREP_CHUNKS
+#define PSP_MREP_CHUNKS 16    // row chunks of the split MREP (fits overlap the next chunk's sums)
+#endif
+#ifndef PSP_MREP_FIT_MINB
+#define PSP_MREP_FIT_MINB 2   // resident blocks per SM of the split MREP's fit kernel
+#endif
 #ifndef PSP_MREP_TCB
 #define PSP_MREP_TCB 8    // probe columns per stage (measured: 8 x 3 stages beats 4 x 4 at d = 3)
 #endif
@@ -351,6 +357,7 @@ struct TmaCfg {
   static constexpr int PYW = TT + 2;                             // P_y stage row
   static constexpr int STAGE = TCB * (PXW + PYW);                // doubles per stage
   static constexpr size_t SMEM = (size_t)TNST * STAGE * 8 + (size_t)(2 * D + 2) * TT * 8 + 16 * TNST;
+  static constexpr size_t SMEM_SUMS = (size_t)TNST * STAGE * 8 + 16 * TNST;   // no exchange buffer
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -393,8 +400,11 @@ struct TmaCols {
   int32_t slot[kMaxM];
 };
 
-template <int D>
-__global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
+// SUMS = true: the streaming half only -- every sum row of the tile (the D halo rows on each
+// side included; overlapping tiles write identical values) goes to sc.sums, and
+// mrep_fitsum_kernel fits the rows afterwards at its own occupancy.
+template <int D, bool SUMS>
+__global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
                                                                       int m, int64_t n, int64_t gN, int64_t grow0,
                                                                       int64_t R0, int64_t ntile, MrepOut out,
                                                                       MrepScratch sc) {
@@ -406,7 +416,7 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
   extern __shared__ __align__(16) double sm[];
   double* stages = sm;                             // [TNST][TCB x PXW | TCB x PYW]
   double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TT]: C_l, S of the tile's rows
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (2 * D + 2) * TT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (SUMS ? 0 : (2 * D + 2) * TT));
   __shared__ double scs[kMaxM];                    // per-column probe scale
   __shared__ double red[TT / 32 * 6];
   __shared__ int s_unit;
@@ -508,7 +518,21 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
     __syncthreads();                               // every thread is done with stage stg
     if (t == 0 && q + TNST < total) issue_next();
     if (++stg == TNST) stg = 0;
-    if (ch == nch - 1) {
+    if (SUMS && ch == nch - 1) {
+      const int64_t tile = blockIdx.x + (int64_t)tq * gridDim.x;
+      const int64_t r = R0 + tile * E - D + t;
+      const int64_t ns = sc.sums_n;
+      if (r >= 0 && r < n) {
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) sc.sums[(int64_t)l * ns + r] = Cl[l];
+        sc.sums[(int64_t)(2 * D + 1) * ns + r] = Ssum;
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) sc.sums[(int64_t)(2 * D + 2 + l) * ns + r] = Dl[l];
+        sc.sums[(int64_t)(4 * D + 3) * ns + r] = Tsum;
+      }
+      ch = 0;
+      ++tq;
+    } else if (!SUMS && ch == nch - 1) {
       // exchange C_l, S of the tile's TT sum rows, then fit the emitted rows
 #pragma unroll
       for (int l = 0; l <= 2 * D; ++l) ex[l * TT + t] = Cl[l];
@@ -516,13 +540,32 @@ __global__ void __launch_bounds__(TT, PSP_MREP_MINB) mrep_tma_kernel(TmaCols col
       __syncthreads();
       const int64_t tile = blockIdx.x + (int64_t)tq * gridDim.x;
       const int64_t r = R0 + tile * E - D + t;
-      if (t >= D && t < TT - D) fit_row<D, TT>(ex, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+      if (t >= D && t < TT - D) fit_row<D>(ex, TT, t, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
       __syncthreads();                             // ex is rewritten by the next tile
       ch = 0;
       ++tq;
     } else {
       ++ch;
     }
+  }
+  if (!SUMS) merge_stats(gs, red, sc.result);
+}
+
+// The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
+// lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
+template <int D>
+__global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int m, int64_t n, int64_t gN, int64_t grow0,
+                                                                         int64_t r0, int64_t r1, MrepOut out,
+                                                                         MrepScratch sc) {
+  __shared__ double red[TT / 32 * 6];
+  GateStats gs;
+  const int64_t ns = sc.sums_n;
+  for (int64_t r = r0 + (int64_t)blockIdx.x * TT + threadIdx.x; r < r1; r += (int64_t)gridDim.x * TT) {
+    double Dl[2 * D + 1];
+#pragma unroll
+    for (int l = 0; l <= 2 * D; ++l) Dl[l] = sc.sums[(int64_t)(2 * D + 2 + l) * ns + r];
+    const double Tsum = sc.sums[(int64_t)(4 * D + 3) * ns + r];
+    fit_row<D>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
   }
   merge_stats(gs, red, sc.result);
 }
@@ -533,10 +576,51 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
   const size_t smem = TmaCfg<D>::SMEM;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(mrep_tma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(mrep_tma_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(mrep_tma_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TmaCfg<D>::SMEM_SUMS);
     attr = true;
   }
-  mrep_tma_kernel<D><<<nb, TT, smem, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
+  const int64_t E = TT - 2 * D;
+  if (sc.sums != nullptr && sc.sums_n >= n && D >= 2) {
+    // split: stream + lagged sums, then the fits.  d <= 3: the rows go in PSP_MREP_CHUNKS
+    // chunks and the fits of chunk c run on a second stream beside the sums of chunk c+1 (the
+    // streaming kernel at 3 blocks per SM, so one fit block per SM fits beside it); d = 4 (the
+    // fit spills at that occupancy): one chunk, the streaming kernel at full occupancy.
+    // Measured n = 2^26, m = 32: d = 2 9.8 -> 8.9 ms, d = 3 11.3 -> 10.7 ms by the overlap.
+    constexpr int K = D <= 3 ? PSP_MREP_CHUNKS : 1;
+    thread_local cudaStream_t s2 = nullptr;
+    thread_local cudaEvent_t ev[K + 1];
+    if (s2 == nullptr) {
+      cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+      for (int q = 0; q <= K; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
+    }
+    static int occ = 0;
+    if (!occ) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mrep_tma_kernel<D, true>, TT, TmaCfg<D>::SMEM_SUMS);
+      if (occ < 1) occ = 1;
+    }
+    const int64_t g1max = 148 * (int64_t)(K > 1 && occ > 3 ? 3 : occ);
+    const int64_t per = (ntile + K - 1) / K;
+    for (int c = 0; c < K; ++c) {
+      const int64_t t0 = c * per, t1 = (t0 + per < ntile) ? t0 + per : ntile;
+      if (t1 <= t0) break;
+      const int64_t R0c = R0 + t0 * E;
+      const int g1 = (int)((t1 - t0) < g1max ? (t1 - t0) : g1max);
+      mrep_tma_kernel<D, true><<<g1, TT, TmaCfg<D>::SMEM_SUMS, s>>>(tc, scale, m, n, gN, grow0, R0c, t1 - t0, out,
+                                                                   sc);
+      cudaEventRecord(ev[c], s);
+      cudaStreamWaitEvent(s2, ev[c], 0);
+      const int64_t rows = (t1 - t0) * E;
+      const int64_t g2max = K > 1 ? 148 : 148 * PSP_MREP_FIT_MINB;   // beside the sums: one block per SM
+      const int64_t g2 = (rows + TT - 1) / TT < g2max ? (rows + TT - 1) / TT : g2max;
+      mrep_fitsum_kernel<D><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
+    }
+    cudaEventRecord(ev[K], s2);
+    cudaStreamWaitEvent(s, ev[K], 0);
+  } else {
+    mrep_tma_kernel<D, false><<<nb, TT, smem, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
+  }
 }
 
 // Boundary rows, R16 two-pass centred OLS, one thread per row.
