@@ -220,7 +220,9 @@ psp_status psp_solve(psp_ctx* ctx, const double* d_b, const double* d_x0, double
 
 /* Algorithm 2 on the probe ring (oldest -> newest, R20), then R18, the R21 gate
  * and the banded LU factorisation of the accepted N (a9).  Rejection or a failed
- * factorisation installs N = I.  PSP_E_SAMPLES if m < 2d+2 (N unchanged). */
+ * factorisation installs N = I.  PSP_E_SAMPLES if m < 2d+2 (N unchanged).
+ * Uses the Krylov basis storage as scratch (4d+4 <= restart+1): call it between solves, as
+ * the time-step driver does. */
 psp_status psp_mrep_fit(psp_ctx* ctx, psp_report* rep);
 
 /* One implicit-Euler step (Eq.3-4; a10): b = u_n, x0 = u_n (R2),
@@ -238,7 +240,8 @@ typedef struct {
   int32_t status;
 } psp_mrep_info;
 
-/* Scratch bytes for psp_mrep_fit_raw / psp_banded_factor_raw / psp_banded_solve_raw. */
+/* Scratch bytes for psp_mrep_fit_raw / psp_banded_factor_raw / psp_banded_solve_raw
+ * (includes (4d+4) x n doubles of lagged-sum rows for the MREP fit). */
 psp_status psp_raw_scratch_bytes(int64_t n, int d, size_t* bytes);
 
 /* Alg.2 on caller probe columns: column c (oldest -> newest) of P_x / P_y starts at
