@@ -36,6 +36,7 @@ namespace {
 
 constexpr int kChunk = 512;      // factor: rows per thread
 constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
+constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four rows)
 constexpr int STPB = 256;        // solve: threads per block
 constexpr int SR = 8;            // solve: rows per thread
 constexpr int STILE = STPB * SR; // solve: rows per tile
@@ -95,6 +96,30 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
   for (int q = 0; q < D; ++q) Ri[q] = 1.0 / Uw[q][0];
   int isbad = 0;
+  // the bands of the next groups of four rows are prefetched into this thread's slots of a
+  // PF-deep shared-memory ring by cp.async (16-byte copies, no registers held): a walk is a
+  // serial recurrence, and without the prefetch every group waits a full DRAM latency
+  extern __shared__ __align__(16) double pf[];   // [PF][NB][blockDim][4]
+  auto pf_at = [&](int buf, int o) -> double* {
+    return pf + ((size_t)(buf * NB + o) * blockDim.x + threadIdx.x) * 4;
+  };
+  constexpr bool PFON = D <= 3;   // d = 4: the ring's shared memory costs more occupancy than it saves
+  auto prefetch = [&](int64_t i0, int buf) {
+    if (!PFON) return;
+    if (vec && i0 + 4 <= r1) {
+#pragma unroll
+      for (int o = 0; o < NB; ++o) {
+        const double* g = bands + (int64_t)o * n + i0;
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pf_at(buf, o));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16), "l"(g + 2) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");   // (possibly empty: keeps the count)
+  };
+#pragma unroll
+  for (int q = 0; q < kPF - 1; ++q) prefetch(rs + 4 * q, q);
+  int buf = 0;
   for (int64_t i0 = rs; i0 < r1; i0 += 4) {
     const bool live = i0 >= r0;                 // warm-up rows: state only
     if (warm > 0 && first_pass && c > 0 && i0 == r0) {
@@ -105,7 +130,15 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
     }
     const int nr = (r1 - i0) < 4 ? (int)(r1 - i0) : 4;
     double bb[NB][4];
-    if (vec && nr == 4) {
+    if (PFON) asm volatile("cp.async.wait_group %0;" ::"n"(kPF - 2) : "memory");   // this group landed
+    if (PFON && vec && nr == 4) {
+#pragma unroll
+      for (int o = 0; o < NB; ++o) {
+        const double2 lo = *reinterpret_cast<const double2*>(pf_at(buf, o));
+        const double2 hi = *reinterpret_cast<const double2*>(pf_at(buf, o) + 2);
+        bb[o][0] = lo.x; bb[o][1] = lo.y; bb[o][2] = hi.x; bb[o][3] = hi.y;
+      }
+    } else if (vec && nr == 4) {
 #pragma unroll
       for (int o = 0; o < NB; ++o) {
         const double2 lo = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0));
@@ -118,6 +151,8 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
     }
+    prefetch(i0 + 4 * (kPF - 1), buf == 0 ? kPF - 1 : buf - 1);   // into the slot read last group
+    buf = (buf + 1 == kPF) ? 0 : buf + 1;
     // results overwrite the consumed band values of their row (bb doubles as the output tile).
     // Groups whose rows all have a full window (no matrix / chunk start within D rows, no matrix
     // end within D rows) take the check-free copy of the row step.
@@ -703,11 +738,18 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
   const int tpb = 64;
   const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
+  const size_t smem = D <= 3 ? (size_t)kPF * (2 * D + 1) * tpb * 4 * 8 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(factor_pass_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(factor_pass_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   if (write)
-    factor_pass_kernel<D, true><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
+    factor_pass_kernel<D, true><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
                                                      has_next, vec, warm, st_start);
   else
-    factor_pass_kernel<D, false><<<grid, tpb, 0, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
+    factor_pass_kernel<D, false><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
                                                       has_next, vec, warm, st_start);
 }
 
