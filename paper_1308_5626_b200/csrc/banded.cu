@@ -27,9 +27,6 @@
 
 #include "internal.h"
 
-#ifndef PSP_SWEEP_MINB
-#define PSP_SWEEP_MINB 2   // resident 256-thread sweep blocks per SM
-#endif
 
 namespace psp {
 namespace {
@@ -37,7 +34,16 @@ namespace {
 constexpr int kChunk = 512;      // factor: rows per thread
 constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
 constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four rows)
-constexpr int STPB = 256;        // solve: threads per block
+// solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks (4 per SM: more
+// independent tiles in flight) for d >= 3 (measured n = 2^26: d = 3 2.34 -> 2.04 ms, d = 4
+// 4.25 -> 3.90 ms; d = 1 prefers 256)
+template <int D>
+struct SW {
+  static constexpr int TPB = D >= 3 ? 128 : 256;
+  static constexpr int MINB = D >= 3 ? 4 : 2;
+  static constexpr int TILE = TPB * 8;
+};
+constexpr int STPB = 128;        // solve: the smallest block (host-side sizing of per-tile arrays)
 constexpr int SR = 8;            // solve: rows per thread
 constexpr int STILE = STPB * SR; // solve: rows per tile
 constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank conflicts)
@@ -352,7 +358,7 @@ __device__ __forceinline__ void push_state(double (&s)[D], double y) {
 template <bool FWD, int D>
 struct TileSmem {
   static constexpr int NA = 1 + D + (FWD ? 0 : 1);
-  static constexpr size_t BYTES = (size_t)NA * STPB * SPAD * sizeof(double);
+  static constexpr size_t BYTES = (size_t)NA * SW<D>::TPB * SPAD * sizeof(double);
 };
 
 // stage the tile's rows (coalesced) into the per-thread padded layout: sv (rhs), sc[k]
@@ -360,16 +366,16 @@ struct TileSmem {
 template <bool FWD, int D>
 __device__ __forceinline__ void stage_tile(double* sv, const double* __restrict__ lu, int64_t n,
                                            const double* __restrict__ vin, double vsc, int64_t base) {
-  double* sc0 = sv + STPB * SPAD;
-  double* su0 = sv + (1 + D) * STPB * SPAD;
-  constexpr int IT = STILE / STPB;              // rows per thread of the coalesced copy
+  double* sc0 = sv + SW<D>::TPB * SPAD;
+  double* su0 = sv + (1 + D) * SW<D>::TPB * SPAD;
+  constexpr int IT = SW<D>::TILE / SW<D>::TPB;              // rows per thread of the coalesced copy
   constexpr int NA = 1 + D + (FWD ? 0 : 1);
   // every load of the tile is issued before the first shared-memory store (one latency per tile)
   double r[IT][NA];
-  const bool full = base + STILE <= n;
+  const bool full = base + SW<D>::TILE <= n;
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
-    const int64_t i = base + threadIdx.x + it * STPB;
+    const int64_t i = base + threadIdx.x + it * SW<D>::TPB;
     const bool in = full || i < n;
     r[it][0] = (in && vin) ? __ldg(vin + i) : 0.0;
 #pragma unroll
@@ -382,11 +388,11 @@ __device__ __forceinline__ void stage_tile(double* sv, const double* __restrict_
   }
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
-    const int q = threadIdx.x + it * STPB;
+    const int q = threadIdx.x + it * SW<D>::TPB;
     const int sidx = (q / SR) * SPAD + (q % SR);
     sv[sidx] = vsc * r[it][0];
 #pragma unroll
-    for (int k = 0; k < D; ++k) sc0[k * STPB * SPAD + sidx] = r[it][1 + k];
+    for (int k = 0; k < D; ++k) sc0[k * SW<D>::TPB * SPAD + sidx] = r[it][1 + k];
     if (!FWD) su0[sidx] = r[it][1 + D];
   }
 }
@@ -394,8 +400,8 @@ __device__ __forceinline__ void stage_tile(double* sv, const double* __restrict_
 // this thread's SR rows as an affine map (FWD ascending, BWD descending)
 template <bool FWD, int D>
 __device__ __forceinline__ Map<D> thread_map(const double* sv, int64_t base, int64_t n) {
-  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
-  const double* su0 = sv + (1 + D) * STPB * SPAD;
+  const double (*sc)[SW<D>::TPB * SPAD] = reinterpret_cast<const double (*)[SW<D>::TPB * SPAD]>(sv + SW<D>::TPB * SPAD);
+  const double* su0 = sv + (1 + D) * SW<D>::TPB * SPAD;
   const int t = threadIdx.x;
   double sz[D];            // zero-state run
   double su[D][D];         // unit-state runs: su[q] starts at e_q
@@ -428,12 +434,12 @@ __device__ __forceinline__ Map<D> thread_map(const double* sv, int64_t base, int
   return my;
 }
 
-// block scan of the thread maps in processing order (FWD thread 0 first, BWD thread STPB-1
+// block scan of the thread maps in processing order (FWD thread 0 first, BWD thread SW<D>::TPB-1
 // first): returns this thread's exclusive prefix; agg (valid in every thread) = the whole tile
 template <bool FWD, int D>
 __device__ __forceinline__ Map<D> block_prefix(const Map<D>& my, Map<D>* wtot, Map<D>& agg) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  constexpr int NW = STPB / 32;
+  constexpr int NW = SW<D>::TPB / 32;
   Map<D> inc = my;  // inclusive prefix within the warp, in processing order
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -481,7 +487,7 @@ __device__ __forceinline__ Map<D> block_prefix(const Map<D>& my, Map<D>* wtot, M
 // map; tile_scan_kernel turns the range maps into exact incoming range states; tile_apply_kernel
 // walks the range again from that state (each tile's map, recomputed, carries the state on).
 template <bool FWD, int D>
-__global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restrict__ lu, int64_t n,
+__global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_map_kernel(const double* __restrict__ lu, int64_t n,
                                                             const double* __restrict__ vin, const double* vscale,
                                                             const double* addend, double* out, int64_t L,
                                                             double* __restrict__ rmap) {
@@ -490,14 +496,14 @@ __global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restr
   // solution differs from y0 only by the homogeneous response to the true incoming state,
   // which tile_fix_kernel adds (it decays geometrically under the dominance gate).
   extern __shared__ double smem_dyn[];
-  __shared__ Map<D> wtot[STPB / 32];
+  __shared__ Map<D> wtot[SW<D>::TPB / 32];
   constexpr int DW = D * D + 2 * D;
   const int t = threadIdx.x;
-  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const double vsc = vscale ? *vscale : 1.0;
   double* sv = smem_dyn;
-  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
-  const double* su0 = sv + (1 + D) * STPB * SPAD;
+  const double (*sc)[SW<D>::TPB * SPAD] = reinterpret_cast<const double (*)[SW<D>::TPB * SPAD]>(sv + SW<D>::TPB * SPAD);
+  const double* su0 = sv + (1 + D) * SW<D>::TPB * SPAD;
   Map<D> range = identity_map<D>();
   double s0[D];
 #pragma unroll
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restr
   const int64_t p0 = (int64_t)blockIdx.x * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
   for (int64_t p = p0; p < p1; ++p) {
     const int64_t tile = FWD ? p : ntiles - 1 - p;
-    const int64_t base = tile * STILE;
+    const int64_t base = tile * SW<D>::TILE;
     stage_tile<FWD, D>(sv, lu, n, vin, vsc, base);
     __syncthreads();
     const Map<D> my = thread_map<FWD, D>(sv, base, n);
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(STPB, 2) tile_map_kernel(const double* __restr
 #pragma unroll
       for (int i = 0; i < D; ++i) s0[i] = s1[i];
       __syncthreads();
-      for (int q = t; q < STILE; q += STPB) {
+      for (int q = t; q < SW<D>::TILE; q += SW<D>::TPB) {
         const int64_t i = base + q;
         if (i < n) {
           const double y = sv[(q / SR) * SPAD + (q % SR)];
@@ -574,11 +580,11 @@ __global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_
   }
   if (!(amax > 0.0)) return;                       // zero incoming state: y0 is exact
   const double stop = amax * 0x1p-60;
-  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const int64_t t0 = (int64_t)r * L, t1 = (t0 + L < ntiles) ? t0 + L : ntiles;
   // rows of the range in processing order
-  const int64_t lo = (FWD ? t0 : ntiles - t1) * STILE;
-  const int64_t hi = ((FWD ? t1 : ntiles - t0) * STILE < n) ? (FWD ? t1 : ntiles - t0) * STILE : n;
+  const int64_t lo = (FWD ? t0 : ntiles - t1) * SW<D>::TILE;
+  const int64_t hi = ((FWD ? t1 : ntiles - t0) * SW<D>::TILE < n) ? (FWD ? t1 : ntiles - t0) * SW<D>::TILE : n;
   const int64_t len = hi - lo;
   const int64_t cap = len < kFixCap ? len : kFixCap;
   int64_t q = 0;
@@ -661,20 +667,20 @@ __global__ void __launch_bounds__(SCAN_T, 1) tile_scan_kernel(int nr, double* __
 }
 
 template <bool FWD, int D>
-__global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __restrict__ lu, int64_t n,
+__global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_apply_kernel(const double* __restrict__ lu, int64_t n,
                                                               const double* __restrict__ vin, const double* vscale,
                                                               const double* addend, double* out, int64_t L,
                                                               const double* __restrict__ rmap,
                                                               const double* __restrict__ full) {
   extern __shared__ double smem_dyn[];
-  __shared__ Map<D> wtot[STPB / 32];
+  __shared__ Map<D> wtot[SW<D>::TPB / 32];
   constexpr int DW = D * D + 2 * D;
   const int t = threadIdx.x;
-  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const double vsc = vscale ? *vscale : 1.0;
   double* sv = smem_dyn;
-  const double (*sc)[STPB * SPAD] = reinterpret_cast<const double (*)[STPB * SPAD]>(sv + STPB * SPAD);
-  const double* su0 = sv + (1 + D) * STPB * SPAD;
+  const double (*sc)[SW<D>::TPB * SPAD] = reinterpret_cast<const double (*)[SW<D>::TPB * SPAD]>(sv + SW<D>::TPB * SPAD);
+  const double* su0 = sv + (1 + D) * SW<D>::TPB * SPAD;
   if (full != nullptr && full[blockIdx.x] == 0.0) return;   // tile_fix_kernel completed this range
   double s0[D];
 #pragma unroll
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __res
   const int64_t p0 = (int64_t)blockIdx.x * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
   for (int64_t p = p0; p < p1; ++p) {
     const int64_t tile = FWD ? p : ntiles - 1 - p;
-    const int64_t base = tile * STILE;
+    const int64_t base = tile * SW<D>::TILE;
     stage_tile<FWD, D>(sv, lu, n, vin, vsc, base);
     __syncthreads();
     const Map<D> my = thread_map<FWD, D>(sv, base, n);
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(STPB, 2) tile_apply_kernel(const double* __res
 #pragma unroll
     for (int i = 0; i < D; ++i) s0[i] = s1[i];
     __syncthreads();
-    for (int q = t; q < STILE; q += STPB) {
+    for (int q = t; q < SW<D>::TILE; q += SW<D>::TPB) {
       const int64_t i = base + q;
       if (i < n) {
         const double y = sv[(q / SR) * SPAD + (q % SR)];
@@ -756,7 +762,7 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
 template <bool FWD, int D>
 void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
                   double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out) {
-  const int64_t ntiles = (n + STILE - 1) / STILE;
+  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const size_t smem = TileSmem<FWD, D>::BYTES;
   const size_t ssmem = (size_t)SCAN_T * sizeof(Map<D>);
   static bool attr_set = false;
@@ -767,18 +773,18 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
     attr_set = true;
   }
   // ranges: at most SCAN_T blocks (2 resident per SM), each a contiguous run of L tiles
-  int64_t nb = ntiles < 148 * 2 * 3 ? ntiles : 148 * 2 * 3;
+  int64_t nb = ntiles < 148 * SW<D>::MINB * 3 ? ntiles : 148 * SW<D>::MINB * 3;
   if (nb > SCAN_T) nb = SCAN_T;
   if (nb < 1) nb = 1;
   const int64_t L = (ntiles + nb - 1) / nb;
   nb = (ntiles + L - 1) / L;
   double* full = sc.states + (size_t)SCAN_T * (D * D + 2 * D);   // per-range flag
   if (ntiles > 0)
-    tile_map_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
+    tile_map_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
   tile_scan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>(ntiles > 0 ? (int)nb : 0, sc.states, s_in0, s_out);
   if (out != nullptr && ntiles > 0) {
     tile_fix_kernel<FWD, D><<<(unsigned)((nb + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nb, out, sc.states, full);
-    tile_apply_kernel<FWD, D><<<(unsigned)nb, STPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states, full);
+    tile_apply_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states, full);
   }
 }
 
