@@ -98,7 +98,7 @@ typedef struct {
                                    /* (1..16) basis columns through the fused pass, the older */
                                    /* k - fused_split_cols through an update pass and a dots  */
                                    /* pass (DESIGN.md s.6); 0 = three separate passes;        */
-                                   /* default 12                                              */
+                                   /* default 16                                              */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */

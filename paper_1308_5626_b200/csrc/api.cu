@@ -269,7 +269,7 @@ void psp_default_opts(psp_opts* o) {
   o->fused = 1;
   o->fused_kmin = 2;
   o->fused_kmax = 16;
-  o->fused_split_cols = 12;
+  o->fused_split_cols = 16;
 }
 
 const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }

@@ -128,7 +128,7 @@ struct FCfg {
   // is released as soon as u is formed (all but one stage in flight; the plane's kappa moves to
   // a kappa plane ring beside the u ring); wider thread column sets (KJ = 16) do not fit the
   // 128-register budget and keep the stage for the t_j and the stencil's kappa instead
-  static constexpr bool RV = KMAX / CS <= 12;
+  static constexpr bool RV = KMAX / CS <= 12 || (KMAX / CS <= 16 && NT * CS + 32 <= 384);
   static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
   static constexpr int STAGE = NB * NT;                      // doubles
   static constexpr int RING = (RV ? 2 : 1) * NUB * NT;       // u (+ kappa) plane rings, doubles
@@ -665,7 +665,10 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     if (kc <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
     if (kc <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
     if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
-    if (kc <= 16) return launch_t<KIND, 32, 15, 16, 1>(a, rpx, rpy, s);
+    // k = 13..16: 32 x 11 tiles (12 warps, up to 168 registers) hold a thread's 16 basis
+    // values in registers, so a stage is released as soon as u is formed (32 x 15 tiles would
+    // keep two stages resident): 4.2-4.9 -> 4.0-4.5 ms at 512^3
+    if (kc <= 16) return launch_t<KIND, 32, 11, 16, 1>(a, rpx, rpy, s);
     if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
     return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, s);
   }
