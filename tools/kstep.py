@@ -30,14 +30,16 @@ torch.cuda.synchronize()
 R = prob.restart
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(R + 2)]
 variants = os.environ.get("KSTEP_VARIANTS", "default").split(",")
+set_keys = set()
 for var in variants:
     # variant "default" or "NAME=VAL+NAME2=VAL2" (environment knobs read per launch)
-    for key in ("PSP_FUSED_CL", "PSP_FUSED_ZC", "PSP_FUSED_PSYNC", "PSP_FUSED_TILE"):
+    for key in [k for k in os.environ if k.startswith("PSP_") and k != "PSP_LIB"] + list(set_keys):
         os.environ.pop(key, None)
     if var != "default":
         for kv in var.split("+"):
             name, val = kv.split("=")
             os.environ[name] = val
+            set_keys.add(name)
     times = np.zeros((cycles, R + 1))
     for c in range(cycles):
         ev[0].record(s)
