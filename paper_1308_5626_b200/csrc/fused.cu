@@ -232,6 +232,12 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
   }
   const double wsc = (k >= 1 && !a.hyb) ? a.ds.alpha[k - 1] : 1.0;
   __syncthreads();
+  // narrow steps: the (negated) MGS coefficients in registers, not re-read from shared memory
+  // every plane
+  constexpr bool HREG = KJ <= 8;
+  double hr[HREG ? KJ : 1];
+#pragma unroll
+  for (int j = 0; j < (HREG ? KJ : 1); ++j) hr[j] = HREG ? -hs[j0 + j] : 0.0;
 
   const int nload = (k == 0 ? 0 : kc) + 1 + (cell ? 1 : 0);
   const unsigned stage_bytes = (unsigned)(nload * NT * 8);
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         if (k == 0) return s0;
         double u = (half == 0) ? wsc * s0 : 0.0;
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) u = fma(-hs[j0 + j], sb[(j0 + j) * NT + pt], u);
+        for (int j = 0; j < KJ; ++j) u = fma(HREG ? hr[j] : -hs[j0 + j], sb[(j0 + j) * NT + pt], u);
         if (CS == 2) {                           // the halves' partial updates, same sum on both
           const double o = __shfl_xor_sync(0xffffffffu, u, 16);
           u = (half == 0) ? u + o : o + u;
@@ -375,6 +381,8 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       release(gb);
       if (!(z0 >= 1 && in_grid)) ub = 0.0;
       int64_t g = col + plane * z0;              // this point's index at plane p
+      double* ox = a.dstx + g;                   // this point's outputs at plane p
+      double* oy = a.dsty + g;
       const double* sbc = acquire(gb + 1);
       double uc = form_u(sbc);
       if (!in_grid) uc = 0.0;
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       publish_u(ub0, uc, kc);
       if (RV && k > 0) load_vr(sbc, vr);
       if (RV) release(gb + 1);
-      if (emit && k > 0) a.dstx[g] = uc;
+      if (emit && k > 0) *ox = uc;
       {
         const double f = own ? uc : 0.0;
         if (half == 0) nu = fma(f, f, nu);
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
           }
           w = c0 + acc;
           if (half == 0) {
-            a.dsty[g] = w;
+            *oy = w;
             tu = fma(c0, w, tu);
           }
         }
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         }
         if (pn < z1) {
           if (RV && k > 0) load_vr(sn, vr);      // V(p+1): its l_j now, its t_j next plane
-          if (emit && k > 0) a.dstx[g + plane] = un;
+          if (emit && k > 0) ox[plane] = un;
           const double f = own ? un : 0.0;
           if (half == 0) nu = fma(f, f, nu);
           if (k > 0) {
@@ -458,7 +466,8 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         if (RV || pn == z1) release(gp + 1);      // stage p+1 done (else: after its t_j)
         ub = uc; uc = un;
         kb = kc; kc = kt;
-        g += plane;
+        ox += plane;
+        oy += plane;
       }
       gs = gb + (uint32_t)(z1 - z0 + 2);          // planes z0-1 .. z1
       us = ub0 + (uint32_t)(z1 - z0);             // u planes z0 .. z1-1
