@@ -60,3 +60,35 @@ def test_create_rejects_bad_arguments_without_gpu():
     s.kind = P.PSP_OP_CONST_DIFF
     assert lib.psp_workspace_bytes(ctypes.byref(g2), ctypes.byref(s), 1, 30, ctypes.byref(o), None,
                                    ctypes.byref(nb)) == P.PSP_E_DIM          # n < 2d+1
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of psp_grid / psp_stencil / psp_opts / psp_report / psp_mrep_info have
+    the C structs' sizes and field offsets (compiled from include/pspgmres.h with gcc)."""
+    import shutil
+    import subprocess
+    from paper_1308_5626_b200 import pspgmres as P
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    structs = [s for s in ("psp_grid", "psp_stencil", "psp_opts", "psp_report", "psp_mrep_info") if hasattr(P, s)]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HDR}"', "int main(void) {"]
+    for s in structs:
+        lines.append(f'  printf("{s} size %zu\\n", sizeof({s}));')
+        for f, _ in getattr(P, s)._fields_:
+            lines.append(f'  printf("{s} {f} %zu\\n", offsetof({s}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln.strip():
+            s, f, v = ln.split()
+            got[(s, f)] = int(v)
+    for s in structs:
+        cs = getattr(P, s)
+        assert got[(s, "size")] == ctypes.sizeof(cs), s
+        for f, _ in cs._fields_:
+            assert got[(s, f)] == getattr(cs, f).offset, (s, f)
