@@ -1,0 +1,179 @@
+"""Parity at BASELINE.json's full sizes, in the configuration bench.py times, on sampled outputs
+the oracle computes one by one (or on properties that hold at any size).
+
+* C5 (configs[4]): n = 2^26, m = 32, d = 3 -- the split MREP, the warm-started factorisation and
+  the two-sweep solve.  Every sampled interior row's fit is the oracle's Algorithm 2 on the
+  4d+1 rows around it (the row's own regression only reads P_x rows i-d..i+d and P_y row i,
+  P:111-122), boundary rows are fitted on the first / last 4d+1 rows; factors and solve are
+  checked by (LU)(i,:) = N(i,:) and (N z)(i) = v(i) on the sampled rows.
+* C4 (configs[3]): one 512^3 time step with the bench's options (fused passes, split-column
+  steps): convergence with the true residual below tol ||b|| and, on sampled points of the
+  newest recorded probes, P_y = A P_x with A applied by the oracle on the 3x3x3 neighbourhood
+  of each point (its row of A only reaches those points, Eq.4 / P:25).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1308_5626_b200 import inputs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+U = np.finfo(np.float64).eps / 2
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu tests need a B200"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1308_5626_b200 import pspgmres
+    pspgmres.lib()
+    return pspgmres
+
+
+def _free(torch):
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _sample_rows(n, d, rng, count=1500):
+    rows = set(rng.integers(2 * d, n - 2 * d, count).tolist())
+    rows |= set(range(0, 2 * d + 1)) | set(range(n - 2 * d - 1, n))   # boundary + first interior rows
+    E = 128 - 2 * d                                                      # TMA tile edges (R0 = 2d+2)
+    for t in range(0, 40):
+        rows |= {2 * d + 2 + t * E - 1, 2 * d + 2 + t * E}
+    rows |= {n // 2 - 1, n // 2, n // 2 + 1}                             # split-MREP chunk seams
+    return np.array(sorted(r for r in rows if 0 <= r < n))
+
+
+def test_c5_full_size_sampled(torch, P, orc):
+    n, m, d = 1 << 26, 32, 3
+    g5 = inputs.c5_torch(n, m, d, seed=0)
+    scratch = P.raw_scratch(n, d)
+    g = P.psp_mrep_fit_raw(g5["px"], g5["py"], d, scratch=scratch)
+    assert g["status"] == P.PSP_OK and g["gate_accepted"]            # A_true is dominant (C5 recipe)
+    rows = _sample_rows(n, d, np.random.default_rng(5))
+    bands = g["bands"][:, torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    kinds = g["row_kind"][torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    W = 4 * d + 1
+    Pn = 2 * d + 2
+    worst = 0.0
+    for col, i in enumerate(rows):
+        lo = min(max(i - 2 * d, 0), n - W)          # rows i-2d..i+2d, clamped inside the matrix:
+        c = i - lo                                  # boundary rows stay boundary rows of the window
+        px = g5["px"][:, lo:lo + W].cpu().numpy()
+        py = g5["py"][:, lo:lo + W].cpu().numpy()
+        r = orc.mrep(px, py, d)
+        assert kinds[col] == r["row_kind"][c], (i, kinds[col], r["row_kind"][c])
+        ref = r["bands"][:, c]
+        scale = max(np.abs(ref).max(), 1e-300)
+        err = np.abs(bands[:, col] - ref).max() / scale
+        if d <= c < W - d:   # interior row: T3 tolerance from the row's Gram condition
+            X = np.vstack([np.ones(m), px[:, c - d:c + d + 1].T])
+            k2 = np.linalg.cond(X @ X.T)
+            tol = 1e-10 if k2 <= 1e5 else 8 * Pn * U * k2
+        else:
+            tol = 1e-12
+        worst = max(worst, err / tol)
+        assert err <= tol, (i, err, tol)
+    # factorisation: (L U)(i, j) = N(i, j) on the sampled rows (property of the exact factors)
+    st, lu = P.psp_banded_factor_raw(g["bands"], d, scratch=scratch)
+    assert st == P.PSP_OK
+    Nb = g["bands"]
+    for i in rows[(rows >= 2 * d) & (rows < n - 2 * d)][:400]:
+        idx = torch.arange(i - d, i + 1, device="cuda")
+        L = lu[:d, i].cpu().numpy()                     # L(i, i-d+q), unit diagonal
+        Urows = lu[d:, idx].cpu().numpy()               # U(k, k+e) for k = i-d..i
+        for o in range(2 * d + 1):
+            j = i + o - d
+            s = 0.0
+            for q in range(d + 1):                      # k = i-d+q
+                lik = 1.0 if q == d else L[q]
+                e = j - (i - d + q)
+                if 0 <= e <= d:
+                    s += lik * Urows[e, q]
+            ref = Nb[o, i].item()
+            assert abs(s - ref) <= 1e-12 * (abs(ref) + 1.0), (i, o, s, ref)
+    # solve: (N z)(i) = v(i) on the sampled rows
+    z = P.psp_banded_solve_raw(lu, d, g5["v"], scratch=scratch)
+    zs = {}
+    for i in rows:
+        acc, mag = 0.0, 0.0
+        for o in range(2 * d + 1):
+            j = i + o - d
+            if 0 <= j < n:
+                if j not in zs:
+                    zs[j] = z[j].item()
+                t = Nb[o, i].item() * zs[j]
+                acc += t
+                mag += abs(t)
+        vi = g5["v"][i].item()
+        assert abs(acc - vi) <= 1e-13 * (1 + d) * (abs(vi) + mag), (i, acc, vi)
+    del g5, g, lu, z, scratch, Nb
+    _free(torch)
+
+
+def test_c4_full_size_sampled(torch, P, orc):
+    size = 512
+    prob = inputs.c4(n=size, steps=1)
+    opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max)    # the bench's defaults
+    ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts)
+    u = torch.as_tensor(prob.u0).cuda()
+    b = prob.u0.copy()
+    rep = ctx.psp_step(u, u)
+    assert rep["converged"]
+    assert rep["final_resid_true"] <= rep["eps"]                # ||b - A u|| <= tol ||b|| (R1, R13)
+    # the newest probes: P_y = A P_x on sampled points, A applied by the oracle on each point's
+    # 3x3x3 neighbourhood (scaled dt keeps dt / h^2 of the full grid)
+    lib = P.lib()
+    cnt = C.c_int()
+    slots = (C.c_int32 * 257)()
+    scale = np.zeros(257)
+    pxp, pyp, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
+    st = lib.psp_ring_view(ctx.h, C.byref(cnt), slots, scale.ctypes.data_as(C.POINTER(C.c_double)),
+                           C.byref(pxp), C.byref(pyp), C.byref(ld))
+    assert st == P.PSP_OK and cnt.value >= 3
+    n = size ** 3
+    ws64 = ctx.ws.view(torch.float64)
+    base = ctx.ws.data_ptr()
+    rng = np.random.default_rng(4)
+    pts = rng.integers(1, size - 1, (300, 3))                   # (z, y, x) interior points
+    pts = np.vstack([pts, [[0, 0, 0], [size - 1, size - 1, size - 1], [0, 5, size - 1]]])
+    kap = prob.op.field.reshape(size, size, size)
+    hfull = 1.0 / (size + 1)
+    for q in range(cnt.value - 3, cnt.value):
+        sl = slots[q]
+        PX = ws64[(pxp.value - base) // 8 + sl * ld.value:(pxp.value - base) // 8 + sl * ld.value + n]
+        PY = ws64[(pyp.value - base) // 8 + sl * ld.value:(pyp.value - base) // 8 + sl * ld.value + n]
+        for (zz, yy, xx) in pts:
+            # a 3x3x3 window clamped inside the grid: an interior point is its centre; a point on
+            # the grid boundary sits on the window's edge, which is then the grid's own boundary
+            z0, y0, x0 = (min(max(v - 1, 0), size - 3) for v in (zz, yy, xx))
+            z1, y1, x1 = z0 + 3, y0 + 3, x0 + 3
+            sub = (3, 3, 3)
+            ids = (np.arange(z0, z1)[:, None, None] * size * size + np.arange(y0, y1)[None, :, None] * size
+                   + np.arange(x0, x1)[None, None, :]).reshape(-1)
+            xs = (PX[torch.as_tensor(ids, device="cuda")] * scale[q]).cpu().numpy()
+            # a window that touches the grid boundary keeps the Dirichlet side; an interior window
+            # edge is only reached by points other than the centre
+            hsub = 1.0 / (np.array(sub, dtype=float) + 1)
+            dt = prob.op.dt * (hsub[0] / hfull) ** 2
+            spec = inputs.OperatorSpec(3, prob.op.kind, sub, dt,
+                                       field=kap[z0:z1, y0:y1, x0:x1].reshape(-1).copy())
+            ys = orc.matvec(spec, xs)
+            cz, cy, cx = zz - z0, yy - y0, xx - x0
+            c = (cz * sub[1] + cy) * sub[0] + cx
+            gi = (zz * size + yy) * size + xx
+            ref = ys[c]
+            got = PY[gi].item() * scale[q]
+            mag = np.abs(xs).max() * (1 + 12 * dt / hsub[0] ** 2 * kap.max())
+            assert abs(got - ref) <= 64 * U * mag, (q, zz, yy, xx, got, ref)
+    ctx.close()
+    del ctx, u
+    _free(torch)
