@@ -31,7 +31,10 @@
 namespace psp {
 namespace {
 
-constexpr int kChunk = 512;      // factor: rows per thread
+#ifndef PSP_FACTOR_CHUNK
+#define PSP_FACTOR_CHUNK 512
+#endif
+constexpr int kChunk = PSP_FACTOR_CHUNK;   // factor: rows per thread
 constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
 constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four rows)
 // solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks (4 per SM: more
