@@ -68,6 +68,8 @@ struct psp_ctx {
   psp_status sticky = PSP_OK;
   int64_t launches = 0;
   int last_k = 0;
+  int combined_k = 0;      // the last step of this ring cycle already formed X0 + Z0, Z1 (krylov.cu)
+  int combined_slot = -1;  // ring slot whose P_x / P_y columns hold them
   cudaEvent_t ev[6] = {};
   // per-kernel-class event timing (opts.timing >= 2)
   struct KRec {
@@ -783,6 +785,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
     }
   }
   c->last_k = 0;
+  c->combined_k = 0;
   return check_cuda(c, "psp_cycle_begin");
 }
 
@@ -815,12 +818,24 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
         PSP_TRY(ring_split_step(c, k, slot, dst));
       }
     } else {
-      // the last step of the cycle: only H(k+1,k) = ||U|| is needed (V(:,k+1) is never used)
+      // the last step of the cycle: only H(k+1,k) = ||U|| is needed (V(:,k+1) is never used).
+      // With N = I it is fused with the cycle's combine (Z = Z0 + y_k Z1, krylov.cu): one pass
+      // over the basis forms ||U||, X0 + Z0 and Z1 into the free ring slot's columns
       h = kt_begin(c);
-      launch_icwy_update(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds,
-                         c->rc, c->stream);
-      kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
-      c->launches += 1;
+      if (c->n_identity && c->opts.fused) {
+        const int spare = ring_peek(c);
+        launch_update_combine(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->X0, px_col(c, spare),
+                              py_col(c, spare), k, c->nA, n, c->ds, c->rc, c->stream);
+        c->combined_k = k;
+        c->combined_slot = spare;
+        kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 4) * dn);
+        c->launches += 2;
+      } else {
+        launch_icwy_update(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds,
+                           c->rc, c->stream);
+        kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
+        c->launches += 1;
+      }
     }
     c->launches += 1;
   } else {
@@ -887,7 +902,14 @@ psp_status psp_cycle_end(psp_ctx* c, int k, double* x) {
     return check_cuda(c, "psp_cycle_end");
   }
   // l.38-42: Q = H^{-1}G; Z = sum Q_j V_j; X = X0 + N^{-1} Z
-  if (c->n_identity) {
+  if (c->cycle_fused && c->combined_k == k && k == c->nA) {
+    // the last step already formed X0 + Z0 and Z1: X = (X0 + Z0) + y_k Z1
+    int h = kt_begin(c);
+    launch_combine_finish(px_col(c, c->combined_slot), py_col(c, c->combined_slot), c->X0, c->n, c->ds,
+                          c->stream);
+    kt_end(c, h, PSP_KC_COMBINE, 24.0 * (double)c->n);
+    c->launches += 1;
+  } else if (c->n_identity) {
     int h = kt_begin(c);
     launch_combine(basis(c), k, c->nA, c->X0, c->X0, c->n, c->ds, c->stream);
     kt_end(c, h, PSP_KC_COMBINE, 8.0 * (k + 2) * (double)c->n);

@@ -125,6 +125,11 @@ void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, i
 // (EPI_HYB, with the fused pass's sums in ds.rpart)
 void launch_icwy_dots_hyb(Basis V, const double* w, const double* u, int J, int k, int nA, int64_t n,
                           DevState ds, const RedCfg& rc, cudaStream_t s);
+// the last step of a full ring cycle fused with the combine (krylov.cu): ||U_k|| + Givens,
+// z0 = x0 + Z0, z1 = Z1 (Z = Z0 + y_k Z1), then x = z0 + y_k z1 at the cycle end
+void launch_update_combine(Basis V, const double* w, const double* ws, const double* x0, double* z0, double* z1,
+                           int k, int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
+void launch_combine_finish(const double* z0, const double* z1, double* x, int64_t n, DevState ds, cudaStream_t s);
 // Q = H^{-1} G (R6) and out = base + sum_j Q_j V_j; base may be NULL (Z only)
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s);

@@ -492,6 +492,171 @@ __global__ void __launch_bounds__(TPB) combine_kernel(Basis V, int k, int nA, co
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// The last step of a full ring cycle (k = n_A, N = I) fused with the cycle's combine (l.38-43).
+// The least-squares solution of the cycle is R y = g (R the rotated H).  Before the last Givens
+// rotation is known (it needs ||U_k||), y is already fixed up to its last entry:
+// y_{1:k-1} = a - y_k b, a = R_{k-1}^{-1} g'_{1:k-1}, b = R_{k-1}^{-1} h'_{1:k-1} (h' = column k
+// after rotations 1..k-1; rows 1..k-1 of column k are untouched by rotation k).  So
+// Z = sum_j y_j V_j = Z0 + y_k Z1 with Z0 = sum_{j<k} a_j V_j, Z1 = V_k - sum_{j<k} b_j V_j, and
+// one pass over the basis forms U_k (its norm), X0 + Z0 and Z1 together; the cycle end is
+// then X = (X0 + Z0) + y_k Z1.  Equal to Q = H^{-1}G (R6) and the combine in exact arithmetic.
+// ------------------------------------------------------------------------------------------
+__global__ void combine_prep_kernel(DevState ds, int k, int nA) {
+  // one thread: c0_j = a_j alpha_j, c1_j = -b_j alpha_j (j < k-1), c1_{k-1} = alpha_{k-1} into
+  // ds.rpart[0, k) / [k, 2k); rpart[2k] = 1 on a zero pivot of R_{k-1} (R6)
+  const int ld = nA + 1;
+  double hp[kMaxRestart], a[kMaxRestart], b[kMaxRestart];
+  const double* Hk = ds.H + (int64_t)(k - 1) * ld;   // column k, MGS coefficients (unrotated)
+  for (int j = 0; j <= k; ++j) hp[j] = Hk[j];
+  for (int j = 1; j <= k - 1; ++j) {                 // rotations 1..k-1 (as givens_update)
+    const double delta = hp[j - 1];
+    hp[j - 1] = delta * ds.C[j - 1] + ds.S[j - 1] * hp[j];
+    hp[j] = -delta * ds.S[j - 1] + ds.C[j - 1] * hp[j];
+  }
+  int bad = 0;
+  for (int j = k - 1; j >= 1; --j) {                 // back-substitution on R_{k-1}
+    double sa = ds.G[j - 1], sb = hp[j - 1];
+    for (int t = j + 1; t <= k - 1; ++t) {
+      const double r = ds.H[(int64_t)(t - 1) * ld + (j - 1)];
+      sa -= r * a[t - 1];
+      sb -= r * b[t - 1];
+    }
+    const double piv = ds.H[(int64_t)(j - 1) * ld + (j - 1)];
+    if (piv == 0.0) { bad = 1; a[j - 1] = b[j - 1] = 0.0; continue; }
+    a[j - 1] = sa / piv;
+    b[j - 1] = sb / piv;
+  }
+  for (int j = 0; j < k - 1; ++j) {
+    ds.rpart[j] = a[j] * ds.alpha[j];
+    ds.rpart[k + j] = -b[j] * ds.alpha[j];
+  }
+  ds.rpart[k - 1] = 0.0;
+  ds.rpart[2 * k - 1] = ds.alpha[k - 1];
+  ds.rpart[2 * k] = bad ? 1.0 : 0.0;
+}
+
+constexpr int CRPT = 4;                               // rows per thread (register tile)
+constexpr int CTILE = TPB * CRPT;
+
+template <bool FULL>
+__device__ __forceinline__ void update_combine_tile(const double* const* cp, const double* w, double wsc,
+                                                    const double* x0, double* z0, double* z1,
+                                                    const double* hs, const double* c0, const double* c1,
+                                                    int k, int64_t n, int64_t r0, double& acc) {
+  double u[CRPT], p[CRPT], q[CRPT];
+#pragma unroll
+  for (int i = 0; i < CRPT; ++i) {
+    const int64_t r = r0 + (int64_t)TPB * i;
+    const bool in = FULL || r < n;
+    u[i] = in ? wsc * w[r] : 0.0;
+    p[i] = in ? x0[r] : 0.0;
+    q[i] = 0.0;
+  }
+  constexpr int CJ = 4;                               // columns per chunk: 16 loads in flight
+  int jb = 0;
+  for (; jb + CJ <= k; jb += CJ) {
+    double v[CJ][CRPT];
+#pragma unroll
+    for (int c = 0; c < CJ; ++c)
+#pragma unroll
+      for (int i = 0; i < CRPT; ++i) {
+        const int64_t r = r0 + (int64_t)TPB * i;
+        v[c][i] = (FULL || r < n) ? cp[jb + c][r] : 0.0;
+      }
+#pragma unroll
+    for (int c = 0; c < CJ; ++c) {
+      const double hj = hs[jb + c], aj = c0[jb + c], bj = c1[jb + c];
+#pragma unroll
+      for (int i = 0; i < CRPT; ++i) {
+        u[i] = fma(-hj, v[c][i], u[i]);
+        p[i] = fma(aj, v[c][i], p[i]);
+        q[i] = fma(bj, v[c][i], q[i]);
+      }
+    }
+  }
+  for (; jb < k; ++jb) {
+    double v[CRPT];
+#pragma unroll
+    for (int i = 0; i < CRPT; ++i) {
+      const int64_t r = r0 + (int64_t)TPB * i;
+      v[i] = (FULL || r < n) ? cp[jb][r] : 0.0;
+    }
+    const double hj = hs[jb], aj = c0[jb], bj = c1[jb];
+#pragma unroll
+    for (int i = 0; i < CRPT; ++i) {
+      u[i] = fma(-hj, v[i], u[i]);
+      p[i] = fma(aj, v[i], p[i]);
+      q[i] = fma(bj, v[i], q[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CRPT; ++i) {
+    const int64_t r = r0 + (int64_t)TPB * i;
+    if (FULL || r < n) {
+      z0[r] = p[i];
+      z1[r] = q[i];
+      acc = fma(u[i], u[i], acc);
+    }
+  }
+}
+
+// U_k = alpha_k w~_k - sum_j h_j alpha_j V_j (only ||U_k|| is kept), z0 = X0 + Z0, z1 = Z1; the
+// last block: H(k+1,k), Givens (l.17-32), then Q = H^{-1}G (R6) with y_k -> ds.scal[SC_TMP].
+__global__ void __launch_bounds__(TPB) update_combine_kernel(Basis V, const double* __restrict__ w,
+                                                             const double* ws, const double* __restrict__ x0,
+                                                             double* __restrict__ z0, double* __restrict__ z1,
+                                                             int k, int nA, int64_t n, DevState ds) {
+  __shared__ double hs[kMaxRestart], c0[kMaxRestart], c1[kMaxRestart];
+  __shared__ double sm[kWarps];
+  __shared__ const double* cp[kMaxRestart + 1];
+  const int ld = nA + 1, t = threadIdx.x;
+  for (int q = t; q < k; q += TPB) {
+    hs[q] = ds.H[(int64_t)(k - 1) * ld + q] * ds.alpha[q];
+    c0[q] = ds.rpart[q];
+    c1[q] = ds.rpart[k + q];
+    cp[q] = V.col(q);
+  }
+  __syncthreads();
+  const double wsc = ws ? *ws : 1.0;
+  double a[1] = {0.0};
+  const int64_t ntiles = (n + CTILE - 1) / CTILE;
+  const int64_t nfull = n / CTILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * CTILE + t;
+    if (tile < nfull) update_combine_tile<true>(cp, w, wsc, x0, z0, z1, hs, c0, c1, k, n, r0, a[0]);
+    else update_combine_tile<false>(cp, w, wsc, x0, z0, z1, hs, c0, c1, k, n, r0, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (t == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double tt = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (t == 0) {
+      epilogue(EPI_UPDATE, ds, k, nA, 0, 0, &tt);     // H(k+1,k) = ||U||, Givens of column k
+      // Q = H^{-1} G (R6), as combine_kernel
+      int bad = ds.rpart[2 * k] != 0.0;
+      for (int j = k; j >= 1; --j) {
+        double sv = ds.G[j - 1];
+        for (int q = j + 1; q <= k; ++q) sv -= ds.H[(int64_t)(q - 1) * ld + (j - 1)] * ds.Q[q - 1];
+        const double piv = ds.H[(int64_t)(j - 1) * ld + (j - 1)];
+        if (piv == 0.0) { bad = 1; ds.Q[j - 1] = 0.0; continue; }
+        ds.Q[j - 1] = sv / piv;
+      }
+      ds.scal[SC_TMP] = ds.Q[k - 1];                  // y_k
+      ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
+    }
+  }
+}
+
+// cycle end after update_combine_kernel: x = z0 + y_k z1
+__global__ void __launch_bounds__(TPB) combine_finish_kernel(const double* __restrict__ z0,
+                                                             const double* __restrict__ z1, double* __restrict__ x,
+                                                             int64_t n, DevState ds) {
+  const double yk = ds.scal[SC_TMP];
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB)
+    x[r] = fma(yk, z1[r], z0[r]);
+}
+
 inline int grid_for(int64_t n, int cap) {
   int64_t b = (n + TPB - 1) / TPB;
   if (b > cap) b = cap;
@@ -565,6 +730,20 @@ void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, i
 }
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s) {
   epilogue_kernel<<<1, 1, 0, s>>>(kind, ds, k, nA, j, slot);
+}
+void launch_update_combine(Basis V, const double* w, const double* ws, const double* x0, double* z0, double* z1,
+                           int k, int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
+  combine_prep_kernel<<<1, 1, 0, s>>>(ds, k, nA);
+  static int wave = 0;
+  if (!wave) wave = wave_blocks(update_combine_kernel, rc.nblocks);
+  int64_t ub = (n + CTILE - 1) / CTILE;
+  if (ub > wave) ub = wave;
+  update_combine_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, x0, z0, z1, k, nA, n, ds);
+}
+void launch_combine_finish(const double* z0, const double* z1, double* x, int64_t n, DevState ds, cudaStream_t s) {
+  int64_t b = (n + TPB - 1) / TPB;
+  if (b > 148 * 8) b = 148 * 8;
+  combine_finish_kernel<<<(int)(b < 1 ? 1 : b), TPB, 0, s>>>(z0, z1, x, n, ds);
 }
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {
