@@ -668,7 +668,8 @@ psp_status psp_precond_apply(psp_ctx* c, const double* v, double* z) {
 // step k of a ring-resident cycle as one fused pass (update + matvec + dots) or as separate
 // passes: the policy of opts.fused_kmin / fused_kmax
 static bool fused_pass(const psp_ctx* c, int k) {
-  return k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, c->nA);
+  // (the pass streams k basis columns: the restart length itself may exceed the fused kernel's 32)
+  return k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, k);
 }
 
 static double fused_bytes(const psp_ctx* c, int k);
@@ -678,7 +679,7 @@ static double fused_bytes(const psp_ctx* c, int k);
 // pass (both stream those columns once each, with no stencil halo)
 static bool hyb_pass(const psp_ctx* c, int k) {
   const int kb = c->opts.fused_split_cols;
-  return kb > 0 && kb <= 16 && k > c->opts.fused_kmax && k - kb >= 1 && fused_supported(c->st, c->nA);
+  return kb > 0 && kb <= 16 && k > c->opts.fused_kmax && k - kb >= 1 && fused_supported(c->st, kb);
 }
 
 // Step k as three passes over the ring: [A] u' = alpha_k w~_k - sum_{j<J} h_j alpha_j V(:,j) into
