@@ -90,7 +90,8 @@ typedef struct {
                                    /* fused_kmin <= k <= fused_kmax as one fused pass         */
                                    /* (update + matvec + dots, DESIGN.md s.6), the other      */
                                    /* steps as update / matvec / dots passes on the ring;     */
-                                   /* default 1                                               */
+                                   /* 1 (default): fused passes from 2^21 rows on (below,     */
+                                   /* their per-plane cost dominates); 2: at any size         */
   int32_t fused_kmin;              /* first step run as a fused pass; default 2               */
   int32_t fused_kmax;              /* last step run as a fused pass; default 16 (wider steps  */
                                    /* hold more basis tiles than shared memory stages well)   */

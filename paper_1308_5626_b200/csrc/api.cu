@@ -667,9 +667,15 @@ psp_status psp_precond_apply(psp_ctx* c, const double* v, double* z) {
 
 // step k of a ring-resident cycle as one fused pass (update + matvec + dots) or as separate
 // passes: the policy of opts.fused_kmin / fused_kmax
+// the fused kernels pay per tile plane, not per byte, below a few million rows (C2, 512^2: a
+// step 9.9 ms with split passes, 45 ms fused; C3, 2048^2: 336 -> 292 ms fused): opts.fused = 1
+// uses them from kFusedMinRows rows on, opts.fused = 2 always (the parity tests' small cases)
+constexpr int64_t kFusedMinRows = (int64_t)1 << 21;
+static bool fused_big(const psp_ctx* c) { return c->opts.fused >= 2 || c->n >= kFusedMinRows; }
+
 static bool fused_pass(const psp_ctx* c, int k) {
   // (the pass streams k basis columns: the restart length itself may exceed the fused kernel's 32)
-  return k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, k);
+  return fused_big(c) && k >= c->opts.fused_kmin && k <= c->opts.fused_kmax && fused_supported(c->st, k);
 }
 
 static double fused_bytes(const psp_ctx* c, int k);
@@ -679,7 +685,7 @@ static double fused_bytes(const psp_ctx* c, int k);
 // pass (both stream those columns once each, with no stencil halo)
 static bool hyb_pass(const psp_ctx* c, int k) {
   const int kb = c->opts.fused_split_cols;
-  return kb > 0 && kb <= 16 && k > c->opts.fused_kmax && k - kb >= 1 && fused_supported(c->st, kb);
+  return fused_big(c) && kb > 0 && kb <= 16 && k > c->opts.fused_kmax && k - kb >= 1 && fused_supported(c->st, kb);
 }
 
 // Step k as three passes over the ring: [A] u' = alpha_k w~_k - sum_{j<J} h_j alpha_j V(:,j) into

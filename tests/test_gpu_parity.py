@@ -232,11 +232,12 @@ def test_mrep_insufficient_samples(torch, P):
 # ------------------------------------------------------------------------------------------
 # T4-T6: Algorithm 1 and the time-step driver
 # ------------------------------------------------------------------------------------------
-MODES = {"fused": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=32),      # every step one fused pass
-         "ring": dict(ortho=0, fused=1),                                      # default mix on the ring
+MODES = {"fused": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=32),      # every step one fused pass
+         "ring": dict(ortho=0, fused=2),                                      # default mix, forced at small n
          # split-column steps (update + fused over the newest columns + dots) from k = 3 / k = 13
-         "hybrid": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=2, fused_split_cols=2),
-         "hybrid12": dict(ortho=0, fused=1, fused_kmin=0, fused_kmax=12, fused_split_cols=12),
+         "hybrid": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=2, fused_split_cols=2),
+         "hybrid12": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=12, fused_split_cols=12),
+         "ringauto": dict(ortho=0, fused=1),                                  # default options (small n: split)
          "ringsplit": dict(ortho=0, fused=1, fused_kmin=99, fused_kmax=0),   # ring, no fused pass
          "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
 
@@ -374,7 +375,7 @@ def test_free_running_c1(torch, P, orc, mode):
     g["ctx"].close()
 
 
-@pytest.mark.parametrize("fused", [1, 0], ids=["fused", "split"])
+@pytest.mark.parametrize("fused", [2, 0], ids=["fused", "split"])
 def test_arnoldi_cycle_invariants(torch, P, orc, fused):
     # one cycle through the step-level ABI: Hessenberg vs oracle trace; V orthonormal;
     # Arnoldi relation on the recorded probes (P_y(:,i_k) = V_{k+1} Hbar(:,k))
