@@ -37,13 +37,13 @@ namespace {
 constexpr int kChunk = PSP_FACTOR_CHUNK;   // factor: rows per thread
 constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
 constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four rows)
-// solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks (4 per SM: more
-// independent tiles in flight) for d >= 3 (measured n = 2^26: d = 3 2.34 -> 2.04 ms, d = 4
-// 4.25 -> 3.90 ms; d = 1 prefers 256)
+// solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks for d >= 3, 4 per SM
+// at d = 3 and 3 per SM at d = 4 (more independent tiles in flight; measured n = 2^26: d = 3
+// 2.34 -> 2.04 ms, d = 4 4.25 -> 3.65 ms; d = 1 prefers 256)
 template <int D>
 struct SW {
   static constexpr int TPB = D >= 3 ? 128 : 256;
-  static constexpr int MINB = D >= 3 ? 4 : 2;
+  static constexpr int MINB = D >= 4 ? 3 : (D == 3 ? 4 : 2);   // d = 4: 3 blocks (168 registers) spill less
   static constexpr int TILE = TPB * 8;
 };
 constexpr int STPB = 128;        // solve: the smallest block (host-side sizing of per-tile arrays)
