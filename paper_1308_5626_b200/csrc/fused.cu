@@ -120,7 +120,7 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int x, i
       : "memory");
 }
 
-template <int TX, int TY, int KMAX, int CS>
+template <int TX, int TY, int KMAX, int CS, int PP = 1>
 struct FCfg {
   static constexpr int NT = TX * TY;
   static constexpr int NUB = 4;                              // u (and kappa) plane ring depth
@@ -128,7 +128,7 @@ struct FCfg {
   // is released as soon as u is formed (all but one stage in flight; the plane's kappa moves to
   // a kappa plane ring beside the u ring); wider thread column sets (KJ = 16) do not fit the
   // 128-register budget and keep the stage for the t_j and the stencil's kappa instead
-  static constexpr bool RV = KMAX / CS <= 12 || (KMAX / CS <= 16 && NT * CS + 32 <= 384);
+  static constexpr bool RV = KMAX / CS <= 12 || (KMAX / CS <= 16 && NT * CS / PP + 32 <= 384);
   static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
   static constexpr int STAGE = NB * NT;                      // doubles
   static constexpr int RING = (RV ? 2 : 1) * NUB * NT;       // u (+ kappa) plane rings, doubles
@@ -168,16 +168,17 @@ __device__ __forceinline__ double butterfly8_half(double (&v)[8], int lane) {
 // through a 4-deep ring of shared-memory planes, each with an mbarrier the compute warps arrive
 // on when they have written it (4 deep: a warp overwriting a plane buffer has already seen
 // every warp's write of the plane two after the one last read from it).
-template <int KIND, int TX, int TY, int KMAX, int CS>
-__global__ void __launch_bounds__(TX * TY * CS + 32, 1)
+template <int KIND, int TX, int TY, int KMAX, int CS, int PP>
+__global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap mpx, const __grid_constant__ CUtensorMap mpy,
                      const __grid_constant__ CUtensorMap mkap, const __grid_constant__ CUtensorMap msrc,
                      FusedArgs a) {
-  using Cfg = FCfg<TX, TY, KMAX, CS>;
+  using Cfg = FCfg<TX, TY, KMAX, CS, PP>;
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
   constexpr bool HASY = TY > 1;
   constexpr int NT = Cfg::NT, NST = Cfg::NST;      // NT points per tile
-  constexpr int NC = NT * CS, NWC = NC / 32;        // compute threads / warps
+  constexpr int NC = NT * CS / PP, NWC = NC / 32;   // compute threads / warps (PP points a thread)
+  constexpr int PSTR = NT / PP;                     // a thread's points: pt, pt + PSTR, ...
   constexpr int NTH = NC + 32, NW = NWC + 1;        // + the producer warp
   constexpr int NUB = Cfg::NUB;
   constexpr int KJ = KMAX / CS;                     // basis columns per thread
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
   constexpr int NACC = REG ? KJ : NCH;
   constexpr bool RV = Cfg::RV;
   static_assert(CS == 1 || CS == 2, "column split 1 or 2");
+  static_assert(PP == 1 || (PP == 2 && CS == 1 && NT % 64 == 0), "two points a thread: CS = 1, whole warps");
   static_assert(NC % 32 == 0, "whole compute warps");
   extern __shared__ __align__(128) double fsm[];
   // 128-byte aligned stage base by index arithmetic on the shared array (stays in .shared)
@@ -206,7 +208,6 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
   // this thread's point and column half (the producer warp aliases points 0..31: unused)
   const int half = (CS == 2) ? (lane >> 4) : 0;
   const int pt = producer ? lane : ((CS == 2) ? warp * 16 + (lane & 15) : t);
-  const int lx = pt % TX, ly = pt / TX;
   const int j0 = half * KJ;
   const int k = a.k;
   const int kc = k - a.jb;                       // basis columns of this pass
@@ -218,7 +219,8 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
   // columns j >= k are never loaded: zero them once in every stage (coefficient 0, product 0)
   if (!producer && half == 0)
     for (int s = 0; s < NST; ++s)
-      for (int j = kc; j < KMAX; ++j) stages[(size_t)s * Cfg::STAGE + j * NT + pt] = 0.0;
+      for (int j = kc; j < KMAX; ++j)
+        for (int i = 0; i < PP; ++i) stages[(size_t)s * Cfg::STAGE + j * NT + pt + i * PSTR] = 0.0;
   if (t == 0) {
     for (int q = 0; q < NST; ++q) {
       mbar_init(full + q, 1);
@@ -283,17 +285,18 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
     uint32_t us = 0;                             // running u-plane count (ring slot us % NUB)
 
     // products of this thread's columns with f (f = 0 for points that are not counted)
-    auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, double f, double (&acc)[NACC]) {
+    auto add_products = [&](const double* vcol /* stage base; column j at j*NT */, int q, double f,
+                            double (&acc)[NACC]) {
       if (REG) {
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) acc[j] = fma(vcol[(j0 + j) * NT + pt], f, acc[j]);
+        for (int j = 0; j < KJ; ++j) acc[j] = fma(vcol[(j0 + j) * NT + q], f, acc[j]);
       } else {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           if (c * 8 >= kc) break;                  // uniform
           double v8[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v8[q] = vcol[(j0 + c * 8 + q) * NT + pt] * f;
+          for (int qq = 0; qq < 8; ++qq) v8[qq] = vcol[(j0 + c * 8 + qq) * NT + q] * f;
           acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
         }
       }
@@ -307,10 +310,13 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + (g % NST))) : "memory");
     };
-    auto publish_u = [&](uint32_t g, double v, double kv) {  // u (+ kappa) of plane g -> ring slot, signal
+    auto publish_u = [&](uint32_t g, const double (&v)[PP], const double (&kv)[PP]) {  // u (+ kappa) of plane g
       if (half == 0) {
-        Us[(g % NUB) * NT + pt] = v;
-        if (RV && cell) Ks[(g % NUB) * NT + pt] = kv;
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+          Us[(g % NUB) * NT + pt + i * PSTR] = v[i];
+          if (RV && cell) Ks[(g % NUB) * NT + pt + i * PSTR] = kv[i];
+        }
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(ubar + (g % NUB))) : "memory");
@@ -330,21 +336,33 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       const int x0 = (int)(txi * (TX - 4)) - 2, y0 = HASY ? (int)(tyi * (TY - 2)) - 1 : 0;
       const int64_t z0 = zci * a.zchunk;
       const int64_t z1 = (z0 + a.zchunk < st.nz) ? z0 + a.zchunk : st.nz;
-      const int64_t gx = x0 + lx, gy = y0 + ly;
-      const bool interior = lx >= 2 && lx <= TX - 3 && (!HASY || (ly >= 1 && ly <= TY - 2));
-      const bool in_grid = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
-      const bool own = interior && in_grid;
-      const bool emit = own && half == 0;        // stores and the u / w~ scalars: one thread per point
-      const int64_t col = in_grid ? gx + st.nx * gy : 0;
-      const bool nb_w = gx > 0, nb_e = gx + 1 < st.nx, nb_s = gy > 0, nb_n = gy + 1 < st.ny;
+      // this thread's points
+      int ptv[PP];
+      bool in_grid[PP], own[PP], emit[PP], nb_w[PP], nb_e[PP], nb_s[PP], nb_n[PP];
+      int64_t col[PP];
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        ptv[i] = pt + i * PSTR;
+        const int lxi = ptv[i] % TX, lyi = ptv[i] / TX;
+        const int64_t gx = x0 + lxi, gy = y0 + lyi;
+        const bool interior = lxi >= 2 && lxi <= TX - 3 && (!HASY || (lyi >= 1 && lyi <= TY - 2));
+        in_grid[i] = gx >= 0 && gx < st.nx && gy >= 0 && gy < st.ny;
+        own[i] = interior && in_grid[i];
+        emit[i] = own[i] && half == 0;           // stores and the u / w~ scalars: one thread per point
+        col[i] = in_grid[i] ? gx + st.nx * gy : 0;
+        nb_w[i] = gx > 0;
+        nb_e[i] = gx + 1 < st.nx;
+        nb_s[i] = gy > 0;
+        nb_n[i] = gy + 1 < st.ny;
+      }
 
-      // u at this point of the staged plane (MGS update of step k, ICWY form)
-      auto form_u = [&](const double* sb) -> double {
-        const double s0 = sb[KMAX * NT + pt];
+      // u at point q of the staged plane (MGS update of step k, ICWY form)
+      auto form_u = [&](const double* sb, int q) -> double {
+        const double s0 = sb[KMAX * NT + q];
         if (k == 0) return s0;
         double u = (half == 0) ? wsc * s0 : 0.0;
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) u = fma(HREG ? hr[j] : -hs[j0 + j], sb[(j0 + j) * NT + pt], u);
+        for (int j = 0; j < KJ; ++j) u = fma(HREG ? hr[j] : -hs[j0 + j], sb[(j0 + j) * NT + q], u);
         if (CS == 2) {                           // the halves' partial updates, same sum on both
           const double o = __shfl_xor_sync(0xffffffffu, u, 16);
           u = (half == 0) ? u + o : o + u;
@@ -353,9 +371,9 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
       };
       // this thread's basis values of a staged plane -> registers (the plane's l_j products now,
       // its t_j products one plane later, after which the stage is long released)
-      auto load_vr = [&](const double* sb, double (&vr)[KJ]) {
+      auto load_vr = [&](const double* sb, int q, double (&vr)[KJ]) {
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) vr[j] = sb[(j0 + j) * NT + pt];
+        for (int j = 0; j < KJ; ++j) vr[j] = sb[(j0 + j) * NT + q];
       };
       auto add_products_r = [&](const double (&vr)[KJ], double f, double (&acc)[NACC]) {
         if (REG) {
@@ -367,39 +385,49 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
             if (c * 8 >= kc) break;              // uniform
             double v8[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v8[q] = vr[c * 8 + q] * f;
+            for (int qq = 0; qq < 8; ++qq) v8[qq] = vr[c * 8 + qq] * f;
             acc[c] += (CS == 2) ? butterfly8_half(v8, lane) : butterfly8(v8, lane);
           }
         }
       };
       // prologue: u(z0-1) (stage released at once), u(z0) (+ l-products of plane z0)
-      double vr[KJ];
+      double vr[PP][KJ];
+      double ub[PP], kb[PP], uc[PP], kc_[PP];
+      double* ox[PP];
+      double* oy[PP];
       const uint32_t gb = gs;                    // stage count of plane z0-1
       const double* sbm = acquire(gb);
-      double ub = form_u(sbm);
-      double kb = cell ? sbm[(KMAX + 1) * NT + pt] : 0.0;
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        ub[i] = form_u(sbm, ptv[i]);
+        kb[i] = cell ? sbm[(KMAX + 1) * NT + ptv[i]] : 0.0;
+        if (!(z0 >= 1 && in_grid[i])) ub[i] = 0.0;
+      }
       release(gb);
-      if (!(z0 >= 1 && in_grid)) ub = 0.0;
-      int64_t g = col + plane * z0;              // this point's index at plane p
-      double* ox = a.dstx + g;                   // this point's outputs at plane p
-      double* oy = a.dsty + g;
       const double* sbc = acquire(gb + 1);
-      double uc = form_u(sbc);
-      if (!in_grid) uc = 0.0;
-      double kc = cell ? sbc[(KMAX + 1) * NT + pt] : 0.0;
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        const int64_t g = col[i] + plane * z0;   // this point's index at plane z0
+        ox[i] = a.dstx + g;
+        oy[i] = a.dsty + g;
+        uc[i] = form_u(sbc, ptv[i]);
+        if (!in_grid[i]) uc[i] = 0.0;
+        kc_[i] = cell ? sbc[(KMAX + 1) * NT + ptv[i]] : 0.0;
+      }
       const uint32_t ub0 = us;                   // u-plane count of plane z0
-      publish_u(ub0, uc, kc);
-      if (RV && k > 0) load_vr(sbc, vr);
-      if (RV) release(gb + 1);
-      if (emit && k > 0) *ox = uc;
-      {
-        const double f = own ? uc : 0.0;
+      publish_u(ub0, uc, kc_);
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        if (RV && k > 0) load_vr(sbc, ptv[i], vr[i]);
+        if (emit[i] && k > 0) *ox[i] = uc[i];
+        const double f = own[i] ? uc[i] : 0.0;
         if (half == 0) nu = fma(f, f, nu);
         if (k > 0) {
-          if (RV) add_products_r(vr, f, accl);
-          else add_products(sbc, f, accl);
+          if (RV) add_products_r(vr[i], f, accl);
+          else add_products(sbc, ptv[i], f, accl);
         }
       }
+      if (RV) release(gb + 1);
 
       for (int64_t p = z0; p < z1; ++p) {
         const uint32_t gp = gb + 1 + (uint32_t)(p - z0);   // stage of plane p
@@ -407,67 +435,84 @@ __global__ void __launch_bounds__(TX * TY * CS + 32, 1)
         const int64_t pn = p + 1;
         // u(p+1) from stage p+1 (plane z1, the halo above the chunk, is staged too)
         const double* sn = acquire(gp + 1);
-        double un = form_u(sn);
-        if (!(pn < st.nz && in_grid)) un = 0.0;
-        const double kt = cell ? sn[(KMAX + 1) * NT + pt] : 0.0;
+        double un[PP], kt[PP];
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+          un[i] = form_u(sn, ptv[i]);
+          if (!(pn < st.nz && in_grid[i])) un[i] = 0.0;
+          kt[i] = cell ? sn[(KMAX + 1) * NT + ptv[i]] : 0.0;
+        }
         if (pn < z1) publish_u(up + 1, un, kt);  // the stencil of plane p+1 needs them
         // w~ = A u at plane p (both halves compute it; the first one stores it)
         const double* Up = await_u(up);
-        double w = 0.0;
-        if (own) {
-          const double c0 = uc;
-          double acc = 0.0;
-          // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
-          // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
-          const double* Kp = RV ? Ks + (up % NUB) * NT : stages + (size_t)(gp % NST) * Cfg::STAGE + (KMAX + 1) * NT;
-          auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
-            const double kf = cell ? hsv * (kc + (nin ? fn : kc)) : s;
-            acc = fma(kf, c0 - xn, acc);
-          };
-          const double xw = Up[pt - 1], xe = Up[pt + 1];
-          face(xw, cell ? Kp[pt - 1] : 0.0, nb_w, st.s[0], hsx);
-          face(xe, cell ? Kp[pt + 1] : 0.0, nb_e, st.s[0], hsx);
-          if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
-          if (HASY) {
-            const double xs_ = Up[pt - TX], xn_ = Up[pt + TX];
-            face(xs_, cell ? Kp[pt - TX] : 0.0, nb_s, st.s[1], hsy);
-            face(xn_, cell ? Kp[pt + TX] : 0.0, nb_n, st.s[1], hsy);
-            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
-          }
-          if (st.nz > 1) {
-            const bool inb = p > 0, int_ = p + 1 < st.nz;
-            face(ub, kb, inb, st.s[2], hsz);
-            face(un, kt, int_, st.s[2], hsz);
-            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub, acc);
-          }
-          w = c0 + acc;
-          if (half == 0) {
-            *oy = w;
-            tu = fma(c0, w, tu);
+        const double* Kp = RV ? Ks + (up % NUB) * NT : stages + (size_t)(gp % NST) * Cfg::STAGE + (KMAX + 1) * NT;
+        double w[PP];
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+          w[i] = 0.0;
+          if (own[i]) {
+            const int q = ptv[i];
+            const double c0 = uc[i], kci = kc_[i];
+            double acc = 0.0;
+            // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
+            // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
+            auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
+              const double kf = cell ? hsv * (kci + (nin ? fn : kci)) : s;
+              acc = fma(kf, c0 - xn, acc);
+            };
+            const double xw = Up[q - 1], xe = Up[q + 1];
+            face(xw, cell ? Kp[q - 1] : 0.0, nb_w[i], st.s[0], hsx);
+            face(xe, cell ? Kp[q + 1] : 0.0, nb_e[i], st.s[0], hsx);
+            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
+            if (HASY) {
+              const double xs_ = Up[q - TX], xn_ = Up[q + TX];
+              face(xs_, cell ? Kp[q - TX] : 0.0, nb_s[i], st.s[1], hsy);
+              face(xn_, cell ? Kp[q + TX] : 0.0, nb_n[i], st.s[1], hsy);
+              if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
+            }
+            if (st.nz > 1) {
+              const bool inb = p > 0, int_ = p + 1 < st.nz;
+              face(ub[i], kb[i], inb, st.s[2], hsz);
+              face(un[i], kt[i], int_, st.s[2], hsz);
+              if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub[i], acc);
+            }
+            w[i] = c0 + acc;
+            if (half == 0) {
+              *oy[i] = w[i];
+              tu = fma(c0, w[i], tu);
+            }
           }
         }
         // t_j = V_j(p)' w~(p); w = 0 off emitted points
-        if (RV) {
-          if (k > 0) add_products_r(vr, w, acct);
-        } else {
-          if (k > 0) add_products(stages + (size_t)(gp % NST) * Cfg::STAGE, w, acct);
-          release(gp);                            // stage p done
-        }
-        if (pn < z1) {
-          if (RV && k > 0) load_vr(sn, vr);      // V(p+1): its l_j now, its t_j next plane
-          if (emit && k > 0) ox[plane] = un;
-          const double f = own ? un : 0.0;
-          if (half == 0) nu = fma(f, f, nu);
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
           if (k > 0) {
-            if (RV) add_products_r(vr, f, accl);
-            else add_products(sn, f, accl);
+            if (RV) add_products_r(vr[i], w[i], acct);
+            else add_products(stages + (size_t)(gp % NST) * Cfg::STAGE, ptv[i], w[i], acct);
+          }
+        }
+        if (!RV) release(gp);                     // stage p done
+        if (pn < z1) {
+#pragma unroll
+          for (int i = 0; i < PP; ++i) {
+            if (RV && k > 0) load_vr(sn, ptv[i], vr[i]);   // V(p+1): its l_j now, its t_j next plane
+            if (emit[i] && k > 0) ox[i][plane] = un[i];
+            const double f = own[i] ? un[i] : 0.0;
+            if (half == 0) nu = fma(f, f, nu);
+            if (k > 0) {
+              if (RV) add_products_r(vr[i], f, accl);
+              else add_products(sn, ptv[i], f, accl);
+            }
           }
         }
         if (RV || pn == z1) release(gp + 1);      // stage p+1 done (else: after its t_j)
-        ub = uc; uc = un;
-        kb = kc; kc = kt;
-        ox += plane;
-        oy += plane;
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+          ub[i] = uc[i]; uc[i] = un[i];
+          kb[i] = kc_[i]; kc_[i] = kt[i];
+          ox[i] += plane;
+          oy[i] += plane;
+        }
       }
       gs = gb + (uint32_t)(z1 - z0 + 2);          // planes z0-1 .. z1
       us = ub0 + (uint32_t)(z1 - z0);             // u planes z0 .. z1-1
@@ -614,9 +659,9 @@ struct MapCache {
   bool ok = false;
 };
 
-template <int KIND, int TX, int TY, int KMAX, int CS>
+template <int KIND, int TX, int TY, int KMAX, int CS, int PP = 1>
 int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
-  using Cfg = FCfg<TX, TY, KMAX, CS>;
+  using Cfg = FCfg<TX, TY, KMAX, CS, PP>;
   static MapCache mc;
   const Stencil& st = a.st;
   if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != st.field || mc.nx != st.nx ||
@@ -629,7 +674,7 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
     mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)Cfg::SMEM);
       attr = true;
     }
@@ -652,9 +697,9 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
     mc.src = a.src_vec;
   }
   if (a.src_px != 2 && mc.src == nullptr) mc.ms = mc.mpx;
-  auto kern = fused_tma_kernel<KIND, TX, TY, KMAX, CS>;
+  auto kern = fused_tma_kernel<KIND, TX, TY, KMAX, CS, PP>;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(TX * TY * CS + 32);         // compute warps + the TMA producer warp
+  cfg.blockDim = dim3(TX * TY * CS / PP + 32);    // compute warps + the TMA producer warp
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
   int64_t grid = 148;                              // one resident block per SM (persistent)
@@ -674,10 +719,12 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     if (kc <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
     if (kc <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
     if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
-    // k = 13..16: 32 x 11 tiles (12 warps, up to 168 registers) hold a thread's 16 basis
-    // values in registers, so a stage is released as soon as u is formed (32 x 15 tiles would
-    // keep two stages resident): 4.2-4.9 -> 4.0-4.5 ms at 512^3
-    if (kc <= 16) return launch_t<KIND, 32, 11, 16, 1>(a, rpx, rpy, s);
+    // k = 13..16: 32 x 14 tiles with two points a thread (8 compute warps, up to 255 registers)
+    // hold a thread's 16 basis values per point in registers, so a stage is released as soon as
+    // u is formed; one thread per point on 32 x 15 tiles would keep two stages resident, on
+    // 32 x 11 tiles (12 warps, 168 registers) carries more halo (cycle ~1.5 % slower); two
+    // points a thread for k <= 12 was slower (2.0 -> 2.6 ms at k = 2)
+    if (kc <= 16) return launch_t<KIND, 32, 14, 16, 1, 2>(a, rpx, rpy, s);
     if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
     return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, s);
   }
