@@ -305,6 +305,10 @@ LOCKSTEP_CASES = [
     ("C4-ragged", lambda: inputs.Problem("C4r", inputs.OperatorSpec(3, "cell_diff", (21, 17, 13), 1e-3 / 400,
                                                                      field=np.exp(np.random.default_rng(2).standard_normal(21 * 17 * 13))),
                                          np.random.default_rng(3).uniform(-1, 1, 21 * 17 * 13), 30, 1e-8, 3, 2, 32, 1000), 2),
+    # nx even (the fused passes need 16-byte TMA rows): partial tiles in x, y and z
+    ("C4-ragged-even", lambda: inputs.Problem("C4re", inputs.OperatorSpec(3, "cell_diff", (34, 19, 23), 1e-3 / 400,
+                                                                          field=np.exp(np.random.default_rng(5).standard_normal(34 * 19 * 23))),
+                                              np.random.default_rng(6).uniform(-1, 1, 34 * 19 * 23), 30, 1e-8, 3, 2, 32, 1000), 2),
 ]
 
 
