@@ -716,8 +716,11 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     // stage = (KMAX + 2) boxes: the narrowest instantiation that holds k columns keeps the most
     // planes in flight (measured at 512^3: k <= 4 1.9 vs 2.3 ms, k = 9..12 3.5-3.8 vs 3.8-4.1 ms).
     // 32 x 8 tiles for k <= 16 or 16 x 8 tiles for k > 16 were slower (more halo points per tile).
-    if (kc <= 4) return launch_t<KIND, 32, 15, 4, 1>(a, rpx, rpy, s);
-    if (kc <= 8) return launch_t<KIND, 32, 15, 8, 1>(a, rpx, rpy, s);
+    // k <= 8: two points a thread on the tallest tiles whose stage ring still holds three
+    // stages (32 x 30 at KMAX 4, 32 x 22 at KMAX 8): less halo work per point, same warps
+    // (k = 2: 2.1 -> 1.97 ms, k = 5..8: 2.8-2.9 -> 2.6 ms at 512^3)
+    if (kc <= 4) return launch_t<KIND, 32, 30, 4, 1, 2>(a, rpx, rpy, s);
+    if (kc <= 8) return launch_t<KIND, 32, 22, 8, 1, 2>(a, rpx, rpy, s);
     if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
     // k = 13..16: 32 x 14 tiles with two points a thread (8 compute warps, up to 255 registers)
     // hold a thread's 16 basis values per point in registers, so a stage is released as soon as
