@@ -2,7 +2,7 @@
 cycle_begin, then psp_arnoldi_step(k) for k = 1..restart, over a few cycles; prints the median
 ms per k.  Variants (KSTEP_VARIANTS="default,PSP_FUSED_TILE=1,...") set environment knobs read per launch.
 
-  python tools/kstep.py [size=512] [cycles=3] [fused_kmin=1] [fused_kmax=30] [fused_split_cols=12]
+  python tools/kstep.py [size=512] [cycles=3] [fused_kmin=1] [fused_kmax=30] [fused_split_cols=16]
 """
 import os
 import sys
@@ -17,7 +17,7 @@ size = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 kmin = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 kmax = int(sys.argv[4]) if len(sys.argv) > 4 else 30
-split_cols = int(sys.argv[5]) if len(sys.argv) > 5 else 12
+split_cols = int(sys.argv[5]) if len(sys.argv) > 5 else 16
 prob = inputs.c4(n=size, steps=1)
 s = torch.cuda.Stream()
 opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, fused=1, fused_kmin=kmin, fused_kmax=kmax,
