@@ -111,6 +111,19 @@ class Clocks:
         return out
 
 
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cpu": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(size, budget_s=20.0):
     """The oracle as it stands (single-threaded C, literal Alg.1) on a bounded sample of C4."""
     import numpy as np
@@ -135,7 +148,7 @@ def cpu_baseline(size, budget_s=20.0):
     n = prob.op.rows
     return {"value": n * iters / t, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"C4 recipe at {size}^3 (n={n}), first time step, {cycles} GMRES(30) cycle(s) "
-                      f"= {iters} iterations in {t:.1f} s, literal MGS, 1 host thread"}
+                      f"= {iters} iterations in {t:.1f} s, literal MGS, 1 host thread", **host_info()}
 
 
 def c5_point(log2n, m, d, peak):
@@ -218,7 +231,8 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "C4 (BASELINE configs[3]) sample", "grid": [size] * 3,
                                             "d": 3, "restart": 30, "tol": 1e-8},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0

@@ -125,6 +125,10 @@ typedef struct {
   double t_solve_ms, t_mrep_ms, t_factor_ms;   /* CUDA-event times (opts.timing)           */
   double* h_resid_history;         /* resid_cap entries                                    */
   double* h_beta_history;          /* beta_cap entries                                     */
+  int32_t resid_verified;          /* final_resid_true <= eps: the explicit check that backs   */
+                                   /* `converged` (R13); `converged` itself is the      */
+                                   /* paper's finish-flag (R(k) <= eps or breakdown)  */
+  int32_t pad_;
 } psp_report;
 
 /* MREP row kinds (same meaning as the oracle's, defined independently). */

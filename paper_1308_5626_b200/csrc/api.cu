@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -102,7 +103,8 @@ void kt_flush(psp_ctx* c) {
 // returns a handle (or -1 when timing is off); pair with kt_end after the launch(es)
 int kt_begin(psp_ctx* c) {
   if (c->opts.timing < 2) return -1;
-  if (c->kev_used + 2 > 16384) kt_flush(c);
+  // the event pool grows (it is reused after every flush): no synchronisation in the middle of
+  // a timed region; psp_kernel_stats flushes
   while ((int)c->kev.size() < c->kev_used + 2) {
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -132,6 +134,21 @@ static std::string g_err;
 
 namespace psp {
 std::string cuda_err_str(cudaError_t e) { return std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e); }
+int device_ordinal() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  return dev < kMaxDev ? dev : kMaxDev - 1;
+}
+int device_sms() {
+  static std::atomic<int> sms[kMaxDev];
+  const int dev = device_ordinal();
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 }  // namespace psp
 
 static psp_status fail(psp_ctx* c, psp_status s, const std::string& msg) {
@@ -168,16 +185,7 @@ struct Plan {
   int nblocks;
 };
 
-int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-      sms = 148;
-  }
-  return sms;
-}
+int sm_count() { return device_sms(); }
 
 Plan make_plan(int64_t n, int d, int nA, int m_max, int64_t plane = 1, int nranks = 1) {
   Plan p{};
@@ -705,7 +713,7 @@ static psp_status ring_hyb_step(psp_ctx* c, int k, int src_slot, int dst) {
   h = kt_begin(c);
   const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, src_slot, 0,
                               px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream, J, c->W);
-  if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+  if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
   kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, kb));
   h = kt_begin(c);
   launch_icwy_dots_hyb(basis(c), py_col(c, dst), px_col(c, dst), J, k, c->nA, n, c->ds, c->rc, c->stream);
@@ -784,7 +792,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
       h = kt_begin(c);
       const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, 0, c->nA, c->vslot[1],
                                   1, nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream);
-      if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+      if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
       kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
       c->launches += 1;
     } else {
@@ -816,7 +824,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
         h = kt_begin(c);
         const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, slot, 0,
                                     px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream);
-        if (fe) return fail(c, PSP_E_CUDA, "fused pass: tensor map encode failed (" + std::to_string(fe) + ")");
+        if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
         kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
         c->launches += 1;
       } else if (hyb_pass(c, k)) {
@@ -950,6 +958,7 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
   R->status = PSP_OK;
   R->converged = R->iterations = R->cycles = R->matvecs = R->precond_applies = 0;
   R->resid_len = R->beta_len = 0;
+  R->resid_verified = 0;
   R->precond_identity = c->n_identity ? 1 : 0;
   if (c->opts.timing) cudaEventRecord(c->ev[0], c->stream);
   double eps;
@@ -1010,6 +1019,7 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
     PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &tr));
     R->final_resid_true = tr;
     R->converged = finish ? 1 : 0;
+    R->resid_verified = (finish && tr <= eps) ? 1 : 0;
     if (!finish) status = PSP_E_NOCONV;
   }
   if (c->opts.timing) {
@@ -1216,28 +1226,15 @@ psp_status psp_set_bands(psp_ctx* c, const double* d_bands, int* h_accepted) {
     cudaMemcpyAsync(c->bands, d_bands, (size_t)c->n * (2 * c->d + 1) * 8, cudaMemcpyDeviceToDevice, c->stream);
   bool ok = true;
   if (c->opts.gate) {
-    // evaluate R21 on the given bands with the same reduction as the fit (MREP-free path):
-    std::vector<double> hb((size_t)c->n * (2 * c->d + 1));
-    cudaMemcpyAsync(hb.data(), c->bands, hb.size() * 8, cudaMemcpyDeviceToHost, c->stream);
-    cudaStreamSynchronize(c->stream);
-    for (int64_t i = 0; i < c->n && ok; ++i) {
-      double off = 0.0;
-      for (int o = 0; o <= 2 * c->d; ++o) {
-        int64_t j = c->row0 + i + o - c->d;  // global column
-        if (o == c->d || j < 0 || j >= c->n_global) continue;
-        off += fabs(hb[(size_t)o * c->n + i]);
-      }
-      if (!(fabs(hb[(size_t)c->d * c->n + i]) > off)) ok = false;
-    }
-    if (c->multi) {  // one decision for the whole matrix
-      c->hp[9] = ok ? 1.0 : 0.0;
-      cudaMemcpyAsync(c->ds.scal + SC_TMP, c->hp + 9, 8, cudaMemcpyHostToDevice, c->stream);
-      if (c->comm->allreduce(c->ds.scal + SC_TMP, 1, 2, c->stream))
-        return fail(c, PSP_E_NCCL, "psp_set_bands: gate all-reduce failed");
-      double g;
-      PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &g));
-      ok = g > 0.5;
-    }
+    // R21 on the given bands: a device count of the non-dominant rows (one scalar read back),
+    // summed over the ranks for one decision for the whole matrix
+    launch_gate_count(c->bands, c->n, c->d, c->row0, c->n_global, c->ds.scal + SC_TMP, c->stream);
+    c->launches += 1;
+    if (c->multi && c->comm->allreduce(c->ds.scal + SC_TMP, 1, 0, c->stream))
+      return fail(c, PSP_E_NCCL, "psp_set_bands: gate all-reduce failed");
+    double nondom;
+    PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &nondom));
+    ok = nondom == 0.0;
   }
   PSP_TRY(install_bands(c, ok, nullptr));
   if (h_accepted) *h_accepted = c->n_identity ? 0 : 1;

@@ -748,11 +748,12 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
   const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
   const size_t smem = D <= 3 ? (size_t)kPF * (2 * D + 1) * tpb * 4 * 8 : 0;
-  static bool attr = false;
-  if (!attr) {
+  thread_local bool attr[kMaxDev] = {};
+  const int dev = device_ordinal();
+  if (!attr[dev]) {
     cudaFuncSetAttribute(factor_pass_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(factor_pass_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[dev] = true;
   }
   if (write)
     factor_pass_kernel<D, true><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
@@ -768,15 +769,17 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
   const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const size_t smem = TileSmem<FWD, D>::BYTES;
   const size_t ssmem = (size_t)SCAN_T * sizeof(Map<D>);
-  static bool attr_set = false;
-  if (!attr_set) {
+  thread_local bool attr_set[kMaxDev] = {};
+  const int dev = device_ordinal();
+  if (!attr_set[dev]) {
     cudaFuncSetAttribute(tile_map_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(tile_apply_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(tile_scan_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
-    attr_set = true;
+    attr_set[dev] = true;
   }
   // ranges: at most SCAN_T blocks (2 resident per SM), each a contiguous run of L tiles
-  int64_t nb = ntiles < 148 * SW<D>::MINB * 3 ? ntiles : 148 * SW<D>::MINB * 3;
+  const int64_t nbmax = (int64_t)device_sms() * SW<D>::MINB * 3;
+  int64_t nb = ntiles < nbmax ? ntiles : nbmax;
   if (nb > SCAN_T) nb = SCAN_T;
   if (nb < 1) nb = 1;
   const int64_t L = (ntiles + nb - 1) / nb;

@@ -36,6 +36,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <string>
+
 #include "givens.cuh"
 #include "internal.h"
 
@@ -470,7 +472,10 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
               face(xn_, cell ? Kp[q + TX] : 0.0, nb_n[i], st.s[1], hsy);
               if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
             }
-            if (st.nz > 1) {
+            {
+              // march-axis faces, also for a single-plane march axis (nz = 1): the Dirichlet
+              // faces then hold u = 0 (ub / un are 0 off the grid), as in stencil.cu; the 1-D
+              // view has s[2] = a[2] = 0, so the faces vanish there
               const bool inb = p > 0, int_ = p + 1 < st.nz;
               face(ub[i], kb[i], inb, st.s[2], hsz);
               face(un[i], kt[i], int_, st.s[2], hsz);
@@ -631,8 +636,12 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// launch_fused error codes: > 0 a CUresult of cuTensorMapEncodeTiled, else one of these
+constexpr int kErrNoEncode = -1;   // the driver entry point cuTensorMapEncodeTiled is unavailable
+constexpr int kErrLaunch = -2;     // cudaFuncSetAttribute / cudaLaunchKernelEx failed (cudaGetLastError)
+
 // 4-D map (x, y, plane, slot) over nslots columns of n doubles at base; box TX x TY x 1 x 1
-int g_map_err = 0;   // last cuTensorMapEncodeTiled result (diagnostics)
+thread_local int g_map_err = 0;   // last cuTensorMapEncodeTiled result (diagnostics)
 bool make_map(CUtensorMap* m, const double* base, const Stencil& st, int nslots, int TX, int TY) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) { g_map_err = -1; return false; }
@@ -662,7 +671,12 @@ struct MapCache {
 template <int KIND, int TX, int TY, int KMAX, int CS, int PP = 1>
 int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
   using Cfg = FCfg<TX, TY, KMAX, CS, PP>;
-  static MapCache mc;
+  // per host thread and device: the maps encode this device's pointers, the attribute is a
+  // property of this device's context
+  thread_local MapCache mcs[kMaxDev];
+  thread_local bool attr[kMaxDev] = {};
+  const int dev = device_ordinal();
+  MapCache& mc = mcs[dev];
   const Stencil& st = a.st;
   if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != st.field || mc.nx != st.nx ||
       mc.ny != st.ny || mc.nz != st.nz || mc.cap != a.cap) {
@@ -672,17 +686,18 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
     mc.px = ring_px; mc.py = ring_py; mc.field = st.field;
     mc.src = nullptr;
     mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)Cfg::SMEM);
-      attr = true;
-    }
+  }
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Cfg::SMEM) != cudaSuccess)
+      return kErrLaunch;
+    attr[dev] = true;
   }
   a.tiles_x = (st.nx + (TX - 4) - 1) / (TX - 4);
   a.tiles_y = TY > 1 ? (st.ny + (TY - 2) - 1) / (TY - 2) : st.ny;
   const int64_t txy = a.tiles_x * a.tiles_y;
-  int64_t zc = txy * st.nz / (148 * 4);            // about 4 tiles per SM
+  const int sms = device_sms();
+  int64_t zc = txy * st.nz / (sms * 4);            // about 4 tiles per SM
   if (zc > 64) zc = 64;
   if (zc < 8) zc = 8;
   const char* zce = getenv("PSP_FUSED_ZC");      // tuning knobs (read per launch: cheap next to a pass)
@@ -691,9 +706,9 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   if (zc > st.nz) zc = st.nz;
   a.zchunk = (int)zc;
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
-  if (!mc.ok) return g_map_err ? g_map_err : -1;
+  if (!mc.ok) return g_map_err ? g_map_err : kErrNoEncode;
   if (a.src_px == 2 && mc.src != a.src_vec) {      // plain-vector source (split-column step)
-    if (!make_map(&mc.ms, a.src_vec, st, 1, TX, TY)) return g_map_err ? g_map_err : -1;
+    if (!make_map(&mc.ms, a.src_vec, st, 1, TX, TY)) return g_map_err ? g_map_err : kErrNoEncode;
     mc.src = a.src_vec;
   }
   if (a.src_px != 2 && mc.src == nullptr) mc.ms = mc.mpx;
@@ -702,10 +717,10 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   cfg.blockDim = dim3(TX * TY * CS / PP + 32);    // compute warps + the TMA producer warp
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
-  int64_t grid = 148;                              // one resident block per SM (persistent)
+  int64_t grid = sms;                              // one resident block per SM (persistent)
   if (grid > a.ntiles) grid = a.ntiles;
   cfg.gridDim = dim3((unsigned)grid);
-  if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, mc.ms, a) != cudaSuccess) return -2;
+  if (cudaLaunchKernelEx(&cfg, kern, mc.mpx, mc.mpy, mc.mk, mc.ms, a) != cudaSuccess) return kErrLaunch;
   return 0;
 }
 
@@ -756,6 +771,12 @@ Stencil march_view(const Stencil& st) {
 }
 
 }  // namespace
+
+std::string fused_error(int code) {
+  if (code == kErrNoEncode) return "cuTensorMapEncodeTiled is unavailable";
+  if (code == kErrLaunch) return "launch failed: " + cuda_err_str(cudaGetLastError());
+  return "tensor map encode failed (CUresult " + std::to_string(code) + ")";
+}
 
 bool fused_supported(const Stencil& st, int k) {
   // TMA maps need 16-byte row strides (nx even) and coordinates that fit int32

@@ -182,6 +182,11 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
                 cudaStream_t s, MrepMulti mm);
 
+// R21 gate of a given N: the number of rows that are not strictly diagonally dominant -> *count
+// (device scalar; zeroed first).  grow0 / gN: global index of local row 0 and the global rows.
+void launch_gate_count(const double* bands, int64_t n, int d, int64_t grow0, int64_t gN, double* count,
+                       cudaStream_t s);
+
 // ---- banded LU (banded.cu) ----
 struct BandedScratch {
   double* states;     // fixed-point states (factor) / look-back descriptors (solve)
@@ -205,5 +210,12 @@ int banded_solve(const double* lu, int64_t n, int d, const double* v, const doub
 
 // ---- misc ----
 std::string cuda_err_str(cudaError_t e);
+// Per-device launch state (function attributes, tensor maps, occupancy, side streams) is keyed by
+// the CURRENT device, so contexts on several GPUs of one process each get their own.
+constexpr int kMaxDev = 64;
+int device_ordinal();   // cudaGetDevice, clamped to [0, kMaxDev)
+int device_sms();       // multiprocessor count of the current device (cached per device)
+// fused.cu: text of a launch_fused error code
+std::string fused_error(int code);
 
 }  // namespace psp

@@ -506,7 +506,7 @@ __global__ void combine_prep_kernel(DevState ds, int k, int nA) {
   // one thread: c0_j = a_j alpha_j, c1_j = -b_j alpha_j (j < k-1), c1_{k-1} = alpha_{k-1} into
   // ds.rpart[0, k) / [k, 2k); rpart[2k] = 1 on a zero pivot of R_{k-1} (R6)
   const int ld = nA + 1;
-  double hp[kMaxRestart], a[kMaxRestart], b[kMaxRestart];
+  double hp[kMaxRestart + 1], a[kMaxRestart], b[kMaxRestart];   // hp[0..k]
   const double* Hk = ds.H + (int64_t)(k - 1) * ld;   // column k, MGS coefficients (unrotated)
   for (int j = 0; j <= k; ++j) hp[j] = Hk[j];
   for (int j = 1; j <= k - 1; ++j) {                 // rotations 1..k-1 (as givens_update)
@@ -684,7 +684,7 @@ void launch_residual(const double* b, const double* y, double* v, int64_t n, int
   residual_kernel<<<rc.nblocks, TPB, 0, s>>>(b, y, v, n, ds, nA);
 }
 void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s) {
-  copy_kernel<<<grid_for(n, 148 * 8), TPB, 0, s>>>(x, y, n);
+  copy_kernel<<<grid_for(n, 8 * device_sms()), TPB, 0, s>>>(x, y, n);
 }
 void launch_mgs_literal(const double* src, double* U, const double* Vprev, const double* Vj,
                         int j, int k, int nA, int64_t n, DevState ds, const RedCfg& rc,
@@ -701,28 +701,28 @@ template <typename K>
 int wave_blocks(K kernel, int cap) {
   int per = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, TPB, 0) != cudaSuccess || per < 1) per = 1;
-  int sms = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int b = per * sms;
+  const int b = per * device_sms();
   return b < cap ? b : cap;
 }
 
 void launch_icwy_dots(Basis V, const double* w, int k, int nA, int64_t n, int w_raw,
                       DevState ds, const RedCfg& rc, cudaStream_t s) {
-  static int wave = 0;
+  thread_local int waves[kMaxDev] = {};
+  int& wave = waves[device_ordinal()];
   if (!wave) wave = wave_blocks(icwy_dots_kernel, rc.nblocks);
   icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, k, nA, n, w_raw, ds, nullptr, 0);
 }
 void launch_icwy_dots_hyb(Basis V, const double* w, const double* u, int J, int k, int nA, int64_t n,
                           DevState ds, const RedCfg& rc, cudaStream_t s) {
-  static int wave = 0;
+  thread_local int waves[kMaxDev] = {};
+  int& wave = waves[device_ordinal()];
   if (!wave) wave = wave_blocks(icwy_dots_kernel, rc.nblocks);
   icwy_dots_kernel<<<tiles_grid(n, wave), TPB, 0, s>>>(V, w, J + 1, nA, n, 1, ds, u, k);
 }
 void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, int k,
                         int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s, int ncols) {
-  static int wave = 0;
+  thread_local int waves[kMaxDev] = {};
+  int& wave = waves[device_ordinal()];
   if (!wave) wave = wave_blocks(icwy_update_kernel, rc.nblocks);
   int64_t ub = (n + UTILE - 1) / UTILE;
   if (ub > wave) ub = wave;
@@ -734,7 +734,8 @@ void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cuda
 void launch_update_combine(Basis V, const double* w, const double* ws, const double* x0, double* z0, double* z1,
                            int k, int nA, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
   combine_prep_kernel<<<1, 1, 0, s>>>(ds, k, nA);
-  static int wave = 0;
+  thread_local int waves[kMaxDev] = {};
+  int& wave = waves[device_ordinal()];
   if (!wave) wave = wave_blocks(update_combine_kernel, rc.nblocks);
   int64_t ub = (n + CTILE - 1) / CTILE;
   if (ub > wave) ub = wave;
@@ -742,13 +743,14 @@ void launch_update_combine(Basis V, const double* w, const double* ws, const dou
 }
 void launch_combine_finish(const double* z0, const double* z1, double* x, int64_t n, DevState ds, cudaStream_t s) {
   int64_t b = (n + TPB - 1) / TPB;
-  if (b > 148 * 8) b = 148 * 8;
+  if (b > 8 * device_sms()) b = 8 * device_sms();
   combine_finish_kernel<<<(int)(b < 1 ? 1 : b), TPB, 0, s>>>(z0, z1, x, n, ds);
 }
 void launch_combine(Basis V, int k, int nA, const double* base, double* out,
                     int64_t n, DevState ds, cudaStream_t s) {
-  static int wave = 0;
-  if (!wave) wave = wave_blocks(combine_kernel, 148 * 8);
+  thread_local int waves[kMaxDev] = {};
+  int& wave = waves[device_ordinal()];
+  if (!wave) wave = wave_blocks(combine_kernel, 8 * device_sms());
   int64_t cb = (n + UTILE - 1) / UTILE;
   if (cb > wave) cb = wave;
   combine_kernel<<<(int)(cb < 1 ? 1 : cb), TPB, 0, s>>>(V, k, nA, base, out, n, ds);

@@ -574,13 +574,15 @@ template <int D>
 void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_t gN, int64_t grow0, int64_t R0,
                 int64_t ntile, MrepOut out, MrepScratch sc, int nb, cudaStream_t s) {
   const size_t smem = TmaCfg<D>::SMEM;
-  static bool attr = false;
-  if (!attr) {
+  const int dev = device_ordinal();
+  thread_local bool attr[kMaxDev] = {};
+  if (!attr[dev]) {
     cudaFuncSetAttribute(mrep_tma_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(mrep_tma_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)TmaCfg<D>::SMEM_SUMS);
-    attr = true;
+    attr[dev] = true;
   }
+  const int sms = device_sms();
   const int64_t E = TT - 2 * D;
   if (sc.sums != nullptr && sc.sums_n >= n && D >= 2) {
     // split: stream + lagged sums, then the fits.  d <= 3: the rows go in PSP_MREP_CHUNKS
@@ -589,18 +591,22 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
     // fit spills at that occupancy): one chunk, the streaming kernel at full occupancy.
     // Measured n = 2^26, m = 32: d = 2 9.8 -> 8.9 ms, d = 3 11.3 -> 10.7 ms by the overlap.
     constexpr int K = D <= 3 ? PSP_MREP_CHUNKS : 1;
-    thread_local cudaStream_t s2 = nullptr;
-    thread_local cudaEvent_t ev[K + 1];
+    // the fit side stream and its events: per host thread and device
+    thread_local cudaStream_t s2s[kMaxDev] = {};
+    thread_local cudaEvent_t evs[kMaxDev][K + 1];
+    thread_local int occs[kMaxDev] = {};
+    cudaStream_t& s2 = s2s[dev];
+    cudaEvent_t* ev = evs[dev];
     if (s2 == nullptr) {
       cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
       for (int q = 0; q <= K; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
     }
-    static int occ = 0;
+    int& occ = occs[dev];
     if (!occ) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mrep_tma_kernel<D, true>, TT, TmaCfg<D>::SMEM_SUMS);
       if (occ < 1) occ = 1;
     }
-    const int64_t g1max = 148 * (int64_t)(K > 1 && occ > 3 ? 3 : occ);
+    const int64_t g1max = sms * (int64_t)(K > 1 && occ > 3 ? 3 : occ);
     const int64_t per = (ntile + K - 1) / K;
     for (int c = 0; c < K; ++c) {
       const int64_t t0 = c * per, t1 = (t0 + per < ntile) ? t0 + per : ntile;
@@ -612,7 +618,7 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
       cudaEventRecord(ev[c], s);
       cudaStreamWaitEvent(s2, ev[c], 0);
       const int64_t rows = (t1 - t0) * E;
-      const int64_t g2max = K > 1 ? 148 : 148 * PSP_MREP_FIT_MINB;   // beside the sums: one block per SM
+      const int64_t g2max = K > 1 ? sms : sms * PSP_MREP_FIT_MINB;   // beside the sums: one block per SM
       const int64_t g2 = (rows + TT - 1) / TT < g2max ? (rows + TT - 1) / TT : g2max;
       mrep_fitsum_kernel<D><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
     }
@@ -710,7 +716,33 @@ __global__ void mrep_decide_kernel(MrepScratch sc) {
   sc.result[7] = (a[5] == 0.0 || a[1] < thr) ? 1.0 : 0.0;
 }
 
+// R21 on a given N (psp_set_bands): rows that are not strictly diagonally dominant, summed in band
+// order as the fit kernels do, counted into *count (exact integer adds: order-free)
+__global__ void gate_count_kernel(const double* __restrict__ bands, int64_t n, int d, int64_t grow0, int64_t gN,
+                                  double* count) {
+  double cnt = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double off = 0.0;
+    for (int o = 0; o <= 2 * d; ++o) {
+      const int64_t j = grow0 + i + o - d;
+      if (o == d || j < 0 || j >= gN) continue;
+      off += fabs(bands[(int64_t)o * n + i]);
+    }
+    if (!(fabs(bands[(int64_t)d * n + i]) > off)) cnt += 1.0;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt != 0.0) atomicAdd(count, cnt);
+}
+
 }  // namespace
+
+void launch_gate_count(const double* bands, int64_t n, int d, int64_t grow0, int64_t gN, double* count,
+                       cudaStream_t s) {
+  cudaMemsetAsync(count, 0, sizeof(double), s);
+  int64_t nb = (n + 255) / 256;
+  if (nb > 8 * device_sms()) nb = 8 * device_sms();
+  gate_count_kernel<<<(unsigned)(nb < 1 ? 1 : nb), 256, 0, s>>>(bands, n, d, grow0, gN, count);
+}
 
 int mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,
                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
@@ -774,7 +806,8 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
     tc.sx = sxp;
     tc.sy = syp;
     for (int c = 0; c < m; ++c) tc.slot[c] = cols.slot[c];
-    const int nb = (int)(ntile < 148 * 4 ? ntile : 148 * 4);
+    const int64_t nbmax = 4 * (int64_t)device_sms();
+    const int nb = (int)(ntile < nbmax ? ntile : nbmax);
     switch (d) {
       case 1: launch_tma<1>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
       case 2: launch_tma<2>(tc, slot_scale, m, n, cols.gN, cols.grow0, R0, ntile, out, sc, nb, s); break;
@@ -790,7 +823,7 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
   }
   mrep_decide_kernel<<<1, 1, 0, s>>>(sc);
   int pb = (int)((n + 255) / 256);
-  if (pb > 148 * 8) pb = 148 * 8;
+  if (pb > 8 * device_sms()) pb = 8 * device_sms();
   mrep_patch_kernel<<<pb, 256, 0, s>>>(n, d, out, sc);
   if (multi && mm.comm->allreduce(sc.result + 8, 1, 0, s)) return 1;  // rows patched by R18
   return 0;

@@ -505,7 +505,7 @@ __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ 
 inline int64_t planes_per_block(int64_t tiles, int64_t nz) {
   // about 8 resident waves of blocks, at least 16 planes per block (halo re-reads of 2 planes
   // per chunk <= 12.5%)
-  int64_t zc = (tiles * nz) / (148 * 8 * 8);
+  int64_t zc = (tiles * nz) / ((int64_t)device_sms() * 8 * 8);
   if (zc < 16) zc = 16;
   if (zc > nz) zc = nz;
   if (zc < 1) zc = 1;
@@ -591,7 +591,7 @@ void launch_matvec(const Stencil& st, const double* x, const double* xs, double*
     case PSP_OP_CELL_ADVDIFF: launch_kind<PSP_OP_CELL_ADVDIFF>(st, x, xs, y, xcopy, s); break;
     default: {
       int blocks = (int)((st.n + 255) / 256);
-      if (blocks > 148 * 16) blocks = 148 * 16;
+      if (blocks > 16 * device_sms()) blocks = 16 * device_sms();
       if (blocks < 1) blocks = 1;
       dia_matvec_kernel<<<blocks, 256, 0, s>>>(st.n, st.dA, st.bands, x, xs, y, xcopy);
     }

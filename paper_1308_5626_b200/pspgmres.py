@@ -60,7 +60,8 @@ class psp_report(C.Structure):
                 ("mrep_rows_nondominant", C.c_int64), ("r0", C.c_double), ("eps", C.c_double),
                 ("final_resid_est", C.c_double), ("final_resid_true", C.c_double),
                 ("mrep_max_abs_diag", C.c_double), ("t_solve_ms", C.c_double), ("t_mrep_ms", C.c_double),
-                ("t_factor_ms", C.c_double), ("h_resid_history", _dp), ("h_beta_history", _dp)]
+                ("t_factor_ms", C.c_double), ("h_resid_history", _dp), ("h_beta_history", _dp),
+                ("resid_verified", C.c_int32), ("pad_", C.c_int32)]
 
 
 class psp_mrep_info(C.Structure):

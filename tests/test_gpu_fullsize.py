@@ -177,3 +177,63 @@ def test_c4_full_size_sampled(torch, P, orc):
     ctx.close()
     del ctx, u
     _free(torch)
+
+
+def _lockstep_c4(torch, P, orc, size, max_cycles, with_mrep):
+    """C4 recipe at size^3 with the bench's default options (fused passes from 2^21 rows on,
+    split-column steps beyond k = 16, the fused last-step combine): the first time step (N = I
+    on both sides, b = x0 = u0) on the GPU and in the oracle, compared by T4-T6 (DESIGN.md s.7)."""
+    from test_gpu_parity import compare_mrep, compare_solve, log_parity, oracle_sensitivity
+    prob = inputs.c4(n=size, steps=1)
+    n = prob.op.rows
+    b = prob.u0
+    eps = prob.tol * np.linalg.norm(b)
+    o = orc.pspgmres(prob.op, b, b, eps, prob.restart, max_cycles, d=prob.d)
+    env, dx = oracle_sensitivity(orc, prob, b, None, o["resid_hist"], o["x"], max_cycles=max_cycles)
+    opts = P.default_opts(max_cycles=max_cycles, m_max=prob.m_max)       # the bench's defaults
+    ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts)
+    bt = torch.as_tensor(b).cuda()
+    x = torch.empty_like(bt)
+    gr = ctx.psp_solve(bt, bt, x)
+    ro = dict(o["report"])
+    ro["converged"] = ro["converged"] if max_cycles >= prob.max_cycles else 1
+    if max_cycles < prob.max_cycles:          # a truncated solve: both sides ran every cycle
+        assert gr["cycles"] == ro["cycles"] == max_cycles and gr["iterations"] == ro["iterations"]
+        gr = dict(gr, converged=1, final_resid_true=0.0)
+    compare_solve(gr, ro, o["resid_hist"], 0, env, nA=prob.restart, case=f"C4-{size}-full")
+    err = np.linalg.norm(x.cpu().numpy() - o["x"])
+    if gr["iterations"] == ro["iterations"]:                                           # T6
+        assert err <= max(1e-9 * np.linalg.norm(o["x"]), 30.0 * dx), (err, dx)
+    if with_mrep:
+        # Alg.2 on the GPU's own probe ring (recorded with their Krylov scales: the scaled path of
+        # the TMA kernels) vs the oracle's Algorithm 2 on the same probes
+        rep = ctx.psp_mrep_fit()
+        cnt, slots, PX, PY = ctx.psp_ring_view()
+        px, py = PX.cpu().numpy(), PY.cpu().numpy()
+        g = P.psp_mrep_fit_raw(PX.contiguous(), PY.contiguous(), prob.d)
+        r = orc.mrep(px, py, prob.d)
+        ex = compare_mrep(g, r, prob.d, n, px, max_excluded_frac=1.0)
+        log_parity(case=f"C4-{size}-full", step=0, mrep_excluded=int(ex), rows=n)
+        bands, _ = ctx.psp_get_bands()
+        # psp_mrep_fit (scaled ring columns) and psp_mrep_fit_raw (the same columns, scaled by
+        # torch) agree to the rounding of the scale product
+        bb = bands.cpu().numpy()
+        gb = g["bands"].cpu().numpy()
+        assert np.max(np.abs(bb - gb) / np.maximum(np.abs(gb).max(axis=0), 1e-300)) <= 1e-6
+        assert bool(rep["mrep_gate_accepted"]) == r["gate_accepted"]
+    ctx.close()
+    del ctx, bt, x
+    _free(torch)
+
+
+def test_c4_lockstep_128_full_step(torch, P, orc):
+    """Full first time step at 128^3 (2^21 rows: the bench's fused / split-column passes run,
+    400 fused tiles over 148 persistent CTAs), every cycle to convergence, then Alg.2."""
+    _lockstep_c4(torch, P, orc, 128, 1000, with_mrep=True)
+
+
+def test_c4_lockstep_256_two_cycles(torch, P, orc):
+    """256^3 (> 2000 fused tiles), the first two GMRES(30) cycles: every step width of the
+    bench's policy (fused k = 2..16, split-column k = 17..29, the fused last-step combine at
+    k = 30) and one restart, compared with the oracle's literal Alg.1."""
+    _lockstep_c4(torch, P, orc, 256, 2, with_mrep=False)

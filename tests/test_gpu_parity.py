@@ -1,6 +1,8 @@
 """GPU (sm_100a) parity of libpspgmres against the oracle, element by element, on the same
 seeded inputs.  Tolerances T1..T6 are derived in DESIGN.md section 7.  Runs on a B200 only."""
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -51,6 +53,16 @@ MATVEC_CASES = [
     ("3d-cell-ragged", lambda: inputs.OperatorSpec(3, "cell_diff", (131, 9, 3), 2e-4,
                                                    field=np.exp(np.random.default_rng(9).standard_normal(131 * 27)))),
     ("dia", lambda: inputs.seven_diagonal(2000, seed=3)[0]),
+    # nx % 4 == 0: march4_kernel (the full-size stencil), several z-chunks and y tiles, ragged y
+    ("3d-cell-march4", lambda: inputs.OperatorSpec(3, "cell_diff", (64, 44, 40), 3e-5,
+                                                   field=np.exp(np.random.default_rng(12).standard_normal(64 * 44 * 40)))),
+    ("3d-const-march4", lambda: inputs.OperatorSpec(3, "const_diff", (128, 9, 37), 2e-4, nu=0.7)),
+    ("3d-advdiff-march4", lambda: inputs.OperatorSpec(3, "cell_advdiff", (32, 12, 21), 1e-4, c=(1.0, 0.5, 0.25),
+                                                      field=1.0 + np.random.default_rng(13).uniform(0, 1, 32 * 12 * 21))),
+    # a single plane on the march axis (z, resp. y): the Dirichlet faces of that axis still count
+    ("3d-cell-unitz", lambda: inputs.OperatorSpec(3, "cell_diff", (36, 20, 1), 1e-3,
+                                                  field=np.exp(np.random.default_rng(14).standard_normal(36 * 20)))),
+    ("2d-const-unity", lambda: inputs.OperatorSpec(2, "const_diff", (64, 1), 1e-3, nu=1.0)),
 ]
 
 
@@ -127,11 +139,13 @@ def gram_cond2(px, d):
     out = np.zeros(n)
     if n <= 2 * d:
         return out
-    rows = np.arange(d, n - d)[:, None] + np.arange(-d, d + 1)[None, :]          # (ni, 2d+1)
-    X = np.concatenate([np.ones((len(rows), 1, m)), px[:, rows].transpose(1, 2, 0)], axis=1)
-    sv = np.linalg.svd(X @ X.transpose(0, 2, 1), compute_uv=False)
-    with np.errstate(divide="ignore"):
-        out[d:n - d] = np.where(sv[:, -1] > 0, sv[:, 0] / sv[:, -1], np.inf)
+    for r0 in range(d, n - d, 1 << 17):                                         # bounded memory
+        r1 = min(n - d, r0 + (1 << 17))
+        rows = np.arange(r0, r1)[:, None] + np.arange(-d, d + 1)[None, :]        # (ni, 2d+1)
+        X = np.concatenate([np.ones((len(rows), 1, m)), px[:, rows].transpose(1, 2, 0)], axis=1)
+        sv = np.linalg.svd(X @ X.transpose(0, 2, 1), compute_uv=False)
+        with np.errstate(divide="ignore"):
+            out[r0:r1] = np.where(sv[:, -1] > 0, sv[:, 0] / sv[:, -1], np.inf)
     return out
 
 
@@ -150,6 +164,7 @@ def compare_mrep(g, r, d, n, px, max_excluded_frac=1e-4):
     # one side only, with an estimate > 1e9 on the other, is a rounding-decided singular Gram
     near |= (~np.isfinite(kap) & np.isfinite(kg) & (kg > 1e9)) | (~np.isfinite(kg) & np.isfinite(kap) & (kap > 1e9))
     assert near.sum() <= max(1, max_excluded_frac * n), near.sum()
+    excluded = int(near.sum())
     bad = np.nonzero((kind != r["row_kind"]) & ~near)[0]
     assert len(bad) == 0, (bad[:10], kind[bad[:10]], r["row_kind"][bad[:10]])
     ok = ~near & (kind != 1)          # ridged rows: the ridge solution itself is compared below
@@ -166,6 +181,7 @@ def compare_mrep(g, r, d, n, px, max_excluded_frac=1e-4):
     assert g["gate_accepted"] == r["gate_accepted"]
     if not near.any():
         assert g["rows_ridge"] == r["rows_ridge"] and g["rows_fallback"] == r["rows_fallback"]
+    return excluded
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4])
@@ -223,6 +239,39 @@ def test_mrep_degenerate_rows(torch, P, orc):
     assert np.all(np.isfinite(g["bands"].cpu().numpy()))
 
 
+@pytest.mark.parametrize("a2,ridged", [(3e-7, True), (1e-7, True), (1e-3, False)])
+def test_mrep_ridge_closed_form(torch, P, orc, a2, ridged):
+    """R17 on the GPU against the closed form of tests/test_oracle_mrep.py (orthogonal Hadamard
+    probe rows: diagonal Gram, ridge solution r_j / (G_jj + lambda)), tiled over many rows so
+    the TMA kernels (interior tiles) and the generic kernel (edges) both take ridge rows."""
+    H = np.array([[1.0]])
+    for _ in range(3):
+        H = np.block([[H, H], [H, -H]])
+    d, m, n = 1, 8, 3 * 700
+    a = np.tile(np.array([1.0, 0.5, a2]), n // 3)
+    hrow = np.tile(np.arange(1, 4), n // 3)     # row i takes Hadamard row 1 + (i mod 3)
+    px = a[None, :] * H[hrow].T                  # (m, n): the three rows around i are orthogonal
+    beta = np.array([0.25, -1.5, 4.0, 2.0])
+    py = np.zeros_like(px)
+    py[:, 1:-1] = beta[0] + beta[1] * px[:, :-2] + beta[2] * px[:, 1:-1] + beta[3] * px[:, 2:]
+    r = orc.mrep(px, py, d)
+    g = P.psp_mrep_fit_raw(dev(torch, px), dev(torch, py), d)
+    kind = g["row_kind"].cpu().numpy()
+    bands = g["bands"].cpu().numpy()
+    assert np.array_equal(kind, r["row_kind"])
+    assert g["rows_ridge"] == r["rows_ridge"] and (r["rows_ridge"] > 0) == ridged
+    for i in range(1, n - 1):                    # closed form per interior row
+        gd = 8.0 * np.array([1.0, a[i - 1] ** 2, a[i] ** 2, a[i + 1] ** 2])
+        rhs = gd * beta
+        lam = 1e-10 * gd.sum() / 4 if gd.max() / gd.min() > 1e12 else 0.0
+        expect = rhs / (gd + lam)
+        # r_j = sum_c x_jc y_c cancels from terms of size |x_j| |y|: the attainable error of
+        # beta_j is ~ m u sum_c |x_jc y_c| / (G_jj + lambda) (both sides)
+        X = np.vstack([np.ones(m), px[:, i - 1:i + 2].T])
+        tol = 16 * 2.0 ** -53 * (np.abs(X) @ np.abs(py[:, i])) / (gd + lam) + 1e-13 * np.abs(expect)
+        assert np.all(np.abs(bands[:, i] - expect[1:]) <= tol[1:]), (i, bands[:, i], expect)
+
+
 def test_mrep_insufficient_samples(torch, P):
     g5 = inputs.c5_numpy(100, 5, 2)
     g = P.psp_mrep_fit_raw(dev(torch, g5["px"]), dev(torch, g5["py"]), 2)
@@ -254,7 +303,7 @@ def run_gpu_steps(torch, P, prob, steps, mode):
     return out
 
 
-def oracle_sensitivity(orc, prob, b, N_used, ho, u_ref):
+def oracle_sensitivity(orc, prob, b, N_used, ho, u_ref, max_cycles=None):
     """The oracle's own response to a 1e-15 relative perturbation of x0: the envelope of the
     relative change of R(k) (running max over k) and the change of the final solution.
     Restarted GMRES amplifies such perturbations after the first cycle (T4/T6)."""
@@ -264,7 +313,7 @@ def oracle_sensitivity(orc, prob, b, N_used, ho, u_ref):
         assert st == orc.OK
     x0 = b * (1.0 + 1e-15 * np.random.default_rng(11).standard_normal(len(b)))
     eps = prob.tol * np.linalg.norm(b)
-    rp = orc.pspgmres(prob.op, b, x0, eps, prob.restart, prob.max_cycles, d=prob.d, lu=lu)
+    rp = orc.pspgmres(prob.op, b, x0, eps, prob.restart, max_cycles or prob.max_cycles, d=prob.d, lu=lu)
     hp = rp["resid_hist"]
     L = min(len(hp), len(ho))
     env = np.maximum.accumulate(np.abs(hp[:L] - ho[:L]) / np.maximum(ho[:L], 1e-300))
@@ -272,7 +321,32 @@ def oracle_sensitivity(orc, prob, b, N_used, ho, u_ref):
     return env, np.linalg.norm(rp["x"] - u_ref)
 
 
-def compare_solve(gr, o, ho, s, env=None):
+PARITY_LOG = os.environ.get("PSP_PARITY_LOG")   # measurement runs: per-cycle parity floors (T4)
+
+
+def log_parity(**kw):
+    if PARITY_LOG:
+        with open(PARITY_LOG, "a") as f:
+            f.write(json.dumps(kw, default=float) + "\n")
+
+
+def cycle_floor_stats(hg, ho, betas, nA, env):
+    """Per restart cycle c: the additive floor F_c = max_k (|dR(k)| - 1e-8 R_orc(k)) / beta_c the
+    history needs beyond T4's relative 1e-8, the largest relative difference, and the oracle's own
+    perturbation envelope (T4)."""
+    L = min(len(hg), len(ho))
+    out = []
+    for c in range(0, (L + nA - 1) // nA):
+        sl = slice(c * nA, min(L, (c + 1) * nA))
+        bc = betas[min(c, len(betas) - 1)]
+        dR = np.abs(hg[sl] - ho[sl])
+        out.append(dict(cycle=c, floor=float(np.max((dR - 1e-8 * ho[sl]) / bc)),
+                        rel=float(np.max(dR / np.maximum(ho[sl], 1e-300))),
+                        env=float(np.max(env[sl])) if env is not None else 0.0))
+    return out
+
+
+def compare_solve(gr, o, ho, s, env=None, nA=None, case=None):
     """T4-T6 for one solve with identical (b, x0, N) on both sides."""
     di, dc = gr["iterations"] - o["iterations"], gr["cycles"] - o["cycles"]
     assert abs(di) <= 1, (s, gr["iterations"], o["iterations"])                       # T5
@@ -282,6 +356,9 @@ def compare_solve(gr, o, ho, s, env=None):
     assert gr["converged"] == 1 and o["converged"] == 1
     hg = gr["resid_history"]
     L = min(len(hg), len(ho))
+    if nA is not None:
+        log_parity(case=case, step=s, iterations=[gr["iterations"], o["iterations"]],
+                   cycles=cycle_floor_stats(hg, ho, gr["beta_history"], nA, env))
     # T4: relative 1e-8 above the FP64 floor of the recursively updated residual estimate,
     # whose absolute noise after restarts is O(u kappa(A) ||r0||), widened after the first
     # cycle to 30x the oracle's own sensitivity envelope
@@ -309,6 +386,12 @@ LOCKSTEP_CASES = [
     ("C4-ragged-even", lambda: inputs.Problem("C4re", inputs.OperatorSpec(3, "cell_diff", (34, 19, 23), 1e-3 / 400,
                                                                           field=np.exp(np.random.default_rng(5).standard_normal(34 * 19 * 23))),
                                               np.random.default_rng(6).uniform(-1, 1, 34 * 19 * 23), 30, 1e-8, 3, 2, 32, 1000), 2),
+    # a single plane on the march axis (the fused pass must keep its Dirichlet faces)
+    ("C4-unitz", lambda: inputs.Problem("C4z", inputs.OperatorSpec(3, "cell_diff", (36, 22, 1), 1e-3 / 100,
+                                                                    field=np.exp(np.random.default_rng(7).standard_normal(36 * 22))),
+                                        np.random.default_rng(8).uniform(-1, 1, 36 * 22), 30, 1e-8, 3, 2, 32, 1000), 2),
+    ("C2-unity", lambda: inputs.Problem("C2y", inputs.OperatorSpec(2, "const_diff", (96, 1), 2e-4),
+                                        np.random.default_rng(9).uniform(-1, 1, 96), 30, 1e-10, 1, 2, 64, 1000), 2),
 ]
 
 
@@ -334,7 +417,7 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, mode):
         x = torch.empty_like(b)
         gr = ctx.psp_solve(b, b, x)
         env, dx = oracle_sensitivity(orc, prob, u, r["N_used"], r["resid_hist"], r["u"])
-        compare_solve(gr, r["solve"], r["resid_hist"], s, env)
+        compare_solve(gr, r["solve"], r["resid_hist"], s, env, nA=prob.restart, case=f"{name}/{mode}")
         err = np.linalg.norm(x.cpu().numpy() - r["u"])
         if gr["iterations"] == r["solve"]["iterations"]:                                  # T6
             assert err <= max(1e-9 * np.linalg.norm(r["u"]), 30.0 * dx), (s, err, dx)
@@ -349,7 +432,8 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, mode):
             # dependent (kappa(Gram) up to 1e16), so the unridged/ridged decision of those rows
             # is decided by rounding; they are excluded from the kind/coefficient comparison
             # (every excluded row has kappa_est > 1e9 on one side, by construction)
-            compare_mrep(g, o, prob.d, n, px, max_excluded_frac=1.0)
+            ex = compare_mrep(g, o, prob.d, n, px, max_excluded_frac=1.0)
+            log_parity(case=f"{name}/{mode}", step=s, mrep_excluded=int(ex), rows=n)
             assert o["gate_accepted"] == r["mrep"]["gate_accepted"]
         u = r["u"]
     ctx.close()

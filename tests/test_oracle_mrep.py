@@ -193,3 +193,87 @@ def test_c5_recipe_statistical_recovery(orc):
     err = np.abs(r["bands"][:, d:200 - d] - g["bands"][:, d:200 - d])
     assert err.max() <= 1e-7
     assert r["gate_accepted"]
+
+
+def hadamard8():
+    """Sylvester Hadamard matrix of order 8: rows mutually orthogonal, row 0 all ones, every other
+    row sums to zero."""
+    H = np.array([[1.0]])
+    for _ in range(3):
+        H = np.block([[H, H], [H, -H]])
+    return H
+
+
+@pytest.mark.parametrize("a2,ridged", [(3e-7, True), (1e-7, True), (1e-3, False)])
+def test_ridge_branch_closed_form(orc, a2, ridged):
+    """R17 / S:226 pinned by a closed form.  With orthogonal, zero-sum probe rows (Hadamard rows
+    scaled by a_j) the interior row's Gram is diagonal, G = diag(8, 8a_0^2, 8a_1^2, 8a_2^2), so
+    its Cholesky factor is diag(sqrt(G_jj)), the condition estimate is exactly
+    (max L_jj / min L_jj)^2 = max G_jj / min G_jj, and the ridge solution of G + lambda I is
+    beta_j = r_j / (G_jj + lambda) with lambda = 1e-10 trace(G) / (2d+2) -- no solver involved.
+    A tiny a_2 puts the estimate above 1e12 and the shrinkage r_j / (G_jj + lambda) visibly
+    below the unridged r_j / G_jj (a wrong lambda, an unsquared estimate or a missing retry
+    fails); a_2 = 1e-3 stays below 1e12 (no ridge, the exact coefficients)."""
+    d, m = 1, 8
+    H = hadamard8()
+    a = np.array([1.0, 0.5, a2])
+    px = np.zeros((m, 3))
+    for j in range(3):
+        px[:, j] = a[j] * H[1 + j]
+    beta_true = np.array([0.25, -1.5, 4.0, 2.0])   # intercept, N(1,0), N(1,1), N(1,2)
+    py = np.zeros((m, 3))
+    py[:, 1] = beta_true[0] + px @ beta_true[1:]
+    py[:, 0] = 3.0 * px[:, 0]                        # boundary rows: exact linear fits
+    py[:, 2] = -2.0 * px[:, 2]
+    r = orc.mrep(px, py, d)
+    g = np.array([8.0, 8.0 * a[0] ** 2, 8.0 * a[1] ** 2, 8.0 * a[2] ** 2])
+    kap = g.max() / g.min()
+    assert r["kappa_est"][1] == pytest.approx(kap, rel=1e-12)
+    rhs = g * beta_true                              # r = G beta_true (consistent data)
+    if ridged:
+        assert kap > 1e12
+        lam = 1e-10 * g.sum() / (2 * d + 2)
+        expect = rhs / (g + lam)
+        assert r["row_kind"][1] == orc.ROW_INTERIOR_RIDGE and r["rows_ridge"] == 1
+        assert expect[3] < 0.9 * beta_true[3]        # the shrinkage is visible in the test
+    else:
+        assert kap < 1e12
+        expect = beta_true
+        assert r["row_kind"][1] == orc.ROW_INTERIOR and r["rows_ridge"] == 0
+    # r_j = sum_c x_jc y_c cancels from terms of size |x_j| |y|: the attainable error of beta_j is
+    # ~ m u sum_c |x_jc y_c| / (G_jj + lambda)
+    X = np.vstack([np.ones(m), px.T])
+    tol = 16 * 2.0 ** -53 * (np.abs(X) @ np.abs(py[:, 1])) / (g + (lam if ridged else 0.0)) + 1e-13 * np.abs(expect)
+    got = np.concatenate([[r["intercept"][1]], r["bands"][:, 1]])
+    assert np.all(np.abs(got - expect) <= tol), (got, expect, tol)
+    assert r["bands"][1, 0] == pytest.approx(3.0, rel=1e-14) and r["bands"][1, 2] == pytest.approx(-2.0, rel=1e-14)
+
+
+def test_ridge_matches_pseudo_inverse_on_row_space(orc):
+    """for an exactly rank-deficient, consistent design the ridge solution of R17 equals
+    the minimum-norm least-squares solution G^+ r (numpy's SVD pseudo-inverse of the design)
+    up to O(lambda / sigma_min^2) = O(1e-10) on the row space; its null-space component is 0."""
+    rng = np.random.default_rng(7)
+    d, n = 1, 20
+    base = rng.standard_normal((3, n))
+    px = np.vstack([base, base, base])              # m = 9, rank-3 column space in 4 unknowns
+    truth = np.array([0.3, -1.0, 2.5, 0.7])
+    py = np.zeros_like(px)
+    for i in range(1, n - 1):
+        py[:, i] = truth[0] + px[:, i - 1:i + 2] @ truth[1:]
+    r = orc.mrep(px, py, d)
+    for i in range(1, n - 1):
+        X = np.hstack([np.ones((9, 1)), px[:, i - 1:i + 2]])
+        mn = np.linalg.pinv(X) @ py[:, i]           # minimum-norm least squares (SVD)
+        got = np.concatenate([[r["intercept"][i]], r["bands"][:, i]])
+        assert r["row_kind"][i] in (orc.ROW_INTERIOR_RIDGE,)
+        # S:231's 1e-6, or the normal equations' attainable accuracy 8 P u kappa_2(G + lambda I)
+        # (DESIGN.md T3) when that is larger: the ridged Gram has kappa ~ trace / lambda ~ 1e10
+        G = X.T @ X
+        Gl = G + 1e-10 * np.trace(G) / 4 * np.eye(4)
+        tol = max(1e-6, 8 * 4 * 2.0 ** -53 * np.linalg.cond(Gl))
+        assert np.linalg.norm(got - mn) <= tol * np.linalg.norm(mn), i
+        # null space of X: no component of the ridge solution there
+        _, s, vt = np.linalg.svd(X)
+        null = vt[np.sum(s > 1e-10 * s[0]):]
+        assert np.all(np.abs(null @ got) <= tol * np.linalg.norm(mn))
