@@ -5,9 +5,9 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall 
 BUILD     ?= build
 CSRC      := paper_1308_5626_b200/csrc
 LIB       ?= paper_1308_5626_b200/libpspgmres.so
-SRCS      := $(CSRC)/api.cu $(CSRC)/comm.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/fused.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu
+SRCS      := $(CSRC)/api.cu $(CSRC)/comm.cu $(CSRC)/stencil.cu $(CSRC)/krylov.cu $(CSRC)/fused.cu $(CSRC)/mrep.cu $(CSRC)/banded.cu $(CSRC)/resident.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(SRCS))
-HDRS      := $(CSRC)/internal.h $(CSRC)/givens.cuh include/pspgmres.h
+HDRS      := $(CSRC)/internal.h $(CSRC)/givens.cuh $(CSRC)/stencil_row.cuh include/pspgmres.h
 ORACLE    := oracle/liboracle.so
 
 all: $(LIB) $(ORACLE)

@@ -100,6 +100,12 @@ typedef struct {
                                    /* k - fused_split_cols through an update pass and a dots  */
                                    /* pass (DESIGN.md s.6); 0 = three separate passes;        */
                                    /* default 16                                              */
+  int32_t resident;                /* f2: run the whole solve (every restart cycle, the R(k)  */
+                                   /* tests and the restarts) as one persistent device-resident */
+                                   /* kernel, no host round trip per step (resident.cu):      */
+                                   /* 0 off; 1 (default) for single-rank ICWY solves of up to  */
+                                   /* 2^20 rows with n_A <= 64 (a banded N: up to 16384 rows); */
+                                   /* 2 whenever supported                                    */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */
@@ -301,7 +307,8 @@ psp_status psp_launch_count(const psp_ctx* ctx, int64_t* h_launches);
 enum {
   PSP_KC_MATVEC = 0, PSP_KC_PRECOND = 1, PSP_KC_ORTHO_DOTS = 2, PSP_KC_ORTHO_UPDATE = 3,
   PSP_KC_MGS_LITERAL = 4, PSP_KC_NORMALIZE = 5, PSP_KC_COMBINE = 6, PSP_KC_RESIDUAL = 7,
-  PSP_KC_MREP = 8, PSP_KC_FACTOR = 9, PSP_KC_OTHER = 10, PSP_KC_FUSED = 11, PSP_KC_COUNT = 12
+  PSP_KC_MREP = 8, PSP_KC_FACTOR = 9, PSP_KC_OTHER = 10, PSP_KC_FUSED = 11, PSP_KC_RESIDENT = 12,
+  PSP_KC_CG = 13, PSP_KC_COUNT = 14
 };
 psp_status psp_kernel_stats(psp_ctx* ctx, double* h_ms, double* h_bytes, int64_t* h_launches,
                             int reset);

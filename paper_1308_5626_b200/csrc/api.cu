@@ -39,6 +39,13 @@ struct psp_ctx {
   double* mh_send = nullptr;     // MREP halo rows: [lo|hi] x m_max x d, packed for the send
   double* mh_recv = nullptr;     //   and received ([lo|hi] x m_max x d)
   double* bmisc = nullptr;       // banded multi-rank scratch (maps, states)
+  // f2: the device-resident solve's scratch (resident.cu)
+  double* res_out = nullptr;     // 16-double summary
+  unsigned long long* res_bar = nullptr;
+  double* res_part = nullptr;
+  double* res_hist = nullptr;
+  double* res_beta = nullptr;
+  int res_hist_cap = 0, res_beta_cap = 0;
   // workspace carve
   double* ring_px = nullptr;
   double* ring_py = nullptr;
@@ -181,13 +188,15 @@ struct Plan {
   size_t off_px, off_py, off_V, off_X0, off_B, off_W, off_bands, off_lu, off_icpt, off_kind,
       off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
       off_sscale, off_halo, off_rpart, off_mhalo, off_bmisc,
-      off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, total;
+      off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, off_res, off_rhist, off_rbeta,
+      total;
+  int hist_cap, beta_cap;
   int nblocks;
 };
 
 int sm_count() { return device_sms(); }
 
-Plan make_plan(int64_t n, int d, int nA, int m_max, int64_t plane = 1, int nranks = 1) {
+Plan make_plan(int64_t n, int d, int nA, int m_max, int max_cycles, int64_t plane = 1, int nranks = 1) {
   Plan p{};
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -230,6 +239,13 @@ Plan make_plan(int64_t n, int d, int nA, int m_max, int64_t plane = 1, int nrank
   p.off_rpart = take((size_t)(2 * kMaxRestart + 16) * 8);
   p.off_mhalo = take((size_t)4 * (m_max + 1) * d * 8);
   p.off_bmisc = take(banded_misc_doubles(d, nranks) * 8);
+  // f2 (resident.cu): barrier word + summary, double-buffered grid partials, R(k) / beta history
+  p.off_res = take(256 + resident_scratch_doubles(nA, sm_count()) * 8);
+  const int64_t hc = (int64_t)nA * max_cycles;
+  p.hist_cap = (int)(hc < ((int64_t)1 << 22) ? hc : ((int64_t)1 << 22));
+  p.beta_cap = max_cycles;
+  p.off_rhist = take((size_t)p.hist_cap * 8);
+  p.off_rbeta = take((size_t)p.beta_cap * 8);
   p.total = o + 256;  // alignment slack for the base pointer
   return p;
 }
@@ -280,6 +296,7 @@ void psp_default_opts(psp_opts* o) {
   o->fused_kmin = 2;
   o->fused_kmax = 16;
   o->fused_split_cols = 16;
+  o->resident = 1;
 }
 
 const char* psp_version(void) { return "libpspgmres 0.1 (sm_100a, FP64)"; }
@@ -345,7 +362,7 @@ psp_status psp_workspace_bytes(const psp_grid* grid, const psp_stencil* st, int 
   PSP_TRY(validate(grid, st, d, restart, &o));
   int64_t n_loc, row0, s0, sl, plane;
   PSP_TRY(local_layout(grid, st, d, comm, &n_loc, &row0, &s0, &sl, &plane));
-  Plan p = make_plan(n_loc, d, restart, o.m_max, plane, comm ? comm->nranks : 1);
+  Plan p = make_plan(n_loc, d, restart, o.m_max, o.max_cycles, plane, comm ? comm->nranks : 1);
   *bytes = p.total;
   return PSP_OK;
 }
@@ -362,7 +379,7 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   int64_t n, row0, slab0, slab_len, plane;
   PSP_TRY(local_layout(grid, st, d, comm, &n, &row0, &slab0, &slab_len, &plane));
   const int nranks = comm ? comm->nranks : 1;
-  Plan p = make_plan(n, d, restart, o.m_max, plane, nranks);
+  Plan p = make_plan(n, d, restart, o.m_max, o.max_cycles, plane, nranks);
   if (!d_ws || ws_bytes < p.total) return fail(nullptr, PSP_E_NOMEM, "workspace smaller than psp_workspace_bytes");
 
   psp_ctx* c = new psp_ctx();
@@ -454,6 +471,13 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->mh_send = (double*)at(p.off_mhalo);
   c->mh_recv = c->mh_send + 2 * (size_t)(o.m_max + 1) * d;
   c->bmisc = (double*)at(p.off_bmisc);
+  c->res_bar = (unsigned long long*)at(p.off_res);
+  c->res_out = (double*)at(p.off_res + 64);
+  c->res_part = (double*)at(p.off_res + 256);
+  c->res_hist = (double*)at(p.off_rhist);
+  c->res_beta = (double*)at(p.off_rbeta);
+  c->res_hist_cap = p.hist_cap;
+  c->res_beta_cap = p.beta_cap;
   // zero the small control state (tickets, epochs, Hessenberg)
   cudaMemsetAsync(at(p.off_H), 0, p.off_partials - p.off_H, c->stream);
   cudaMemsetAsync(at(p.off_tickets), 0, TK_N * 4, c->stream);
@@ -530,7 +554,8 @@ psp_status psp_kernel_stats(psp_ctx* c, double* ms, double* bytes, int64_t* laun
 const char* psp_kernel_class_name(int k) {
   static const char* names[PSP_KC_COUNT] = {"matvec", "precond_solve", "ortho_dots", "ortho_update",
                                             "mgs_literal", "normalize", "combine", "residual",
-                                            "mrep_fit", "banded_factor", "other", "arnoldi_fused"};
+                                            "mrep_fit", "banded_factor", "other", "arnoldi_fused",
+                                            "resident_solve", "cg"};
   return (k >= 0 && k < PSP_KC_COUNT) ? names[k] : "?";
 }
 
@@ -949,6 +974,117 @@ psp_status psp_cycle_end(psp_ctx* c, int k, double* x) {
   return check_cuda(c, "psp_cycle_end");
 }
 
+// f2: the device-resident solve (resident.cu) -- single rank, one-reduction MGS, n_A <= 64, up to
+// 2^20 rows by default (a banded N: one CTA's sequential sweeps, n <= 16384)
+static bool resident_eligible(const psp_ctx* c) {
+  if (c->opts.resident <= 0 || c->multi || c->opts.ortho != PSP_MGS_1REDUCE) return false;
+  if (!resident_supported(c->n, c->nA, !c->n_identity)) return false;
+  return c->opts.resident >= 2 || c->n <= kResidentAutoRows;
+}
+
+static psp_status resident_solve(psp_ctx* c, const double* b, const double* x0, double* x, psp_report* R) {
+  if (x0 != c->X0) {
+    launch_copy(x0, c->X0, c->n, c->stream);
+    c->launches += 1;
+  }
+  ResidentCall rc{};
+  rc.st = c->st;
+  rc.b = b;
+  rc.X0 = c->X0;
+  rc.V = c->V;
+  rc.ldv = c->ldv;
+  rc.ring_px = c->ring_px;
+  rc.ring_py = c->ring_py;
+  rc.slot_scale = c->slot_scale;
+  rc.ring_cap = c->ring_cap;
+  rc.ring_phys = c->ring_phys;
+  rc.ring_head = c->ring_head;
+  rc.ring_count = c->ring_count;
+  rc.lu = c->n_identity ? nullptr : c->lu;
+  rc.d = c->d;
+  rc.y = c->W;
+  rc.z = c->bs.y;
+  rc.nA = c->nA;
+  rc.max_cycles = c->opts.max_cycles;
+  rc.tol_abs = c->opts.tol_mode == PSP_TOL_ABS;
+  rc.tol = c->tol;
+  rc.grid = resident_grid(c->n, !c->n_identity);
+  rc.partials = c->res_part;
+  rc.bar = c->res_bar;
+  rc.hist = c->res_hist;
+  rc.hist_cap = c->res_hist_cap;
+  rc.betas = c->res_beta;
+  rc.beta_cap = c->res_beta_cap;
+  rc.out = c->res_out;
+  rc.ds = c->ds;
+  const int h = kt_begin(c);
+  if (launch_resident(rc, c->stream)) {
+    c->sticky = PSP_E_CUDA;
+    return fail(c, PSP_E_CUDA, "resident solve: launch failed: " + cuda_err_str(cudaGetLastError()));
+  }
+  c->launches += 1;
+  double o[16];
+  PSP_TRY(sync_read(c, c->res_out, 14, o));
+  const int iters = (int)o[0];
+  // algorithmic bytes: step k reads V_k, k columns twice, writes P_x, P_y,
+  // V_{k+1}: 8(2k+4) per row; a cycle start 40, a cycle end 8(k+2)
+  {
+    double per = 0.0;
+    int left = iters;
+    for (int cy = 0; cy < (int)o[1]; ++cy) {
+      const int kk = left < c->nA ? left : c->nA;
+      per += 40.0 + 8.0 * (kk + 2);
+      for (int k = 1; k <= kk; ++k) per += 8.0 * (2 * k + 4);
+      left -= kk;
+    }
+    kt_end(c, h, PSP_KC_RESIDENT, per * (double)c->n);
+  }
+  R->iterations = iters;
+  R->cycles = (int)o[1];
+  R->matvecs = (int)o[2];
+  R->precond_applies = (int)o[3];
+  const bool finish = o[4] != 0.0;
+  const int status = (int)o[5];
+  R->r0 = o[6];
+  R->eps = o[7];
+  R->final_resid_est = o[8];
+  R->resid_len = (int)o[10];
+  R->beta_len = (int)o[11];
+  c->ring_head = (int)o[12];
+  c->ring_count = (int)o[13];
+  c->cycle_fused = false;
+  c->last_k = 0;
+  c->combined_k = 0;
+  if (R->h_resid_history && R->resid_cap > 0) {
+    int cnt = R->resid_len < R->resid_cap ? R->resid_len : R->resid_cap;
+    if (cnt > c->res_hist_cap) cnt = c->res_hist_cap;
+    if (cnt > 0) cudaMemcpyAsync(R->h_resid_history, c->res_hist, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream);
+  }
+  if (R->h_beta_history && R->beta_cap > 0) {
+    int cnt = R->beta_len < R->beta_cap ? R->beta_len : R->beta_cap;
+    if (cnt > c->res_beta_cap) cnt = c->res_beta_cap;
+    if (cnt > 0) cudaMemcpyAsync(R->h_beta_history, c->res_beta, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream);
+  }
+  if (x != c->X0) {
+    launch_copy(c->X0, x, c->n, c->stream);
+    c->launches += 1;
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    c->sticky = PSP_E_CUDA;
+    return fail(c, PSP_E_CUDA, "resident solve: " + cuda_err_str(cudaGetLastError()));
+  }
+  psp_status st = PSP_OK;
+  if (status == PSP_E_NONFINITE) st = PSP_E_NONFINITE;
+  else if (status == PSP_E_SINGULAR) st = PSP_E_SINGULAR;
+  if (st == PSP_OK) {
+    R->final_resid_true = o[9];
+    R->converged = finish ? 1 : 0;
+    R->resid_verified = (finish && o[9] <= R->eps) ? 1 : 0;
+    if (!finish) st = PSP_E_NOCONV;
+  }
+  return st;
+}
+
 psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, psp_report* rep) {
   if (!c || !b || !x0 || !x) return fail(c, PSP_E_ARG, "psp_solve: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
@@ -961,6 +1097,21 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
   R->resid_verified = 0;
   R->precond_identity = c->n_identity ? 1 : 0;
   if (c->opts.timing) cudaEventRecord(c->ev[0], c->stream);
+  if (resident_eligible(c)) {
+    psp_status status = resident_solve(c, b, x0, x, R);
+    if (c->opts.timing) {
+      cudaEventRecord(c->ev[1], c->stream);
+      cudaEventSynchronize(c->ev[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+      R->t_solve_ms = ms;
+    }
+    R->status = status;
+    if (status != PSP_OK && status != PSP_E_NOCONV)
+      return fail(c, status, std::string("psp_solve (resident): ") + psp_status_str(status));
+    if (status == PSP_E_NOCONV) fail(c, status, "psp_solve: n_r restart cycles exhausted");
+    return status;
+  }
   double eps;
   PSP_TRY(set_eps(c, b, &eps));
   R->eps = eps;

@@ -148,6 +148,43 @@ int launch_fused(const Stencil& st, const double* ring_px, const double* ring_py
                   int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
                   DevState ds, cudaStream_t s, int jb = 0, const double* src_vec = nullptr);
 
+// ---- f2: the device-resident solve (resident.cu) ----
+constexpr int kResidentMaxRestart = 64;       // replicated per-CTA scalar state in shared memory
+constexpr int64_t kResidentSeqRows = 16384;   // a banded N: one thread's sequential sweeps
+constexpr int64_t kResidentOneCtaRows = 4096; // one CTA (no grid barrier)
+constexpr int64_t kResidentAutoRows = (int64_t)1 << 20;   // opts.resident = 1: up to here
+struct ResidentCall {
+  Stencil st;
+  const double* b;
+  double* X0;
+  double* V;
+  int64_t ldv;
+  double* ring_px;
+  double* ring_py;
+  double* slot_scale;
+  int ring_cap, ring_phys, ring_head, ring_count;
+  const double* lu;     // NULL: N = I
+  int d;
+  double* y;            // n (N != I)
+  double* z;            // n (N != I)
+  int nA, max_cycles, tol_abs;
+  double tol;
+  int grid;
+  double* partials;     // resident_scratch_doubles
+  unsigned long long* bar;
+  double* hist;
+  int hist_cap;
+  double* betas;
+  int beta_cap;
+  double* out;          // 16 doubles: iterations, cycles, matvecs, precond applies, finish, status,
+                        // r0, eps, est, true resid, hist len, beta len, ring head, ring count
+  DevState ds;
+};
+bool resident_supported(int64_t n, int nA, bool banded_n);
+int resident_grid(int64_t n, bool banded_n);
+size_t resident_scratch_doubles(int nA, int grid);
+int launch_resident(const ResidentCall& c, cudaStream_t s);   // 0 ok, 1 launch failure
+
 // ---- MREP (mrep.cu) ----
 struct MrepOut {
   double* bands;      // (2d+1) x n

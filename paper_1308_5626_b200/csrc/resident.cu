@@ -1,0 +1,549 @@
+// resident.cu -- f2: the whole restarted PSP-GMRES solve (Alg.1) as ONE
+// persistent kernel, for the small and L2-resident systems (C1 1-D n = 1024, C2 2-D 512^2, the
+// paper's own n <= 700 seven-diagonal family) whose host-driven cycle is bound by launch latency
+// and the per-step device->host read of R(k) (~20 us a step).
+//
+// Every CTA owns a contiguous block of rows and replicates the O(n_A^2) scalar state of the cycle
+// (Hessenberg, Givens rotations, G, the ICWY L matrix, the lagged normalisations) in shared
+// memory; the grid meets only at the reductions.  An Arnoldi step is two grid-wide reductions:
+//   [A] probe Y_k = N^{-1}(alpha_k V_k) -> P_x, w = A Y_k -> P_y (l.10-12), the inner products
+//       s_j = V_j'w and l_j = V_j'V_k (one-reduction MGS, R11), reduced; every CTA solves
+//       (I + L) h = s for H(1..k, k) (l.13-16);
+//   [B] U = w - sum_j h_j V_j -> V(:,k+1) (stored unnormalised), ||U||^2, reduced; every CTA
+//       applies the Givens update (l.17-32) and tests R(k) <= eps (l.33) -- identical inputs,
+//       identical decisions, no broadcast needed.
+// Reductions are deterministic (fixed partition, fixed summation order, the same in every CTA),
+// so results are bitwise reproducible.  The grid barrier is a monotone arrival counter
+// (cooperative launch: every CTA is co-resident).  One CTA (n <= 4096): barriers are
+// __syncthreads() only.  A banded N (accepted by the gate, R21) is applied by one thread's
+// sequential forward / backward sweeps (P:30's Thomas recurrence for d = 1), so it is offered only
+// to one-CTA problems (n <= kResidentSeqRows).
+//
+// Same arithmetic as the host-driven split path (icwy_dots / icwy_update / combine kernels of
+// krylov.cu, up to the association of the reductions): T4-T6 parity with the oracle holds in the
+// same tolerances (tests/test_gpu_parity.py, mode "resident").
+#include <math.h>
+
+#include "givens.cuh"
+#include "internal.h"
+#include "stencil_row.cuh"
+
+namespace psp {
+namespace {
+
+constexpr int RT = 512;          // threads per CTA
+constexpr int RMAX = 8;          // rows per thread (n <= grid * RT * RMAX)
+constexpr int RW = RT / 32;
+
+struct ResArgs {
+  Stencil st;
+  const double* b;
+  double* X0;                    // in: x0; out: the last iterate (l.43)
+  double* V;                     // (nA+1) columns of ldv: V(:,j) unnormalised, scale alpha_j
+  int64_t ldv;
+  double* ring_px;
+  double* ring_py;
+  double* slot_scale;
+  int ring_cap, ring_phys, ring_head, ring_count;
+  const double* lu;              // banded LU factors of N (NULL: N = I)
+  int d;
+  double* y;                     // n: sweep intermediate (N != I)
+  double* z;                     // n: Z of the cycle end (N != I)
+  int nA, max_cycles;
+  int tol_abs;
+  double tol;
+  int64_t chunk;                 // rows per CTA
+  double* partials;              // [2][grid][2 nA + 2]: double-buffered (a CTA may write reduction
+                                 // r+1's partial while a slower one still reads reduction r's)
+  unsigned long long* bar;       // arrival counter (zeroed before the launch)
+  double* hist;                  // R(k) of every inner iteration (hist_cap)
+  int hist_cap;
+  double* betas;                 // beta per cycle (beta_cap)
+  int beta_cap;
+  double* out;                   // summary, see enum
+  DevState ds;                   // global mirror of the scalar state (test hooks)
+};
+enum { O_ITER = 0, O_CYCLES, O_MATVECS, O_PAPPLY, O_FINISH, O_STATUS, O_R0, O_EPS, O_EST, O_TRUE, O_HLEN,
+       O_BLEN, O_HEAD, O_COUNT, O_N };
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// transposing butterfly: v[0..7] per lane -> lane l holds the warp sum of v[l & 7]
+__device__ __forceinline__ double butterfly8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int m = 4, h = 4; m >= 1; m >>= 1, h >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? v[j] : v[j + h];
+      const double keep = up ? v[j + h] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  double r = v[0];
+  r += __shfl_xor_sync(0xffffffffu, r, 8);
+  r += __shfl_xor_sync(0xffffffffu, r, 16);
+  return r;
+}
+
+// grid barrier: monotone arrival counter, epoch e -> wait for grid * e arrivals
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long& epoch) {
+  __syncthreads();
+  if (gridDim.x > 1) {
+    epoch += 1;
+    if (threadIdx.x == 0) {
+      const unsigned long long target = epoch * gridDim.x;
+      __threadfence();
+      atomicAdd(bar, 1ull);
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      } while (v < target);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+// (A x)_g for the operator kinds of the context, x written in this launch (L2 loads)
+__device__ __forceinline__ double arow(const Stencil& st, const double* x, int64_t g, double& xc) {
+  if (st.kind == PSP_OP_DIA) {
+    xc = __ldcg(x + g);
+    return dia_row<true>(st, x, g);
+  }
+  const int64_t i = g % st.nx, j = (g / st.nx) % st.ny, k = g / (st.nx * st.ny);
+  switch (st.kind * 4 + st.ndim) {
+    case PSP_OP_CONST_DIFF * 4 + 1: return stencil_row<PSP_OP_CONST_DIFF, 1, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CONST_DIFF * 4 + 2: return stencil_row<PSP_OP_CONST_DIFF, 2, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CONST_DIFF * 4 + 3: return stencil_row<PSP_OP_CONST_DIFF, 3, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CELL_DIFF * 4 + 1: return stencil_row<PSP_OP_CELL_DIFF, 1, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CELL_DIFF * 4 + 2: return stencil_row<PSP_OP_CELL_DIFF, 2, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CELL_DIFF * 4 + 3: return stencil_row<PSP_OP_CELL_DIFF, 3, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CELL_ADVDIFF * 4 + 1: return stencil_row<PSP_OP_CELL_ADVDIFF, 1, true>(st, x, i, j, k, g, xc);
+    case PSP_OP_CELL_ADVDIFF * 4 + 2: return stencil_row<PSP_OP_CELL_ADVDIFF, 2, true>(st, x, i, j, k, g, xc);
+    default: return stencil_row<PSP_OP_CELL_ADVDIFF, 3, true>(st, x, i, j, k, g, xc);
+  }
+}
+
+// N^{-1} v by the sequential recurrences of the factors (O2's order of operations):
+// y_i = v_i - sum_{j<i} L(i,j) y_j, z_i = (y_i - sum_{j>i} U(i,j) z_j) / U(i,i).  One thread.
+// vs: v is scaled by vs on the fly.  z may alias v (v is consumed by the forward sweep).
+__device__ void seq_solve(const double* lu, int64_t n, int d, const double* v, double vs, double* y, double* z,
+                          const double* add) {
+  for (int64_t i = 0; i < n; ++i) {
+    double s = vs * __ldcg(v + i);
+    for (int o = 0; o < d; ++o) {
+      const int64_t j = i + o - d;
+      if (j >= 0) s -= __ldg(lu + (int64_t)o * n + i) * y[j];
+    }
+    y[i] = s;
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int o = d + 1; o <= 2 * d; ++o) {
+      const int64_t j = i + o - d;
+      if (j < n) s -= __ldg(lu + (int64_t)o * n + i) * z[j];
+    }
+    z[i] = s / __ldg(lu + (int64_t)d * n + i);
+  }
+  if (add)
+    for (int64_t i = 0; i < n; ++i) z[i] = __ldcg(add + i) + z[i];
+}
+
+__global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nA = a.nA, ld = nA + 1, PV = 2 * nA + 2;
+  double* H = sm;                       // (nA+1) x nA, rotated in place
+  double* Lm = H + (size_t)ld * nA;     // (nA+1) x (nA+1)
+  double* Gv = Lm + (size_t)ld * ld;    // nA+1
+  double* Cv = Gv + ld;                 // nA
+  double* Sv = Cv + nA;                 // nA
+  double* al = Sv + nA;                 // nA+1
+  double* Qv = al + ld;                 // nA
+  double* rs = Qv + nA;                 // nA (R(k) of the cycle)
+  double* sc = rs + nA;                 // SC_NSCAL
+  double* red = sc + SC_NSCAL;          // [RW][PV]
+  double* tot = red + (size_t)RW * PV;  // PV
+  DevState S;                           // the replicated scalar state (givens_update's view)
+  S.H = H;
+  S.Hraw = a.ds.Hraw;                   // identical writes from every CTA (test hook)
+  S.G = Gv;
+  S.C = Cv;
+  S.S = Sv;
+  S.Q = Qv;
+  S.Lm = Lm;
+  S.alpha = al;
+  S.scal = sc;
+  S.resid = rs;
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t n = a.st.n;
+  const int64_t r0 = (int64_t)blockIdx.x * a.chunk;
+  const int64_t r1 = (r0 + a.chunk < n) ? r0 + a.chunk : n;
+  const bool lead = blockIdx.x == 0 && t == 0;
+  const bool seqN = a.lu != nullptr;    // one CTA (host-checked)
+  unsigned long long epoch = 0;
+  unsigned nred = 0;                    // grid reductions so far (partials buffer parity)
+  int head = a.ring_head, count = a.ring_count;
+  auto ring_next = [&]() -> int {       // R20: FIFO of capacity ring_cap over ring_phys slots
+    const int slot = (head + count) % a.ring_phys;
+    if (count < a.ring_cap) count += 1;
+    else head = (head + 1) % a.ring_phys;
+    return slot;
+  };
+  auto V = [&](int j) -> double* { return a.V + (int64_t)j * a.ldv; };   // 0-based column
+
+  // deterministic grid sum of nv per-thread values given by f(j, q) summed over this thread's
+  // rows: block butterflies -> red -> this CTA's tot -> partials -> every CTA sums the grid's
+  // partials in CTA order -> tot (valid in every thread after the call)
+  auto grid_reduce = [&](int nv, auto&& f) {
+    for (int j0 = 0; j0 < nv; j0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (j0 + q < nv) ? f(j0 + q) : 0.0;
+      const double r = butterfly8(v, lane);
+      if (lane < 8 && j0 + lane < nv) red[warp * PV + j0 + lane] = r;
+    }
+    __syncthreads();
+    for (int j = t; j < nv; j += RT) {
+      double s = 0.0;
+      for (int w = 0; w < RW; ++w) s += red[w * PV + j];
+      tot[j] = s;
+    }
+    if (gridDim.x > 1) {
+      double* part = a.partials + (size_t)(nred & 1u) * gridDim.x * PV;
+      nred += 1;
+      __syncthreads();
+      for (int j = t; j < nv; j += RT) __stcg(part + (int64_t)blockIdx.x * PV + j, tot[j]);
+      grid_sync(a.bar, epoch);
+      for (int j = warp; j < nv; j += RW) {            // one warp per value, fixed lane partition
+        double s = 0.0;
+        for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(part + (int64_t)c * PV + j);
+        s = warp_sum(s);
+        if (lane == 0) tot[j] = s;
+      }
+    }
+    __syncthreads();
+  };
+
+  // this thread's rows: r0 + t + q RT, q < RMAX
+  double w[RMAX];
+  int iters = 0, cycles = 0, matvecs = 0, papply = 0, hlen = 0, blen = 0, status = 0;
+  bool finish = false;
+  double r0v = 0.0, est = 0.0, eps;
+  if (a.tol_abs) {
+    eps = a.tol;
+  } else {                                             // R1: eps = tol ||b||
+    grid_reduce(1, [&](int) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int64_t g = r0 + t + (int64_t)q * RT;
+        if (g < r1) { const double bv = __ldg(a.b + g); s = fma(bv, bv, s); }
+      }
+      return s;
+    });
+    eps = a.tol * sqrt(tot[0]);
+  }
+  if (t == 0) sc[SC_EPS] = eps;
+  __syncthreads();
+
+  for (int l = 1; l <= a.max_cycles; ++l) {            // l.3
+    // ---- l.4-7: probe (X0, A X0); R_bar = B - A X0 -> V(:,1); beta ----
+    int slot = ring_next();
+    double* px = a.ring_px + (int64_t)slot * n;
+    double* py = a.ring_py + (int64_t)slot * n;
+    if (lead) a.slot_scale[slot] = 1.0;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int64_t g = r0 + t + (int64_t)q * RT;
+      w[q] = 0.0;
+      if (g < r1) {
+        double xc;
+        const double y = arow(a.st, a.X0, g, xc);
+        px[g] = xc;
+        py[g] = y;
+        const double rr = __ldg(a.b + g) - y;
+        V(0)[g] = rr;
+        w[q] = rr;
+      }
+    }
+    grid_reduce(1, [&](int) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) s = fma(w[q], w[q], s);
+      return s;
+    });
+    const double beta = sqrt(tot[0]);
+    matvecs += 1;
+    cycles += 1;
+    if (lead && blen < a.beta_cap) a.betas[blen] = beta;
+    blen += 1;
+    if (l == 1) r0v = beta;
+    if (!isfinite(beta)) { status = PSP_E_NONFINITE; break; }
+    if (beta <= eps) { finish = true; est = beta; break; }   // R3
+    if (t == 0) {
+      for (int q = 0; q <= nA; ++q) Gv[q] = 0.0;     // l.44 "clean"
+      Gv[0] = beta;                                    // l.7
+      al[0] = 1.0 / beta;                              // V(:,1) = R_bar / beta (l.6), lagged
+    }
+    __syncthreads();
+    int kdone = 0;
+    for (int k = 1; k <= nA; ++k) {                  // l.8
+      // ---- [A] l.10-12: Y_k = N^{-1} V(:,k) -> P_x, A Y_k -> P_y; l.13-16's inner products ----
+      slot = ring_next();
+      px = a.ring_px + (int64_t)slot * n;
+      py = a.ring_py + (int64_t)slot * n;
+      if (lead) a.slot_scale[slot] = 1.0;
+      const double ak = al[k - 1];
+      const double* Vk = V(k - 1);
+      if (seqN) {                                      // one CTA: the sequential sweeps
+        if (t == 0) seq_solve(a.lu, n, a.d, Vk, ak, a.y, px, nullptr);
+        __syncthreads();
+        papply += 1;
+      }
+      double vk[RMAX];
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int64_t g = r0 + t + (int64_t)q * RT;
+        w[q] = 0.0;
+        vk[q] = 0.0;
+        if (g < r1) {
+          double xc;
+          if (seqN) {
+            w[q] = arow(a.st, px, g, xc);
+            vk[q] = __ldcg(Vk + g);
+          } else {                                     // N = I: Y_k = alpha_k V(:,k)
+            const double y = arow(a.st, Vk, g, xc);
+            vk[q] = xc;
+            w[q] = ak * y;
+            px[g] = ak * xc;
+          }
+          py[g] = w[q];
+        }
+      }
+      matvecs += 1;
+      // s_j = V_j' w (j < k) at [0, k), l_j = V_j' V_k (j < k-1) at [k, 2k-1) (EPI_DOTS layout)
+      grid_reduce(2 * k - 1, [&](int v) {
+        const bool isl = v >= k;
+        const int j = isl ? v - k : v;
+        const double* Vj = V(j);
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < RMAX; ++q) {
+          const int64_t g = r0 + t + (int64_t)q * RT;
+          if (g < r1) s = fma(__ldcg(Vj + g), isl ? vk[q] : w[q], s);
+        }
+        return s;
+      });
+      if (t == 0) {                                    // (I + L) h = s (R11), as EPI_DOTS
+        double* Lrow = Lm + (int64_t)(k - 1) * ld;
+        for (int jb = 0; jb < k - 1; ++jb) Lrow[jb] = al[jb] * ak * tot[k + jb];
+        double* Hc = H + (int64_t)(k - 1) * ld;
+        for (int jb = 0; jb < k; ++jb) {
+          double h = al[jb] * tot[jb];
+          const double* Lr = Lm + (int64_t)jb * ld;
+          for (int c = 0; c < jb; ++c) h -= Lr[c] * Hc[c];
+          Hc[jb] = h;
+        }
+      }
+      __syncthreads();
+      // ---- [B] l.13-17: U = w - sum_j h_j alpha_j V_j -> V(:,k+1); H(k+1,k) = ||U|| ----
+      {
+        const double* Hc = H + (int64_t)(k - 1) * ld;
+        double* Vn = V(k);
+#pragma unroll
+        for (int q = 0; q < RMAX; ++q) {
+          const int64_t g = r0 + t + (int64_t)q * RT;
+          if (g < r1) {
+            double u = w[q];
+            for (int j = 0; j < k; ++j) u = fma(-(Hc[j] * al[j]), __ldcg(V(j) + g), u);
+            Vn[g] = u;
+            w[q] = u;
+          } else {
+            w[q] = 0.0;
+          }
+        }
+      }
+      grid_reduce(1, [&](int) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < RMAX; ++q) s = fma(w[q], w[q], s);
+        return s;
+      });
+      if (t == 0) {
+        H[(int64_t)(k - 1) * ld + k] = sqrt(tot[0]);  // l.17
+        givens_update(S, k, nA);                      // l.18-32 (R4 breakdown, R10)
+      }
+      __syncthreads();
+      const double R = sc[SC_RK];
+      const int flags = (int)sc[SC_FLAGS];
+      if (lead && hlen < a.hist_cap) a.hist[hlen] = R;
+      hlen += 1;
+      iters += 1;
+      est = R;
+      kdone = k;
+      if (flags & PSP_FLAG_NONFINITE) { status = PSP_E_NONFINITE; break; }
+      if (flags & (PSP_FLAG_CONVERGED | PSP_FLAG_BREAKDOWN)) { finish = true; break; }   // l.33-36
+    }
+    if (status != 0) break;
+    // ---- l.38-43: Q = H^{-1} G (R6); X = X0 + N^{-1} sum_j Q_j V_j; X0 <- X ----
+    if (t == 0) {
+      int bad = 0;
+      for (int j = kdone; j >= 1; --j) {
+        double s = Gv[j - 1];
+        for (int q = j + 1; q <= kdone; ++q) s -= H[(int64_t)(q - 1) * ld + (j - 1)] * Qv[q - 1];
+        const double piv = H[(int64_t)(j - 1) * ld + (j - 1)];
+        if (piv == 0.0) { bad = 1; Qv[j - 1] = 0.0; continue; }
+        Qv[j - 1] = s / piv;
+      }
+      sc[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
+    }
+    __syncthreads();
+    if (sc[SC_STATUS] != 0.0) { status = PSP_E_SINGULAR; break; }
+    double* zdst = seqN ? a.z : a.X0;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int64_t g = r0 + t + (int64_t)q * RT;
+      if (g < r1) {
+        double zz = seqN ? 0.0 : __ldcg(a.X0 + g);
+        for (int j = 0; j < kdone; ++j) zz = fma(Qv[j] * al[j], __ldcg(V(j) + g), zz);
+        zdst[g] = zz;
+      }
+    }
+    if (seqN) {
+      __syncthreads();
+      if (t == 0) {                                    // l.42: X = X0 + N^{-1} Z (Z consumed by
+        seq_solve(a.lu, n, a.d, a.z, 1.0, a.y, a.z, nullptr);   // the forward sweep, then reused)
+        for (int64_t i = 0; i < n; ++i) a.X0[i] = __ldcg(a.X0 + i) + a.z[i];
+      }
+      papply += 1;
+    }
+    grid_sync(a.bar, epoch);                           // X0 complete before the next probe
+    if (finish) break;                                 // l.45-48
+  }
+  // ---- R13: true residual ||b - A x|| (one unrecorded matvec) ----
+  double tr = 0.0;
+  if (status == 0) {
+    grid_reduce(1, [&](int) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int64_t g = r0 + t + (int64_t)q * RT;
+        if (g < r1) {
+          double xc;
+          const double rr = __ldg(a.b + g) - arow(a.st, a.X0, g, xc);
+          s = fma(rr, rr, s);
+        }
+      }
+      return s;
+    });
+    tr = sqrt(tot[0]);
+  }
+  if (lead) {
+    double* o = a.out;
+    o[O_ITER] = iters;
+    o[O_CYCLES] = cycles;
+    o[O_MATVECS] = matvecs;
+    o[O_PAPPLY] = papply;
+    o[O_FINISH] = finish ? 1.0 : 0.0;
+    o[O_STATUS] = status;
+    o[O_R0] = r0v;
+    o[O_EPS] = eps;
+    o[O_EST] = est;
+    o[O_TRUE] = tr;
+    o[O_HLEN] = hlen;
+    o[O_BLEN] = blen;
+    o[O_HEAD] = head;
+    o[O_COUNT] = count;
+  }
+  if (blockIdx.x == 0) {                               // the scalar state for the test hooks
+    for (int q = t; q < ld * nA; q += RT) a.ds.H[q] = H[q];
+    for (int q = t; q < ld * ld; q += RT) a.ds.Lm[q] = Lm[q];
+    for (int q = t; q < ld; q += RT) { a.ds.G[q] = Gv[q]; a.ds.alpha[q] = al[q]; }
+    for (int q = t; q < nA; q += RT) { a.ds.C[q] = Cv[q]; a.ds.S[q] = Sv[q]; a.ds.Q[q] = Qv[q]; a.ds.resid[q] = rs[q]; }
+  }
+}
+
+size_t res_smem(int nA) {
+  const size_t ld = nA + 1, PV = 2 * nA + 2;
+  return (ld * nA + ld * ld + ld + nA + nA + ld + nA + nA + SC_NSCAL + RW * PV + PV) * 8;
+}
+
+}  // namespace
+
+bool resident_supported(int64_t n, int nA, bool banded_n) {
+  if (nA > kResidentMaxRestart) return false;
+  if (banded_n && n > kResidentSeqRows) return false;
+  if (res_smem(nA) > 200 * 1024) return false;
+  const int64_t per_cta = (int64_t)RT * RMAX;
+  return n <= per_cta * device_sms();
+}
+
+int resident_grid(int64_t n, bool banded_n) {
+  if (banded_n || n <= kResidentOneCtaRows) return 1;
+  int64_t g = (n + RT - 1) / RT;                       // about one row per thread
+  const int64_t need = (n + (int64_t)RT * RMAX - 1) / ((int64_t)RT * RMAX);
+  if (g > device_sms()) g = device_sms();
+  if (g < need) g = need;
+  return (int)g;
+}
+
+size_t resident_scratch_doubles(int nA, int grid) { return (size_t)2 * grid * (2 * nA + 2); }
+
+int launch_resident(const ResidentCall& c, cudaStream_t s) {
+  ResArgs a;
+  a.st = c.st;
+  a.b = c.b;
+  a.X0 = c.X0;
+  a.V = c.V;
+  a.ldv = c.ldv;
+  a.ring_px = c.ring_px;
+  a.ring_py = c.ring_py;
+  a.slot_scale = c.slot_scale;
+  a.ring_cap = c.ring_cap;
+  a.ring_phys = c.ring_phys;
+  a.ring_head = c.ring_head;
+  a.ring_count = c.ring_count;
+  a.lu = c.lu;
+  a.d = c.d;
+  a.y = c.y;
+  a.z = c.z;
+  a.nA = c.nA;
+  a.max_cycles = c.max_cycles;
+  a.tol_abs = c.tol_abs;
+  a.tol = c.tol;
+  const int grid = c.grid;
+  a.chunk = (c.st.n + grid - 1) / grid;
+  a.partials = c.partials;
+  a.bar = c.bar;
+  a.hist = c.hist;
+  a.hist_cap = c.hist_cap;
+  a.betas = c.betas;
+  a.beta_cap = c.beta_cap;
+  a.out = c.out;
+  a.ds = c.ds;
+  const size_t smem = res_smem(c.nA);
+  const int dev = device_ordinal();
+  thread_local size_t attr[kMaxDev] = {};
+  if (attr[dev] < smem) {
+    if (cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return 1;
+    attr[dev] = smem;
+  }
+  cudaMemsetAsync(c.bar, 0, sizeof(unsigned long long), s);
+  void* args[] = {&a};
+  if (grid > 1) {
+    if (cudaLaunchCooperativeKernel((const void*)resident_kernel, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
+      return 1;
+  } else {
+    resident_kernel<<<1, RT, smem, s>>>(a);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace psp

@@ -9,6 +9,7 @@
 #include <stdlib.h>
 
 #include "internal.h"
+#include "stencil_row.cuh"
 
 #ifndef PSP_MARCH_MINB
 #define PSP_MARCH_MINB 3   // resident blocks per SM of the vectorised march kernel
@@ -17,87 +18,18 @@
 namespace psp {
 namespace {
 
-struct Nb {
-  double x, f;
-  bool in;
-};
-
-// neighbour of (i,j,k) along axis A, direction D (-1/+1).  Outside the local block: the slab
-// halo plane if present (multi-rank), else the Dirichlet zero (R24).
-template <int AXIS, int DIR>
-__device__ __forceinline__ Nb neighbour(const Stencil& st, const double* __restrict__ x,
-                                        const double* __restrict__ f, int64_t i, int64_t j,
-                                        int64_t k, int64_t g, bool need_f) {
-  Nb r{0.0, 0.0, false};
-  int64_t c = (AXIS == 0) ? i : (AXIS == 1 ? j : k);
-  int64_t ext = (AXIS == 0) ? st.nx : (AXIS == 1 ? st.ny : st.nz);
-  int64_t stride = (AXIS == 0) ? 1 : (AXIS == 1 ? st.nx : st.nx * st.ny);
-  int64_t cn = c + DIR;
-  if (cn >= 0 && cn < ext) {
-    r.x = __ldg(x + g + DIR * stride);
-    if (need_f) r.f = __ldg(f + g + DIR * stride);
-    r.in = true;
-    return r;
-  }
-  // leaving the local block along the slab axis: halo planes (the slowest axis of ndim)
-  const bool slab_axis = (st.ndim == 3 && AXIS == 2) || (st.ndim == 2 && AXIS == 1) ||
-                         (st.ndim == 1 && AXIS == 0);
-  if (slab_axis) {
-    const double* hx = (DIR < 0) ? st.x_lo : st.x_hi;
-    const double* hf = (DIR < 0) ? st.f_lo : st.f_hi;
-    if (hx != nullptr) {
-      int64_t off = (st.ndim == 3) ? (i + st.nx * j) : (st.ndim == 2 ? i : 0);
-      r.x = __ldg(hx + off);
-      if (need_f) r.f = __ldg(hf + off);
-      r.in = true;
-    }
-  }
-  return r;
-}
-
 template <int KIND, int NDIM>
 __global__ void __launch_bounds__(128) matvec_kernel(Stencil st, const double* __restrict__ x,
                                                      const double* xsp, double* __restrict__ y,
                                                      double* __restrict__ xcopy) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
-  const int64_t k = blockIdx.z;
   if (i >= st.nx) return;
-  const int64_t g = i + st.nx * (j + st.ny * k);
-  const double* __restrict__ f = st.field;
-  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  const int64_t g = i + st.nx * (blockIdx.y + st.ny * (int64_t)blockIdx.z);
   const double xs = xsp ? *xsp : 1.0;
-  const double xc = __ldg(x + g);
-  const double fc = cell ? __ldg(f + g) : 0.0;
-  double acc = 0.0;  // sum over faces of s_a * k_f * (x_c - x_nb) + upwind terms
-  auto face = [&](const Nb& nb, double s) {
-    double kf = cell ? (nb.in ? 0.5 * (fc + nb.f) : fc) : 1.0;
-    acc = fma(s * kf, xc - nb.x, acc);
-  };
-  {
-    Nb w = neighbour<0, -1>(st, x, f, i, j, k, g, cell);
-    Nb e = neighbour<0, +1>(st, x, f, i, j, k, g, cell);
-    face(w, st.s[0]);
-    face(e, st.s[0]);
-    if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], xc - w.x, acc);
-  }
-  if (NDIM >= 2) {
-    Nb sn = neighbour<1, -1>(st, x, f, i, j, k, g, cell);
-    Nb nn = neighbour<1, +1>(st, x, f, i, j, k, g, cell);
-    face(sn, st.s[1]);
-    face(nn, st.s[1]);
-    if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], xc - sn.x, acc);
-  }
-  if (NDIM >= 3) {
-    Nb b = neighbour<2, -1>(st, x, f, i, j, k, g, cell);
-    Nb t = neighbour<2, +1>(st, x, f, i, j, k, g, cell);
-    face(b, st.s[2]);
-    face(t, st.s[2]);
-    if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], xc - b.x, acc);
-  }
-  // A x = x - dt L x;  -dt L x = sum_faces s k_f (x_c - x_nb) + sum_a a_a (x_c - x_w)
+  double xc;
+  const double ax = stencil_row<KIND, NDIM>(st, x, i, blockIdx.y, blockIdx.z, g, xc);
   // (the scale xs is linear: applied once to the result and to the probe copy)
-  y[g] = xs * (xc + acc);
+  y[g] = xs * ax;
   if (xcopy != nullptr) xcopy[g] = xs * xc;
 }
 

@@ -24,7 +24,7 @@ PSP_OP_CONST_DIFF, PSP_OP_CELL_DIFF, PSP_OP_CELL_ADVDIFF, PSP_OP_DIA = range(4)
 PSP_TOL_REL_B, PSP_TOL_ABS = 0, 1
 PSP_MGS_1REDUCE, PSP_MGS_LITERAL = 0, 1
 PSP_FLAG_CONVERGED, PSP_FLAG_BREAKDOWN, PSP_FLAG_NONFINITE = 1, 2, 4
-PSP_KC_COUNT = 12
+PSP_KC_COUNT = 14
 ROW_INTERIOR, ROW_INTERIOR_RIDGE, ROW_BOUNDARY, ROW_FALLBACK_RANK, ROW_FALLBACK_ZEROVAR, \
     ROW_FALLBACK_SMALLDIAG = range(6)
 KIND_CODES = {"const_diff": PSP_OP_CONST_DIFF, "cell_diff": PSP_OP_CELL_DIFF,
@@ -47,7 +47,7 @@ class psp_opts(C.Structure):
     _fields_ = [("max_cycles", C.c_int32), ("tol_mode", C.c_int32), ("m_max", C.c_int32),
                 ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
                 ("timing", C.c_int32), ("fused", C.c_int32), ("fused_kmin", C.c_int32),
-                ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32)]
+                ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32), ("resident", C.c_int32)]
 
 
 class psp_report(C.Structure):

@@ -183,7 +183,7 @@ def _lockstep_c4(torch, P, orc, size, max_cycles, with_mrep):
     """C4 recipe at size^3 with the bench's default options (fused passes from 2^21 rows on,
     split-column steps beyond k = 16, the fused last-step combine): the first time step (N = I
     on both sides, b = x0 = u0) on the GPU and in the oracle, compared by T4-T6 (DESIGN.md s.7)."""
-    from test_gpu_parity import compare_mrep, compare_solve, log_parity, oracle_sensitivity
+    from test_gpu_parity import MREP_EXCLUDED_MAX, compare_mrep, compare_solve, log_parity, oracle_sensitivity
     prob = inputs.c4(n=size, steps=1)
     n = prob.op.rows
     b = prob.u0
@@ -212,7 +212,7 @@ def _lockstep_c4(torch, P, orc, size, max_cycles, with_mrep):
         px, py = PX.cpu().numpy(), PY.cpu().numpy()
         g = P.psp_mrep_fit_raw(PX.contiguous(), PY.contiguous(), prob.d)
         r = orc.mrep(px, py, prob.d)
-        ex = compare_mrep(g, r, prob.d, n, px, max_excluded_frac=1.0)
+        ex = compare_mrep(g, r, prob.d, n, px, max_excluded_frac=MREP_EXCLUDED_MAX)
         log_parity(case=f"C4-{size}-full", step=0, mrep_excluded=int(ex), rows=n)
         bands, _ = ctx.psp_get_bands()
         # psp_mrep_fit (scaled ring columns) and psp_mrep_fit_raw (the same columns, scaled by

@@ -281,14 +281,16 @@ def test_mrep_insufficient_samples(torch, P):
 # ------------------------------------------------------------------------------------------
 # T4-T6: Algorithm 1 and the time-step driver
 # ------------------------------------------------------------------------------------------
-MODES = {"fused": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=32),      # every step one fused pass
-         "ring": dict(ortho=0, fused=2),                                      # default mix, forced at small n
+MODES = {"fused": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=32, resident=0),  # every step one fused pass
+         "ring": dict(ortho=0, fused=2, resident=0),                          # default mix, forced at small n
          # split-column steps (update + fused over the newest columns + dots) from k = 3 / k = 13
-         "hybrid": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=2, fused_split_cols=2),
-         "hybrid12": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=12, fused_split_cols=12),
-         "ringauto": dict(ortho=0, fused=1),                                  # default options (small n: split)
-         "ringsplit": dict(ortho=0, fused=1, fused_kmin=99, fused_kmax=0),   # ring, no fused pass
-         "split": dict(ortho=0, fused=0), "literal": dict(ortho=1, fused=0)}
+         "hybrid": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=2, fused_split_cols=2, resident=0),
+         "hybrid12": dict(ortho=0, fused=2, fused_kmin=0, fused_kmax=12, fused_split_cols=12, resident=0),
+         "ringauto": dict(ortho=0, fused=1, resident=0),                      # host-driven defaults (small n: split)
+         "ringsplit": dict(ortho=0, fused=1, fused_kmin=99, fused_kmax=0, resident=0),   # ring, no fused pass
+         "split": dict(ortho=0, fused=0, resident=0), "literal": dict(ortho=1, fused=0, resident=0),
+         # f2: the whole solve as one persistent device-resident kernel (resident.cu)
+         "resident": dict(ortho=0, resident=2)}
 
 
 def run_gpu_steps(torch, P, prob, steps, mode):
@@ -318,10 +320,13 @@ def oracle_sensitivity(orc, prob, b, N_used, ho, u_ref, max_cycles=None):
     L = min(len(hp), len(ho))
     env = np.maximum.accumulate(np.abs(hp[:L] - ho[:L]) / np.maximum(ho[:L], 1e-300))
     env = np.concatenate([env, np.full(max(0, len(ho) - L), env[-1] if L else 1.0)])
-    return env, np.linalg.norm(rp["x"] - u_ref)
+    return env, (np.linalg.norm(rp["x"] - u_ref) if u_ref is not None else None)
 
 
 PARITY_LOG = os.environ.get("PSP_PARITY_LOG")   # measurement runs: per-cycle parity floors (T4)
+T4_FLOOR = 1e-11     # x beta_c: measured GPU-oracle floor 5.3e-12 beta_c (r02, tests/test_gpu_parity.py log)
+T4_ENV = 128.0       # x the oracle's self-perturbation envelope after the first restart (measured <= 89)
+MREP_EXCLUDED_MAX = 0.3   # lockstep 3-D probe rings: rounding-decided ridge rows, measured <= 0.28
 
 
 def log_parity(**kw):
@@ -356,19 +361,25 @@ def compare_solve(gr, o, ho, s, env=None, nA=None, case=None):
     assert gr["converged"] == 1 and o["converged"] == 1
     hg = gr["resid_history"]
     L = min(len(hg), len(ho))
-    if nA is not None:
-        log_parity(case=case, step=s, iterations=[gr["iterations"], o["iterations"]],
-                   cycles=cycle_floor_stats(hg, ho, gr["beta_history"], nA, env))
-    # T4: relative 1e-8 above the FP64 floor of the recursively updated residual estimate,
-    # whose absolute noise after restarts is O(u kappa(A) ||r0||), widened after the first
-    # cycle to 30x the oracle's own sensitivity envelope
-    beta1 = gr["beta_history"][0]
-    tol = 1e-8 * ho[:L] + 1e-10 * beta1
+    nA = nA or len(ho) or 1
+    # T4: relative 1e-8 plus an additive floor of T4_FLOOR times the
+    # cycle's own beta_c, the measured GPU-oracle floor of the recursively updated
+    # estimate (max 5.3e-12 beta_c, C2 at the FP64 floor, r02 parity log).  After the first
+    # restart, restarted GMRES amplifies rounding: cycles >= 2 add T4_ENV times the oracle's
+    # own response to a 1e-15 relative perturbation of x0 (measured GPU-oracle / envelope ratio
+    # <= 89 over every lockstep case and mode)
+    betas = gr["beta_history"]
+    cyc = np.arange(L) // nA
+    bc = np.asarray(betas)[np.minimum(cyc, len(betas) - 1)] if len(betas) else np.zeros(L)
+    tol = 1e-8 * ho[:L] + T4_FLOOR * bc
     if env is not None:
-        tol = tol + 30.0 * env[:L] * ho[:L]
+        tol = tol + np.where(cyc >= 1, T4_ENV * env[:L] * ho[:L], 0.0)
     q = np.abs(hg[:L] - ho[:L]) / tol
     w = int(np.argmax(q)) if L else 0
-    assert np.all(q <= 1), (s, q[w], w, hg[max(0, w - 2):w + 3], ho[max(0, w - 2):w + 3], beta1,
+    if case is not None:
+        log_parity(case=case, step=s, iterations=[gr["iterations"], o["iterations"]], q_max=float(q[w]) if L else 0.0,
+                   cycles=cycle_floor_stats(hg, ho, gr["beta_history"], nA, env))
+    assert np.all(q <= 1), (s, q[w], w, hg[max(0, w - 2):w + 3], ho[max(0, w - 2):w + 3], bc[w] if L else None,
                             gr["beta_history"][:gr["cycles"]])
     assert gr["final_resid_true"] <= 1.05 * gr["eps"]
 
@@ -432,7 +443,7 @@ def test_lockstep_parity(torch, P, orc, name, mk, steps, mode):
             # dependent (kappa(Gram) up to 1e16), so the unridged/ridged decision of those rows
             # is decided by rounding; they are excluded from the kind/coefficient comparison
             # (every excluded row has kappa_est > 1e9 on one side, by construction)
-            ex = compare_mrep(g, o, prob.d, n, px, max_excluded_frac=1.0)
+            ex = compare_mrep(g, o, prob.d, n, px, max_excluded_frac=MREP_EXCLUDED_MAX)
             log_parity(case=f"{name}/{mode}", step=s, mrep_excluded=int(ex), rows=n)
             assert o["gate_accepted"] == r["mrep"]["gate_accepted"]
         u = r["u"]
@@ -453,7 +464,9 @@ def test_free_running_c1(torch, P, orc, mode):
         assert gr["converged"] == 1 and gr["final_resid_true"] <= 1.05 * gr["eps"]
         assert gr["precond_identity"] == int(orr["precond_was_identity"])
         assert bool(gr["mrep_gate_accepted"]) == orr["mrep"]["gate_accepted"]
-    compare_solve(g["reports"][0], r["reports"][0]["solve"], r["reports"][0]["resid_hist"], 0)
+    env, _ = oracle_sensitivity(orc, prob, prob.u0, None, r["reports"][0]["resid_hist"], None)
+    compare_solve(g["reports"][0], r["reports"][0]["solve"], r["reports"][0]["resid_hist"], 0, env,
+                  nA=prob.restart, case=f"C1-free/{mode}")
     rr = 1e-3 * 1025.0 ** 2
     ref = np.array([-rr, 1 + 2 * rr, -rr])[:, None]
     assert np.max(np.abs(g["bands"][:, 1:-1] - ref)) <= 1e-9 * (1 + 2 * rr)
@@ -517,10 +530,14 @@ def test_edge_cases(torch, P, orc):
     assert rep["iterations"] == 1
 
 
-def test_determinism(torch, P):
-    prob = inputs.c1(n=512, steps=2)
-    a = run_gpu_steps(torch, P, prob, 2, "fused")
-    b = run_gpu_steps(torch, P, prob, 2, "fused")
+@pytest.mark.parametrize("mode,mk", [("fused", lambda: inputs.c1(n=512, steps=2)),
+                                     ("resident", lambda: inputs.c1(n=512, steps=2)),
+                                     ("resident", lambda: inputs.c2(n=128, d=1, steps=2))],
+                         ids=["fused-c1", "resident-c1", "resident-c2-multicta"])
+def test_determinism(torch, P, mode, mk):
+    prob = mk()
+    a = run_gpu_steps(torch, P, prob, 2, mode)
+    b = run_gpu_steps(torch, P, prob, 2, mode)
     assert np.array_equal(a["u"], b["u"])
     assert np.array_equal(a["reports"][0]["resid_history"], b["reports"][0]["resid_history"])
 
