@@ -545,6 +545,99 @@ int orc_mrep(int64_t n, int m, const double* px, const double* py, int64_t ld, c
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* f4. PSP with conjugate gradients ("the methodology can be readily applied to all   */
+/* Krylov subspace methods"); readings R27-R31.                                           */
+/* ------------------------------------------------------------------------------------ */
+void orc_sym_bands(int64_t n, int d, const double* bands, double* sym) {
+  /* R29: N_s(i, j) = (N(i, j) + N(j, i)) / 2, j = i + o - d; N(j, i) = band 2d - o of row j */
+  for (int o = 0; o <= 2 * d; ++o) {
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t j = i + o - d;
+      if (j < 0 || j >= n) { BAND(sym, n, o, i) = 0.0; continue; }
+      BAND(sym, n, o, i) = 0.5 * (BAND(bands, n, o, i) + BAND(bands, n, 2 * d - o, j));
+    }
+  }
+}
+
+int orc_gate_spd(int64_t n, int d, const double* bands) {
+  /* R29: positive diagonal and strict diagonal dominance => symmetric positive definite */
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(BAND(bands, n, d, i) > 0.0)) return 0;
+  }
+  return orc_gate_dominant(n, d, bands);
+}
+
+int orc_pcg(const orc_operator* A, const double* b, const double* x0, double* x, int d, const double* lu,
+            double eps, int max_iters, orc_ring* ring, orc_solve_report* rep, double* resid_hist,
+            int hist_cap) {
+  const int64_t n = orc_op_rows(A);
+  memset(rep, 0, sizeof(*rep));
+  rep->eps = eps;
+  double* r = (double*)malloc((size_t)n * sizeof(double));
+  double* z = (double*)malloc((size_t)n * sizeof(double));
+  double* p = (double*)malloc((size_t)n * sizeof(double));
+  double* q = (double*)malloc((size_t)n * sizeof(double));
+  double* w = (double*)malloc((size_t)n * sizeof(double));
+  int status = ORC_OK, finish = 0;
+  copy(n, x0, x);
+  orc_matvec(A, x, q);                                  /* the probe (x0, A x0), as Alg.1 l.4 */
+  if (ring) orc_ring_record(ring, x, q);
+  rep->matvecs = 1;
+  rep->cycles = 1;
+  for (int64_t t = 0; t < n; ++t) r[t] = b[t] - q[t];   /* r = b - A x0 */
+  double rn = norm2(n, r);
+  rep->r0 = rn;
+  rep->final_resid_est = rn;
+  if (!isfinite(rn)) status = ORC_E_NONFINITE;
+  else if (rn <= eps) finish = 1;                       /* R3 */
+  double rho = 0.0;
+  if (status == ORC_OK && !finish) {
+    precond_solve(n, d, lu, r, z);                      /* z = M^-1 r */
+    if (lu) rep->precond_applies += 1;
+    copy(n, z, p);                                      /* p = z */
+    rho = dot(n, r, z);
+  }
+  for (int k = 1; status == ORC_OK && !finish && k <= max_iters; ++k) {
+    orc_matvec(A, p, q);                                /* q = A p */
+    rep->matvecs += 1;
+    if (ring) {                                         /* R28: the probe (p, A p) / ||p||     */
+      double pn = norm2(n, p);
+      for (int64_t t = 0; t < n; ++t) { z[t] = p[t] / pn; w[t] = q[t] / pn; }
+      orc_ring_record(ring, z, w);
+    }
+    double pq = dot(n, p, q);
+    if (!isfinite(pq)) { status = ORC_E_NONFINITE; break; }
+    if (!(pq > 0.0)) { status = ORC_E_SINGULAR; break; } /* R30: A (or M) not SPD */
+    double alpha = rho / pq;
+    for (int64_t t = 0; t < n; ++t) x[t] = x[t] + alpha * p[t];
+    for (int64_t t = 0; t < n; ++t) r[t] = r[t] - alpha * q[t];
+    double Rk = norm2(n, r);                            /* R(k): the recursive residual */
+    if (resid_hist && rep->hist_len < hist_cap) resid_hist[rep->hist_len] = Rk;
+    rep->hist_len += 1;
+    rep->iterations += 1;
+    rep->final_resid_est = Rk;
+    if (!isfinite(Rk)) { status = ORC_E_NONFINITE; break; }
+    if (Rk <= eps) { finish = 1; break; }
+    precond_solve(n, d, lu, r, z);                      /* z = M^-1 r */
+    if (lu) rep->precond_applies += 1;
+    double rho1 = dot(n, r, z);
+    double beta = rho1 / rho;
+    rho = rho1;
+    for (int64_t t = 0; t < n; ++t) p[t] = z[t] + beta * p[t];
+  }
+  if (status == ORC_OK) {
+    orc_matvec(A, x, q);                                /* R13: true residual, not recorded */
+    for (int64_t t = 0; t < n; ++t) r[t] = b[t] - q[t];
+    rep->final_resid_true = norm2(n, r);
+    rep->converged = finish;
+    if (!finish) status = ORC_E_NOCONV;
+  }
+  rep->status = status;
+  free(r); free(z); free(p); free(q); free(w);
+  return status;
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* O5. Time-step driver: N_1 = I; u^{n+1} = PSPGMRES(A, u^n, N_n, ...); N_{n+1} = MREP.  */
 /* (Eq.3-4; "used as a preconditioner ... for the next time step").       */
 /* ------------------------------------------------------------------------------------ */
@@ -565,10 +658,16 @@ int orc_time_steps(const orc_operator* A, double* u, int steps, const orc_step_o
     copy(n, u, b);                                 /* b := u^n (Eq.4 right-hand side) */
     double eps = opt->tol * norm2(n, b);           /* R1 */
     R->precond_was_identity = *n_is_identity;
-    int st = orc_pspgmres(A, b, u, x, d, *n_is_identity ? NULL : lu_N, eps, opt->restart,
-                          opt->max_cycles, ring, &R->solve,
-                          resid_hist ? resid_hist + hist_used : NULL,
-                          resid_hist ? hist_cap - hist_used : 0, NULL, 0, NULL);
+    int st;
+    if (opt->method == ORC_METHOD_CG)                /* f4: PSP-CG (R27-R31) */
+      st = orc_pcg(A, b, u, x, d, *n_is_identity ? NULL : lu_N, eps, opt->restart * opt->max_cycles, ring,
+                   &R->solve, resid_hist ? resid_hist + hist_used : NULL,
+                   resid_hist ? hist_cap - hist_used : 0);
+    else
+      st = orc_pspgmres(A, b, u, x, d, *n_is_identity ? NULL : lu_N, eps, opt->restart,
+                        opt->max_cycles, ring, &R->solve,
+                        resid_hist ? resid_hist + hist_used : NULL,
+                        resid_hist ? hist_cap - hist_used : 0, NULL, 0, NULL);
     if (resid_hist) hist_used += (R->solve.hist_len < hist_cap - hist_used ? R->solve.hist_len : hist_cap - hist_used);
     if (st == ORC_E_NONFINITE || st == ORC_E_SINGULAR || st == ORC_E_ARG) { worst = st; break; }
     if (st != ORC_OK && worst == ORC_OK) worst = st;
@@ -580,6 +679,15 @@ int orc_time_steps(const orc_operator* A, double* u, int steps, const orc_step_o
       for (int c = 0; c < m; ++c) order[c] = orc_ring_slot(ring, c);
       int mst = orc_mrep(n, m, ring->px, ring->py, n, order, d, fit, NULL, NULL, NULL, &R->mrep);
       R->mrep_ran = (mst == ORC_OK);
+      if (mst == ORC_OK && opt->method == ORC_METHOD_CG) {
+        /* R29: CG needs a symmetric positive definite preconditioner: N_s = (N + N^T) / 2,
+         * gated by positive-diagonal strict dominance */
+        double* sym = (double*)malloc((size_t)n * (size_t)(2 * d + 1) * sizeof(double));
+        orc_sym_bands(n, d, fit, sym);
+        copy(n * (int64_t)(2 * d + 1), sym, fit);
+        free(sym);
+        R->mrep.gate_accepted = orc_gate_spd(n, d, fit);
+      }
       int accept = (mst == ORC_OK) && (R->mrep.gate_accepted || !opt->gate);
       if (accept) {
         if (orc_banded_lu(n, d, fit, lu_N) == ORC_OK) {

@@ -133,15 +133,38 @@ int orc_mrep(int64_t n, int m, const double* px, const double* py, int64_t ld, c
              int d, double* bands, double* intercept, uint8_t* row_kind, double* kappa_est,
              orc_mrep_report* rep);
 
+/* ---- f4: PSP with conjugate gradients (the method "can be readily applied to all
+ * Krylov subspace methods"; readings R27-R31 of DESIGN.md) ---- */
+/* R29: the symmetric part N_s = (N + N^T) / 2 of a DIA banded N: sym[o*n+i] = (N(i,i+o-d) +
+ * N(i+o-d,i)) / 2, the second term read from band 2d-o of row i+o-d. */
+void orc_sym_bands(int64_t n, int d, const double* bands, double* sym);
+/* R29: 1 iff every row of the (symmetric) bands is strictly diagonally dominant with a
+ * positive diagonal -- then N_s is symmetric positive definite (Gershgorin). */
+int orc_gate_spd(int64_t n, int d, const double* bands);
+/* R27/R28/R30: preconditioned CG (Hestenes-Stiefel) with M = the banded matrix whose LU factors
+ * are lu (NULL: M = I):  r = b - A x0 (the probe (x0, A x0) is recorded, as Alg.1 l.4),
+ * z = M^-1 r, p = z, rho = r'z; for k = 1..max_iters: q = A p (the probe (p, q)/||p|| is
+ * recorded: unit-norm like Alg.1's Krylov probes, so Alg.2's intercept row is commensurate),
+ * pq = p'q (pq <= 0 or non-finite: A or M not SPD -> ORC_E_SINGULAR), alpha = rho / pq,
+ * x += alpha p, r -= alpha q, R(k) = ||r|| (history; R(k) <= eps stops), z = M^-1 r,
+ * rho' = r'z, p = z + (rho'/rho) p.  Then the true residual ||b - A x|| (R13).  cycles = 1;
+ * ORC_E_NOCONV after max_iters. */
+int orc_pcg(const orc_operator* A, const double* b, const double* x0, double* x, int d, const double* lu,
+            double eps, int max_iters, orc_ring* ring, orc_solve_report* rep, double* resid_hist,
+            int hist_cap);
+
 /* ---- O5: time-step driver (Eq.3-4; "next time step") ---- */
+enum { ORC_METHOD_GMRES = 0, ORC_METHOD_CG = 1 };
 typedef struct {
   int32_t restart;          /* n_A                                                  */
-  int32_t max_cycles;       /* n_r                                                  */
+  int32_t max_cycles;       /* n_r (CG: at most n_A * n_r iterations, R31)          */
   double tol;               /* eps = tol * ||b||_2 (R1)                             */
   int32_t d;                /* MREP half-bandwidth                                  */
   int32_t m_max;            /* ring capacity                                        */
   int32_t reset_history;    /* clear the ring at the start of every step     */
   int32_t gate;             /* apply R21 (1) or accept any factorable N (0)          */
+  int32_t method;           /* ORC_METHOD_*: the Krylov method of the step (f4)      */
+  int32_t pad_;
 } orc_step_opts;
 
 typedef struct {

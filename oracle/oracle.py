@@ -54,7 +54,11 @@ class _MrepReport(C.Structure):
 
 class _StepOpts(C.Structure):
     _fields_ = [("restart", C.c_int32), ("max_cycles", C.c_int32), ("tol", C.c_double), ("d", C.c_int32),
-                ("m_max", C.c_int32), ("reset_history", C.c_int32), ("gate", C.c_int32)]
+                ("m_max", C.c_int32), ("reset_history", C.c_int32), ("gate", C.c_int32), ("method", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+METHOD_GMRES, METHOD_CG = 0, 1
 
 
 class _StepReport(C.Structure):
@@ -93,6 +97,11 @@ def lib():
         L.orc_pspgmres.argtypes = [C.POINTER(_Operator), _dp, _dp, _dp, C.c_int, _dp, C.c_double, C.c_int,
                                    C.c_int, C.POINTER(_Ring), C.POINTER(_SolveReport), _dp, C.c_int, _dp,
                                    C.c_int, C.POINTER(_Trace)]
+        L.orc_pcg.argtypes = [C.POINTER(_Operator), _dp, _dp, _dp, C.c_int, _dp, C.c_double, C.c_int,
+                              C.POINTER(_Ring), C.POINTER(_SolveReport), _dp, C.c_int]
+        L.orc_sym_bands.argtypes = [C.c_int64, C.c_int, _dp, _dp]
+        L.orc_sym_bands.restype = None
+        L.orc_gate_spd.argtypes = [C.c_int64, C.c_int, _dp]
         L.orc_mrep.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.c_int64, C.POINTER(C.c_int), C.c_int, _dp, _dp,
                                C.POINTER(C.c_uint8), _dp, C.POINTER(_MrepReport)]
         L.orc_time_steps.argtypes = [C.POINTER(_Operator), _dp, C.c_int, C.POINTER(_StepOpts),
@@ -258,6 +267,35 @@ def pspgmres(spec, b, x0, eps, n_A, n_r, d=1, lu=None, ring: Ring | None = None,
     return out
 
 
+def pcg(spec, b, x0, eps, max_iters, d=1, lu=None, ring: Ring | None = None, hist_cap=None):
+    """f4: preconditioned CG with probe recording (orc_pcg, readings R27-R31).  lu = LU factors of the
+    (symmetric) preconditioner, None for M = I.  Returns dict(x, report, resid_hist)."""
+    o, _k = _op(spec)
+    b = _f64(np.asarray(b).reshape(-1))
+    x0 = _f64(np.asarray(x0).reshape(-1))
+    x = np.empty_like(b)
+    hist_cap = hist_cap or max_iters
+    hist = np.zeros(hist_cap)
+    rep = _SolveReport()
+    lu_a = _f64(lu) if lu is not None else None
+    st = lib().orc_pcg(C.byref(o), _p(b), _p(x0), _p(x), d, _p(lu_a), float(eps), int(max_iters),
+                       C.byref(ring.s) if ring is not None else None, C.byref(rep), _p(hist), hist_cap)
+    return dict(status=st, x=x, report=_report(rep), resid_hist=hist[:min(rep.hist_len, hist_cap)])
+
+
+def sym_bands(bands, d):
+    """R29: N_s = (N + N^T) / 2 in DIA storage."""
+    bands = _f64(bands)
+    out = np.zeros_like(bands)
+    lib().orc_sym_bands(bands.shape[1], d, _p(bands), _p(out))
+    return out
+
+
+def gate_spd(bands, d) -> bool:
+    bands = _f64(bands)
+    return bool(lib().orc_gate_spd(bands.shape[1], d, _p(bands)))
+
+
 def mrep(px, py, d, order=None):
     """Literal Algorithm 2.  px, py: (m, n) arrays (row c = probe column c, oldest -> newest
     unless ``order`` gives the slot of each column)."""
@@ -284,7 +322,8 @@ def mrep(px, py, d, order=None):
 class Driver:
     """O5 one step at a time, keeping the ring and N across calls (for lockstep parity)."""
 
-    def __init__(self, spec, n, restart, max_cycles, tol, d, m_max, reset_history=False, gate=True):
+    def __init__(self, spec, n, restart, max_cycles, tol, d, m_max, reset_history=False, gate=True,
+                 method=METHOD_GMRES):
         self.spec = spec
         self.n = n
         self.d = d
@@ -292,7 +331,7 @@ class Driver:
         self.bands = np.zeros((2 * d + 1, n))
         self.lu = np.zeros((2 * d + 1, n))
         self.ident = C.c_int(1)
-        self.opts = _StepOpts(restart, max_cycles, float(tol), d, m_max, int(reset_history), int(gate))
+        self.opts = _StepOpts(restart, max_cycles, float(tol), d, m_max, int(reset_history), int(gate), int(method))
         self.hist_cap = restart * max_cycles
 
     def step(self, u):
@@ -313,7 +352,7 @@ class Driver:
 
 
 def time_steps(spec, u0, steps, restart, max_cycles, tol, d, m_max, reset_history=False, gate=True,
-               hist_cap=None):
+               hist_cap=None, method=METHOD_GMRES):
     """O5: the implicit-Euler driver.  Returns dict(u, reports, resid_hist, bands, is_identity)."""
     o, _k = _op(spec)
     u = _f64(np.asarray(u0).reshape(-1)).copy()
@@ -326,7 +365,7 @@ def time_steps(spec, u0, steps, restart, max_cycles, tol, d, m_max, reset_histor
     reps = (_StepReport * steps)()
     hist_cap = hist_cap or restart * max_cycles * steps
     hist = np.zeros(hist_cap)
-    opts = _StepOpts(restart, max_cycles, float(tol), d, m_max, int(reset_history), int(gate))
+    opts = _StepOpts(restart, max_cycles, float(tol), d, m_max, int(reset_history), int(gate), int(method))
     st = lib().orc_time_steps(C.byref(o), _p(u), steps, C.byref(opts), C.byref(ring.s), _p(bands), _p(lu),
                               C.byref(ident), reps, _p(hist), hist_cap)
     reports = []
