@@ -76,6 +76,12 @@ typedef struct {
 
 enum { PSP_TOL_REL_B = 0, PSP_TOL_ABS = 1 };       /* eps = tol*||b|| (R1) or eps = tol    */
 enum { PSP_MGS_1REDUCE = 0, PSP_MGS_LITERAL = 1 }; /* R11                                   */
+/* PSP_METHOD_CG (f4; R27-R31): preconditioned conjugate gradients (Hestenes-Stiefel) for
+ * symmetric positive definite A (C1, C2, C4), at most restart * max_cycles iterations; the
+ * probes are (p_k, A p_k) / ||p_k|| (plus (x0, A x0)); the preconditioner is the symmetric part
+ * N_s = (N + N^T) / 2 of the fitted N, accepted when every row is strictly diagonally dominant
+ * with a positive diagonal (so N_s is SPD).  One rank. */
+enum { PSP_METHOD_GMRES = 0, PSP_METHOD_CG = 1 };
 
 typedef struct {
   int32_t max_cycles;              /* n_r (R9); default 1000                                */
@@ -106,6 +112,9 @@ typedef struct {
                                    /* 0 off; 1 (default) for single-rank ICWY solves of up to  */
                                    /* 2^20 rows with n_A <= 64 (a banded N: up to 16384 rows); */
                                    /* 2 whenever supported                                    */
+  int32_t method;                  /* PSP_METHOD_*: the Krylov method of psp_solve / psp_step */
+                                   /* (f4: "readily applied to all Krylov subspace       */
+                                   /* methods"); default PSP_METHOD_GMRES                     */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */

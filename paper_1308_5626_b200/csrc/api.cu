@@ -376,6 +376,9 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   if (opts) o = *opts; else psp_default_opts(&o);
   PSP_TRY(validate(grid, st, d, restart, &o));
   if (!(tol > 0.0) || !(dt >= 0.0)) return fail(nullptr, PSP_E_ARG, "tol must be > 0 and dt >= 0");
+  if (o.method != PSP_METHOD_GMRES && o.method != PSP_METHOD_CG) return fail(nullptr, PSP_E_ARG, "bad method");
+  if (o.method == PSP_METHOD_CG && comm && comm->nranks > 1)
+    return fail(nullptr, PSP_E_ARG, "PSP-CG is single-rank (the symmetric part of N needs the neighbours' rows)");
   int64_t n, row0, slab0, slab_len, plane;
   PSP_TRY(local_layout(grid, st, d, comm, &n, &row0, &slab0, &slab_len, &plane));
   const int nranks = comm ? comm->nranks : 1;
@@ -451,6 +454,7 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ds.partials = (double*)at(p.off_partials);
   c->ds.tickets = (unsigned*)at(p.off_tickets);
   c->ds.rpart = (double*)at(p.off_rpart);
+  c->ds.slot_scale = c->slot_scale;
   c->ds.multi = c->multi ? 1 : 0;
   c->rc.nblocks = p.nblocks;
   c->rc.max_vals = 2 * kMaxRestart;
@@ -974,10 +978,105 @@ psp_status psp_cycle_end(psp_ctx* c, int k, double* x) {
   return check_cuda(c, "psp_cycle_end");
 }
 
+// f4: PSP with preconditioned conjugate gradients (readings R27-R31; oracle/oracle.c orc_pcg).
+// Vectors: x in X0, r = V(:,1), z = V(:,2) (z aliases r when N = I); the direction p_k and A p_k
+// live in the probe ring slot of step k (the probe (p_k, A p_k) / ||p_k|| is recorded with
+// slot_scale = 1/||p_k||, so recording costs no copy), p_{k-1} in the previous slot.
+static psp_status cg_solve(psp_ctx* c, const double* b, const double* x0, psp_report* R, double eps) {
+  const int64_t n = c->n;
+  const double dn = (double)n;
+  const bool ident = c->n_identity;
+  if (x0 != c->X0) {
+    launch_copy(x0, c->X0, n, c->stream);
+    c->launches += 1;
+  }
+  c->cycle_fused = false;
+  double* r = Vcol(c, 1);
+  double* z = ident ? r : Vcol(c, 2);
+  // the probe (x0, A x0) (as Alg.1 l.4), r0 = b - A x0
+  const int s0 = ring_next(c);
+  set_unit_scale(c, s0);
+  int h = kt_begin(c);
+  PSP_TRY(matvec(c, c->X0, nullptr, py_col(c, s0), px_col(c, s0)));
+  kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+  h = kt_begin(c);
+  launch_cg_start(b, py_col(c, s0), r, n, c->ds, c->rc, c->stream);
+  c->launches += 1;
+  PSP_TRY(finish_reduce(c, EPI_CG_START, 1, 0, 1, 0));
+  kt_end(c, h, PSP_KC_CG, 24.0 * dn);
+  R->matvecs = 1;
+  R->cycles = 1;
+  if (!ident) {                                       // z0 = M^-1 r0, rho = r0'z0
+    h = kt_begin(c);
+    PSP_TRY(precond_scaled(c, r, nullptr, z));
+    kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
+    launch_cg_rz(r, z, n, c->ds, c->rc, c->stream);
+    c->launches += 1;
+    PSP_TRY(finish_reduce(c, EPI_CG_RHO, 1, 0, 0, 0));
+    R->precond_applies += 1;
+  }
+  double beta;
+  PSP_TRY(sync_read(c, c->ds.scal + SC_BETA, 1, &beta));
+  R->r0 = beta;
+  R->final_resid_est = beta;
+  if (R->h_beta_history && R->beta_cap > 0) R->h_beta_history[0] = beta;
+  R->beta_len = 1;
+  if (!isfinite(beta)) return PSP_E_NONFINITE;
+  if (beta <= eps) return PSP_OK;                      // R3
+  const int64_t max_iters = (int64_t)c->nA * c->opts.max_cycles;   // R31
+  int prev = -1;
+  for (int64_t k = 1; k <= max_iters; ++k) {
+    const int s = ring_next(c);
+    const double* pold = prev >= 0 ? px_col(c, prev) : nullptr;
+    // p = z + beta p_old -> P_x slot, q = A p -> P_y slot, p'q, p'p (alpha, the probe scale)
+    h = kt_begin(c);
+    if (!c->multi && launch_cg_dir_fused(c->st, z, pold, px_col(c, s), py_col(c, s), s, c->ds, c->stream)) {
+      c->launches += 1;
+      kt_end(c, h, PSP_KC_CG, (pold ? 40.0 : 32.0) * dn);
+    } else {
+      launch_cg_pupdate(z, pold, px_col(c, s), n, c->ds, c->stream);
+      PSP_TRY(matvec(c, px_col(c, s), nullptr, py_col(c, s), nullptr));
+      launch_cg_dirdots(px_col(c, s), py_col(c, s), n, s, c->ds, c->rc, c->stream);
+      c->launches += 2;
+      PSP_TRY(finish_reduce(c, EPI_CG_DIR, 2, 0, 1, s));
+      kt_end(c, h, PSP_KC_CG, (pold ? 24.0 : 16.0) * dn + matvec_bytes(c, false) + 16.0 * dn);
+    }
+    R->matvecs += 1;
+    // x += alpha p, r -= alpha q, R(k) = ||r||
+    h = kt_begin(c);
+    launch_cg_update(c->X0, px_col(c, s), py_col(c, s), r, n, ident ? 1 : 0, c->ds, c->rc, c->stream);
+    c->launches += 1;
+    PSP_TRY(finish_reduce(c, EPI_CG_UPD, 1, 0, ident ? 1 : 0, 0));
+    kt_end(c, h, PSP_KC_CG, 48.0 * dn);
+    if (!ident) {                                     // z = M^-1 r, rho' = r'z, beta
+      h = kt_begin(c);
+      PSP_TRY(precond_scaled(c, r, nullptr, z));
+      kt_end(c, h, PSP_KC_PRECOND, 8.0 * (2 * c->d + 5) * dn);
+      launch_cg_rz(r, z, n, c->ds, c->rc, c->stream);
+      c->launches += 1;
+      PSP_TRY(finish_reduce(c, EPI_CG_RHO, 1, 0, 0, 0));
+      R->precond_applies += 1;
+    }
+    double sc[2];
+    PSP_TRY(sync_read(c, c->ds.scal + SC_RK, 2, sc));
+    const int flags = (int)sc[1];
+    if (flags & PSP_FLAG_NONFINITE) return PSP_E_NONFINITE;
+    if (flags & PSP_FLAG_BREAKDOWN) return fail(c, PSP_E_SINGULAR, "CG: p'Ap <= 0 (A or N_s not SPD, R30)");
+    if (R->h_resid_history && R->resid_len < R->resid_cap) R->h_resid_history[R->resid_len] = sc[0];
+    R->resid_len += 1;
+    R->iterations += 1;
+    R->final_resid_est = sc[0];
+    if (flags & PSP_FLAG_CONVERGED) return PSP_OK;
+    prev = s;
+  }
+  return PSP_E_NOCONV;
+}
+
 // f2: the device-resident solve (resident.cu) -- single rank, one-reduction MGS, n_A <= 64, up to
 // 2^20 rows by default (a banded N: one CTA's sequential sweeps, n <= 16384)
 static bool resident_eligible(const psp_ctx* c) {
   if (c->opts.resident <= 0 || c->multi || c->opts.ortho != PSP_MGS_1REDUCE) return false;
+  if (c->opts.method != PSP_METHOD_GMRES) return false;
   if (!resident_supported(c->n, c->nA, !c->n_identity)) return false;
   return c->opts.resident >= 2 || c->n <= kResidentAutoRows;
 }
@@ -1097,6 +1196,40 @@ psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, p
   R->resid_verified = 0;
   R->precond_identity = c->n_identity ? 1 : 0;
   if (c->opts.timing) cudaEventRecord(c->ev[0], c->stream);
+  if (c->opts.method == PSP_METHOD_CG) {
+    double eps;
+    PSP_TRY(set_eps(c, b, &eps));
+    R->eps = eps;
+    psp_status status = cg_solve(c, b, x0, R, eps);
+    const bool finish = status == PSP_OK;
+    if (finish || status == PSP_E_NOCONV) {
+      if (x != c->X0) {
+        launch_copy(c->X0, x, c->n, c->stream);
+        c->launches += 1;
+      }
+      PSP_TRY(matvec(c, x, nullptr, c->W, nullptr));  // R13: true residual, not recorded
+      launch_diff_norm(b, c->W, c->n, c->ds, SC_TMP, c->rc, c->stream);
+      c->launches += 1;
+      PSP_TRY(finish_reduce(c, EPI_NORM, 1, 0, 0, SC_TMP));
+      double tr;
+      PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &tr));
+      R->final_resid_true = tr;
+      R->converged = finish ? 1 : 0;
+      R->resid_verified = (finish && tr <= eps) ? 1 : 0;
+    }
+    if (c->opts.timing) {
+      cudaEventRecord(c->ev[1], c->stream);
+      cudaEventSynchronize(c->ev[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+      R->t_solve_ms = ms;
+    }
+    R->status = status;
+    if (status != PSP_OK && status != PSP_E_NOCONV)
+      return fail(c, status, std::string("psp_solve (CG): ") + psp_status_str(status));
+    if (status == PSP_E_NOCONV) fail(c, status, "psp_solve (CG): iteration limit reached");
+    return status;
+  }
   if (resident_eligible(c)) {
     psp_status status = resident_solve(c, b, x0, x, R);
     if (c->opts.timing) {
@@ -1345,7 +1478,19 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
   R->mrep_rows_ridge = (int64_t)r[3];
   R->mrep_rows_fallback = (int64_t)(r[4] + r[8]);
   R->mrep_rows_nondominant = (int64_t)r[5];
-  const bool gate_ok = c->opts.gate ? (r[7] != 0.0) : true;
+  bool gate_ok = c->opts.gate ? (r[7] != 0.0) : true;
+  if (c->opts.method == PSP_METHOD_CG) {
+    // R29: CG takes the symmetric part N_s = (N + N^T) / 2, accepted when it is SPD by positive-
+    // diagonal strict dominance (the factors' buffer is the scratch: it is refactored below)
+    launch_sym_bands(c->bands, c->lu, c->n, c->d, c->stream);
+    cudaMemcpyAsync(c->bands, c->lu, (size_t)c->n * (2 * c->d + 1) * 8, cudaMemcpyDeviceToDevice, c->stream);
+    launch_gate_count(c->bands, c->n, c->d, c->row0, c->n_global, c->ds.scal + SC_TMP, c->stream, 1);
+    c->launches += 2;
+    double nondom;
+    PSP_TRY(sync_read(c, c->ds.scal + SC_TMP, 1, &nondom));
+    R->mrep_rows_nondominant = (int64_t)nondom;
+    gate_ok = c->opts.gate ? (nondom == 0.0) : true;
+  }
   return install_bands(c, gate_ok, R);
 }
 
@@ -1379,7 +1524,8 @@ psp_status psp_set_bands(psp_ctx* c, const double* d_bands, int* h_accepted) {
   if (c->opts.gate) {
     // R21 on the given bands: a device count of the non-dominant rows (one scalar read back),
     // summed over the ranks for one decision for the whole matrix
-    launch_gate_count(c->bands, c->n, c->d, c->row0, c->n_global, c->ds.scal + SC_TMP, c->stream);
+    launch_gate_count(c->bands, c->n, c->d, c->row0, c->n_global, c->ds.scal + SC_TMP, c->stream,
+                      c->opts.method == PSP_METHOD_CG ? 1 : 0);
     c->launches += 1;
     if (c->multi && c->comm->allreduce(c->ds.scal + SC_TMP, 1, 0, c->stream))
       return fail(c, PSP_E_NCCL, "psp_set_bands: gate all-reduce failed");

@@ -72,6 +72,7 @@ struct DevState {
   double* partials;  // grid-reduction partials: kMaxPartialVals x nblocks
   unsigned* tickets; // last-block counters (one per reduction slot)
   double* rpart;     // multi-rank: this rank's totals, all-reduced before the epilogue
+  double* slot_scale;  // per probe-ring slot: the recorded probe is slot_scale[slot] * column
   int multi;         // 1: reductions stop at rpart (the host all-reduces, then epilogue_kernel)
 };
 // scalar epilogues of the grid reductions (krylov.cu); multi-rank runs them as a 1-thread
@@ -79,10 +80,12 @@ struct DevState {
 // EPI_DOTS_RAW: the ring-resident step, w = A V_k unnormalised (scale alpha_k), so h_j carries alpha_k too
 // EPI_HYB: the split-column ring step (fused pass over the last columns + dots over the rest)
 enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5, EPI_DOTS_RAW = 6,
-       EPI_HYB = 7 };
+       EPI_HYB = 7,
+       // f4, PSP-CG (cg.cuh): r0 = b - A x0; p'q and p'p of a direction; the x / r update; r'z
+       EPI_CG_START = 8, EPI_CG_DIR = 9, EPI_CG_UPD = 10, EPI_CG_RHO = 11 };
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s);
 enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
-       SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_NSCAL = 16 };
+       SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_RHO = 9, SC_ALPHA = 10, SC_BETACG = 11, SC_NSCAL = 16 };
 enum { TK_MAIN = 0, TK_AUX = 1, TK_MREP = 2, TK_N = 8 };
 
 struct RedCfg {
@@ -138,6 +141,26 @@ void launch_copy(const double* x, double* y, int64_t n, cudaStream_t s);
 // ||b - y|| -> scal[slot]
 void launch_diff_norm(const double* b, const double* y, int64_t n, DevState ds, int slot,
                       const RedCfg& rc, cudaStream_t s);
+
+// ---- f4: PSP-CG passes (krylov.cu; the fused direction pass in stencil.cu) ----
+// r = b - y (y = A x0, the recorded x0 probe), r'r -> EPI_CG_START (beta, rho for N = I)
+void launch_cg_start(const double* b, const double* y, double* r, int64_t n, DevState ds, const RedCfg& rc,
+                     cudaStream_t s);
+// p = z + beta p_old (p_old NULL: p = z), into the ring slot (no reduction)
+void launch_cg_pupdate(const double* z, const double* pold, double* p, int64_t n, DevState ds, cudaStream_t s);
+// p'q, p'p -> EPI_CG_DIR (alpha, the slot's probe scale 1/||p||)
+void launch_cg_dirdots(const double* p, const double* q, int64_t n, int slot, DevState ds, const RedCfg& rc,
+                       cudaStream_t s);
+// x += alpha p, r -= alpha q, r'r -> EPI_CG_UPD (R(k), flags; N = I: beta, rho)
+void launch_cg_update(double* x, const double* p, const double* q, double* r, int64_t n, int identity,
+                      DevState ds, const RedCfg& rc, cudaStream_t s);
+// r'z -> EPI_CG_RHO (beta, rho)
+void launch_cg_rz(const double* r, const double* z, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s);
+// the fused direction pass (stencil.cu): p = z + beta p_old -> px, q = A p -> py, p'q and p'p ->
+// EPI_CG_DIR, one pass over HBM (3-D grids with nx % 4 == 0 and 16-byte aligned vectors, one
+// rank); returns false when the shape is not supported (the caller runs the three passes)
+bool launch_cg_dir_fused(const Stencil& st, const double* z, const double* pold, double* px, double* py, int slot,
+                         DevState ds, cudaStream_t s);
 
 // ---- fused single-pass Arnoldi step for N = I (fused.cu) ----
 bool fused_supported(const Stencil& st, int k);
@@ -221,8 +244,11 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
 
 // R21 gate of a given N: the number of rows that are not strictly diagonally dominant -> *count
 // (device scalar; zeroed first).  grow0 / gN: global index of local row 0 and the global rows.
+// spd != 0 (PSP-CG, R29): a non-positive diagonal also counts
 void launch_gate_count(const double* bands, int64_t n, int d, int64_t grow0, int64_t gN, double* count,
-                       cudaStream_t s);
+                       cudaStream_t s, int spd = 0);
+// R29: sym = (N + N^T) / 2 in DIA storage (one rank); sym must not alias bands
+void launch_sym_bands(const double* bands, double* sym, int64_t n, int d, cudaStream_t s);
 
 // ---- banded LU (banded.cu) ----
 struct BandedScratch {

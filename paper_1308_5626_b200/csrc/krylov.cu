@@ -16,8 +16,10 @@
 // loads in flight: enough bytes in flight per SM to cover the HBM latency.
 #include <math.h>
 
+#include "cg.cuh"
 #include "givens.cuh"
 #include "internal.h"
+#include "reduce.cuh"
 
 namespace psp {
 namespace {
@@ -28,61 +30,15 @@ constexpr int RPT = 8;            // rows per thread in the register-tiled passe
 constexpr int TILE = TPB * RPT;   // 2048 rows
 constexpr int JC = 4;             // basis vectors per chunk
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// block-wide sum of NV values held per thread; result valid in thread 0
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* kWarps*NV */) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) smem[warp * NV + q] = v[q];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double s = 0.0;
-      for (int w = 0; w < kWarps; ++w) s += smem[w * NV + q];
-      v[q] = s;
-    }
-  }
-  __syncthreads();
-}
-
-// Publish this block's partials; returns true in every thread of the last block to finish.
-__device__ bool finish_block(unsigned* ticket) {
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned t = atomicAdd(ticket, 1u);
-    s_last = (t == gridDim.x - 1);
-    if (s_last) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
-  }
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last;
-}
-
-// Last block: total of partials[v*nb + b] over b, fixed order.  Result valid in thread 0.
-__device__ double reduce_partials(const double* partials, int v, int nb, double* smem) {
-  double a[1] = {0.0};
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) a[0] += ((volatile const double*)partials)[v * nb + b];
-  block_sum<1>(a, smem);
-  return a[0];
-}
-
 // ------------------------------------------------------------------------------------------
 // Scalar epilogues of the reductions (one thread), from the totals tot[]
 // ------------------------------------------------------------------------------------------
 __device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, const double* tot) {
   const int ld = nA + 1;
+  if (kind >= EPI_CG_START) {                     // f4 (cg.cuh); j = 1: N = I
+    cg_epilogue(kind, ds, slot, j, tot);
+    return;
+  }
   switch (kind) {
     case EPI_NORM:
       ds.scal[slot] = sqrt(tot[0]);
@@ -657,6 +613,94 @@ __global__ void __launch_bounds__(TPB) combine_finish_kernel(const double* __res
     x[r] = fma(yk, z1[r], z0[r]);
 }
 
+// ------------------------------------------------------------------------------------------
+// f4: PSP-CG passes (readings R27-R31; oracle/oracle.c orc_pcg for the recurrences)
+// ------------------------------------------------------------------------------------------
+// r = b - A x0 (y = A x0 was recorded as the probe of x0); r'r
+__global__ void __launch_bounds__(TPB) cg_start_kernel(const double* __restrict__ b, const double* __restrict__ y,
+                                                       double* __restrict__ r, int64_t n, DevState ds) {
+  __shared__ double sm[kWarps];
+  double a[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    const double t = b[i] - y[i];
+    r[i] = t;
+    a[0] = fma(t, t, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_CG_START, 0, 0, 1, 0, &t, 1);
+  }
+}
+
+// p = z + beta p_old (R27); p_old == NULL: p = z (the first direction)
+__global__ void __launch_bounds__(TPB) cg_pupdate_kernel(const double* __restrict__ z, const double* __restrict__ pold,
+                                                         double* __restrict__ p, int64_t n, DevState ds) {
+  const double beta = ds.scal[SC_BETACG];
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB)
+    p[i] = pold ? fma(beta, pold[i], z[i]) : z[i];
+}
+
+// p'q and p'p of the direction just applied -> alpha and the slot's probe scale
+__global__ void __launch_bounds__(TPB) cg_dirdots_kernel(const double* __restrict__ p, const double* __restrict__ q,
+                                                         int64_t n, int slot, DevState ds) {
+  __shared__ double sm[kWarps * 2];
+  double a[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    const double pv = p[i];
+    a[0] = fma(pv, q[i], a[0]);
+    a[1] = fma(pv, pv, a[1]);
+  }
+  block_sum<2>(a, sm);
+  if (threadIdx.x == 0) {
+    ds.partials[blockIdx.x] = a[0];
+    ds.partials[gridDim.x + blockIdx.x] = a[1];
+  }
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t[2];
+    t[0] = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    t[1] = reduce_partials(ds.partials, 1, gridDim.x, sm);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_CG_DIR, 0, 0, 1, slot, t, 2);
+  }
+}
+
+// x += alpha p, r -= alpha q; r'r
+__global__ void __launch_bounds__(TPB) cg_update_kernel(double* __restrict__ x, const double* __restrict__ p,
+                                                        const double* __restrict__ q, double* __restrict__ r, int64_t n,
+                                                        int identity, DevState ds) {
+  __shared__ double sm[kWarps];
+  const double alpha = ds.scal[SC_ALPHA];
+  double a[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double rv = fma(-alpha, q[i], r[i]);
+    r[i] = rv;
+    a[0] = fma(rv, rv, a[0]);
+  }
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_CG_UPD, 0, 0, identity, 0, &t, 1);
+  }
+}
+
+// r'z (N != I)
+__global__ void __launch_bounds__(TPB) cg_rz_kernel(const double* __restrict__ r, const double* __restrict__ z,
+                                                    int64_t n, DevState ds) {
+  __shared__ double sm[kWarps];
+  double a[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB)
+    a[0] = fma(r[i], z[i], a[0]);
+  block_sum<1>(a, sm);
+  if (threadIdx.x == 0) ds.partials[blockIdx.x] = a[0];
+  if (finish_block(ds.tickets + TK_MAIN)) {
+    double t = reduce_partials(ds.partials, 0, gridDim.x, sm);
+    if (threadIdx.x == 0) finish_scalar(ds, EPI_CG_RHO, 0, 0, 0, 0, &t, 1);
+  }
+}
+
 inline int grid_for(int64_t n, int cap) {
   int64_t b = (n + TPB - 1) / TPB;
   if (b > cap) b = cap;
@@ -727,6 +771,24 @@ void launch_icwy_update(Basis V, const double* w, const double* ws, double* U, i
   int64_t ub = (n + UTILE - 1) / UTILE;
   if (ub > wave) ub = wave;
   icwy_update_kernel<<<(int)(ub < 1 ? 1 : ub), TPB, 0, s>>>(V, w, ws, U, k, nA, n, ds, ncols < 0 ? k : ncols);
+}
+void launch_cg_start(const double* b, const double* y, double* r, int64_t n, DevState ds, const RedCfg& rc,
+                     cudaStream_t s) {
+  cg_start_kernel<<<rc.nblocks, TPB, 0, s>>>(b, y, r, n, ds);
+}
+void launch_cg_pupdate(const double* z, const double* pold, double* p, int64_t n, DevState ds, cudaStream_t s) {
+  cg_pupdate_kernel<<<grid_for(n, 8 * device_sms()), TPB, 0, s>>>(z, pold, p, n, ds);
+}
+void launch_cg_dirdots(const double* p, const double* q, int64_t n, int slot, DevState ds, const RedCfg& rc,
+                       cudaStream_t s) {
+  cg_dirdots_kernel<<<rc.nblocks, TPB, 0, s>>>(p, q, n, slot, ds);
+}
+void launch_cg_update(double* x, const double* p, const double* q, double* r, int64_t n, int identity,
+                      DevState ds, const RedCfg& rc, cudaStream_t s) {
+  cg_update_kernel<<<rc.nblocks, TPB, 0, s>>>(x, p, q, r, n, identity, ds);
+}
+void launch_cg_rz(const double* r, const double* z, int64_t n, DevState ds, const RedCfg& rc, cudaStream_t s) {
+  cg_rz_kernel<<<rc.nblocks, TPB, 0, s>>>(r, z, n, ds);
 }
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s) {
   epilogue_kernel<<<1, 1, 0, s>>>(kind, ds, k, nA, j, slot);

@@ -719,7 +719,7 @@ __global__ void mrep_decide_kernel(MrepScratch sc) {
 // R21 on a given N (psp_set_bands): rows that are not strictly diagonally dominant, summed in band
 // order as the fit kernels do, counted into *count (exact integer adds: order-free)
 __global__ void gate_count_kernel(const double* __restrict__ bands, int64_t n, int d, int64_t grow0, int64_t gN,
-                                  double* count) {
+                                  double* count, int spd) {
   double cnt = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double off = 0.0;
@@ -728,7 +728,8 @@ __global__ void gate_count_kernel(const double* __restrict__ bands, int64_t n, i
       if (o == d || j < 0 || j >= gN) continue;
       off += fabs(bands[(int64_t)o * n + i]);
     }
-    if (!(fabs(bands[(int64_t)d * n + i]) > off)) cnt += 1.0;
+    const double dg = bands[(int64_t)d * n + i];
+    if (!(fabs(dg) > off) || (spd && !(dg > 0.0))) cnt += 1.0;
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt != 0.0) atomicAdd(count, cnt);
@@ -737,11 +738,29 @@ __global__ void gate_count_kernel(const double* __restrict__ bands, int64_t n, i
 }  // namespace
 
 void launch_gate_count(const double* bands, int64_t n, int d, int64_t grow0, int64_t gN, double* count,
-                       cudaStream_t s) {
+                       cudaStream_t s, int spd) {
   cudaMemsetAsync(count, 0, sizeof(double), s);
   int64_t nb = (n + 255) / 256;
   if (nb > 8 * device_sms()) nb = 8 * device_sms();
-  gate_count_kernel<<<(unsigned)(nb < 1 ? 1 : nb), 256, 0, s>>>(bands, n, d, grow0, gN, count);
+  gate_count_kernel<<<(unsigned)(nb < 1 ? 1 : nb), 256, 0, s>>>(bands, n, d, grow0, gN, count, spd);
+}
+
+namespace {
+// R29: N_s(i, i+o-d) = (N(i, i+o-d) + N(i+o-d, i)) / 2, the second term from band 2d-o of row i+o-d
+__global__ void sym_bands_kernel(const double* __restrict__ b, double* __restrict__ sym, int64_t n, int d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int o = 0; o <= 2 * d; ++o) {
+      const int64_t j = i + o - d;
+      sym[(int64_t)o * n + i] = (j < 0 || j >= n) ? 0.0 : 0.5 * (b[(int64_t)o * n + i] + b[(int64_t)(2 * d - o) * n + j]);
+    }
+  }
+}
+}  // namespace
+
+void launch_sym_bands(const double* bands, double* sym, int64_t n, int d, cudaStream_t s) {
+  int64_t nb = (n + 255) / 256;
+  if (nb > 8 * device_sms()) nb = 8 * device_sms();
+  sym_bands_kernel<<<(unsigned)(nb < 1 ? 1 : nb), 256, 0, s>>>(bands, sym, n, d);
 }
 
 int mrep_launch(const double* px, const double* py, const double* slot_scale, int64_t ld,

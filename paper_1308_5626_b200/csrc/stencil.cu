@@ -8,7 +8,9 @@
 // 126 MB L2), so DRAM sees each array once.
 #include <stdlib.h>
 
+#include "cg.cuh"
 #include "internal.h"
+#include "reduce.cuh"
 #include "stencil_row.cuh"
 
 #ifndef PSP_MARCH_MINB
@@ -417,6 +419,146 @@ __global__ void __launch_bounds__(32 * BY, 2) march4_kernel(MarchView v, const d
   }
 }
 
+// f4 (PSP-CG, R27/R28): the direction pass p = z + beta p_old -> px, q = A p -> py (the probe
+// (p, A p), recorded with scale 1/||p||) and p'q, p'p, in one pass over HBM: 8 (z) + 8 (p_old) +
+// 8 (field) read, 16 written per row.  march4_kernel's layout (four x-adjacent points a thread,
+// march-axis register queue, x neighbours by shuffles, y neighbours from the neighbouring lines),
+// with every loaded value of p formed on the fly from z and p_old.  One rank (no halo planes).
+template <int KIND, int BY>
+__global__ void __launch_bounds__(32 * BY, 2) cg_dir4_kernel(MarchView v, const double* __restrict__ z,
+                                                             const double* __restrict__ pold, double* __restrict__ pout,
+                                                             double* __restrict__ q, int slot, DevState ds) {
+  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
+  constexpr bool HASY = BY > 1;
+  constexpr int TW = 128;
+  const double* __restrict__ f = v.field;
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * TW + 4 * lane;
+  const int64_t j = HASY ? (int64_t)blockIdx.y * BY + ty : 0;
+  const int64_t z0 = (int64_t)blockIdx.z * v.zc;
+  const int64_t z1 = (z0 + v.zc < v.nz) ? z0 + v.zc : v.nz;
+  const bool in = i < v.nx && j < v.ny;
+  const int64_t plane = v.nx * v.ny;
+  const int64_t col = in ? i + v.nx * j : 0;
+  const bool has_w = i > 0, has_e = i + 4 < v.nx;
+  const bool has_s = HASY && in && j > 0, has_n = HASY && in && j + 1 < v.ny;
+  const double beta = pold ? ds.scal[SC_BETACG] : 0.0;
+  const double hs0 = 0.5 * v.s[0], hs1 = 0.5 * v.s[1], hs2 = 0.5 * v.s[2];
+  const double s0c = v.s[0], s1c = v.s[1], s2c = v.s[2];
+  struct Q4 { double a, b, c, d; };
+  auto ld4 = [&](const double* base, int64_t off) -> Q4 {
+    const double2 p0 = __ldg(reinterpret_cast<const double2*>(base + off));
+    const double2 p1 = __ldg(reinterpret_cast<const double2*>(base + off + 2));
+    return Q4{p0.x, p0.y, p1.x, p1.y};
+  };
+  auto dir4 = [&](int64_t off) -> Q4 {            // p = z + beta p_old at four points
+    Q4 r = ld4(z, off);
+    if (pold) {
+      const Q4 o = ld4(pold, off);
+      r = Q4{fma(beta, o.a, r.a), fma(beta, o.b, r.b), fma(beta, o.c, r.c), fma(beta, o.d, r.d)};
+    }
+    return r;
+  };
+  auto dir1 = [&](int64_t off) -> double { return pold ? fma(beta, __ldg(pold + off), __ldg(z + off)) : __ldg(z + off); };
+  const Q4 zero4{0.0, 0.0, 0.0, 0.0};
+  auto plane4 = [&](const double* a, int64_t p) -> Q4 { return (p >= 0 && p < v.nz) ? ld4(a, col + plane * p) : zero4; };
+  auto dplane4 = [&](int64_t p) -> Q4 { return (p >= 0 && p < v.nz) ? dir4(col + plane * p) : zero4; };
+  Q4 xb = dplane4(z0 - 1), xc = dplane4(z0), xt = dplane4(z0 + 1);
+  Q4 fb = zero4, fc = zero4, ft = zero4;
+  if (cell) {
+    fb = plane4(f, z0 - 1); fc = plane4(f, z0); ft = plane4(f, z0 + 1);
+  }
+  double pq = 0.0, pp = 0.0;
+  int64_t g = col + plane * z0;
+  for (int64_t zz = z0; zz < z1; ++zz) {
+    Q4 xt2 = zero4, ft2 = zero4;
+    if (zz + 2 < v.nz) {
+      xt2 = dir4(g + 2 * plane);
+      if (cell) ft2 = ld4(f, g + 2 * plane);
+    }
+    Q4 xsn = zero4, xnn = zero4, fsn = fc, fnn = fc;
+    if (has_s) { xsn = dir4(g - v.nx); if (cell) fsn = ld4(f, g - v.nx); }
+    if (has_n) { xnn = dir4(g + v.nx); if (cell) fnn = ld4(f, g + v.nx); }
+    double xw = __shfl_up_sync(0xffffffffu, xc.d, 1), xe = __shfl_down_sync(0xffffffffu, xc.a, 1);
+    double fw = 0.0, fe = 0.0;
+    if (cell) {
+      fw = __shfl_up_sync(0xffffffffu, fc.d, 1);
+      fe = __shfl_down_sync(0xffffffffu, fc.a, 1);
+    }
+    if (lane == 0 && in && has_w) { xw = dir1(g - 1); if (cell) fw = __ldg(f + g - 1); }
+    if (lane == 31 && in && has_e) { xe = dir1(g + 4); if (cell) fe = __ldg(f + g + 4); }
+    if (!has_w) { xw = 0.0; fw = fc.a; }
+    if (!has_e) { xe = 0.0; fe = fc.d; }
+    if (zz == 0) fb = fc;
+    if (zz + 1 == v.nz) ft = fc;
+    auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
+                     double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
+      double acc = 0.0;
+      if (cell) {
+        acc = fma(hs0 * (k + fwv), c - xwv, acc);
+        acc = fma(hs0 * (k + fev), c - xev, acc);
+      } else {
+        acc = fma(s0c, c - xwv, acc);
+        acc = fma(s0c, c - xev, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
+      if (HASY) {
+        if (cell) {
+          acc = fma(hs1 * (k + fsv), c - xsv, acc);
+          acc = fma(hs1 * (k + fnv), c - xnv, acc);
+        } else {
+          acc = fma(s1c, c - xsv, acc);
+          acc = fma(s1c, c - xnv, acc);
+        }
+        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
+      }
+      if (cell) {
+        acc = fma(hs2 * (k + fbv), c - xbv, acc);
+        acc = fma(hs2 * (k + ftv), c - xtv, acc);
+      } else {
+        acc = fma(s2c, c - xbv, acc);
+        acc = fma(s2c, c - xtv, acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
+      return c + acc;
+    };
+    if (in) {
+      const double o0 = point(xc.a, fc.a, xw, fw, xc.b, fc.b, xsn.a, fsn.a, xnn.a, fnn.a, xb.a, fb.a, xt.a, ft.a);
+      const double o1 = point(xc.b, fc.b, xc.a, fc.a, xc.c, fc.c, xsn.b, fsn.b, xnn.b, fnn.b, xb.b, fb.b, xt.b, ft.b);
+      const double o2 = point(xc.c, fc.c, xc.b, fc.b, xc.d, fc.d, xsn.c, fsn.c, xnn.c, fnn.c, xb.c, fb.c, xt.c, ft.c);
+      const double o3 = point(xc.d, fc.d, xc.c, fc.c, xe, fe, xsn.d, fsn.d, xnn.d, fnn.d, xb.d, fb.d, xt.d, ft.d);
+      *reinterpret_cast<double2*>(q + g) = make_double2(o0, o1);
+      *reinterpret_cast<double2*>(q + g + 2) = make_double2(o2, o3);
+      *reinterpret_cast<double2*>(pout + g) = make_double2(xc.a, xc.b);
+      *reinterpret_cast<double2*>(pout + g + 2) = make_double2(xc.c, xc.d);
+      pq = fma(xc.a, o0, pq); pq = fma(xc.b, o1, pq); pq = fma(xc.c, o2, pq); pq = fma(xc.d, o3, pq);
+      pp = fma(xc.a, xc.a, pp); pp = fma(xc.b, xc.b, pp); pp = fma(xc.c, xc.c, pp); pp = fma(xc.d, xc.d, pp);
+    }
+    g += plane;
+    xb = xc; xc = xt; xt = xt2;
+    fb = fc; fc = ft; ft = ft2;
+  }
+  // deterministic grid reduction of (p'q, p'p) -> EPI_CG_DIR
+  __shared__ double sm[BY * 2];
+  double a[2] = {pq, pp};
+  block_sum<2, BY>(a, sm);
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    ds.partials[bid] = a[0];
+    ds.partials[nb + bid] = a[1];
+  }
+  if (finish_block(ds.tickets + TK_MAIN, nb)) {
+    double t[2];
+    t[0] = reduce_partials<BY>(ds.partials, 0, (int)nb, sm);
+    t[1] = reduce_partials<BY>(ds.partials, 1, (int)nb, sm);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      if (ds.multi) { ds.rpart[0] = t[0]; ds.rpart[1] = t[1]; }
+      else cg_epilogue(EPI_CG_DIR, ds, slot, 1, t);
+    }
+  }
+}
+
 __global__ void dia_matvec_kernel(int64_t n, int dA, const double* __restrict__ bands,
                                   const double* __restrict__ x, const double* xsp, double* __restrict__ y,
                                   double* __restrict__ xcopy) {
@@ -514,6 +656,29 @@ void launch_kind(const Stencil& st, const double* x, const double* xs, double* y
 }
 
 }  // namespace
+
+bool launch_cg_dir_fused(const Stencil& st, const double* z, const double* pold, double* px, double* py, int slot,
+                         DevState ds, cudaStream_t s) {
+  if (st.ndim != 3 || st.kind == PSP_OP_DIA || st.nx % 4 != 0 || st.x_lo || st.x_hi) return false;
+  if (!aligned16(z) || !aligned16(pold) || !aligned16(px) || !aligned16(py) || !aligned16(st.field)) return false;
+  MarchView v;
+  v.field = st.field;
+  v.x_lo = v.x_hi = v.f_lo = v.f_hi = nullptr;
+  v.nx = st.nx; v.ny = st.ny; v.nz = st.nz;
+  for (int a = 0; a < 3; ++a) { v.s[a] = st.s[a]; v.a[a] = st.a[a]; }
+  constexpr int BY = 8;
+  const int64_t zc = planes_per_block(((v.nx + 127) / 128) * ((v.ny + BY - 1) / BY), v.nz);
+  v.zc = (int)zc;
+  dim3 grid((unsigned)((v.nx + 127) / 128), (unsigned)((v.ny + BY - 1) / BY), (unsigned)((v.nz + zc - 1) / zc));
+  const int64_t nb = (int64_t)grid.x * grid.y * grid.z;
+  if (2 * nb > (int64_t)2 * kMaxRestart * 8 * device_sms()) return false;   // partials capacity
+  switch (st.kind) {
+    case PSP_OP_CONST_DIFF: cg_dir4_kernel<PSP_OP_CONST_DIFF, BY><<<grid, dim3(32, BY), 0, s>>>(v, z, pold, px, py, slot, ds); break;
+    case PSP_OP_CELL_DIFF: cg_dir4_kernel<PSP_OP_CELL_DIFF, BY><<<grid, dim3(32, BY), 0, s>>>(v, z, pold, px, py, slot, ds); break;
+    default: cg_dir4_kernel<PSP_OP_CELL_ADVDIFF, BY><<<grid, dim3(32, BY), 0, s>>>(v, z, pold, px, py, slot, ds); break;
+  }
+  return true;
+}
 
 void launch_matvec(const Stencil& st, const double* x, const double* xs, double* y, double* xcopy,
                    cudaStream_t s) {

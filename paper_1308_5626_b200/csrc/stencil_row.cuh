@@ -13,10 +13,16 @@ struct Nb {
 
 // neighbour of (i,j,k) along axis A, direction D (-1/+1).  Outside the local block: the slab
 // halo plane if present (multi-rank), else the Dirichlet zero (R24).
-template <bool CG>
-static __device__ __forceinline__ double ldx(const double* p) { return CG ? __ldcg(p) : __ldg(p); }
+// load policy of x: 0 read-only path (x not written in this launch), 1 L2 only (written by other
+// blocks of this launch), 2 plain (written by this block: one-CTA launches)
+template <int CG>
+static __device__ __forceinline__ double ldx(const double* p) {
+  if (CG == 1) return __ldcg(p);
+  if (CG == 2) return *p;
+  return __ldg(p);
+}
 
-template <int AXIS, int DIR, bool CG = false>
+template <int AXIS, int DIR, int CG = 0>
 static __device__ __forceinline__ Nb neighbour(const Stencil& st, const double* __restrict__ x,
                                         const double* __restrict__ f, int64_t i, int64_t j,
                                         int64_t k, int64_t g, bool need_f) {
@@ -50,7 +56,7 @@ static __device__ __forceinline__ Nb neighbour(const Stencil& st, const double* 
 // (A x)_g at grid point (i, j, k) of the local block, g = i + nx (j + ny k); xc <- x_g.
 // A x = x - dt L x;  -dt L x = sum_faces s k_f (x_c - x_nb) + sum_a a_a (x_c - x_w).
 // CG = true: x was written earlier in the same launch by other blocks (read through L2 only)
-template <int KIND, int NDIM, bool CG = false>
+template <int KIND, int NDIM, int CG = 0>
 static __device__ __forceinline__ double stencil_row(const Stencil& st, const double* __restrict__ x, int64_t i,
                                                     int64_t j, int64_t k, int64_t g, double& xc) {
   const double* __restrict__ f = st.field;
@@ -88,7 +94,7 @@ static __device__ __forceinline__ double stencil_row(const Stencil& st, const do
 }
 
 // (A x)_g of a DIA operator (PSP_OP_DIA; the paper's banded test matrices)
-template <bool CG = false>
+template <int CG = 0>
 static __device__ __forceinline__ double dia_row(const Stencil& st, const double* __restrict__ x, int64_t g) {
   double s = 0.0;
   for (int o = 0; o <= 2 * st.dA; ++o) {

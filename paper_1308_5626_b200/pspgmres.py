@@ -23,6 +23,7 @@ PSP_OK, PSP_E_ARG, PSP_E_DIM, PSP_E_SAMPLES, PSP_E_RANK, PSP_E_SINGULAR, PSP_E_N
 PSP_OP_CONST_DIFF, PSP_OP_CELL_DIFF, PSP_OP_CELL_ADVDIFF, PSP_OP_DIA = range(4)
 PSP_TOL_REL_B, PSP_TOL_ABS = 0, 1
 PSP_MGS_1REDUCE, PSP_MGS_LITERAL = 0, 1
+PSP_METHOD_GMRES, PSP_METHOD_CG = 0, 1
 PSP_FLAG_CONVERGED, PSP_FLAG_BREAKDOWN, PSP_FLAG_NONFINITE = 1, 2, 4
 PSP_KC_COUNT = 14
 ROW_INTERIOR, ROW_INTERIOR_RIDGE, ROW_BOUNDARY, ROW_FALLBACK_RANK, ROW_FALLBACK_ZEROVAR, \
@@ -47,7 +48,8 @@ class psp_opts(C.Structure):
     _fields_ = [("max_cycles", C.c_int32), ("tol_mode", C.c_int32), ("m_max", C.c_int32),
                 ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
                 ("timing", C.c_int32), ("fused", C.c_int32), ("fused_kmin", C.c_int32),
-                ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32), ("resident", C.c_int32)]
+                ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32), ("resident", C.c_int32),
+                ("method", C.c_int32)]
 
 
 class psp_report(C.Structure):
