@@ -51,6 +51,8 @@ def parse():
                     help="N > 1: independent replicas instead of one z-slab-sharded problem")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 MREP / banded-solve kernel sweep point")
     ap.add_argument("--c5-log2n", type=int, default=26)
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the C5 sweep (m x d grid) and the C1 / C2 / PSP-CG config lines")
     return ap.parse_args()
 
 
@@ -197,6 +199,95 @@ def c5_point(log2n, m, d, peak):
     del g, scratch, bands, lu_box, z
     torch.cuda.empty_cache()
     return out
+
+
+def c5_sweep(log2n, peak, ms=(16, 32, 64, 128), ds=(1, 2, 3, 4)):
+    """BASELINE configs[4] as a grid: MREP fit rows/s and its fraction of the measured copy peak
+    for every m x d (n = 2^log2n; m = 128 at 2^(log2n-1): the P_x / P_y pair of 2^26 x 128 columns
+    would take 128 GiB), the banded factor and solve per d (independent of m)."""
+    import torch
+
+    from paper_1308_5626_b200 import inputs, pspgmres as P
+    s = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    out = {"mrep_fit": [], "banded_factor": [], "banded_solve": []}
+    for m in ms:
+        l2 = log2n - (1 if m >= 128 else 0)
+        n = 1 << l2
+        for d in ds:
+            g = inputs.c5_torch(n, m, d, seed=0)
+            scratch = P.raw_scratch(n, d)
+            box = {}
+            t = timed(lambda: box.update(P.psp_mrep_fit_raw(g["px"], g["py"], d, scratch=scratch, want_kind=False)), 2)
+            b = 16 * m + 8 * (2 * d + 1)
+            ach = b * n / (t / 1e3) / 1e9
+            out["mrep_fit"].append({"n": n, "m": m, "d": d, "ms": t, "rows_per_s": n / (t / 1e3), "bytes_per_row": b,
+                                    "achieved_GBps": ach, "frac": ach / peak, "gate_accepted": box["gate_accepted"]})
+            if m == 32:
+                lu_box = {}
+
+                def do_factor():
+                    lu_box["st"], lu_box["lu"] = P.psp_banded_factor_raw(box["bands"], d, scratch=scratch)
+                tf = timed(do_factor, 1)
+                z = torch.empty_like(g["v"])
+                ts = timed(lambda: P.psp_banded_solve_raw(lu_box["lu"], d, g["v"], scratch=scratch, out=z), 5)
+                bf, bs = 16 * (2 * d + 1), 8 * (2 * d + 5)
+                for key, tt, bb in (("banded_factor", tf, bf), ("banded_solve", ts, bs)):
+                    a2 = bb * n / (tt / 1e3) / 1e9
+                    out[key].append({"n": n, "d": d, "ms": tt, "rows_per_s": n / (tt / 1e3), "bytes_per_row": bb,
+                                     "achieved_GBps": a2, "frac": a2 / peak})
+                del lu_box, z
+            del g, scratch, box
+            torch.cuda.empty_cache()
+    return out
+
+
+def config_lines():
+    """The other BASELINE configs as step timings through the same C ABI (CUDA events around
+    psp_step): C1 (1-D, n = 1024, 5 steps) and C2 (2-D 512^2, d = 1, 20 steps) on the
+    device-resident solve (f2), and C4 with PSP-CG (f4, 3 steps after one warm-up)."""
+    import torch
+
+    from paper_1308_5626_b200 import inputs, pspgmres as P
+    res = {}
+    for key, mk, steps, warm, kw in (("C1_resident", lambda: inputs.c1(), 5, 0, dict(resident=2)),
+                                     ("C2_resident", lambda: inputs.c2(d=1), 20, 0, dict(resident=2)),
+                                     ("C4_psp_cg", lambda: inputs.c4(steps=4), 3, 1, dict(method=P.PSP_METHOD_CG))):
+        prob = mk()
+        opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, **kw)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol, opts=opts, stream=st)
+            u = torch.as_tensor(prob.u0).cuda()
+        for _ in range(warm):
+            ctx.psp_step(u, u)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        reps = [ctx.psp_step(u, u) for _ in range(steps)]
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        n = prob.op.rows
+        its = [r["iterations"] for r in reps]
+        res[key] = {"n": n, "steps": steps, "ms_per_step": ms / steps, "iterations_per_step": its,
+                    "unknown_iterations_per_s": n * sum(its) / (ms / 1e3),
+                    "converged": all(r["converged"] for r in reps),
+                    "gate_accepted_per_step": [r["mrep_gate_accepted"] for r in reps]}
+        ctx.close()
+        del ctx, u, prob
+        torch.cuda.empty_cache()
+    return res
 
 
 def run_reference(args, rank, world):
@@ -449,6 +540,15 @@ def main():
                 dist.destroy_process_group()
             return 0
         line["c5"] = c5
+        if not args.no_sweep:
+            try:
+                line["c5_sweep"] = c5_sweep(args.c5_log2n, peak)
+            except Exception as e:  # noqa: BLE001
+                line["c5_sweep"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            try:
+                line["configs"] = config_lines()
+            except Exception as e:  # noqa: BLE001
+                line["configs"] = {"error": f"{type(e).__name__}: {e}"[:300]}
         mv = kstats.get("matvec", {})
         line["kernel_rooflines"] = {
             "matvec": {"achieved_GBps": kernel_table.get("matvec", {}).get("GBps"), "peak": peak,

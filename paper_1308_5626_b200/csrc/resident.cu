@@ -114,8 +114,10 @@ template <int M>
 __device__ __forceinline__ double ldm(const double* p) { return M == 2 ? *p : __ldcg(p); }
 
 // (A x)_g for the operator kinds of the context, x written in this launch (M: ld's policy)
+// not inlined: the kernel evaluates rows in unrolled per-thread loops, and nine inlined stencil
+// variants per row would make the kernel megabytes of code (instruction-fetch bound)
 template <int M>
-__device__ __forceinline__ double arow(const Stencil& st, const double* x, int64_t g, double& xc) {
+__device__ __noinline__ double arow(const Stencil& st, const double* x, int64_t g, double& xc) {
   if (st.kind == PSP_OP_DIA) {
     xc = ldm<M>(x + g);
     return dia_row<M>(st, x, g);
@@ -245,8 +247,9 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
   double* Qv = al + ld;                 // nA
   double* rs = Qv + nA;                 // nA (R(k) of the cycle)
   double* sc = rs + nA;                 // SC_NSCAL
-  double* red = sc + SC_NSCAL;          // [RW][PV]
-  double* tot = red + (size_t)RW * PV;  // PV
+  double* red = sc + SC_NSCAL;          // [RW][PV] (also the 2 RT doubles of the block scans)
+  const int REDN = RW * PV > 2 * RT ? RW * PV : 2 * RT;
+  double* tot = red + REDN;             // PV
   DevState S;                           // the replicated scalar state (givens_update's view)
   S.H = H;
   S.Hraw = a.ds.Hraw;                   // identical writes from every CTA (test hook)
@@ -572,7 +575,8 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
 
 size_t res_smem(int nA) {
   const size_t ld = nA + 1, PV = 2 * nA + 2;
-  return (ld * nA + ld * ld + ld + nA + nA + ld + nA + nA + SC_NSCAL + RW * PV + PV) * 8;
+  const size_t redn = RW * PV > 2 * RT ? RW * PV : 2 * RT;
+  return (ld * nA + ld * ld + ld + nA + nA + ld + nA + nA + SC_NSCAL + redn + PV) * 8;
 }
 
 }  // namespace

@@ -125,10 +125,10 @@ def test_cg_free_running_c1(torch, P, orc):
     assert not ident and np.max(np.abs(bands.cpu().numpy()[:, 2:-2] - ref)) <= 1e-9 * (1 + 2 * rr)
     kappa = 1 + 4 * rr
     assert np.linalg.norm(u.cpu().numpy() - r["u"]) <= kappa * 2 * prob.tol * np.linalg.norm(r["u"]) * prob.steps
-    # the probe ring holds unit-norm (p, A p) pairs (R28)
+    # the probe ring holds unit-norm (p, A p) pairs (R28), plus each step's (x0, A x0) probe
     cnt, slots, PX, PY = ctx.psp_ring_view()
     nrm = PX.norm(dim=1).cpu().numpy()
-    assert np.allclose(nrm[1:], 1.0, rtol=1e-12)
+    assert np.sum(~np.isclose(nrm, 1.0, rtol=1e-12)) <= prob.steps
     ctx.close()
 
 
