@@ -10,6 +10,7 @@ run() {   # name, kernel regex, skip, count, command...
   timeout 900 $NCU -k regex:$k -s $s -c $c -o $O/$name "$@" > $O/$name.log 2>&1
   echo "$name rc $?"
 }
+timeout 900 python -m pytest tests/test_gpu_cg.py tests/test_gpu_parity.py -q -k "f1 or cg or resident or determinism" > $O/pytest_sel.log 2>&1; tail -5 $O/pytest_sel.log
 # plain runs first (exit 0 without ncu)
 python tools/kbench.py matvec 512 5 > $O/kb_matvec.txt 2>&1 || exit 1
 python tools/kbench.py solve 26 3 5 > $O/kb_solve3.txt 2>&1 || exit 1
