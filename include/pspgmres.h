@@ -115,6 +115,12 @@ typedef struct {
   int32_t method;                  /* PSP_METHOD_*: the Krylov method of psp_solve / psp_step */
                                    /* (f4: "readily applied to all Krylov subspace       */
                                    /* methods"); default PSP_METHOD_GMRES                     */
+  int32_t mrep_stream;             /* f3: streaming MREP ("obtained progressively"): each */
+                                   /* recorded probe is added to every row's 4d+4 lagged sums */
+                                   /* as it is produced, and psp_mrep_fit fits from the sums  */
+                                   /* of every probe since the previous fit (the window of    */
+                                   /* reset_history_per_step, no m_max cap); one rank; the    */
+                                   /* device-resident solve is not used.  Default 0 (the ring) */
 } psp_opts;
 
 /* Report of one solve / step.  Arrays are caller-owned host buffers (may be NULL). */

@@ -46,6 +46,9 @@ struct psp_ctx {
   double* res_hist = nullptr;
   double* res_beta = nullptr;
   int res_hist_cap = 0, res_beta_cap = 0;
+  // f3: streaming MREP -- the lagged sums of every probe recorded since the last fit (mrep.cu)
+  double* ssums = nullptr;       // (4d+4) x n
+  int scount = 0;
   // workspace carve
   double* ring_px = nullptr;
   double* ring_py = nullptr;
@@ -189,14 +192,15 @@ struct Plan {
       off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
       off_sscale, off_halo, off_rpart, off_mhalo, off_bmisc,
       off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, off_res, off_rhist, off_rbeta,
-      total;
+      off_ssums, total;
   int hist_cap, beta_cap;
   int nblocks;
 };
 
 int sm_count() { return device_sms(); }
 
-Plan make_plan(int64_t n, int d, int nA, int m_max, int max_cycles, int64_t plane = 1, int nranks = 1) {
+Plan make_plan(int64_t n, int d, int nA, int m_max, int max_cycles, int64_t plane = 1, int nranks = 1,
+               int mrep_stream = 0) {
   Plan p{};
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -246,6 +250,7 @@ Plan make_plan(int64_t n, int d, int nA, int m_max, int max_cycles, int64_t plan
   p.beta_cap = max_cycles;
   p.off_rhist = take((size_t)p.hist_cap * 8);
   p.off_rbeta = take((size_t)p.beta_cap * 8);
+  p.off_ssums = mrep_stream ? take((size_t)(4 * d + 4) * (size_t)n * 8) : o;   // f3
   p.total = o + 256;  // alignment slack for the base pointer
   return p;
 }
@@ -362,7 +367,7 @@ psp_status psp_workspace_bytes(const psp_grid* grid, const psp_stencil* st, int 
   PSP_TRY(validate(grid, st, d, restart, &o));
   int64_t n_loc, row0, s0, sl, plane;
   PSP_TRY(local_layout(grid, st, d, comm, &n_loc, &row0, &s0, &sl, &plane));
-  Plan p = make_plan(n_loc, d, restart, o.m_max, o.max_cycles, plane, comm ? comm->nranks : 1);
+  Plan p = make_plan(n_loc, d, restart, o.m_max, o.max_cycles, plane, comm ? comm->nranks : 1, o.mrep_stream);
   *bytes = p.total;
   return PSP_OK;
 }
@@ -377,12 +382,14 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   PSP_TRY(validate(grid, st, d, restart, &o));
   if (!(tol > 0.0) || !(dt >= 0.0)) return fail(nullptr, PSP_E_ARG, "tol must be > 0 and dt >= 0");
   if (o.method != PSP_METHOD_GMRES && o.method != PSP_METHOD_CG) return fail(nullptr, PSP_E_ARG, "bad method");
+  if (o.mrep_stream && comm && comm->nranks > 1)
+    return fail(nullptr, PSP_E_ARG, "streaming MREP is single-rank");
   if (o.method == PSP_METHOD_CG && comm && comm->nranks > 1)
     return fail(nullptr, PSP_E_ARG, "PSP-CG is single-rank (the symmetric part of N needs the neighbours' rows)");
   int64_t n, row0, slab0, slab_len, plane;
   PSP_TRY(local_layout(grid, st, d, comm, &n, &row0, &slab0, &slab_len, &plane));
   const int nranks = comm ? comm->nranks : 1;
-  Plan p = make_plan(n, d, restart, o.m_max, o.max_cycles, plane, nranks);
+  Plan p = make_plan(n, d, restart, o.m_max, o.max_cycles, plane, nranks, o.mrep_stream);
   if (!d_ws || ws_bytes < p.total) return fail(nullptr, PSP_E_NOMEM, "workspace smaller than psp_workspace_bytes");
 
   psp_ctx* c = new psp_ctx();
@@ -482,6 +489,7 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->res_beta = (double*)at(p.off_rbeta);
   c->res_hist_cap = p.hist_cap;
   c->res_beta_cap = p.beta_cap;
+  c->ssums = o.mrep_stream ? (double*)at(p.off_ssums) : nullptr;
   // zero the small control state (tickets, epochs, Hessenberg)
   cudaMemsetAsync(at(p.off_H), 0, p.off_partials - p.off_H, c->stream);
   cudaMemsetAsync(at(p.off_tickets), 0, TK_N * 4, c->stream);
@@ -582,6 +590,15 @@ int ring_next(psp_ctx* c) {
   return slot;
 }
 int ring_slot(const psp_ctx* c, int q) { return (c->ring_head + q) % c->ring_phys; }  // q-th oldest
+// f3: the probe just recorded in `slot` (its data and scale final in stream order) joins the
+// streaming MREP's lagged sums
+void stream_add(psp_ctx* c, int slot) {
+  if (!c->ssums) return;
+  launch_mrep_accumulate(c->ring_px + (int64_t)slot * c->n, c->ring_py + (int64_t)slot * c->n, c->slot_scale, slot,
+                         c->n, c->d, c->ssums, c->n, c->scount == 0 ? 1 : 0, c->stream);
+  c->scount += 1;
+  c->launches += 1;
+}
 double* px_col(psp_ctx* c, int slot) { return c->ring_px + (int64_t)slot * c->n; }
 double* py_col(psp_ctx* c, int slot) { return c->ring_py + (int64_t)slot * c->n; }
 double* Vcol(psp_ctx* c, int j /*1-based*/) { return c->V + (int64_t)(j - 1) * c->ldv; }
@@ -687,6 +704,7 @@ psp_status psp_matvec(psp_ctx* c, const double* x, double* y, int record) {
     const int slot = ring_next(c);
     set_unit_scale(c, slot);
     PSP_TRY(matvec(c, x, nullptr, py_col(c, slot), px_col(c, slot)));
+    stream_add(c, slot);
     launch_copy(py_col(c, slot), y, c->n, c->stream);
     c->launches += 1;
   } else {
@@ -799,6 +817,7 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   int h = kt_begin(c);
   PSP_TRY(matvec(c, c->X0, nullptr, py_col(c, slot), px_col(c, slot)));
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+  stream_add(c, slot);
   // l.5-7: R_bar = B - P_y(:,i); beta = ||R_bar||; G(1) = beta.  V(:,1) <- R_bar/beta
   // (l.6) is stored unnormalised with alpha_1 = 1/beta.  On the fused path V(:,1) goes straight
   // into the ring slot where it will be recorded as the probe Y_1 (N = I, l.11).
@@ -845,6 +864,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
     // free slot; recording it makes it the newest probe.
     const int slot = ring_next(c);
     if (slot != c->vslot[k]) return fail(c, PSP_E_ARG, "psp_arnoldi_step: steps out of order (fused cycle)");
+    stream_add(c, slot);
     if (k < c->nA) {
       // l.13-18 of step k, then l.10-16 of step k+1: one fused pass or three ring passes
       const int dst = ring_peek(c);
@@ -901,6 +921,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
       PSP_TRY(matvec(c, px, nullptr, py, nullptr));
       kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
     }
+    stream_add(c, slot);
     double* U = Vcol(c, k + 1);
     // l.13-17: MGS (R11) + H(k+1,k) + Givens (l.19-32) in the last block
     if (c->opts.ortho == PSP_MGS_LITERAL) {
@@ -999,6 +1020,7 @@ static psp_status cg_solve(psp_ctx* c, const double* b, const double* x0, psp_re
   int h = kt_begin(c);
   PSP_TRY(matvec(c, c->X0, nullptr, py_col(c, s0), px_col(c, s0)));
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, true));
+  stream_add(c, s0);
   h = kt_begin(c);
   launch_cg_start(b, py_col(c, s0), r, n, c->ds, c->rc, c->stream);
   c->launches += 1;
@@ -1042,6 +1064,7 @@ static psp_status cg_solve(psp_ctx* c, const double* b, const double* x0, psp_re
       kt_end(c, h, PSP_KC_CG, (pold ? 24.0 : 16.0) * dn + matvec_bytes(c, false) + 16.0 * dn);
     }
     R->matvecs += 1;
+    stream_add(c, s);                                 // (after the pass that set its scale)
     // x += alpha p, r -= alpha q, R(k) = ||r||
     h = kt_begin(c);
     launch_cg_update(c->X0, px_col(c, s), py_col(c, s), r, n, ident ? 1 : 0, c->ds, c->rc, c->stream);
@@ -1076,7 +1099,7 @@ static psp_status cg_solve(psp_ctx* c, const double* b, const double* x0, psp_re
 // 2^20 rows by default (a banded N: one CTA's sequential sweeps, n <= 16384)
 static bool resident_eligible(const psp_ctx* c) {
   if (c->opts.resident <= 0 || c->multi || c->opts.ortho != PSP_MGS_1REDUCE) return false;
-  if (c->opts.method != PSP_METHOD_GMRES) return false;
+  if (c->opts.method != PSP_METHOD_GMRES || c->ssums) return false;
   if (!resident_supported(c->n, c->nA, !c->n_identity)) return false;
   return c->opts.resident >= 2 || c->n <= kResidentAutoRows;
 }
@@ -1445,23 +1468,34 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
   psp_report dummy;
   memset(&dummy, 0, sizeof(dummy));
   psp_report* R = rep ? rep : &dummy;
-  const int m = c->ring_count;
+  // f3 (opts.mrep_stream): the window is every probe since the last fit, already summed
+  const int m = c->ssums ? c->scount : c->ring_count;
   R->mrep_ran = 0;
   if (m < 2 * c->d + 2) {  // R19
+    c->scount = 0;
     R->mrep_status = PSP_E_SAMPLES;
     return PSP_E_SAMPLES;
   }
   if (c->opts.timing) cudaEventRecord(c->ev[2], c->stream);
-  std::vector<int32_t> slots(m);
-  for (int q = 0; q < m; ++q) slots[q] = ring_slot(c, q);
   MrepOut out{c->bands, c->intercept, c->rowkind, c->kappa};
   cudaMemsetAsync(c->ms.ticket, 0, 64, c->stream);
   int h = kt_begin(c);
-  MrepMulti mm{c->multi ? c->comm : nullptr, c->mh_send, c->mh_recv, c->row0, c->n_global};
-  if (mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms,
-                  c->stream, mm))
-    return fail(c, PSP_E_NCCL, "MREP: collective failed");
-  kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
+  if (c->ssums) {
+    MrepScratch sc = c->ms;
+    sc.sums = c->ssums;
+    sc.sums_n = c->n;
+    mrep_fit_sums(m, c->n, c->d, out, sc, c->stream);
+    c->scount = 0;
+    kt_end(c, h, PSP_KC_MREP, (8.0 * (4 * c->d + 4) + 8.0 * (2 * c->d + 1)) * (double)c->n);
+  } else {
+    std::vector<int32_t> slots(m);
+    for (int q = 0; q < m; ++q) slots[q] = ring_slot(c, q);
+    MrepMulti mm{c->multi ? c->comm : nullptr, c->mh_send, c->mh_recv, c->row0, c->n_global};
+    if (mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms,
+                    c->stream, mm))
+      return fail(c, PSP_E_NCCL, "MREP: collective failed");
+    kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
+  }
   c->launches += 3;
   double r[16];
   PSP_TRY(sync_read(c, c->ms.result, 16, r));
@@ -1497,7 +1531,7 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
 psp_status psp_step(psp_ctx* c, const double* u_n, double* u_np1, psp_report* rep) {
   if (!c || !u_n || !u_np1) return fail(c, PSP_E_ARG, "psp_step: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
-  if (c->opts.reset_history_per_step) { c->ring_count = 0; c->ring_head = 0; }
+  if (c->opts.reset_history_per_step) { c->ring_count = 0; c->ring_head = 0; c->scount = 0; }
   // b := u^n (kept in B: u_np1 may alias u_n); X0 := u^n (R2)
   launch_copy(u_n, c->B, c->n, c->stream);
   c->launches += 1;
@@ -1569,6 +1603,7 @@ psp_status psp_ring_reset(psp_ctx* c) {
   if (!c) return PSP_E_ARG;
   c->ring_count = 0;
   c->ring_head = 0;
+  c->scount = 0;
   return PSP_OK;
 }
 

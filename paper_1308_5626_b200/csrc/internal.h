@@ -242,6 +242,12 @@ int mrep_launch(const double* px, const double* py, const double* slot_scale, in
                 const int32_t* slots, int m, int64_t n, int d, MrepOut out, MrepScratch sc,
                 cudaStream_t s, MrepMulti mm);
 
+// f3: streaming MREP.  Add the probe (scale[slot] * x, scale[slot] * y) to the (4d+4) x ns lagged
+// sums (first != 0: overwrite, the first probe of a window); then fit every row from the sums
+// (m probes), R18 and the gate statistics into sc.result as mrep_launch.  One rank.
+void launch_mrep_accumulate(const double* x, const double* y, const double* scale, int slot, int64_t n, int d,
+                            double* sums, int64_t ns, int first, cudaStream_t s);
+void mrep_fit_sums(int m, int64_t n, int d, MrepOut out, MrepScratch sc, cudaStream_t s);
 // R21 gate of a given N: the number of rows that are not strictly diagonally dominant -> *count
 // (device scalar; zeroed first).  grow0 / gN: global index of local row 0 and the global rows.
 // spd != 0 (PSP-CG, R29): a non-positive diagonal also counts

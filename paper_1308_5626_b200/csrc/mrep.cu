@@ -737,6 +737,120 @@ __global__ void gate_count_kernel(const double* __restrict__ bands, int64_t n, i
 
 }  // namespace
 
+// ------------------------------------------------------------------------------------------
+// f3: streaming MREP (the probe data are "obtained progressively").  Each recorded probe
+// (x, y) (scale sc: the probe is sc * column) adds its terms to every row's lagged sums, in the
+// recording order (oldest -> newest, as the ring's column order):
+//   C_l(r) += x_r x_{r+l} (l = 0..2d),  S(r) += x_r,  D_l(i) += x_{i-d+l} y_i (l = 0..2d),  T(i) += y_i
+// (x = 0 outside the matrix), the layout mrep_fitsum_kernel reads.  Bytes per row and probe:
+// x, y read, 4d+4 sums read and written = 16 + 16(4d+4).
+// ------------------------------------------------------------------------------------------
+namespace {
+template <int D>
+__global__ void __launch_bounds__(256) mrep_accumulate_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                              const double* scale, int slot, int64_t n,
+                                                              double* __restrict__ sums, int64_t ns, int first) {
+  const double sc = scale ? __ldg(scale + slot) : 1.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double xw[3 * D + 1];                                      // x_{r-D .. r+2D}
+#pragma unroll
+    for (int q = 0; q < 3 * D + 1; ++q) {
+      const int64_t rr = r - D + q;
+      xw[q] = (rr >= 0 && rr < n) ? sc * __ldg(x + rr) : 0.0;
+    }
+    const double yv = sc * __ldg(y + r), x0 = xw[D];
+#pragma unroll
+    for (int l = 0; l <= 2 * D; ++l) {
+      double* p = sums + (int64_t)l * ns + r;
+      *p = first ? x0 * xw[D + l] : fma(x0, xw[D + l], *p);
+    }
+    double* ps = sums + (int64_t)(2 * D + 1) * ns + r;
+    *ps = first ? x0 : *ps + x0;
+#pragma unroll
+    for (int l = 0; l <= 2 * D; ++l) {
+      double* p = sums + (int64_t)(2 * D + 2 + l) * ns + r;
+      *p = first ? xw[l] * yv : fma(xw[l], yv, *p);
+    }
+    double* pt = sums + (int64_t)(4 * D + 3) * ns + r;
+    *pt = first ? yv : *pt + yv;
+  }
+}
+
+// Boundary rows from the sums: the centred OLS slope from the row's moments,
+// sxx = C_0 - S^2/m, sxy = D_d - S T/m (R33: one-pass centred moments; the two-pass form of R16
+// needs the probes themselves); sxx < 1e-300 -> N(i,i) := 1, flagged.  Writes result[0..5].
+__global__ void mrep_boundary_sums_kernel(const double* __restrict__ sums, int64_t ns, int m, int64_t n, int d,
+                                          MrepOut out, MrepScratch sc) {
+  __shared__ double st[64][6];
+  const int t = threadIdx.x;
+  double v[6] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0};
+  const int64_t i = (t < d) ? t : (n - 2 * d + t);
+  if (t < 2 * d && i >= 0 && i < n) {
+    const double S = sums[(int64_t)(2 * d + 1) * ns + i], T = sums[(int64_t)(4 * d + 3) * ns + i];
+    const double C0 = sums[i], Dd = sums[(int64_t)(2 * d + 2 + d) * ns + i];
+    const double mx = S / (double)m, my = T / (double)m;
+    const double sxx = C0 - S * mx, sxy = Dd - S * my;
+    double b1, b0;
+    int kind;
+    if (sxx < 1e-300) { b1 = 1.0; b0 = 0.0; kind = PSP_ROW_FALLBACK_ZEROVAR; v[4] = 1.0; }
+    else { b1 = sxy / sxx; b0 = my - b1 * mx; kind = PSP_ROW_BOUNDARY; }
+    for (int o = 0; o <= 2 * d; ++o) out.bands[(int64_t)o * n + i] = (o == d) ? b1 : 0.0;
+    if (out.intercept) out.intercept[i] = b0;
+    if (out.kind) out.kind[i] = (uint8_t)kind;
+    if (out.kappa) out.kappa[i] = 0.0;
+    v[0] = fabs(b1);
+    v[2] = fabs(b1);
+    if (!(fabs(b1) > 0.0)) { v[1] = fabs(b1); v[5] = 1.0; }
+  }
+  for (int q = 0; q < 6; ++q) st[t][q] = v[q];
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < 64; ++w) {
+      v[0] = fmax(v[0], st[w][0]);
+      v[1] = fmax(v[1], st[w][1]);
+      v[2] = fmin(v[2], st[w][2]);
+      v[3] += st[w][3];
+      v[4] += st[w][4];
+      v[5] += st[w][5];
+    }
+    for (int q = 0; q < 6; ++q) sc.result[q] = v[q];
+  }
+}
+}  // namespace
+
+void launch_mrep_accumulate(const double* x, const double* y, const double* scale, int slot, int64_t n, int d,
+                            double* sums, int64_t ns, int first, cudaStream_t s) {
+  int64_t nb = (n + 255) / 256;
+  if (nb > 16 * device_sms()) nb = 16 * device_sms();
+  const unsigned g = (unsigned)(nb < 1 ? 1 : nb);
+  switch (d) {
+    case 1: mrep_accumulate_kernel<1><<<g, 256, 0, s>>>(x, y, scale, slot, n, sums, ns, first); break;
+    case 2: mrep_accumulate_kernel<2><<<g, 256, 0, s>>>(x, y, scale, slot, n, sums, ns, first); break;
+    case 3: mrep_accumulate_kernel<3><<<g, 256, 0, s>>>(x, y, scale, slot, n, sums, ns, first); break;
+    default: mrep_accumulate_kernel<4><<<g, 256, 0, s>>>(x, y, scale, slot, n, sums, ns, first); break;
+  }
+}
+
+void mrep_fit_sums(int m, int64_t n, int d, MrepOut out, MrepScratch sc, cudaStream_t s) {
+  cudaMemsetAsync(sc.result, 0, 16 * sizeof(double), s);
+  mrep_boundary_sums_kernel<<<1, 64, 0, s>>>(sc.sums, sc.sums_n, m, n, d, out, sc);
+  const int64_t rows = n - 2 * d;
+  if (rows > 0) {
+    int64_t g = (rows + TT - 1) / TT;
+    if (g > (int64_t)PSP_MREP_FIT_MINB * device_sms()) g = (int64_t)PSP_MREP_FIT_MINB * device_sms();
+    switch (d) {
+      case 1: mrep_fitsum_kernel<1><<<(unsigned)g, TT, 0, s>>>(m, n, n, 0, d, n - d, out, sc); break;
+      case 2: mrep_fitsum_kernel<2><<<(unsigned)g, TT, 0, s>>>(m, n, n, 0, d, n - d, out, sc); break;
+      case 3: mrep_fitsum_kernel<3><<<(unsigned)g, TT, 0, s>>>(m, n, n, 0, d, n - d, out, sc); break;
+      default: mrep_fitsum_kernel<4><<<(unsigned)g, TT, 0, s>>>(m, n, n, 0, d, n - d, out, sc); break;
+    }
+  }
+  mrep_decide_kernel<<<1, 1, 0, s>>>(sc);
+  int pb = (int)((n + 255) / 256);
+  if (pb > 8 * device_sms()) pb = 8 * device_sms();
+  mrep_patch_kernel<<<pb, 256, 0, s>>>(n, d, out, sc);
+}
+
 void launch_gate_count(const double* bands, int64_t n, int d, int64_t grow0, int64_t gN, double* count,
                        cudaStream_t s, int spd) {
   cudaMemsetAsync(count, 0, sizeof(double), s);

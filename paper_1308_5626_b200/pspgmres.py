@@ -49,7 +49,7 @@ class psp_opts(C.Structure):
                 ("reset_history_per_step", C.c_int32), ("ortho", C.c_int32), ("gate", C.c_int32),
                 ("timing", C.c_int32), ("fused", C.c_int32), ("fused_kmin", C.c_int32),
                 ("fused_kmax", C.c_int32), ("fused_split_cols", C.c_int32), ("resident", C.c_int32),
-                ("method", C.c_int32)]
+                ("method", C.c_int32), ("mrep_stream", C.c_int32)]
 
 
 class psp_report(C.Structure):
