@@ -173,6 +173,22 @@ psp_status psp_comm_init(const void* h_nccl_unique_id, int nranks, int rank, psp
  * caller's stream, meets the other ranks at a host barrier and moves data with cudaMemcpy, so
  * no kernel ever waits on another rank.  Same call sequence and results as NCCL ranks. */
 psp_status psp_comm_loopback_create(int nranks, psp_comm** out);
+/* Process-level backend: one process per rank, the collectives carried by the caller's own
+ * transport (e.g. torch.distributed over gloo) on HOST buffers.  Every callback is collective
+ * over the nranks processes and returns 0 on success; the library synchronises the stream and
+ * stages device data through pinned host memory around each call (host-mediated: no kernel ever
+ * waits on another rank).  allreduce: in place, op 0 sum / 1 max / 2 min, the same result on
+ * every rank.  sendrecv: send_lo goes to rank-1, whose send_hi arrives in recv_lo, and
+ * symmetrically with rank+1; the pointers of a missing neighbour are NULL with count 0.
+ * allgather: recv = the count values of rank 0, then rank 1, ... */
+typedef struct {
+  void* user;
+  int (*allreduce)(void* user, double* h_buf, size_t count, int op);
+  int (*sendrecv)(void* user, const double* h_send_lo, double* h_recv_lo, size_t n_lo, const double* h_send_hi,
+                  double* h_recv_hi, size_t n_hi);
+  int (*allgather)(void* user, const double* h_send, double* h_recv, size_t count);
+} psp_host_transport;
+psp_status psp_comm_host_create(const psp_host_transport* transport, int nranks, int rank, psp_comm** out);
 psp_status psp_comm_destroy(psp_comm* comm);
 
 /* The slab decomposition of a multi-rank context: contiguous blocks of the slowest

@@ -166,9 +166,75 @@ struct LoopComm : psp_comm {
   }
 };
 
+// ---- process-level host transport: the caller's collective callbacks on host buffers ----
+// (one process per rank, any transport the caller has -- e.g. torch.distributed over gloo; the
+// tests run two processes on one GPU this way, host-mediated so no kernel waits on another rank)
+struct HostComm : psp_comm {
+  psp_host_transport t{};
+  double* hb = nullptr;                     // pinned staging, grown on demand
+  size_t cap = 0;
+  ~HostComm() override {
+    if (hb) cudaFreeHost(hb);
+  }
+  double* stage(size_t count) {
+    if (count > cap) {
+      if (hb) cudaFreeHost(hb);
+      hb = nullptr;
+      cap = 0;
+      if (cudaMallocHost((void**)&hb, count * 8) != cudaSuccess) return nullptr;
+      cap = count;
+    }
+    return hb;
+  }
+  int d2h(double* h, const double* d, size_t count, cudaStream_t s) {
+    return (count == 0 || (cudaMemcpyAsync(h, d, count * 8, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+                           cudaStreamSynchronize(s) == cudaSuccess)) ? 0 : 1;
+  }
+  int h2d(double* d, const double* h, size_t count, cudaStream_t s) {
+    return (count == 0 || (cudaMemcpyAsync(d, h, count * 8, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+                           cudaStreamSynchronize(s) == cudaSuccess)) ? 0 : 1;
+  }
+  int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
+    double* h = stage(count);
+    if (!h || cudaStreamSynchronize(s) != cudaSuccess || d2h(h, d, count, s)) return 1;
+    if (t.allreduce(t.user, h, count, op)) return 1;
+    return h2d(d, h, count, s);
+  }
+  int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
+               double* recv_hi, size_t n_hi, cudaStream_t s) override {
+    const bool lo = rank > 0 && n_lo, hi = rank < nranks - 1 && n_hi;
+    double* h = stage(2 * (n_lo + n_hi) + 1);
+    if (!h || cudaStreamSynchronize(s) != cudaSuccess) return 1;
+    double *sl = h, *rl = h + n_lo, *sh = h + 2 * n_lo, *rh = h + 2 * n_lo + n_hi;
+    if ((lo && d2h(sl, send_lo, n_lo, s)) || (hi && d2h(sh, send_hi, n_hi, s))) return 1;
+    if (t.sendrecv(t.user, lo ? sl : nullptr, lo ? rl : nullptr, lo ? n_lo : 0, hi ? sh : nullptr,
+                   hi ? rh : nullptr, hi ? n_hi : 0))
+      return 1;
+    if ((lo && h2d(recv_lo, rl, n_lo, s)) || (hi && h2d(recv_hi, rh, n_hi, s))) return 1;
+    return 0;
+  }
+  int allgather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+    double* h = stage(count * (nranks + 1));
+    if (!h || cudaStreamSynchronize(s) != cudaSuccess || d2h(h, send, count, s)) return 1;
+    if (t.allgather(t.user, h, h + count, count)) return 1;
+    return h2d(recv, h + count, count * nranks, s);
+  }
+};
+
 }  // namespace
 
 extern "C" {
+
+psp_status psp_comm_host_create(const psp_host_transport* t, int nranks, int rank, psp_comm** out) {
+  if (!t || !out || nranks < 1 || rank < 0 || rank >= nranks || !t->allreduce || !t->sendrecv || !t->allgather)
+    return PSP_E_ARG;
+  auto* c = new HostComm();
+  c->t = *t;
+  c->nranks = nranks;
+  c->rank = rank;
+  *out = c;
+  return PSP_OK;
+}
 
 psp_status psp_comm_unique_id(void* id) {
   if (!id) return PSP_E_ARG;

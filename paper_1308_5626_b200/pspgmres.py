@@ -66,6 +66,15 @@ class psp_report(C.Structure):
                 ("resid_verified", C.c_int32), ("pad_", C.c_int32)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, C.c_size_t, C.c_int)
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _dp, C.c_size_t, _dp, _dp, C.c_size_t)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _dp, C.c_size_t)
+
+
+class psp_host_transport(C.Structure):
+    _fields_ = [("user", _vp), ("allreduce", ALLREDUCE_FN), ("sendrecv", SENDRECV_FN), ("allgather", ALLGATHER_FN)]
+
+
 class psp_mrep_info(C.Structure):
     _fields_ = [("rows_ridge", C.c_int64), ("rows_fallback", C.c_int64), ("rows_nondominant", C.c_int64),
                 ("max_abs_diag", C.c_double), ("gate_accepted", C.c_int32), ("status", C.c_int32)]
@@ -126,6 +135,7 @@ def lib():
         "psp_comm_unique_id": (C.c_int, [_vp]),
         "psp_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, P(_vp)]),
         "psp_comm_loopback_create": (C.c_int, [C.c_int, P(_vp)]),
+        "psp_comm_host_create": (C.c_int, [P(psp_host_transport), C.c_int, C.c_int, P(_vp)]),
         "psp_comm_destroy": (C.c_int, [_vp]),
         "psp_partition": (C.c_int, [P(psp_grid), C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                     P(C.c_int64)]),
@@ -145,7 +155,7 @@ EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destro
             "psp_ring_reset", "psp_get_hessenberg", "psp_get_basis", "psp_launch_count", "psp_kernel_stats",
             "psp_kernel_class_name", "psp_status_str",
             "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_loopback_create",
-            "psp_comm_destroy", "psp_partition"]
+            "psp_comm_host_create", "psp_comm_destroy", "psp_partition"]
 
 
 def psp_partition(n_axes, nranks, rank):
@@ -173,6 +183,64 @@ def psp_comm_loopback_create(nranks: int):
     arr = (_vp * nranks)()
     _check(lib().psp_comm_loopback_create(nranks, arr))
     return [_vp(a) for a in arr]
+
+
+class TorchDistTransport:
+    """The host collectives of psp_comm_host_create carried by torch.distributed on CPU tensors (a
+    gloo process group): argument marshalling only -- the library stages device data through
+    pinned host buffers around each call.  Keep the object alive while the communicator lives
+    (it owns the ctypes callbacks)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._ops = [dist.ReduceOp.SUM, dist.ReduceOp.MAX, dist.ReduceOp.MIN]
+        self._cbs = (ALLREDUCE_FN(self._allreduce), SENDRECV_FN(self._sendrecv), ALLGATHER_FN(self._allgather))
+        self.struct = psp_host_transport(None, *self._cbs)
+
+    @staticmethod
+    def _t(ptr, count):
+        import torch
+        return torch.from_numpy(np.ctypeslib.as_array(ptr, shape=(count,)))
+
+    def _allreduce(self, user, buf, count, op):
+        try:
+            self.dist.all_reduce(self._t(buf, count), op=self._ops[op], group=self.group)
+            return 0
+        except Exception:  # noqa: BLE001 -- a failed collective is PSP_E_NCCL in the library
+            return 1
+
+    def _sendrecv(self, user, send_lo, recv_lo, n_lo, send_hi, recv_hi, n_hi):
+        try:
+            reqs = []
+            if n_lo:
+                reqs.append(self.dist.isend(self._t(send_lo, n_lo), self.rank - 1, group=self.group))
+                reqs.append(self.dist.irecv(self._t(recv_lo, n_lo), self.rank - 1, group=self.group))
+            if n_hi:
+                reqs.append(self.dist.isend(self._t(send_hi, n_hi), self.rank + 1, group=self.group))
+                reqs.append(self.dist.irecv(self._t(recv_hi, n_hi), self.rank + 1, group=self.group))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _allgather(self, user, send, recv, count):
+        try:
+            out = self._t(recv, count * self.world)
+            self.dist.all_gather(list(out.split(count)), self._t(send, count).clone(), group=self.group)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+
+def psp_comm_host_create(transport: TorchDistTransport, nranks: int, rank: int):
+    h = _vp()
+    _check(lib().psp_comm_host_create(C.byref(transport.struct), nranks, rank, C.byref(h)))
+    return h
 
 
 def psp_comm_destroy(h):
