@@ -50,8 +50,12 @@ struct psp_ctx {
   double* ssums = nullptr;       // (4d+4) x n
   int scount = 0;
   // workspace carve
-  double* ring_px = nullptr;
+  double* ring_px = nullptr;      // column starts, ldr apart
   double* ring_py = nullptr;
+  int64_t ldr = 0;               // ring column stride: n, or n + 2 planes (multi-rank ghost planes)
+  int64_t goff = 0;              // the owned rows start goff into a column (a ghost plane when multi)
+  double* Wbase = nullptr;       // W's column start (W = Wbase + goff)
+  double* kpad = nullptr;        // multi-rank: the coefficient field with its ghost planes
   double* slot_scale = nullptr;  // per physical slot: the recorded probe is scale * column
   int ring_cap = 0, ring_count = 0, ring_head = 0;
   int ring_phys = 0;             // ring_cap + 1: the slot after the newest is always free
@@ -192,7 +196,7 @@ struct Plan {
       off_kappa, off_H, off_Hraw, off_G, off_C, off_S, off_Q, off_Lm, off_alpha, off_scal, off_resid,
       off_sscale, off_halo, off_rpart, off_mhalo, off_bmisc,
       off_partials, off_tickets, off_mpart, off_mtick, off_mres, off_banded, off_res, off_rhist, off_rbeta,
-      off_ssums, total;
+      off_ssums, off_kpad, total;
   int hist_cap, beta_cap;
   int nblocks;
 };
@@ -210,18 +214,20 @@ Plan make_plan(int64_t n, int d, int nA, int m_max, int max_cycles, int64_t plan
   };
   const size_t vec = (size_t)n * 8;
   p.nblocks = 8 * sm_count();
-  p.off_px = take(vec * (m_max + 1));  // m_max probes + the free slot (fused path)
-  p.off_py = take(vec * (m_max + 1));
+  // multi-rank: every ring column (and W) carries a ghost plane below / above the slab (the
+  // neighbours' boundary planes), so the fused passes run on slabs (fused.cu, FusedLayout)
+  const size_t gvec = (size_t)(n + (nranks > 1 ? 2 * plane : 0)) * 8;
+  p.off_px = take(gvec * (m_max + 1));  // m_max probes + the free slot (fused path)
+  p.off_py = take(gvec * (m_max + 1));
   p.off_sscale = take((size_t)(m_max + 1) * 8);
   p.off_V = take(vec * (nA + 1));
   p.off_X0 = take(vec);
   p.off_B = take(vec);
-  p.off_W = take(vec);
+  p.off_W = take(gvec);
+  p.off_kpad = nranks > 1 ? take(gvec) : 0;
   p.off_bands = take(vec * (2 * d + 1));
   p.off_lu = take(vec * (2 * d + 1));
-  p.off_icpt = take(vec);
-  p.off_kind = take((size_t)n);
-  p.off_kappa = take(vec);
+  p.off_icpt = p.off_kind = p.off_kappa = 0;   // (diagnostics: psp_mrep_fit_raw only)
   const size_t hs = (size_t)(nA + 1) * nA * 8;
   p.off_H = take(hs);
   p.off_Hraw = take(hs);
@@ -435,6 +441,8 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   auto at = [&](size_t off) { return base + off; };
   c->ring_px = (double*)at(p.off_px);
   c->ring_py = (double*)at(p.off_py);
+  c->goff = c->multi ? plane : 0;
+  c->ldr = n + 2 * c->goff;
   c->ring_cap = o.m_max;
   c->ring_phys = o.m_max + 1;
   c->slot_scale = (double*)at(p.off_sscale);
@@ -442,12 +450,14 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   c->ldv = n;
   c->X0 = (double*)at(p.off_X0);
   c->B = (double*)at(p.off_B);
-  c->W = (double*)at(p.off_W);
+  c->Wbase = (double*)at(p.off_W);
+  c->W = c->Wbase + c->goff;
+  c->kpad = c->multi ? (double*)at(p.off_kpad) : nullptr;
   c->bands = (double*)at(p.off_bands);
   c->lu = (double*)at(p.off_lu);
-  c->intercept = (double*)at(p.off_icpt);
-  c->rowkind = (uint8_t*)at(p.off_kind);
-  c->kappa = (double*)at(p.off_kappa);
+  c->intercept = nullptr;
+  c->rowkind = nullptr;
+  c->kappa = nullptr;
   c->ds.H = (double*)at(p.off_H);
   c->ds.Hraw = (double*)at(p.off_Hraw);
   c->ds.G = (double*)at(p.off_G);
@@ -512,6 +522,23 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
     }
     S.f_lo = c->rank > 0 ? c->hf_lo : nullptr;
     S.f_hi = c->rank < nranks - 1 ? c->hf_hi : nullptr;
+  }
+  if (c->multi) {
+    // ghost planes: zero (the Dirichlet value at the global boundary) until a neighbour fills them
+    for (int q = 0; q <= o.m_max; ++q) {
+      for (double* base : {c->ring_px, c->ring_py}) {
+        double* col = base + (int64_t)q * c->ldr;
+        cudaMemsetAsync(col, 0, (size_t)plane * 8, c->stream);
+        cudaMemsetAsync(col + plane + n, 0, (size_t)plane * 8, c->stream);
+      }
+    }
+    cudaMemsetAsync(c->Wbase, 0, (size_t)c->ldr * 8, c->stream);
+    cudaMemsetAsync(c->kpad, 0, (size_t)c->ldr * 8, c->stream);
+    if (S.field) {                                 // [kappa ghost below | kappa | kappa ghost above]
+      cudaMemcpyAsync(c->kpad + plane, S.field, (size_t)n * 8, cudaMemcpyDeviceToDevice, c->stream);
+      if (S.f_lo) cudaMemcpyAsync(c->kpad, S.f_lo, (size_t)plane * 8, cudaMemcpyDeviceToDevice, c->stream);
+      if (S.f_hi) cudaMemcpyAsync(c->kpad + plane + n, S.f_hi, (size_t)plane * 8, cudaMemcpyDeviceToDevice, c->stream);
+    }
   }
   psp_status s = check_cuda(c, "psp_create");
   if (s != PSP_OK) {
@@ -590,17 +617,17 @@ int ring_next(psp_ctx* c) {
   return slot;
 }
 int ring_slot(const psp_ctx* c, int q) { return (c->ring_head + q) % c->ring_phys; }  // q-th oldest
+double* px_col(psp_ctx* c, int slot) { return c->ring_px + (int64_t)slot * c->ldr + c->goff; }
+double* py_col(psp_ctx* c, int slot) { return c->ring_py + (int64_t)slot * c->ldr + c->goff; }
 // f3: the probe just recorded in `slot` (its data and scale final in stream order) joins the
 // streaming MREP's lagged sums
 void stream_add(psp_ctx* c, int slot) {
   if (!c->ssums) return;
-  launch_mrep_accumulate(c->ring_px + (int64_t)slot * c->n, c->ring_py + (int64_t)slot * c->n, c->slot_scale, slot,
+  launch_mrep_accumulate(px_col(c, slot), py_col(c, slot), c->slot_scale, slot,
                          c->n, c->d, c->ssums, c->n, c->scount == 0 ? 1 : 0, c->stream);
   c->scount += 1;
   c->launches += 1;
 }
-double* px_col(psp_ctx* c, int slot) { return c->ring_px + (int64_t)slot * c->n; }
-double* py_col(psp_ctx* c, int slot) { return c->ring_py + (int64_t)slot * c->n; }
 double* Vcol(psp_ctx* c, int j /*1-based*/) { return c->V + (int64_t)(j - 1) * c->ldv; }
 // a probe recorded normalised (scale 1)
 void set_unit_scale(psp_ctx* c, int slot) {
@@ -608,14 +635,35 @@ void set_unit_scale(psp_ctx* c, int slot) {
 }
 // the Krylov basis of the current cycle
 Basis basis(const psp_ctx* c) {
-  if (c->cycle_fused) return Basis{c->ring_px, c->n, c->vslot[1], c->ring_phys};
+  if (c->cycle_fused) return Basis{c->ring_px + c->goff, c->ldr, c->vslot[1], c->ring_phys};
   return Basis{c->V, c->ldv, 0, c->nA + 1};
 }
 // a ring-resident cycle: the Krylov basis lives in the probe ring (single rank: the fused pass
 // would need the halo planes of u in the middle of the pass)
 bool fused_eligible(const psp_ctx* c) {
-  return c->opts.fused && !c->multi && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE &&
-         c->ring_cap >= c->nA + 1;
+  // multi-rank: the ring columns carry ghost planes (exchanged after every pass), so the fused
+  // passes run on slabs; 1-D grids shard along x, which the fused pass does not march
+  return c->opts.fused && c->n_identity && c->opts.ortho == PSP_MGS_1REDUCE && c->ring_cap >= c->nA + 1 &&
+         (!c->multi || c->grid.ndim >= 2);
+}
+
+// multi-rank ring steps: the boundary planes of a freshly written column go to the neighbours'
+// ghost planes (one plane each way); no-op on one rank
+psp_status ghost_exchange(psp_ctx* c, double* col /* owned start */) {
+  if (!c->multi) return PSP_OK;
+  const int64_t pl = c->plane;
+  if (c->comm->sendrecv(col, col - pl, (size_t)pl, col + c->n - pl, col + c->n, (size_t)pl, c->stream))
+    return fail(c, PSP_E_NCCL, "ghost plane exchange failed");
+  return PSP_OK;
+}
+FusedLayout flayout(const psp_ctx* c) {
+  FusedLayout l;
+  l.ld = c->ldr;
+  l.zoff = c->multi ? 1 : 0;
+  l.lo_in = c->multi && c->rank > 0;
+  l.hi_in = c->multi && c->rank < c->nranks - 1;
+  l.field = c->multi ? c->kpad : c->st.field;
+  return l;
 }
 
 // y = A (xs x) [+ probe copy]; multi-rank: first the slab halo planes of x from rank-1 / rank+1
@@ -757,13 +805,22 @@ static psp_status ring_hyb_step(psp_ctx* c, int k, int src_slot, int dst) {
   launch_icwy_update(basis(c), py_col(c, src_slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds, c->rc,
                      c->stream, J);
   kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (J + 2) * dn);
+  PSP_TRY(ghost_exchange(c, c->W));                 // multi-rank: u' on the ghost planes
   h = kt_begin(c);
   const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, src_slot, 0,
-                              px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream, J, c->W);
+                              px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream, flayout(c), J,
+                              c->Wbase);
   if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
   kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, kb));
+  if (c->multi) {
+    if (c->comm->allreduce(c->ds.rpart + kHybOff, (size_t)(2 * kb + 2), 0, c->stream))
+      return fail(c, PSP_E_NCCL, "all-reduce failed");
+    PSP_TRY(ghost_exchange(c, px_col(c, dst)));
+    PSP_TRY(ghost_exchange(c, py_col(c, dst)));
+  }
   h = kt_begin(c);
   launch_icwy_dots_hyb(basis(c), py_col(c, dst), px_col(c, dst), J, k, c->nA, n, c->ds, c->rc, c->stream);
+  PSP_TRY(finish_reduce(c, EPI_HYB, 2 * J + 1, k, J, 0));
   kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (J + 2) * dn);
   cudaMemcpyAsync(c->slot_scale + dst, c->ds.alpha + k, sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
   c->launches += 3;
@@ -782,6 +839,7 @@ static psp_status ring_split_step(psp_ctx* c, int k, int src_slot, int dst) {
     h = kt_begin(c);
     launch_icwy_update(basis(c), py_col(c, src_slot), c->ds.alpha + (k - 1), px_col(c, dst), k, c->nA, n, c->ds,
                        c->rc, c->stream);
+    PSP_TRY(finish_reduce(c, EPI_UPDATE, 1, k, 0, 0));
     kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
     c->launches += 1;
   }
@@ -791,8 +849,13 @@ static psp_status ring_split_step(psp_ctx* c, int k, int src_slot, int dst) {
   kt_end(c, h, PSP_KC_MATVEC, matvec_bytes(c, false));
   h = kt_begin(c);
   launch_icwy_dots(basis(c), py_col(c, dst), k + 1, c->nA, n, 1, c->ds, c->rc, c->stream);
+  PSP_TRY(finish_reduce(c, EPI_DOTS_RAW, 2 * k + 1, k + 1, 0, 0));
   kt_end(c, h, PSP_KC_ORTHO_DOTS, 8.0 * (k + 2) * dn);
   c->launches += 1;
+  if (c->multi) {                                   // ghost planes for the fused passes that follow
+    PSP_TRY(ghost_exchange(c, px_col(c, dst)));
+    PSP_TRY(ghost_exchange(c, py_col(c, dst)));
+  }
   return PSP_OK;
 }
 
@@ -837,12 +900,18 @@ psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double
   if (c->cycle_fused && beta > 0.0 && isfinite(beta)) {
     // cycle-start pass: A V(:,1) -> P_y of the next slot and step 1's MGS coefficient
     if (fused_pass(c, 0)) {
+      PSP_TRY(ghost_exchange(c, px_col(c, c->vslot[1])));   // multi-rank: V(:,1) on the ghost planes
       h = kt_begin(c);
       const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, 0, c->nA, c->vslot[1],
-                                  1, nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream);
+                                  1, nullptr, py_col(c, c->vslot[1]), c->slot_scale, c->vslot[1], c->ds, c->stream,
+                                  flayout(c));
       if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
       kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, 0));
       c->launches += 1;
+      if (c->multi) {
+        PSP_TRY(ghost_exchange(c, py_col(c, c->vslot[1])));
+        PSP_TRY(finish_reduce(c, EPI_FUSED, 2, 0, 0, c->vslot[1]));
+      }
     } else {
       PSP_TRY(ring_split_step(c, 0, c->vslot[1], c->vslot[1]));
     }
@@ -872,10 +941,15 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
       if (fused_pass(c, k)) {
         h = kt_begin(c);
         const int fe = launch_fused(c->st, c->ring_px, c->ring_py, c->vslot[1], c->ring_phys, k, c->nA, slot, 0,
-                                    px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream);
+                                    px_col(c, dst), py_col(c, dst), c->slot_scale, dst, c->ds, c->stream, flayout(c));
         if (fe) return fail(c, PSP_E_CUDA, "fused pass: " + fused_error(fe));
         kt_end(c, h, PSP_KC_FUSED, fused_bytes(c, k));
         c->launches += 1;
+        if (c->multi) {                               // ghost planes of V(:,k+1), w~_{k+1}; the sums
+          PSP_TRY(ghost_exchange(c, px_col(c, dst)));
+          PSP_TRY(ghost_exchange(c, py_col(c, dst)));
+          PSP_TRY(finish_reduce(c, EPI_FUSED, 2 * k + 2, k, 0, dst));
+        }
       } else if (hyb_pass(c, k)) {
         PSP_TRY(ring_hyb_step(c, k, slot, dst));
       } else {
@@ -890,6 +964,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
         const int spare = ring_peek(c);
         launch_update_combine(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->X0, px_col(c, spare),
                               py_col(c, spare), k, c->nA, n, c->ds, c->rc, c->stream);
+        PSP_TRY(finish_reduce(c, EPI_UPDCOMB, 1, k, 0, 0));
         c->combined_k = k;
         c->combined_slot = spare;
         kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 4) * dn);
@@ -897,6 +972,7 @@ psp_status psp_arnoldi_step(psp_ctx* c, int k, double* h_resid, int* h_flags) {
       } else {
         launch_icwy_update(basis(c), py_col(c, slot), c->ds.alpha + (k - 1), c->W, k, c->nA, n, c->ds,
                            c->rc, c->stream);
+        PSP_TRY(finish_reduce(c, EPI_UPDATE, 1, k, 0, 0));
         kt_end(c, h, PSP_KC_ORTHO_UPDATE, 8.0 * (k + 2) * dn);
         c->launches += 1;
       }
@@ -1477,7 +1553,9 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
     return PSP_E_SAMPLES;
   }
   if (c->opts.timing) cudaEventRecord(c->ev[2], c->stream);
-  MrepOut out{c->bands, c->intercept, c->rowkind, c->kappa};
+  // the per-row diagnostics (intercept R15, row kind, condition estimate R17) are not written on
+  // the hot path: psp_mrep_fit_raw returns them (17 bytes a row less traffic)
+  MrepOut out{c->bands, nullptr, nullptr, nullptr};
   cudaMemsetAsync(c->ms.ticket, 0, 64, c->stream);
   int h = kt_begin(c);
   if (c->ssums) {
@@ -1491,8 +1569,8 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
     std::vector<int32_t> slots(m);
     for (int q = 0; q < m; ++q) slots[q] = ring_slot(c, q);
     MrepMulti mm{c->multi ? c->comm : nullptr, c->mh_send, c->mh_recv, c->row0, c->n_global};
-    if (mrep_launch(c->ring_px, c->ring_py, c->slot_scale, c->n, slots.data(), m, c->n, c->d, out, c->ms,
-                    c->stream, mm))
+    if (mrep_launch(c->ring_px + c->goff, c->ring_py + c->goff, c->slot_scale, c->ldr, slots.data(), m, c->n, c->d,
+                    out, c->ms, c->stream, mm))
       return fail(c, PSP_E_NCCL, "MREP: collective failed");
     kt_end(c, h, PSP_KC_MREP, (16.0 * m + 8.0 * (2 * c->d + 1)) * (double)c->n);
   }
@@ -1593,9 +1671,9 @@ psp_status psp_ring_view(const psp_ctx* c, int* count, int32_t* slots, double* s
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;
     for (int q = 0; q < c->ring_count; ++q) scale[q] = all[ring_slot(c, q)];
   }
-  if (px) *px = c->ring_px;
-  if (py) *py = c->ring_py;
-  if (ld) *ld = c->n;
+  if (px) *px = c->ring_px + c->goff;
+  if (py) *py = c->ring_py + c->goff;
+  if (ld) *ld = c->ldr;
   return PSP_OK;
 }
 
@@ -1620,7 +1698,7 @@ psp_status psp_get_hessenberg(const psp_ctx* c, double* H, double* Hraw, double*
 
 psp_status psp_get_basis(const psp_ctx* c, int j, const double** d_vj, double* h_scale) {
   if (!c || !d_vj || j < 1 || j > c->nA + 1) return PSP_E_ARG;
-  *d_vj = c->cycle_fused ? c->ring_px + (int64_t)c->vslot[j] * c->n : c->V + (int64_t)(j - 1) * c->ldv;
+  *d_vj = c->cycle_fused ? c->ring_px + (int64_t)c->vslot[j] * c->ldr + c->goff : c->V + (int64_t)(j - 1) * c->ldv;
   if (h_scale) {
     cudaMemcpyAsync(c->hp + 16, c->ds.alpha + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return PSP_E_CUDA;

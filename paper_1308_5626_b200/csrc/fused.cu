@@ -63,6 +63,8 @@ struct FusedArgs {
   double* slot_scale;  // per-slot probe scale
   int dst_slot;
   int zchunk;          // planes per tile along the march axis
+  int zoff;            // multi-rank ghost-plane layout: plane p of a column is TMA plane p + zoff
+  int lo_in, hi_in;    // the neighbour rank's planes exist below / above (ghost planes hold them)
   int64_t tiles_x, tiles_y, ntiles;
   DevState ds;
 };
@@ -272,10 +274,11 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
         if (lane == 0) mbar_expect_tx(full + si, stage_bytes);
         __syncwarp();
         for (int j = lane; j < nload; j += 32) {
-          if (j < (k > 0 ? kc : 0)) tma4(sb + j * NT, &mpx, x0, y0, zq, vslot[j], full + si);
+          const int zt = zq + a.zoff;            // (the ghost planes of the multi-rank layout)
+          if (j < (k > 0 ? kc : 0)) tma4(sb + j * NT, &mpx, x0, y0, zt, vslot[j], full + si);
           else if (j == (k > 0 ? kc : 0))
-            tma4(sb + KMAX * NT, a.src_px == 2 ? &msrc : (a.src_px ? &mpx : &mpy), x0, y0, zq, a.src_slot, full + si);
-          else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zq, 0, full + si);
+            tma4(sb + KMAX * NT, a.src_px == 2 ? &msrc : (a.src_px ? &mpx : &mpy), x0, y0, zt, a.src_slot, full + si);
+          else tma4(sb + (KMAX + 1) * NT, &mkap, x0, y0, zt, 0, full + si);
         }
       }
     }
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
       for (int i = 0; i < PP; ++i) {
         ub[i] = form_u(sbm, ptv[i]);
         kb[i] = cell ? sbm[(KMAX + 1) * NT + ptv[i]] : 0.0;
-        if (!(z0 >= 1 && in_grid[i])) ub[i] = 0.0;
+        if (!((z0 >= 1 || a.lo_in) && in_grid[i])) ub[i] = 0.0;
       }
       release(gb);
       const double* sbc = acquire(gb + 1);
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
 #pragma unroll
         for (int i = 0; i < PP; ++i) {
           un[i] = form_u(sn, ptv[i]);
-          if (!(pn < st.nz && in_grid[i])) un[i] = 0.0;
+          if (!((pn < st.nz || a.hi_in) && in_grid[i])) un[i] = 0.0;
           kt[i] = cell ? sn[(KMAX + 1) * NT + ptv[i]] : 0.0;
         }
         if (pn < z1) publish_u(up + 1, un, kt);  // the stencil of plane p+1 needs them
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
               // march-axis faces, also for a single-plane march axis (nz = 1): the Dirichlet
               // faces then hold u = 0 (ub / un are 0 off the grid), as in stencil.cu; the 1-D
               // view has s[2] = a[2] = 0, so the faces vanish there
-              const bool inb = p > 0, int_ = p + 1 < st.nz;
+              const bool inb = p > 0 || a.lo_in, int_ = p + 1 < st.nz || a.hi_in;
               face(ub[i], kb[i], inb, st.s[2], hsz);
               face(un[i], kt[i], int_, st.s[2], hsz);
               if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub[i], acc);
@@ -591,33 +594,15 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
   }
   __syncthreads();
   if (a.hyb) {                                    // the dots pass that follows finishes the step
-    for (int v = t; v < nv; v += NTH) a.ds.rpart[v] = tot[v];
+    for (int v = t; v < nv; v += NTH) a.ds.rpart[kHybOff + v] = tot[v];
+    return;
+  }
+  if (a.ds.multi) {                               // every rank's totals are all-reduced first,
+    for (int v = t; v < nv; v += NTH) a.ds.rpart[v] = tot[v];   // then EPI_FUSED (fused_tail)
     return;
   }
   if (t != 0) return;
-  DevState& ds = a.ds;
-  const int ldl = a.nA + 1;
-  const double t_u = tot[2 * k], s_nu = tot[2 * k + 1];
-  double an;  // alpha of u = V_{k+1}
-  if (k >= 1) {
-    ds.H[(int64_t)(k - 1) * ld + k] = sqrt(s_nu);  // l.17: H(k+1,k) = ||U_k||
-    givens_update(ds, k, a.nA);                    // l.19-32, sets alpha[k] (0 on breakdown)
-    an = ds.alpha[k];
-  } else {
-    an = ds.alpha[0];                              // 1/beta from the residual kernel (l.6)
-  }
-  a.slot_scale[a.dst_slot] = an;
-  if (k >= a.nA) return;
-  // MGS coefficients of step k+1 (column index k): (I + L) h = s (R11)
-  double* Lrow = ds.Lm + (int64_t)k * ldl;
-  for (int j = 0; j < k; ++j) Lrow[j] = ds.alpha[j] * an * tot[k + j];
-  double* Hc = ds.H + (int64_t)k * ld;
-  for (int j = 0; j <= k; ++j) {
-    double h = (j < k) ? ds.alpha[j] * an * tot[j] : an * an * t_u;
-    const double* Lr = ds.Lm + (int64_t)j * ldl;
-    for (int c = 0; c < j; ++c) h -= Lr[c] * Hc[c];
-    Hc[j] = h;
-  }
+  fused_tail(a.ds, k, a.nA, tot, a.slot_scale, a.dst_slot);
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime: no -lcuda) ----
@@ -642,12 +627,13 @@ constexpr int kErrLaunch = -2;     // cudaFuncSetAttribute / cudaLaunchKernelEx 
 
 // 4-D map (x, y, plane, slot) over nslots columns of n doubles at base; box TX x TY x 1 x 1
 thread_local int g_map_err = 0;   // last cuTensorMapEncodeTiled result (diagnostics)
-bool make_map(CUtensorMap* m, const double* base, const Stencil& st, int nslots, int TX, int TY) {
+// ld: slot stride (doubles); nzx: planes per column (nz, or nz + 2 with the ghost planes)
+bool make_map(CUtensorMap* m, const double* base, const Stencil& st, int nslots, int TX, int TY, int64_t ld,
+              int64_t nzx) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) { g_map_err = -1; return false; }
-  cuuint64_t dims[4] = {(cuuint64_t)st.nx, (cuuint64_t)st.ny, (cuuint64_t)st.nz, (cuuint64_t)nslots};
-  cuuint64_t strides[3] = {(cuuint64_t)st.nx * 8, (cuuint64_t)(st.nx * st.ny) * 8,
-                           (cuuint64_t)(st.nx * st.ny * st.nz) * 8};
+  cuuint64_t dims[4] = {(cuuint64_t)st.nx, (cuuint64_t)st.ny, (cuuint64_t)nzx, (cuuint64_t)nslots};
+  cuuint64_t strides[3] = {(cuuint64_t)st.nx * 8, (cuuint64_t)(st.nx * st.ny) * 8, (cuuint64_t)ld * 8};
   cuuint32_t box[4] = {(cuuint32_t)TX, (cuuint32_t)TY, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
@@ -661,15 +647,17 @@ struct MapCache {
   const double* px = nullptr;
   const double* py = nullptr;
   const double* field = nullptr;
-  int64_t nx = 0, ny = 0, nz = 0;
-  int cap = 0, tx = 0, ty = 0;
+  int64_t nx = 0, ny = 0, nz = 0, ld = 0;
+  int cap = 0, tx = 0, ty = 0, zoff = 0;
   const double* src = nullptr;
   CUtensorMap mpx, mpy, mk, ms;
   bool ok = false;
 };
 
+// ring_px / ring_py / field / src_vec: the column STARTS (the ghost plane when zoff = 1)
 template <int KIND, int TX, int TY, int KMAX, int CS, int PP = 1>
-int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStream_t s) {
+int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, const double* field, int64_t ld,
+             cudaStream_t s) {
   using Cfg = FCfg<TX, TY, KMAX, CS, PP>;
   // per host thread and device: the maps encode this device's pointers, the attribute is a
   // property of this device's context
@@ -678,14 +666,15 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   const int dev = device_ordinal();
   MapCache& mc = mcs[dev];
   const Stencil& st = a.st;
-  if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != st.field || mc.nx != st.nx ||
-      mc.ny != st.ny || mc.nz != st.nz || mc.cap != a.cap) {
-    mc.ok = make_map(&mc.mpx, ring_px, st, a.cap, TX, TY) && make_map(&mc.mpy, ring_py, st, a.cap, TX, TY) &&
-            (st.field == nullptr || make_map(&mc.mk, st.field, st, 1, TX, TY));
-    if (st.field == nullptr) mc.mk = mc.mpx;
-    mc.px = ring_px; mc.py = ring_py; mc.field = st.field;
+  const int64_t nzx = st.nz + 2 * a.zoff;
+  if (!mc.ok || mc.px != ring_px || mc.py != ring_py || mc.field != field || mc.nx != st.nx ||
+      mc.ny != st.ny || mc.nz != st.nz || mc.cap != a.cap || mc.ld != ld || mc.zoff != a.zoff) {
+    mc.ok = make_map(&mc.mpx, ring_px, st, a.cap, TX, TY, ld, nzx) && make_map(&mc.mpy, ring_py, st, a.cap, TX, TY, ld, nzx) &&
+            (field == nullptr || make_map(&mc.mk, field, st, 1, TX, TY, ld, nzx));
+    if (field == nullptr) mc.mk = mc.mpx;
+    mc.px = ring_px; mc.py = ring_py; mc.field = field;
     mc.src = nullptr;
-    mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap;
+    mc.nx = st.nx; mc.ny = st.ny; mc.nz = st.nz; mc.cap = a.cap; mc.ld = ld; mc.zoff = a.zoff;
   }
   if (!attr[dev]) {
     if (cudaFuncSetAttribute(fused_tma_kernel<KIND, TX, TY, KMAX, CS, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -708,7 +697,7 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
   a.ntiles = txy * ((st.nz + zc - 1) / zc);
   if (!mc.ok) return g_map_err ? g_map_err : kErrNoEncode;
   if (a.src_px == 2 && mc.src != a.src_vec) {      // plain-vector source (split-column step)
-    if (!make_map(&mc.ms, a.src_vec, st, 1, TX, TY)) return g_map_err ? g_map_err : kErrNoEncode;
+    if (!make_map(&mc.ms, a.src_vec, st, 1, TX, TY, ld, nzx)) return g_map_err ? g_map_err : kErrNoEncode;
     mc.src = a.src_vec;
   }
   if (a.src_px != 2 && mc.src == nullptr) mc.ms = mc.mpx;
@@ -725,7 +714,8 @@ int launch_t(FusedArgs a, const double* ring_px, const double* ring_py, cudaStre
 }
 
 template <int KIND>
-int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, cudaStream_t s) {
+int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const double* rpy, const double* fld, int64_t ld,
+                cudaStream_t s) {
   const int kc = a.k - a.jb;                       // basis columns of the pass
   if (three_d) {
     // stage = (KMAX + 2) boxes: the narrowest instantiation that holds k columns keeps the most
@@ -734,21 +724,21 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     // k <= 8: two points a thread on the tallest tiles whose stage ring still holds three
     // stages (32 x 30 at KMAX 4, 32 x 22 at KMAX 8): less halo work per point, same warps
     // (k = 2: 2.1 -> 1.97 ms, k = 5..8: 2.8-2.9 -> 2.6 ms at 512^3)
-    if (kc <= 4) return launch_t<KIND, 32, 30, 4, 1, 2>(a, rpx, rpy, s);
-    if (kc <= 8) return launch_t<KIND, 32, 22, 8, 1, 2>(a, rpx, rpy, s);
-    if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, s);
+    if (kc <= 4) return launch_t<KIND, 32, 30, 4, 1, 2>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 8) return launch_t<KIND, 32, 22, 8, 1, 2>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, fld, ld, s);
     // k = 13..16: 32 x 14 tiles with two points a thread (8 compute warps, up to 255 registers)
     // hold a thread's 16 basis values per point in registers, so a stage is released as soon as
     // u is formed; one thread per point on 32 x 15 tiles would keep two stages resident, on
     // 32 x 11 tiles (12 warps, 168 registers) carries more halo (cycle ~1.5 % slower); two
     // points a thread for k <= 12 was slower (2.0 -> 2.6 ms at k = 2)
-    if (kc <= 16) return launch_t<KIND, 32, 14, 16, 1, 2>(a, rpx, rpy, s);
-    if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, s);
-    return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, s);
+    if (kc <= 16) return launch_t<KIND, 32, 14, 16, 1, 2>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, fld, ld, s);
+    return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, fld, ld, s);
   }
-  if (kc <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, s);
-  if (kc <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, s);
-  return launch_t<KIND, 224, 1, 32, 2>(a, rpx, rpy, s);
+  if (kc <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, fld, ld, s);
+  if (kc <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, fld, ld, s);
+  return launch_t<KIND, 224, 1, 32, 2>(a, rpx, rpy, fld, ld, s);
 }
 
 // 3-D view of the local grid for the fused pass: the march axis is the slowest one
@@ -786,8 +776,11 @@ bool fused_supported(const Stencil& st, int k) {
 
 int launch_fused(const Stencil& st0, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
                   int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
-                  DevState ds, cudaStream_t s, int jb, const double* src_vec) {
+                  DevState ds, cudaStream_t s, const FusedLayout& lay, int jb, const double* src_vec) {
   FusedArgs a;
+  a.zoff = lay.zoff;
+  a.lo_in = lay.lo_in;
+  a.hi_in = lay.hi_in;
   a.jb = jb;
   a.hyb = src_vec != nullptr;
   a.src_vec = src_vec;
@@ -811,9 +804,9 @@ int launch_fused(const Stencil& st0, const double* ring_px, const double* ring_p
   a.ds = ds;
   const bool three_d = st0.ndim == 3;
   switch (st0.kind) {
-    case PSP_OP_CONST_DIFF: return launch_kind<PSP_OP_CONST_DIFF>(a, three_d, ring_px, ring_py, s);
-    case PSP_OP_CELL_DIFF: return launch_kind<PSP_OP_CELL_DIFF>(a, three_d, ring_px, ring_py, s);
-    default: return launch_kind<PSP_OP_CELL_ADVDIFF>(a, three_d, ring_px, ring_py, s);
+    case PSP_OP_CONST_DIFF: return launch_kind<PSP_OP_CONST_DIFF>(a, three_d, ring_px, ring_py, lay.field, lay.ld, s);
+    case PSP_OP_CELL_DIFF: return launch_kind<PSP_OP_CELL_DIFF>(a, three_d, ring_px, ring_py, lay.field, lay.ld, s);
+    default: return launch_kind<PSP_OP_CELL_ADVDIFF>(a, three_d, ring_px, ring_py, lay.field, lay.ld, s);
   }
 }
 

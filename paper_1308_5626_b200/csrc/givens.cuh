@@ -54,4 +54,36 @@ static __device__ __forceinline__ void givens_update(DevState ds, int k, int nA)
   ds.scal[SC_FLAGS] = (double)flags;
 }
 
+// ------------------------------------------------------------------------------------------
+// Scalar tail of a ring-resident step k (the fused pass of fused.cu, or EPI_FUSED after the
+// multi-rank all-reduce): from tot = [t_0..t_{k-1}, l_0..l_{k-1}, t_u, nu] (t_j = V_j' w~,
+// l_j = V_j' u, t_u = u' w~, nu = u'u of u = V(:,k+1) unnormalised) -- H(k+1,k) = ||U_k||, the
+// Givens update of column k (l.17-32), alpha_{k+1} -> slot_scale[dst_slot], and step k+1's MGS
+// coefficients by (I + L) h = s (R11).  k = 0: the cycle-start pass (no column to finish).
+// ------------------------------------------------------------------------------------------
+static __device__ void fused_tail(DevState ds, int k, int nA, const double* tot, double* slot_scale, int dst_slot) {
+  const int ld = nA + 1;
+  const double t_u = tot[2 * k], s_nu = tot[2 * k + 1];
+  double an;  // alpha of u = V_{k+1}
+  if (k >= 1) {
+    ds.H[(int64_t)(k - 1) * ld + k] = sqrt(s_nu);  // l.17: H(k+1,k) = ||U_k||
+    givens_update(ds, k, nA);                      // l.19-32, sets alpha[k] (0 on breakdown)
+    an = ds.alpha[k];
+  } else {
+    an = ds.alpha[0];                              // 1/beta from the residual kernel (l.6)
+  }
+  slot_scale[dst_slot] = an;
+  if (k >= nA) return;
+  // MGS coefficients of step k+1 (column index k): (I + L) h = s (R11)
+  double* Lrow = ds.Lm + (int64_t)k * ld;
+  for (int j = 0; j < k; ++j) Lrow[j] = ds.alpha[j] * an * tot[k + j];
+  double* Hc = ds.H + (int64_t)k * ld;
+  for (int j = 0; j <= k; ++j) {
+    double h = (j < k) ? ds.alpha[j] * an * tot[j] : an * an * t_u;
+    const double* Lr = ds.Lm + (int64_t)j * ld;
+    for (int c = 0; c < j; ++c) h -= Lr[c] * Hc[c];
+    Hc[j] = h;
+  }
+}
+
 }  // namespace psp

@@ -28,6 +28,7 @@ namespace psp {
 constexpr int kMaxD = 4;         // MREP / banded half-bandwidth supported by the kernels
 constexpr int kMaxRestart = 128; // n_A limit (device Hessenberg state is O(n_A^2))
 constexpr int kRedThreads = 256; // block size of the grid-reduction kernels
+constexpr int kHybOff = 2 * kMaxRestart + 16;   // ds.rpart offset of a split-column fused pass's sums
 
 // ------------------------------------------------------------------------------------------
 // Operator data (A = I - dt L, Eq.4).  Coefficients are precomputed on the host.
@@ -82,7 +83,10 @@ struct DevState {
 enum { EPI_NORM = 0, EPI_RESIDUAL = 1, EPI_MGS = 2, EPI_MGS_FINAL = 3, EPI_DOTS = 4, EPI_UPDATE = 5, EPI_DOTS_RAW = 6,
        EPI_HYB = 7,
        // f4, PSP-CG (cg.cuh): r0 = b - A x0; p'q and p'p of a direction; the x / r update; r'z
-       EPI_CG_START = 8, EPI_CG_DIR = 9, EPI_CG_UPD = 10, EPI_CG_RHO = 11 };
+       EPI_CG_START = 8, EPI_CG_DIR = 9, EPI_CG_UPD = 10, EPI_CG_RHO = 11,
+       // multi-rank ring steps: the fused pass's tail (givens.cuh fused_tail; slot = dst slot) and
+       // the last step's update + combine coefficients (krylov.cu)
+       EPI_FUSED = 12, EPI_UPDCOMB = 13 };
 void launch_epilogue(int kind, DevState ds, int k, int nA, int j, int slot, cudaStream_t s);
 enum { SC_BETA = 0, SC_EPS = 1, SC_RK = 2, SC_FLAGS = 3, SC_STATUS = 4, SC_NORM = 5,
        SC_MAXDIAG = 6, SC_GATE = 7, SC_TMP = 8, SC_RHO = 9, SC_ALPHA = 10, SC_BETACG = 11, SC_NSCAL = 16 };
@@ -166,10 +170,19 @@ bool launch_cg_dir_fused(const Stencil& st, const double* z, const double* pold,
 bool fused_supported(const Stencil& st, int k);
 // finish step k (u = V_{k+1} -> dstx, A u -> dsty, H(k+1,k), Givens, alpha_{k+1} ->
 // slot_scale[dst_slot]) and compute step k+1's MGS coefficients; k = 0 is the cycle-start pass
-// returns 0, or the cuTensorMapEncodeTiled error of the operand maps
+// returns 0, or the cuTensorMapEncodeTiled error of the operand maps.
+// Layout of the ring columns: ring_px / ring_py / lay.field / src_vec are column STARTS, columns
+// lay.ld apart; with lay.zoff = 1 (multi-rank slabs) every column carries a ghost plane below and
+// above the nz owned planes (the neighbour ranks' boundary planes, zero at the global boundary),
+// and lo_in / hi_in say whether the neighbour exists (its ghost plane is interior, not Dirichlet).
+struct FusedLayout {
+  int64_t ld;
+  int zoff, lo_in, hi_in;
+  const double* field;   // the coefficient field's column start (NULL: constant coefficients)
+};
 int launch_fused(const Stencil& st, const double* ring_px, const double* ring_py, int vs1, int cap, int k, int nA,
                   int src_slot, int src_px, double* dstx, double* dsty, double* slot_scale, int dst_slot,
-                  DevState ds, cudaStream_t s, int jb = 0, const double* src_vec = nullptr);
+                  DevState ds, cudaStream_t s, const FusedLayout& lay, int jb = 0, const double* src_vec = nullptr);
 
 // ---- f2: the device-resident solve (resident.cu) ----
 constexpr int kResidentMaxRestart = 64;       // replicated per-CTA scalar state in shared memory

@@ -33,8 +33,18 @@ constexpr int JC = 4;             // basis vectors per chunk
 // ------------------------------------------------------------------------------------------
 // Scalar epilogues of the reductions (one thread), from the totals tot[]
 // ------------------------------------------------------------------------------------------
+__device__ void updcomb_tail(DevState ds, int k, int nA, double tt);
+
 __device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, const double* tot) {
   const int ld = nA + 1;
+  if (kind == EPI_FUSED) {                        // multi-rank fused ring step (givens.cuh)
+    fused_tail(ds, k, nA, tot, ds.slot_scale, slot);
+    return;
+  }
+  if (kind == EPI_UPDCOMB) {                      // multi-rank last step of a ring cycle
+    updcomb_tail(ds, k, nA, tot[0]);
+    return;
+  }
   if (kind >= EPI_CG_START) {                     // f4 (cg.cuh); j = 1: N = I
     cg_epilogue(kind, ds, slot, j, tot);
     return;
@@ -77,7 +87,7 @@ __device__ void epilogue(int kind, DevState ds, int k, int nA, int j, int slot, 
       // columns [0, J): tot = [s_0..s_J, l_0..l_{J-1}] of the dots pass (s_J = u'w~);
       // columns [J, k): ds.rpart = [t_J..t_{k-1}, l_J..l_{k-1}, t_u, nu] of the fused pass
       const int J = j, kk = k - J;
-      const double* hb = ds.rpart;
+      const double* hb = ds.rpart + kHybOff;
       const double t_u = hb[2 * kk], s_nu = hb[2 * kk + 1];
       ds.H[(int64_t)(k - 1) * ld + k] = sqrt(s_nu);  // l.17: H(k+1,k) = ||U_k||
       givens_update(ds, k, nA);                       // l.19-32, sets alpha[k] (0 on breakdown)
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(TPB) icwy_dots_kernel(Basis V,
     }
     __syncthreads();
     if (t == 0) {
-      if (last != nullptr) epilogue(EPI_HYB, ds, kstep, nA, k - 1, 0, tot);
+      if (last != nullptr) finish_scalar(ds, EPI_HYB, kstep, nA, k - 1, 0, tot, nv);
       else finish_scalar(ds, w_raw ? EPI_DOTS_RAW : EPI_DOTS, k, nA, 0, 0, tot, nv);
     }
   }
@@ -559,6 +569,22 @@ __device__ __forceinline__ void update_combine_tile(const double* const* cp, con
 
 // U_k = alpha_k w~_k - sum_j h_j alpha_j V_j (only ||U_k|| is kept), z0 = X0 + Z0, z1 = Z1; the
 // last block: H(k+1,k), Givens (l.17-32), then Q = H^{-1}G (R6) with y_k -> ds.scal[SC_TMP].
+__device__ void updcomb_tail(DevState ds, int k, int nA, double tt) {
+  const int ld = nA + 1;
+  epilogue(EPI_UPDATE, ds, k, nA, 0, 0, &tt);       // H(k+1,k) = ||U||, Givens of column k
+  // Q = H^{-1} G (R6), as combine_kernel
+  int bad = ds.rpart[2 * k] != 0.0;
+  for (int j = k; j >= 1; --j) {
+    double sv = ds.G[j - 1];
+    for (int q = j + 1; q <= k; ++q) sv -= ds.H[(int64_t)(q - 1) * ld + (j - 1)] * ds.Q[q - 1];
+    const double piv = ds.H[(int64_t)(j - 1) * ld + (j - 1)];
+    if (piv == 0.0) { bad = 1; ds.Q[j - 1] = 0.0; continue; }
+    ds.Q[j - 1] = sv / piv;
+  }
+  ds.scal[SC_TMP] = ds.Q[k - 1];                    // y_k
+  ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
+}
+
 __global__ void __launch_bounds__(TPB) update_combine_kernel(Basis V, const double* __restrict__ w,
                                                              const double* ws, const double* __restrict__ x0,
                                                              double* __restrict__ z0, double* __restrict__ z1,
@@ -588,20 +614,11 @@ __global__ void __launch_bounds__(TPB) update_combine_kernel(Basis V, const doub
   if (finish_block(ds.tickets + TK_MAIN)) {
     double tt = reduce_partials(ds.partials, 0, gridDim.x, sm);
     if (t == 0) {
-      epilogue(EPI_UPDATE, ds, k, nA, 0, 0, &tt);     // H(k+1,k) = ||U||, Givens of column k
-      // Q = H^{-1} G (R6), as combine_kernel
-      int bad = ds.rpart[2 * k] != 0.0;
-      for (int j = k; j >= 1; --j) {
-        double sv = ds.G[j - 1];
-        for (int q = j + 1; q <= k; ++q) sv -= ds.H[(int64_t)(q - 1) * ld + (j - 1)] * ds.Q[q - 1];
-        const double piv = ds.H[(int64_t)(j - 1) * ld + (j - 1)];
-        if (piv == 0.0) { bad = 1; ds.Q[j - 1] = 0.0; continue; }
-        ds.Q[j - 1] = sv / piv;
-      }
-      ds.scal[SC_TMP] = ds.Q[k - 1];                  // y_k
-      ds.scal[SC_STATUS] = bad ? (double)PSP_E_SINGULAR : 0.0;
+      if (ds.multi) ds.rpart[0] = tt;                 // (c0 / c1 were read; rpart[2k] stays)
+      else updcomb_tail(ds, k, nA, tt);
     }
   }
+  (void)ld;
 }
 
 // cycle end after update_combine_kernel: x = z0 + y_k z1

@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
   double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TT]: C_l, S of the tile's rows
   uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (SUMS ? 0 : (2 * D + 2) * TT));
   __shared__ double scs[kMaxM];                    // per-column probe scale
+  __shared__ double scs2[kMaxM];                   //   and its square
   __shared__ double red[TT / 32 * 6];
   __shared__ int s_unit;
   const int t = threadIdx.x;
@@ -425,6 +426,7 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
   __syncthreads();
   for (int c = t; c < m; c += TT) {
     scs[c] = scale ? scale[cols.slot[c]] : 1.0;
+    scs2[c] = scs[c] * scs[c];
     if (scs[c] != 1.0) s_unit = 0;
   }
   if (t == 0) {
@@ -496,23 +498,26 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
         for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
       }
     } else {
+      // scaled probes (s x, s y): the scale enters the products once, as s^2 on one factor
+      // (2 multiplies a column instead of 3d+2; equal to the scaled sums up to rounding)
       const int c0 = ch * TCB;
 #pragma unroll
       for (int cc = 0; cc < TCB; ++cc) {
         if (cc >= ccn) break;                      // uniform
-        const double sc = scs[c0 + cc];
+        const double sc = scs[c0 + cc], s2 = scs2[c0 + cc];
         const double* xr = st + cc * Cfg::PXW + xo;
         double xw[3 * D + 1];
 #pragma unroll
-        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = sc * xr[k];
-        const double yv = sc * st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
+        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
+        const double yr = st[TCB * Cfg::PXW + cc * Cfg::PYW + yo];
         const double x0 = xw[D];
-        Ssum += x0;
-        Tsum += yv;
+        Ssum = fma(sc, x0, Ssum);
+        Tsum = fma(sc, yr, Tsum);
+        const double ax = s2 * x0, by = s2 * yr;
 #pragma unroll
-        for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+        for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(ax, xw[D + l], Cl[l]);
 #pragma unroll
-        for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yv, Dl[l]);
+        for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], by, Dl[l]);
       }
     }
     __syncthreads();                               // every thread is done with stage stg

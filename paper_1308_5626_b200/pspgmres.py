@@ -433,8 +433,9 @@ class Context:
         phys = self.opts.m_max + 1
         t = self.torch
         ws64 = self.ws.view(t.float64)
-        PXr = ws64[(px.value - base) // 8:(px.value - base) // 8 + phys * self.n].view(phys, self.n)
-        PYr = ws64[(py.value - base) // 8:(py.value - base) // 8 + phys * self.n].view(phys, self.n)
+        L = ld.value                     # column stride (multi-rank columns carry ghost planes)
+        PXr = ws64[(px.value - base) // 8:(px.value - base) // 8 + (phys - 1) * L + self.n].as_strided((phys, self.n), (L, 1))
+        PYr = ws64[(py.value - base) // 8:(py.value - base) // 8 + (phys - 1) * L + self.n].as_strided((phys, self.n), (L, 1))
         m = cnt.value
         sl = list(slots[:m])
         sc = t.tensor(scale[:m], dtype=t.float64, device=self.device)[:, None]

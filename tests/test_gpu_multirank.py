@@ -180,3 +180,40 @@ def test_banded_precond_multirank(torch, P, orc, nranks, d):
             return zl.cpu().numpy()
     z = np.concatenate(run_ranks(P, nranks, fn))
     assert np.linalg.norm(z - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
+
+
+FUSED_MODES = {"fused": dict(fused=2, fused_kmin=0, fused_kmax=32, resident=0),
+               "ring": dict(fused=2, resident=0),
+               "hybrid": dict(fused=2, fused_kmin=0, fused_kmax=2, fused_split_cols=2, resident=0)}
+
+
+@pytest.mark.parametrize("mode", list(FUSED_MODES))
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("case", ["C4s", "C2s"])
+def test_fused_ring_on_slabs(torch, P, orc, mode, nranks, case):
+    """The ring-resident fused / split-column passes on z-slabs (y-slabs in 2-D): every ring column
+    carries ghost planes, refreshed after each pass by one plane exchange each way, so a sharded
+    Arnoldi step streams the same bytes per row as one GPU's.  Against the single-rank run of the
+    same mode: T5, the first cycle to T4's floor, the true residual; and against the oracle."""
+    if case == "C4s":
+        prob = inputs.Problem("C4s", inputs.OperatorSpec(3, "cell_diff", (20, 18, 16), 2e-4,
+                                                         field=np.exp(np.random.default_rng(5).standard_normal(20 * 18 * 16))),
+                              np.random.default_rng(6).uniform(-1, 1, 20 * 18 * 16), 30, 1e-8, 3, 2, 32, 1000)
+    else:
+        prob = inputs.c2(n=64, d=1, steps=2)
+    kw = FUSED_MODES[mode]
+    m = multi_steps(torch, P, prob, nranks, 2, kw)
+    s = single_steps(torch, P, prob, 2, kw)
+    for rm, rs in zip(m["reps"], s["reps"]):
+        assert abs(rm["iterations"] - rs["iterations"]) <= 1
+        L = min(rm["resid_len"], rs["resid_len"], prob.restart)
+        beta = rs["beta_history"][0]
+        assert np.all(np.abs(rm["resid_history"][:L] - rs["resid_history"][:L])
+                      <= 1e-8 * rs["resid_history"][:L] + 1e-11 * beta)
+        assert rm["final_resid_true"] <= 1.05 * rm["eps"]
+        assert bool(rm["mrep_gate_accepted"]) == bool(rs["mrep_gate_accepted"])
+    for p in m["parts"][1:]:
+        assert [r["iterations"] for r in p["reps"]] == [r["iterations"] for r in m["reps"]]
+    r = orc.time_steps(prob.op, prob.u0, 2, prob.restart, prob.max_cycles, prob.tol, prob.d, prob.m_max)
+    assert abs(m["reps"][0]["iterations"] - r["reports"][0]["solve"]["iterations"]) <= 1
+    assert np.linalg.norm(m["u"] - s["u"]) <= 4 * prob.tol * np.linalg.norm(prob.u0) * 50
