@@ -13,6 +13,7 @@ run() {   # name, kernel regex, skip, count, command...
   python tools/ncu_box_summary.py $O > /dev/null 2>&1
   tail -c 2000 $O/$name.log > $O/$name.logtail; rm -f $O/$name.log
 }
+timeout 1200 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_fullsize.py > $O/pytest.log 2>&1; tail -15 $O/pytest.log
 python tools/kbench.py matvec 512 5 > $O/kb_matvec.txt 2>&1 || exit 1
 for d in 1 2 3 4; do python tools/kbench.py solve 26 $d 5 > $O/kb_solve$d.txt 2>&1 || exit 1; done
 python tools/kbench.py mrep 27 32 3 3 > $O/kb_mrep3.txt 2>&1 || exit 1
