@@ -763,9 +763,12 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
                                                       has_next, vec, warm, st_start);
 }
 
+// phase 0: the whole sweep; 1: map (zero-state rows written to out) + scan (s_out = the state after
+// the last row from s_in0); 2: scan from s_in0 + fix + apply over the maps and rows phase 1 left
+// (multi-rank: the incoming state is known only after the ranks' outgoing states are gathered)
 template <bool FWD, int D>
 void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
-                  double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out) {
+                  double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out, int phase) {
   const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const size_t smem = TileSmem<FWD, D>::BYTES;
   const size_t ssmem = (size_t)SCAN_T * sizeof(Map<D>);
@@ -785,10 +788,10 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
   const int64_t L = (ntiles + nb - 1) / nb;
   nb = (ntiles + L - 1) / L;
   double* full = sc.states + (size_t)SCAN_T * (D * D + 2 * D);   // per-range flag
-  if (ntiles > 0)
+  if (ntiles > 0 && phase != 2)
     tile_map_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
   tile_scan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>(ntiles > 0 ? (int)nb : 0, sc.states, s_in0, s_out);
-  if (out != nullptr && ntiles > 0) {
+  if (out != nullptr && ntiles > 0 && phase != 1) {
     tile_fix_kernel<FWD, D><<<(unsigned)((nb + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nb, out, sc.states, full);
     tile_apply_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states, full);
   }
@@ -796,10 +799,10 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
 
 void sweep(bool fwd, int d, const double* lu, int64_t n, const double* v, const double* vs,
            const double* add, double* out, BandedScratch sc, cudaStream_t s, const double* s_in0,
-           double* s_out) {
-#define PSP_SWEEP(DD)                                                            \
-  if (fwd) sweep_launch<true, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out); \
-  else sweep_launch<false, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out);
+           double* s_out, int phase = 0) {
+#define PSP_SWEEP(DD)                                                                   \
+  if (fwd) sweep_launch<true, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out, phase); \
+  else sweep_launch<false, DD>(lu, n, v, vs, add, out, sc, s, s_in0, s_out, phase);
   switch (d) {
     case 1: PSP_SWEEP(1) break;
     case 2: PSP_SWEEP(2) break;
@@ -1001,9 +1004,11 @@ int banded_factor(const double* bands, int64_t n, int d, double* lu, BandedScrat
   return PSP_OK;
 }
 
-// z = x0 + N^{-1}(vs v).  Multi-rank: each sweep runs twice -- a zero-state pass that only
-// yields this rank's outgoing state t_r, an all-gather of the t's, the state entering this rank
-// composed from the ranks before it (maps from banded_factor), then the exact pass.
+// z = x0 + N^{-1}(vs v).  Multi-rank: each sweep is still ONE pass over the rows -- the zero-
+// state pass writes its rows and yields this rank's outgoing state t_r; an all-gather of the t's;
+// the state entering this rank composed from the ranks before it (maps from banded_factor); then
+// only the range scan and the decaying homogeneous corrections from that state (tile_fix, and
+// tile_apply for a range whose correction has not decayed).
 int banded_solve(const double* lu, int64_t n, int d, const double* v, const double* vs,
                  const double* x0, double* z, BandedScratch sc, cudaStream_t s, int64_t* launches,
                  psp_comm* comm, double* misc) {
@@ -1017,13 +1022,15 @@ int banded_solve(const double* lu, int64_t n, int d, const double* v, const doub
   for (int fwd = 1; fwd >= 0; --fwd) {
     const double* vin = fwd ? v : sc.y;
     const double* vsc = fwd ? vs : nullptr;
-    sweep(fwd != 0, d, lu, n, vin, vsc, nullptr, nullptr, sc, s, nullptr, M.t);
+    const double* add = fwd ? nullptr : x0;
+    double* out = fwd ? sc.y : z;
+    sweep(fwd != 0, d, lu, n, vin, vsc, add, out, sc, s, nullptr, M.t, 1);
     if (comm->allgather(M.t, M.tall, (size_t)d, s)) return PSP_E_NCCL;
     compose_states_kernel<<<1, 1, 0, s>>>(fwd ? M.Mf : M.Mb, M.tall, d, comm->nranks, comm->rank, fwd,
                                           M.sin);
-    sweep(fwd != 0, d, lu, n, vin, vsc, fwd ? nullptr : x0, fwd ? sc.y : z, sc, s, M.sin, nullptr);
+    sweep(fwd != 0, d, lu, n, vin, vsc, add, out, sc, s, M.sin, nullptr, 2);
   }
-  if (launches) *launches += 6;
+  if (launches) *launches += 8;
   return PSP_OK;
 }
 
