@@ -311,6 +311,11 @@ psp_status psp_banded_solve_raw(const double* d_lu, int64_t n, int d, const doub
  * gate when opts.gate, then factors.  *h_accepted = 1 if installed, 0 if N = I.
  * d_bands == NULL installs N = I. */
 psp_status psp_set_bands(psp_ctx* ctx, const double* d_bands, int* h_accepted);
+/* Fault injection (SPEC AC10): zero rows h_rows[0..count) (local indices) of the current
+ * N's bands and re-install it through the R21 gate and the factorisation (as psp_set_bands):
+ * the corrupted N is rejected (gate) or fails the factorisation (zero pivot), N := I and
+ * *h_accepted = 0 -- the identity fallback of S:281 / S:345.  Test hook. */
+psp_status psp_inject_fault_rows(psp_ctx* ctx, const int64_t* h_rows, int count, int* h_accepted);
 /* Copy the current N into d_bands_out ((2d+1) x n_loc); *h_is_identity = 1 when N = I. */
 psp_status psp_get_bands(const psp_ctx* ctx, double* d_bands_out, int* h_is_identity);
 /* Probe ring view: the c-th oldest recorded probe (c < *h_count) is

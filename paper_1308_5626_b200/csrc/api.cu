@@ -13,9 +13,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 using namespace psp;
+
+namespace {
+// NVTX ranges around the host API (header-only NVTX3: free unless a profiler is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct psp_ctx {
   // configuration
@@ -867,6 +877,7 @@ static double fused_bytes(const psp_ctx* c, int k) {
 }
 
 psp_status psp_cycle_begin(psp_ctx* c, const double* b, const double* x0, double* h_beta) {
+  NvtxRange nv("psp_cycle_begin");
   if (!c || !b || !x0) return fail(c, PSP_E_ARG, "psp_cycle_begin: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
   if (x0 != c->X0) {
@@ -1284,6 +1295,7 @@ static psp_status resident_solve(psp_ctx* c, const double* b, const double* x0, 
 }
 
 psp_status psp_solve(psp_ctx* c, const double* b, const double* x0, double* x, psp_report* rep) {
+  NvtxRange nv("psp_solve");
   if (!c || !b || !x0 || !x) return fail(c, PSP_E_ARG, "psp_solve: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
   psp_report dummy;
@@ -1514,6 +1526,7 @@ psp_status psp_banded_solve_raw(const double* lu, int64_t n, int d, const double
 }
 
 static psp_status install_bands(psp_ctx* c, bool gate_ok, psp_report* R) {
+  NvtxRange nv("banded_factor");
   bool accept = gate_ok;
   if (accept) {
     if (c->opts.timing) cudaEventRecord(c->ev[4], c->stream);
@@ -1539,6 +1552,7 @@ static psp_status install_bands(psp_ctx* c, bool gate_ok, psp_report* R) {
 }
 
 psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
+  NvtxRange nv("psp_mrep_fit");
   if (!c) return fail(c, PSP_E_ARG, "psp_mrep_fit: NULL ctx");
   if (c->sticky != PSP_OK) return c->sticky;
   psp_report dummy;
@@ -1607,6 +1621,7 @@ psp_status psp_mrep_fit(psp_ctx* c, psp_report* rep) {
 }
 
 psp_status psp_step(psp_ctx* c, const double* u_n, double* u_np1, psp_report* rep) {
+  NvtxRange nv("psp_step");
   if (!c || !u_n || !u_np1) return fail(c, PSP_E_ARG, "psp_step: NULL argument");
   if (c->sticky != PSP_OK) return c->sticky;
   if (c->opts.reset_history_per_step) { c->ring_count = 0; c->ring_head = 0; c->scount = 0; }
@@ -1648,6 +1663,21 @@ psp_status psp_set_bands(psp_ctx* c, const double* d_bands, int* h_accepted) {
   PSP_TRY(install_bands(c, ok, nullptr));
   if (h_accepted) *h_accepted = c->n_identity ? 0 : 1;
   return check_cuda(c, "psp_set_bands");
+}
+
+// AC10: zero the given local rows of the current N (all 2d+1 bands), then re-install it
+// through the gate and the factorisation, exactly as psp_set_bands: a gated N with a zero row is
+// rejected (R21), an ungated one fails the factorisation (zero pivot) -- either way the
+// identity fallback takes over and the next solve runs with N = I.
+psp_status psp_inject_fault_rows(psp_ctx* c, const int64_t* h_rows, int count, int* h_accepted) {
+  if (!c || (count > 0 && !h_rows)) return fail(c, PSP_E_ARG, "psp_inject_fault_rows: bad argument");
+  if (c->sticky != PSP_OK) return c->sticky;
+  for (int q = 0; q < count; ++q) {
+    if (h_rows[q] < 0 || h_rows[q] >= c->n) return fail(c, PSP_E_DIM, "psp_inject_fault_rows: row out of range");
+    for (int o = 0; o <= 2 * c->d; ++o)
+      cudaMemsetAsync(c->bands + (int64_t)o * c->n + h_rows[q], 0, sizeof(double), c->stream);
+  }
+  return psp_set_bands(c, c->bands, h_accepted);
 }
 
 psp_status psp_get_bands(const psp_ctx* c, double* d_out, int* h_ident) {

@@ -122,6 +122,7 @@ def lib():
         "psp_banded_solve_raw": (C.c_int, [_vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
         "psp_set_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
         "psp_get_bands": (C.c_int, [_vp, _vp, P(C.c_int)]),
+        "psp_inject_fault_rows": (C.c_int, [_vp, P(C.c_int64), C.c_int, P(C.c_int)]),
         "psp_ring_view": (C.c_int, [_vp, P(C.c_int), P(C.c_int32), _dp, P(_vp), P(_vp), P(C.c_int64)]),
         "psp_ring_reset": (C.c_int, [_vp]),
         "psp_get_hessenberg": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),
@@ -151,7 +152,8 @@ def lib():
 EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destroy", "psp_local_rows",
             "psp_matvec", "psp_precond_apply", "psp_cycle_begin", "psp_arnoldi_step", "psp_cycle_end",
             "psp_solve", "psp_mrep_fit", "psp_step", "psp_raw_scratch_bytes", "psp_mrep_fit_raw",
-            "psp_banded_factor_raw", "psp_banded_solve_raw", "psp_set_bands", "psp_get_bands", "psp_ring_view",
+            "psp_banded_factor_raw", "psp_banded_solve_raw", "psp_set_bands", "psp_get_bands", "psp_inject_fault_rows",
+            "psp_ring_view",
             "psp_ring_reset", "psp_get_hessenberg", "psp_get_basis", "psp_launch_count", "psp_kernel_stats",
             "psp_kernel_class_name", "psp_status_str",
             "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_loopback_create",
@@ -411,6 +413,12 @@ class Context:
     def psp_set_bands(self, bands):
         acc = C.c_int()
         _check(lib().psp_set_bands(self.h, _ptr(bands), C.byref(acc)), self.h)
+        return bool(acc.value)
+
+    def psp_inject_fault_rows(self, rows):
+        arr = (C.c_int64 * len(rows))(*[int(r) for r in rows])
+        acc = C.c_int()
+        _check(lib().psp_inject_fault_rows(self.h, arr, len(rows), C.byref(acc)), self.h)
         return bool(acc.value)
 
     def psp_get_bands(self):

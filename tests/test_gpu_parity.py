@@ -563,3 +563,31 @@ def test_paper_experiment_f1(torch, P, orc, n):
         assert (o2 is None) == (g2 is None)
         if isinstance(o2, int) and isinstance(g2, int):
             assert abs(g2 - o2) <= 1, (gate, g2, o2)
+
+
+@pytest.mark.parametrize("gate", [1, 0], ids=["gated", "ungated"])
+def test_fault_injection_identity_fallback(torch, P, orc, gate):
+    """SPEC AC10: rows of the installed N zeroed by the fault hook -> the gate rejects it
+    (or, ungated, the factorisation meets a zero pivot) -> N := I, and the next
+    solve still converges (true residual <= eps); 10 seeds of the paper's seven-diagonal family at
+    n = 80 (P:142)."""
+    for seed in range(10):
+        op, b = inputs.seven_diagonal(80, seed=seed)
+        opts = P.default_opts(max_cycles=1000, m_max=64, tol_mode=P.PSP_TOL_ABS, gate=gate)
+        ctx = P.Context(op, d=1, restart=10, tol=1e-8, opts=opts)
+        bt = dev(torch, b)
+        x = torch.zeros_like(bt)
+        r1 = ctx.psp_solve(bt, torch.zeros_like(bt), x)
+        assert r1["converged"] == 1
+        ctx.psp_mrep_fit()
+        rng = np.random.default_rng(seed)
+        acc = ctx.psp_inject_fault_rows(list(rng.choice(np.arange(2, 78), 3, replace=False)))
+        assert not acc
+        bands, ident = ctx.psp_get_bands()
+        assert ident
+        r2 = ctx.psp_solve(bt, torch.zeros_like(bt), x)
+        assert r2["converged"] == 1 and r2["precond_identity"] == 1
+        assert r2["final_resid_true"] <= 1e-8
+        ref = np.linalg.solve(dense(orc, op), b)
+        assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-6 * np.linalg.norm(ref)
+        ctx.close()
