@@ -16,6 +16,7 @@
 // shared-memory tile) + 8(2d+1) bytes of bands written.  Blocks of 256 threads own 256 rows of
 // sums and emit 256-2d rows (the 2d halo rows are recomputed by the neighbour block).
 #include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -556,6 +557,188 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
   if (!SUMS) merge_stats(gs, red, sc.result);
 }
 
+// ------------------------------------------------------------------------------------------
+// Warp-specialised MREP (d >= 2): the streaming and the fitting run in the same persistent CTA on
+// different warps.  Warps 0-3 (the sum group, thread t = sum row t of a 128-row tile) consume
+// the TMA stage ring exactly as mrep_tma_kernel and, at the end of a tile, hand its 4d+4 lagged
+// sums per row to a double-buffered shared-memory exchange (mbarriers ex_full / ex_empty) and go
+// straight on with the next tile's columns; warps 4-7 (the fit group, thread f = emitted row
+// f + d) assemble each row's Gram from the exchange and solve it (fit_row: Cholesky, R17 ridge
+// retry, R14 install) while the next tile streams.  The lagged sums never leave the SM: HBM sees
+// only the probes and the bands (568 B a row at m = 32, d = 3).  One CTA per SM (the fit's
+// register budget sets the occupancy; the TMA ring, not the warp count, keeps the bytes in
+// flight).
+// ------------------------------------------------------------------------------------------
+#ifndef PSP_MREP_WS_NST
+#define PSP_MREP_WS_NST 6     // TMA stages of the warp-specialised kernel (more bytes in flight)
+#endif
+constexpr int WNST = PSP_MREP_WS_NST;
+
+template <int D>
+struct WsCfg {
+  static constexpr int STAGE = TmaCfg<D>::STAGE;
+  static constexpr int EXR = 4 * D + 4;                                  // exchange rows (sums)
+  static constexpr size_t SMEM = (size_t)WNST * STAGE * 8 + (size_t)2 * EXR * TT * 8 + 16 * WNST + 64;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(2 * TT, 1) mrep_ws_kernel(TmaCols cols, const double* __restrict__ scale, int m,
+                                                           int64_t n, int64_t gN, int64_t grow0, int64_t R0,
+                                                           int64_t ntile, MrepOut out, MrepScratch sc) {
+  using Cfg = WsCfg<D>;
+  constexpr int E = TT - 2 * D;                    // rows emitted per tile
+  constexpr int LX = ((TT + 3 * D) + 1) & ~1;
+  constexpr int LX1 = ((TT + 3 * D + 1) + 1) & ~1;
+  constexpr int LY = TT, LY1 = TT + 2;
+  constexpr int EXR = Cfg::EXR;
+  extern __shared__ __align__(16) double sm[];
+  double* stages = sm;                             // [WNST][TCB x PXW | TCB x PYW]
+  double* exb = sm + WNST * TmaCfg<D>::STAGE;      // [2][EXR][TT]: C_0..C_2D, S, D_0..D_2D, T
+  uint64_t* bars = reinterpret_cast<uint64_t*>(exb + 2 * EXR * TT);
+  uint64_t* ex_full = bars + WNST;
+  uint64_t* ex_empty = ex_full + 2;
+  __shared__ double scs[kMaxM];
+  __shared__ double scs2[kMaxM];
+  __shared__ double red[2 * TT / 32 * 6];
+  __shared__ int s_unit;
+  const int t = threadIdx.x;
+  const bool sums = t < TT;
+  if (t == 0) s_unit = 1;
+  __syncthreads();
+  for (int c = t; c < m; c += 2 * TT) {
+    scs[c] = scale ? scale[cols.slot[c]] : 1.0;
+    scs2[c] = scs[c] * scs[c];
+    if (scs[c] != 1.0) s_unit = 0;
+  }
+  if (t == 0) {
+    for (int q = 0; q < WNST; ++q) mbar_init(bars + q, 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(ex_full + q, TT);
+      mbar_init(ex_empty + q, TT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const bool unit = s_unit != 0;
+  const int nch = (m + TCB - 1) / TCB;
+  const int my_tiles = (int)((ntile - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  GateStats gs;
+  if (sums) {
+    // ---- the sum group: TMA issue (thread 0) + lagged sums, as mrep_tma_kernel ----
+    const int lx = cols.sx ? LX1 : LX, ly = cols.sy ? LY1 : LY;
+    const int total = my_tiles * nch;
+    int is_tq = 0, is_ch = 0, is_stg = 0;
+    auto issue_next = [&]() {
+      const int64_t tile = blockIdx.x + (int64_t)is_tq * gridDim.x;
+      double* st = stages + (size_t)is_stg * TmaCfg<D>::STAGE;
+      const int64_t s0 = R0 + tile * E - D;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int ncols = (m - is_ch * TCB) < TCB ? (m - is_ch * TCB) : TCB;
+      mbar_expect_tx(bars + is_stg, 8u * (unsigned)(ncols * (lx + ly)));
+#pragma unroll
+      for (int cc = 0; cc < TCB; ++cc) {
+        const int c = is_ch * TCB + cc;
+        if (c >= m) break;
+        const double* bxp = cols.px + (int64_t)cols.slot[c] * cols.ld;
+        const double* byp = cols.py + (int64_t)cols.slot[c] * cols.ld;
+        bulk_g2s(st + cc * TmaCfg<D>::PXW, bxp + (s0 - D - cols.sx), 8u * lx, bars + is_stg);
+        bulk_g2s(st + TCB * TmaCfg<D>::PXW + cc * TmaCfg<D>::PYW, byp + (s0 - cols.sy), 8u * ly, bars + is_stg);
+      }
+      if (++is_ch == nch) { is_ch = 0; ++is_tq; }
+      if (++is_stg == WNST) is_stg = 0;
+    };
+    if (t == 0)
+      for (int q = 0; q < total && q < WNST; ++q) issue_next();
+    double Cl[2 * D + 1], Dl[2 * D + 1], Ssum = 0.0, Tsum = 0.0;
+    const int xo = cols.sx + t, yo = cols.sy + t;
+    int stg = 0, ch = 0, tq = 0;
+    unsigned phase = 0;
+    for (int q = 0; q < total; ++q) {
+      if (ch == 0) {
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) { Cl[l] = 0.0; Dl[l] = 0.0; }
+        Ssum = Tsum = 0.0;
+      }
+      mbar_wait(bars + stg, (phase >> stg) & 1u);
+      phase ^= 1u << stg;
+      const double* st = stages + (size_t)stg * TmaCfg<D>::STAGE;
+      const int ccn = (m - ch * TCB) < TCB ? (m - ch * TCB) : TCB;
+      const int c0 = ch * TCB;
+#pragma unroll
+      for (int cc = 0; cc < TCB; ++cc) {
+        if (cc >= ccn) break;
+        const double* xr = st + cc * TmaCfg<D>::PXW + xo;
+        double xw[3 * D + 1];
+#pragma unroll
+        for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
+        const double yr = st[TCB * TmaCfg<D>::PXW + cc * TmaCfg<D>::PYW + yo];
+        const double x0 = xw[D];
+        if (unit) {
+          Ssum += x0;
+          Tsum += yr;
+#pragma unroll
+          for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(x0, xw[D + l], Cl[l]);
+#pragma unroll
+          for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], yr, Dl[l]);
+        } else {
+          const double scv = scs[c0 + cc], s2 = scs2[c0 + cc];
+          Ssum = fma(scv, x0, Ssum);
+          Tsum = fma(scv, yr, Tsum);
+          const double ax = s2 * x0, by = s2 * yr;
+#pragma unroll
+          for (int l = 0; l <= 2 * D; ++l) Cl[l] = fma(ax, xw[D + l], Cl[l]);
+#pragma unroll
+          for (int l = 0; l <= 2 * D; ++l) Dl[l] = fma(xw[l], by, Dl[l]);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(TT) : "memory");   // the sum group is done with stage stg
+      if (t == 0 && q + WNST < total) issue_next();
+      if (++stg == WNST) stg = 0;
+      if (ch == nch - 1) {
+        // hand the tile's sums to the fit group (buffer tq & 1, its (tq >> 1)-th use)
+        const int b = tq & 1;
+        mbar_wait(ex_empty + b, ((tq >> 1) & 1u) ^ 1u);
+        double* ex = exb + (size_t)b * EXR * TT;
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) ex[l * TT + t] = Cl[l];
+        ex[(2 * D + 1) * TT + t] = Ssum;
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) ex[(2 * D + 2 + l) * TT + t] = Dl[l];
+        ex[(4 * D + 3) * TT + t] = Tsum;
+        mbar_arrive(ex_full + b);
+        ch = 0;
+        ++tq;
+      } else {
+        ++ch;
+      }
+    }
+  } else {
+    // ---- the fit group: one thread per emitted row of the tile handed over ----
+    const int f = t - TT;
+    for (int tq = 0; tq < my_tiles; ++tq) {
+      const int b = tq & 1;
+      mbar_wait(ex_full + b, (tq >> 1) & 1u);
+      const double* ex = exb + (size_t)b * EXR * TT;
+      const int64_t tile = blockIdx.x + (int64_t)tq * gridDim.x;
+      const int tr = f + D;                        // this thread's row in the tile
+      if (f < E) {
+        const int64_t r = R0 + tile * E - D + tr;
+        double Dl[2 * D + 1];
+#pragma unroll
+        for (int l = 0; l <= 2 * D; ++l) Dl[l] = ex[(2 * D + 2 + l) * TT + tr];
+        const double Tsum = ex[(4 * D + 3) * TT + tr];
+        fit_row<D>(ex, TT, tr, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+      }
+      mbar_arrive(ex_empty + b);
+    }
+  }
+  merge_stats(gs, red, sc.result);
+}
+
 // The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
 // lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
 template <int D>
@@ -589,6 +772,17 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
   }
   const int sms = device_sms();
   const int64_t E = TT - 2 * D;
+  if (D >= 2 && !getenv("PSP_MREP_SPLIT")) {
+    // the warp-specialised fused kernel: sums and fits on different warps of one persistent CTA
+    thread_local bool wattr[kMaxDev] = {};
+    if (!wattr[dev]) {
+      cudaFuncSetAttribute(mrep_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsCfg<D>::SMEM);
+      wattr[dev] = true;
+    }
+    const int64_t g = ntile < sms ? ntile : sms;
+    mrep_ws_kernel<D><<<(unsigned)g, 2 * TT, WsCfg<D>::SMEM, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
+    return;
+  }
   if (sc.sums != nullptr && sc.sums_n >= n && D >= 2) {
     // split: stream + lagged sums, then the fits.  d <= 3: the rows go in PSP_MREP_CHUNKS
     // chunks and the fits of chunk c run on a second stream beside the sums of chunk c+1 (the
