@@ -341,14 +341,16 @@ __device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], dou
 // chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
 
 // One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
-//                        BWD: z = (v - sum_k c[k] s[k]) / u0 (c[k] = U(i,i+k+1), s[k] = z_{i+k+1})
+//                        BWD: z = (v - sum_k c[k] s[k]) / U(i,i) (c[k] = U(i,i+k+1), s[k] = z_{i+k+1}),
+// evaluated with ui = 1 / U(i,i) formed once per row (the D unit-state runs of a tile map share
+// it; one rounding more than a division, inside T2)
 template <bool FWD, int D>
 __device__ __forceinline__ double rec_step(double v, const double (&c)[D], const double (&s)[D],
-                                           double u0) {
+                                           double ui) {
   double acc = v;
 #pragma unroll
   for (int k = 0; k < D; ++k) acc -= c[k] * s[k];
-  return FWD ? acc : acc / u0;
+  return FWD ? acc : acc * ui;
 }
 
 template <int D>
@@ -396,7 +398,7 @@ __device__ __forceinline__ void stage_tile(double* sv, const double* __restrict_
     sv[sidx] = vsc * r[it][0];
 #pragma unroll
     for (int k = 0; k < D; ++k) sc0[k * SW<D>::TPB * SPAD + sidx] = r[it][1 + k];
-    if (!FWD) su0[sidx] = r[it][1 + D];
+    if (!FWD) su0[sidx] = 1.0 / r[it][1 + D];   // the reciprocal pivot (padding rows: 1)
   }
 }
 
@@ -605,7 +607,7 @@ __global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_
         const int o = FWD ? (D - 1 - k) : (D + 1 + k);
         c8[e][k] = ok ? __ldg(lu + (int64_t)o * n + idx[e]) : 0.0;
       }
-      u8[e] = (!FWD && ok) ? __ldg(lu + (int64_t)D * n + idx[e]) : 1.0;
+      u8[e] = (!FWD && ok) ? 1.0 / __ldg(lu + (int64_t)D * n + idx[e]) : 1.0;   // reciprocal pivot
       o8[e] = ok ? out[idx[e]] : 0.0;
     }
 #pragma unroll

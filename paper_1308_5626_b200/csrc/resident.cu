@@ -117,12 +117,11 @@ __device__ __forceinline__ double ldm(const double* p) { return M == 2 ? *p : __
 // not inlined: the kernel evaluates rows in unrolled per-thread loops, and nine inlined stencil
 // variants per row would make the kernel megabytes of code (instruction-fetch bound)
 template <int M>
-__device__ __noinline__ double arow(const Stencil& st, const double* x, int64_t g, double& xc) {
+__device__ __noinline__ double arow(const Stencil& st, const double* x, int64_t g, int i, int j, int k, double& xc) {
   if (st.kind == PSP_OP_DIA) {
     xc = ldm<M>(x + g);
     return dia_row<M>(st, x, g);
   }
-  const int64_t i = g % st.nx, j = (g / st.nx) % st.ny, k = g / (st.nx * st.ny);
   switch (st.kind * 4 + st.ndim) {
     case PSP_OP_CONST_DIFF * 4 + 1: return stencil_row<PSP_OP_CONST_DIFF, 1, M>(st, x, i, j, k, g, xc);
     case PSP_OP_CONST_DIFF * 4 + 2: return stencil_row<PSP_OP_CONST_DIFF, 2, M>(st, x, i, j, k, g, xc);
@@ -234,7 +233,7 @@ __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, doub
   __syncthreads();
 }
 
-template <int M>
+template <int M, int R>
 __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nA = a.nA, ld = nA + 1, PV = 2 * nA + 2;
@@ -323,8 +322,21 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     __syncthreads();
   };
 
-  // this thread's rows: r0 + t + q RT, q < RMAX
-  double w[RMAX];
+  // this thread's rows: r0 + t + q RT, q < R; with few rows a thread their grid coordinates are
+  // kept (no integer divisions in the step), else recomputed per use (registers)
+  double w[R];
+  constexpr bool PRE = R <= 2;
+  int ci0[PRE ? R : 1], cj0[PRE ? R : 1], ck0[PRE ? R : 1];
+#pragma unroll
+  for (int q = 0; q < (PRE ? R : 1); ++q) {
+    const int64_t g = r0 + t + (int64_t)q * RT;
+    ci0[q] = (int)(g % a.st.nx);
+    cj0[q] = (int)((g / a.st.nx) % a.st.ny);
+    ck0[q] = (int)(g / (a.st.nx * a.st.ny));
+  }
+  auto ci = [&](int q) { return PRE ? ci0[q] : (int)((r0 + t + (int64_t)q * RT) % a.st.nx); };
+  auto cj = [&](int q) { return PRE ? cj0[q] : (int)(((r0 + t + (int64_t)q * RT) / a.st.nx) % a.st.ny); };
+  auto ck = [&](int q) { return PRE ? ck0[q] : (int)((r0 + t + (int64_t)q * RT) / (a.st.nx * a.st.ny)); };
   int iters = 0, cycles = 0, matvecs = 0, papply = 0, hlen = 0, blen = 0, status = 0;
   bool finish = false;
   double r0v = 0.0, est = 0.0, eps;
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     grid_reduce(1, [&](int) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
+      for (int q = 0; q < R; ++q) {
         const int64_t g = r0 + t + (int64_t)q * RT;
         if (g < r1) { const double bv = __ldg(a.b + g); s = fma(bv, bv, s); }
       }
@@ -352,12 +364,12 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     double* py = a.ring_py + (int64_t)slot * n;
     if (lead) a.slot_scale[slot] = 1.0;
 #pragma unroll
-    for (int q = 0; q < RMAX; ++q) {
+    for (int q = 0; q < R; ++q) {
       const int64_t g = r0 + t + (int64_t)q * RT;
       w[q] = 0.0;
       if (g < r1) {
         double xc;
-        const double y = arow<M>(a.st, a.X0, g, xc);
+        const double y = arow<M>(a.st, a.X0, g, ci(q), cj(q), ck(q), xc);
         px[g] = xc;
         py[g] = y;
         const double rr = __ldg(a.b + g) - y;
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     grid_reduce(1, [&](int) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < RMAX; ++q) s = fma(w[q], w[q], s);
+      for (int q = 0; q < R; ++q) s = fma(w[q], w[q], s);
       return s;
     });
     const double beta = sqrt(tot[0]);
@@ -403,19 +415,19 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         }
         papply += 1;
       }
-      double vk[RMAX];
+      double vk[R];
 #pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
+      for (int q = 0; q < R; ++q) {
         const int64_t g = r0 + t + (int64_t)q * RT;
         w[q] = 0.0;
         vk[q] = 0.0;
         if (g < r1) {
           double xc;
           if (seqN) {
-            w[q] = arow<M>(a.st, px, g, xc);
+            w[q] = arow<M>(a.st, px, g, ci(q), cj(q), ck(q), xc);
             vk[q] = ldm<M>(Vk + g);
           } else {                                     // N = I: Y_k = alpha_k V(:,k)
-            const double y = arow<M>(a.st, Vk, g, xc);
+            const double y = arow<M>(a.st, Vk, g, ci(q), cj(q), ck(q), xc);
             vk[q] = xc;
             w[q] = ak * y;
             px[g] = ak * xc;
@@ -431,7 +443,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         const double* Vj = V(j);
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < RMAX; ++q) {
+        for (int q = 0; q < R; ++q) {
           const int64_t g = r0 + t + (int64_t)q * RT;
           if (g < r1) s = fma(ldm<M>(Vj + g), isl ? vk[q] : w[q], s);
         }
@@ -457,7 +469,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         const double* Hc = H + (int64_t)(k - 1) * ld;
         double* Vn = V(k);
 #pragma unroll
-        for (int q = 0; q < RMAX; ++q) {
+        for (int q = 0; q < R; ++q) {
           const int64_t g = r0 + t + (int64_t)q * RT;
           if (g < r1) {
             double u = w[q];
@@ -472,7 +484,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       grid_reduce(1, [&](int) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < RMAX; ++q) s = fma(w[q], w[q], s);
+        for (int q = 0; q < R; ++q) s = fma(w[q], w[q], s);
         return s;
       });
       if (t == 0) {
@@ -507,7 +519,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     if (sc[SC_STATUS] != 0.0) { status = PSP_E_SINGULAR; break; }
     double* zdst = seqN ? a.z : a.X0;
 #pragma unroll
-    for (int q = 0; q < RMAX; ++q) {
+    for (int q = 0; q < R; ++q) {
       const int64_t g = r0 + t + (int64_t)q * RT;
       if (g < r1) {
         double zz = seqN ? 0.0 : ldm<M>(a.X0 + g);
@@ -536,11 +548,11 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     grid_reduce(1, [&](int) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
+      for (int q = 0; q < R; ++q) {
         const int64_t g = r0 + t + (int64_t)q * RT;
         if (g < r1) {
           double xc;
-          const double rr = __ldg(a.b + g) - arow<M>(a.st, a.X0, g, xc);
+          const double rr = __ldg(a.b + g) - arow<M>(a.st, a.X0, g, ci(q), cj(q), ck(q), xc);
           s = fma(rr, rr, s);
         }
       }
@@ -636,18 +648,21 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   const int dev = device_ordinal();
   thread_local size_t attr[kMaxDev] = {};
   if (attr[dev] < smem) {
-    if (cudaFuncSetAttribute(resident_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(resident_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(resident_kernel<1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(resident_kernel<2, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(resident_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 1;
     attr[dev] = smem;
   }
   cudaMemsetAsync(c.bar, 0, sizeof(unsigned long long), s);
   void* args[] = {&a};
   if (grid > 1) {
-    if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
+    if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1, RMAX>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
       return 1;
+  } else if (c.st.n <= 2 * RT) {
+    resident_kernel<2, 2><<<1, RT, smem, s>>>(a);   // one CTA, two rows a thread (C1)
   } else {
-    resident_kernel<2><<<1, RT, smem, s>>>(a);   // one CTA: L1-cached loads, no grid barrier
+    resident_kernel<2, RMAX><<<1, RT, smem, s>>>(a);   // one CTA: L1-cached loads, no grid barrier
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

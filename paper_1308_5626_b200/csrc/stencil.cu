@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(32 * BY, (BY > 1 ? PSP_MARCH_MINB : 16)) march
 // cost of loop control, address arithmetic and the y-neighbour loads halves against
 // march3_kernel; z neighbours in a register queue prefetched two planes ahead.  Needs nx % 4 == 0
 // and 16-byte aligned vectors.
-template <int KIND, int BY>
-__global__ void __launch_bounds__(32 * BY, 2) march4_kernel(MarchView v, const double* __restrict__ x,
+template <int KIND, int BY, int MINB = 2>
+__global__ void __launch_bounds__(32 * BY, MINB) march4_kernel(MarchView v, const double* __restrict__ x,
                                                            const double* xsp, double* __restrict__ y,
                                                            double* __restrict__ xcopy) {
   constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
@@ -604,7 +604,10 @@ void launch_march4(const MarchView& v0, const double* x, const double* xs, doubl
   const int64_t zc = planes_per_block(((v.nx + 127) / 128) * ((v.ny + BY - 1) / BY), v.nz);
   v.zc = (int)zc;
   dim3 grid((unsigned)((v.nx + 127) / 128), (unsigned)((v.ny + BY - 1) / BY), (unsigned)((v.nz + zc - 1) / zc));
-  march4_kernel<KIND, BY><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
+  // PSP_MARCH4_MINB=3: the 3-blocks-per-SM build of the kernel (85 registers; A/B knob)
+  static const int minb = getenv("PSP_MARCH4_MINB") ? atoi(getenv("PSP_MARCH4_MINB")) : 2;
+  if (minb >= 3) march4_kernel<KIND, BY, 3><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
+  else march4_kernel<KIND, BY><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
 }
 
 template <int KIND, int BY>
