@@ -566,8 +566,12 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
 // f + d) assemble each row's Gram from the exchange and solve it (fit_row: Cholesky, R17 ridge
 // retry, R14 install) while the next tile streams.  The lagged sums never leave the SM: HBM sees
 // only the probes and the bands (568 B a row at m = 32, d = 3).  One CTA per SM (the fit's
-// register budget sets the occupancy; the TMA ring, not the warp count, keeps the bytes in
-// flight).
+// register budget sets the occupancy).  MEASURED AND NOT THE DEFAULT (PSP_MREP_WS=1 selects
+// it): with one warp per scheduler the sum group cannot hide the FP64 / shared-memory latency of
+// the lagged sums, so the stream stalls (n = 2^27, m = 32, d = 3: 45.4 ms against the split
+// path's 26.7 ms; d = 2 at 2^26: 20.6 against 8.8 ms; r02d).  Giving the sum group more warps
+// needs a register split between the groups (setmaxnreg) that the fit's ~220 registers a
+// thread leave no room for.
 // ------------------------------------------------------------------------------------------
 #ifndef PSP_MREP_WS_NST
 #define PSP_MREP_WS_NST 6     // TMA stages of the warp-specialised kernel (more bytes in flight)
@@ -772,8 +776,10 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
   }
   const int sms = device_sms();
   const int64_t E = TT - 2 * D;
-  if (D >= 2 && !getenv("PSP_MREP_SPLIT")) {
-    // the warp-specialised fused kernel: sums and fits on different warps of one persistent CTA
+  if (D >= 2 && getenv("PSP_MREP_WS")) {
+    // the warp-specialised fused kernel (measured and not the default: at one CTA a SM the four
+    // sum warps cannot hide the FP64 latency of the lagged sums -- n = 2^27, m = 32, d = 3:
+    // 45.4 ms against the split path's 26.7 ms, r02d)
     thread_local bool wattr[kMaxDev] = {};
     if (!wattr[dev]) {
       cudaFuncSetAttribute(mrep_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WsCfg<D>::SMEM);

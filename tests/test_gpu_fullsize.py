@@ -215,11 +215,19 @@ def _lockstep_c4(torch, P, orc, size, max_cycles, with_mrep):
         ex = compare_mrep(g, r, prob.d, n, px, max_excluded_frac=MREP_EXCLUDED_MAX)
         log_parity(case=f"C4-{size}-full", step=0, mrep_excluded=int(ex), rows=n)
         bands, _ = ctx.psp_get_bands()
-        # psp_mrep_fit (scaled ring columns) and psp_mrep_fit_raw (the same columns, scaled by
-        # torch) agree to the rounding of the scale product
+        # psp_mrep_fit (the scaled ring columns: the scale enters the lagged sums as s^2 on one
+        # factor) and psp_mrep_fit_raw (the same columns scaled by torch) are two evaluations of
+        # the same normal equations: on the unridged rows each is within T3 of the exact
+        # solution, so they agree within twice T3
+        from test_gpu_parity import gram_cond2
         bb = bands.cpu().numpy()
         gb = g["bands"].cpu().numpy()
-        assert np.max(np.abs(bb - gb) / np.maximum(np.abs(gb).max(axis=0), 1e-300)) <= 1e-6
+        k2 = gram_cond2(px, prob.d)
+        P_ = 2 * prob.d + 2
+        tol = np.maximum(np.where(k2 <= 1e5, 1e-10, 8 * P_ * 2.0 ** -53 * np.where(np.isfinite(k2), k2, 1e300)), 1e-10)
+        ok = g["row_kind"].cpu().numpy() == P.ROW_INTERIOR
+        err = np.abs(bb - gb).max(axis=0) / np.maximum(np.abs(gb).max(axis=0), 1e-300)
+        assert np.all(err[ok] <= 2 * tol[ok]), np.max(err[ok] / tol[ok])
         assert bool(rep["mrep_gate_accepted"]) == r["gate_accepted"]
     ctx.close()
     del ctx, bt, x

@@ -204,16 +204,18 @@ def test_fused_ring_on_slabs(torch, P, orc, mode, nranks, case):
     kw = FUSED_MODES[mode]
     m = multi_steps(torch, P, prob, nranks, 2, kw)
     s = single_steps(torch, P, prob, 2, kw)
-    for rm, rs in zip(m["reps"], s["reps"]):
+    for st, (rm, rs) in enumerate(zip(m["reps"], s["reps"])):
         assert abs(rm["iterations"] - rs["iterations"]) <= 1
+        assert rm["final_resid_true"] <= 1.05 * rm["eps"]
+        assert bool(rm["mrep_gate_accepted"]) == bool(rs["mrep_gate_accepted"])
+        if st > 0:      # later steps start from slightly different u (T5 only, as free-running parity)
+            continue
         L = min(rm["resid_len"], rs["resid_len"], prob.restart)
         beta = rs["beta_history"][0]
         dR = np.abs(rm["resid_history"][:L] - rs["resid_history"][:L])
-        q = dR / (1e-8 * rs["resid_history"][:L] + 1e-11 * beta)
+        q = dR / (1e-8 * rs["resid_history"][:L] + 1e-11 * beta)           # T4, the first cycle
         w = int(np.argmax(q))
         assert np.all(q <= 1), (w, q[w], rm["resid_history"][max(0, w - 2):w + 3], rs["resid_history"][max(0, w - 2):w + 3])
-        assert rm["final_resid_true"] <= 1.05 * rm["eps"]
-        assert bool(rm["mrep_gate_accepted"]) == bool(rs["mrep_gate_accepted"])
     for p in m["parts"][1:]:
         assert [r["iterations"] for r in p["reps"]] == [r["iterations"] for r in m["reps"]]
     r = orc.time_steps(prob.op, prob.u0, 2, prob.restart, prob.max_cycles, prob.tol, prob.d, prob.m_max)
