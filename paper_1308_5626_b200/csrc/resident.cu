@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
   // deterministic grid sum of nv per-thread values given by f(j, q) summed over this thread's
   // rows: block butterflies -> red -> this CTA's tot -> partials -> every CTA sums the grid's
   // partials in CTA order -> tot (valid in every thread after the call)
-  auto grid_reduce = [&](int nv, auto&& f) {
+  // w0 (one CTA): the totals are formed by warp 0 and valid only there (its caller consumes
+  // them in warp 0 and meets the block at its own barrier) -- one __syncthreads fewer
+  auto grid_reduce = [&](int nv, auto&& f, bool w0 = false) {
     for (int j0 = 0; j0 < nv; j0 += 8) {
       double v[8];
 #pragma unroll
@@ -290,6 +292,17 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       if (lane < 8 && j0 + lane < nv) red[warp * PV + j0 + lane] = r;
     }
     __syncthreads();
+    if (w0 && gridDim.x == 1) {
+      if (warp == 0) {
+        for (int j = lane; j < nv; j += 32) {
+          double s = 0.0;
+          for (int w = 0; w < RW; ++w) s += red[w * PV + j];
+          tot[j] = s;
+        }
+        __syncwarp();
+      }
+      return;
+    }
     for (int j = t; j < nv; j += RT) {
       double s = 0.0;
       for (int w = 0; w < RW; ++w) s += red[w * PV + j];
@@ -437,7 +450,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       }
       matvecs += 1;
       // s_j = V_j' w (j < k) at [0, k), l_j = V_j' V_k (j < k-1) at [k, 2k-1) (EPI_DOTS layout)
-      grid_reduce(2 * k - 1, [&](int v) {
+      grid_reduce(2 * k - 1, [&](int v) -> double {
         const bool isl = v >= k;
         const int j = isl ? v - k : v;
         const double* Vj = V(j);
@@ -448,20 +461,21 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
           if (g < r1) s = fma(ldm<M>(Vj + g), isl ? vk[q] : w[q], s);
         }
         return s;
-      });
-      if (warp == 0) {                                 // (I + L) h = s (R11), as EPI_DOTS: warp 0,
-        double* Lrow = Lm + (int64_t)(k - 1) * ld;     // the sum over c split across the lanes
-        for (int jb = lane; jb < k - 1; jb += 32) Lrow[jb] = al[jb] * ak * tot[k + jb];
+      }, true);
+      if (warp == 0) {                                 // (I + L) h = s (R11), as EPI_DOTS, by warp 0:
+        double* Lrow = Lm + (int64_t)(k - 1) * ld;     // right-looking -- lane i holds s_i (and
+        for (int jb = lane; jb < k - 1; jb += 32) Lrow[jb] = al[jb] * ak * tot[k + jb];   // s_{i+32})
         __syncwarp();
-        double* Hc = H + (int64_t)(k - 1) * ld;
-        for (int jb = 0; jb < k; ++jb) {
-          const double* Lr = Lm + (int64_t)jb * ld;
-          double part = 0.0;
-          for (int c = lane; c < jb; c += 32) part = fma(Lr[c], Hc[c], part);
-          part = warp_sum(part);
-          if (lane == 0) Hc[jb] = al[jb] * tot[jb] - part;
-          __syncwarp();
+        double s0 = lane < k ? al[lane] * tot[lane] : 0.0;
+        double s1 = lane + 32 < k ? al[lane + 32] * tot[lane + 32] : 0.0;
+        for (int jb = 0; jb < k; ++jb) {               // h_jb final: broadcast, update the rest
+          const double hj = __shfl_sync(0xffffffffu, jb < 32 ? s0 : s1, jb & 31);
+          if (lane > jb && lane < k) s0 = fma(-Lm[(int64_t)lane * ld + jb], hj, s0);
+          if (lane + 32 > jb && lane + 32 < k) s1 = fma(-Lm[(int64_t)(lane + 32) * ld + jb], hj, s1);
         }
+        double* Hc = H + (int64_t)(k - 1) * ld;
+        if (lane < k) Hc[lane] = s0;
+        if (lane + 32 < k) Hc[lane + 32] = s1;
       }
       __syncthreads();
       // ---- [B] l.13-17: U = w - sum_j h_j alpha_j V_j -> V(:,k+1); H(k+1,k) = ||U|| ----
@@ -486,7 +500,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
 #pragma unroll
         for (int q = 0; q < R; ++q) s = fma(w[q], w[q], s);
         return s;
-      });
+      }, true);
       if (t == 0) {
         H[(int64_t)(k - 1) * ld + k] = sqrt(tot[0]);  // l.17
         givens_update(S, k, nA);                      // l.18-32 (R4 breakdown, R10)
