@@ -419,7 +419,6 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
   double* ex = sm + TNST * Cfg::STAGE;             // [(2D+2)][TT]: C_l, S of the tile's rows
   uint64_t* bars = reinterpret_cast<uint64_t*>(ex + (SUMS ? 0 : (2 * D + 2) * TT));
   __shared__ double scs[kMaxM];                    // per-column probe scale
-  __shared__ double scs2[kMaxM];                   //   and its square
   __shared__ double red[TT / 32 * 6];
   __shared__ int s_unit;
   const int t = threadIdx.x;
@@ -427,7 +426,6 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
   __syncthreads();
   for (int c = t; c < m; c += TT) {
     scs[c] = scale ? scale[cols.slot[c]] : 1.0;
-    scs2[c] = scs[c] * scs[c];
     if (scs[c] != 1.0) s_unit = 0;
   }
   if (t == 0) {
@@ -505,8 +503,8 @@ __global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(
 #pragma unroll
       for (int cc = 0; cc < TCB; ++cc) {
         if (cc >= ccn) break;                      // uniform
-        const double sc = scs[c0 + cc], s2 = scs2[c0 + cc];
-        const double* xr = st + cc * Cfg::PXW + xo;
+        const double sc = scs[c0 + cc], s2 = sc * sc;   // (no s^2 table: its 2 KB of shared memory
+        const double* xr = st + cc * Cfg::PXW + xo;      //  cost a resident block per SM)
         double xw[3 * D + 1];
 #pragma unroll
         for (int k = 0; k < 3 * D + 1; ++k) xw[k] = xr[k];
@@ -830,7 +828,16 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
     cudaEventRecord(ev[K], s2);
     cudaStreamWaitEvent(s, ev[K], 0);
   } else {
-    mrep_tma_kernel<D, false><<<nb, TT, smem, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
+    // one full wave at the kernel's occupancy (a partial second wave of a persistent grid leaves
+    // SMs idle for a third of the launch)
+    thread_local int occn[kMaxDev] = {};
+    if (!occn[dev]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occn[dev], mrep_tma_kernel<D, false>, TT, smem);
+      if (occn[dev] < 1) occn[dev] = 1;
+    }
+    const int64_t g = (int64_t)occn[dev] * sms < ntile ? (int64_t)occn[dev] * sms : ntile;
+    (void)nb;
+    mrep_tma_kernel<D, false><<<(unsigned)g, TT, smem, s>>>(tc, scale, m, n, gN, grow0, R0, ntile, out, sc);
   }
 }
 

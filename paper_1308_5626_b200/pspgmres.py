@@ -142,6 +142,8 @@ def lib():
                                     P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("PSP_LIB") and not hasattr(L, name):
+            continue                    # an older build under A/B (tools/): bind what it has
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args
