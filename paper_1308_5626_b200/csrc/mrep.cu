@@ -150,6 +150,55 @@ __device__ __forceinline__ bool chol_packed(double (&A)[P * (P + 1) / 2], double
   return ok;
 }
 
+// 1/s for s > 0: the hardware approximation refined by two Newton steps (~23 -> 46 -> 92 bits)
+__device__ __forceinline__ double rcp_nr(double s) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = fma(y, fma(-s, y, 1.0), y);
+  return y;
+}
+
+// The same factorisation as LDL^T (G = L D L^T, L unit lower; L_chol = L sqrt(D)): no square
+// roots on the critical path, one reciprocal a column.  Stores 1/D_jj on the diagonal and the
+// strictly-lower L; the condition estimate (max L_jj / min L_jj)^2 of R17 is max D / min D =
+// dmax * imax.  Failure (R17): a pivot D_jj <= 0 or non-finite.
+template <int P>
+__device__ __forceinline__ bool ldl_packed(double (&A)[P * (P + 1) / 2], double& dmax, double& imax) {
+  bool ok = true;
+  double dv[P];
+  static_for<0, P>([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    double w[j > 0 ? j : 1];                       // w_k = L_jk D_k
+    static_for<0, j>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      w[k] = A[pk(j, k)] * dv[k];
+    });
+    double sj = A[pk(j, j)];
+    static_for<0, j>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      sj -= A[pk(j, k)] * w[k];
+    });
+    ok = ok && (sj > 0.0) && isfinite(sj);
+    const double sv = ok ? sj : 1.0;
+    const double inv = rcp_nr(sv);
+    dv[j] = sv;
+    dmax = (j == 0) ? sv : fmax(dmax, sv);
+    imax = (j == 0) ? inv : fmax(imax, inv);
+    A[pk(j, j)] = inv;
+    static_for<j + 1, P>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      double u = A[pk(i, j)];
+      static_for<0, j>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        u -= A[pk(i, k)] * w[k];
+      });
+      A[pk(i, j)] = u * inv;
+    });
+  });
+  return ok;
+}
+
 // Gate statistics of one block: max|diag|, max|diag| over non-dominant rows, min|diag|,
 // rows ridged, rows fallen back, rows non-dominant (R18 / R21)
 struct GateStats {
@@ -160,7 +209,8 @@ struct GateStats {
 // Cholesky + condition estimate + one ridge retry (R17), solve, band install (R14, R15),
 // diagnostics and gate statistics.  ex: (2D+2) x TS sums of the tile's rows; t: this row's
 // index in the tile; r: local row; gr: global row.
-template <int D>
+// LDL: the LDL^T form of the factorisation (ldl_packed) instead of Cholesky (chol_packed)
+template <int D, bool LDL = false>
 __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
                                         int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
   constexpr int P = 2 * D + 2;
@@ -172,9 +222,9 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
 #pragma unroll 1
   for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
     assemble<D>(A, ex, TS, t, m, lambda);
-    ok = chol_packed<P>(A, lmax, imax);
+    ok = LDL ? ldl_packed<P>(A, lmax, imax) : chol_packed<P>(A, lmax, imax);
     if (attempt == 0) {
-      kap = ok ? (lmax * imax) * (lmax * imax) : INFINITY;
+      kap = ok ? (LDL ? lmax * imax : (lmax * imax) * (lmax * imax)) : INFINITY;
       if (ok && kap <= 1e12) break;
       // S:226 ridge retry on G + lambda I
       double tr = (double)m;
@@ -194,6 +244,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
     for (int o = 0; o <= 2 * D; ++o) row[o] = (o == D) ? 1.0 : 0.0;
   } else {
     double z[P];
+    // Cholesky: (L L^T) x = b, each triangle scaled by 1/L_ii;  LDL: unit triangles, 1/D_ii once
     static_for<0, P>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       double sum = (i == 0) ? Tsum : Dl[i > 0 ? i - 1 : 0];
@@ -201,8 +252,12 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
         constexpr int k = decltype(kc)::value;
         sum -= A[pk(i, k)] * z[k];
       });
-      z[i] = sum * A[pk(i, i)];
+      z[i] = LDL ? sum : sum * A[pk(i, i)];
     });
+    if (LDL) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) z[i] *= A[pk(i, i)];
+    }
     static_for<0, P>([&](auto ic) {
       constexpr int i = P - 1 - decltype(ic)::value;
       double sum = z[i];
@@ -210,7 +265,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
         constexpr int k = decltype(kc)::value;
         sum -= A[pk(k, i)] * z[k];
       });
-      z[i] = sum * A[pk(i, i)];
+      z[i] = LDL ? sum : sum * A[pk(i, i)];
     });
     icpt = z[0];                                  // R15: reported, never installed
 #pragma unroll
@@ -743,7 +798,7 @@ __global__ void __launch_bounds__(2 * TT, 1) mrep_ws_kernel(TmaCols cols, const 
 
 // The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
 // lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
-template <int D>
+template <int D, bool LDL = false>
 __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int m, int64_t n, int64_t gN, int64_t grow0,
                                                                          int64_t r0, int64_t r1, MrepOut out,
                                                                          MrepScratch sc) {
@@ -755,7 +810,7 @@ __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int 
 #pragma unroll
     for (int l = 0; l <= 2 * D; ++l) Dl[l] = sc.sums[(int64_t)(2 * D + 2 + l) * ns + r];
     const double Tsum = sc.sums[(int64_t)(4 * D + 3) * ns + r];
-    fit_row<D>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+    fit_row<D, LDL>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
   }
   merge_stats(gs, red, sc.result);
 }
@@ -823,7 +878,9 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
       const int64_t rows = (t1 - t0) * E;
       const int64_t g2max = K > 1 ? sms : sms * PSP_MREP_FIT_MINB;   // beside the sums: one block per SM
       const int64_t g2 = (rows + TT - 1) / TT < g2max ? (rows + TT - 1) / TT : g2max;
-      mrep_fitsum_kernel<D><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
+      static const bool ldl = getenv("PSP_MREP_LDL") != nullptr;   // A/B knob (the LDL^T fit)
+      if (ldl) mrep_fitsum_kernel<D, true><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
+      else mrep_fitsum_kernel<D><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
     }
     cudaEventRecord(ev[K], s2);
     cudaStreamWaitEvent(s, ev[K], 0);
