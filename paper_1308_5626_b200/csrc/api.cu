@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -1232,8 +1233,11 @@ static psp_status resident_solve(psp_ctx* c, const double* b, const double* x0, 
     return fail(c, PSP_E_CUDA, "resident solve: launch failed: " + cuda_err_str(cudaGetLastError()));
   }
   c->launches += 1;
-  double o[16];
-  PSP_TRY(sync_read(c, c->res_out, 14, o));
+  double o[24];
+  PSP_TRY(sync_read(c, c->res_out, 22, o));
+  if (getenv("PSP_RES_PROFILE"))   // instrumented builds: per-phase cycles of CTA 0 (resident.cu)
+    fprintf(stderr, "resident phases (cycles): probe+matvec %.3g dots %.3g solve %.3g update+norm %.3g givens %.3g\n",
+            o[17], o[18], o[19], o[20], o[21]);
   const int iters = (int)o[0];
   // algorithmic bytes: step k reads V_k, k columns twice, writes P_x, P_y,
   // V_{k+1}: 8(2k+4) per row; a cycle start 40, a cycle end 8(k+2)

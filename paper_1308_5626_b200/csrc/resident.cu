@@ -233,8 +233,27 @@ __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, doub
   __syncthreads();
 }
 
+#ifdef PSP_RES_PROFILE
+// phase timer (instrumented builds only): cycles from mark q-1 to mark q summed into out[16 + q]
+#define PROF_MARK(q)                                                        \
+  do {                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      const long long now = clock64();                                      \
+      if ((q) > 0) a.out[16 + (q)] += (double)(now - prof_t);               \
+      prof_t = now;                                                         \
+    }                                                                       \
+  } while (0)
+#else
+#define PROF_MARK(q) do {} while (0)
+#endif
+
 template <int M, int R>
 __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
+#ifdef PSP_RES_PROFILE
+  long long prof_t = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int q = 16; q < 22; ++q) a.out[q] = 0.0;
+#endif
   extern __shared__ __align__(16) double sm[];
   const int nA = a.nA, ld = nA + 1, PV = 2 * nA + 2;
   double* H = sm;                       // (nA+1) x nA, rotated in place
@@ -413,6 +432,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     int kdone = 0;
     for (int k = 1; k <= nA; ++k) {                  // l.8
       // ---- [A] l.10-12: Y_k = N^{-1} V(:,k) -> P_x, A Y_k -> P_y; l.13-16's inner products ----
+      PROF_MARK(0);
       slot = ring_next();
       px = a.ring_px + (int64_t)slot * n;
       py = a.ring_py + (int64_t)slot * n;
@@ -450,6 +470,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       }
       matvecs += 1;
       // s_j = V_j' w (j < k) at [0, k), l_j = V_j' V_k (j < k-1) at [k, 2k-1) (EPI_DOTS layout)
+      PROF_MARK(1);
       grid_reduce(2 * k - 1, [&](int v) -> double {
         const bool isl = v >= k;
         const int j = isl ? v - k : v;
@@ -462,6 +483,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         }
         return s;
       }, true);
+      PROF_MARK(2);
       if (warp == 0) {                                 // (I + L) h = s (R11), as EPI_DOTS, by warp 0:
         double* Lrow = Lm + (int64_t)(k - 1) * ld;     // right-looking -- lane i holds s_i (and
         for (int jb = lane; jb < k - 1; jb += 32) Lrow[jb] = al[jb] * ak * tot[k + jb];   // s_{i+32})
@@ -478,6 +500,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         if (lane + 32 < k) Hc[lane + 32] = s1;
       }
       __syncthreads();
+      PROF_MARK(3);
       // ---- [B] l.13-17: U = w - sum_j h_j alpha_j V_j -> V(:,k+1); H(k+1,k) = ||U|| ----
       {
         const double* Hc = H + (int64_t)(k - 1) * ld;
@@ -503,9 +526,11 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       }, true);
       if (t == 0) {
         H[(int64_t)(k - 1) * ld + k] = sqrt(tot[0]);  // l.17
+        PROF_MARK(4);
         givens_update(S, k, nA);                      // l.18-32 (R4 breakdown, R10)
       }
       __syncthreads();
+      PROF_MARK(5);
       const double R = sc[SC_RK];
       const int flags = (int)sc[SC_FLAGS];
       if (lead && hlen < a.hist_cap) a.hist[hlen] = R;
