@@ -167,16 +167,17 @@ __device__ void seq_solve(const double* lu, int64_t n, int d, const double* v, d
 // incoming state, and each thread re-walks its chunk from it.  Equal to the sequential sweeps in
 // exact arithmetic (composition of affine maps is associative).  y: n-vector scratch; z may
 // alias v (v is consumed by the forward sweep).  sm2: 2 RT doubles.
+template <int T>
 __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, double vs, double* y, double* z,
                               double* sm2) {
   const int t = threadIdx.x;
-  const int64_t L = (n + RT - 1) / RT;
+  const int64_t L = (n + T - 1) / T;
   const int64_t i0 = t * L, i1 = (i0 + L < n) ? i0 + L : n;
   const double* lo = lu;              // band 0: L(i, i-1)
   const double* dg = lu + n;          // band 1: U(i, i)
   const double* up = lu + 2 * n;      // band 2: U(i, i+1)
   double* A = sm2;
-  double* B = sm2 + RT;
+  double* B = sm2 + T;
   // forward: y_i = a_i y_{i-1} + b_i, a_i = -l_i, b_i = vs v_i; chunk map y_out = A y_in + B
   double ca = 1.0, cb = 0.0;
   for (int64_t i = i0; i < i1; ++i) {
@@ -187,7 +188,7 @@ __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, doub
   A[t] = ca;
   B[t] = cb;
   __syncthreads();
-  for (int off = 1; off < RT; off <<= 1) {          // inclusive scan: (A,B)_t <- (A,B)_t o (A,B)_{t-off}
+  for (int off = 1; off < T; off <<= 1) {          // inclusive scan: (A,B)_t <- (A,B)_t o (A,B)_{t-off}
     double na = A[t], nb = B[t];
     if (t >= off) { nb = fma(A[t], B[t - off], B[t]); na = A[t] * A[t - off]; }
     __syncthreads();
@@ -211,11 +212,11 @@ __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, doub
     ca = ei * ca;
     cb = fma(ei, cb, fi);
   }
-  const int tr = RT - 1 - t;                        // reversed order: chunk RT-1 first
+  const int tr = T - 1 - t;                        // reversed order: chunk T-1 first
   A[tr] = ca;
   B[tr] = cb;
   __syncthreads();
-  for (int off = 1; off < RT; off <<= 1) {
+  for (int off = 1; off < T; off <<= 1) {
     double na = A[t], nb = B[t];
     if (t >= off) { nb = fma(A[t], B[t - off], B[t]); na = A[t] * A[t - off]; }
     __syncthreads();
@@ -247,8 +248,9 @@ __device__ void scan_solve_d1(const double* lu, int64_t n, const double* v, doub
 #define PROF_MARK(q) do {} while (0)
 #endif
 
-template <int M, int R>
-__global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
+template <int M, int R, int T>
+__global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
+  constexpr int TW = T / 32;
 #ifdef PSP_RES_PROFILE
   long long prof_t = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -265,8 +267,8 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
   double* Qv = al + ld;                 // nA
   double* rs = Qv + nA;                 // nA (R(k) of the cycle)
   double* sc = rs + nA;                 // SC_NSCAL
-  double* red = sc + SC_NSCAL;          // [RW][PV] (also the 2 RT doubles of the block scans)
-  const int REDN = RW * PV > 2 * RT ? RW * PV : 2 * RT;
+  double* red = sc + SC_NSCAL;          // [TW][PV] (also the 2 T doubles of the block scans)
+  const int REDN = TW * PV > 2 * T ? TW * PV : 2 * T;
   double* tot = red + REDN;             // PV
   DevState S;                           // the replicated scalar state (givens_update's view)
   S.H = H;
@@ -315,60 +317,60 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       if (warp == 0) {
         for (int j = lane; j < nv; j += 32) {
           double s = 0.0;
-          for (int w = 0; w < RW; ++w) s += red[w * PV + j];
+          for (int w = 0; w < TW; ++w) s += red[w * PV + j];
           tot[j] = s;
         }
         __syncwarp();
       }
       return;
     }
-    for (int j = t; j < nv; j += RT) {
+    for (int j = t; j < nv; j += T) {
       double s = 0.0;
-      for (int w = 0; w < RW; ++w) s += red[w * PV + j];
+      for (int w = 0; w < TW; ++w) s += red[w * PV + j];
       tot[j] = s;
     }
     if (gridDim.x > 1) {
       double* part = a.partials + (size_t)(nred & 1u) * gridDim.x * PV;
       nred += 1;
       __syncthreads();
-      for (int j = t; j < nv; j += RT) __stcg(part + (int64_t)blockIdx.x * PV + j, tot[j]);
+      for (int j = t; j < nv; j += T) __stcg(part + (int64_t)blockIdx.x * PV + j, tot[j]);
       grid_sync(a.bar, epoch);
-      // values j = warp + RW q: every lane sums CTAs lane, lane + 32, ... for up to 4 values at
+      // values j = warp + TW q: every lane sums CTAs lane, lane + 32, ... for up to 4 values at
       // once (independent loads in flight), then a warp butterfly; fixed order in every CTA
-      for (int j0 = warp; j0 < nv; j0 += 4 * RW) {
+      for (int j0 = warp; j0 < nv; j0 += 4 * TW) {
         double s4[4] = {0.0, 0.0, 0.0, 0.0};
         for (int c = lane; c < (int)gridDim.x; c += 32) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int j = j0 + q * RW;
+            const int j = j0 + q * TW;
             if (j < nv) s4[q] += ldm<M>(part + (int64_t)c * PV + j);
           }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const double sv = warp_sum(s4[q]);
-          if (lane == 0 && j0 + q * RW < nv) tot[j0 + q * RW] = sv;
+          if (lane == 0 && j0 + q * TW < nv) tot[j0 + q * TW] = sv;
         }
       }
     }
     __syncthreads();
   };
 
-  // this thread's rows: r0 + t + q RT, q < R; with few rows a thread their grid coordinates are
+  // this thread's rows: r0 + t + q T, q < R; with few rows a thread their grid coordinates are
   // kept (no integer divisions in the step), else recomputed per use (registers)
   double w[R];
   constexpr bool PRE = R <= 2;
   int ci0[PRE ? R : 1], cj0[PRE ? R : 1], ck0[PRE ? R : 1];
 #pragma unroll
   for (int q = 0; q < (PRE ? R : 1); ++q) {
-    const int64_t g = r0 + t + (int64_t)q * RT;
+    const int64_t g = r0 + t + (int64_t)q * T;
     ci0[q] = (int)(g % a.st.nx);
     cj0[q] = (int)((g / a.st.nx) % a.st.ny);
     ck0[q] = (int)(g / (a.st.nx * a.st.ny));
   }
-  auto ci = [&](int q) { return PRE ? ci0[q] : (int)((r0 + t + (int64_t)q * RT) % a.st.nx); };
-  auto cj = [&](int q) { return PRE ? cj0[q] : (int)(((r0 + t + (int64_t)q * RT) / a.st.nx) % a.st.ny); };
-  auto ck = [&](int q) { return PRE ? ck0[q] : (int)((r0 + t + (int64_t)q * RT) / (a.st.nx * a.st.ny)); };
+  auto ci = [&](int q) { return PRE ? ci0[q] : (int)((r0 + t + (int64_t)q * T) % a.st.nx); };
+  auto cj = [&](int q) { return PRE ? cj0[q] : (int)(((r0 + t + (int64_t)q * T) / a.st.nx) % a.st.ny); };
+  auto ck = [&](int q) { return PRE ? ck0[q] : (int)((r0 + t + (int64_t)q * T) / (a.st.nx * a.st.ny)); };
   int iters = 0, cycles = 0, matvecs = 0, papply = 0, hlen = 0, blen = 0, status = 0;
   bool finish = false;
   double r0v = 0.0, est = 0.0, eps;
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int64_t g = r0 + t + (int64_t)q * RT;
+        const int64_t g = r0 + t + (int64_t)q * T;
         if (g < r1) { const double bv = __ldg(a.b + g); s = fma(bv, bv, s); }
       }
       return s;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     if (lead) a.slot_scale[slot] = 1.0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const int64_t g = r0 + t + (int64_t)q * RT;
+      const int64_t g = r0 + t + (int64_t)q * T;
       w[q] = 0.0;
       if (g < r1) {
         double xc;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       const double* Vk = V(k - 1);
       if (seqN) {                                      // one CTA: the sweeps of P:30 (d = 1: a
         if (a.d == 1) {                                // block scan of the affine recurrences)
-          scan_solve_d1(a.lu, n, Vk, ak, a.y, px, red);
+          scan_solve_d1<T>(a.lu, n, Vk, ak, a.y, px, red);
         } else {
           if (t == 0) seq_solve(a.lu, n, a.d, Vk, ak, a.y, px, nullptr);
           __syncthreads();
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       double vk[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int64_t g = r0 + t + (int64_t)q * RT;
+        const int64_t g = r0 + t + (int64_t)q * T;
         w[q] = 0.0;
         vk[q] = 0.0;
         if (g < r1) {
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         double s = 0.0;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-          const int64_t g = r0 + t + (int64_t)q * RT;
+          const int64_t g = r0 + t + (int64_t)q * T;
           if (g < r1) s = fma(ldm<M>(Vj + g), isl ? vk[q] : w[q], s);
         }
         return s;
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
         double* Vn = V(k);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-          const int64_t g = r0 + t + (int64_t)q * RT;
+          const int64_t g = r0 + t + (int64_t)q * T;
           if (g < r1) {
             double u = w[q];
             for (int j = 0; j < k; ++j) u = fma(-(Hc[j] * al[j]), ldm<M>(V(j) + g), u);
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     double* zdst = seqN ? a.z : a.X0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const int64_t g = r0 + t + (int64_t)q * RT;
+      const int64_t g = r0 + t + (int64_t)q * T;
       if (g < r1) {
         double zz = seqN ? 0.0 : ldm<M>(a.X0 + g);
         for (int j = 0; j < kdone; ++j) zz = fma(Qv[j] * al[j], ldm<M>(V(j) + g), zz);
@@ -570,8 +572,8 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       __syncthreads();
       // l.42: X = X0 + N^{-1} Z (Z consumed by the forward sweep, then reused for N^{-1} Z)
       if (a.d == 1) {
-        scan_solve_d1(a.lu, n, a.z, 1.0, a.y, a.z, red);
-        for (int64_t i = t; i < n; i += RT) a.X0[i] = a.X0[i] + a.z[i];
+        scan_solve_d1<T>(a.lu, n, a.z, 1.0, a.y, a.z, red);
+        for (int64_t i = t; i < n; i += T) a.X0[i] = a.X0[i] + a.z[i];
       } else if (t == 0) {
         seq_solve(a.lu, n, a.d, a.z, 1.0, a.y, a.z, nullptr);
         for (int64_t i = 0; i < n; ++i) a.X0[i] = a.X0[i] + a.z[i];
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int64_t g = r0 + t + (int64_t)q * RT;
+        const int64_t g = r0 + t + (int64_t)q * T;
         if (g < r1) {
           double xc;
           const double rr = __ldg(a.b + g) - arow<M>(a.st, a.X0, g, ci(q), cj(q), ck(q), xc);
@@ -617,10 +619,10 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(ResArgs a) {
     o[O_COUNT] = count;
   }
   if (blockIdx.x == 0) {                               // the scalar state for the test hooks
-    for (int q = t; q < ld * nA; q += RT) a.ds.H[q] = H[q];
-    for (int q = t; q < ld * ld; q += RT) a.ds.Lm[q] = Lm[q];
-    for (int q = t; q < ld; q += RT) { a.ds.G[q] = Gv[q]; a.ds.alpha[q] = al[q]; }
-    for (int q = t; q < nA; q += RT) { a.ds.C[q] = Cv[q]; a.ds.S[q] = Sv[q]; a.ds.Q[q] = Qv[q]; a.ds.resid[q] = rs[q]; }
+    for (int q = t; q < ld * nA; q += T) a.ds.H[q] = H[q];
+    for (int q = t; q < ld * ld; q += T) a.ds.Lm[q] = Lm[q];
+    for (int q = t; q < ld; q += T) { a.ds.G[q] = Gv[q]; a.ds.alpha[q] = al[q]; }
+    for (int q = t; q < nA; q += T) { a.ds.C[q] = Cv[q]; a.ds.S[q] = Sv[q]; a.ds.Q[q] = Qv[q]; a.ds.resid[q] = rs[q]; }
   }
 }
 
@@ -687,21 +689,23 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   const int dev = device_ordinal();
   thread_local size_t attr[kMaxDev] = {};
   if (attr[dev] < smem) {
-    if (cudaFuncSetAttribute(resident_kernel<1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(resident_kernel<2, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(resident_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(resident_kernel<1, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(resident_kernel<2, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(resident_kernel<2, RMAX, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 1;
     attr[dev] = smem;
   }
   cudaMemsetAsync(c.bar, 0, sizeof(unsigned long long), s);
   void* args[] = {&a};
   if (grid > 1) {
-    if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1, RMAX>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
+    if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1, RMAX, RT>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
       return 1;
-  } else if (c.st.n <= 2 * RT) {
-    resident_kernel<2, 2><<<1, RT, smem, s>>>(a);   // one CTA, two rows a thread (C1)
+  } else if (c.st.n <= (int64_t)128 * RMAX) {
+    // one CTA of four warps, eight rows a thread (C1): the block reductions, barriers and scalar
+    // phases cost per warp, the rows per thread are independent loads in flight
+    resident_kernel<2, RMAX, 128><<<1, 128, smem, s>>>(a);
   } else {
-    resident_kernel<2, RMAX><<<1, RT, smem, s>>>(a);   // one CTA: L1-cached loads, no grid barrier
+    resident_kernel<2, RMAX, RT><<<1, RT, smem, s>>>(a);   // one CTA: L1-cached loads, no grid barrier
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
