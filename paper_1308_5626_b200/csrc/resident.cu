@@ -691,7 +691,7 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   if (attr[dev] < smem) {
     if (cudaFuncSetAttribute(resident_kernel<1, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaFuncSetAttribute(resident_kernel<2, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(resident_kernel<2, RMAX, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        cudaFuncSetAttribute(resident_kernel<2, 2, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 1;
     attr[dev] = smem;
   }
@@ -700,10 +700,10 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   if (grid > 1) {
     if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1, RMAX, RT>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
       return 1;
-  } else if (c.st.n <= (int64_t)128 * RMAX) {
-    // one CTA of four warps, eight rows a thread (C1): the block reductions, barriers and scalar
-    // phases cost per warp, the rows per thread are independent loads in flight
-    resident_kernel<2, RMAX, 128><<<1, 128, smem, s>>>(a);
+  } else if (c.st.n <= 2 * RT) {
+    // one CTA, two rows a thread (C1; measured against four warps with eight rows a thread:
+    // 27 ms against 49 ms for C1's first step -- the per-row work is latency, not issue)
+    resident_kernel<2, 2, RT><<<1, RT, smem, s>>>(a);
   } else {
     resident_kernel<2, RMAX, RT><<<1, RT, smem, s>>>(a);   // one CTA: L1-cached loads, no grid barrier
   }
