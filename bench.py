@@ -255,13 +255,15 @@ def c5_sweep(log2n, peak, ms=(16, 32, 64, 128), ds=(1, 2, 3, 4)):
 def config_lines():
     """The other BASELINE configs as step timings through the same C ABI (CUDA events around
     psp_step): C1 (1-D, n = 1024, 5 steps) and C2 (2-D 512^2, d = 1, 20 steps) on the
-    device-resident solve (f2), and C4 with PSP-CG (f4, 3 steps after one warm-up)."""
+    device-resident solve (f2), C3 (2-D 2048^2 advection-diffusion, the first 2 of its 10 steps,
+    default options: fused passes) and C4 with PSP-CG (f4, 3 steps after one warm-up)."""
     import torch
 
     from paper_1308_5626_b200 import inputs, pspgmres as P
     res = {}
     for key, mk, steps, warm, kw in (("C1_resident", lambda: inputs.c1(), 5, 0, dict(resident=2)),
                                      ("C2_resident", lambda: inputs.c2(d=1), 20, 0, dict(resident=2)),
+                                     ("C3", lambda: inputs.c3(steps=2), 2, 0, {}),
                                      ("C4_psp_cg", lambda: inputs.c4(steps=4), 3, 1, dict(method=P.PSP_METHOD_CG))):
         prob = mk()
         opts = P.default_opts(max_cycles=prob.max_cycles, m_max=prob.m_max, **kw)
