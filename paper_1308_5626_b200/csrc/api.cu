@@ -97,6 +97,9 @@ struct psp_ctx {
   int combined_k = 0;      // the last step of this ring cycle already formed X0 + Z0, Z1 (krylov.cu)
   int combined_slot = -1;  // ring slot whose P_x / P_y columns hold them
   cudaEvent_t ev[6] = {};
+  // multi-rank matvec: the halo exchange runs on a side stream beside the slab's interior planes
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t hev[2] = {};
   // per-kernel-class event timing (opts.timing >= 2)
   struct KRec {
     int klass;
@@ -524,6 +527,10 @@ psp_status psp_create(const psp_grid* grid, const psp_stencil* st, double dt, in
   memset(c->hp, 0, 64 * sizeof(double));
   c->hp[32] = 1.0;  // the pinned constant 1.0 (scale of probes recorded normalised)
   for (int i = 0; i < 6; ++i) cudaEventCreate(&c->ev[i]);
+  if (c->multi) {
+    cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&c->hev[i], cudaEventDisableTiming);
+  }
   // multi-rank: the coefficient field's halo planes, once (the field is fixed per context)
   if (c->multi && S.field) {
     if (comm->sendrecv(S.field, c->hf_lo, plane, S.field + (n - plane), c->hf_hi, plane, c->stream)) {
@@ -566,6 +573,9 @@ psp_status psp_destroy(psp_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int i = 0; i < 6; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (c->hev[i]) cudaEventDestroy(c->hev[i]);
+  if (c->hstream) cudaStreamDestroy(c->hstream);
   for (auto e : c->kev) cudaEventDestroy(e);
   if (c->hp) cudaFreeHost(c->hp);
   delete c;
@@ -678,14 +688,53 @@ FusedLayout flayout(const psp_ctx* c) {
 }
 
 // y = A (xs x) [+ probe copy]; multi-rank: first the slab halo planes of x from rank-1 / rank+1
+// planes [p0, p0 + cnt) of this rank's slab as a stencil of their own: the planes just outside
+// are local data or the received halo (lo / hi), so the march kernels treat them as halo planes
+static Stencil slab_part(const psp_ctx* c, int64_t p0, int64_t cnt, const double* x, const double* lo,
+                         const double* hi) {
+  Stencil v = c->st;
+  const int64_t pl = c->plane, nzl = c->n / pl;
+  if (v.ndim == 3) v.nz = cnt;
+  else v.ny = cnt;
+  v.n = cnt * pl;
+  v.field = c->st.field ? c->st.field + p0 * pl : nullptr;
+  v.x_lo = p0 > 0 ? x + (p0 - 1) * pl : lo;
+  v.x_hi = p0 + cnt < nzl ? x + (p0 + cnt) * pl : hi;
+  v.f_lo = c->st.field ? (p0 > 0 ? c->st.field + (p0 - 1) * pl : c->st.f_lo) : nullptr;
+  v.f_hi = c->st.field ? (p0 + cnt < nzl ? c->st.field + (p0 + cnt) * pl : c->st.f_hi) : nullptr;
+  return v;
+}
+
+// y = A (xs x) [+ probe copy].  Multi-rank: the halo planes of x from rank-1 / rank+1 (NCCL
+// send/recv) travel on a side stream while the slab's interior planes [1, nz-1) -- whose
+// neighbour planes are all local -- are computed; the two boundary planes follow the exchange.
 psp_status matvec(psp_ctx* c, const double* x, const double* xs, double* y, double* xcopy) {
   Stencil st = c->st;
   if (c->multi) {
-    const int64_t pl = c->plane;
+    const int64_t pl = c->plane, nzl = c->n / pl;
+    const double* lo = c->rank > 0 ? c->hx_lo : nullptr;
+    const double* hi = c->rank < c->nranks - 1 ? c->hx_hi : nullptr;
+    if (nzl >= 3 && st.ndim >= 2 && st.kind != PSP_OP_DIA) {
+      cudaEventRecord(c->hev[0], c->stream);               // x is ready
+      const int64_t off = pl;                              // the interior planes (enqueued first: a
+      launch_matvec(slab_part(c, 1, nzl - 2, x, lo, hi), x + off, xs, y + off,   // host-mediated exchange
+                    xcopy ? xcopy + off : nullptr, c->stream);                   // blocks the host thread)
+      cudaStreamWaitEvent(c->hstream, c->hev[0], 0);
+      if (c->comm->sendrecv(x, c->hx_lo, (size_t)pl, x + (c->n - pl), c->hx_hi, (size_t)pl, c->hstream))
+        return fail(c, PSP_E_NCCL, "matvec halo exchange failed");
+      cudaEventRecord(c->hev[1], c->hstream);
+      cudaStreamWaitEvent(c->stream, c->hev[1], 0);       // then the two boundary planes
+      launch_matvec(slab_part(c, 0, 1, x, lo, hi), x, xs, y, xcopy, c->stream);
+      const int64_t last = (nzl - 1) * pl;
+      launch_matvec(slab_part(c, nzl - 1, 1, x, lo, hi), x + last, xs, y + last, xcopy ? xcopy + last : nullptr,
+                    c->stream);
+      c->launches += 3;
+      return PSP_OK;
+    }
     if (c->comm->sendrecv(x, c->hx_lo, (size_t)pl, x + (c->n - pl), c->hx_hi, (size_t)pl, c->stream))
       return fail(c, PSP_E_NCCL, "matvec halo exchange failed");
-    st.x_lo = c->rank > 0 ? c->hx_lo : nullptr;
-    st.x_hi = c->rank < c->nranks - 1 ? c->hx_hi : nullptr;
+    st.x_lo = lo;
+    st.x_hi = hi;
   }
   launch_matvec(st, x, xs, y, xcopy, c->stream);
   c->launches += 1;
