@@ -44,6 +44,12 @@
 #ifndef PSP_FUSED_NSTMAX
 #define PSP_FUSED_NSTMAX 12   // stage ring depth cap (narrow steps: many planes in flight)
 #endif
+#ifndef PSP_FUSED_UCH
+#define PSP_FUSED_UCH 1       // independent FMA chains of the MGS update u (power of two)
+#endif
+#ifndef PSP_FUSED_SCH
+#define PSP_FUSED_SCH 1       // stencil accumulators: 1 (one chain) or 3 (one per axis)
+#endif
 
 namespace psp {
 namespace {
@@ -365,9 +371,20 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
       auto form_u = [&](const double* sb, int q) -> double {
         const double s0 = sb[KMAX * NT + q];
         if (k == 0) return s0;
-        double u = (half == 0) ? wsc * s0 : 0.0;
+        // UCH independent FMA chains (the k-long chain of one accumulator is the pass's critical
+        // path: ncu "wait" stalls on the dependent DFMAs, r02_ncu/fused_k10)
+        constexpr int UC = (KJ >= 2 * PSP_FUSED_UCH) ? PSP_FUSED_UCH : 1;
+        double uu[UC];
+        uu[0] = (half == 0) ? wsc * s0 : 0.0;
 #pragma unroll
-        for (int j = 0; j < KJ; ++j) u = fma(HREG ? hr[j] : -hs[j0 + j], sb[(j0 + j) * NT + q], u);
+        for (int c = 1; c < UC; ++c) uu[c] = 0.0;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) uu[j % UC] = fma(HREG ? hr[j] : -hs[j0 + j], sb[(j0 + j) * NT + q], uu[j % UC]);
+#pragma unroll
+        for (int w = 1; w < UC; w <<= 1)
+#pragma unroll
+          for (int c = 0; c + w < UC; c += 2 * w) uu[c] += uu[c + w];
+        double u = uu[0];
         if (CS == 2) {                           // the halves' partial updates, same sum on both
           const double o = __shfl_xor_sync(0xffffffffu, u, 16);
           u = (half == 0) ? u + o : o + u;
@@ -458,32 +475,35 @@ __global__ void __launch_bounds__(TX * TY * CS / PP + 32, 1)
           if (own[i]) {
             const int q = ptv[i];
             const double c0 = uc[i], kci = kc_[i];
-            double acc = 0.0;
+            // SCH = 3: one accumulator per axis (three short chains), else one chain over the faces
+            double acc3[3] = {0.0, 0.0, 0.0};
+            constexpr int AY = PSP_FUSED_SCH >= 3 ? 1 : 0, AZ = PSP_FUSED_SCH >= 3 ? 2 : 0;
             // a neighbour outside the grid holds u = 0 (TMA zero fill), and its face takes
             // (s/2)(k_c + k_c) = s k_c exactly: only kappa needs the select
-            auto face = [&](double xn, double fn, bool nin, double s, double hsv) {
+            auto face = [&](double& acc, double xn, double fn, bool nin, double s, double hsv) {
               const double kf = cell ? hsv * (kci + (nin ? fn : kci)) : s;
               acc = fma(kf, c0 - xn, acc);
             };
             const double xw = Up[q - 1], xe = Up[q + 1];
-            face(xw, cell ? Kp[q - 1] : 0.0, nb_w[i], st.s[0], hsx);
-            face(xe, cell ? Kp[q + 1] : 0.0, nb_e[i], st.s[0], hsx);
-            if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[0], c0 - xw, acc);
+            face(acc3[0], xw, cell ? Kp[q - 1] : 0.0, nb_w[i], st.s[0], hsx);
+            face(acc3[0], xe, cell ? Kp[q + 1] : 0.0, nb_e[i], st.s[0], hsx);
+            if (KIND == PSP_OP_CELL_ADVDIFF) acc3[0] = fma(st.a[0], c0 - xw, acc3[0]);
             if (HASY) {
               const double xs_ = Up[q - TX], xn_ = Up[q + TX];
-              face(xs_, cell ? Kp[q - TX] : 0.0, nb_s[i], st.s[1], hsy);
-              face(xn_, cell ? Kp[q + TX] : 0.0, nb_n[i], st.s[1], hsy);
-              if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[1], c0 - xs_, acc);
+              face(acc3[AY], xs_, cell ? Kp[q - TX] : 0.0, nb_s[i], st.s[1], hsy);
+              face(acc3[AY], xn_, cell ? Kp[q + TX] : 0.0, nb_n[i], st.s[1], hsy);
+              if (KIND == PSP_OP_CELL_ADVDIFF) acc3[AY] = fma(st.a[1], c0 - xs_, acc3[AY]);
             }
             {
               // march-axis faces, also for a single-plane march axis (nz = 1): the Dirichlet
               // faces then hold u = 0 (ub / un are 0 off the grid), as in stencil.cu; the 1-D
               // view has s[2] = a[2] = 0, so the faces vanish there
               const bool inb = p > 0 || a.lo_in, int_ = p + 1 < st.nz || a.hi_in;
-              face(ub[i], kb[i], inb, st.s[2], hsz);
-              face(un[i], kt[i], int_, st.s[2], hsz);
-              if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[2], c0 - ub[i], acc);
+              face(acc3[AZ], ub[i], kb[i], inb, st.s[2], hsz);
+              face(acc3[AZ], un[i], kt[i], int_, st.s[2], hsz);
+              if (KIND == PSP_OP_CELL_ADVDIFF) acc3[AZ] = fma(st.a[2], c0 - ub[i], acc3[AZ]);
             }
+            const double acc = PSP_FUSED_SCH >= 3 ? (acc3[0] + acc3[1]) + acc3[2] : acc3[0];
             w[i] = c0 + acc;
             if (half == 0) {
               *oy[i] = w[i];
