@@ -48,7 +48,7 @@
 #define PSP_FUSED_UCH 1       // independent FMA chains of the MGS update u (power of two)
 #endif
 #ifndef PSP_FUSED_SCH
-#define PSP_FUSED_SCH 1       // stencil accumulators: 1 (one chain) or 3 (one per axis)
+#define PSP_FUSED_SCH 3       // stencil accumulators: 1 (one chain) or 3 (one per axis; 0-5 % faster)
 #endif
 
 namespace psp {
@@ -138,7 +138,9 @@ struct FCfg {
   // is released as soon as u is formed (all but one stage in flight; the plane's kappa moves to
   // a kappa plane ring beside the u ring); wider thread column sets (KJ = 16) do not fit the
   // 128-register budget and keep the stage for the t_j and the stencil's kappa instead
-  static constexpr bool RV = KMAX / CS <= 12 || (KMAX / CS <= 16 && NT * CS / PP + 32 <= 384);
+  // (blocks of <= 288 threads have up to 224 registers a thread: room for 30 held values)
+  static constexpr bool RV = KMAX / CS <= 12 || (KMAX / CS <= 16 && NT * CS / PP + 32 <= 384) ||
+                             NT * CS / PP + 32 <= 288;
   static constexpr int NB = KMAX + 2;                        // boxes per stage: V_0..V_{KMAX-1}, w~, kappa
   static constexpr int STAGE = NB * NT;                      // doubles
   static constexpr int RING = (RV ? 2 : 1) * NUB * NT;       // u (+ kappa) plane rings, doubles
@@ -753,6 +755,12 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     // 32 x 11 tiles (12 warps, 168 registers) carries more halo (cycle ~1.5 % slower); two
     // points a thread for k <= 12 was slower (2.0 -> 2.6 ms at k = 2)
     if (kc <= 16) return launch_t<KIND, 32, 14, 16, 1, 2>(a, rpx, rpy, fld, ld, s);
+    {
+      const char* we = getenv("PSP_FUSED_WIDE");   // A/B knob: one thread per point for k > 16
+      const int wide = we ? atoi(we) : 0;
+      if (wide == 1 && kc <= 30) return launch_t<KIND, 32, 8, 30, 1>(a, rpx, rpy, fld, ld, s);
+      if (wide == 2) return launch_t<KIND, 32, 6, 32, 1>(a, rpx, rpy, fld, ld, s);
+    }
     if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, fld, ld, s);
     return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, fld, ld, s);
   }

@@ -398,6 +398,9 @@ constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kerne
 #ifndef PSP_MREP_CHUNKS
 #define PSP_MREP_CHUNKS 16    // row chunks of the split MREP (fits overlap the next chunk's sums)
 #endif
+#ifndef PSP_MREP_SUMS_BPS
+#define PSP_MREP_SUMS_BPS 3   // streaming blocks per SM of a chunked split MREP (a fit block beside)
+#endif
 #ifndef PSP_MREP_FIT_MINB
 #define PSP_MREP_FIT_MINB 2   // resident blocks per SM of the split MREP's fit kernel
 #endif
@@ -864,7 +867,7 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mrep_tma_kernel<D, true>, TT, TmaCfg<D>::SMEM_SUMS);
       if (occ < 1) occ = 1;
     }
-    const int64_t g1max = sms * (int64_t)(K > 1 && occ > 3 ? 3 : occ);
+    const int64_t g1max = sms * (int64_t)(K > 1 && occ > PSP_MREP_SUMS_BPS ? PSP_MREP_SUMS_BPS : occ);
     const int64_t per = (ntile + K - 1) / K;
     for (int c = 0; c < K; ++c) {
       const int64_t t0 = c * per, t1 = (t0 + per < ntile) ? t0 + per : ntile;

@@ -3,6 +3,7 @@
   python tools/kbench.py matvec [size=512] [reps=20]
   python tools/kbench.py mrep   [log2n=27] [m=32] [d=3] [reps=5]
   python tools/kbench.py solve  [log2n=27] [d=3] [reps=10]
+  python tools/kbench.py mrepring [size=512] [reps=5]   (psp_mrep_fit on a C4 context's full ring)
 
 Times with CUDA events on the launching stream (after a warm-up launch) and prints GB/s at the
 algorithmic bytes of DESIGN.md section 6.
@@ -77,7 +78,25 @@ def solve(log2n=27, d=3, reps=10):
     print(f"banded factor n=2^{log2n} d={d}: {msf:.3f} ms  {bf * n / msf / 1e6:.0f} GB/s ({bf} B/row)")
 
 
+def mrepring(size=512, reps=5):
+    prob = inputs.c4(n=size, steps=1)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = P.Context(prob.op, d=prob.d, restart=prob.restart, tol=prob.tol,
+                        opts=P.default_opts(max_cycles=2, m_max=prob.m_max), stream=s)
+        b = torch.as_tensor(prob.u0).cuda()
+        x = torch.zeros_like(b)
+        ctx.psp_solve(b, b, x)                   # two cycles: a full probe ring
+    torch.cuda.synchronize()
+    ms = timed(lambda: ctx.psp_mrep_fit(), reps, s)
+    n = size ** 3
+    bb = 16 * prob.m_max + 8 * (2 * prob.d + 1)
+    print(f"mrep ring {size}^3 m={prob.m_max} d={prob.d}: {ms:.3f} ms  {n / ms / 1e6:.2f} G rows/s  "
+          f"{bb * n / ms / 1e6:.0f} GB/s ({bb} B/row)")
+    ctx.close()
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     args = [int(a) for a in sys.argv[2:]]
-    {"matvec": matvec, "mrep": mrep, "solve": solve}[what](*args)
+    {"matvec": matvec, "mrep": mrep, "solve": solve, "mrepring": mrepring}[what](*args)
