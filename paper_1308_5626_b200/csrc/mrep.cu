@@ -398,6 +398,9 @@ constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kerne
 #ifndef PSP_MREP_CHUNKS
 #define PSP_MREP_CHUNKS 16    // row chunks of the split MREP (fits overlap the next chunk's sums)
 #endif
+#ifndef PSP_MREP_SUMS_LB
+#define PSP_MREP_SUMS_LB 4    // launch bound (blocks per SM) of the streaming kernel: its register cap
+#endif
 #ifndef PSP_MREP_SUMS_BPS
 #define PSP_MREP_SUMS_BPS 3   // streaming blocks per SM of a chunked split MREP (a fit block beside)
 #endif
@@ -463,7 +466,7 @@ struct TmaCols {
 // side included; overlapping tiles write identical values) goes to sc.sums, and
 // mrep_fitsum_kernel fits the rows afterwards at its own occupancy.
 template <int D, bool SUMS>
-__global__ void __launch_bounds__(TT, SUMS ? 4 : PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
+__global__ void __launch_bounds__(TT, SUMS ? PSP_MREP_SUMS_LB : PSP_MREP_MINB) mrep_tma_kernel(TmaCols cols, const double* __restrict__ scale,
                                                                       int m, int64_t n, int64_t gN, int64_t grow0,
                                                                       int64_t R0, int64_t ntile, MrepOut out,
                                                                       MrepScratch sc) {
