@@ -40,14 +40,17 @@ constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four 
 // solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks for d >= 3, 4 per SM
 // at d = 3 and 3 per SM at d = 4 (more independent tiles in flight; measured n = 2^26: d = 3
 // 2.34 -> 2.04 ms, d = 4 4.25 -> 3.65 ms; d = 1 prefers 256)
+#ifndef PSP_SOLVE_SR
+#define PSP_SOLVE_SR 8
+#endif
+constexpr int SR = PSP_SOLVE_SR; // solve: rows per thread (the block scan of thread maps is per SR rows)
 template <int D>
 struct SW {
   static constexpr int TPB = D >= 3 ? 128 : 256;
   static constexpr int MINB = D >= 4 ? 3 : (D == 3 ? 4 : 2);   // d = 4: 3 blocks (168 registers) spill less
-  static constexpr int TILE = TPB * 8;
+  static constexpr int TILE = TPB * SR;
 };
 constexpr int STPB = 128;        // solve: the smallest block (host-side sizing of per-tile arrays)
-constexpr int SR = 8;            // solve: rows per thread
 constexpr int STILE = STPB * SR; // solve: rows per tile
 constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank conflicts)
 
@@ -375,30 +378,36 @@ __device__ __forceinline__ void stage_tile(double* sv, const double* __restrict_
   double* su0 = sv + (1 + D) * SW<D>::TPB * SPAD;
   constexpr int IT = SW<D>::TILE / SW<D>::TPB;              // rows per thread of the coalesced copy
   constexpr int NA = 1 + D + (FWD ? 0 : 1);
-  // every load of the tile is issued before the first shared-memory store (one latency per tile)
-  double r[IT][NA];
+  // every load of a group of (up to) eight rows a thread is issued before its first shared-
+  // memory store (one latency per group)
+  constexpr int IG = IT <= 8 ? IT : (IT % 8 == 0 ? 8 : (IT % 6 == 0 ? 6 : 4));
+  static_assert(IT % IG == 0, "row groups");
   const bool full = base + SW<D>::TILE <= n;
 #pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const int64_t i = base + threadIdx.x + it * SW<D>::TPB;
-    const bool in = full || i < n;
-    r[it][0] = (in && vin) ? __ldg(vin + i) : 0.0;
+  for (int g0 = 0; g0 < IT; g0 += IG) {
+    double r[IG][NA];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
-      const int o = FWD ? (D - 1 - k) : (D + 1 + k);
-      r[it][1 + k] = in ? __ldg(lu + (int64_t)o * n + i) : 0.0;
+    for (int ig = 0; ig < IG; ++ig) {
+      const int64_t i = base + threadIdx.x + (g0 + ig) * SW<D>::TPB;
+      const bool in = full || i < n;
+      r[ig][0] = (in && vin) ? __ldg(vin + i) : 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
+        const int o = FWD ? (D - 1 - k) : (D + 1 + k);
+        r[ig][1 + k] = in ? __ldg(lu + (int64_t)o * n + i) : 0.0;
+      }
+      if (!FWD) r[ig][1 + D] = in ? __ldg(lu + (int64_t)D * n + i) : 1.0;
     }
-    if (!FWD) r[it][1 + D] = in ? __ldg(lu + (int64_t)D * n + i) : 1.0;
-  }
 #pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const int q = threadIdx.x + it * SW<D>::TPB;
-    const int sidx = (q / SR) * SPAD + (q % SR);
-    sv[sidx] = vsc * r[it][0];
+    for (int ig = 0; ig < IG; ++ig) {
+      const int q = threadIdx.x + (g0 + ig) * SW<D>::TPB;
+      const int sidx = (q / SR) * SPAD + (q % SR);
+      sv[sidx] = vsc * r[ig][0];
 #pragma unroll
-    for (int k = 0; k < D; ++k) sc0[k * SW<D>::TPB * SPAD + sidx] = r[it][1 + k];
-    if (!FWD) su0[sidx] = 1.0 / r[it][1 + D];   // the reciprocal pivot (padding rows: 1)
+      for (int k = 0; k < D; ++k) sc0[k * SW<D>::TPB * SPAD + sidx] = r[ig][1 + k];
+      if (!FWD) su0[sidx] = 1.0 / r[ig][1 + D];   // the reciprocal pivot (padding rows: 1)
+    }
   }
 }
 
