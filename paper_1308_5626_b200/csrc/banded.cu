@@ -479,21 +479,19 @@ __device__ __forceinline__ Map<D> block_prefix(const Map<D>& my, Map<D>* wtot, M
   if (FWD ? (lane == 0) : (lane == 31)) exw = identity_map<D>();
   if (FWD ? (lane == 31) : (lane == 0)) wtot[warp] = inc;
   __syncthreads();
-  // thread q < NW composes the exclusive prefix of warp q, thread NW the whole tile (each in
-  // processing order, the same compositions as a serial walk over the warp totals), into
-  // wtot[NW + q]: one chain per thread instead of every thread walking all NW totals
-  if (t <= NW) {
-    Map<D> acc = identity_map<D>();
-    if (FWD) {
-      for (int w = 0; w < (t < NW ? t : NW); ++w) acc = compose<D>(wtot[w], acc);
-    } else {
-      for (int w = NW - 1; w > (t < NW ? t : -1); --w) acc = compose<D>(wtot[w], acc);
+  Map<D> wpre = identity_map<D>();
+  agg = identity_map<D>();
+  if (FWD) {
+    for (int w = 0; w < NW; ++w) {
+      if (w == warp) wpre = agg;
+      agg = compose<D>(wtot[w], agg);
     }
-    wtot[NW + t] = acc;
+  } else {
+    for (int w = NW - 1; w >= 0; --w) {
+      if (w == warp) wpre = agg;
+      agg = compose<D>(wtot[w], agg);
+    }
   }
-  __syncthreads();
-  const Map<D> wpre = wtot[NW + warp];
-  agg = wtot[2 * NW];
   __syncthreads();   // wtot may be reused
   return compose<D>(exw, wpre);   // warp prefix first, then the in-warp prefix
 }
@@ -512,7 +510,7 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_map_kernel(const
   // solution differs from y0 only by the homogeneous response to the true incoming state,
   // which tile_fix_kernel adds (it decays geometrically under the dominance gate).
   extern __shared__ double smem_dyn[];
-  __shared__ Map<D> wtot[2 * (SW<D>::TPB / 32) + 1];   // warp totals, warp prefixes, tile
+  __shared__ Map<D> wtot[SW<D>::TPB / 32];
   constexpr int DW = D * D + 2 * D;
   const int t = threadIdx.x;
   const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
@@ -533,7 +531,7 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_map_kernel(const
     const Map<D> my = thread_map<FWD, D>(sv, base, n);
     Map<D> agg;
     const Map<D> pre = block_prefix<FWD, D>(my, wtot, agg);
-    if (t == 0) range = compose<D>(agg, range);   // (read by thread 0 only)
+    range = compose<D>(agg, range);
     if (out != nullptr) {
       double st[D];
       apply<D>(pre, s0, st);
@@ -689,7 +687,7 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_apply_kernel(con
                                                               const double* __restrict__ rmap,
                                                               const double* __restrict__ full) {
   extern __shared__ double smem_dyn[];
-  __shared__ Map<D> wtot[2 * (SW<D>::TPB / 32) + 1];   // warp totals, warp prefixes, tile
+  __shared__ Map<D> wtot[SW<D>::TPB / 32];
   constexpr int DW = D * D + 2 * D;
   const int t = threadIdx.x;
   const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
