@@ -304,14 +304,8 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
   // partials in CTA order -> tot (valid in every thread after the call)
   // w0 (one CTA): the totals are formed by warp 0 and valid only there (its caller consumes
   // them in warp 0 and meets the block at its own barrier) -- one __syncthreads fewer
-  auto grid_reduce = [&](int nv, auto&& f, bool w0 = false) {
-    for (int j0 = 0; j0 < nv; j0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = (j0 + q < nv) ? f(j0 + q) : 0.0;
-      const double r = butterfly8(v, lane);
-      if (lane < 8 && j0 + lane < nv) red[warp * PV + j0 + lane] = r;
-    }
+  // the totals of the warp partials in red (red_finish) -- see grid_reduce
+  auto red_finish = [&](int nv, bool w0) {
     __syncthreads();
     if (w0 && gridDim.x == 1) {
       if (warp == 0) {
@@ -354,6 +348,16 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       }
     }
     __syncthreads();
+  };
+  auto grid_reduce = [&](int nv, auto&& f, bool w0 = false) {
+    for (int j0 = 0; j0 < nv; j0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (j0 + q < nv) ? f(j0 + q) : 0.0;
+      const double r = butterfly8(v, lane);
+      if (lane < 8 && j0 + lane < nv) red[warp * PV + j0 + lane] = r;
+    }
+    red_finish(nv, w0);
   };
 
   // this thread's rows: r0 + t + q T, q < R; with few rows a thread their grid coordinates are
@@ -473,18 +477,35 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       matvecs += 1;
       // s_j = V_j' w (j < k) at [0, k), l_j = V_j' V_k (j < k-1) at [k, 2k-1) (EPI_DOTS layout)
       PROF_MARK(1);
-      grid_reduce(2 * k - 1, [&](int v) -> double {
-        const bool isl = v >= k;
-        const int j = isl ? v - k : v;
-        const double* Vj = V(j);
-        double s = 0.0;
+      // one load of V_j for both of its products, eight columns (all their loads in flight) a
+      // round; the per-thread values and the butterfly / warp-sum order are grid_reduce's
+      for (int j0 = 0; j0 < k; j0 += 8) {
+        double vs[8], vl[8];
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int64_t g = r0 + t + (int64_t)q * T;
-          if (g < r1) s = fma(ldm<M>(Vj + g), isl ? vk[q] : w[q], s);
+        for (int q8 = 0; q8 < 8; ++q8) {
+          const int j = j0 + q8;
+          double ss = 0.0, sl = 0.0;
+          if (j < k) {
+            const double* Vj = V(j);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const int64_t g = r0 + t + (int64_t)q * T;
+              if (g < r1) {
+                const double x = ldm<M>(Vj + g);
+                ss = fma(x, w[q], ss);
+                sl = fma(x, vk[q], sl);
+              }
+            }
+          }
+          vs[q8] = ss;
+          vl[q8] = (j < k - 1) ? sl : 0.0;
         }
-        return s;
-      }, true);
+        const double rs = butterfly8(vs, lane);
+        const double rl = butterfly8(vl, lane);
+        if (lane < 8 && j0 + lane < k) red[warp * PV + j0 + lane] = rs;
+        if (lane < 8 && j0 + lane < k - 1) red[warp * PV + k + j0 + lane] = rl;
+      }
+      red_finish(2 * k - 1, true);
       PROF_MARK(2);
       if (warp == 0) {                                 // (I + L) h = s (R11), as EPI_DOTS, by warp 0:
         double* Lrow = Lm + (int64_t)(k - 1) * ld;     // right-looking -- lane i holds s_i (and
