@@ -90,6 +90,9 @@ __device__ __forceinline__ double butterfly8(double (&v)[8], int lane) {
   return r;
 }
 
+// the cooperative grid is at most one CTA per SM: 148 on B200 -> five rounds of 32 (host-checked)
+constexpr int kCtaRounds = 5;
+
 // grid barrier: monotone arrival counter, epoch e -> wait for grid * e arrivals
 __device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long& epoch) {
   __syncthreads();
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
 #ifdef PSP_RES_PROFILE
   long long prof_t = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int q = 16; q < 22; ++q) a.out[q] = 0.0;
+    for (int q = 16; q < 24; ++q) a.out[q] = 0.0;
 #endif
   extern __shared__ __align__(16) double sm[];
   const int nA = a.nA, ld = nA + 1, PV = 2 * nA + 2;
@@ -328,16 +331,31 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       nred += 1;
       __syncthreads();
       for (int j = t; j < nv; j += T) __stcg(part + (int64_t)blockIdx.x * PV + j, tot[j]);
+      PROF_MARK(6);                                   // (instrumented: local work + CTA totals)
       grid_sync(a.bar, epoch);
+      PROF_MARK(7);                                   // (instrumented: the grid barrier)
       // values j = warp + TW q: every lane sums CTAs lane, lane + 32, ... for up to 4 values at
       // once (independent loads in flight), then a warp butterfly; fixed order in every CTA
+      // (kCtaRounds rounds of 32 CTAs: every load of a value set is issued before the adds, which
+      // keep the CTA order c = lane, lane + 32, ...; a partial written by another SM is an L2
+      // round trip, so a dependent load per round was most of the reduction, r02 profile)
       for (int j0 = warp; j0 < nv; j0 += 4 * TW) {
         double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int c = lane; c < (int)gridDim.x; c += 32) {
+        double x4[kCtaRounds][4];
+#pragma unroll
+        for (int rr = 0; rr < kCtaRounds; ++rr) {
+          const int c = lane + 32 * rr;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int j = j0 + q * TW;
-            if (j < nv) s4[q] += ldm<M>(part + (int64_t)c * PV + j);
+            x4[rr][q] = (c < (int)gridDim.x && j < nv) ? ldm<M>(part + (int64_t)c * PV + j) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kCtaRounds; ++rr) {
+          if (lane + 32 * rr < (int)gridDim.x) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s4[q] += x4[rr][q];
           }
         }
 #pragma unroll
@@ -372,9 +390,12 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
     cj0[q] = (int)((g / a.st.nx) % a.st.ny);
     ck0[q] = (int)(g / (a.st.nx * a.st.ny));
   }
-  auto ci = [&](int q) { return PRE ? ci0[q] : (int)((r0 + t + (int64_t)q * T) % a.st.nx); };
-  auto cj = [&](int q) { return PRE ? cj0[q] : (int)(((r0 + t + (int64_t)q * T) / a.st.nx) % a.st.ny); };
-  auto ck = [&](int q) { return PRE ? ck0[q] : (int)((r0 + t + (int64_t)q * T) / (a.st.nx * a.st.ny)); };
+  // (32-bit: the resident solve's n < 2^31 -- a 64-bit division is an out-of-line call)
+  const unsigned unx = (unsigned)a.st.nx, uny = (unsigned)a.st.ny;
+  auto ug = [&](int q) { return (unsigned)(r0 + t + (int64_t)q * T); };
+  auto ci = [&](int q) { return PRE ? ci0[q] : (int)(ug(q) % unx); };
+  auto cj = [&](int q) { return PRE ? cj0[q] : (int)((ug(q) / unx) % uny); };
+  auto ck = [&](int q) { return PRE ? ck0[q] : (int)(ug(q) / (unx * uny)); };
   int iters = 0, cycles = 0, matvecs = 0, papply = 0, hlen = 0, blen = 0, status = 0;
   bool finish = false;
   double r0v = 0.0, est = 0.0, eps;
@@ -528,17 +549,21 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       {
         const double* Hc = H + (int64_t)(k - 1) * ld;
         double* Vn = V(k);
+        // columns outer, this thread's rows inner: R independent chains (each row's in j order)
+        for (int j = 0; j < k; ++j) {
+          const double cj = -(Hc[j] * al[j]);
+          const double* Vj = V(j);
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            const int64_t g = r0 + t + (int64_t)q * T;
+            if (g < r1) w[q] = fma(cj, ldm<M>(Vj + g), w[q]);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int64_t g = r0 + t + (int64_t)q * T;
-          if (g < r1) {
-            double u = w[q];
-            for (int j = 0; j < k; ++j) u = fma(-(Hc[j] * al[j]), ldm<M>(V(j) + g), u);
-            Vn[g] = u;
-            w[q] = u;
-          } else {
-            w[q] = 0.0;
-          }
+          if (g < r1) Vn[g] = w[q];
+          else w[q] = 0.0;
         }
       }
       grid_reduce(1, [&](int) {
@@ -580,13 +605,26 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
     __syncthreads();
     if (sc[SC_STATUS] != 0.0) { status = PSP_E_SINGULAR; break; }
     double* zdst = seqN ? a.z : a.X0;
+    {
+      double zz[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int64_t g = r0 + t + (int64_t)q * T;
-      if (g < r1) {
-        double zz = seqN ? 0.0 : ldm<M>(a.X0 + g);
-        for (int j = 0; j < kdone; ++j) zz = fma(Qv[j] * al[j], ldm<M>(V(j) + g), zz);
-        zdst[g] = zz;
+      for (int q = 0; q < R; ++q) {
+        const int64_t g = r0 + t + (int64_t)q * T;
+        zz[q] = (g < r1 && !seqN) ? ldm<M>(a.X0 + g) : 0.0;
+      }
+      for (int j = 0; j < kdone; ++j) {            // (as the update: R chains, each in j order)
+        const double cj = Qv[j] * al[j];
+        const double* Vj = V(j);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int64_t g = r0 + t + (int64_t)q * T;
+          if (g < r1) zz[q] = fma(cj, ldm<M>(Vj + g), zz[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int64_t g = r0 + t + (int64_t)q * T;
+        if (g < r1) zdst[g] = zz[q];
       }
     }
     if (seqN) {
@@ -655,19 +693,22 @@ size_t res_smem(int nA) {
 
 }  // namespace
 
+// one CTA per SM, at most 32 kCtaRounds (the partials readback's unrolled rounds)
+static int max_grid() { return device_sms() < 32 * kCtaRounds ? device_sms() : 32 * kCtaRounds; }
+
 bool resident_supported(int64_t n, int nA, bool banded_n) {
   if (nA > kResidentMaxRestart) return false;
   if (banded_n && n > kResidentSeqRows) return false;
   if (res_smem(nA) > 200 * 1024) return false;
   const int64_t per_cta = (int64_t)RT * RMAX;
-  return n <= per_cta * device_sms();
+  return n <= per_cta * max_grid();
 }
 
 int resident_grid(int64_t n, bool banded_n) {
   if (banded_n || n <= kResidentOneCtaRows) return 1;
   int64_t g = (n + RT - 1) / RT;                       // about one row per thread
   const int64_t need = (n + (int64_t)RT * RMAX - 1) / ((int64_t)RT * RMAX);
-  if (g > device_sms()) g = device_sms();
+  if (g > max_grid()) g = max_grid();
   if (g < need) g = need;
   return (int)g;
 }
