@@ -549,8 +549,32 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       {
         const double* Hc = H + (int64_t)(k - 1) * ld;
         double* Vn = V(k);
-        // columns outer, this thread's rows inner: R independent chains (each row's in j order)
-        for (int j = 0; j < k; ++j) {
+        // columns outer, this thread's rows inner: R independent chains (each row's in j order),
+        // the loads of JC columns issued before their FMAs (one load round trip per JC columns)
+        constexpr int JC = R <= 2 ? 8 : (R <= 4 ? 4 : 2);
+        int j = 0;
+        for (; j + JC <= k; j += JC) {
+          double x[JC][R];
+#pragma unroll
+          for (int jj = 0; jj < JC; ++jj) {
+            const double* Vj = V(j + jj);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const int64_t g = r0 + t + (int64_t)q * T;
+              x[jj][q] = (g < r1) ? ldm<M>(Vj + g) : 0.0;
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < JC; ++jj) {
+            const double cj = -(Hc[j + jj] * al[j + jj]);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const int64_t g = r0 + t + (int64_t)q * T;
+              if (g < r1) w[q] = fma(cj, x[jj][q], w[q]);
+            }
+          }
+        }
+        for (; j < k; ++j) {
           const double cj = -(Hc[j] * al[j]);
           const double* Vj = V(j);
 #pragma unroll
@@ -752,6 +776,7 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   thread_local size_t attr[kMaxDev] = {};
   if (attr[dev] < smem) {
     if (cudaFuncSetAttribute(resident_kernel<1, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(resident_kernel<1, 4, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaFuncSetAttribute(resident_kernel<2, RMAX, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaFuncSetAttribute(resident_kernel<2, 2, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 1;
@@ -760,7 +785,10 @@ int launch_resident(const ResidentCall& c, cudaStream_t s) {
   cudaMemsetAsync(c.bar, 0, sizeof(unsigned long long), s);
   void* args[] = {&a};
   if (grid > 1) {
-    if (cudaLaunchCooperativeKernel((const void*)resident_kernel<1, RMAX, RT>, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
+    // at most four rows a thread (C2: 1772 rows a CTA): the register tile of four rows keeps
+    // more column loads in flight than eight mostly idle ones
+    const void* kern = a.chunk <= 4 * RT ? (const void*)resident_kernel<1, 4, RT> : (const void*)resident_kernel<1, RMAX, RT>;
+    if (cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(RT), args, smem, s) != cudaSuccess)
       return 1;
   } else if (c.st.n <= 2 * RT) {
     // one CTA, two rows a thread (C1; measured against four warps with eight rows a thread:
