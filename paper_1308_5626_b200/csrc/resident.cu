@@ -138,6 +138,92 @@ __device__ __noinline__ double arow(const Stencil& st, const double* x, int64_t 
   }
 }
 
+// (A x) at this thread's rows g_q = gb + q T (q < R, g_q < r1) -> y[q], with x_g -> xc[q]:
+// every load of the R rows is issued (predicated) before any face is evaluated, then the faces
+// in stencil_row's order and arithmetic (bitwise its result).  One rank only (the resident solve):
+// a neighbour outside the grid is the Dirichlet zero, never a halo plane.
+template <int KIND, int NDIM, int M, int R, int T>
+__device__ __forceinline__ void rows_eval(const Stencil& st, const double* __restrict__ x, int64_t gb, int64_t r1,
+                                          double (&y)[R], double (&xc)[R]) {
+  constexpr bool cell = KIND != PSP_OP_CONST_DIFF;
+  constexpr int NB = 2 * NDIM;
+  const double* __restrict__ f = st.field;
+  const unsigned unx = (unsigned)st.nx, uny = (unsigned)st.ny;
+  const int64_t strides[3] = {1, st.nx, st.nx * st.ny};
+  double xn[R][NB], fn[R][NB], fc[R];
+  bool in[R][NB];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int64_t g = gb + (int64_t)q * T;
+    const bool valid = g < r1;
+    const unsigned ug = valid ? (unsigned)g : 0u;
+    const unsigned ci = NDIM == 1 ? ug : ug % unx;
+    const unsigned cj = NDIM == 1 ? 0u : (NDIM == 2 ? ug / unx : (ug / unx) % uny);
+    const unsigned ck = NDIM == 3 ? ug / (unx * uny) : 0u;
+    const unsigned cc[3] = {ci, cj, ck};
+    const int64_t ext[3] = {st.nx, st.ny, st.nz};
+    xc[q] = valid ? ldx<M>(x + g) : 0.0;
+    fc[q] = (cell && valid) ? __ldg(f + g) : 0.0;
+#pragma unroll
+    for (int a = 0; a < NDIM; ++a) {
+#pragma unroll
+      for (int dd = 0; dd < 2; ++dd) {                 // dd 0: -1 (w / s / b), 1: +1 (e / n / t)
+        const int nb = 2 * a + dd;
+        const bool ok = valid && (dd == 0 ? cc[a] > 0u : (int64_t)cc[a] + 1 < ext[a]);
+        const int64_t gn = g + (dd == 0 ? -strides[a] : strides[a]);
+        in[q][nb] = ok;
+        xn[q][nb] = ok ? ldx<M>(x + gn) : 0.0;
+        fn[q][nb] = (cell && ok) ? __ldg(f + gn) : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const double c0 = xc[q];
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < NDIM; ++a) {
+#pragma unroll
+      for (int dd = 0; dd < 2; ++dd) {
+        const int nb = 2 * a + dd;
+        const double kf = cell ? (in[q][nb] ? 0.5 * (fc[q] + fn[q][nb]) : fc[q]) : 1.0;
+        acc = fma(st.s[a] * kf, c0 - xn[q][nb], acc);
+      }
+      if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(st.a[a], c0 - xn[q][2 * a], acc);
+    }
+    y[q] = c0 + acc;
+  }
+}
+
+// the R rows of rows_eval for the context's operator kind (one body per kind and dimension; not
+// inlined: three call sites of nine variants would be megabytes of code).  y, xc: R doubles.
+template <int M, int R, int T>
+__device__ __noinline__ void arow_rows(const Stencil& st, const double* x, int64_t gb, int64_t r1, double* y,
+                                       double* xc) {
+  constexpr int G = R < 4 ? R : 4;                  // rows a group (more would spill the loads)
+#pragma unroll 1
+  for (int g0 = 0; g0 < R; g0 += G) {
+    const int64_t gg = gb + (int64_t)g0 * T;
+    double yy[G], xx[G];
+    switch (st.kind * 4 + st.ndim) {
+      case PSP_OP_CONST_DIFF * 4 + 1: rows_eval<PSP_OP_CONST_DIFF, 1, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CONST_DIFF * 4 + 2: rows_eval<PSP_OP_CONST_DIFF, 2, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CONST_DIFF * 4 + 3: rows_eval<PSP_OP_CONST_DIFF, 3, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CELL_DIFF * 4 + 1: rows_eval<PSP_OP_CELL_DIFF, 1, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CELL_DIFF * 4 + 2: rows_eval<PSP_OP_CELL_DIFF, 2, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CELL_DIFF * 4 + 3: rows_eval<PSP_OP_CELL_DIFF, 3, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CELL_ADVDIFF * 4 + 1: rows_eval<PSP_OP_CELL_ADVDIFF, 1, M, G, T>(st, x, gg, r1, yy, xx); break;
+      case PSP_OP_CELL_ADVDIFF * 4 + 2: rows_eval<PSP_OP_CELL_ADVDIFF, 2, M, G, T>(st, x, gg, r1, yy, xx); break;
+      default: rows_eval<PSP_OP_CELL_ADVDIFF, 3, M, G, T>(st, x, gg, r1, yy, xx); break;
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      y[g0 + q] = yy[q];
+      xc[g0 + q] = xx[q];
+    }
+  }
+}
+
 // N^{-1} v by the sequential recurrences of the factors (O2's order of operations):
 // y_i = v_i - sum_{j<i} L(i,j) y_j, z_i = (y_i - sum_{j>i} U(i,j) z_j) / U(i,i).  One thread.
 // vs: v is scaled by vs on the fly.  z may alias v (v is consumed by the forward sweep).
@@ -255,7 +341,7 @@ template <int M, int R, int T>
 __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
   constexpr int TW = T / 32;
 #ifdef PSP_RES_PROFILE
-  long long prof_t = 0;
+  long long prof_t = clock64();
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int q = 16; q < 24; ++q) a.out[q] = 0.0;
 #endif
@@ -476,6 +562,27 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
         papply += 1;
       }
       double vk[R];
+      if (a.st.kind != PSP_OP_DIA) {                   // every row's loads in flight together
+        double yr[R], xr[R];
+        arow_rows<M, R, T>(a.st, seqN ? px : Vk, r0 + t, r1, yr, xr);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int64_t g = r0 + t + (int64_t)q * T;
+          w[q] = 0.0;
+          vk[q] = 0.0;
+          if (g < r1) {
+            if (seqN) {
+              w[q] = yr[q];
+              vk[q] = ldm<M>(Vk + g);
+            } else {                                   // N = I: Y_k = alpha_k V(:,k)
+              vk[q] = xr[q];
+              w[q] = ak * yr[q];
+              px[g] = ak * xr[q];
+            }
+            py[g] = w[q];
+          }
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int64_t g = r0 + t + (int64_t)q * T;
@@ -494,6 +601,7 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
           }
           py[g] = w[q];
         }
+      }
       }
       matvecs += 1;
       // s_j = V_j' w (j < k) at [0, k), l_j = V_j' V_k (j < k-1) at [k, 2k-1) (EPI_DOTS layout)
