@@ -1286,7 +1286,7 @@ static psp_status resident_solve(psp_ctx* c, const double* b, const double* x0, 
   PSP_TRY(sync_read(c, c->res_out, 24, o));
   if (getenv("PSP_RES_PROFILE"))   // instrumented builds: per-phase cycles of CTA 0 (resident.cu)
     fprintf(stderr, "resident phases (cycles): probe+matvec %.3g dots %.3g solve %.3g update+norm %.3g givens %.3g"
-            " | grid reductions: to the barrier %.3g, barrier %.3g\n",
+            " | grid reductions: local work %.3g, CTA totals + barrier %.3g\n",
             o[17], o[18], o[19], o[20], o[21], o[22], o[23]);
   const int iters = (int)o[0];
   // algorithmic bytes: step k reads V_k, k columns twice, writes P_x, P_y,

@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
   // them in warp 0 and meets the block at its own barrier) -- one __syncthreads fewer
   // the totals of the warp partials in red (red_finish) -- see grid_reduce
   auto red_finish = [&](int nv, bool w0) {
+    if (gridDim.x > 1) PROF_MARK(6);                  // (instrumented: the local work)
     __syncthreads();
     if (w0 && gridDim.x == 1) {
       if (warp == 0) {
@@ -417,9 +418,8 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       nred += 1;
       __syncthreads();
       for (int j = t; j < nv; j += T) __stcg(part + (int64_t)blockIdx.x * PV + j, tot[j]);
-      PROF_MARK(6);                                   // (instrumented: local work + CTA totals)
       grid_sync(a.bar, epoch);
-      PROF_MARK(7);                                   // (instrumented: the grid barrier)
+      PROF_MARK(7);                                   // (instrumented: CTA totals + the grid barrier)
       // values j = warp + TW q: every lane sums CTAs lane, lane + 32, ... for up to 4 values at
       // once (independent loads in flight), then a warp butterfly; fixed order in every CTA
       // (kCtaRounds rounds of 32 CTAs: every load of a value set is issued before the adds, which
@@ -515,8 +515,8 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
       if (g < r1) {
         double xc;
         const double y = arow<M>(a.st, a.X0, g, ci(q), cj(q), ck(q), xc);
-        px[g] = xc;
-        py[g] = y;
+        __stcs(px + g, xc);                              // probes: evict-first (V stays in L2)
+        __stcs(py + g, y);
         const double rr = __ldg(a.b + g) - y;
         V(0)[g] = rr;
         w[q] = rr;
@@ -577,9 +577,9 @@ __global__ void __launch_bounds__(T, 1) resident_kernel(ResArgs a) {
             } else {                                   // N = I: Y_k = alpha_k V(:,k)
               vk[q] = xr[q];
               w[q] = ak * yr[q];
-              px[g] = ak * xr[q];
+              __stcs(px + g, ak * xr[q]);               // probes: evict-first (V stays in L2)
             }
-            py[g] = w[q];
+            __stcs(py + g, w[q]);
           }
         }
       } else {
