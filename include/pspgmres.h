@@ -348,6 +348,11 @@ enum {
 };
 psp_status psp_kernel_stats(psp_ctx* ctx, double* h_ms, double* h_bytes, int64_t* h_launches,
                             int reset);
+/* Change opts.timing of a live context (0 none, 1 the report's t_solve / t_mrep / t_factor, 2 also
+ * the per-kernel-class event pairs above): a measurement can time its headline region without
+ * the per-launch events and a second region with them.  PSP_E_ARG for a level outside 0..2;
+ * pending per-class records are kept until psp_kernel_stats flushes them.  No GPU work. */
+psp_status psp_set_timing(psp_ctx* ctx, int level);
 const char* psp_kernel_class_name(int klass);
 
 const char* psp_status_str(psp_status s);

@@ -595,6 +595,13 @@ psp_status psp_launch_count(const psp_ctx* c, int64_t* l) {
   return PSP_OK;
 }
 
+psp_status psp_set_timing(psp_ctx* c, int level) {
+  if (!c) return PSP_E_ARG;
+  if (level < 0 || level > 2) return fail(c, PSP_E_ARG, "psp_set_timing: level must be 0, 1 or 2");
+  c->opts.timing = level;
+  return PSP_OK;
+}
+
 psp_status psp_kernel_stats(psp_ctx* c, double* ms, double* bytes, int64_t* launches, int reset) {
   if (!c) return PSP_E_ARG;
   kt_flush(c);

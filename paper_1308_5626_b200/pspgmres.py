@@ -129,6 +129,7 @@ def lib():
         "psp_get_basis": (C.c_int, [_vp, C.c_int, P(_vp), P(C.c_double)]),
         "psp_launch_count": (C.c_int, [_vp, P(C.c_int64)]),
         "psp_kernel_stats": (C.c_int, [_vp, _dp, _dp, P(C.c_int64), C.c_int]),
+        "psp_set_timing": (C.c_int, [_vp, C.c_int]),
         "psp_kernel_class_name": (C.c_char_p, [C.c_int]),
         "psp_status_str": (C.c_char_p, [C.c_int]),
         "psp_last_error": (C.c_char_p, [_vp]),
@@ -157,6 +158,7 @@ EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destro
             "psp_banded_factor_raw", "psp_banded_solve_raw", "psp_set_bands", "psp_get_bands", "psp_inject_fault_rows",
             "psp_ring_view",
             "psp_ring_reset", "psp_get_hessenberg", "psp_get_basis", "psp_launch_count", "psp_kernel_stats",
+            "psp_set_timing",
             "psp_kernel_class_name", "psp_status_str",
             "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_loopback_create",
             "psp_comm_host_create", "psp_comm_destroy", "psp_partition"]
@@ -478,6 +480,9 @@ class Context:
         v = C.c_int64()
         _check(lib().psp_launch_count(self.h, C.byref(v)), self.h)
         return v.value
+
+    def psp_set_timing(self, level):
+        _check(lib().psp_set_timing(self.h, int(level)), self.h)
 
     def psp_kernel_stats(self, reset=True):
         """{class name: dict(ms, bytes, launches)} (needs opts.timing >= 2)."""
