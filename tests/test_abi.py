@@ -92,3 +92,11 @@ def test_struct_layouts_match_header(tmp_path):
         assert got[(s, "size")] == ctypes.sizeof(cs), s
         for f, _ in cs._fields_:
             assert got[(s, f)] == getattr(cs, f).offset, (s, f)
+
+
+def test_set_timing_rejects_null_context_without_gpu():
+    # psp_set_timing validates before touching a context (bench.py switches levels 1 <-> 2)
+    from paper_1308_5626_b200 import pspgmres as P
+    lib = P.lib()
+    assert lib.psp_set_timing(None, 1) == P.PSP_E_ARG
+    assert lib.psp_launch_count(None, None) == P.PSP_E_ARG
