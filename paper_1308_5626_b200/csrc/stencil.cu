@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(32 * M4S<KIND, BY>::NW, M4S<KIND, BY>::MINB)
       }
     }
     __syncthreads();
-    if (in) {
+    if (compute) {                                            // warp-uniform: full-mask shuffles
       // in-plane y neighbours from the tile: missing -> x = 0, k = k_c
       Q4 xsn = zero4, xnn = zero4, fsn = fc, fnn = fc;
       if (has_s) {
@@ -533,8 +533,8 @@ __global__ void __launch_bounds__(32 * M4S<KIND, BY>::NW, M4S<KIND, BY>::MINB)
         fw = __shfl_up_sync(0xffffffffu, fc.d, 1);
         fe = __shfl_down_sync(0xffffffffu, fc.a, 1);
       }
-      if (lane == 0 && has_w) { xw = __ldg(x + g - 1); if (cell) fw = __ldg(f + g - 1); }
-      if (lane == 31 && has_e) { xe = __ldg(x + g + 4); if (cell) fe = __ldg(f + g + 4); }
+      if (lane == 0 && in && has_w) { xw = __ldg(x + g - 1); if (cell) fw = __ldg(f + g - 1); }
+      if (lane == 31 && in && has_e) { xe = __ldg(x + g + 4); if (cell) fe = __ldg(f + g + 4); }
       if (!has_w) { xw = 0.0; fw = fc.a; }
       if (!has_e) { xe = 0.0; fe = fc.d; }
       Q4 fbz = fb, ftz = ft;
@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(32 * M4S<KIND, BY>::NW, M4S<KIND, BY>::MINB)
         if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
         return xs * (c + acc);
       };
+      if (in) {
       const double o0 = point(xc.a, fc.a, xw, fw, xc.b, fc.b, xsn.a, fsn.a, xnn.a, fnn.a, xb.a, fbz.a, xt.a, ftz.a);
       const double o1 = point(xc.b, fc.b, xc.a, fc.a, xc.c, fc.c, xsn.b, fsn.b, xnn.b, fnn.b, xb.b, fbz.b, xt.b, ftz.b);
       const double o2 = point(xc.c, fc.c, xc.b, fc.b, xc.d, fc.d, xsn.c, fsn.c, xnn.c, fnn.c, xb.c, fbz.c, xt.c, ftz.c);
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(32 * M4S<KIND, BY>::NW, M4S<KIND, BY>::MINB)
       if (xcopy) {
         *reinterpret_cast<double2*>(xcopy + g) = make_double2(xs * xc.a, xs * xc.b);
         *reinterpret_cast<double2*>(xcopy + g + 2) = make_double2(xs * xc.c, xs * xc.d);
+      }
       }
     }
     buf ^= 1;
