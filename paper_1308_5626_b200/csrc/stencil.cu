@@ -780,12 +780,13 @@ void launch_march4(const MarchView& v0, const double* x, const double* xs, doubl
   const char* se = getenv("PSP_MARCH4S");
   const int sby = se ? atoi(se) : 0;
   if (sby == 6 || sby == 14) {
+    thread_local bool attr[2][kMaxDev] = {};              // per variant (same kernel type)
     auto launch_s = [&](auto kern, int by, size_t smem) {
-      thread_local bool attr[kMaxDev] = {};
       const int dev = device_ordinal();
-      if (!attr[dev]) {
+      bool& set = attr[by == 6 ? 0 : 1][dev];
+      if (!set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr[dev] = true;
+        set = true;
       }
       MarchView vs = v0;
       const int64_t zcs = planes_per_block(((vs.nx + 127) / 128) * ((vs.ny + by - 1) / by), vs.nz);
