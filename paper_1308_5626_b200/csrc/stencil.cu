@@ -419,176 +419,6 @@ __global__ void __launch_bounds__(32 * BY, MINB) march4_kernel(MarchView v, cons
   }
 }
 
-// march4 with the in-plane y neighbours from shared memory: every warp publishes its row of plane
-// z (x and kappa, loaded two planes ahead like the march-axis queue) to a double-buffered tile,
-// one block barrier a plane, and the compute warps read rows j-1 / j+1 from it instead of from
-// L1 / L2 on the critical path (march4's hottest stall).  Two extra warps load the block's halo
-// rows (j0 - 1, j0 + BY).  Same faces, same order, same arithmetic as march4: bitwise its result.
-template <int KIND, int BY>
-struct M4S {
-  static constexpr int NW = BY + 2;                        // warps: halo, BY compute rows, halo
-  static constexpr int NA = KIND != PSP_OP_CONST_DIFF ? 2 : 1;
-  static constexpr size_t SMEM = (size_t)2 * NA * NW * 128 * sizeof(double);
-  static constexpr int MINB = 32 * NW <= 256 ? 2 : 1;
-};
-template <int KIND, int BY>
-__global__ void __launch_bounds__(32 * M4S<KIND, BY>::NW, M4S<KIND, BY>::MINB)
-    march4s_kernel(MarchView v, const double* __restrict__ x, const double* xsp, double* __restrict__ y,
-                   double* __restrict__ xcopy) {
-  using C = M4S<KIND, BY>;
-  constexpr bool cell = (KIND != PSP_OP_CONST_DIFF);
-  constexpr int NW = C::NW;
-  extern __shared__ __align__(16) double m4s[];
-  // [buf][array x / f][warp][64 double2: (a, b) at lane, (c, d) at 32 + lane]
-  double2* tile = reinterpret_cast<double2*>(m4s);
-  auto slot = [&](int buf, int arr, int w) { return tile + ((size_t)(buf * C::NA + arr) * NW + w) * 64; };
-  const double* __restrict__ f = v.field;
-  const int lane = threadIdx.x, w = threadIdx.y;
-  const bool compute = w >= 1 && w <= BY;
-  const int64_t i = (int64_t)blockIdx.x * 128 + 4 * lane;
-  const int64_t j = (int64_t)blockIdx.y * BY + w - 1;         // this warp's row (halo warps: -1 / BY)
-  const int64_t z0 = (int64_t)blockIdx.z * v.zc;
-  const int64_t z1 = (z0 + v.zc < v.nz) ? z0 + v.zc : v.nz;
-  const bool row_ok = j >= 0 && j < v.ny;
-  const bool ld_ok = i < v.nx && row_ok;                      // this warp loads its row
-  const bool in = compute && ld_ok;                           // this thread emits four points
-  const int64_t plane = v.nx * v.ny;
-  const int64_t col = ld_ok ? i + v.nx * j : 0;
-  const bool has_w = i > 0, has_e = i + 4 < v.nx;
-  const bool has_s = in && j > 0, has_n = in && j + 1 < v.ny;
-  const bool lo_in = v.x_lo != nullptr, hi_in = v.x_hi != nullptr;
-  const double xs = xsp ? *xsp : 1.0;
-  const double hs0 = 0.5 * v.s[0], hs1 = 0.5 * v.s[1], hs2 = 0.5 * v.s[2];
-  const double s0c = v.s[0], s1c = v.s[1], s2c = v.s[2];
-  struct Q4 { double a, b, c, d; };
-  auto ld4 = [&](const double* base, int64_t off) -> Q4 {
-    const double2 p = __ldg(reinterpret_cast<const double2*>(base + off));
-    const double2 q = __ldg(reinterpret_cast<const double2*>(base + off + 2));
-    return Q4{p.x, p.y, q.x, q.y};
-  };
-  const Q4 zero4{0.0, 0.0, 0.0, 0.0};
-  auto plane4 = [&](const double* a, const double* lo, const double* hi, int64_t p) -> Q4 {
-    if (!ld_ok) return zero4;
-    if (p >= 0 && p < v.nz) return ld4(a, col + plane * p);
-    if (p < 0 && lo) return ld4(lo, col);
-    if (p >= v.nz && hi) return ld4(hi, col);
-    return zero4;
-  };
-  Q4 xb = plane4(x, v.x_lo, v.x_hi, z0 - 1), xc = plane4(x, v.x_lo, v.x_hi, z0), xt = plane4(x, v.x_lo, v.x_hi, z0 + 1);
-  Q4 fb = zero4, fc = zero4, ft = zero4;
-  if (cell) {
-    fb = plane4(f, v.f_lo, v.f_hi, z0 - 1); fc = plane4(f, v.f_lo, v.f_hi, z0); ft = plane4(f, v.f_lo, v.f_hi, z0 + 1);
-  }
-  int64_t g = col + plane * z0;
-  int buf = 0;
-  for (int64_t z = z0; z < z1; ++z) {
-    Q4 xt2 = zero4, ft2 = zero4;                              // prefetch plane z+2
-    if (ld_ok) {
-      if (z + 2 < v.nz) {
-        xt2 = ld4(x, g + 2 * plane);
-        if (cell) ft2 = ld4(f, g + 2 * plane);
-      } else if (z + 2 == v.nz) {
-        xt2 = plane4(x, v.x_lo, v.x_hi, z + 2);
-        if (cell) ft2 = plane4(f, v.f_lo, v.f_hi, z + 2);
-      }
-    }
-    // publish this row's plane z
-    {
-      double2* sx = slot(buf, 0, w);
-      sx[lane] = make_double2(xc.a, xc.b);
-      sx[32 + lane] = make_double2(xc.c, xc.d);
-      if (cell) {
-        double2* sf = slot(buf, 1, w);
-        sf[lane] = make_double2(fc.a, fc.b);
-        sf[32 + lane] = make_double2(fc.c, fc.d);
-      }
-    }
-    __syncthreads();
-    if (compute) {                                            // warp-uniform: full-mask shuffles
-      // in-plane y neighbours from the tile: missing -> x = 0, k = k_c
-      Q4 xsn = zero4, xnn = zero4, fsn = fc, fnn = fc;
-      if (has_s) {
-        const double2* r0 = slot(buf, 0, w - 1);
-        const double2 p = r0[lane], q = r0[32 + lane];
-        xsn = Q4{p.x, p.y, q.x, q.y};
-        if (cell) {
-          const double2* r1 = slot(buf, 1, w - 1);
-          const double2 pf = r1[lane], qf = r1[32 + lane];
-          fsn = Q4{pf.x, pf.y, qf.x, qf.y};
-        }
-      }
-      if (has_n) {
-        const double2* r0 = slot(buf, 0, w + 1);
-        const double2 p = r0[lane], q = r0[32 + lane];
-        xnn = Q4{p.x, p.y, q.x, q.y};
-        if (cell) {
-          const double2* r1 = slot(buf, 1, w + 1);
-          const double2 pf = r1[lane], qf = r1[32 + lane];
-          fnn = Q4{pf.x, pf.y, qf.x, qf.y};
-        }
-      }
-      double xw = __shfl_up_sync(0xffffffffu, xc.d, 1), xe = __shfl_down_sync(0xffffffffu, xc.a, 1);
-      double fw = 0.0, fe = 0.0;
-      if (cell) {
-        fw = __shfl_up_sync(0xffffffffu, fc.d, 1);
-        fe = __shfl_down_sync(0xffffffffu, fc.a, 1);
-      }
-      if (lane == 0 && in && has_w) { xw = __ldg(x + g - 1); if (cell) fw = __ldg(f + g - 1); }
-      if (lane == 31 && in && has_e) { xe = __ldg(x + g + 4); if (cell) fe = __ldg(f + g + 4); }
-      if (!has_w) { xw = 0.0; fw = fc.a; }
-      if (!has_e) { xe = 0.0; fe = fc.d; }
-      Q4 fbz = fb, ftz = ft;
-      if (z == 0 && !lo_in) fbz = fc;
-      if (z + 1 == v.nz && !hi_in) ftz = fc;
-      auto point = [&](double c, double k, double xwv, double fwv, double xev, double fev, double xsv,
-                       double fsv, double xnv, double fnv, double xbv, double fbv, double xtv, double ftv) {
-        double acc = 0.0;
-        if (cell) {
-          acc = fma(hs0 * (k + fwv), c - xwv, acc);
-          acc = fma(hs0 * (k + fev), c - xev, acc);
-        } else {
-          acc = fma(s0c, c - xwv, acc);
-          acc = fma(s0c, c - xev, acc);
-        }
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[0], c - xwv, acc);
-        if (cell) {
-          acc = fma(hs1 * (k + fsv), c - xsv, acc);
-          acc = fma(hs1 * (k + fnv), c - xnv, acc);
-        } else {
-          acc = fma(s1c, c - xsv, acc);
-          acc = fma(s1c, c - xnv, acc);
-        }
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[1], c - xsv, acc);
-        if (cell) {
-          acc = fma(hs2 * (k + fbv), c - xbv, acc);
-          acc = fma(hs2 * (k + ftv), c - xtv, acc);
-        } else {
-          acc = fma(s2c, c - xbv, acc);
-          acc = fma(s2c, c - xtv, acc);
-        }
-        if (KIND == PSP_OP_CELL_ADVDIFF) acc = fma(v.a[2], c - xbv, acc);
-        return xs * (c + acc);
-      };
-      if (in) {
-      const double o0 = point(xc.a, fc.a, xw, fw, xc.b, fc.b, xsn.a, fsn.a, xnn.a, fnn.a, xb.a, fbz.a, xt.a, ftz.a);
-      const double o1 = point(xc.b, fc.b, xc.a, fc.a, xc.c, fc.c, xsn.b, fsn.b, xnn.b, fnn.b, xb.b, fbz.b, xt.b, ftz.b);
-      const double o2 = point(xc.c, fc.c, xc.b, fc.b, xc.d, fc.d, xsn.c, fsn.c, xnn.c, fnn.c, xb.c, fbz.c, xt.c, ftz.c);
-      const double o3 = point(xc.d, fc.d, xc.c, fc.c, xe, fe, xsn.d, fsn.d, xnn.d, fnn.d, xb.d, fbz.d, xt.d, ftz.d);
-      *reinterpret_cast<double2*>(y + g) = make_double2(o0, o1);
-      *reinterpret_cast<double2*>(y + g + 2) = make_double2(o2, o3);
-      if (xcopy) {
-        *reinterpret_cast<double2*>(xcopy + g) = make_double2(xs * xc.a, xs * xc.b);
-        *reinterpret_cast<double2*>(xcopy + g + 2) = make_double2(xs * xc.c, xs * xc.d);
-      }
-      }
-    }
-    buf ^= 1;
-    g += plane;
-    xb = xc; xc = xt; xt = xt2;
-    fb = fc; fc = ft; ft = ft2;
-  }
-}
-
 // f4 (PSP-CG, R27/R28): the direction pass p = z + beta p_old -> px, q = A p -> py (the probe
 // (p, A p), recorded with scale 1/||p||) and p'q, p'p, in one pass over HBM: 8 (z) + 8 (p_old) +
 // 8 (field) read, 16 written per row.  march4_kernel's layout (four x-adjacent points a thread,
@@ -776,28 +606,6 @@ void launch_march4(const MarchView& v0, const double* x, const double* xs, doubl
   dim3 grid((unsigned)((v.nx + 127) / 128), (unsigned)((v.ny + BY - 1) / BY), (unsigned)((v.nz + zc - 1) / zc));
   // PSP_MARCH4_MINB=3: the 3-blocks-per-SM build of the kernel (85 registers; A/B knob)
   static const int minb = getenv("PSP_MARCH4_MINB") ? atoi(getenv("PSP_MARCH4_MINB")) : 2;
-  // PSP_MARCH4S=BY (6 or 14): the shared-memory-tile variant with BY compute rows a block
-  const char* se = getenv("PSP_MARCH4S");
-  const int sby = se ? atoi(se) : 0;
-  if (sby == 6 || sby == 14) {
-    thread_local bool attr[2][kMaxDev] = {};              // per variant (same kernel type)
-    auto launch_s = [&](auto kern, int by, size_t smem) {
-      const int dev = device_ordinal();
-      bool& set = attr[by == 6 ? 0 : 1][dev];
-      if (!set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set = true;
-      }
-      MarchView vs = v0;
-      const int64_t zcs = planes_per_block(((vs.nx + 127) / 128) * ((vs.ny + by - 1) / by), vs.nz);
-      vs.zc = (int)zcs;
-      dim3 gs((unsigned)((vs.nx + 127) / 128), (unsigned)((vs.ny + by - 1) / by), (unsigned)((vs.nz + zcs - 1) / zcs));
-      kern<<<gs, dim3(32, by + 2), smem, s>>>(vs, x, xs, y, xcopy);
-    };
-    if (sby == 6) launch_s(march4s_kernel<KIND, 6>, 6, M4S<KIND, 6>::SMEM);
-    else launch_s(march4s_kernel<KIND, 14>, 14, M4S<KIND, 14>::SMEM);
-    return;
-  }
   if (minb >= 3) march4_kernel<KIND, BY, 3><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
   else march4_kernel<KIND, BY><<<grid, dim3(32, BY), 0, s>>>(v, x, xs, y, xcopy);
 }
