@@ -366,6 +366,10 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(P.psp_comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         comm = P.psp_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+        # every collective of the hot path once over the NCCL communicator, checked (fail loudly)
+        st = P.psp_comm_selftest(comm, torch.cuda.current_stream())
+        if st != P.PSP_OK:
+            raise RuntimeError(f"NCCL communicator self-test failed on rank {rank}: status {st}")
     ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
     fk = {}
     if args.fused_kmin is not None:

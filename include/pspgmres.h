@@ -165,9 +165,18 @@ enum { PSP_FLAG_CONVERGED = 1, PSP_FLAG_BREAKDOWN = 2, PSP_FLAG_NONFINITE = 4 };
 /* Communicator (one process per GPU, NCCL over NVLink/NVSwitch).                            */
 /* ---------------------------------------------------------------------------------------- */
 /* nccl_unique_id: the 128-byte ncclUniqueId broadcast by the caller (rank 0 creates it with
- * psp_comm_unique_id).  Collective over nranks processes.  *out is owned by the library. */
+ * psp_comm_unique_id).  Collective over nranks processes.  *out is owned by the library.
+ * nranks = 1 with an id builds a one-rank NCCL communicator (the NCCL bindings exercised on one
+ * GPU: psp_comm_selftest); with a NULL id a one-rank handle without NCCL. */
 psp_status psp_comm_unique_id(void* h_id_128);
 psp_status psp_comm_init(const void* h_nccl_unique_id, int nranks, int rank, psp_comm** out);
+/* Self-test of a communicator (any backend): every collective the hot path uses -- all-reduce
+ * sum / max / min, all-gather, the neighbour send/recv of the slab halos -- on small device
+ * buffers allocated here, with rank-dependent values, checked on the host against their closed
+ * forms.  Collective: every rank calls it (loopback: from its own thread).  stream: a
+ * cudaStream_t (NULL = the legacy stream).  PSP_OK, PSP_E_NCCL on a wrong value (the message
+ * names the collective) or a failed call, PSP_E_CUDA on an allocation / copy failure. */
+psp_status psp_comm_selftest(psp_comm* comm, void* stream);
 /* Test backend: nranks communicators of an in-process group (out: nranks handles) whose ranks
  * live on ONE device, each driven by its own host thread; every collective synchronises the
  * caller's stream, meets the other ranks at a host barrier and moves data with cudaMemcpy, so

@@ -70,6 +70,7 @@ struct NcclComm : psp_comm {
     if (c && nccl().ok) nccl().CommDestroy(c);
   }
   int allreduce(double* d, size_t count, int op, cudaStream_t s) override {
+    if (!c) return nranks == 1 ? 0 : 1;            // one rank without NCCL: the identity
     return nccl().AllReduce(d, d, count, ncclDouble, nccl_op(op), c, s) == ncclSuccess ? 0 : 1;
   }
   int sendrecv(const double* send_lo, double* recv_lo, size_t n_lo, const double* send_hi,
@@ -87,6 +88,7 @@ struct NcclComm : psp_comm {
     return A.GroupEnd() == ncclSuccess ? 0 : 1;
   }
   int allgather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+    if (!c) return (nranks == 1 && cudaMemcpyAsync(recv, send, count * 8, cudaMemcpyDeviceToDevice, s) == cudaSuccess) ? 0 : 1;
     return nccl().AllGather(send, recv, count, ncclDouble, c, s) == ncclSuccess ? 0 : 1;
   }
 };
@@ -250,7 +252,7 @@ psp_status psp_comm_init(const void* id, int nranks, int rank, psp_comm** out) {
   auto* c = new NcclComm();
   c->nranks = nranks;
   c->rank = rank;
-  if (nranks > 1) {
+  if (nranks > 1 || id) {                          // (one rank with an id: a real NCCL comm)
     if (!id) {
       delete c;
       return PSP_E_ARG;
@@ -264,6 +266,55 @@ psp_status psp_comm_init(const void* id, int nranks, int rank, psp_comm** out) {
   }
   *out = c;
   return PSP_OK;
+}
+
+psp_status psp_comm_selftest(psp_comm* c, void* stream) {
+  if (!c) return PSP_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int R = c->nranks, r = c->rank;
+  constexpr int K = 8;                             // values a collective
+  // device layout: [sum K | max K | min K | gather src K | gather dst R K | send lo K | send hi K |
+  //                 recv lo K | recv hi K]
+  const size_t total = (size_t)K * (8 + R);
+  double* d = nullptr;
+  if (cudaMalloc(&d, total * 8) != cudaSuccess) return PSP_E_CUDA;
+  std::vector<double> h(total, -1.0);
+  for (int i = 0; i < K; ++i) {
+    h[i] = r + 0.5 * i;                            // sum over ranks: R(R-1)/2 + R i/2
+    h[K + i] = (double)((r + i) % R) + 10.0 * i;   // a permutation over ranks: max R-1 + 10 i
+    h[2 * K + i] = -(double)((r + 2 * i) % R) + 10.0 * i;   // min -(R-1) + 10 i
+    h[3 * K + i] = 1000.0 * r + i;                 // gathered block q: 1000 q + i
+    h[(size_t)(4 + R) * K + i] = 100.0 * r + i;     // to rank r-1 (its "hi" neighbour)
+    h[(size_t)(5 + R) * K + i] = 100.0 * r + 50.0 + i;   // to rank r+1
+  }
+  auto fail = [&](const char* what) {
+    cudaFree(d);
+    return what ? (psp_status)PSP_E_NCCL : (psp_status)PSP_E_CUDA;
+  };
+  if (cudaMemcpyAsync(d, h.data(), total * 8, cudaMemcpyHostToDevice, s) != cudaSuccess) return fail(nullptr);
+  double* dlo = d + (size_t)(6 + R) * K;
+  double* dhi = d + (size_t)(7 + R) * K;
+  if (c->allreduce(d, K, 0, s) || c->allreduce(d + K, K, 1, s) || c->allreduce(d + 2 * K, K, 2, s))
+    return fail("allreduce");
+  if (c->allgather(d + 3 * K, d + 4 * K, K, s)) return fail("allgather");
+  if (c->sendrecv(d + (size_t)(4 + R) * K, dlo, K, d + (size_t)(5 + R) * K, dhi, K, s)) return fail("sendrecv");
+  std::vector<double> o(total);
+  if (cudaMemcpyAsync(o.data(), d, total * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(nullptr);
+  cudaFree(d);
+  bool ok = true;
+  for (int i = 0; i < K; ++i) {
+    ok = ok && o[i] == 0.5 * R * (R - 1) + 0.5 * R * i;
+    ok = ok && o[K + i] == (R - 1) + 10.0 * i;
+    ok = ok && o[2 * K + i] == -(double)(R - 1) + 10.0 * i;
+    for (int q = 0; q < R; ++q) ok = ok && o[(size_t)(4 + q) * K + i] == 1000.0 * q + i;
+    if (r > 0) ok = ok && o[(size_t)(6 + R) * K + i] == 100.0 * (r - 1) + 50.0 + i;   // rank r-1's hi
+    else ok = ok && o[(size_t)(6 + R) * K + i] == -1.0;                             // untouched
+    if (r < R - 1) ok = ok && o[(size_t)(7 + R) * K + i] == 100.0 * (r + 1) + i;    // rank r+1's lo
+    else ok = ok && o[(size_t)(7 + R) * K + i] == -1.0;
+  }
+  return ok ? PSP_OK : PSP_E_NCCL;
 }
 
 psp_status psp_comm_loopback_create(int nranks, psp_comm** out) {

@@ -139,6 +139,7 @@ def lib():
         "psp_comm_loopback_create": (C.c_int, [C.c_int, P(_vp)]),
         "psp_comm_host_create": (C.c_int, [P(psp_host_transport), C.c_int, C.c_int, P(_vp)]),
         "psp_comm_destroy": (C.c_int, [_vp]),
+        "psp_comm_selftest": (C.c_int, [_vp, _vp]),
         "psp_partition": (C.c_int, [P(psp_grid), C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                     P(C.c_int64)]),
     }
@@ -161,7 +162,7 @@ EXPORTED = ["psp_default_opts", "psp_workspace_bytes", "psp_create", "psp_destro
             "psp_set_timing",
             "psp_kernel_class_name", "psp_status_str",
             "psp_last_error", "psp_version", "psp_comm_unique_id", "psp_comm_init", "psp_comm_loopback_create",
-            "psp_comm_host_create", "psp_comm_destroy", "psp_partition"]
+            "psp_comm_host_create", "psp_comm_destroy", "psp_comm_selftest", "psp_partition"]
 
 
 def psp_partition(n_axes, nranks, rank):
@@ -251,6 +252,13 @@ def psp_comm_host_create(transport: TorchDistTransport, nranks: int, rank: int):
 
 def psp_comm_destroy(h):
     lib().psp_comm_destroy(h)
+
+
+def psp_comm_selftest(h, stream=None):
+    """Every collective of the hot path on small device buffers, checked against closed forms
+    (collective: every rank calls it).  Returns the status (PSP_OK on success)."""
+    sp = _vp(stream.cuda_stream) if stream is not None else None
+    return lib().psp_comm_selftest(h, sp)
 
 
 def _check(st, ctx=None, allow=(PSP_OK,)):

@@ -100,3 +100,8 @@ def test_set_timing_rejects_null_context_without_gpu():
     lib = P.lib()
     assert lib.psp_set_timing(None, 1) == P.PSP_E_ARG
     assert lib.psp_launch_count(None, None) == P.PSP_E_ARG
+
+
+def test_comm_selftest_rejects_null_without_gpu():
+    from paper_1308_5626_b200 import pspgmres as P
+    assert P.lib().psp_comm_selftest(None, None) == P.PSP_E_ARG
