@@ -537,6 +537,12 @@ def main():
                             "unit": UNIT, "ms_per_step": solve_ms / args.steps,
                             "definition": "n x sum(iterations) / sum(t_solve), CUDA events (opts.timing)"}
                            if solve_ms else None),
+            # the steady-state time per Arnoldi iteration (t_solve / iterations of
+            # each timed step, its median over the steps)
+            "ms_per_iteration": ({"median": statistics.median([r["t_solve_ms"] / r["iterations"] for r in reps
+                                                                if r["iterations"]]),
+                                  "per_step": [r["t_solve_ms"] / r["iterations"] for r in reps if r["iterations"]]}
+                                 if solve_ms else None),
             "kernels": kernel_table,
             # the kernel table and the roofline come from this second region of K steps (event
             # pairs around every launch); `value` / ms_per_step from the headline region without them
