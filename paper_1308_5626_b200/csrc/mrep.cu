@@ -210,9 +210,13 @@ struct GateStats {
 // diagnostics and gate statistics.  ex: (2D+2) x TS sums of the tile's rows; t: this row's
 // index in the tile; r: local row; gr: global row.
 // LDL: the LDL^T form of the factorisation (ldl_packed) instead of Cholesky (chol_packed)
-template <int D, bool LDL = false>
-__device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
-                                        int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
+// MODE 0: both attempts here.  MODE 1: the first attempt only -- a row that needs the ridge
+// retry returns true (nothing written; kap_io <- its condition estimate) for a later MODE 2 call,
+// which runs the retry alone from that estimate (the rows' arithmetic is MODE 0's either way).
+template <int D, bool LDL = false, int MODE = 0>
+__device__ __forceinline__ bool fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
+                                        int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g,
+                                        double* kap_io = nullptr) {
   constexpr int P = 2 * D + 2;
   constexpr int NP = P * (P + 1) / 2;
   double A[NP];
@@ -220,12 +224,9 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
   bool ok = false;
   int kind = PSP_ROW_INTERIOR;
 #pragma unroll 1
-  for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
-    assemble<D>(A, ex, TS, t, m, lambda);
-    ok = LDL ? ldl_packed<P>(A, lmax, imax) : chol_packed<P>(A, lmax, imax);
-    if (attempt == 0) {
-      kap = ok ? (LDL ? lmax * imax : (lmax * imax) * (lmax * imax)) : INFINITY;
-      if (ok && kap <= 1e12) break;
+  for (int attempt = (MODE == 2 ? 1 : 0); attempt < (MODE == 1 ? 1 : 2); ++attempt) {  // one code copy
+    if (attempt == 1) {
+      if (MODE == 2) kap = *kap_io;
       // S:226 ridge retry on G + lambda I
       double tr = (double)m;
 #pragma unroll
@@ -233,6 +234,16 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
       lambda = (1e-10 / (double)P) * tr;
       kind = PSP_ROW_INTERIOR_RIDGE;
       g.v[3] += 1.0;
+    }
+    assemble<D>(A, ex, TS, t, m, lambda);
+    ok = LDL ? ldl_packed<P>(A, lmax, imax) : chol_packed<P>(A, lmax, imax);
+    if (attempt == 0) {
+      kap = ok ? (LDL ? lmax * imax : (lmax * imax) * (lmax * imax)) : INFINITY;
+      if (ok && kap <= 1e12) break;
+      if (MODE == 1) {
+        *kap_io = kap;
+        return true;
+      }
     }
   }
   double row[2 * D + 1];
@@ -280,6 +291,7 @@ __device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int
   g.v[0] = fmax(g.v[0], ad);
   g.v[2] = fmin(g.v[2], ad);
   if (!(ad > band_abs_off_sum<D>(row, gr, gN))) { g.v[5] += 1.0; g.v[1] = fmax(g.v[1], ad); }
+  return false;
 }
 
 // Merge a block's gate statistics into result[0..5]: max / min of non-negative doubles through
@@ -804,20 +816,59 @@ __global__ void __launch_bounds__(2 * TT, 1) mrep_ws_kernel(TmaCols cols, const 
 
 // The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
 // lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
+// The rows that need the ridge retry (R17) are not refitted by the thread that met them: they go
+// to a block queue in shared memory (row, first-attempt condition estimate), and whenever the
+// queue holds TT of them every thread of the block refits one -- the retry runs in full warps
+// instead of in the one or two lanes of a warp that needed it (on the C4 ring two thirds of the
+// rows do, scattered: every warp ran the retry).  Same arithmetic per row as MODE 0; the gate
+// statistics are merged order-free, so the result does not depend on the queue order.
 template <int D, bool LDL = false>
 __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int m, int64_t n, int64_t gN, int64_t grow0,
                                                                          int64_t r0, int64_t r1, MrepOut out,
                                                                          MrepScratch sc) {
   __shared__ double red[TT / 32 * 6];
+  __shared__ int64_t qrow[2 * TT];
+  __shared__ double qkap[2 * TT];
+  __shared__ int qn;
   GateStats gs;
+  const int t = threadIdx.x;
   const int64_t ns = sc.sums_n;
-  for (int64_t r = r0 + (int64_t)blockIdx.x * TT + threadIdx.x; r < r1; r += (int64_t)gridDim.x * TT) {
-    double Dl[2 * D + 1];
+  auto sums_of = [&](int64_t r, double (&Dl)[2 * D + 1]) -> double {
 #pragma unroll
     for (int l = 0; l <= 2 * D; ++l) Dl[l] = sc.sums[(int64_t)(2 * D + 2 + l) * ns + r];
-    const double Tsum = sc.sums[(int64_t)(4 * D + 3) * ns + r];
-    fit_row<D, LDL>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
+    return sc.sums[(int64_t)(4 * D + 3) * ns + r];
+  };
+  auto retry = [&](int i) {
+    const int64_t r = qrow[i];
+    double kap = qkap[i];
+    double Dl[2 * D + 1];
+    const double Tsum = sums_of(r, Dl);
+    fit_row<D, LDL, 2>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs, &kap);
+  };
+  if (t == 0) qn = 0;
+  __syncthreads();
+  for (int64_t base = r0 + (int64_t)blockIdx.x * TT; base < r1; base += (int64_t)gridDim.x * TT) {
+    const int64_t r = base + t;
+    if (r < r1) {
+      double Dl[2 * D + 1];
+      const double Tsum = sums_of(r, Dl);
+      double kap = 0.0;
+      if (fit_row<D, LDL, 1>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs, &kap)) {
+        const int pos = atomicAdd(&qn, 1);
+        qrow[pos] = r;
+        qkap[pos] = kap;
+      }
+    }
+    __syncthreads();
+    const int q = qn;                                  // (the same value in every thread)
+    if (q >= TT) {
+      retry(q - TT + t);                               // the newest TT entries, one a thread
+      __syncthreads();
+      if (t == 0) qn = q - TT;
+    }
+    __syncthreads();
   }
+  if (t < qn) retry(t);
   merge_stats(gs, red, sc.result);
 }
 
