@@ -816,22 +816,23 @@ __global__ void __launch_bounds__(2 * TT, 1) mrep_ws_kernel(TmaCols cols, const 
 
 // The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
 // lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
-// The rows that need the ridge retry (R17) are not refitted by the thread that met them: they go
-// to a block queue in shared memory (row, first-attempt condition estimate), and whenever the
-// queue holds TT of them every thread of the block refits one -- the retry runs in full warps
-// instead of in the one or two lanes of a warp that needed it (on the C4 ring two thirds of the
-// rows do, scattered: every warp ran the retry).  Same arithmetic per row as MODE 0; the gate
+// The rows that need the ridge retry (R17) are not refitted by the lane that met them: they go to
+// its warp's queue in shared memory (row, first-attempt condition estimate), and whenever the
+// queue holds 32 of them the warp refits them one a lane -- the retry runs in full warps instead
+// of in the few lanes of a warp that needed it (on the C4 ring two thirds of the rows do,
+// scattered, so every warp ran it).  Warp-synchronous (ballot positions, __syncwarp): no block
+// barrier, the warps keep drifting past each other's FP64 latency (a block-wide queue with two
+// barriers a round measured 25 % slower).  Same arithmetic per row as MODE 0; the gate
 // statistics are merged order-free, so the result does not depend on the queue order.
 template <int D, bool LDL = false>
 __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int m, int64_t n, int64_t gN, int64_t grow0,
                                                                          int64_t r0, int64_t r1, MrepOut out,
                                                                          MrepScratch sc) {
   __shared__ double red[TT / 32 * 6];
-  __shared__ int64_t qrow[2 * TT];
-  __shared__ double qkap[2 * TT];
-  __shared__ int qn;
+  __shared__ int64_t qrow[TT / 32][64];
+  __shared__ double qkap[TT / 32][64];
   GateStats gs;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t ns = sc.sums_n;
   auto sums_of = [&](int64_t r, double (&Dl)[2 * D + 1]) -> double {
 #pragma unroll
@@ -839,36 +840,37 @@ __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int 
     return sc.sums[(int64_t)(4 * D + 3) * ns + r];
   };
   auto retry = [&](int i) {
-    const int64_t r = qrow[i];
-    double kap = qkap[i];
+    const int64_t r = qrow[w][i];
+    double kap = qkap[w][i];
     double Dl[2 * D + 1];
     const double Tsum = sums_of(r, Dl);
     fit_row<D, LDL, 2>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs, &kap);
   };
-  if (t == 0) qn = 0;
-  __syncthreads();
+  int qc = 0;                                          // this warp's queue length (warp-uniform)
   for (int64_t base = r0 + (int64_t)blockIdx.x * TT; base < r1; base += (int64_t)gridDim.x * TT) {
     const int64_t r = base + t;
+    bool defer = false;
+    double kap = 0.0;
     if (r < r1) {
       double Dl[2 * D + 1];
       const double Tsum = sums_of(r, Dl);
-      double kap = 0.0;
-      if (fit_row<D, LDL, 1>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs, &kap)) {
-        const int pos = atomicAdd(&qn, 1);
-        qrow[pos] = r;
-        qkap[pos] = kap;
-      }
+      defer = fit_row<D, LDL, 1>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs, &kap);
     }
-    __syncthreads();
-    const int q = qn;                                  // (the same value in every thread)
-    if (q >= TT) {
-      retry(q - TT + t);                               // the newest TT entries, one a thread
-      __syncthreads();
-      if (t == 0) qn = q - TT;
+    const unsigned mask = __ballot_sync(0xffffffffu, defer);
+    if (defer) {
+      const int pos = qc + __popc(mask & ((1u << lane) - 1u));
+      qrow[w][pos] = r;
+      qkap[w][pos] = kap;
     }
-    __syncthreads();
+    qc += __popc(mask);
+    __syncwarp();
+    if (qc >= 32) {
+      retry(qc - 32 + lane);                           // the newest 32 entries, one a lane
+      qc -= 32;
+      __syncwarp();
+    }
   }
-  if (t < qn) retry(t);
+  if (lane < qc) retry(lane);
   merge_stats(gs, red, sc.result);
 }
 
