@@ -210,14 +210,9 @@ struct GateStats {
 // diagnostics and gate statistics.  ex: (2D+2) x TS sums of the tile's rows; t: this row's
 // index in the tile; r: local row; gr: global row.
 // LDL: the LDL^T form of the factorisation (ldl_packed) instead of Cholesky (chol_packed)
-// mode 0: both attempts here.  mode 1: the first attempt only -- a row that needs the ridge
-// retry returns true (nothing written; kap_io <- its condition estimate) for a later mode-2 call,
-// which runs the retry alone from that estimate (the rows' arithmetic is mode 0's either way).
-// A runtime mode: one code copy of the factorisation for every caller (instruction cache).
 template <int D, bool LDL = false>
-__device__ __forceinline__ bool fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
-                                        int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g,
-                                        int mode = 0, double* kap_io = nullptr) {
+__device__ __forceinline__ void fit_row(const double* ex, int64_t TS, int t, int m, double Tsum, const double (&Dl)[2 * D + 1],
+                                        int64_t r, int64_t n, int64_t gr, int64_t gN, MrepOut out, GateStats& g) {
   constexpr int P = 2 * D + 2;
   constexpr int NP = P * (P + 1) / 2;
   double A[NP];
@@ -225,9 +220,12 @@ __device__ __forceinline__ bool fit_row(const double* ex, int64_t TS, int t, int
   bool ok = false;
   int kind = PSP_ROW_INTERIOR;
 #pragma unroll 1
-  for (int attempt = (mode == 2 ? 1 : 0); attempt < (mode == 1 ? 1 : 2); ++attempt) {  // one code copy
-    if (attempt == 1) {
-      if (mode == 2) kap = *kap_io;
+  for (int attempt = 0; attempt < 2; ++attempt) {  // one code copy for the try and the retry
+    assemble<D>(A, ex, TS, t, m, lambda);
+    ok = LDL ? ldl_packed<P>(A, lmax, imax) : chol_packed<P>(A, lmax, imax);
+    if (attempt == 0) {
+      kap = ok ? (LDL ? lmax * imax : (lmax * imax) * (lmax * imax)) : INFINITY;
+      if (ok && kap <= 1e12) break;
       // S:226 ridge retry on G + lambda I
       double tr = (double)m;
 #pragma unroll
@@ -235,16 +233,6 @@ __device__ __forceinline__ bool fit_row(const double* ex, int64_t TS, int t, int
       lambda = (1e-10 / (double)P) * tr;
       kind = PSP_ROW_INTERIOR_RIDGE;
       g.v[3] += 1.0;
-    }
-    assemble<D>(A, ex, TS, t, m, lambda);
-    ok = LDL ? ldl_packed<P>(A, lmax, imax) : chol_packed<P>(A, lmax, imax);
-    if (attempt == 0) {
-      kap = ok ? (LDL ? lmax * imax : (lmax * imax) * (lmax * imax)) : INFINITY;
-      if (ok && kap <= 1e12) break;
-      if (mode == 1) {
-        *kap_io = kap;
-        return true;
-      }
     }
   }
   double row[2 * D + 1];
@@ -292,7 +280,6 @@ __device__ __forceinline__ bool fit_row(const double* ex, int64_t TS, int t, int
   g.v[0] = fmax(g.v[0], ad);
   g.v[2] = fmin(g.v[2], ad);
   if (!(ad > band_abs_off_sum<D>(row, gr, gN))) { g.v[5] += 1.0; g.v[1] = fmax(g.v[1], ad); }
-  return false;
 }
 
 // Merge a block's gate statistics into result[0..5]: max / min of non-negative doubles through
@@ -817,59 +804,19 @@ __global__ void __launch_bounds__(2 * TT, 1) mrep_ws_kernel(TmaCols cols, const 
 
 // The fitting half of the split MREP: one thread per row r in [r0, r1), its Gram from the
 // lagged sums of rows r-D..r+D in sc.sums (rows of neighbouring tiles: L2 / L1 hits).
-// The rows that need the ridge retry (R17) are not refitted by the lane that met them: they go to
-// its warp's queue in shared memory (row, first-attempt condition estimate), and once the queue
-// holds 32 of them the warp's next round refits them, one a lane -- the retry runs in full warps
-// instead of in the few lanes of a warp that needed it (on the C4 ring two thirds of the rows do,
-// scattered, so every warp ran it).  One fit_row call site (a round is fresh rows or queued ones)
-// and warp-synchronous queues (ballot positions, __syncwarp, no block barrier).  Same arithmetic
-// per row as mode 0; the gate statistics are merged order-free, so the result does not depend on
-// the queue order.
 template <int D, bool LDL = false>
 __global__ void __launch_bounds__(TT, PSP_MREP_FIT_MINB) mrep_fitsum_kernel(int m, int64_t n, int64_t gN, int64_t grow0,
                                                                          int64_t r0, int64_t r1, MrepOut out,
                                                                          MrepScratch sc) {
   __shared__ double red[TT / 32 * 6];
-  __shared__ int64_t qrow[TT / 32][64];
-  __shared__ double qkap[TT / 32][64];
   GateStats gs;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t ns = sc.sums_n;
-  int qc = 0;                                          // this warp's queue length (warp-uniform)
-  int64_t base = r0 + (int64_t)blockIdx.x * TT;
-  const int64_t stride = (int64_t)gridDim.x * TT;
-  for (;;) {
-    const bool fresh = qc < 32 && base < r1;           // warp-uniform
-    if (!fresh && qc == 0) break;
-    // a round: 32 fresh rows, or (queue full, or no rows left) the queued retries
-    const bool drain = !fresh;
-    const int take = drain ? (qc < 32 ? qc : 32) : 0;
-    int64_t r = fresh ? base + t : (lane < take ? qrow[w][qc - take + lane] : 0);
-    double kap = drain && lane < take ? qkap[w][qc - take + lane] : 0.0;
-    const bool active = fresh ? r < r1 : lane < take;
-    bool defer = false;
-    if (active) {
-      double Dl[2 * D + 1];
+  for (int64_t r = r0 + (int64_t)blockIdx.x * TT + threadIdx.x; r < r1; r += (int64_t)gridDim.x * TT) {
+    double Dl[2 * D + 1];
 #pragma unroll
-      for (int l = 0; l <= 2 * D; ++l) Dl[l] = sc.sums[(int64_t)(2 * D + 2 + l) * ns + r];
-      const double Tsum = sc.sums[(int64_t)(4 * D + 3) * ns + r];
-      defer = fit_row<D, LDL>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs,
-                              fresh ? 1 : 2, &kap);
-    }
-    __syncwarp();
-    if (fresh) {
-      base += stride;
-      const unsigned mask = __ballot_sync(0xffffffffu, defer);
-      if (defer) {
-        const int pos = qc + __popc(mask & ((1u << lane) - 1u));
-        qrow[w][pos] = r;
-        qkap[w][pos] = kap;
-      }
-      qc += __popc(mask);
-    } else {
-      qc -= take;
-    }
-    __syncwarp();
+    for (int l = 0; l <= 2 * D; ++l) Dl[l] = sc.sums[(int64_t)(2 * D + 2 + l) * ns + r];
+    const double Tsum = sc.sums[(int64_t)(4 * D + 3) * ns + r];
+    fit_row<D, LDL>(sc.sums + (r - D), ns, D, m, Tsum, Dl, r, n, grow0 + r, gN, out, gs);
   }
   merge_stats(gs, red, sc.result);
 }
