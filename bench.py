@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of one z-slab-sharded problem")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 MREP / banded-solve kernel sweep point")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="multi-rank collectives: NCCL (one GPU a rank), or the library's host transport over "
+                         "torch.distributed gloo (the sharded path with several ranks on one GPU: testing)")
     ap.add_argument("--c5-log2n", type=int, default=26)
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the C5 sweep (m x d grid) and the C1 / C2 / PSP-CG config lines")
@@ -345,11 +348,16 @@ def main():
     from paper_1308_5626_b200 import inputs, pspgmres as P
 
     assert torch.cuda.is_available(), "bench.py needs a GPU (libpspgmres has no CPU path)"
-    torch.cuda.set_device(local)
+    host_tr = args.transport == "host"
+    torch.cuda.set_device(local % torch.cuda.device_count() if host_tr else local)
+    red_dev = "cpu" if host_tr else "cuda"              # device of the bench's own reductions
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_tr:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     # ---- workload: C4 512^3.  N > 1: one problem, z-slab sharded over the ranks (SURVEY 8(e):
     #      halo planes by NCCL send/recv, all-reduced Arnoldi scalars); --replicas: one
@@ -360,16 +368,21 @@ def main():
     n = prob.op.rows
     sharded = world > 1 and not args.replicas
     comm = None
+    transport = None
     if sharded:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(P.psp_comm_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        comm = P.psp_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
-        # every collective of the hot path once over the NCCL communicator, checked (fail loudly)
+        if host_tr:
+            transport = P.TorchDistTransport()                # (kept alive with the communicator)
+            comm = P.psp_comm_host_create(transport, world, rank)
+        else:
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(P.psp_comm_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            comm = P.psp_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+        # every collective of the hot path once over the communicator, checked (fail loudly)
         st = P.psp_comm_selftest(comm, torch.cuda.current_stream())
         if st != P.PSP_OK:
-            raise RuntimeError(f"NCCL communicator self-test failed on rank {rank}: status {st}")
+            raise RuntimeError(f"communicator self-test failed on rank {rank}: status {st}")
     ortho = P.PSP_MGS_1REDUCE if args.ortho == "1reduce" else P.PSP_MGS_LITERAL
     fk = {}
     if args.fused_kmin is not None:
@@ -404,7 +417,7 @@ def main():
     l0 = ctx.psp_launch_count()
 
     # ---- timed region: K steps, device time via CUDA events on the solver stream ----
-    clocks = Clocks(local)
+    clocks = Clocks(torch.cuda.current_device())
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -440,11 +453,11 @@ def main():
     ctx.psp_set_timing(1)
     iters_instr = sum(r["iterations"] for r in reps_i)
     if dist is not None:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
         # sharded: every rank iterates the same global problem (n unknowns); replicas: sum
-        it = torch.tensor([float(n * iters)], dtype=torch.float64, device="cuda")
+        it = torch.tensor([float(n * iters)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(it, op=dist.ReduceOp.MAX if sharded else dist.ReduceOp.SUM)
         total_unknown_iters = float(it.item())
     else:
@@ -497,10 +510,10 @@ def main():
         te = e0.elapsed_time(e1)
         tot = float(n * it_e2e)
         if dist is not None:
-            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([te], dtype=torch.float64, device=red_dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-            it = torch.tensor([tot], dtype=torch.float64, device="cuda")
+            it = torch.tensor([tot], dtype=torch.float64, device=red_dev)
             dist.all_reduce(it, op=dist.ReduceOp.MAX if sharded else dist.ReduceOp.SUM)
             tot = float(it.item())
         e2e = {"value": tot / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,
@@ -522,7 +535,7 @@ def main():
                        "ortho": args.ortho + (f"-ring(fused k={opts.fused_kmin}..{opts.fused_kmax})" if args.fused else "-split"),
                        "dt": prob.op.dt,
                        "l2": "inputs larger than L2 (each vector 8n bytes >> 126 MB); no flush needed",
-                       "parallelism": (f"z-slab x{world} (NCCL halo + all-reduce)" if sharded else
+                       "parallelism": (f"z-slab x{world} ({'host transport over gloo' if host_tr else 'NCCL'} halo + all-reduce)" if sharded else
                                        ("replicas" if world > 1 else "single"))},
             "iterations_per_step": [r["iterations"] for r in reps],
             "cycles_per_step": [r["cycles"] for r in reps],
