@@ -25,4 +25,4 @@ import json
 d=json.loads(open('$O/single_128.json').read().strip().splitlines()[-1])
 print('single', {k: d[k] for k in ('value','ms_per_step','iterations_per_step','true_resid_over_eps')})
 "
-tail -3 $O/*.err
+for f in $O/*.err; do tail -n 3 $f; done
