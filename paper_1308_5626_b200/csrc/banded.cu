@@ -581,7 +581,8 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_map_kernel(const
 constexpr int64_t kFixCap = 16384;
 template <bool FWD, int D>
 __global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_t L, int nr, double* out,
-                                const double* __restrict__ rmap, double* __restrict__ full) {
+                                const double* __restrict__ rmap, double* __restrict__ full, int64_t T) {
+  // T: rows a tile (SW<D>::TILE for the tile kernels, WT for the warp-range kernels)
   constexpr int DW = D * D + 2 * D;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nr) return;
@@ -594,11 +595,11 @@ __global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_
   }
   if (!(amax > 0.0)) return;                       // zero incoming state: y0 is exact
   const double stop = amax * 0x1p-60;
-  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
+  const int64_t ntiles = (n + T - 1) / T;
   const int64_t t0 = (int64_t)r * L, t1 = (t0 + L < ntiles) ? t0 + L : ntiles;
   // rows of the range in processing order
-  const int64_t lo = (FWD ? t0 : ntiles - t1) * SW<D>::TILE;
-  const int64_t hi = ((FWD ? t1 : ntiles - t0) * SW<D>::TILE < n) ? (FWD ? t1 : ntiles - t0) * SW<D>::TILE : n;
+  const int64_t lo = (FWD ? t0 : ntiles - t1) * T;
+  const int64_t hi = ((FWD ? t1 : ntiles - t0) * T < n) ? (FWD ? t1 : ntiles - t0) * T : n;
   const int64_t len = hi - lo;
   const int64_t cap = len < kFixCap ? len : kFixCap;
   int64_t q = 0;
@@ -739,6 +740,255 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_apply_kernel(con
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Warp-range sweeps (the default): the same decomposition as the tile kernels above with the
+// warp as the unit.  Each warp owns a contiguous range of L warp-tiles (32 lanes x WSR rows) in
+// processing order; a lane loads its WSR contiguous rows straight into registers (16-byte loads,
+// whole sectors per warp), runs the zero-state and d unit-state recurrences over them, and a
+// 5-level shuffle scan composes the lane maps.  No shared memory and no block barrier: the tile
+// kernels spent ~10 warp instructions a row on staging, two block barriers and the serial
+// cross-warp composition (ncu r02: tile_map issue-bound at 49 % issue-active, 21 % warps active,
+// 32 % DRAM throughput); here a row costs ~3.  The lane's incoming state is the previous lane's
+// inclusive state (one 3-double shuffle, not an exclusive map), the range map is composed only
+// by the last lane in processing order (its inclusive map is the tile's), and the state carried
+// to the next warp-tile is broadcast from that lane.
+// ---------------------------------------------------------------------------------------
+constexpr int WSR = 8;            // rows a lane
+constexpr int WT = 32 * WSR;      // rows a warp-tile
+constexpr int WWPB = 4;           // warps a block (independent ranges)
+constexpr int NRMAX = 4096;       // ranges a sweep (scan capacity: 4 maps a scan thread)
+#ifndef PSP_WSWEEP_RELOAD
+#define PSP_WSWEEP_RELOAD 0       // 1: reload a lane's rows for the final walk instead of holding them
+#endif
+#ifndef PSP_WSWEEP_MINB
+#define PSP_WSWEEP_MINB 1         // resident blocks per SM asked of the register allocator
+#endif
+
+template <bool FWD, int D>
+__device__ __forceinline__ Map<D> shfl_scan_src(const Map<D>& m, int off) {
+  Map<D> r;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    r.t[i] = FWD ? __shfl_up_sync(0xffffffffu, m.t[i], off) : __shfl_down_sync(0xffffffffu, m.t[i], off);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      r.M[i][j] = FWD ? __shfl_up_sync(0xffffffffu, m.M[i][j], off) : __shfl_down_sync(0xffffffffu, m.M[i][j], off);
+  }
+  return r;
+}
+
+// APPLY = false: walk every range from a zero incoming state, write out = addend + y0 (if out)
+//                and the range map (M, t) into rmap.
+// APPLY = true:  re-walk, from the exact incoming state in rmap, only the ranges flagged in full.
+template <bool FWD, int D, bool APPLY>
+__global__ void __launch_bounds__(32 * WWPB, PSP_WSWEEP_MINB) wsweep_kernel(const double* __restrict__ lu, int64_t n,
+                                                           const double* __restrict__ vin, const double* vscale,
+                                                           const double* addend, double* out, int64_t L, int nr,
+                                                           double* __restrict__ rmap,
+                                                           const double* __restrict__ full, int vec) {
+  constexpr int DW = D * D + 2 * D;
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * WWPB + (threadIdx.x >> 5);
+  if (r >= nr) return;                               // warp-uniform
+  if (APPLY && full[r] == 0.0) return;               // tile_fix_kernel completed this range
+  constexpr int last = FWD ? 31 : 0;                 // last lane of a warp-tile in processing order
+  const int64_t ntiles = (n + WT - 1) / WT;
+  const double vsc = vscale ? *vscale : 1.0;
+  double carried[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) carried[i] = APPLY ? rmap[(int64_t)r * DW + D * D + D + i] : 0.0;
+  Map<D> range = identity_map<D>();                  // valid in lane `last`
+  const int64_t p0 = (int64_t)r * L, p1 = (p0 + L < ntiles) ? p0 + L : ntiles;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int64_t tile = FWD ? p : ntiles - 1 - p;
+    const int64_t rb = tile * WT + (int64_t)lane * WSR;   // this lane's first row
+    const bool whole = rb + WSR <= n;
+    double vv[WSR], cc[D][WSR], uu[WSR];
+    auto load_rows = [&]() {
+      if (vec && whole) {
+#pragma unroll
+        for (int q = 0; q < WSR; q += 2) {
+          double2 a = vin ? __ldg(reinterpret_cast<const double2*>(vin + rb + q)) : make_double2(0.0, 0.0);
+          vv[q] = vsc * a.x;
+          vv[q + 1] = vsc * a.y;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            // FWD: c[k] = L(i, i-k-1) = lu[(D-1-k) n + i];  BWD: c[k] = U(i, i+k+1) = lu[(D+1+k) n + i]
+            const int o = FWD ? (D - 1 - k) : (D + 1 + k);
+            const double2 c2 = __ldg(reinterpret_cast<const double2*>(lu + (int64_t)o * n + rb + q));
+            cc[k][q] = c2.x;
+            cc[k][q + 1] = c2.y;
+          }
+          if (!FWD) {
+            const double2 u2 = __ldg(reinterpret_cast<const double2*>(lu + (int64_t)D * n + rb + q));
+            uu[q] = u2.x;
+            uu[q + 1] = u2.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < WSR; ++q) {
+          const int64_t i = rb + q;
+          const bool in = i < n;
+          vv[q] = (in && vin) ? vsc * __ldg(vin + i) : 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const int o = FWD ? (D - 1 - k) : (D + 1 + k);
+            cc[k][q] = in ? __ldg(lu + (int64_t)o * n + i) : 0.0;
+          }
+          uu[q] = (!FWD && in) ? __ldg(lu + (int64_t)D * n + i) : 1.0;
+        }
+      }
+      if (!FWD) {
+#pragma unroll
+        for (int q = 0; q < WSR; ++q) uu[q] = 1.0 / uu[q];   // the reciprocal pivot, once a row
+      }
+    };
+    load_rows();
+    // the lane's map: zero-state run + the D unit-state runs (padding rows >= n are skipped)
+    double sz[D], su[D][D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      sz[k] = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) su[q][k] = (q == k) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int rr = 0; rr < WSR; ++rr) {
+      const int q = FWD ? rr : (WSR - 1 - rr);
+      if (rb + q >= n) continue;
+      double c[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) c[k] = cc[k][q];
+      const double u0 = FWD ? 1.0 : uu[q];
+      push_state<D>(sz, rec_step<FWD, D>(vv[q], c, sz, u0));
+#pragma unroll
+      for (int s = 0; s < D; ++s) push_state<D>(su[s], rec_step<FWD, D>(0.0, c, su[s], u0));
+    }
+    Map<D> inc;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      inc.t[i] = sz[i];
+#pragma unroll
+      for (int s = 0; s < D; ++s) inc.M[i][s] = su[s][i];
+    }
+    // inclusive scan of the lane maps in processing order
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Map<D> o = shfl_scan_src<FWD, D>(inc, off);
+      const bool has = FWD ? (lane >= off) : (lane + off < 32);
+      if (has) inc = compose<D>(inc, o);
+    }
+    double sinc[D], st[D];
+    apply<D>(inc, carried, sinc);                    // the state after this lane's rows
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const double prev = FWD ? __shfl_up_sync(0xffffffffu, sinc[i], 1) : __shfl_down_sync(0xffffffffu, sinc[i], 1);
+      st[i] = (lane == (FWD ? 0 : 31)) ? carried[i] : prev;   // the state entering this lane
+    }
+    if (!APPLY && lane == last) range = compose<D>(inc, range);
+#pragma unroll
+    for (int i = 0; i < D; ++i) carried[i] = __shfl_sync(0xffffffffu, sinc[i], last);
+    if (out != nullptr) {
+      // RELOAD: the rows again (L1 / L2 hits), so that they are not live across the scan
+      if (PSP_WSWEEP_RELOAD) load_rows();
+      double y[WSR];
+#pragma unroll
+      for (int rr = 0; rr < WSR; ++rr) {
+        const int q = FWD ? rr : (WSR - 1 - rr);
+        if (rb + q >= n) { y[q] = 0.0; continue; }
+        double c[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) c[k] = cc[k][q];
+        y[q] = rec_step<FWD, D>(vv[q], c, st, FWD ? 1.0 : uu[q]);
+        push_state<D>(st, y[q]);
+      }
+      if (vec && whole) {
+#pragma unroll
+        for (int q = 0; q < WSR; q += 2) {
+          double2 w = make_double2(y[q], y[q + 1]);
+          if (addend) {
+            const double2 a = *reinterpret_cast<const double2*>(addend + rb + q);
+            w.x += a.x;
+            w.y += a.y;
+          }
+          *reinterpret_cast<double2*>(out + rb + q) = w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < WSR; ++q)
+          if (rb + q < n) out[rb + q] = addend ? addend[rb + q] + y[q] : y[q];
+      }
+    }
+  }
+  if (!APPLY && lane == last) {
+    double* dd = rmap + (int64_t)r * DW;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      dd[D * D + i] = range.t[i];
+#pragma unroll
+      for (int j = 0; j < D; ++j) dd[i * D + j] = range.M[i][j];
+    }
+  }
+}
+
+// one block: exact incoming state of up to NRMAX ranges (G consecutive ranges a thread: a local
+// composition, the block scan of the thread aggregates, then the thread's ranges in order)
+template <bool FWD, int D>
+__global__ void __launch_bounds__(SCAN_T, 1) wscan_kernel(int nr, double* __restrict__ rmap,
+                                                          const double* s_in0, double* s_out) {
+  extern __shared__ double smem_dyn[];
+  Map<D>* sm = reinterpret_cast<Map<D>*>(smem_dyn);   // [SCAN_T]
+  constexpr int DW = D * D + 2 * D;
+  const int t = threadIdx.x;
+  const int G = (nr + SCAN_T - 1) / SCAN_T;
+  const int j0 = t * G, j1 = (j0 + G < nr) ? j0 + G : nr;
+  auto load = [&](int j) {
+    Map<D> m;
+    const double* dd = rmap + (int64_t)j * DW;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      m.t[i] = dd[D * D + i];
+#pragma unroll
+      for (int k = 0; k < D; ++k) m.M[i][k] = dd[i * D + k];
+    }
+    return m;
+  };
+  Map<D> agg = identity_map<D>();
+  for (int j = j0; j < j1; ++j) agg = compose<D>(load(j), agg);
+  sm[t] = agg;
+  __syncthreads();
+  for (int off = 1; off < SCAN_T; off <<= 1) {      // inclusive (later ranges applied last)
+    Map<D> o = identity_map<D>();
+    if (t >= off) o = sm[t - off];
+    __syncthreads();
+    if (t >= off) sm[t] = compose<D>(sm[t], o);
+    __syncthreads();
+  }
+  double s0[D], s[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) s0[i] = s_in0 ? s_in0[i] : 0.0;
+  if (t > 0) apply<D>(sm[t - 1], s0, s);
+  else
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = s0[i];
+  for (int j = j0; j < j1; ++j) {
+    const Map<D> m = load(j);
+#pragma unroll
+    for (int i = 0; i < D; ++i) rmap[(int64_t)j * DW + D * D + D + i] = s[i];
+    double s1[D];
+    apply<D>(m, s, s1);
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = s1[i];
+  }
+  if (s_out && t == SCAN_T - 1) {
+    double so[D];
+    apply<D>(sm[SCAN_T - 1], s0, so);
+#pragma unroll
+    for (int i = 0; i < D; ++i) s_out[i] = so[i];
+  }
+}
+
 // Warm-start check: chunk c's start state (from its warm-up rows) against chunk c-1's end state,
 // bitwise; any difference sends the factorisation to the exact fixed-point passes.
 __global__ void factor_verify_kernel(const double* __restrict__ st_start, const double* __restrict__ st_end,
@@ -780,17 +1030,47 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
 template <bool FWD, int D>
 void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs, const double* add,
                   double* out, BandedScratch sc, cudaStream_t s, const double* s_in0, double* s_out, int phase) {
-  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   const size_t smem = TileSmem<FWD, D>::BYTES;
   const size_t ssmem = (size_t)SCAN_T * sizeof(Map<D>);
   thread_local bool attr_set[kMaxDev] = {};
+  thread_local int wblocks[kMaxDev] = {};            // resident warp-range blocks per SM
   const int dev = device_ordinal();
   if (!attr_set[dev]) {
     cudaFuncSetAttribute(tile_map_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(tile_apply_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(tile_scan_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+    cudaFuncSetAttribute(wscan_kernel<FWD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wsweep_kernel<FWD, D, false>, 32 * WWPB, 0) !=
+            cudaSuccess || per < 1)
+      per = 1;
+    wblocks[dev] = per;
     attr_set[dev] = true;
   }
+  double* full = sc.states + (size_t)NRMAX * (D * D + 2 * D);   // per-range flag
+  static const bool block_sweeps = getenv("PSP_SOLVE_BLOCK") != nullptr;   // A/B: the tile kernels
+  if (!block_sweeps) {
+    // one range per resident warp (one wave), at most NRMAX
+    const int64_t ntiles = (n + WT - 1) / WT;
+    int64_t nr = (int64_t)device_sms() * wblocks[dev] * WWPB;
+    if (nr > NRMAX) nr = NRMAX;
+    if (nr > ntiles) nr = ntiles;
+    if (nr < 1) nr = 1;
+    const int64_t L = (ntiles + nr - 1) / nr;
+    nr = ntiles > 0 ? (ntiles + L - 1) / L : 0;
+    const unsigned nb = (unsigned)((nr + WWPB - 1) / WWPB);
+    const int vec = (n % 2 == 0) && ((((uintptr_t)lu) | ((uintptr_t)v) | ((uintptr_t)add) | ((uintptr_t)out)) & 15) == 0;
+    if (ntiles > 0 && phase != 2)
+      wsweep_kernel<FWD, D, false><<<nb, 32 * WWPB, 0, s>>>(lu, n, v, vs, add, out, L, (int)nr, sc.states,
+                                                             nullptr, vec);
+    wscan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>((int)nr, sc.states, s_in0, s_out);
+    if (out != nullptr && ntiles > 0 && phase != 1) {
+      tile_fix_kernel<FWD, D><<<(unsigned)((nr + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nr, out, sc.states, full, WT);
+      wsweep_kernel<FWD, D, true><<<nb, 32 * WWPB, 0, s>>>(lu, n, v, vs, add, out, L, (int)nr, sc.states, full, vec);
+    }
+    return;
+  }
+  const int64_t ntiles = (n + SW<D>::TILE - 1) / SW<D>::TILE;
   // ranges: at most SCAN_T blocks (2 resident per SM), each a contiguous run of L tiles
   const int64_t nbmax = (int64_t)device_sms() * SW<D>::MINB * 3;
   int64_t nb = ntiles < nbmax ? ntiles : nbmax;
@@ -798,12 +1078,12 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
   if (nb < 1) nb = 1;
   const int64_t L = (ntiles + nb - 1) / nb;
   nb = (ntiles + L - 1) / L;
-  double* full = sc.states + (size_t)SCAN_T * (D * D + 2 * D);   // per-range flag
   if (ntiles > 0 && phase != 2)
     tile_map_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states);
   tile_scan_kernel<FWD, D><<<1, SCAN_T, ssmem, s>>>(ntiles > 0 ? (int)nb : 0, sc.states, s_in0, s_out);
   if (out != nullptr && ntiles > 0 && phase != 1) {
-    tile_fix_kernel<FWD, D><<<(unsigned)((nb + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nb, out, sc.states, full);
+    tile_fix_kernel<FWD, D><<<(unsigned)((nb + 63) / 64), 64, 0, s>>>(lu, n, L, (int)nb, out, sc.states, full,
+                                                                      SW<D>::TILE);
     tile_apply_kernel<FWD, D><<<(unsigned)nb, SW<D>::TPB, smem, s>>>(lu, n, v, vs, add, out, L, sc.states, full);
   }
 }
@@ -871,7 +1151,7 @@ size_t banded_scratch_bytes(int64_t n, int d) {
   const int64_t DW = d * d + 2 * d;
   size_t b = 64 + 256;
   b += (size_t)ntiles * 8 + 256;
-  b += (size_t)((ntiles > SCAN_T ? ntiles : SCAN_T) * DW + SCAN_T) * 8 + 256;   // range maps + flags
+  b += (size_t)((ntiles > NRMAX ? ntiles : NRMAX) * DW + NRMAX) * 8 + 256;   // range maps + flags
   b += (size_t)2 * nchunks * d * (d + 1) * 8 + 256;
   b += (size_t)n * 8 + 256;
   return b;
@@ -888,7 +1168,7 @@ BandedScratch banded_scratch(void* base, int64_t n, int d) {
   sc.changed = (int*)(p + 32);                  // [0] changed, [1] bad
   p = align256(p + 64 + (size_t)ntiles * 8 + 64);
   sc.states = (double*)p;                       // range maps / states + flags (solve)
-  p = align256(p + (size_t)((ntiles > SCAN_T ? ntiles : SCAN_T) * DW + SCAN_T) * 8);
+  p = align256(p + (size_t)((ntiles > NRMAX ? ntiles : NRMAX) * DW + NRMAX) * 8);
   sc.y = (double*)p;                            // intermediate vector, then factor states
   sc.desc_count = ntiles;
   return sc;
@@ -1026,7 +1306,7 @@ int banded_solve(const double* lu, int64_t n, int d, const double* v, const doub
   if (!(comm && comm->nranks > 1)) {
     sweep(true, d, lu, n, v, vs, nullptr, sc.y, sc, s, nullptr, nullptr);
     sweep(false, d, lu, n, sc.y, nullptr, x0, z, sc, s, nullptr, nullptr);
-    if (launches) *launches += 2;
+    if (launches) *launches += 8;   // per sweep: map, scan, fix, apply
     return PSP_OK;
   }
   Misc M(misc, d, comm->nranks);
@@ -1041,7 +1321,7 @@ int banded_solve(const double* lu, int64_t n, int d, const double* v, const doub
                                           M.sin);
     sweep(fwd != 0, d, lu, n, vin, vsc, add, out, sc, s, M.sin, nullptr, 2);
   }
-  if (launches) *launches += 8;
+  if (launches) *launches += 12;   // per sweep: map + scan, compose, scan + fix + apply
   return PSP_OK;
 }
 

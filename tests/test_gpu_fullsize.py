@@ -245,3 +245,33 @@ def test_c4_lockstep_256_two_cycles(torch, P, orc):
     bench's policy (fused k = 2..16, split-column k = 17..29, the fused last-step combine at
     k = 30) and one restart, compared with the oracle's literal Alg.1."""
     _lockstep_c4(torch, P, orc, 256, 2, with_mrep=False)
+
+
+@pytest.mark.parametrize("d", [1, 3])
+def test_banded_solve_slow_decay_full_size(torch, P, orc, d):
+    """The banded sweeps' exact fallback: a dominant N whose homogeneous
+    response decays only by ~1e-4 a row (off-diagonals -1, diagonal margin 1e-8), so the decaying
+    correction of a 28 K-row warp range has not died out within its 16384-row cap and the range is
+    re-walked from its exact incoming state.  n = 2^26 + 38 (a ragged last warp-tile); the solve
+    runs on the oracle's own LU factors (T2 against the oracle's sweeps on the same factors)."""
+    n = (1 << 26) + 38
+    rng = np.random.default_rng(26 + d)
+    bands = np.zeros((2 * d + 1, n))
+    bands[d - 1] = -1.0
+    bands[d + 1] = -1.0
+    for o in range(2 * d + 1):
+        if abs(o - d) >= 2:
+            bands[o] = 1e-3 * rng.uniform(-1, 1, n)
+    inputs._mask_outside(bands, d)
+    bands[d] = np.abs(bands).sum(axis=0) + 1e-8
+    v = rng.standard_normal(n)
+    st, lu_ref = orc.banded_lu(bands, d)
+    assert st == orc.OK
+    z_ref = orc.banded_lu_solve(lu_ref, d, v)
+    del bands
+    scratch = P.raw_scratch(n, d)
+    z = P.psp_banded_solve_raw(torch.from_numpy(lu_ref).cuda(), d, torch.from_numpy(v).cuda(),
+                               scratch=scratch).cpu().numpy()
+    # rounding differences travel ~1e4 rows (the decay length) before they fade: 1e-9 relative
+    assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
+    _free(torch)
