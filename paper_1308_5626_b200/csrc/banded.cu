@@ -36,7 +36,13 @@ namespace {
 #endif
 constexpr int kChunk = PSP_FACTOR_CHUNK;   // factor: rows per thread
 constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first pass)
-constexpr int kPF = 3;           // factor: prefetch ring depth (groups of four rows)
+#ifndef PSP_FACTOR_PF
+#define PSP_FACTOR_PF 3
+#endif
+#ifndef PSP_FACTOR_TPB
+#define PSP_FACTOR_TPB 64
+#endif
+constexpr int kPF = PSP_FACTOR_PF; // factor: prefetch ring depth (staged groups)
 // solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks for d >= 3, 4 per SM
 // at d = 3 and 3 per SM at d = 4 (more independent tiles in flight; measured n = 2^26: d = 3
 // 2.34 -> 2.04 ms, d = 4 4.25 -> 3.65 ms; d = 1 prefers 256)
@@ -57,11 +63,18 @@ constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank con
 // ---------------------------------------------------------------------------------------
 // Factorisation pass
 // ---------------------------------------------------------------------------------------
-// One pass over every chunk.  Rows are read (and LU written) four at a time with 16-byte
-// accesses: a thread walks its own chunk, so a warp touches 32 chunks at once and only
-// whole-sector accesses keep DRAM traffic at the algorithmic bytes.  WRITE = 0: a state-only
-// pass (the fixed point is iterated without storing LU; one WRITE pass follows convergence).
-template <int D, bool WRITE>
+// One pass over every chunk.  Rows are walked four at a time: a thread walks its own chunk, so a
+// warp touches 32 chunks at once.  WRITE = 0: a state-only pass (the fixed point is iterated
+// without storing LU; one WRITE pass follows convergence).
+//
+// COOP = 1 (d <= 3, 16-byte aligned bands, the default): the bands of the warp's 32 chunks are
+// staged in groups of eight rows by the warp together -- lane j copies 16-byte piece (j & 3) of
+// chunk 8q + (j >> 2), so one cp.async instruction covers eight 64-byte runs instead of 32
+// scattered 16-byte pieces (ncu r02: the per-thread copies left the LSU throttled, mio/lg
+// throttle and long-scoreboard stalls, 37 % DRAM throughput) -- and the LU rows of a staged group
+// go back to HBM the same way from the stage they were computed in.  COOP = 0: each thread copies
+// its own rows (groups of four; d = 4 without the shared-memory ring).
+template <int D, bool WRITE, bool COOP>
 __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, double* __restrict__ lu,
                                    const double* __restrict__ st_in, double* __restrict__ st_out,
                                    int first_pass, int* __restrict__ changed, int* __restrict__ bad,
@@ -71,11 +84,23 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   // of this block (rows of rank-1 / rank+1), so the band entries reaching there are real
   constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
   constexpr int NB = 2 * D + 1;
+  constexpr bool PFON = D <= 3;   // d = 4: the ring's shared memory costs more occupancy than it saves
+  static_assert(!COOP || PFON, "cooperative staging uses the prefetch ring");
+  constexpr int G = COOP ? 8 : 4; // rows a staged group (COOP: two walk steps of four rows)
+  static_assert(kWarm % 8 == 0, "warm-up rows: whole groups");
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  const int64_t r0 = c * kChunk;
-  const int64_t r1 = (r0 + kChunk < n) ? r0 + kChunk : n;
+  if (!COOP && c >= nchunks) return;
+  const bool valid = c < nchunks;  // COOP: lanes past the last chunk still copy for the others
+  const int lane = threadIdx.x & 31;
+  // chunk cc's rows [r0c, r1c) and walk start rsc (warm start: `warm` rows early from the zero state)
+  auto geom = [&](int64_t cc, int64_t& r0c, int64_t& r1c, int64_t& rsc) {
+    r0c = cc * kChunk;
+    r1c = (r0c + kChunk < n) ? r0c + kChunk : n;
+    rsc = (warm > 0 && first_pass && cc > 0) ? (r0c - warm > 0 ? r0c - warm : 0) : r0c;
+  };
+  int64_t r0, r1, rs;
+  geom(valid ? c : 0, r0, r1, rs);
   double Uw[D][D + 1];
   // chunk 0 of rank r > 0 (after the first pass): the last-D-U-rows state of rank r-1
   const bool from_prev = (c == 0) && (prev != nullptr) && !first_pass;
@@ -84,7 +109,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
     for (int q = 0; q < D; ++q)
 #pragma unroll
       for (int e = 0; e <= D; ++e) Uw[q][e] = prev[q * (D + 1) + e];
-  } else if (c == 0 || first_pass) {
+  } else if (c == 0 || first_pass || !valid) {
     // matrix start (exact for chunk 0; the initial guess for the others)
 #pragma unroll
     for (int q = 0; q < D; ++q)
@@ -98,152 +123,232 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
       for (int e = 0; e <= D; ++e) Uw[q][e] = s[q * (D + 1) + e];
   }
   const bool at_start = !from_prev && ((c == 0) || first_pass);
-  // warm start (first pass, warm > 0): the walk begins `warm` rows before the chunk from the
-  // zero state; for a dominant N the state has converged bitwise by the chunk start, which the
-  // caller verifies against the previous chunk's end state (st_start)
-  const int64_t rs = (warm > 0 && first_pass && c > 0) ? (r0 - warm > 0 ? r0 - warm : 0) : r0;
   // first row of the walk's existing window rows: rows below lo do not exist
   const int64_t lo = at_start ? rs : (has_prev ? INT64_MIN / 2 : 0);
   double Ri[D];       // 1 / U(k,k) of the window rows (unused for rows that do not exist)
 #pragma unroll
   for (int q = 0; q < D; ++q) Ri[q] = 1.0 / Uw[q][0];
   int isbad = 0;
-  // the bands of the next groups of four rows are prefetched into this thread's slots of a
-  // PF-deep shared-memory ring by cp.async (16-byte copies, no registers held): a walk is a
-  // serial recurrence, and without the prefetch every group waits a full DRAM latency
-  extern __shared__ __align__(16) double pf[];   // [PF][NB][blockDim][4]
-  auto pf_at = [&](int buf, int o) -> double* {
-    return pf + ((size_t)(buf * NB + o) * blockDim.x + threadIdx.x) * 4;
+  // the bands of the next groups are prefetched into a PF-deep shared-memory ring by cp.async
+  // (16-byte copies, no registers held): a walk is a serial recurrence, and without the prefetch
+  // every group waits a full DRAM latency
+  // [PF][NB][blockDim][GS]: a thread's G rows padded to GS doubles (COOP: 80-byte rows, so
+  // the 16-byte accesses of eight consecutive threads fall in distinct banks)
+  constexpr int GS = COOP ? G + 2 : G;
+  extern __shared__ __align__(16) double pf[];
+  auto pf_of = [&](int buf, int o, int t) -> double* {
+    return pf + ((size_t)(buf * NB + o) * PSP_FACTOR_TPB + t) * GS;
   };
-  constexpr bool PFON = D <= 3;   // d = 4: the ring's shared memory costs more occupancy than it saves
-  auto prefetch = [&](int64_t i0, int buf) {
-    if (!PFON) return;
-    if (vec && i0 + 4 <= r1) {
+  // COOP: the four chunks this lane copies for (cl = 8q + lane/4, piece lane & 3): walk start,
+  // rows of the walk, and the first live row, relative to the walk start
+  int64_t qrs[COOP ? 4 : 1];
+  int qlen[COOP ? 4 : 1], qoff[COOP ? 4 : 1];
+  uint32_t qsa[COOP ? 4 : 1];
+  if (COOP) {
+    const int64_t wbase = c - lane;               // chunk of lane 0 of this warp
 #pragma unroll
-      for (int o = 0; o < NB; ++o) {
-        const double* g = bands + (int64_t)o * n + i0;
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pf_at(buf, o));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16), "l"(g + 2) : "memory");
+    for (int q = 0; q < 4; ++q) {
+      const int cl = 8 * q + (lane >> 2);
+      int64_t r0c, r1c, rsc;
+      geom(wbase + cl, r0c, r1c, rsc);
+      const bool ex = wbase + cl < nchunks;
+      qrs[q] = rsc + 2 * (lane & 3);
+      qlen[q] = ex ? (int)(r1c - rsc) : 0;
+      qoff[q] = (int)(r0c - rsc);
+      qsa[q] = (uint32_t)__cvta_generic_to_shared(pf_of(0, 0, threadIdx.x - lane + cl) + 2 * (lane & 3));
+    }
+  }
+  constexpr uint32_t kStageB = (uint32_t)PSP_FACTOR_TPB * GS * 8;   // bytes a band of a stage
+  auto prefetch = [&](int64_t sg, int buf) {      // group sg of the walk(s)
+    if (!PFON) return;
+    if (COOP) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (G * ((int)sg + 1) <= qlen[q]) {
+          const double* g = bands + qrs[q] + (int64_t)G * sg;
+#pragma unroll
+          for (int o = 0; o < NB; ++o) {
+            const uint32_t sa = qsa[q] + (uint32_t)(buf * NB + o) * kStageB;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g + (int64_t)o * n) : "memory");
+          }
+        }
+      }
+    } else {
+      const int64_t i0 = rs + (int64_t)G * sg;
+      if (vec && i0 + 4 <= r1) {
+#pragma unroll
+        for (int o = 0; o < NB; ++o) {
+          const double* g = bands + (int64_t)o * n + i0;
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pf_of(buf, o, threadIdx.x));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16), "l"(g + 2) : "memory");
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");   // (possibly empty: keeps the count)
   };
+  // COOP: the LU rows of the warp's staged, live groups from the stage to HBM (coalesced)
+  auto store_group = [&](int64_t sg, int buf) {
 #pragma unroll
-  for (int q = 0; q < kPF - 1; ++q) prefetch(rs + 4 * q, q);
-  int buf = 0;
-  for (int64_t i0 = rs; i0 < r1; i0 += 4) {
-    const bool live = i0 >= r0;                 // warm-up rows: state only
-    if (warm > 0 && first_pass && c > 0 && i0 == r0) {
-#pragma unroll
-      for (int q = 0; q < D; ++q)
-#pragma unroll
-        for (int e = 0; e <= D; ++e) st_start[c * W + q * (D + 1) + e] = Uw[q][e];
-    }
-    const int nr = (r1 - i0) < 4 ? (int)(r1 - i0) : 4;
-    double bb[NB][4];
-    if (PFON) asm volatile("cp.async.wait_group %0;" ::"n"(kPF - 2) : "memory");   // this group landed
-    if (PFON && vec && nr == 4) {
-#pragma unroll
-      for (int o = 0; o < NB; ++o) {
-        const double2 lo = *reinterpret_cast<const double2*>(pf_at(buf, o));
-        const double2 hi = *reinterpret_cast<const double2*>(pf_at(buf, o) + 2);
-        bb[o][0] = lo.x; bb[o][1] = lo.y; bb[o][2] = hi.x; bb[o][3] = hi.y;
-      }
-    } else if (vec && nr == 4) {
-#pragma unroll
-      for (int o = 0; o < NB; ++o) {
-        const double2 lo = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0));
-        const double2 hi = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0 + 2));
-        bb[o][0] = lo.x; bb[o][1] = lo.y; bb[o][2] = hi.x; bb[o][3] = hi.y;
-      }
-    } else {
-#pragma unroll
-      for (int o = 0; o < NB; ++o)
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
-    }
-    prefetch(i0 + 4 * (kPF - 1), buf == 0 ? kPF - 1 : buf - 1);   // into the slot read last group
-    buf = (buf + 1 == kPF) ? 0 : buf + 1;
-    // results overwrite the consumed band values of their row (bb doubles as the output tile).
-    // Groups whose rows all have a full window (no matrix / chunk start within D rows, no matrix
-    // end within D rows) take the check-free copy of the row step.
-    const bool full = (i0 - D >= lo) && (i0 + 3 + D < n || has_next);
-    auto step = [&](auto chk) {
-      constexpr bool C = decltype(chk)::value;
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        if (rr >= nr) break;
-        const int64_t i = i0 + rr;
-        double Lr[D];       // L(i, i-D+q), q = 0..D-1
-        double Ur[D + 1];   // U(i, i+e)
-        // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D (compile-time after
-        // unrolling).  Rows before the matrix start (or before the walk start of a zero-state
-        // walk) do not exist.
-        auto row_exists = [&](int q) -> bool {
-          if (!C) return true;
-          const int64_t k = i - D + q;
-          return (k >= 0 || has_prev) && !(at_start && k < rs);
-        };
-#pragma unroll
-        for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
-          if (!row_exists(q)) { Lr[q] = 0.0; continue; }
-          double sum = bb[q][rr];                 // N(i,j), band o = j-i+D = q
-#pragma unroll
-          for (int p = 0; p < q; ++p)           // U(k, j), k = i-D+p: window entry e = q - p
-            if (row_exists(p)) sum -= Lr[p] * Uw[p][q - p];
-          Lr[q] = sum * Ri[q];                  // / U(j,j), by its reciprocal
-        }
-#pragma unroll
-        for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
-          if (C && i + e >= n && !has_next) { Ur[e] = 0.0; continue; }
-          double sum = bb[D + e][rr];
-#pragma unroll
-          for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]: window entry D - p + e
-            if (p >= e && row_exists(p)) sum -= Lr[p] * Uw[p][D - p + e];
-          Ur[e] = sum;
-        }
-        if (live && !(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-          if (live && !(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
-          bb[q][rr] = Lr[q];
-        }
-#pragma unroll
-        for (int e = 0; e <= D; ++e) {
-          if (live && !(fabs(Ur[e]) <= 1e100)) isbad = 1;
-          bb[D + e][rr] = Ur[e];
-        }
-        // shift the window (and the pivot reciprocals: one division per row)
-#pragma unroll
-        for (int q = 0; q < D - 1; ++q) {
-#pragma unroll
-          for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
-          Ri[q] = Ri[q + 1];
-        }
-#pragma unroll
-        for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
-        Ri[D - 1] = 1.0 / Ur[0];
-      }
-    };
-    if (full) step(std::false_type{});
-    else step(std::true_type{});
-    if (WRITE && live) {
-      if (vec && nr == 4) {
+    for (int q = 0; q < 4; ++q) {
+      if (G * ((int)sg + 1) <= qlen[q] && G * (int)sg >= qoff[q]) {
+        double* g = lu + qrs[q] + (int64_t)G * sg;
 #pragma unroll
         for (int o = 0; o < NB; ++o) {
-          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0) = make_double2(bb[o][0], bb[o][1]);
-          *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0 + 2) = make_double2(bb[o][2], bb[o][3]);
+          double2 v;
+          const uint32_t sa = qsa[q] + (uint32_t)(buf * NB + o) * kStageB;
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(sa));
+          *reinterpret_cast<double2*>(g + (int64_t)o * n) = v;
+        }
+      }
+    }
+  };
+  int itmax = valid ? (int)((r1 - rs + 3) / 4) : 0;   // walk steps of four rows
+  if (COOP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) itmax = max(itmax, __shfl_xor_sync(0xffffffffu, itmax, o));
+  }
+#pragma unroll
+  for (int q = 0; q < kPF - 1; ++q) prefetch(q, q);
+  int buf = 0;
+  for (int it = 0; it < itmax; ++it) {
+    const int h = COOP ? (it & 1) : 0;            // walk step within the staged group
+    const int64_t sg = COOP ? (it >> 1) : it;     // staged group
+    const int64_t i0 = rs + 4 * (int64_t)it;
+    if (h == 0) {
+      if (PFON) asm volatile("cp.async.wait_group %0;" ::"n"(kPF - 2) : "memory");   // group sg landed
+      if (COOP) __syncwarp();                     // (copied by the other lanes)
+      prefetch(sg + kPF - 1, buf == 0 ? kPF - 1 : buf - 1);   // into the slot read last group
+    }
+    if (valid && i0 < r1) {
+      const bool live = i0 >= r0;                 // warm-up rows: state only
+      if (warm > 0 && first_pass && c > 0 && i0 == r0) {
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+#pragma unroll
+          for (int e = 0; e <= D; ++e) st_start[c * W + q * (D + 1) + e] = Uw[q][e];
+      }
+      const int nr = (r1 - i0) < 4 ? (int)(r1 - i0) : 4;
+      // staged: COOP the whole group of eight (rows rs + 8 sg ..), else this step's four rows
+      const bool staged = PFON && vec && (COOP ? (rs + (int64_t)G * sg + G <= r1) : (nr == 4));
+      double bb[NB][4];
+      if (staged) {
+#pragma unroll
+        for (int o = 0; o < NB; ++o) {
+          const double* sp = pf_of(buf, o, threadIdx.x) + 4 * h;
+          const double2 a = *reinterpret_cast<const double2*>(sp);
+          const double2 b = *reinterpret_cast<const double2*>(sp + 2);
+          bb[o][0] = a.x; bb[o][1] = a.y; bb[o][2] = b.x; bb[o][3] = b.y;
+        }
+      } else if (vec && nr == 4) {
+#pragma unroll
+        for (int o = 0; o < NB; ++o) {
+          const double2 a = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0));
+          const double2 b = __ldg(reinterpret_cast<const double2*>(bands + (int64_t)o * n + i0 + 2));
+          bb[o][0] = a.x; bb[o][1] = a.y; bb[o][2] = b.x; bb[o][3] = b.y;
         }
       } else {
 #pragma unroll
         for (int o = 0; o < NB; ++o)
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr)
-            if (rr < nr) lu[(int64_t)o * n + i0 + rr] = bb[o][rr];
+          for (int rr = 0; rr < 4; ++rr) bb[o][rr] = (rr < nr) ? __ldg(bands + (int64_t)o * n + i0 + rr) : 0.0;
+      }
+      // results overwrite the consumed band values of their row (bb doubles as the output tile).
+      // Steps whose rows all have a full window (no matrix / chunk start within D rows, no matrix
+      // end within D rows) take the check-free copy of the row step.
+      const bool full = (i0 - D >= lo) && (i0 + 3 + D < n || has_next);
+      auto step = [&](auto chk) {
+        constexpr bool C = decltype(chk)::value;
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          if (rr >= nr) break;
+          const int64_t i = i0 + rr;
+          double Lr[D];       // L(i, i-D+q), q = 0..D-1
+          double Ur[D + 1];   // U(i, i+e)
+          // U(k, j) for window row k = i-D+q: Uw[q][j-k] when 0 <= j-k <= D (compile-time after
+          // unrolling).  Rows before the matrix start (or before the walk start of a zero-state
+          // walk) do not exist.
+          auto row_exists = [&](int q) -> bool {
+            if (!C) return true;
+            const int64_t k = i - D + q;
+            return (k >= 0 || has_prev) && !(at_start && k < rs);
+          };
+#pragma unroll
+          for (int q = 0; q < D; ++q) {           // L(i,j), j = i-D+q  (ascending j)
+            if (!row_exists(q)) { Lr[q] = 0.0; continue; }
+            double sum = bb[q][rr];                 // N(i,j), band o = j-i+D = q
+#pragma unroll
+            for (int p = 0; p < q; ++p)           // U(k, j), k = i-D+p: window entry e = q - p
+              if (row_exists(p)) sum -= Lr[p] * Uw[p][q - p];
+            Lr[q] = sum * Ri[q];                  // / U(j,j), by its reciprocal
+          }
+#pragma unroll
+          for (int e = 0; e <= D; ++e) {          // U(i,j), j = i+e
+            if (C && i + e >= n && !has_next) { Ur[e] = 0.0; continue; }
+            double sum = bb[D + e][rr];
+#pragma unroll
+            for (int p = 0; p < D; ++p)           // k = i-D+p in [j-D, i-1]: window entry D - p + e
+              if (p >= e && row_exists(p)) sum -= Lr[p] * Uw[p][D - p + e];
+            Ur[e] = sum;
+          }
+          if (live && !(fabs(Ur[0]) >= 1e-300)) isbad = 1;   // S:272 (also catches NaN)
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            if (live && !(fabs(Lr[q]) <= 1e100)) isbad = 1;  // S:293 growth / non-finite
+            bb[q][rr] = Lr[q];
+          }
+#pragma unroll
+          for (int e = 0; e <= D; ++e) {
+            if (live && !(fabs(Ur[e]) <= 1e100)) isbad = 1;
+            bb[D + e][rr] = Ur[e];
+          }
+          // shift the window (and the pivot reciprocals: one division per row)
+#pragma unroll
+          for (int q = 0; q < D - 1; ++q) {
+#pragma unroll
+            for (int e = 0; e <= D; ++e) Uw[q][e] = Uw[q + 1][e];
+            Ri[q] = Ri[q + 1];
+          }
+#pragma unroll
+          for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
+          Ri[D - 1] = 1.0 / Ur[0];
+        }
+      };
+      if (full) step(std::false_type{});
+      else step(std::true_type{});
+      if (WRITE && live) {
+        if (COOP && staged) {                     // back into the stage: store_group writes it out
+#pragma unroll
+          for (int o = 0; o < NB; ++o) {
+            double* sp = pf_of(buf, o, threadIdx.x) + 4 * h;
+            *reinterpret_cast<double2*>(sp) = make_double2(bb[o][0], bb[o][1]);
+            *reinterpret_cast<double2*>(sp + 2) = make_double2(bb[o][2], bb[o][3]);
+          }
+        } else if (vec && nr == 4) {
+#pragma unroll
+          for (int o = 0; o < NB; ++o) {
+            *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0) = make_double2(bb[o][0], bb[o][1]);
+            *reinterpret_cast<double2*>(lu + (int64_t)o * n + i0 + 2) = make_double2(bb[o][2], bb[o][3]);
+          }
+        } else {
+#pragma unroll
+          for (int o = 0; o < NB; ++o)
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr)
+              if (rr < nr) lu[(int64_t)o * n + i0 + rr] = bb[o][rr];
+        }
       }
     }
+    if (h == G / 4 - 1) {                         // end of the staged group
+      if (COOP && WRITE) {
+        __syncwarp();
+        store_group(sg, buf);
+        __syncwarp();                             // stage read before the next prefetch into it
+      }
+      buf = (buf + 1 == kPF) ? 0 : buf + 1;
+    }
   }
+  if (!valid) return;
   double* so = st_out + c * W;
   bool diff = first_pass != 0;
 #pragma unroll
@@ -1005,23 +1110,35 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
                    int first, int* changed, int* bad, const double* prev, int has_prev, int has_next,
                    cudaStream_t s, bool write, int warm = 0, double* st_start = nullptr) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  const int tpb = 64;
+  const int tpb = PSP_FACTOR_TPB;
   const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
+  static const bool no_coop = getenv("PSP_FACTOR_NOCOOP") != nullptr;   // A/B: per-thread copies
+  const bool coop = D <= 3 && vec && !no_coop;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
-  const size_t smem = D <= 3 ? (size_t)kPF * (2 * D + 1) * tpb * 4 * 8 : 0;
+  const size_t smem = D <= 3 ? (size_t)kPF * (2 * D + 1) * tpb * (coop ? 10 : 4) * 8 : 0;
   thread_local bool attr[kMaxDev] = {};
   const int dev = device_ordinal();
   if (!attr[dev]) {
-    cudaFuncSetAttribute(factor_pass_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(factor_pass_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int s4 = D <= 3 ? kPF * (2 * D + 1) * tpb * 4 * 8 : 0, s8 = s4 * 10 / 4;
+    cudaFuncSetAttribute(factor_pass_kernel<D, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
+    cudaFuncSetAttribute(factor_pass_kernel<D, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
+    if (D <= 3) {
+      cudaFuncSetAttribute(factor_pass_kernel<D, true, (D <= 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
+      cudaFuncSetAttribute(factor_pass_kernel<D, false, (D <= 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
+    }
     attr[dev] = true;
   }
-  if (write)
-    factor_pass_kernel<D, true><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
-                                                     has_next, vec, warm, st_start);
-  else
-    factor_pass_kernel<D, false><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, has_prev,
-                                                      has_next, vec, warm, st_start);
+#define PSP_FACTOR_GO(WR, CO)                                                                      \
+  factor_pass_kernel<D, WR, CO><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, \
+                                                        has_prev, has_next, vec, warm, st_start)
+  if (coop) {
+    if (write) PSP_FACTOR_GO(true, (D <= 3));
+    else PSP_FACTOR_GO(false, (D <= 3));
+  } else {
+    if (write) PSP_FACTOR_GO(true, false);
+    else PSP_FACTOR_GO(false, false);
+  }
+#undef PSP_FACTOR_GO
 }
 
 // phase 0: the whole sweep; 1: map (zero-state rows written to out) + scan (s_out = the state after
