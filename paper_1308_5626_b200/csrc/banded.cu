@@ -39,10 +39,16 @@ constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first p
 #ifndef PSP_FACTOR_PF
 #define PSP_FACTOR_PF 3
 #endif
+#ifndef PSP_FACTOR_PFMAXD
+#define PSP_FACTOR_PFMAXD 4
+#endif
 #ifndef PSP_FACTOR_TPB
 #define PSP_FACTOR_TPB 64
 #endif
-constexpr int kPF = PSP_FACTOR_PF; // factor: prefetch ring depth (staged groups)
+// factor: prefetch ring depth (staged groups); d = 4 takes two (its nine bands a stage: three
+// stages would leave one 64-thread block an SM; n = 2^26: 4.2 -> 2.9 ms with the ring)
+template <int D>
+constexpr int kPFd = D >= 4 ? 2 : PSP_FACTOR_PF;
 // solve sweeps: 256-thread blocks (2 per SM) for d <= 2; 128-thread blocks for d >= 3, 4 per SM
 // at d = 3 and 3 per SM at d = 4 (more independent tiles in flight; measured n = 2^26: d = 3
 // 2.34 -> 2.04 ms, d = 4 4.25 -> 3.65 ms; d = 1 prefers 256)
@@ -84,7 +90,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   // of this block (rows of rank-1 / rank+1), so the band entries reaching there are real
   constexpr int W = D * (D + 1);  // last D rows of U: Uw[q][e] = U(r0-D+q, r0-D+q+e)
   constexpr int NB = 2 * D + 1;
-  constexpr bool PFON = D <= 3;   // d = 4: the ring's shared memory costs more occupancy than it saves
+  constexpr bool PFON = D <= PSP_FACTOR_PFMAXD;   // the cp.async ring (every d by default)
   static_assert(!COOP || PFON, "cooperative staging uses the prefetch ring");
   constexpr int G = COOP ? 8 : 4; // rows a staged group (COOP: two walk steps of four rows)
   static_assert(kWarm % 8 == 0, "warm-up rows: whole groups");
@@ -209,6 +215,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
     for (int o = 16; o > 0; o >>= 1) itmax = max(itmax, __shfl_xor_sync(0xffffffffu, itmax, o));
   }
 #pragma unroll
+  constexpr int kPF = kPFd<D>;
   for (int q = 0; q < kPF - 1; ++q) prefetch(q, q);
   int buf = 0;
   for (int it = 0; it < itmax; ++it) {
@@ -858,12 +865,24 @@ __global__ void __launch_bounds__(SW<D>::TPB, SW<D>::MINB) tile_apply_kernel(con
 // by the last lane in processing order (its inclusive map is the tile's), and the state carried
 // to the next warp-tile is broadcast from that lane.
 // ---------------------------------------------------------------------------------------
-constexpr int WSR = 8;            // rows a lane
-constexpr int WT = 32 * WSR;      // rows a warp-tile
+// rows a lane: 6 for d = 2, 3 (measured n = 2^26: d = 3 1.45 -> 1.40 ms, d = 2 0.89 -> 0.86 ms
+// against 8; 4 is slower everywhere), 8 for d = 1 (0.63 vs 0.68 ms) and d = 4
+template <int D>
+struct WS {
+#ifdef PSP_WSWEEP_SR
+  static constexpr int SR = PSP_WSWEEP_SR;
+#else
+  static constexpr int SR = (D == 2 || D == 3) ? 6 : 8;
+#endif
+  static constexpr int T = 32 * SR;   // rows a warp-tile
+};
 constexpr int WWPB = 4;           // warps a block (independent ranges)
 constexpr int NRMAX = 4096;       // ranges a sweep (scan capacity: 4 maps a scan thread)
 #ifndef PSP_WSWEEP_RELOAD
 #define PSP_WSWEEP_RELOAD 0       // 1: reload a lane's rows for the final walk instead of holding them
+#endif
+#ifndef PSP_WSWEEP_PF
+#define PSP_WSWEEP_PF 1           // L2 bulk prefetch distance in warp-tiles (0: none)
 #endif
 #ifndef PSP_WSWEEP_MINB
 #define PSP_WSWEEP_MINB 1         // resident blocks per SM asked of the register allocator
@@ -892,6 +911,7 @@ __global__ void __launch_bounds__(32 * WWPB, PSP_WSWEEP_MINB) wsweep_kernel(cons
                                                            double* __restrict__ rmap,
                                                            const double* __restrict__ full, int vec) {
   constexpr int DW = D * D + 2 * D;
+  constexpr int WSR = WS<D>::SR, WT = WS<D>::T;
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * WWPB + (threadIdx.x >> 5);
   if (r >= nr) return;                               // warp-uniform
@@ -908,6 +928,18 @@ __global__ void __launch_bounds__(32 * WWPB, PSP_WSWEEP_MINB) wsweep_kernel(cons
     const int64_t tile = FWD ? p : ntiles - 1 - p;
     const int64_t rb = tile * WT + (int64_t)lane * WSR;   // this lane's first row
     const bool whole = rb + WSR <= n;
+    if (PSP_WSWEEP_PF > 0 && vec && p + PSP_WSWEEP_PF < p1 && lane < 2 + D) {
+      // the rows of the warp-tile PSP_WSWEEP_PF ahead into L2 (one bulk prefetch per array), so
+      // its loads do not wait a full DRAM latency after the scans before it
+      const int64_t nb0 = (FWD ? tile + PSP_WSWEEP_PF : tile - PSP_WSWEEP_PF) * WT;
+      if (nb0 + WT <= n) {
+        const double* a = lane == 0 ? vin
+                        : lane <= D ? lu + (int64_t)(FWD ? (D - lane) : (D + lane)) * n
+                                    : lu + (int64_t)D * n;
+        if (a != nullptr && (FWD ? lane <= D : true))
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + nb0), "r"((unsigned)(WT * 8)) : "memory");
+      }
+    }
     double vv[WSR], cc[D][WSR], uu[WSR];
     auto load_rows = [&]() {
       if (vec && whole) {
@@ -1113,18 +1145,19 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
   const int tpb = PSP_FACTOR_TPB;
   const int vec = (n % 2 == 0) && (((uintptr_t)bands | (uintptr_t)lu) & 15) == 0;
   static const bool no_coop = getenv("PSP_FACTOR_NOCOOP") != nullptr;   // A/B: per-thread copies
-  const bool coop = D <= 3 && vec && !no_coop;
+  const bool coop = D <= PSP_FACTOR_PFMAXD && vec && !no_coop;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
-  const size_t smem = D <= 3 ? (size_t)kPF * (2 * D + 1) * tpb * (coop ? 10 : 4) * 8 : 0;
+  constexpr int kPF = kPFd<D>;
+  const size_t smem = D <= PSP_FACTOR_PFMAXD ? (size_t)kPF * (2 * D + 1) * tpb * (coop ? 10 : 4) * 8 : 0;
   thread_local bool attr[kMaxDev] = {};
   const int dev = device_ordinal();
   if (!attr[dev]) {
-    const int s4 = D <= 3 ? kPF * (2 * D + 1) * tpb * 4 * 8 : 0, s8 = s4 * 10 / 4;
+    const int s4 = D <= PSP_FACTOR_PFMAXD ? kPF * (2 * D + 1) * tpb * 4 * 8 : 0, s8 = s4 * 10 / 4;
     cudaFuncSetAttribute(factor_pass_kernel<D, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
     cudaFuncSetAttribute(factor_pass_kernel<D, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
-    if (D <= 3) {
-      cudaFuncSetAttribute(factor_pass_kernel<D, true, (D <= 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
-      cudaFuncSetAttribute(factor_pass_kernel<D, false, (D <= 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
+    if (D <= PSP_FACTOR_PFMAXD) {
+      cudaFuncSetAttribute(factor_pass_kernel<D, true, (D <= PSP_FACTOR_PFMAXD)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
+      cudaFuncSetAttribute(factor_pass_kernel<D, false, (D <= PSP_FACTOR_PFMAXD)>, cudaFuncAttributeMaxDynamicSharedMemorySize, s8);
     }
     attr[dev] = true;
   }
@@ -1132,8 +1165,8 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
   factor_pass_kernel<D, WR, CO><<<grid, tpb, smem, s>>>(bands, n, lu, a, b, first, changed, bad, prev, \
                                                         has_prev, has_next, vec, warm, st_start)
   if (coop) {
-    if (write) PSP_FACTOR_GO(true, (D <= 3));
-    else PSP_FACTOR_GO(false, (D <= 3));
+    if (write) PSP_FACTOR_GO(true, (D <= PSP_FACTOR_PFMAXD));
+    else PSP_FACTOR_GO(false, (D <= PSP_FACTOR_PFMAXD));
   } else {
     if (write) PSP_FACTOR_GO(true, false);
     else PSP_FACTOR_GO(false, false);
@@ -1168,6 +1201,7 @@ void sweep_launch(const double* lu, int64_t n, const double* v, const double* vs
   static const bool block_sweeps = getenv("PSP_SOLVE_BLOCK") != nullptr;   // A/B: the tile kernels
   if (!block_sweeps) {
     // one range per resident warp (one wave), at most NRMAX
+    constexpr int WT = WS<D>::T;
     const int64_t ntiles = (n + WT - 1) / WT;
     int64_t nr = (int64_t)device_sms() * wblocks[dev] * WWPB;
     if (nr > NRMAX) nr = NRMAX;
