@@ -455,6 +455,21 @@ __device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], dou
 // backward per row, plus the short corrections), with no look-back chain: a single-pass
 // chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
 
+// 1 / U(i,i) for the warp-range sweeps and their corrections: the hardware approximation and two
+// Newton steps (within an ulp; unlike '/', no out-of-line special-case path -- a gated pivot is
+// a normal number), PSP_WSWEEP_FASTRCP = 0: the IEEE division.  Measured n = 2^26: d = 1 0.63 ->
+// 0.61 ms, d = 3 1.40 -> 1.34 ms, d = 4 2.21 -> 2.15 ms.
+#ifndef PSP_WSWEEP_FASTRCP
+#define PSP_WSWEEP_FASTRCP 1
+#endif
+__device__ __forceinline__ double recip_pivot(double u) {
+  if (!PSP_WSWEEP_FASTRCP) return 1.0 / u;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  r = fma(r, fma(-u, r, 1.0), r);
+  return fma(r, fma(-u, r, 1.0), r);
+}
+
 // One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
 //                        BWD: z = (v - sum_k c[k] s[k]) / U(i,i) (c[k] = U(i,i+k+1), s[k] = z_{i+k+1}),
 // evaluated with ui = 1 / U(i,i) formed once per row (the D unit-state runs of a tile map share
@@ -729,7 +744,7 @@ __global__ void tile_fix_kernel(const double* __restrict__ lu, int64_t n, int64_
         const int o = FWD ? (D - 1 - k) : (D + 1 + k);
         c8[e][k] = ok ? __ldg(lu + (int64_t)o * n + idx[e]) : 0.0;
       }
-      u8[e] = (!FWD && ok) ? 1.0 / __ldg(lu + (int64_t)D * n + idx[e]) : 1.0;   // reciprocal pivot
+      u8[e] = (!FWD && ok) ? recip_pivot(__ldg(lu + (int64_t)D * n + idx[e])) : 1.0;   // reciprocal pivot
       o8[e] = ok ? out[idx[e]] : 0.0;
     }
 #pragma unroll
@@ -884,6 +899,9 @@ constexpr int NRMAX = 4096;       // ranges a sweep (scan capacity: 4 maps a sca
 #ifndef PSP_WSWEEP_PF
 #define PSP_WSWEEP_PF 1           // L2 bulk prefetch distance in warp-tiles (0: none)
 #endif
+#ifndef PSP_WSWEEP_BMINB
+#define PSP_WSWEEP_BMINB 3        // blocks per SM asked of the d = 3 backward sweep (202 -> 166
+#endif                            // registers, no spills: n = 2^26 1.34 -> 1.23 ms)
 #ifndef PSP_WSWEEP_MINB
 #define PSP_WSWEEP_MINB 1         // resident blocks per SM asked of the register allocator
 #endif
@@ -905,7 +923,7 @@ __device__ __forceinline__ Map<D> shfl_scan_src(const Map<D>& m, int off) {
 //                and the range map (M, t) into rmap.
 // APPLY = true:  re-walk, from the exact incoming state in rmap, only the ranges flagged in full.
 template <bool FWD, int D, bool APPLY>
-__global__ void __launch_bounds__(32 * WWPB, PSP_WSWEEP_MINB) wsweep_kernel(const double* __restrict__ lu, int64_t n,
+__global__ void __launch_bounds__(32 * WWPB, (!FWD && D == 3) ? PSP_WSWEEP_BMINB : PSP_WSWEEP_MINB) wsweep_kernel(const double* __restrict__ lu, int64_t n,
                                                            const double* __restrict__ vin, const double* vscale,
                                                            const double* addend, double* out, int64_t L, int nr,
                                                            double* __restrict__ rmap,
@@ -978,7 +996,7 @@ __global__ void __launch_bounds__(32 * WWPB, PSP_WSWEEP_MINB) wsweep_kernel(cons
       }
       if (!FWD) {
 #pragma unroll
-        for (int q = 0; q < WSR; ++q) uu[q] = 1.0 / uu[q];   // the reciprocal pivot, once a row
+        for (int q = 0; q < WSR; ++q) uu[q] = recip_pivot(uu[q]);   // once a row
       }
     };
     load_rows();

@@ -16,5 +16,7 @@ python tools/kbench.py solve 26 3 3 > $O/kbench_solve3.txt 2>&1 || exit 1
 run factor_d3 factor_pass 0 1 python tools/kbench.py solve 26 3 3
 run wsweep_d3 wsweep 0 4 python tools/kbench.py solve 26 3 3
 run wsweep_d1 wsweep 0 2 python tools/kbench.py solve 26 1 3
+run factor_d1 factor_pass 0 1 python tools/kbench.py solve 26 1 3
+run factor_d4 factor_pass 0 1 python tools/kbench.py solve 26 4 3
 ${PROF_EXTRA:-true}
 du -sh $O; ls $O
