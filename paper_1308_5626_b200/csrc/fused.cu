@@ -746,9 +746,15 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     // k <= 8: two points a thread on the tallest tiles whose stage ring still holds three
     // stages (32 x 30 at KMAX 4, 32 x 22 at KMAX 8): less halo work per point, same warps
     // (k = 2: 2.1 -> 1.97 ms, k = 5..8: 2.8-2.9 -> 2.6 ms at 512^3)
+    // Odd widths in between (KMAX 6 / 10 / 14): a pass computes KMAX columns (the ones past kc
+    // are zero), so a step of width kc runs at most one idle column instead of up to three
+    const bool coarse = getenv("PSP_FUSED_COARSE") != nullptr;   // A/B knob (read per launch): KMAX 4/8/12/16 only
     if (kc <= 4) return launch_t<KIND, 32, 30, 4, 1, 2>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 6 && !coarse) return launch_t<KIND, 32, 22, 6, 1, 2>(a, rpx, rpy, fld, ld, s);
     if (kc <= 8) return launch_t<KIND, 32, 22, 8, 1, 2>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 10 && !coarse) return launch_t<KIND, 32, 15, 10, 1>(a, rpx, rpy, fld, ld, s);
     if (kc <= 12) return launch_t<KIND, 32, 15, 12, 1>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 14 && !coarse) return launch_t<KIND, 32, 14, 14, 1, 2>(a, rpx, rpy, fld, ld, s);
     // k = 13..16: 32 x 14 tiles with two points a thread (8 compute warps, up to 255 registers)
     // hold a thread's 16 basis values per point in registers, so a stage is released as soon as
     // u is formed; one thread per point on 32 x 15 tiles would keep two stages resident, on
