@@ -39,6 +39,9 @@ constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first p
 #ifndef PSP_FACTOR_PF
 #define PSP_FACTOR_PF 3
 #endif
+#ifndef PSP_FACTOR_FASTRCP
+#define PSP_FACTOR_FASTRCP 1   // factor: the pivot reciprocal by rcp.approx + Newton (recip_pivot)
+#endif
 #ifndef PSP_FACTOR_PFMAXD
 #define PSP_FACTOR_PFMAXD 4
 #endif
@@ -65,6 +68,21 @@ struct SW {
 constexpr int STPB = 128;        // solve: the smallest block (host-side sizing of per-tile arrays)
 constexpr int STILE = STPB * SR; // solve: rows per tile
 constexpr int SPAD = SR + 1;     // padded row stride in shared memory (bank conflicts)
+
+// 1 / U(i,i) for the warp-range sweeps and their corrections: the hardware approximation and two
+// Newton steps (within an ulp; unlike '/', no out-of-line special-case path -- a gated pivot is
+// a normal number), PSP_WSWEEP_FASTRCP = 0: the IEEE division.  Measured n = 2^26: d = 1 0.63 ->
+// 0.61 ms, d = 3 1.40 -> 1.34 ms, d = 4 2.21 -> 2.15 ms.
+#ifndef PSP_WSWEEP_FASTRCP
+#define PSP_WSWEEP_FASTRCP 1
+#endif
+__device__ __forceinline__ double recip_pivot(double u) {
+  if (!PSP_WSWEEP_FASTRCP) return 1.0 / u;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  r = fma(r, fma(-u, r, 1.0), r);
+  return fma(r, fma(-u, r, 1.0), r);
+}
 
 // ---------------------------------------------------------------------------------------
 // Factorisation pass
@@ -133,7 +151,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   const int64_t lo = at_start ? rs : (has_prev ? INT64_MIN / 2 : 0);
   double Ri[D];       // 1 / U(k,k) of the window rows (unused for rows that do not exist)
 #pragma unroll
-  for (int q = 0; q < D; ++q) Ri[q] = 1.0 / Uw[q][0];
+  for (int q = 0; q < D; ++q) Ri[q] = PSP_FACTOR_FASTRCP ? recip_pivot(Uw[q][0]) : 1.0 / Uw[q][0];
   int isbad = 0;
   // the bands of the next groups are prefetched into a PF-deep shared-memory ring by cp.async
   // (16-byte copies, no registers held): a walk is a serial recurrence, and without the prefetch
@@ -318,7 +336,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
           }
 #pragma unroll
           for (int e = 0; e <= D; ++e) Uw[D - 1][e] = Ur[e];
-          Ri[D - 1] = 1.0 / Ur[0];
+          Ri[D - 1] = PSP_FACTOR_FASTRCP ? recip_pivot(Ur[0]) : 1.0 / Ur[0];
         }
       };
       if (full) step(std::false_type{});
@@ -454,21 +472,6 @@ __device__ __forceinline__ void apply(const Map<D>& m, const double (&s)[D], dou
 // So the coefficients and the right-hand side are read about once (8(d+2) forward, 8(d+3)
 // backward per row, plus the short corrections), with no look-back chain: a single-pass
 // chained scan over 2^16 tiles was latency-bound at ~1/4 of these rates.
-
-// 1 / U(i,i) for the warp-range sweeps and their corrections: the hardware approximation and two
-// Newton steps (within an ulp; unlike '/', no out-of-line special-case path -- a gated pivot is
-// a normal number), PSP_WSWEEP_FASTRCP = 0: the IEEE division.  Measured n = 2^26: d = 1 0.63 ->
-// 0.61 ms, d = 3 1.40 -> 1.34 ms, d = 4 2.21 -> 2.15 ms.
-#ifndef PSP_WSWEEP_FASTRCP
-#define PSP_WSWEEP_FASTRCP 1
-#endif
-__device__ __forceinline__ double recip_pivot(double u) {
-  if (!PSP_WSWEEP_FASTRCP) return 1.0 / u;
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
-  r = fma(r, fma(-u, r, 1.0), r);
-  return fma(r, fma(-u, r, 1.0), r);
-}
 
 // One recurrence step.  FWD: y = v - sum_k c[k] s[k]   (c[k] = L(i,i-k-1), s[k] = y_{i-k-1})
 //                        BWD: z = (v - sum_k c[k] s[k]) / U(i,i) (c[k] = U(i,i+k+1), s[k] = z_{i+k+1}),
