@@ -42,6 +42,9 @@ constexpr int kWarm = 64;        // factor: warm-up rows before a chunk (first p
 #ifndef PSP_FACTOR_FASTRCP
 #define PSP_FACTOR_FASTRCP 1   // factor: the pivot reciprocal by rcp.approx + Newton (recip_pivot)
 #endif
+#ifndef PSP_FACTOR_G
+#define PSP_FACTOR_G 8     // factor (cooperative staging): rows a staged group (4 or 8)
+#endif
 #ifndef PSP_FACTOR_PFMAXD
 #define PSP_FACTOR_PFMAXD 4
 #endif
@@ -110,7 +113,9 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   constexpr int NB = 2 * D + 1;
   constexpr bool PFON = D <= PSP_FACTOR_PFMAXD;   // the cp.async ring (every d by default)
   static_assert(!COOP || PFON, "cooperative staging uses the prefetch ring");
-  constexpr int G = COOP ? 8 : 4; // rows a staged group (COOP: two walk steps of four rows)
+  constexpr int G = COOP ? PSP_FACTOR_G : 4;   // rows a staged group (COOP 8: two walk steps of four rows)
+  constexpr int NPC = G / 2;       // COOP: 16-byte pieces of a chunk's group in one band
+  constexpr int CPI = 32 / NPC;    // COOP: chunks one warp-wide copy instruction covers
   static_assert(kWarm % 8 == 0, "warm-up rows: whole groups");
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -163,23 +168,23 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   auto pf_of = [&](int buf, int o, int t) -> double* {
     return pf + ((size_t)(buf * NB + o) * PSP_FACTOR_TPB + t) * GS;
   };
-  // COOP: the four chunks this lane copies for (cl = 8q + lane/4, piece lane & 3): walk start,
+  // COOP: the NPC chunks this lane copies for (cl = CPI q + lane / NPC, piece lane % NPC): walk start,
   // rows of the walk, and the first live row, relative to the walk start
-  int64_t qrs[COOP ? 4 : 1];
-  int qlen[COOP ? 4 : 1], qoff[COOP ? 4 : 1];
-  uint32_t qsa[COOP ? 4 : 1];
+  int64_t qrs[COOP ? NPC : 1];
+  int qlen[COOP ? NPC : 1], qoff[COOP ? NPC : 1];
+  uint32_t qsa[COOP ? NPC : 1];
   if (COOP) {
     const int64_t wbase = c - lane;               // chunk of lane 0 of this warp
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int cl = 8 * q + (lane >> 2);
+    for (int q = 0; q < NPC; ++q) {
+      const int cl = CPI * q + lane / NPC;
       int64_t r0c, r1c, rsc;
       geom(wbase + cl, r0c, r1c, rsc);
       const bool ex = wbase + cl < nchunks;
-      qrs[q] = rsc + 2 * (lane & 3);
+      qrs[q] = rsc + 2 * (lane % NPC);
       qlen[q] = ex ? (int)(r1c - rsc) : 0;
       qoff[q] = (int)(r0c - rsc);
-      qsa[q] = (uint32_t)__cvta_generic_to_shared(pf_of(0, 0, threadIdx.x - lane + cl) + 2 * (lane & 3));
+      qsa[q] = (uint32_t)__cvta_generic_to_shared(pf_of(0, 0, threadIdx.x - lane + cl) + 2 * (lane % NPC));
     }
   }
   constexpr uint32_t kStageB = (uint32_t)PSP_FACTOR_TPB * GS * 8;   // bytes a band of a stage
@@ -187,7 +192,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
     if (!PFON) return;
     if (COOP) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NPC; ++q) {
         if (G * ((int)sg + 1) <= qlen[q]) {
           const double* g = bands + qrs[q] + (int64_t)G * sg;
 #pragma unroll
@@ -214,7 +219,7 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   // COOP: the LU rows of the warp's staged, live groups from the stage to HBM (coalesced)
   auto store_group = [&](int64_t sg, int buf) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NPC; ++q) {
       if (G * ((int)sg + 1) <= qlen[q] && G * (int)sg >= qoff[q]) {
         double* g = lu + qrs[q] + (int64_t)G * sg;
 #pragma unroll
@@ -237,8 +242,8 @@ __global__ void factor_pass_kernel(const double* __restrict__ bands, int64_t n, 
   for (int q = 0; q < kPF - 1; ++q) prefetch(q, q);
   int buf = 0;
   for (int it = 0; it < itmax; ++it) {
-    const int h = COOP ? (it & 1) : 0;            // walk step within the staged group
-    const int64_t sg = COOP ? (it >> 1) : it;     // staged group
+    const int h = COOP ? (it % (G / 4)) : 0;      // walk step within the staged group
+    const int64_t sg = COOP ? (it / (G / 4)) : it; // staged group
     const int64_t i0 = rs + 4 * (int64_t)it;
     if (h == 0) {
       if (PFON) asm volatile("cp.async.wait_group %0;" ::"n"(kPF - 2) : "memory");   // group sg landed
@@ -1169,11 +1174,11 @@ void factor_launch(const double* bands, int64_t n, double* lu, const double* a, 
   const bool coop = D <= PSP_FACTOR_PFMAXD && vec && !no_coop;
   const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
   constexpr int kPF = kPFd<D>;
-  const size_t smem = D <= PSP_FACTOR_PFMAXD ? (size_t)kPF * (2 * D + 1) * tpb * (coop ? 10 : 4) * 8 : 0;
+  const size_t smem = D <= PSP_FACTOR_PFMAXD ? (size_t)kPF * (2 * D + 1) * tpb * (coop ? PSP_FACTOR_G + 2 : 4) * 8 : 0;
   thread_local bool attr[kMaxDev] = {};
   const int dev = device_ordinal();
   if (!attr[dev]) {
-    const int s4 = D <= PSP_FACTOR_PFMAXD ? kPF * (2 * D + 1) * tpb * 4 * 8 : 0, s8 = s4 * 10 / 4;
+    const int s4 = D <= PSP_FACTOR_PFMAXD ? kPF * (2 * D + 1) * tpb * 4 * 8 : 0, s8 = s4 * (PSP_FACTOR_G + 2) / 4;
     cudaFuncSetAttribute(factor_pass_kernel<D, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
     cudaFuncSetAttribute(factor_pass_kernel<D, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
     if (D <= PSP_FACTOR_PFMAXD) {
