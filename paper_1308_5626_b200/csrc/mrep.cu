@@ -404,6 +404,9 @@ constexpr int TT = 128;        // threads (= sum rows) per tile of the TMA kerne
 #ifndef PSP_MREP_SUMS_BPS
 #define PSP_MREP_SUMS_BPS 3   // streaming blocks per SM of a chunked split MREP (a fit block beside)
 #endif
+#ifndef PSP_MREP_LASTFULL
+#define PSP_MREP_LASTFULL 1  // the last chunk's fit kernel on the full grid
+#endif
 #ifndef PSP_MREP_FIT_MINB
 #define PSP_MREP_FIT_MINB 2   // resident blocks per SM of the split MREP's fit kernel
 #endif
@@ -882,7 +885,10 @@ void launch_tma(const TmaCols& tc, const double* scale, int m, int64_t n, int64_
       cudaEventRecord(ev[c], s);
       cudaStreamWaitEvent(s2, ev[c], 0);
       const int64_t rows = (t1 - t0) * E;
-      const int64_t g2max = K > 1 ? sms : sms * PSP_MREP_FIT_MINB;   // beside the sums: one block per SM
+      // beside the sums: one block per SM; the last chunk's fits run alone (no sums beside them):
+      // every resident block
+      const bool last = (c == K - 1) || (t1 >= ntile);
+      const int64_t g2max = (K > 1 && !(PSP_MREP_LASTFULL && last)) ? sms : sms * PSP_MREP_FIT_MINB;
       const int64_t g2 = (rows + TT - 1) / TT < g2max ? (rows + TT - 1) / TT : g2max;
       static const bool ldl = getenv("PSP_MREP_LDL") != nullptr;   // A/B knob (the LDL^T fit)
       if (ldl) mrep_fitsum_kernel<D, true><<<(int)g2, TT, 0, s2>>>(m, n, gN, grow0, R0c, R0c + rows, out, sc);
