@@ -3,23 +3,27 @@
 // unpivoted banded LU of N (Doolittle; for d = 1 the same operations as Thomas).
 //
 // Factorisation (a9, once per time step).  Doolittle's row recurrence is sequential: row i
-// needs the U rows i-d..i-1.  It is split into chunks of kChunk rows, one thread each, and
-// iterated to a fixed point: pass p recomputes every chunk from the last-d-U-rows state its
-// left neighbour produced in pass p-1 (chunk 0 starts from the matrix start).  After pass p,
-// chunks 0..p-1 are bitwise the sequential result; the iteration stops at the first pass in
-// which no chunk's outgoing state changed, which is then the sequential LU for every chunk.
-// Under the R21 gate (strict diagonal dominance) the Schur-complement recurrence contracts,
-// so 2-4 passes suffice; termination is guaranteed after #chunks+1 passes in any case.
+// needs the U rows i-d..i-1.  It is split into chunks of kChunk rows, one thread each.  The
+// default is one LU-writing pass in which every chunk starts kWarm rows early from the zero
+// state, followed by a bitwise check of each chunk's start state against its left neighbour's
+// end state; only on a mismatch does the exact chunked fixed point follow: pass p recomputes
+// every chunk from the state its left neighbour produced in pass p-1, chunks 0..p-1 are then
+// bitwise the sequential result, and the iteration stops at the first pass in which no chunk's
+// outgoing state changed (at most #chunks+1 passes).  A warp's 32 chunks are staged by the warp
+// together (cooperative cp.async copies of eight-row groups, factor_pass_kernel COOP).
 //
 // Solve (a2, every iteration).  Two sweeps, each a linear recurrence of order d:
 //   forward  y_i = v_i - sum_{k=1..d} L(i,i-k) y_{i-k}
 //   backward z_i = (y_i - sum_{k=1..d} U(i,i+k) z_{i+k}) / U(i,i)
-// Each sweep is ONE pass over HBM: a block stages a tile of TPB*R rows in shared memory,
-// every thread runs its R rows with d+1 simultaneous recurrences (zero state + the d unit
-// states) to get its affine map state_out = M state_in + t, a warp-shuffle / block scan
-// composes the maps, and a decoupled look-back across tiles (in-order tickets, epoch-tagged
-// descriptors) delivers the exact incoming state; the rows are then recomputed from that
-// state and stored.  Algorithmic bytes: forward 8(d+2), backward 8(d+3) per row.
+// Each sweep reads the coefficients about once (wsweep_kernel): every warp walks a contiguous
+// range of warp-tiles from a zero incoming state -- a lane runs its rows with d+1 simultaneous
+// recurrences (zero state + the d unit states) for its affine map state_out = M state_in + t,
+// a shuffle scan composes the lane maps -- and writes the zero-state rows and the range's map;
+// one block scans the range maps into exact incoming states (wscan_kernel); one thread per range
+// adds the homogeneous response to that state until it has decayed below 2^-60 of it
+// (tile_fix_kernel), and a range whose response has not decayed is re-walked in full.
+// Algorithmic bytes: forward 8(d+2), backward 8(d+3) per row.  The r01-r02 tile kernels
+// (tile_map/scan/fix/apply: shared-memory tiles and a block scan) stay behind PSP_SOLVE_BLOCK.
 #include <math.h>
 #include <stdint.h>
 
