@@ -770,7 +770,13 @@ int launch_kind(const FusedArgs& a, bool three_d, const double* rpx, const doubl
     if (kc <= 24) return launch_t<KIND, 32, 7, 24, 2>(a, rpx, rpy, fld, ld, s);
     return launch_t<KIND, 32, 7, 32, 2>(a, rpx, rpy, fld, ld, s);
   }
-  if (kc <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, fld, ld, s);
+  {
+    // 2-D / 1-D rows: KMAX 4 / 12 between 8 and 16 as in 3-D (at most three idle columns)
+    const bool coarse = getenv("PSP_FUSED_COARSE") != nullptr;
+    if (kc <= 4 && !coarse) return launch_t<KIND, 256, 1, 4, 1>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 8) return launch_t<KIND, 256, 1, 8, 1>(a, rpx, rpy, fld, ld, s);
+    if (kc <= 12 && !coarse) return launch_t<KIND, 256, 1, 12, 1>(a, rpx, rpy, fld, ld, s);
+  }
   if (kc <= 16) return launch_t<KIND, 256, 1, 16, 1>(a, rpx, rpy, fld, ld, s);
   return launch_t<KIND, 224, 1, 32, 2>(a, rpx, rpy, fld, ld, s);
 }
